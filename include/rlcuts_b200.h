@@ -1,0 +1,214 @@
+/*
+ * rlcuts_b200.h -- C-ABI drop-in boundary of the B200-native RL-lightcuts
+ * direct-lighting path.
+ *
+ * The reference (`/root/reference/proj`, CPU C++20 `rlcuts`) exposes the
+ * per-frame direct-lighting step as C++ functions in proj/include/rlcuts/.
+ * Every entry point below replaces one of them; the citation on each line is
+ * the reference interface it stands in for.  Plain pointers and sizes only:
+ * no C++ or torch types cross this boundary.
+ *
+ * Error convention: every call returns an rlc_status.  The reference throws
+ * C++ exceptions; RLC_ERR_INVALID_ARGUMENT stands for std::invalid_argument
+ * and RLC_ERR_OUT_OF_RANGE for std::out_of_range (e.g.
+ * proj/src/render.cpp:161-166, proj/src/cut.cpp:77-80).  rlc_last_error()
+ * returns the thread-local message of the last failing call.
+ *
+ * Threading: calls are synchronous with respect to the host unless noted
+ * (the reference fans out and joins std::threads inside each call,
+ * proj/src/render.cpp:23-38).  Device work is issued on the context stream
+ * (rlc_context_set_stream), and a call returns after that stream drained,
+ * except rlc_render_pass_async / rlc_end_of_pass_update_async.
+ *
+ * There is no CPU fallback: on a host without a usable sm_100 device every
+ * create call fails with RLC_ERR_NO_DEVICE.
+ */
+#ifndef RLCUTS_B200_H
+#define RLCUTS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLC_ABI_VERSION 1
+
+typedef enum rlc_status {
+  RLC_OK = 0,
+  RLC_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  RLC_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range in the reference */
+  RLC_ERR_CUDA = 3,             /* CUDA runtime / kernel failure */
+  RLC_ERR_NO_DEVICE = 4,        /* no sm_100 device: there is no CPU fallback */
+  RLC_ERR_INTERNAL = 5
+} rlc_status;
+
+/* proj/include/rlcuts/estimators.hpp:16-20 (SamplerKind) */
+enum { RLC_SAMPLER_UNIFORM = 0, RLC_SAMPLER_ENERGY = 1, RLC_SAMPLER_RL_LIGHTCUTS = 2 };
+/* proj/include/rlcuts/cut.hpp:16-19 (AlphaSchedule) */
+enum { RLC_ALPHA_FIXED = 0, RLC_ALPHA_HARMONIC = 1 };
+
+/* proj/include/rlcuts/cut.hpp:21-28 (CutConfig) */
+typedef struct rlc_cut_config {
+  uint32_t cut_size;       /* M; clamped to the light count */
+  uint32_t iterations;     /* split-collapse repeats per pass */
+  double alpha;            /* learning rate in (0,1] */
+  double split_threshold;  /* T */
+  double eps_q;            /* < 0 resolves to 1e-4 / M */
+  uint32_t alpha_schedule; /* RLC_ALPHA_* */
+  uint32_t _pad;
+} rlc_cut_config;
+
+/* proj/include/rlcuts/hash_grid.hpp:17-23 (HashConfig) */
+typedef struct rlc_hash_config {
+  uint32_t capacity;
+  uint32_t probe_limit;
+  uint32_t normal_bits;
+  uint32_t _pad;
+  double base_tile;    /* <= 0: derive from scene (diag / 256) */
+  double jitter_scale; /* 0 keeps key derivation a pure function */
+} rlc_hash_config;
+
+/* proj/include/rlcuts/render.hpp:17-26 (RenderConfig) */
+typedef struct rlc_render_config {
+  uint32_t spp;
+  uint32_t passes;
+  uint32_t max_depth;
+  uint32_t sampler; /* RLC_SAMPLER_* */
+  rlc_cut_config cut;
+  rlc_hash_config hash;
+  uint64_t seed;
+  uint32_t workers; /* accepted for interface parity; the device ignores it */
+  uint32_t _pad;
+} rlc_render_config;
+
+/* proj/include/rlcuts/scene.hpp:13-67 (Material, Triangle, Camera, Scene),
+ * flattened: vertices[t*9 + v*3 + axis] = triangles[t].p{v}[axis],
+ * materials[m*6 + 0..2] = albedo, materials[m*6 + 3..5] = emission. */
+typedef struct rlc_scene_desc {
+  uint32_t num_triangles;
+  uint32_t num_materials;
+  const double* vertices;
+  const uint32_t* material_ids;
+  const double* materials;
+  double cam_origin[3];
+  double cam_look_at[3];
+  double cam_up[3];
+  double vfov_degrees;
+  int32_t width;
+  int32_t height;
+} rlc_scene_desc;
+
+/* proj/include/rlcuts/hash_grid.hpp:26-34 (CellKey) */
+typedef struct rlc_cell_key {
+  int32_t qx, qy, qz;
+  uint32_t qn;
+  uint32_t level;
+} rlc_cell_key;
+
+/* proj/include/rlcuts/render.hpp:56-64 (RenderResult, minus the image) */
+typedef struct rlc_render_result {
+  double wall_ms;
+  uint32_t occupied_cells;
+  uint32_t num_passes;
+  uint64_t lookups;
+  uint64_t fallback_hits;
+  uint32_t* sc_changes; /* optional caller array [passes] */
+} rlc_render_result;
+
+/* proj/include/rlcuts/hash_grid.hpp:101-103 (occupied_count, lookup_count,
+ * fallback_hits) */
+typedef struct rlc_grid_stats {
+  uint32_t occupied;
+  uint32_t cut_size;
+  uint64_t lookups;
+  uint64_t fallback_hits;
+} rlc_grid_stats;
+
+typedef struct rlc_context_info {
+  uint32_t num_triangles;
+  uint32_t num_emitters;
+  uint32_t bvh_nodes;
+  uint32_t light_tree_nodes;
+  double base_tile;  /* resolved, proj/src/render.cpp:153-155 */
+  double shadow_eps; /* proj/src/bvh.cpp:120 */
+  uint64_t device_bytes;
+} rlc_context_info;
+
+typedef struct rlc_context rlc_context;         /* RenderContext, render.hpp:28-37 */
+typedef struct rlc_grid rlc_grid;               /* HashGrid, hash_grid.hpp:80-133 */
+typedef struct rlc_framebuffer rlc_framebuffer; /* Framebuffer, image.hpp:47-63 */
+
+/* ---- library ---------------------------------------------------------- */
+const char* rlc_last_error(void);
+int rlc_abi_version(void);
+/* Number of kernel launches this process issued so far (bench evidence). */
+uint64_t rlc_kernel_launches(void);
+/* Reference defaults: render.hpp:17-26, cut.hpp:21-28, hash_grid.hpp:17-23 */
+rlc_status rlc_render_config_default(rlc_render_config* config);
+
+/* ---- context: build_context (proj/src/render.cpp:143-157) ------------- */
+rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_config* config,
+                              int device, rlc_context** out);
+rlc_status rlc_context_destroy(rlc_context* ctx);
+rlc_status rlc_context_info_get(const rlc_context* ctx, rlc_context_info* info);
+/* Issue device work on `stream` (a cudaStream_t); NULL = the context's own. */
+rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream);
+rlc_status rlc_context_synchronize(rlc_context* ctx);
+
+/* ---- hash grid: HashGrid(hash, init_cut(tree, M, eps))
+ *      (proj/src/render.cpp:211-216, proj/src/hash_grid.cpp:102-111,
+ *       proj/src/cut.cpp:27-74) --------------------------------------- */
+rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* config,
+                           rlc_grid** out);
+rlc_status rlc_grid_destroy(rlc_grid* grid);
+rlc_status rlc_grid_stats_get(const rlc_grid* grid, rlc_grid_stats* stats);
+/* Parity export keyed by CellKey (slot ids are insertion-order dependent,
+ * SURVEY 0 fact 9).  Arrays are [max_cells] / [max_cells * cut_size]; any
+ * pointer may be NULL.  *num_cells receives the occupied count. */
+rlc_status rlc_grid_export(const rlc_grid* grid, uint32_t max_cells, rlc_cell_key* keys,
+                           uint32_t* node_ids, uint32_t* ends, double* q, double* cdf,
+                           uint32_t* visits, uint32_t* num_cells);
+/* The template cut every new cell starts from (init_cut, cut.cpp:27-74). */
+rlc_status rlc_grid_template(const rlc_grid* grid, uint32_t* node_ids, uint32_t* ends,
+                             double* q, double* cdf, uint32_t* visits, double* eps_q);
+
+/* ---- framebuffer: Framebuffer (proj/include/rlcuts/image.hpp:47-63) ---- */
+rlc_status rlc_framebuffer_create(const rlc_context* ctx, int32_t width, int32_t height,
+                                  rlc_framebuffer** out);
+rlc_status rlc_framebuffer_destroy(rlc_framebuffer* fb);
+rlc_status rlc_framebuffer_clear(rlc_framebuffer* fb);
+/* sum: [h*w*3] doubles, count: [h*w]; either may be NULL. */
+rlc_status rlc_framebuffer_download(const rlc_framebuffer* fb, double* sum, uint64_t* count);
+/* Framebuffer::resolve (proj/src/image.cpp:35-41): image [h*w*3]. */
+rlc_status rlc_framebuffer_resolve(const rlc_framebuffer* fb, double* image);
+
+/* ---- per-frame step ---------------------------------------------------- */
+/* render_pass (proj/src/render.cpp:159-183). */
+rlc_status rlc_render_pass(const rlc_context* ctx, const rlc_render_config* config,
+                           uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb);
+/* Same, restricted to image rows [row_begin, row_end) (screen-band sharding). */
+rlc_status rlc_render_pass_rows(const rlc_context* ctx, const rlc_render_config* config,
+                                uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb,
+                                uint32_t row_begin, uint32_t row_end);
+/* end_of_pass_update (proj/src/render.cpp:185-200); *changes may be NULL. */
+rlc_status rlc_end_of_pass_update(rlc_grid* grid, const rlc_context* ctx,
+                                  const rlc_cut_config* cut, uint32_t* changes);
+/* Asynchronous variants: enqueue on the context stream and return; the
+ * change count stays on the device (read it with rlc_grid_last_changes). */
+rlc_status rlc_render_pass_async(const rlc_context* ctx, const rlc_render_config* config,
+                                 uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb);
+rlc_status rlc_end_of_pass_update_async(rlc_grid* grid, const rlc_context* ctx,
+                                        const rlc_cut_config* cut);
+rlc_status rlc_grid_last_changes(const rlc_grid* grid, uint32_t* changes);
+/* render_frame (proj/src/render.cpp:202-240): image_out [h*w*3] host,
+ * resolved; result may be NULL. */
+rlc_status rlc_render_frame(const rlc_context* ctx, const rlc_render_config* config,
+                            double* image_out, rlc_render_result* result);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RLCUTS_B200_H */

@@ -1,0 +1,381 @@
+// rlc_build.cpp -- host construction of everything the device path reads.
+//
+// The scene BVH is built with the reference's splitting rule (median of the
+// centroids on the longest centroid axis via std::nth_element, leaves of at
+// most four triangles; proj/src/bvh.cpp:64-122).  std::nth_element is the
+// libstdc++ (GCC 13.3) introselect; calling it on the same array state with
+// the same ordering predicate reproduces the reference's leaf partition,
+// which is what closest-hit tie breaking (bvh.cpp:139-142) depends on.
+//
+// The light tree follows proj/src/light_tree.cpp:56-119: 10-bit Morton
+// codes, a total order on (code, emitter index), preorder node ids, split at
+// the highest differing code bit (median when a range shares one code).
+#include "rlc_build.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <numeric>
+
+namespace rlc {
+
+namespace {
+
+struct Box {
+  V3 lo{HUGE_VAL, HUGE_VAL, HUGE_VAL};
+  V3 hi{-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+  void grow(V3 p) {  // AABB::extend, math.hpp:71
+    lo = V3{smin(lo.x, p.x), smin(lo.y, p.y), smin(lo.z, p.z)};
+    hi = V3{smax(hi.x, p.x), smax(hi.y, p.y), smax(hi.z, p.z)};
+  }
+  void grow(const Box& b) {
+    lo = V3{smin(lo.x, b.lo.x), smin(lo.y, b.lo.y), smin(lo.z, b.lo.z)};
+    hi = V3{smax(hi.x, b.hi.x), smax(hi.y, b.hi.y), smax(hi.z, b.hi.z)};
+  }
+  V3 extent() const { return hi - lo; }
+  V3 center() const { return (lo + hi) * 0.5; }
+  int longest_axis() const {  // math.hpp:78-82
+    const V3 e = extent();
+    if (e.x >= e.y && e.x >= e.z) return 0;
+    return e.y >= e.z ? 1 : 2;
+  }
+};
+
+double comp(V3 v, int a) { return a == 0 ? v.x : (a == 1 ? v.y : v.z); }
+
+V3 vert(const rlc_scene_desc& d, uint32_t t, int k) {
+  const double* p = d.vertices + size_t(t) * 9 + size_t(k) * 3;
+  return V3{p[0], p[1], p[2]};
+}
+
+void put3(double* dst, V3 v) {
+  dst[0] = v.x;
+  dst[1] = v.y;
+  dst[2] = v.z;
+}
+
+uint32_t spread10(uint32_t x) {  // 10 bits -> every third bit
+  x &= 0x3ffu;
+  x = (x | (x << 16)) & 0x030000ffu;
+  x = (x | (x << 8)) & 0x0300f00fu;
+  x = (x | (x << 4)) & 0x030c30c3u;
+  x = (x | (x << 2)) & 0x09249249u;
+  return x;
+}
+
+// Scene BVH over all triangles; returns the leaf order.
+void build_bvh(const rlc_scene_desc& d, HostScene& out) {
+  const uint32_t n = d.num_triangles;
+  std::vector<Box> tb(n);
+  std::vector<V3> cen(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    Box b;
+    b.grow(vert(d, i, 0));
+    b.grow(vert(d, i, 1));
+    b.grow(vert(d, i, 2));
+    tb[i] = b;
+    cen[i] = b.center();
+  }
+  std::vector<uint32_t> perm(n);
+  std::iota(perm.begin(), perm.end(), 0u);
+
+  struct Todo {
+    uint32_t node, begin, end;
+  };
+  std::vector<BvhNode>& nodes = out.nodes;
+  nodes.clear();
+  nodes.reserve(size_t(2) * n);
+  nodes.push_back(BvhNode{});
+  std::vector<Todo> todo{{0, 0, n}};
+  while (!todo.empty()) {
+    const Todo t = todo.back();
+    todo.pop_back();
+    Box bounds, cb;
+    for (uint32_t i = t.begin; i < t.end; ++i) {
+      bounds.grow(tb[perm[i]]);
+      cb.grow(cen[perm[i]]);
+    }
+    BvhNode& nd = nodes[t.node];
+    put3(nd.lo, bounds.lo);
+    put3(nd.hi, bounds.hi);
+    const uint32_t count = t.end - t.begin;
+    if (count <= 4) {
+      nd.a = t.begin;
+      nd.b = 0;
+      nd.count = count;
+      continue;
+    }
+    const int axis = cb.longest_axis();
+    const uint32_t mid = t.begin + count / 2;
+    std::nth_element(perm.begin() + t.begin, perm.begin() + mid, perm.begin() + t.end,
+                     [&](uint32_t x, uint32_t y) { return comp(cen[x], axis) < comp(cen[y], axis); });
+    const uint32_t child = uint32_t(nodes.size());
+    nodes.push_back(BvhNode{});
+    nodes.push_back(BvhNode{});
+    nodes[t.node].a = child;
+    nodes[t.node].b = child + 1;
+    nodes[t.node].count = 0;
+    todo.push_back({child, t.begin, mid});
+    todo.push_back({child + 1, mid, t.end});
+  }
+  out.tris.resize(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t id = perm[i];
+    const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
+    TriAccel& ta = out.tris[i];
+    put3(ta.p0, p0);
+    put3(ta.e1, p1 - p0);
+    put3(ta.e2, p2 - p0);
+    ta.tri_id = id;
+    ta.pad = 0;
+  }
+  for (int a = 0; a < 3; ++a) {
+    out.scene_lo[a] = nodes[0].lo[a];
+    out.scene_hi[a] = nodes[0].hi[a];
+  }
+  const V3 ext = V3{nodes[0].hi[0], nodes[0].hi[1], nodes[0].hi[2]} -
+                 V3{nodes[0].lo[0], nodes[0].lo[1], nodes[0].lo[2]};
+  out.shadow_eps = 1e-4 * length(ext);  // bvh.cpp:120
+}
+
+}  // namespace
+
+void build_light_tree(const std::vector<double>& centroids, const std::vector<double>& energy,
+                      std::vector<uint32_t>& order, std::vector<LtNode>& nodes,
+                      std::vector<uint32_t>& node_begin, std::vector<double>& node_energy) {
+  const uint32_t n = uint32_t(energy.size());
+  if (n == 0) throw InvalidArgument("build_light_tree: no emitters");
+  Box cb;  // emitter_centroid_bounds, light_tree.cpp:50-54
+  for (uint32_t i = 0; i < n; ++i)
+    cb.grow(V3{centroids[3 * i], centroids[3 * i + 1], centroids[3 * i + 2]});
+  const V3 lo = cb.lo - V3{1e-6, 1e-6, 1e-6};
+  const V3 e0 = cb.extent() + V3{2e-6, 2e-6, 2e-6};
+  const V3 ext{smax(e0.x, 1e-12), smax(e0.y, 1e-12), smax(e0.z, 1e-12)};
+
+  std::vector<uint64_t> keyed(n);  // (code << 32) | emitter: the total order
+  for (uint32_t i = 0; i < n; ++i) {
+    const V3 rel = V3{centroids[3 * i], centroids[3 * i + 1], centroids[3 * i + 2]} - lo;
+    uint32_t qa[3];
+    for (int a = 0; a < 3; ++a) {
+      const double s = comp(rel, a) / comp(ext, a) * 1024.0;
+      qa[a] = uint32_t(smin(1023.0, smax(0.0, s)));
+    }
+    const uint32_t code = spread10(qa[0]) | (spread10(qa[1]) << 1) | (spread10(qa[2]) << 2);
+    keyed[i] = (uint64_t(code) << 32) | i;
+  }
+  std::sort(keyed.begin(), keyed.end());
+  order.resize(n);
+  std::vector<uint32_t> code(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    order[i] = uint32_t(keyed[i]);
+    code[i] = uint32_t(keyed[i] >> 32);
+  }
+
+  nodes.assign(0, LtNode{});
+  nodes.reserve(size_t(2) * n);
+  node_begin.clear();
+  node_begin.reserve(size_t(2) * n);
+  struct Todo {
+    uint32_t begin, end;
+    int32_t parent;
+    int side;  // 0 left child of parent, 1 right child
+  };
+  std::vector<Todo> todo{{0, n, -1, 0}};
+  while (!todo.empty()) {  // preorder: node, then left subtree, then right subtree
+    const Todo t = todo.back();
+    todo.pop_back();
+    const int32_t id = int32_t(nodes.size());
+    nodes.push_back(LtNode{t.end, -1, -1, t.parent});
+    node_begin.push_back(t.begin);
+    if (t.parent >= 0) {
+      if (t.side == 0) nodes[size_t(t.parent)].left = id;
+      else nodes[size_t(t.parent)].right = id;
+    }
+    if (t.end - t.begin == 1) continue;
+    const uint32_t first = code[t.begin], last = code[t.end - 1];
+    uint32_t mid;
+    if (first == last) {
+      mid = t.begin + (t.end - t.begin) / 2;
+    } else {
+      const int bit = 31 - __builtin_clz(first ^ last);
+      const uint32_t cut = (first & ~((1u << (bit + 1)) - 1u)) | (1u << bit);
+      mid = uint32_t(std::lower_bound(code.begin() + t.begin, code.begin() + t.end, cut) -
+                     code.begin());
+    }
+    todo.push_back({mid, t.end, id, 1});
+    todo.push_back({t.begin, mid, id, 0});
+  }
+  node_energy.assign(nodes.size(), 0.0);
+  for (size_t k = nodes.size(); k-- > 0;) {  // children carry larger preorder ids
+    if (nodes[k].left < 0) node_energy[k] = energy[order[node_begin[k]]];
+    else node_energy[k] = node_energy[size_t(nodes[k].left)] + node_energy[size_t(nodes[k].right)];
+  }
+}
+
+HostCut make_template_cut(const std::vector<LtNode>& nodes, const std::vector<uint32_t>& begin,
+                          const std::vector<double>& energy, uint32_t light_count, uint32_t M,
+                          double eps_q) {
+  if (M == 0) throw InvalidArgument("init_cut: cut size must be positive");
+  const uint32_t target = std::min(M, light_count);
+  std::deque<uint32_t> frontier_q{0u};
+  std::vector<uint32_t> done;
+  uint32_t count = 1;
+  while (count < target && !frontier_q.empty()) {  // breadth-first, cut.cpp:36-50
+    const uint32_t id = frontier_q.front();
+    frontier_q.pop_front();
+    if (nodes[id].left < 0) {
+      done.push_back(id);
+    } else {
+      frontier_q.push_back(uint32_t(nodes[id].left));
+      frontier_q.push_back(uint32_t(nodes[id].right));
+      ++count;
+    }
+  }
+  done.insert(done.end(), frontier_q.begin(), frontier_q.end());
+  std::sort(done.begin(), done.end(), [&](uint32_t a, uint32_t b) { return begin[a] < begin[b]; });
+
+  HostCut c;
+  const uint32_t m = uint32_t(done.size());
+  c.node_ids = done;
+  c.eps_q = eps_q < 0 ? 1e-4 / double(m) : eps_q;
+  c.ends.resize(m);
+  c.q.resize(m);
+  c.cdf.resize(m);
+  c.visits.assign(m, 1u);
+  double total = 0;
+  for (uint32_t i = 0; i < m; ++i) {
+    c.ends[i] = nodes[done[i]].range_end;
+    total += energy[done[i]];
+  }
+  double run = 0;
+  for (uint32_t i = 0; i < m; ++i) {
+    const double e = energy[done[i]];
+    const double share = total > 0 ? e / total : 1.0 / double(m);
+    c.q[i] = smax(share, c.eps_q);
+    run += c.q[i];
+    c.cdf[i] = run;
+  }
+  return c;
+}
+
+void level_thresholds(double out[kMaxLevel + 1]) {
+  auto level_of = [](double r) {
+    const double l = std::round(std::log2(r));
+    return uint32_t(clampd(l, 0.0, double(kMaxLevel)));
+  };
+  out[0] = 0.0;
+  for (uint32_t k = 1; k <= kMaxLevel; ++k) {
+    uint64_t lo = 1, hi = 0x7fefffffffffffffull;  // level(lo) < k <= level(hi)
+    while (hi - lo > 1) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      double r;
+      std::memcpy(&r, &mid, 8);
+      if (level_of(r) >= k) hi = mid;
+      else lo = mid;
+    }
+    std::memcpy(&out[k], &hi, 8);
+  }
+}
+
+void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, HostScene& out) {
+  if (d.num_triangles == 0 || d.vertices == nullptr || d.material_ids == nullptr)
+    throw InvalidArgument("build_scene_bvh: empty scene");
+  if (d.num_materials == 0 || d.materials == nullptr)
+    throw InvalidArgument("build_context: scene has no materials");
+  if (d.width <= 0 || d.height <= 0) throw InvalidArgument("build_context: empty camera raster");
+  for (uint32_t t = 0; t < d.num_triangles; ++t)
+    if (d.material_ids[t] >= d.num_materials)
+      throw OutOfRange("build_context: material id out of range");
+
+  out.mats.resize(d.num_materials);
+  for (uint32_t m = 0; m < d.num_materials; ++m) {
+    const double* v = d.materials + size_t(m) * 6;
+    MatRec& r = out.mats[m];
+    for (int a = 0; a < 3; ++a) {
+      r.albedo[a] = v[a];
+      r.emission[a] = v[3 + a];
+    }
+    r.is_emitter = luminance(V3{v[3], v[4], v[5]}) > 0 ? 1u : 0u;
+    r.reflective = luminance(V3{v[0], v[1], v[2]}) > 0 ? 1u : 0u;
+  }
+  out.tri_mat.assign(d.material_ids, d.material_ids + d.num_triangles);
+  out.tri_normal.resize(size_t(3) * d.num_triangles);
+  for (uint32_t t = 0; t < d.num_triangles; ++t) {
+    const V3 p0 = vert(d, t, 0);
+    put3(&out.tri_normal[size_t(3) * t], normalize(cross(vert(d, t, 1) - p0, vert(d, t, 2) - p0)));
+  }
+
+  build_bvh(d, out);  // render.cpp:145
+
+  // collect_emitters (light_tree.cpp:30-42) over derive_emitters order
+  out.lights.clear();
+  out.emitter_tri.clear();
+  out.emitter_energy.clear();
+  out.emitter_centroid.clear();
+  for (uint32_t t = 0; t < d.num_triangles; ++t) {
+    const MatRec& m = out.mats[d.material_ids[t]];
+    if (!m.is_emitter) continue;
+    const V3 p0 = vert(d, t, 0), p1 = vert(d, t, 1), p2 = vert(d, t, 2);
+    const V3 cr = cross(p1 - p0, p2 - p0);
+    const double area = 0.5 * length(cr);
+    const V3 c = (p0 + p1 + p2) / 3.0;
+    LightRec lr{};
+    put3(lr.p0, p0);
+    put3(lr.p1, p1);
+    put3(lr.p2, p2);
+    put3(lr.n, normalize(cr));
+    for (int a = 0; a < 3; ++a) lr.emission[a] = m.emission[a];
+    // sample_triangle_point throws on area <= 0 (scene.cpp:50-51); the
+    // device checks pdf_area <= 0 and raises the same error when drawn.
+    lr.pdf_area = area > 0 ? 1.0 / area : 0.0;
+    out.lights.push_back(lr);
+    out.emitter_tri.push_back(t);
+    out.emitter_energy.push_back(luminance(V3{m.emission[0], m.emission[1], m.emission[2]}) * area);
+    out.emitter_centroid.push_back(c.x);
+    out.emitter_centroid.push_back(c.y);
+    out.emitter_centroid.push_back(c.z);
+  }
+  if (out.lights.empty()) throw InvalidArgument("build_context: scene has no emitters");
+  build_light_tree(out.emitter_centroid, out.emitter_energy, out.order, out.lt_nodes,
+                   out.lt_begin, out.lt_energy);
+
+  out.energy_cdf.resize(out.emitter_energy.size());  // estimators.cpp:12-26
+  double run = 0;
+  for (size_t i = 0; i < out.emitter_energy.size(); ++i) {
+    run += out.emitter_energy[i];
+    out.energy_cdf[i] = run;
+  }
+  if (!(out.energy_cdf.back() > 0))
+    throw InvalidArgument("build_energy_cdf: total emitter energy must be positive");
+
+  const V3 ext = V3{out.scene_hi[0], out.scene_hi[1], out.scene_hi[2]} -
+                 V3{out.scene_lo[0], out.scene_lo[1], out.scene_lo[2]};
+  out.base_tile = cfg.hash.base_tile > 0 ? cfg.hash.base_tile : length(ext) / 256.0;
+
+  // camera_ray / pixel_solid_angle constants (scene.cpp:10-31)
+  CameraConst& cam = out.cam;
+  const V3 org{d.cam_origin[0], d.cam_origin[1], d.cam_origin[2]};
+  const V3 look{d.cam_look_at[0], d.cam_look_at[1], d.cam_look_at[2]};
+  const V3 up{d.cam_up[0], d.cam_up[1], d.cam_up[2]};
+  const V3 w = normalize(org - look);
+  const V3 u = normalize(cross(up, w));
+  const V3 v = cross(w, u);
+  put3(cam.origin, org);
+  put3(cam.u, u);
+  put3(cam.v, v);
+  put3(cam.w, w);
+  cam.tan_half = std::tan(0.5 * d.vfov_degrees * kPi / 180.0);
+  cam.aspect = double(d.width) / double(d.height);
+  cam.width = d.width;
+  cam.height = d.height;
+  cam.width_d = double(d.width);
+  cam.height_d = double(d.height);
+  const double plane_h = 2.0 * cam.tan_half;
+  const double plane_w = plane_h * cam.aspect;
+  cam.pdf_omega = 1.0 / ((plane_w / d.width) * (plane_h / d.height));
+
+  level_thresholds(out.level_threshold);
+}
+
+}  // namespace rlc

@@ -1,0 +1,75 @@
+// rlc_build.h -- host-side, once-per-context construction of the structures
+// the device path reads: the scene BVH in the reference topology, the
+// Morton light tree, emitter records, material flags, camera constants, the
+// template cut and the footprint-level thresholds.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rlc_common.h"
+#include "rlcuts_b200.h"
+
+namespace rlc {
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct OutOfRange : std::out_of_range {
+  using std::out_of_range::out_of_range;
+};
+
+constexpr uint32_t kMaxLevel = 16;  // proj/src/hash_grid.cpp:20
+
+struct HostScene {
+  // scene BVH (reference topology, bvh.cpp:64-122)
+  std::vector<BvhNode> nodes;
+  std::vector<TriAccel> tris;  // BVH leaf order
+  double scene_lo[3], scene_hi[3];
+  double shadow_eps = 0;
+  // materials / triangles
+  std::vector<MatRec> mats;
+  std::vector<uint32_t> tri_mat;  // by triangle id
+  std::vector<double> tri_normal; // by triangle id, [3] (triangle_normal)
+  // emitters + light tree (light_tree.cpp:30-119)
+  std::vector<LightRec> lights;          // by emitter index
+  std::vector<uint32_t> emitter_tri;     // emitter index -> triangle id
+  std::vector<double> emitter_energy;    // luminance(emission) * area
+  std::vector<double> emitter_centroid;  // [3] per emitter
+  std::vector<uint32_t> order;           // sorted position -> emitter index
+  std::vector<LtNode> lt_nodes;          // preorder ids, root 0
+  std::vector<uint32_t> lt_begin;        // range_begin per node
+  std::vector<double> lt_energy;
+  std::vector<double> energy_cdf;        // estimators.cpp:12-26
+  CameraConst cam;
+  double base_tile = 0;                  // render.cpp:153-155
+  double level_threshold[kMaxLevel + 1]; // see level_thresholds()
+};
+
+// Whole-context build (proj/src/render.cpp:143-157).  Throws InvalidArgument
+// with the reference's messages for empty scenes / no emitters.
+void build_host_scene(const rlc_scene_desc& desc, const rlc_render_config& cfg, HostScene& out);
+
+// Light tree alone over emitter centroids/energies (light_tree.cpp:56-119),
+// exposed for the unit-level entry points.
+void build_light_tree(const std::vector<double>& centroids, const std::vector<double>& energy,
+                      std::vector<uint32_t>& order, std::vector<LtNode>& nodes,
+                      std::vector<uint32_t>& node_begin, std::vector<double>& node_energy);
+
+struct HostCut {
+  std::vector<uint32_t> node_ids, ends, visits;
+  std::vector<double> q, cdf;
+  double eps_q = 0;
+};
+// init_cut (proj/src/cut.cpp:27-74).
+HostCut make_template_cut(const std::vector<LtNode>& nodes, const std::vector<uint32_t>& begin,
+                          const std::vector<double>& energy, uint32_t light_count, uint32_t M,
+                          double eps_q);
+
+// Smallest r with clamp(round(log2(r)), 0, 16) >= k for k = 1..16, found by
+// bisection over the doubles with the host libm, so the device reproduces
+// level_for_footprint (hash_grid.cpp:34-44) without its own log2.
+void level_thresholds(double out[kMaxLevel + 1]);
+
+}  // namespace rlc

@@ -1,0 +1,644 @@
+// rlc_capi.cpp -- the C-ABI drop-in boundary (include/rlcuts_b200.h) and the
+// host runtime behind it: device-resident context, hash grid and framebuffer,
+// and the per-pass launch sequence.  There is no CPU fallback: without an
+// sm_100 device every create call fails with RLC_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rlc_build.h"
+#include "rlc_kernels.h"
+#include "rlcuts_b200.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoDevice : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define RLC_CK(x)                                                                       \
+  do {                                                                                  \
+    const cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess)                                                              \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                 \
+  } while (0)
+
+template <class F>
+rlc_status guarded(F&& f) {
+  try {
+    f();
+    return RLC_OK;
+  } catch (const NoDevice& e) {
+    g_err = e.what();
+    return RLC_ERR_NO_DEVICE;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return RLC_ERR_CUDA;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return RLC_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return RLC_ERR_OUT_OF_RANGE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RLC_ERR_INTERNAL;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw rlc::InvalidArgument(msg);
+}
+
+// Owns a set of device allocations.
+struct DeviceArena {
+  std::vector<void*> ptrs;
+  uint64_t bytes = 0;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    const size_t b = count * sizeof(T) > 0 ? count * sizeof(T) : 16;
+    RLC_CK(cudaMalloc(&p, b));
+    ptrs.push_back(p);
+    bytes += b;
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (!v.empty()) RLC_CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+    bytes = 0;
+  }
+  ~DeviceArena() { release(); }
+};
+
+void check_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw NoDevice("no CUDA device: the rlcuts_b200 path has no CPU fallback");
+  }
+  if (device < 0 || device >= n) throw rlc::InvalidArgument("rlc_context_create: bad device index");
+  cudaDeviceProp prop;
+  RLC_CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    throw NoDevice("rlcuts_b200 is built for sm_100a (B200); device " + std::string(prop.name) +
+                   " is not supported");
+  RLC_CK(cudaSetDevice(device));
+}
+
+const char* device_error_message(uint32_t bits) {
+  if (bits & rlc::kErrNonUnitNormal) return "make_key: normal must be unit length";
+  if (bits & rlc::kErrBadValue) return "update_q: value must be finite and non-negative";
+  if (bits & rlc::kErrDegenerateLight) return "sample_triangle_point: degenerate triangle";
+  if (bits & rlc::kErrBadAreaPdf) return "level_for_footprint: area pdf must be positive";
+  if (bits & rlc::kErrStackOverflow) return "scene BVH deeper than the 64-entry traversal stack";
+  return "device error";
+}
+
+}  // namespace
+
+struct rlc_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  rlc::HostScene host;
+  rlc::DevScene dev{};
+  DeviceArena arena;
+  unsigned long long* counters = nullptr;  // error bits for grid-less passes
+  // per-pass scratch, grown on demand
+  DeviceArena scratch;
+  rlc::PassBuffers pb{};
+  uint32_t pb_cap = 0;
+
+  void ensure_scratch(uint32_t n) {
+    if (n <= pb_cap) return;
+    RLC_CK(cudaStreamSynchronize(stream));
+    scratch.release();
+    const uint32_t cap = n;
+    pb.gbuf = scratch.alloc<rlc::GBuf>(cap);
+    pb.srec = scratch.alloc<rlc::SampleRec>(cap);
+    pb.keys = scratch.alloc<uint32_t>(cap);
+    pb.vals = scratch.alloc<uint32_t>(cap);
+    pb.keys_alt = scratch.alloc<uint32_t>(cap);
+    pb.vals_alt = scratch.alloc<uint32_t>(cap);
+    pb.q_before = scratch.alloc<double>(cap);
+    pb.sort_hist_cap = ((cap + 4095u) / 4096u + 1u) * 256u;
+    pb.sort_hist = scratch.alloc<uint32_t>(pb.sort_hist_cap);
+    pb_cap = cap;
+  }
+};
+
+struct rlc_grid {
+  const rlc_context* ctx = nullptr;
+  rlc::DevGrid dev{};
+  rlc::HostCut tmpl;
+  uint32_t key_bits = 0;
+  DeviceArena arena;
+  uint32_t* d_changes = nullptr;
+  double alpha = 0.2;
+  uint32_t harmonic = 0;
+};
+
+struct rlc_framebuffer {
+  const rlc_context* ctx = nullptr;
+  int32_t width = 0, height = 0;
+  DeviceArena arena;
+  rlc::Framebuf fb{};
+  double* d_image = nullptr;
+};
+
+namespace {
+
+uint32_t read_and_clear_err(cudaStream_t st, unsigned long long* counters) {
+  unsigned long long e = 0;
+  RLC_CK(cudaMemcpyAsync(&e, counters + rlc::kCntErr, sizeof(e), cudaMemcpyDeviceToHost, st));
+  RLC_CK(cudaStreamSynchronize(st));
+  if (e) RLC_CK(cudaMemsetAsync(counters + rlc::kCntErr, 0, sizeof(e), st));
+  return uint32_t(e);
+}
+
+void throw_device_error(uint32_t bits) {
+  if (bits & rlc::kErrStackOverflow) throw std::runtime_error(device_error_message(bits));
+  throw rlc::InvalidArgument(device_error_message(bits));
+}
+
+// render_pass body (proj/src/render.cpp:159-183) for rows [r0, r1).
+void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_t pass_index,
+                  rlc_grid* grid, rlc_framebuffer* fb, uint32_t r0, uint32_t r1) {
+  rlc_context* ctx = const_cast<rlc_context*>(cctx);
+  require(cfg->passes != 0 && cfg->spp % cfg->passes == 0,
+          "render_pass: spp must be divisible by passes");
+  require(!(cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && grid == nullptr),
+          "render_pass: learned sampler needs a hash grid");
+  require(cfg->sampler <= RLC_SAMPLER_RL_LIGHTCUTS, "render_pass: unknown sampler");
+  require(cfg->max_depth == 1,
+          "render_pass: the device path implements max_depth == 1 (direct lighting)");
+  require(fb != nullptr && fb->width == ctx->host.cam.width && fb->height == ctx->host.cam.height,
+          "render_pass: framebuffer size must match the camera");
+  require(r0 <= r1 && r1 <= uint32_t(ctx->host.cam.height), "render_pass: bad row range");
+  require(grid == nullptr || grid->ctx == cctx, "render_pass: grid belongs to another context");
+  const uint32_t spp_pp = cfg->spp / cfg->passes;
+  const uint64_t n64 = uint64_t(r1 - r0) * uint64_t(ctx->host.cam.width) * spp_pp;
+  require(n64 < (1ull << 31), "render_pass: too many paths for one launch");
+  const uint32_t n = uint32_t(n64);
+  if (n == 0) return;
+  ctx->ensure_scratch(n);
+
+  rlc::PassParams p{};
+  p.width = uint32_t(ctx->host.cam.width);
+  p.row_begin = r0;
+  p.spp_pp = spp_pp;
+  p.pass_index = pass_index;
+  p.n = n;
+  p.sampler = cfg->sampler;
+  p.seed_mixed = rlc::mix64(cfg->seed);
+  p.zero_mixed = rlc::mix64(0);
+  p.alpha = grid ? grid->alpha : cfg->cut.alpha;
+  p.harmonic = grid ? grid->harmonic : 0u;
+
+  rlc::DevGrid g{};
+  if (grid) g = grid->dev;
+  else g.counters = ctx->counters;
+  cudaStream_t st = ctx->stream;
+  rlc::launch_primary(ctx->dev, g, p, ctx->pb, st);
+  rlc::launch_sample(ctx->dev, g, p, ctx->pb, st);
+  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS) {
+    uint32_t *k, *v;
+    rlc::launch_sort(ctx->pb, n, grid->key_bits, st, &k, &v);
+    rlc::launch_fold(g, p, k, v, ctx->pb, st);
+  }
+  rlc::launch_accumulate(ctx->dev, p, ctx->pb, fb->fb, st);
+  RLC_CK(cudaGetLastError());
+}
+
+void finish_sync(const rlc_context* ctx, rlc_grid* grid) {
+  const uint32_t bits =
+      read_and_clear_err(ctx->stream, grid ? grid->dev.counters : ctx->counters);
+  if (bits) throw_device_error(bits);
+}
+
+void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* cut,
+                 uint32_t* d_changes) {
+  require(grid != nullptr && ctx != nullptr && cut != nullptr,
+          "end_of_pass_update: null argument");
+  require(grid->ctx == ctx, "end_of_pass_update: grid belongs to another context");
+  rlc::launch_split_collapse(ctx->dev, grid->dev, cut->split_threshold, cut->iterations,
+                             d_changes, ctx->stream);
+  RLC_CK(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rlc_last_error(void) { return g_err.c_str(); }
+int rlc_abi_version(void) { return RLC_ABI_VERSION; }
+uint64_t rlc_kernel_launches(void) { return rlc::launches(); }
+
+rlc_status rlc_render_config_default(rlc_render_config* c) {
+  return guarded([&] {
+    require(c != nullptr, "rlc_render_config_default: null config");
+    std::memset(c, 0, sizeof(*c));
+    c->spp = 16;  // render.hpp:18-25
+    c->passes = 4;
+    c->max_depth = 1;
+    c->sampler = RLC_SAMPLER_UNIFORM;
+    c->cut.cut_size = 128;  // cut.hpp:22-27
+    c->cut.alpha = 0.2;
+    c->cut.split_threshold = 4.0;
+    c->cut.eps_q = -1;
+    c->cut.iterations = 1;
+    c->cut.alpha_schedule = RLC_ALPHA_FIXED;
+    c->hash.capacity = 1u << 16;  // hash_grid.hpp:18-22
+    c->hash.base_tile = 0;
+    c->hash.probe_limit = 32;
+    c->hash.normal_bits = 4;
+    c->hash.jitter_scale = 0;
+    c->seed = 1;
+    c->workers = 1;
+  });
+}
+
+rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_config* config,
+                              int device, rlc_context** out) {
+  return guarded([&] {
+    require(scene != nullptr && config != nullptr && out != nullptr,
+            "rlc_context_create: null argument");
+    *out = nullptr;
+    check_device(device);
+    auto ctx = std::make_unique<rlc_context>();
+    ctx->device = device;
+    rlc::build_host_scene(*scene, *config, ctx->host);
+    const rlc::HostScene& h = ctx->host;
+    DeviceArena& A = ctx->arena;
+    rlc::DevScene& d = ctx->dev;
+    d.nodes = A.upload(h.nodes);
+    d.tris = A.upload(h.tris);
+    d.mats = A.upload(h.mats);
+    d.tri_mat = A.upload(h.tri_mat);
+    d.tri_normal = A.upload(h.tri_normal);
+    d.lights = A.upload(h.lights);
+    d.order = A.upload(h.order);
+    d.lt = A.upload(h.lt_nodes);
+    d.energy_cdf = A.upload(h.energy_cdf);
+    d.emitter_energy = A.upload(h.emitter_energy);
+    d.num_lights = uint32_t(h.lights.size());
+    d.num_tris = uint32_t(h.tri_mat.size());
+    d.shadow_eps = h.shadow_eps;
+    d.base_tile = h.base_tile;
+    for (int k = 0; k <= 16; ++k) d.level_thr[k] = h.level_threshold[k];
+    d.cam = h.cam;
+    ctx->counters = A.alloc<unsigned long long>(rlc::kCntNum);
+    RLC_CK(cudaMemset(ctx->counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
+    RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    *out = ctx.release();
+  });
+}
+
+rlc_status rlc_context_destroy(rlc_context* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+  });
+}
+
+rlc_status rlc_context_info_get(const rlc_context* ctx, rlc_context_info* info) {
+  return guarded([&] {
+    require(ctx != nullptr && info != nullptr, "rlc_context_info_get: null argument");
+    info->num_triangles = uint32_t(ctx->host.tri_mat.size());
+    info->num_emitters = uint32_t(ctx->host.lights.size());
+    info->bvh_nodes = uint32_t(ctx->host.nodes.size());
+    info->light_tree_nodes = uint32_t(ctx->host.lt_nodes.size());
+    info->base_tile = ctx->host.base_tile;
+    info->shadow_eps = ctx->host.shadow_eps;
+    info->device_bytes = ctx->arena.bytes + ctx->scratch.bytes;
+  });
+}
+
+rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_set_stream: null context");
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  });
+}
+
+rlc_status rlc_context_synchronize(rlc_context* ctx) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_synchronize: null context");
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg, rlc_grid** out) {
+  return guarded([&] {
+    require(ctx != nullptr && cfg != nullptr && out != nullptr, "rlc_grid_create: null argument");
+    *out = nullptr;
+    RLC_CK(cudaSetDevice(ctx->device));
+    require(cfg->hash.capacity >= 1, "HashGrid: capacity must be at least 1");
+    require(ctx->host.base_tile > 0, "HashGrid: base tile must be resolved before build");
+    require(cfg->hash.normal_bits <= 13,
+            "HashGrid: the device key packs at most 13 octahedral bits per component");
+    require(cfg->cut.alpha_schedule <= RLC_ALPHA_HARMONIC, "CutConfig: unknown alpha schedule");
+    auto g = std::make_unique<rlc_grid>();
+    g->ctx = ctx;
+    const rlc::HostScene& h = ctx->host;
+    g->tmpl = rlc::make_template_cut(h.lt_nodes, h.lt_begin, h.lt_energy,
+                                     uint32_t(h.lights.size()), cfg->cut.cut_size, cfg->cut.eps_q);
+    const uint32_t M = uint32_t(g->tmpl.q.size());
+    const uint64_t cap = cfg->hash.capacity;
+    require(cap * M < 0xffffffffull, "HashGrid: capacity * cut size exceeds 32-bit segment keys");
+    uint32_t bits = 8;
+    while (bits < 32 && (cap * M) >= ((1ull << bits) - 1)) bits += 8;
+    g->key_bits = bits;
+    DeviceArena& A = g->arena;
+    rlc::DevGrid& d = g->dev;
+    d.slot_keys = A.alloc<unsigned long long>(2 * cap);
+    RLC_CK(cudaMemset(d.slot_keys, 0, 16 * cap));
+    d.slot_cell = A.alloc<uint32_t>(cap);
+    d.capacity = uint32_t(cap);
+    d.probe_limit = cfg->hash.probe_limit;
+    d.normal_bits = cfg->hash.normal_bits;
+    d.M = M;
+    d.jitter_scale = cfg->hash.jitter_scale;
+    d.node_ids = A.alloc<uint32_t>(cap * M);
+    d.ends = A.alloc<uint32_t>(cap * M);
+    d.q = A.alloc<double>(cap * M);
+    d.cdf = A.alloc<double>(cap * M);
+    d.visits = A.alloc<uint32_t>(cap * M);
+    d.cell_key = A.alloc<uint32_t>(5 * cap);
+    d.touched = A.alloc<uint32_t>(cap);
+    RLC_CK(cudaMemset(d.touched, 0, 4 * cap));
+    d.t_node = A.upload(g->tmpl.node_ids);
+    d.t_ends = A.upload(g->tmpl.ends);
+    d.t_q = A.upload(g->tmpl.q);
+    d.t_cdf = A.upload(g->tmpl.cdf);
+    d.t_visits = A.upload(g->tmpl.visits);
+    d.eps_q = g->tmpl.eps_q;
+    d.counters = A.alloc<unsigned long long>(rlc::kCntNum);
+    RLC_CK(cudaMemset(d.counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
+    g->d_changes = A.alloc<uint32_t>(1);
+    RLC_CK(cudaMemset(g->d_changes, 0, 4));
+    g->alpha = cfg->cut.alpha;
+    g->harmonic = cfg->cut.alpha_schedule == RLC_ALPHA_HARMONIC ? 1u : 0u;
+    *out = g.release();
+  });
+}
+
+rlc_status rlc_grid_destroy(rlc_grid* grid) {
+  return guarded([&] {
+    if (!grid) return;
+    cudaSetDevice(grid->ctx->device);
+    cudaStreamSynchronize(grid->ctx->stream);
+    delete grid;
+  });
+}
+
+rlc_status rlc_grid_stats_get(const rlc_grid* grid, rlc_grid_stats* stats) {
+  return guarded([&] {
+    require(grid != nullptr && stats != nullptr, "rlc_grid_stats_get: null argument");
+    unsigned long long c[rlc::kCntNum];
+    RLC_CK(cudaStreamSynchronize(grid->ctx->stream));
+    RLC_CK(cudaMemcpy(c, grid->dev.counters, sizeof(c), cudaMemcpyDeviceToHost));
+    stats->occupied = uint32_t(c[rlc::kCntCells]);
+    stats->cut_size = grid->dev.M;
+    stats->lookups = c[rlc::kCntLookups];
+    stats->fallback_hits = c[rlc::kCntFallback];
+  });
+}
+
+rlc_status rlc_grid_export(const rlc_grid* grid, uint32_t max_cells, rlc_cell_key* keys,
+                           uint32_t* node_ids, uint32_t* ends, double* q, double* cdf,
+                           uint32_t* visits, uint32_t* num_cells) {
+  return guarded([&] {
+    require(grid != nullptr, "rlc_grid_export: null grid");
+    RLC_CK(cudaStreamSynchronize(grid->ctx->stream));
+    unsigned long long nc = 0;
+    RLC_CK(cudaMemcpy(&nc, grid->dev.counters + rlc::kCntCells, 8, cudaMemcpyDeviceToHost));
+    if (num_cells) *num_cells = uint32_t(nc);
+    const size_t n = std::min<size_t>(nc, max_cells);
+    const size_t M = grid->dev.M;
+    if (n == 0) return;
+    if (keys) {
+      std::vector<uint32_t> k(5 * n);
+      RLC_CK(cudaMemcpy(k.data(), grid->dev.cell_key, 20 * n, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < n; ++i)
+        keys[i] = rlc_cell_key{int32_t(k[5 * i]), int32_t(k[5 * i + 1]), int32_t(k[5 * i + 2]),
+                               k[5 * i + 3], k[5 * i + 4]};
+    }
+    if (node_ids) RLC_CK(cudaMemcpy(node_ids, grid->dev.node_ids, 4 * n * M, cudaMemcpyDeviceToHost));
+    if (ends) RLC_CK(cudaMemcpy(ends, grid->dev.ends, 4 * n * M, cudaMemcpyDeviceToHost));
+    if (q) RLC_CK(cudaMemcpy(q, grid->dev.q, 8 * n * M, cudaMemcpyDeviceToHost));
+    if (cdf) RLC_CK(cudaMemcpy(cdf, grid->dev.cdf, 8 * n * M, cudaMemcpyDeviceToHost));
+    if (visits) RLC_CK(cudaMemcpy(visits, grid->dev.visits, 4 * n * M, cudaMemcpyDeviceToHost));
+  });
+}
+
+rlc_status rlc_grid_template(const rlc_grid* grid, uint32_t* node_ids, uint32_t* ends, double* q,
+                             double* cdf, uint32_t* visits, double* eps_q) {
+  return guarded([&] {
+    require(grid != nullptr, "rlc_grid_template: null grid");
+    const rlc::HostCut& t = grid->tmpl;
+    const size_t M = t.q.size();
+    if (node_ids) std::memcpy(node_ids, t.node_ids.data(), 4 * M);
+    if (ends) std::memcpy(ends, t.ends.data(), 4 * M);
+    if (q) std::memcpy(q, t.q.data(), 8 * M);
+    if (cdf) std::memcpy(cdf, t.cdf.data(), 8 * M);
+    if (visits) std::memcpy(visits, t.visits.data(), 4 * M);
+    if (eps_q) *eps_q = t.eps_q;
+  });
+}
+
+rlc_status rlc_framebuffer_create(const rlc_context* ctx, int32_t width, int32_t height,
+                                  rlc_framebuffer** out) {
+  return guarded([&] {
+    require(ctx != nullptr && out != nullptr, "rlc_framebuffer_create: null argument");
+    require(width > 0 && height > 0, "rlc_framebuffer_create: empty raster");
+    *out = nullptr;
+    RLC_CK(cudaSetDevice(ctx->device));
+    auto fb = std::make_unique<rlc_framebuffer>();
+    fb->ctx = ctx;
+    fb->width = width;
+    fb->height = height;
+    const size_t npix = size_t(width) * size_t(height);
+    fb->fb.sum = fb->arena.alloc<double>(3 * npix);
+    fb->fb.count = fb->arena.alloc<unsigned long long>(npix);
+    fb->fb.width = uint32_t(width);
+    fb->d_image = fb->arena.alloc<double>(3 * npix);
+    RLC_CK(cudaMemset(fb->fb.sum, 0, 24 * npix));
+    RLC_CK(cudaMemset(fb->fb.count, 0, 8 * npix));
+    *out = fb.release();
+  });
+}
+
+rlc_status rlc_framebuffer_destroy(rlc_framebuffer* fb) {
+  return guarded([&] {
+    if (!fb) return;
+    cudaStreamSynchronize(fb->ctx->stream);
+    delete fb;
+  });
+}
+
+rlc_status rlc_framebuffer_clear(rlc_framebuffer* fb) {
+  return guarded([&] {
+    require(fb != nullptr, "rlc_framebuffer_clear: null framebuffer");
+    const size_t npix = size_t(fb->width) * size_t(fb->height);
+    RLC_CK(cudaMemsetAsync(fb->fb.sum, 0, 24 * npix, fb->ctx->stream));
+    RLC_CK(cudaMemsetAsync(fb->fb.count, 0, 8 * npix, fb->ctx->stream));
+  });
+}
+
+rlc_status rlc_framebuffer_download(const rlc_framebuffer* fb, double* sum, uint64_t* count) {
+  return guarded([&] {
+    require(fb != nullptr, "rlc_framebuffer_download: null framebuffer");
+    const size_t npix = size_t(fb->width) * size_t(fb->height);
+    RLC_CK(cudaStreamSynchronize(fb->ctx->stream));
+    if (sum) RLC_CK(cudaMemcpy(sum, fb->fb.sum, 24 * npix, cudaMemcpyDeviceToHost));
+    if (count) RLC_CK(cudaMemcpy(count, fb->fb.count, 8 * npix, cudaMemcpyDeviceToHost));
+  });
+}
+
+rlc_status rlc_framebuffer_resolve(const rlc_framebuffer* fb, double* image) {
+  return guarded([&] {
+    require(fb != nullptr && image != nullptr, "rlc_framebuffer_resolve: null argument");
+    const uint32_t npix = uint32_t(size_t(fb->width) * size_t(fb->height));
+    rlc::launch_resolve(fb->fb, npix, fb->d_image, fb->ctx->stream);
+    RLC_CK(cudaMemcpyAsync(image, fb->d_image, 24 * size_t(npix), cudaMemcpyDeviceToHost,
+                           fb->ctx->stream));
+    RLC_CK(cudaStreamSynchronize(fb->ctx->stream));
+  });
+}
+
+rlc_status rlc_render_pass(const rlc_context* ctx, const rlc_render_config* config,
+                           uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb) {
+  return guarded([&] {
+    require(ctx != nullptr && config != nullptr, "render_pass: null argument");
+    enqueue_pass(ctx, config, pass_index, grid, fb, 0, uint32_t(ctx->host.cam.height));
+    finish_sync(ctx, grid);
+  });
+}
+
+rlc_status rlc_render_pass_rows(const rlc_context* ctx, const rlc_render_config* config,
+                                uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb,
+                                uint32_t row_begin, uint32_t row_end) {
+  return guarded([&] {
+    require(ctx != nullptr && config != nullptr, "render_pass: null argument");
+    enqueue_pass(ctx, config, pass_index, grid, fb, row_begin, row_end);
+    finish_sync(ctx, grid);
+  });
+}
+
+rlc_status rlc_render_pass_async(const rlc_context* ctx, const rlc_render_config* config,
+                                 uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb) {
+  return guarded([&] {
+    require(ctx != nullptr && config != nullptr, "render_pass: null argument");
+    enqueue_pass(ctx, config, pass_index, grid, fb, 0, uint32_t(ctx->host.cam.height));
+  });
+}
+
+rlc_status rlc_end_of_pass_update(rlc_grid* grid, const rlc_context* ctx,
+                                  const rlc_cut_config* cut, uint32_t* changes) {
+  return guarded([&] {
+    require(grid != nullptr, "end_of_pass_update: null grid");
+    RLC_CK(cudaMemsetAsync(grid->d_changes, 0, 4, ctx->stream));
+    enqueue_eop(grid, ctx, cut, grid->d_changes);
+    uint32_t c = 0;
+    RLC_CK(cudaMemcpyAsync(&c, grid->d_changes, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    finish_sync(ctx, grid);
+    if (changes) *changes = c;
+  });
+}
+
+rlc_status rlc_end_of_pass_update_async(rlc_grid* grid, const rlc_context* ctx,
+                                        const rlc_cut_config* cut) {
+  return guarded([&] {
+    require(grid != nullptr, "end_of_pass_update: null grid");
+    RLC_CK(cudaMemsetAsync(grid->d_changes, 0, 4, ctx->stream));
+    enqueue_eop(grid, ctx, cut, grid->d_changes);
+  });
+}
+
+rlc_status rlc_grid_last_changes(const rlc_grid* grid, uint32_t* changes) {
+  return guarded([&] {
+    require(grid != nullptr && changes != nullptr, "rlc_grid_last_changes: null argument");
+    RLC_CK(cudaMemcpyAsync(changes, grid->d_changes, 4, cudaMemcpyDeviceToHost, grid->ctx->stream));
+    RLC_CK(cudaStreamSynchronize(grid->ctx->stream));
+  });
+}
+
+rlc_status rlc_render_frame(const rlc_context* ctx, const rlc_render_config* config,
+                            double* image_out, rlc_render_result* result) {
+  return guarded([&] {
+    require(ctx != nullptr && config != nullptr, "render_frame: null argument");
+    require(config->passes != 0 && config->spp != 0 && config->spp % config->passes == 0,
+            "render_frame: spp must be divisible by passes");
+    const auto t0 = std::chrono::steady_clock::now();
+    rlc_framebuffer* fbp = nullptr;
+    rlc_grid* gp = nullptr;
+    rlc_status st = rlc_framebuffer_create(ctx, ctx->host.cam.width, ctx->host.cam.height, &fbp);
+    if (st != RLC_OK) throw std::runtime_error(g_err);
+    std::unique_ptr<rlc_framebuffer> fb(fbp);
+    std::unique_ptr<rlc_grid> grid;
+    if (config->sampler == RLC_SAMPLER_RL_LIGHTCUTS) {
+      st = rlc_grid_create(ctx, config, &gp);
+      if (st == RLC_ERR_INVALID_ARGUMENT) throw rlc::InvalidArgument(g_err);
+      if (st != RLC_OK) throw std::runtime_error(g_err);
+      grid.reset(gp);
+    }
+    DeviceArena hist;
+    uint32_t* d_hist = hist.alloc<uint32_t>(config->passes);
+    RLC_CK(cudaMemsetAsync(d_hist, 0, 4 * size_t(config->passes), ctx->stream));
+    for (uint32_t pass = 0; pass < config->passes; ++pass) {
+      enqueue_pass(ctx, config, pass, grid.get(), fb.get(), 0, uint32_t(ctx->host.cam.height));
+      if (grid) enqueue_eop(grid.get(), ctx, &config->cut, d_hist + pass);
+    }
+    const uint32_t npix = uint32_t(size_t(fb->width) * size_t(fb->height));
+    if (image_out) {
+      rlc::launch_resolve(fb->fb, npix, fb->d_image, ctx->stream);
+      RLC_CK(cudaMemcpyAsync(image_out, fb->d_image, 24 * size_t(npix), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    }
+    std::vector<uint32_t> h(config->passes);
+    RLC_CK(cudaMemcpyAsync(h.data(), d_hist, 4 * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    finish_sync(ctx, grid.get());
+    if (result) {
+      result->num_passes = config->passes;
+      if (result->sc_changes) std::memcpy(result->sc_changes, h.data(), 4 * h.size());
+      if (grid) {
+        rlc_grid_stats s;
+        rlc_grid_stats_get(grid.get(), &s);
+        result->occupied_cells = s.occupied;
+        result->lookups = s.lookups;
+        result->fallback_hits = s.fallback_hits;
+      } else {
+        result->occupied_cells = 0;
+        result->lookups = 0;
+        result->fallback_hits = 0;
+      }
+      result->wall_ms = std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// rlc_common.h -- FP64 vector math, counter RNG and plain-data layouts shared
+// by the host build code (g++, -ffp-contract=off) and the sm_100a kernels
+// (nvcc --fmad=false).  Every expression keeps the operand order of the
+// reference so that host-precomputed and device-computed values are
+// bit-identical to the reference's doubles (contraction
+// into FMA changes cell keys).
+#pragma once
+
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define RLC_HD __host__ __device__ __forceinline__
+#else
+#define RLC_HD inline
+#include <cmath>
+#endif
+
+namespace rlc {
+
+constexpr double kPi = 3.14159265358979323846;  // proj/include/rlcuts/math.hpp:12
+
+// ---- Vec3: proj/include/rlcuts/math.hpp:15-53 ----------------------------
+struct V3 {
+  double x, y, z;
+};
+RLC_HD V3 v3(double x, double y, double z) { return V3{x, y, z}; }
+RLC_HD V3 operator+(V3 a, V3 b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+RLC_HD V3 operator-(V3 a, V3 b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+RLC_HD V3 operator-(V3 a) { return V3{-a.x, -a.y, -a.z}; }
+RLC_HD V3 operator*(V3 a, V3 b) { return V3{a.x * b.x, a.y * b.y, a.z * b.z}; }
+RLC_HD V3 operator*(V3 a, double s) { return V3{a.x * s, a.y * s, a.z * s}; }
+RLC_HD V3 operator/(V3 a, double s) { return V3{a.x / s, a.y / s, a.z / s}; }
+RLC_HD double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+RLC_HD V3 cross(V3 a, V3 b) {
+  return V3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+RLC_HD double length(V3 v) { return sqrt(dot(v, v)); }
+RLC_HD V3 normalize(V3 v) { return v / length(v); }
+// std::min / std::max argument semantics: min(a,b) = (b < a) ? b : a,
+// max(a,b) = (a < b) ? b : a (NaN handling follows from that).
+RLC_HD double smin(double a, double b) { return (b < a) ? b : a; }
+RLC_HD double smax(double a, double b) { return (a < b) ? b : a; }
+RLC_HD double clampd(double v, double lo, double hi) {  // std::clamp
+  return v < lo ? lo : (hi < v ? hi : v);
+}
+// Rec.709 luminance, math.hpp:56
+RLC_HD double luminance(V3 c) { return 0.2126 * c.x + 0.7152 * c.y + 0.0722 * c.z; }
+
+// ---- counter RNG: proj/include/rlcuts/rng.hpp:12-43 -----------------------
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+RLC_HD uint64_t mix64(uint64_t x) {
+  x += kGolden;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+RLC_HD uint64_t hash_combine(uint64_t a, uint64_t b) { return mix64(a ^ mix64(b)); }
+RLC_HD double to_unit(uint64_t bits) { return double(bits >> 11) * 0x1.0p-53; }
+// RandomSequence(seed, a, b, c).key_ with mix64(seed) precomputed.
+RLC_HD uint64_t rng_key(uint64_t seed_mixed, uint64_t a, uint64_t b, uint64_t c_mixed) {
+  uint64_t k = hash_combine(seed_mixed, a);
+  k = hash_combine(k, b);
+  return mix64(k ^ c_mixed);  // hash_combine(k, c) with c_mixed = mix64(c)
+}
+// The d-th draw (d = 1, 2, ...) of the sequence: rng.hpp:37.
+RLC_HD double rng_draw(uint64_t key, uint64_t d) { return to_unit(mix64(key + kGolden * d)); }
+
+// Draw indices of one depth-1 path (proj/src/render.cpp:65-66, 90-95).
+enum : uint32_t { kDrawJx = 1, kDrawJy = 2, kDrawU1 = 3, kDrawU2 = 4, kDrawU3 = 5,
+                  kDrawJu1 = 6, kDrawJu2 = 7 };
+
+// ---- plain-data device layouts ------------------------------------------
+// Scene BVH node, reference topology (proj/include/rlcuts/bvh.hpp:16-22),
+// 64 B so one node is four 16-byte loads.
+struct alignas(64) BvhNode {
+  double lo[3];
+  double hi[3];
+  uint32_t a;      // internal: left child; leaf: first index into the tri arrays
+  uint32_t b;      // internal: right child
+  uint32_t count;  // 0 for internal nodes
+  uint32_t pad;
+};
+
+// Triangle as the Moller-Trumbore test consumes it (bvh.cpp:44-62): p0 and
+// the two edges, precomputed with the reference's own subtraction.  Stored
+// in BVH leaf order.  80 B.
+struct alignas(16) TriAccel {
+  double p0[3];
+  double e1[3];
+  double e2[3];
+  uint32_t tri_id;
+  uint32_t pad;
+};
+
+// Emitter in reference emitter order (light_tree.cpp:30-42): everything
+// sample_triangle_point (scene.cpp:49-59) and nee_estimate
+// (estimators.cpp:82-106) read.  128 B, one line.
+struct alignas(128) LightRec {
+  double p0[3], p1[3], p2[3];
+  double n[3];         // triangle_normal (scene.hpp:27)
+  double emission[3];  // material emission
+  double pdf_area;     // 1 / triangle_area
+};
+
+// Material flags precomputed with the reference predicates.
+struct alignas(16) MatRec {
+  double albedo[3];
+  double emission[3];
+  uint32_t is_emitter;  // luminance(emission) > 0   (scene.hpp:17)
+  uint32_t reflective;  // luminance(albedo) > 0     (render.cpp:84)
+};
+
+// Light-tree node as split-collapse reads it (light_tree.hpp:29-36).
+struct alignas(16) LtNode {
+  uint32_t range_end;
+  int32_t left;
+  int32_t right;
+  int32_t parent;
+};
+
+// Camera constants precomputed on the host exactly as camera_ray
+// (proj/src/scene.cpp:10-23) and pixel_solid_angle (:25-31) do.
+struct CameraConst {
+  double origin[3];
+  double u[3], v[3], w[3];
+  double tan_half, aspect;
+  double width_d, height_d;
+  double pdf_omega;  // 1 / pixel_solid_angle
+  int32_t width, height;
+};
+
+}  // namespace rlc

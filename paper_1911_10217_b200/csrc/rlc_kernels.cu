@@ -1,0 +1,918 @@
+// rlc_kernels.cu -- sm_100a kernels of the per-pass RL-lightcuts path.
+//
+// Per pass (render_pass + end_of_pass_update, proj/src/render.cpp:159-200):
+//   k_primary      camera ray, closest hit, shading point, footprint level,
+//                  5-D cell key and hash-grid lookup/insert      (one thread/path)
+//   k_sample       cut sampling from the pass-frozen cdf, emitter point,
+//                  NEE geometry, any-hit shadow ray, feedback v  (one thread/path)
+//   radix sort     stable, update records by (cell, cluster)     (hand-written)
+//   k_fold         sequential update_q per (cell, cluster) segment in canonical
+//                  order -> live q, visits and per-sample q_before
+//   k_accumulate   deferred radiance with q_before, Framebuffer::add_sample
+//   k_split        split-collapse + ends + serial cdf per touched cell (one warp/cell)
+//
+// All FP64 arithmetic keeps the reference's operand order and this file is
+// compiled with --fmad=false: the path is bit-exact with the reference
+// (SURVEY 0 facts 1-6 and Appendix B give the argument).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+
+#include "rlc_kernels.h"
+
+namespace rlc {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+constexpr unsigned kFull = 0xffffffffu;
+}  // namespace
+
+uint64_t launches() { return g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// geometry helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ V3 ld3(const double* p) { return V3{p[0], p[1], p[2]}; }
+
+struct NodeView {
+  double lo0, lo1, lo2, hi0, hi1, hi2;
+  uint32_t a, b, count;
+};
+
+__device__ __forceinline__ NodeView load_node(const BvhNode* nodes, uint32_t i) {
+  const double2* p = reinterpret_cast<const double2*>(nodes + i);
+  const double2 x = __ldg(p), y = __ldg(p + 1), z = __ldg(p + 2);
+  const uint4 w = __ldg(reinterpret_cast<const uint4*>(nodes + i) + 3);
+  return NodeView{x.x, x.y, y.x, y.y, z.x, z.y, w.x, w.y, w.z};
+}
+
+// intersect_aabb, proj/src/bvh.cpp:29-40 (std::max/std::min semantics).
+__device__ __forceinline__ bool slab(double lo, double hi, double o, double inv, double& tmin,
+                                     double& tmax) {
+  double t0 = (lo - o) * inv;
+  double t1 = (hi - o) * inv;
+  if (inv < 0) {
+    const double t = t0;
+    t0 = t1;
+    t1 = t;
+  }
+  tmin = smax(tmin, t0);
+  tmax = smin(tmax, t1);
+  return !(tmax < tmin);
+}
+
+__device__ __forceinline__ bool box_hit(const NodeView& n, V3 o, V3 inv, double tmin,
+                                        double tmax) {
+  if (!slab(n.lo0, n.hi0, o.x, inv.x, tmin, tmax)) return false;
+  if (!slab(n.lo1, n.hi1, o.y, inv.y, tmin, tmax)) return false;
+  return slab(n.lo2, n.hi2, o.z, inv.z, tmin, tmax);
+}
+
+// Moller-Trumbore, proj/src/bvh.cpp:44-62.
+__device__ __forceinline__ bool tri_hit(const TriAccel* tris, uint32_t i, V3 o, V3 d,
+                                        double tmin, double tmax, double* tout) {
+  const double2* p = reinterpret_cast<const double2*>(tris + i);
+  const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), e = __ldg(p + 3),
+                f = __ldg(p + 4);
+  const V3 p0{a.x, a.y, b.x};
+  const V3 e1{b.y, c.x, c.y};
+  const V3 e2{e.x, e.y, f.x};
+  const V3 pv = cross(d, e2);
+  const double det = dot(e1, pv);
+  if (fabs(det) < 1e-14) return false;
+  const double inv_det = 1.0 / det;
+  const V3 tv = o - p0;
+  const double u = dot(tv, pv) * inv_det;
+  if (u < 0 || u > 1) return false;
+  const V3 qv = cross(tv, e1);
+  const double v = dot(d, qv) * inv_det;
+  if (v < 0 || u + v > 1) return false;
+  const double t = dot(e2, qv) * inv_det;
+  if (t <= tmin || t >= tmax) return false;
+  *tout = t;
+  return true;
+}
+
+constexpr int kStack = 64;  // bvh.cpp:134 uses a 64-entry stack too
+
+// occluded(), proj/src/bvh.cpp:159-188.  The any-hit boolean does not depend
+// on traversal order, so any order over the same tree and slab test gives
+// the reference's answer.
+__device__ bool occluded(const DevScene& sc, V3 a, V3 b, uint32_t* err) {
+  const V3 d = b - a;
+  const double len = length(d);
+  if (len <= 2 * sc.shadow_eps) return false;
+  const V3 dir = d / len;
+  const double tmin = sc.shadow_eps;
+  const double tmax = len - sc.shadow_eps;
+  const V3 inv{1.0 / dir.x, 1.0 / dir.y, 1.0 / dir.z};
+  uint32_t stack[kStack];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp > 0) {
+    const NodeView n = load_node(sc.nodes, stack[--sp]);
+    if (!box_hit(n, a, inv, tmin, tmax)) continue;
+    if (n.count > 0) {
+      for (uint32_t i = n.a; i < n.a + n.count; ++i) {
+        double t;
+        if (tri_hit(sc.tris, i, a, dir, tmin, tmax, &t)) return true;
+      }
+    } else {
+      if (sp + 2 > kStack) {
+        atomicOr(err, kErrStackOverflow);
+        return false;
+      }
+      stack[sp++] = n.a;
+      stack[sp++] = n.b;
+    }
+  }
+  return false;
+}
+
+// intersect(), proj/src/bvh.cpp:124-157: closest hit, exact-t ties go to the
+// first triangle tested in the reference traversal order (right child first).
+__device__ bool intersect(const DevScene& sc, V3 o, V3 d, double tmin, double* t_out,
+                          uint32_t* tri_out, uint32_t* err) {
+  const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+  double closest = HUGE_VAL;
+  uint32_t hit = kNoSlot;
+  uint32_t stack[kStack];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp > 0) {
+    const NodeView n = load_node(sc.nodes, stack[--sp]);
+    if (!box_hit(n, o, inv, tmin, closest)) continue;
+    if (n.count > 0) {
+      for (uint32_t i = n.a; i < n.a + n.count; ++i) {
+        double t;
+        if (tri_hit(sc.tris, i, o, d, tmin, closest, &t)) {
+          closest = t;
+          hit = i;
+        }
+      }
+    } else {
+      if (sp + 2 > kStack) {
+        atomicOr(err, kErrStackOverflow);
+        break;
+      }
+      stack[sp++] = n.a;
+      stack[sp++] = n.b;
+    }
+  }
+  if (hit == kNoSlot) return false;
+  *t_out = closest;
+  *tri_out = sc.tris[hit].tri_id;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// hash-grid key (proj/src/hash_grid.cpp:27-100)
+// ---------------------------------------------------------------------------
+struct Key {
+  int32_t qx, qy, qz;
+  uint32_t qn, level;
+};
+
+__device__ __forceinline__ double sign_nz(double v) { return v >= 0 ? 1.0 : -1.0; }
+
+__device__ __forceinline__ Key make_key(V3 p, V3 n, uint32_t level, double ju1, double ju2,
+                                        double base_tile, uint32_t bits, double js) {
+  const double cell = base_tile * ldexp(1.0, int(level));  // base_tile * exp2(level), exact
+  const double offset = js * cell * (ju1 - 0.5);
+  Key k;
+  k.qx = int32_t(floor((p.x + offset) / cell));
+  k.qy = int32_t(floor((p.y + offset) / cell));
+  k.qz = int32_t(floor((p.z + offset) / cell));
+  k.level = level;
+  const uint32_t steps = 1u << bits;
+  const double quantum = 1.0 / double(steps);
+  const double noffset = js * quantum * (ju2 - 0.5);
+  // octa_encode, hash_grid.cpp:50-61
+  const double norm = fabs(n.x) + fabs(n.y) + fabs(n.z);
+  double ox = n.x / norm;
+  double oy = n.y / norm;
+  if (n.z < 0) {
+    const double tx = (1.0 - fabs(oy)) * sign_nz(ox);
+    const double ty = (1.0 - fabs(ox)) * sign_nz(oy);
+    ox = tx;
+    oy = ty;
+  }
+  const double eu = ox * 0.5 + 0.5;
+  const double ev = oy * 0.5 + 0.5;
+  const double top = double(steps - 1);
+  const uint32_t qu = uint32_t(clampd(floor((eu + noffset) * double(steps)), 0.0, top));
+  const uint32_t qv = uint32_t(clampd(floor((ev + noffset) * double(steps)), 0.0, top));
+  k.qn = (qu << bits) | qv;
+  return k;
+}
+
+__device__ __forceinline__ uint64_t hash_key(const Key& k) {
+  const uint64_t w0 = (uint64_t(uint32_t(k.qx)) << 32) | uint64_t(uint32_t(k.qy));
+  const uint64_t w1 = (uint64_t(uint32_t(k.qz)) << 32) | (uint64_t(k.qn & 0xffffu) << 16) |
+                      uint64_t(k.level & 0xffffu);
+  return hash_combine(mix64(w0), w1);
+}
+
+// Packed 128-bit slot word: lo = qx | qy << 32, hi = qz | qn << 32 (26 bits)
+// | level << 58 (5 bits) | valid << 63.  An all-zero word is an empty slot.
+__device__ __forceinline__ void pack_key(const Key& k, uint64_t& lo, uint64_t& hi) {
+  lo = uint64_t(uint32_t(k.qx)) | (uint64_t(uint32_t(k.qy)) << 32);
+  hi = uint64_t(uint32_t(k.qz)) | (uint64_t(k.qn & 0x3ffffffu) << 32) |
+       (uint64_t(k.level & 0x1fu) << 58) | (1ull << 63);
+}
+
+__device__ __forceinline__ void cas128(unsigned long long* addr, uint64_t new_lo, uint64_t new_hi,
+                                       uint64_t& old_lo, uint64_t& old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 d, c, s;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 s, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, s;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}\n"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(0ull), "l"(0ull), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+}
+
+// lookup_or_insert (hash_grid.cpp:113-141): linear probing from hash %
+// capacity, at most min(probe_limit, capacity) slots, CAS-claim of an empty
+// slot; the claimer takes a dense cell id and copies the template cut in.
+// The dense id is published to other paths at the kernel boundary.
+__device__ uint32_t probe_insert(const DevGrid& g, const Key& k, uint64_t h) {
+  uint64_t lo, hi;
+  pack_key(k, lo, hi);
+  const uint32_t probes = min(g.probe_limit, g.capacity);
+  uint32_t slot = uint32_t(h % uint64_t(g.capacity));
+  for (uint32_t i = 0; i < probes; ++i) {
+    uint64_t olo, ohi;
+    cas128(g.slot_keys + 2 * size_t(slot), lo, hi, olo, ohi);
+    if (olo == 0 && ohi == 0) {  // claimed: new cell
+      const uint32_t cid = uint32_t(atomicAdd(g.counters + kCntCells, 1ull));
+      g.slot_cell[slot] = cid;
+      uint32_t* ck = g.cell_key + size_t(5) * cid;
+      ck[0] = uint32_t(k.qx);
+      ck[1] = uint32_t(k.qy);
+      ck[2] = uint32_t(k.qz);
+      ck[3] = k.qn;
+      ck[4] = k.level;
+      const size_t row = size_t(cid) * g.M;
+      for (uint32_t j = 0; j < g.M; ++j) {
+        g.node_ids[row + j] = g.t_node[j];
+        g.ends[row + j] = g.t_ends[j];
+        g.q[row + j] = g.t_q[j];
+        g.cdf[row + j] = g.t_cdf[j];
+        g.visits[row + j] = g.t_visits[j];
+      }
+      g.touched[cid] = 0;
+      return slot;
+    }
+    if (olo == lo && ohi == hi) return slot;
+    slot = slot + 1 == g.capacity ? 0 : slot + 1;
+  }
+  return kFallback;
+}
+
+// ---------------------------------------------------------------------------
+// k_primary: PassRenderer::trace up to the cell lookup (render.cpp:59-99)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassParams P,
+                                                 GBuf* __restrict__ gbuf) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = idx < P.n;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
+
+  bool need = false;
+  Key key{};
+  uint64_t h = 0;
+  GBuf out;
+  out.slot = kNoSlot;
+  out.flags = 0;
+  if (active) {
+    const uint32_t s = idx % P.spp_pp;
+    const uint32_t pix = idx / P.spp_pp;
+    const uint32_t px = pix % P.width;
+    const uint32_t py = P.row_begin + pix / P.width;
+    const uint64_t pixel_index = uint64_t(py) * uint64_t(P.width) + px;
+    const uint64_t sample_index = uint64_t(P.pass_index) * P.spp_pp + s;
+    const uint64_t rk = rng_key(P.seed_mixed, pixel_index, sample_index, P.zero_mixed);
+    out.rng = rk;
+    const double jx = rng_draw(rk, kDrawJx);
+    const double jy = rng_draw(rk, kDrawJy);
+    // camera_ray, scene.cpp:10-23
+    const CameraConst& c = sc.cam;
+    const double fx = double(px) + jx;
+    const double fy = double(py) + jy;
+    const double sx = (2.0 * fx / c.width_d - 1.0) * c.tan_half * c.aspect;
+    const double sy = (1.0 - 2.0 * fy / c.height_d) * c.tan_half;
+    const V3 dir = normalize(ld3(c.u) * sx + ld3(c.v) * sy - ld3(c.w));
+    const V3 org = ld3(c.origin);
+    double t;
+    uint32_t tri;
+    if (intersect(sc, org, dir, 0.0, &t, &tri, err)) {
+      const V3 pos = org + dir * t;
+      const V3 ng = ld3(sc.tri_normal + size_t(3) * tri);
+      const V3 wo = -dir;
+      const double cos_facing = dot(ng, wo);
+      const uint32_t mat = sc.tri_mat[tri];
+      const MatRec& m = sc.mats[mat];
+      uint32_t flags = kGHit | mat;
+      if (m.is_emitter && cos_facing > 0) flags |= kGEmit;
+      const V3 ns = dot(ng, wo) < 0 ? -ng : ng;  // faceforward, math.hpp:59-61
+      out.pos[0] = pos.x;
+      out.pos[1] = pos.y;
+      out.pos[2] = pos.z;
+      out.ns[0] = ns.x;
+      out.ns[1] = ns.y;
+      out.ns[2] = ns.z;
+      if (m.reflective) {
+        flags |= kGReflective;
+        if (P.sampler == 2u) {
+          const double cos_in = fabs(cos_facing);
+          const double area_pdf =
+              smax(c.pdf_omega * cos_in / smax(t * t, 1e-24), 1e-12);  // render.cpp:86-88
+          if (!(area_pdf > 0)) atomicOr(err, kErrBadAreaPdf);
+          // level_for_footprint (hash_grid.cpp:34-44) via host-derived thresholds
+          const double r = 1.0 / sqrt(area_pdf) / sc.base_tile;
+          uint32_t level = 0;
+#pragma unroll
+          for (int k = 1; k <= 16; ++k) level += (r >= sc.level_thr[k]) ? 1u : 0u;
+          if (fabs(length(ns) - 1.0) > 1e-4) atomicOr(err, kErrNonUnitNormal);
+          const double ju1 = rng_draw(rk, kDrawJu1);
+          const double ju2 = rng_draw(rk, kDrawJu2);
+          key = make_key(pos, ns, level, ju1, ju2, sc.base_tile, g.normal_bits, g.jitter_scale);
+          h = hash_key(key);
+          need = true;
+        }
+      }
+      out.flags = flags;
+    }
+  }
+
+  // Warp-cooperative lookup: one probe per distinct hash in the warp.
+  const unsigned need_mask = __ballot_sync(kFull, need);
+  if (need) {
+    const unsigned peers = __match_any_sync(need_mask, h) & need_mask;
+    const int leader = __ffs(peers) - 1;
+    uint32_t slot = 0;
+    if (int(lane) == leader) slot = probe_insert(g, key, h);
+    slot = __shfl_sync(peers, slot, leader);
+    const int lqx = __shfl_sync(peers, key.qx, leader);
+    const int lqy = __shfl_sync(peers, key.qy, leader);
+    const int lqz = __shfl_sync(peers, key.qz, leader);
+    const uint32_t lqn = __shfl_sync(peers, key.qn, leader);
+    const uint32_t llv = __shfl_sync(peers, key.level, leader);
+    if (lqx != key.qx || lqy != key.qy || lqz != key.qz || lqn != key.qn || llv != key.level)
+      slot = probe_insert(g, key, h);  // 64-bit hash collision inside the warp
+    out.slot = slot;
+    const unsigned fb = __ballot_sync(need_mask, slot == kFallback);
+    if (int(lane) == __ffs(need_mask) - 1) {
+      atomicAdd(g.counters + kCntLookups, (unsigned long long)__popc(need_mask));
+      if (fb) atomicAdd(g.counters + kCntFallback, (unsigned long long)__popc(fb));
+    }
+  }
+  if (active) gbuf[idx] = out;
+}
+
+// ---------------------------------------------------------------------------
+// k_sample: sample_light + nee_estimate (estimators.cpp:28-106)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassParams P,
+                                                const GBuf* __restrict__ gbuf,
+                                                SampleRec* __restrict__ srec,
+                                                uint32_t* __restrict__ keys,
+                                                uint32_t* __restrict__ vals,
+                                                double* __restrict__ q_before) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= P.n) return;
+  uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
+  const GBuf gb = gbuf[idx];
+  keys[idx] = kInvalidKey;
+  vals[idx] = idx;
+  if (!(gb.flags & kGReflective)) return;
+  const double u1 = rng_draw(gb.rng, kDrawU1);
+  const double u2 = rng_draw(gb.rng, kDrawU2);
+  const double u3 = rng_draw(gb.rng, kDrawU3);
+
+  SampleRec r;
+  r.flags = 0;
+  r.s = 0;
+  r.total = 0;
+  uint32_t e;
+  if (P.sampler == 2u) {
+    const bool fallback = gb.slot == kFallback;
+    const uint32_t cell = fallback ? 0u : g.slot_cell[gb.slot];
+    const size_t row = fallback ? 0 : size_t(cell) * g.M;
+    const double* cdf = fallback ? g.t_cdf : g.cdf + row;
+    const uint32_t* ends = fallback ? g.t_ends : g.ends + row;
+    // sample_cluster (cut.cpp:97-106): upper_bound of u1 * total
+    const double total = cdf[g.M - 1];
+    const double target = u1 * total;
+    uint32_t lo = 0, cnt = g.M;
+    while (cnt > 0) {
+      const uint32_t step = cnt >> 1;
+      if (!(target < cdf[lo + step])) {
+        lo += step + 1;
+        cnt -= step + 1;
+      } else {
+        cnt = step;
+      }
+    }
+    const uint32_t s = lo == g.M ? g.M - 1 : lo;
+    const uint32_t begin = s == 0 ? 0u : ends[s - 1];
+    const uint32_t size = ends[s] - begin;
+    const double clo = s == 0 ? 0.0 : cdf[s - 1];
+    const double span = cdf[s] - clo;
+    const double frac = span > 0 ? clampd((u1 * total - clo) / span, 0.0, 1.0) : 0.0;
+    const uint32_t offset = min(size - 1, uint32_t(frac * double(size)));
+    e = sc.order[begin + offset];
+    r.pin = 1.0 / double(size);
+    r.total = total;
+    r.s = s;
+    r.flags = kSLearned;
+    if (fallback) {
+      q_before[idx] = g.t_q[s];  // the fallback cut is never updated
+    } else {
+      keys[idx] = cell * g.M + s;
+    }
+  } else if (P.sampler == 0u) {
+    const uint32_t n = sc.num_lights;
+    e = min(n - 1, uint32_t(u1 * double(n)));
+    r.pin = 1.0 / double(n);
+  } else {
+    const uint32_t n = sc.num_lights;
+    const double back = sc.energy_cdf[n - 1];
+    const double target = u1 * back;
+    uint32_t lo = 0, cnt = n;
+    while (cnt > 0) {
+      const uint32_t step = cnt >> 1;
+      if (!(target < sc.energy_cdf[lo + step])) {
+        lo += step + 1;
+        cnt -= step + 1;
+      } else {
+        cnt = step;
+      }
+    }
+    e = lo == n ? n - 1 : lo;
+    r.pin = sc.emitter_energy[e] / back;
+  }
+
+  const LightRec& L = sc.lights[e];
+  r.pdf_area = L.pdf_area;
+  if (!(L.pdf_area > 0)) atomicOr(err, kErrDegenerateLight);
+  // sample_triangle_point, scene.cpp:49-59
+  const double su = sqrt(u2);
+  const double b0 = 1.0 - su;
+  const double b1 = u3 * su;
+  const V3 point = ld3(L.p0) * b0 + ld3(L.p1) * b1 + ld3(L.p2) * (1.0 - b0 - b1);
+  // nee_estimate, estimators.cpp:82-106
+  const V3 pos = ld3(gb.pos);
+  const V3 ns = ld3(gb.ns);
+  r.c[0] = r.c[1] = r.c[2] = 0;
+  r.v = 0;
+  V3 to_light = point - pos;
+  const double d2 = dot(to_light, to_light);
+  if (!(d2 < 1e-24)) {
+    const double d = sqrt(d2);
+    to_light = to_light / d;
+    const double cos_x = dot(ns, to_light);
+    if (!(cos_x <= 0)) {
+      const double cos_y = dot(ld3(L.n), -to_light);
+      if (!(cos_y <= 0) && !occluded(sc, pos, point, err)) {
+        const MatRec& m = sc.mats[gb.flags & kGMatMask];
+        const double geometry = cos_x * cos_y / d2;
+        const V3 contrib = ld3(m.albedo) * (1.0 / kPi) * ld3(L.emission) * geometry;
+        r.c[0] = contrib.x;
+        r.c[1] = contrib.y;
+        r.c[2] = contrib.z;
+        r.flags |= kSNonzero;
+        if (P.sampler == 2u) r.v = luminance(contrib) / (r.pin * r.pdf_area);
+      }
+    }
+  }
+  // update_q's argument check (cut.cpp:78-80); the fallback cut is never updated
+  if (P.sampler == 2u && gb.slot != kFallback && !(r.v >= 0 && isfinite(r.v)))
+    atomicOr(err, kErrBadValue);
+  srec[idx] = r;
+}
+
+// ---------------------------------------------------------------------------
+// stable LSD radix sort of (key, val) pairs, 8-bit digits
+// ---------------------------------------------------------------------------
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsItems = 16;  // per thread
+constexpr int kRsTile = kRsThreads * kRsItems;
+constexpr int kRsWarpSpan = 32 * kRsItems;
+
+__global__ void __launch_bounds__(kRsThreads) rs_hist(const uint32_t* __restrict__ keys,
+                                                      uint32_t n, int shift,
+                                                      uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * kRsTile;
+  for (int i = 0; i < kRsItems; ++i) {
+    const uint32_t j = base + i * kRsThreads + threadIdx.x;
+    if (j < n) atomicAdd(&h[(keys[j] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of `total` counters in place, one block.
+__global__ void __launch_bounds__(1024) rs_scan(uint32_t* __restrict__ hist, uint32_t total) {
+  __shared__ uint32_t warp_sums[32];
+  const uint32_t t = threadIdx.x;
+  const uint32_t per = (total + 1023u) / 1024u;
+  const uint32_t b = t * per, e = min(total, b + per);
+  uint32_t sum = 0;
+  for (uint32_t i = b; i < e; ++i) sum += hist[i];
+  // block exclusive scan of `sum`
+  uint32_t x = sum;
+  const uint32_t lane = t & 31u, w = t >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= uint32_t(o)) x += y;
+  }
+  if (lane == 31) warp_sums[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t ws = warp_sums[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, ws, o);
+      if (lane >= uint32_t(o)) ws += y;
+    }
+    warp_sums[lane] = ws;
+  }
+  __syncthreads();
+  uint32_t run = x - sum + (w > 0 ? warp_sums[w - 1] : 0u);
+  for (uint32_t i = b; i < e; ++i) {
+    const uint32_t v = hist[i];
+    hist[i] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin,
+                                                         uint32_t* __restrict__ kout,
+                                                         uint32_t* __restrict__ vout,
+                                                         uint32_t n, int shift,
+                                                         const uint32_t* __restrict__ offs) {
+  __shared__ uint32_t wh[kRsWarps][256];
+  __shared__ uint32_t base_off[256];
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  for (int d = lane; d < 256; d += 32) wh[w][d] = 0;
+  base_off[threadIdx.x] = offs[threadIdx.x * gridDim.x + blockIdx.x];
+  __syncwarp();
+  const uint32_t base = blockIdx.x * kRsTile + w * kRsWarpSpan;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint32_t k[kRsItems], v[kRsItems], rank[kRsItems];
+#pragma unroll
+  for (int r = 0; r < kRsItems; ++r) {
+    const uint32_t j = base + r * 32 + lane;
+    const bool ok = j < n;
+    k[r] = ok ? kin[j] : 0u;
+    v[r] = ok ? vin[j] : 0u;
+    const uint32_t d = ok ? (k[r] >> shift) & 255u : 256u + lane;
+    const unsigned peers = __match_any_sync(kFull, d);
+    const uint32_t before = ok ? wh[w][d] : 0u;
+    rank[r] = before + __popc(peers & lt_mask);
+    __syncwarp();
+    if (ok && (peers & lt_mask) == 0) wh[w][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {  // cross-warp exclusive prefix per digit
+    const uint32_t d = threadIdx.x;
+    uint32_t run = 0;
+    for (int ww = 0; ww < kRsWarps; ++ww) {
+      const uint32_t c = wh[ww][d];
+      wh[ww][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRsItems; ++r) {
+    const uint32_t j = base + r * 32 + lane;
+    if (j < n) {
+      const uint32_t d = (k[r] >> shift) & 255u;
+      const uint32_t pos = base_off[d] + wh[w][d] + rank[r];
+      kout[pos] = k[r];
+      vout[pos] = v[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_fold: update_q (cut.cpp:76-86) applied per (cell, cluster) segment in
+// canonical order; q_before feeds the deferred radiance.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
+                                              const uint32_t* __restrict__ keys,
+                                              const uint32_t* __restrict__ vals,
+                                              const SampleRec* __restrict__ srec,
+                                              double* __restrict__ q_before) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const uint32_t k = keys[i];
+  if (k == kInvalidKey) return;
+  if (i > 0 && keys[i - 1] == k) return;
+  const uint32_t cell = k / g.M;
+  const size_t at = size_t(k);
+  double q = g.q[at];
+  uint32_t vis = g.visits[at];
+  for (uint32_t j = i; j < P.n && keys[j] == k; ++j) {
+    const uint32_t idx = vals[j];
+    const double v = srec[idx].v;
+    q_before[idx] = q;
+    const double a = P.harmonic ? 1.0 / (1.0 + double(vis)) : P.alpha;
+    q = smax((1.0 - a) * q + a * v, g.eps_q);
+    ++vis;
+  }
+  g.q[at] = q;
+  g.visits[at] = vis;
+  g.touched[cell] = 1u;
+}
+
+// ---------------------------------------------------------------------------
+// k_accumulate: deferred radiance (estimators.cpp:100-101 with the live
+// q_before of sample_cluster, cut.cpp:105) + Framebuffer::add_sample
+// (image.hpp:56-60) in per-pixel sample order.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
+                                                    const GBuf* __restrict__ gbuf,
+                                                    const SampleRec* __restrict__ srec,
+                                                    const double* __restrict__ q_before,
+                                                    Framebuf fb) {
+  const uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t npix = P.n / P.spp_pp;
+  if (pix >= npix) return;
+  const uint32_t px = pix % P.width;
+  const uint32_t py = P.row_begin + pix / P.width;
+  const size_t fi = size_t(py) * P.width + px;
+  V3 sum = ld3(fb.sum + 3 * fi);
+  unsigned long long cnt = fb.count[fi];
+  for (uint32_t s = 0; s < P.spp_pp; ++s) {
+    const uint32_t idx = pix * P.spp_pp + s;
+    const uint32_t flags = gbuf[idx].flags;
+    V3 L{0.0, 0.0, 0.0};
+    if (flags & kGEmit) L = L + ld3(sc.mats[flags & kGMatMask].emission);
+    if (flags & kGReflective) {
+      const SampleRec& r = srec[idx];
+      V3 rad{0.0, 0.0, 0.0};
+      if (r.flags & kSNonzero) {
+        double pdf_sel;
+        if (r.flags & kSLearned) {
+          const double p = q_before[idx] / r.total;
+          pdf_sel = p * r.pin;
+        } else {
+          pdf_sel = r.pin;
+        }
+        const double den = pdf_sel * r.pdf_area;
+        rad = V3{r.c[0], r.c[1], r.c[2]} / den;
+      }
+      L = L + V3{1.0, 1.0, 1.0} * rad;
+    }
+    sum = sum + L;
+    cnt += 1;
+  }
+  fb.sum[3 * fi] = sum.x;
+  fb.sum[3 * fi + 1] = sum.y;
+  fb.sum[3 * fi + 2] = sum.z;
+  fb.count[fi] = cnt;
+}
+
+// ---------------------------------------------------------------------------
+// k_split: split_collapse (cut.cpp:119-190) + rebuild_ends + serial
+// rebuild_cdf for every touched cell (render.cpp:185-200).  One warp per
+// cell, cut rows staged in shared memory.
+// ---------------------------------------------------------------------------
+struct WarpArg {
+  double val;
+  uint32_t idx;  // kNoSlot = none
+};
+
+// max val, lowest index on ties (cut.cpp:125-131: strict '>' scanning up)
+__device__ __forceinline__ WarpArg warp_argmax(WarpArg a) {
+  for (int o = 16; o > 0; o >>= 1) {
+    WarpArg b;
+    b.val = __shfl_xor_sync(kFull, a.val, o);
+    b.idx = __shfl_xor_sync(kFull, a.idx, o);
+    if (b.idx != kNoSlot &&
+        (a.idx == kNoSlot || b.val > a.val || (b.val == a.val && b.idx < a.idx)))
+      a = b;
+  }
+  return a;
+}
+// min val, lowest index on ties (cut.cpp:146-151: strict '<' scanning up)
+__device__ __forceinline__ WarpArg warp_argmin(WarpArg a) {
+  for (int o = 16; o > 0; o >>= 1) {
+    WarpArg b;
+    b.val = __shfl_xor_sync(kFull, a.val, o);
+    b.idx = __shfl_xor_sync(kFull, a.idx, o);
+    if (b.idx != kNoSlot &&
+        (a.idx == kNoSlot || b.val < a.val || (b.val == a.val && b.idx < a.idx)))
+      a = b;
+  }
+  return a;
+}
+
+__global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t iterations,
+                        uint32_t* changes_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint32_t wpb = blockDim.x >> 5;
+  const uint32_t M = g.M;
+  // per warp: qA, qB (double), nA, nB, vA, vB (u32)
+  double* qA = reinterpret_cast<double*>(smem) + size_t(wib) * 2 * M;
+  double* qB = qA + M;
+  uint32_t* nA = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(smem) + size_t(wpb) * 2 * M) +
+                 size_t(wib) * 4 * M;
+  uint32_t* nB = nA + M;
+  uint32_t* vA = nB + M;
+  uint32_t* vB = vA + M;
+  const uint32_t ncells = uint32_t(*reinterpret_cast<volatile unsigned long long*>(g.counters + kCntCells));
+  const double eps = g.eps_q;
+  uint32_t my_changes = 0;
+  for (uint32_t cell = blockIdx.x * wpb + wib; cell < ncells; cell += gridDim.x * wpb) {
+    if (!g.touched[cell]) continue;  // warp-uniform
+    const size_t row = size_t(cell) * M;
+    for (uint32_t i = lane; i < M; i += 32) {
+      qA[i] = g.q[row + i];
+      nA[i] = g.node_ids[row + i];
+      vA[i] = g.visits[row + i];
+    }
+    __syncwarp();
+    for (uint32_t it = 0; it < iterations; ++it) {
+      WarpArg sp{0.0, kNoSlot};
+      for (uint32_t i = lane; i < M; i += 32) {
+        if (sc.lt[nA[i]].left < 0) continue;   // tree leaf: unsplittable
+        if (qA[i] * 0.5 < eps) continue;       // halves would fall below the floor
+        if (sp.idx == kNoSlot || qA[i] > sp.val) sp = WarpArg{qA[i], i};
+      }
+      sp = warp_argmax(sp);
+      if (sp.idx == kNoSlot) break;
+      const uint32_t split_at = sp.idx;
+      // Collapse candidates: adjacent leaves with a common parent.  The
+      // parent is a proper ancestor of the split leaf iff the split leaf is
+      // one of the pair (cut leaves are disjoint ranges), cut.cpp:133-145.
+      WarpArg cp{0.0, kNoSlot};
+      for (uint32_t i = lane; i + 1 < M; i += 32) {
+        const int32_t pa = sc.lt[nA[i]].parent;
+        if (pa < 0 || pa != sc.lt[nA[i + 1]].parent) continue;
+        if (i == split_at || i + 1 == split_at) continue;
+        const double mass = qA[i] + qA[i + 1];
+        if (cp.idx == kNoSlot || mass < cp.val) cp = WarpArg{mass, i};
+      }
+      cp = warp_argmin(cp);
+      if (cp.idx == kNoSlot) break;
+      const uint32_t col = cp.idx;
+      if (!(qA[split_at] > threshold * cp.val)) break;
+      // emit the new leaf sequence (cut.cpp:156-181)
+      for (uint32_t i = lane; i < M; i += 32) {
+        if (i == col + 1) continue;
+        const uint32_t pos = i + (i > split_at ? 1u : 0u) - (i > col + 1 ? 1u : 0u);
+        if (i == split_at) {
+          const LtNode nd = sc.lt[nA[i]];
+          const double half = qA[i] * 0.5;
+          nB[pos] = uint32_t(nd.left);
+          nB[pos + 1] = uint32_t(nd.right);
+          qB[pos] = half;
+          qB[pos + 1] = half;
+          vB[pos] = vA[i];
+          vB[pos + 1] = vA[i];
+        } else if (i == col) {
+          nB[pos] = uint32_t(sc.lt[nA[i]].parent);
+          qB[pos] = qA[i] + qA[i + 1];
+          vB[pos] = vA[i] + vA[i + 1];
+        } else {
+          nB[pos] = nA[i];
+          qB[pos] = qA[i];
+          vB[pos] = vA[i];
+        }
+      }
+      __syncwarp();
+      for (uint32_t i = lane; i < M; i += 32) {
+        qA[i] = qB[i];
+        nA[i] = nB[i];
+        vA[i] = vB[i];
+      }
+      __syncwarp();
+      ++my_changes;
+    }
+    // write back node ids, q, visits, ends; serial cdf (cut.cpp:88-95)
+    for (uint32_t i = lane; i < M; i += 32) {
+      g.q[row + i] = qA[i];
+      g.node_ids[row + i] = nA[i];
+      g.visits[row + i] = vA[i];
+      g.ends[row + i] = sc.lt[nA[i]].range_end;
+    }
+    if (lane == 0) {
+      double run = 0;
+      for (uint32_t i = 0; i < M; ++i) {
+        run += qA[i];
+        g.cdf[row + i] = run;
+      }
+      g.touched[cell] = 0u;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && my_changes) atomicAdd(changes_out, my_changes);
+}
+
+__global__ void k_resolve(Framebuf fb, uint32_t npix, double* __restrict__ image) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  const unsigned long long c = fb.count[i];
+  for (int a = 0; a < 3; ++a) image[3 * i + a] = c > 0 ? fb.sum[3 * i + a] / double(c) : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline uint32_t blocks_for(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
+
+void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
+                    const PassBuffers& b, cudaStream_t st) {
+  if (p.n == 0) return;
+  k_primary<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, b.gbuf);
+  count_launch();
+}
+
+void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
+                   const PassBuffers& b, cudaStream_t st) {
+  if (p.n == 0) return;
+  k_sample<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.keys, b.vals,
+                                                  b.q_before);
+  count_launch();
+}
+
+void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
+                 uint32_t** keys_out, uint32_t** vals_out) {
+  uint32_t* ka = b.keys;
+  uint32_t* va = b.vals;
+  uint32_t* kb = b.keys_alt;
+  uint32_t* vb = b.vals_alt;
+  if (n > 1) {
+    const uint32_t nb = blocks_for(n, kRsTile);
+    for (uint32_t shift = 0; shift < key_bits; shift += 8) {
+      rs_hist<<<nb, kRsThreads, 0, st>>>(ka, n, int(shift), b.sort_hist);
+      rs_scan<<<1, 1024, 0, st>>>(b.sort_hist, nb * 256u);
+      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, int(shift), b.sort_hist);
+      count_launch(3);
+      uint32_t* t = ka;
+      ka = kb;
+      kb = t;
+      t = va;
+      va = vb;
+      vb = t;
+    }
+  }
+  *keys_out = ka;
+  *vals_out = va;
+}
+
+void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
+                 const uint32_t* vals, const PassBuffers& b, cudaStream_t st) {
+  if (p.n == 0) return;
+  k_fold<<<blocks_for(p.n, 256), 256, 0, st>>>(g, p, keys, vals, b.srec, b.q_before);
+  count_launch();
+}
+
+void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffers& b,
+                       const Framebuf& fb, cudaStream_t st) {
+  const uint32_t npix = p.spp_pp ? p.n / p.spp_pp : 0;
+  if (npix == 0) return;
+  k_accumulate<<<blocks_for(npix, 256), 256, 0, st>>>(sc, p, b.gbuf, b.srec, b.q_before, fb);
+  count_launch();
+}
+
+void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshold,
+                           uint32_t iterations, uint32_t* changes_out, cudaStream_t st) {
+  const size_t per_warp = size_t(g.M) * 32;  // 2 doubles + 4 u32 per entry
+  uint32_t wpb = uint32_t(96 * 1024 / per_warp);
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1) wpb = 1;
+  const size_t smem = per_warp * wpb;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  k_split<<<148 * 4, wpb * 32, smem, st>>>(sc, g, threshold, iterations, changes_out);
+  count_launch();
+}
+
+void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st) {
+  if (npix == 0) return;
+  k_resolve<<<blocks_for(npix, 256), 256, 0, st>>>(fb, npix, image);
+  count_launch();
+}
+
+}  // namespace rlc

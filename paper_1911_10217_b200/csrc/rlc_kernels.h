@@ -1,0 +1,150 @@
+// rlc_kernels.h -- device-side views and the launchers the host runtime calls.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rlc_common.h"
+
+namespace rlc {
+
+constexpr uint32_t kNoSlot = 0xffffffffu;    // path without an RL lookup
+constexpr uint32_t kFallback = 0xfffffffeu;  // probe exhaustion -> fallback cut
+constexpr uint32_t kInvalidKey = 0xffffffffu;
+
+// G-buffer flags (per path)
+enum : uint32_t {
+  kGHit = 1u << 29,
+  kGEmit = 1u << 30,        // primary hit on the emitting side (render.cpp:79-81)
+  kGReflective = 1u << 31,  // NEE vertex (render.cpp:84)
+  kGMatMask = (1u << 29) - 1,
+};
+// Sample-record flags
+enum : uint32_t { kSNonzero = 1u, kSLearned = 2u };
+
+// Device error bits (mapped to the reference's exceptions by the host).
+enum : uint32_t {
+  kErrNonUnitNormal = 1u,     // make_key, hash_grid.cpp:78-80
+  kErrBadValue = 2u,          // update_q, cut.cpp:78-80
+  kErrDegenerateLight = 4u,   // sample_triangle_point, scene.cpp:50-51
+  kErrBadAreaPdf = 8u,        // level_for_footprint, hash_grid.cpp:35-37
+  kErrStackOverflow = 16u,    // BVH deeper than the traversal stack
+};
+
+// Counters block (u64 each).
+enum : uint32_t { kCntCells = 0, kCntLookups = 1, kCntFallback = 2, kCntChanges = 3,
+                  kCntErr = 4, kCntNum = 8 };
+
+struct alignas(16) GBuf {  // 64 B per path
+  double pos[3];
+  double ns[3];
+  uint64_t rng;
+  uint32_t slot;
+  uint32_t flags;
+};
+
+struct alignas(16) SampleRec {  // 64 B per path
+  double c[3];      // contribution (estimators.cpp:100-101)
+  double pdf_area;
+  double pin;       // learned: pdf_in_cluster; baselines: pdf_light_selection
+  double total;     // learned: frozen cdf total of the cell cut
+  double v;         // feedback value
+  uint32_t s;       // cluster index
+  uint32_t flags;
+};
+
+struct DevScene {
+  const BvhNode* nodes;
+  const TriAccel* tris;
+  const MatRec* mats;
+  const uint32_t* tri_mat;
+  const double* tri_normal;
+  const LightRec* lights;
+  const uint32_t* order;
+  const LtNode* lt;
+  const double* energy_cdf;
+  const double* emitter_energy;
+  uint32_t num_lights;
+  uint32_t num_tris;
+  double shadow_eps;
+  double base_tile;
+  double level_thr[17];
+  CameraConst cam;
+};
+
+struct DevGrid {
+  unsigned long long* slot_keys;  // [capacity][2] packed CellKey (0 = empty)
+  uint32_t* slot_cell;            // [capacity]
+  uint32_t capacity;
+  uint32_t probe_limit;
+  uint32_t normal_bits;
+  uint32_t M;                     // cut size (cluster count)
+  double jitter_scale;
+  // per-cell cut rows [cell][M]
+  uint32_t* node_ids;
+  uint32_t* ends;
+  double* q;
+  double* cdf;
+  uint32_t* visits;
+  uint32_t* cell_key;             // [cell][5]
+  uint32_t* touched;              // [cell]
+  // template cut == fallback cut [M]
+  const uint32_t* t_node;
+  const uint32_t* t_ends;
+  const double* t_q;
+  const double* t_cdf;
+  const uint32_t* t_visits;
+  double eps_q;
+  unsigned long long* counters;   // kCnt*
+};
+
+struct PassParams {
+  uint32_t width;
+  uint32_t row_begin;
+  uint32_t spp_pp;
+  uint32_t pass_index;
+  uint32_t n;           // paths in this launch: rows * width * spp_pp
+  uint32_t sampler;
+  uint64_t seed_mixed;  // mix64(seed)
+  uint64_t zero_mixed;  // mix64(0): the c component of the RNG key
+  double alpha;
+  uint32_t harmonic;
+};
+
+struct PassBuffers {
+  GBuf* gbuf;
+  SampleRec* srec;
+  uint32_t* keys;
+  uint32_t* vals;
+  uint32_t* keys_alt;
+  uint32_t* vals_alt;
+  double* q_before;
+  uint32_t* sort_hist;
+  uint32_t sort_hist_cap;  // entries
+};
+
+struct Framebuf {
+  double* sum;                // [h*w*3]
+  unsigned long long* count;  // [h*w]
+  uint32_t width;
+};
+
+// Each launcher adds its kernel launches to a process-wide counter.
+uint64_t launches();
+
+void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
+                    const PassBuffers& b, cudaStream_t st);
+void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
+                   const PassBuffers& b, cudaStream_t st);
+// Sorts (keys, vals) by key; returns which buffer pair holds the result.
+void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
+                 uint32_t** keys_out, uint32_t** vals_out);
+void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
+                 const uint32_t* vals, const PassBuffers& b, cudaStream_t st);
+void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffers& b,
+                       const Framebuf& fb, cudaStream_t st);
+void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshold,
+                           uint32_t iterations, uint32_t* changes_out, cudaStream_t st);
+void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
+
+}  // namespace rlc

@@ -1,0 +1,309 @@
+"""Python mirror of the reference's public render API (proj/include/rlcuts/)
+over the C-ABI (include/rlcuts_b200.h).
+
+Same names, argument meaning and error behaviour as the reference:
+``std::invalid_argument`` -> ``ValueError``, ``std::out_of_range`` ->
+``IndexError``.  Every call runs on the B200 through librlcuts_b200.so; there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .scenes import Scene
+
+
+class NoDeviceError(RuntimeError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+def _check(status: int):
+    if status == _lib.RLC_OK:
+        return
+    msg = _lib.load().rlc_last_error().decode(errors="replace")
+    if status == _lib.RLC_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == _lib.RLC_ERR_OUT_OF_RANGE:
+        raise IndexError(msg)
+    if status == _lib.RLC_ERR_NO_DEVICE:
+        raise NoDeviceError(msg)
+    raise DeviceError(msg)
+
+
+class SamplerKind(enum.IntEnum):  # estimators.hpp:16-20
+    uniform = 0
+    energy = 1
+    rl_lightcuts = 2
+
+
+class AlphaSchedule(enum.IntEnum):  # cut.hpp:16-19
+    fixed = 0
+    harmonic = 1
+
+
+@dataclass
+class CutConfig:  # cut.hpp:21-28
+    cut_size: int = 128
+    alpha: float = 0.2
+    split_threshold: float = 4.0
+    eps_q: float = -1.0
+    iterations: int = 1
+    alpha_schedule: AlphaSchedule = AlphaSchedule.fixed
+
+    def c(self) -> _lib.CutConfigC:
+        return _lib.CutConfigC(self.cut_size, self.iterations, self.alpha, self.split_threshold,
+                               self.eps_q, int(self.alpha_schedule), 0)
+
+
+@dataclass
+class HashConfig:  # hash_grid.hpp:17-23
+    capacity: int = 1 << 16
+    base_tile: float = 0.0
+    probe_limit: int = 32
+    normal_bits: int = 4
+    jitter_scale: float = 0.0
+
+    def c(self) -> _lib.HashConfigC:
+        return _lib.HashConfigC(self.capacity, self.probe_limit, self.normal_bits, 0,
+                                self.base_tile, self.jitter_scale)
+
+
+@dataclass
+class RenderConfig:  # render.hpp:17-26
+    spp: int = 16
+    passes: int = 4
+    max_depth: int = 1
+    sampler: SamplerKind = SamplerKind.uniform
+    cut: CutConfig = field(default_factory=CutConfig)
+    hash: HashConfig = field(default_factory=HashConfig)
+    seed: int = 1
+    workers: int = 1
+
+    def c(self) -> _lib.RenderConfigC:
+        return _lib.RenderConfigC(self.spp, self.passes, self.max_depth, int(self.sampler),
+                                  self.cut.c(), self.hash.c(), self.seed, self.workers, 0)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _uptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+class RenderContext:
+    """build_context (proj/src/render.cpp:143-157), device resident."""
+
+    def __init__(self, scene: Scene, config: RenderConfig, device: int = 0):
+        lib = _lib.load()
+        self.scene = scene
+        self._desc = scene.desc()
+        self._cfg = config.c()
+        h = C.c_void_p()
+        _check(lib.rlc_context_create(C.byref(self._desc), C.byref(self._cfg), device, C.byref(h)))
+        self.handle = h
+
+    def info(self) -> dict:
+        i = _lib.ContextInfoC()
+        _check(_lib.load().rlc_context_info_get(self.handle, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in _lib.ContextInfoC._fields_}
+
+    @property
+    def base_tile(self) -> float:
+        return self.info()["base_tile"]
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(_lib.load().rlc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+
+    def synchronize(self):
+        _check(_lib.load().rlc_context_synchronize(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.load().rlc_context_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_context(scene: Scene, config: RenderConfig, device: int = 0) -> RenderContext:
+    return RenderContext(scene, config, device)
+
+
+class HashGrid:
+    """HashGrid(hash, init_cut(tree, M, eps)) (proj/src/render.cpp:211-216)."""
+
+    def __init__(self, ctx: RenderContext, config: RenderConfig):
+        self.ctx = ctx
+        self._cfg = config.c()
+        h = C.c_void_p()
+        _check(_lib.load().rlc_grid_create(ctx.handle, C.byref(self._cfg), C.byref(h)))
+        self.handle = h
+
+    def stats(self) -> dict:
+        s = _lib.GridStatsC()
+        _check(_lib.load().rlc_grid_stats_get(self.handle, C.byref(s)))
+        return {"occupied": s.occupied, "cut_size": s.cut_size, "lookups": s.lookups,
+                "fallback_hits": s.fallback_hits}
+
+    def occupied_count(self) -> int:
+        return self.stats()["occupied"]
+
+    def lookup_count(self) -> int:
+        return self.stats()["lookups"]
+
+    def fallback_hits(self) -> int:
+        return self.stats()["fallback_hits"]
+
+    def export(self) -> dict:
+        """Per-cell cut state keyed by CellKey (qx, qy, qz, qn, level)."""
+        st = self.stats()
+        n, m = st["occupied"], st["cut_size"]
+        keys = (_lib.CellKeyC * max(n, 1))()
+        node = np.zeros((max(n, 1), m), np.uint32)
+        ends = np.zeros_like(node)
+        vis = np.zeros_like(node)
+        q = np.zeros((max(n, 1), m), np.float64)
+        cdf = np.zeros_like(q)
+        got = C.c_uint32()
+        _check(_lib.load().rlc_grid_export(self.handle, n, keys, _uptr(node), _uptr(ends), _dptr(q),
+                                           _dptr(cdf), _uptr(vis), C.byref(got)))
+        out = {}
+        for i in range(n):
+            k = keys[i]
+            out[(k.qx, k.qy, k.qz, k.qn, k.level)] = {
+                "node_ids": node[i], "ends": ends[i], "q": q[i], "cdf": cdf[i], "visits": vis[i]}
+        return out
+
+    def template(self) -> dict:
+        m = self.stats()["cut_size"]
+        node = np.zeros(m, np.uint32)
+        ends = np.zeros(m, np.uint32)
+        vis = np.zeros(m, np.uint32)
+        q = np.zeros(m, np.float64)
+        cdf = np.zeros(m, np.float64)
+        eps = C.c_double()
+        _check(_lib.load().rlc_grid_template(self.handle, _uptr(node), _uptr(ends), _dptr(q),
+                                             _dptr(cdf), _uptr(vis), C.byref(eps)))
+        return {"node_ids": node, "ends": ends, "q": q, "cdf": cdf, "visits": vis,
+                "eps_q": eps.value}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.load().rlc_grid_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Framebuffer:
+    """Framebuffer (proj/include/rlcuts/image.hpp:47-63), device resident."""
+
+    def __init__(self, ctx: RenderContext, width: int | None = None, height: int | None = None):
+        self.ctx = ctx
+        self.width = int(width if width is not None else ctx.scene.camera.width)
+        self.height = int(height if height is not None else ctx.scene.camera.height)
+        h = C.c_void_p()
+        _check(_lib.load().rlc_framebuffer_create(ctx.handle, self.width, self.height, C.byref(h)))
+        self.handle = h
+
+    def download(self) -> tuple[np.ndarray, np.ndarray]:
+        s = np.zeros((self.height, self.width, 3), np.float64)
+        c = np.zeros((self.height, self.width), np.uint64)
+        _check(_lib.load().rlc_framebuffer_download(
+            self.handle, _dptr(s), c.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return s, c
+
+    def resolve(self) -> np.ndarray:
+        img = np.zeros((self.height, self.width, 3), np.float64)
+        _check(_lib.load().rlc_framebuffer_resolve(self.handle, _dptr(img)))
+        return img
+
+    def clear(self):
+        _check(_lib.load().rlc_framebuffer_clear(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.load().rlc_framebuffer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def render_pass(ctx: RenderContext, config: RenderConfig, pass_index: int,
+                grid: HashGrid | None, framebuffer: Framebuffer, rows: tuple | None = None,
+                sync: bool = True):
+    """render_pass (proj/src/render.cpp:159-183)."""
+    lib = _lib.load()
+    cfg = config.c()
+    g = grid.handle if grid is not None else None
+    if rows is not None:
+        _check(lib.rlc_render_pass_rows(ctx.handle, C.byref(cfg), pass_index, g,
+                                        framebuffer.handle, rows[0], rows[1]))
+    elif sync:
+        _check(lib.rlc_render_pass(ctx.handle, C.byref(cfg), pass_index, g, framebuffer.handle))
+    else:
+        _check(lib.rlc_render_pass_async(ctx.handle, C.byref(cfg), pass_index, g,
+                                         framebuffer.handle))
+
+
+def end_of_pass_update(grid: HashGrid, ctx: RenderContext, config: CutConfig,
+                       sync: bool = True) -> int | None:
+    """end_of_pass_update (proj/src/render.cpp:185-200); returns the change count."""
+    lib = _lib.load()
+    cut = config.c()
+    if not sync:
+        _check(lib.rlc_end_of_pass_update_async(grid.handle, ctx.handle, C.byref(cut)))
+        return None
+    ch = C.c_uint32()
+    _check(lib.rlc_end_of_pass_update(grid.handle, ctx.handle, C.byref(cut), C.byref(ch)))
+    return ch.value
+
+
+@dataclass
+class RenderResult:  # render.hpp:56-64
+    image: np.ndarray
+    wall_ms: float
+    occupied_cells: int
+    lookups: int
+    fallback_hits: int
+    sc_changes: list
+
+
+def render_frame(ctx: RenderContext, config: RenderConfig) -> RenderResult:
+    """render_frame (proj/src/render.cpp:202-240)."""
+    cam = ctx.scene.camera
+    img = np.zeros((cam.height, cam.width, 3), np.float64)
+    changes = (C.c_uint32 * max(config.passes, 1))()
+    res = _lib.RenderResultC()
+    res.sc_changes = C.cast(changes, C.POINTER(C.c_uint32))
+    cfg = config.c()
+    _check(_lib.load().rlc_render_frame(ctx.handle, C.byref(cfg), _dptr(img), C.byref(res)))
+    return RenderResult(img, res.wall_ms, res.occupied_cells, res.lookups, res.fallback_hits,
+                        list(changes)[:config.passes])
+
+
+def kernel_launches() -> int:
+    return int(_lib.load().rlc_kernel_launches())

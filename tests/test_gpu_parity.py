@@ -1,0 +1,118 @@
+"""GPU parity of the whole per-pass path against the compiled reference
+(oracle/_ref): same scene arrays, same config, workers = 1 (the reference's
+only deterministic mode).  Bit-exact: light selection (through the cut
+state it produces), cut topology, learnt q / cdf / visits, framebuffer sums
+and counts, split-collapse change counts and grid statistics."""
+import numpy as np
+import pytest
+
+from paper_1911_10217_b200 import rlcuts, scenes
+
+pytestmark = pytest.mark.gpu
+
+RL = rlcuts.SamplerKind.rl_lightcuts
+
+
+def run_both(ref, scene, cfg):
+    ctx = rlcuts.build_context(scene, cfg)
+    grid = rlcuts.HashGrid(ctx, cfg) if cfg.sampler == RL else None
+    fb = rlcuts.Framebuffer(ctx)
+    rr = ref.RefRun(scene, cfg)
+    info, rinfo = ctx.info(), rr.info()
+    for k in ("base_tile", "shadow_eps", "num_emitters", "light_tree_nodes", "bvh_nodes"):
+        assert info[k] == rinfo[k], k
+    for p in range(cfg.passes):
+        rlcuts.render_pass(ctx, cfg, p, grid, fb)
+        ch = rlcuts.end_of_pass_update(grid, ctx, cfg.cut) if grid else 0
+        rch, _ = rr.run_pass(p)
+        assert ch == rch, f"pass {p}: split-collapse changes {ch} vs reference {rch}"
+    return ctx, grid, fb, rr
+
+
+def assert_same_state(grid, fb, rr):
+    s, c = fb.download()
+    rs, rc = rr.framebuffer()
+    assert np.array_equal(c, rc)
+    bad = np.argwhere(s != rs)
+    assert bad.size == 0, f"{len(bad)} radiance mismatches, max |d| {np.abs(s - rs).max()}"
+    if grid is None:
+        return
+    st, rst = grid.stats(), rr.stats()
+    assert st == rst
+    cells, rcells = grid.export(), rr.export()
+    assert set(cells) == set(rcells)
+    for k, v in cells.items():
+        for f in ("node_ids", "ends", "q", "cdf", "visits"):
+            assert np.array_equal(v[f], rcells[k][f]), (k, f)
+
+
+def test_cornell2_rl_bit_exact(ref):
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=64, height=48)
+    cfg = rlcuts.RenderConfig(spp=4, passes=4, sampler=RL)
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+    assert grid.fallback_hits() == 0 and grid.occupied_count() > 100
+
+
+def test_c1_analog_rl_bit_exact(ref):
+    scene, st = scenes.config_scene("c1")
+    scene = scene.with_resolution(64, 64)
+    cfg = rlcuts.RenderConfig(spp=8, passes=8, sampler=RL,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+
+
+def test_harmonic_multi_iteration_small_cut(ref):
+    scene = scenes.cornell_grid(2, 3, dome_triangles=512, width=40, height=40)
+    cfg = rlcuts.RenderConfig(
+        spp=6, passes=3, sampler=RL, seed=9,
+        cut=rlcuts.CutConfig(cut_size=32, split_threshold=2.0, iterations=3,
+                             alpha_schedule=rlcuts.AlphaSchedule.harmonic))
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+
+
+def test_jittered_keys_and_fine_normals(ref):
+    scene = scenes.cornell_grid(1, 2, dome_triangles=128, width=48, height=48)
+    cfg = rlcuts.RenderConfig(spp=4, passes=2, sampler=RL,
+                              hash=rlcuts.HashConfig(jitter_scale=1.0, normal_bits=6))
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+
+
+@pytest.mark.parametrize("sampler", [rlcuts.SamplerKind.uniform, rlcuts.SamplerKind.energy])
+def test_baseline_samplers_bit_exact(ref, sampler):
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=40)
+    cfg = rlcuts.RenderConfig(spp=2, passes=2, sampler=sampler)
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+
+
+def test_render_frame_matches_reference(ref):
+    scene = scenes.cornell_grid(2, 1, dome_triangles=32, width=32, height=32)
+    cfg = rlcuts.RenderConfig(spp=4, passes=2, sampler=RL)
+    ctx = rlcuts.build_context(scene, cfg)
+    res = rlcuts.render_frame(ctx, cfg)
+    rres = ref.ref_render_frame(scene, cfg)
+    assert np.array_equal(res.image, rres["image"])
+    assert res.sc_changes == rres["sc_changes"]
+    assert (res.occupied_cells, res.lookups, res.fallback_hits) == (
+        rres["occupied"], rres["lookups"], rres["fallback_hits"])
+
+
+def test_errors_match_reference_exceptions(ref):
+    scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=8, height=8)
+    cfg = rlcuts.RenderConfig(spp=3, passes=2, sampler=RL)
+    ctx = rlcuts.build_context(scene, cfg)
+    fb = rlcuts.Framebuffer(ctx)
+    grid = rlcuts.HashGrid(ctx, cfg)
+    with pytest.raises(ValueError, match="divisible"):
+        rlcuts.render_pass(ctx, cfg, 0, grid, fb)
+    cfg2 = rlcuts.RenderConfig(spp=2, passes=2, sampler=RL)
+    with pytest.raises(ValueError, match="hash grid"):
+        rlcuts.render_pass(ctx, cfg2, 0, None, fb)
+    with pytest.raises(ValueError, match="capacity"):
+        rlcuts.HashGrid(ctx, rlcuts.RenderConfig(sampler=RL, hash=rlcuts.HashConfig(capacity=0)))
+    with pytest.raises(ValueError, match="cut size"):
+        rlcuts.HashGrid(ctx, rlcuts.RenderConfig(sampler=RL, cut=rlcuts.CutConfig(cut_size=0)))
