@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the RL-lightcuts direct-lighting path (arXiv 1911.10217).
+
+Metric (BASELINE.json): learnt light samples per second -- each one a cut
+sample, a shadow ray and an RL update -- counted exactly like the
+reference's RenderResult::lookups (proj/src/hash_grid.cpp:114).
+
+A step is one frame of the configured workload: render_pass (primary ray,
+cell hash, cut sample, shadow ray, deferred RL fold, radiance) followed by
+end_of_pass_update (split-collapse + cdf rebuild), the real-time temporal
+learning loop of config c3 (1 spp per frame).  Inputs (scene, BVH, light
+tree, cut tables) are resident in HBM before the timed region; the working
+set (~0.5 GB for c3) is larger than L2, so no explicit flush is done.
+
+  python bench.py                       # our B200 path, N=1, config c3
+  python bench.py --impl reference      # the reference CPU library arm
+  torchrun --nproc-per-node N bench.py --gpus N   # N ranks, screen-band sharded
+
+One JSON line is printed by rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "light samples/sec (sample+shadow ray+RL update)"
+UNIT = "light samples/s"
+WORKLOADS = {
+    "c1": "c1: 1 Cornell box, light tessellated into 1,024 emissive tris, 256x256, "
+          "1 spp/frame, base_tile 1/16, M=128",
+    "c2": "c2: 4x4 mutually occluding Cornell boxes, 16,384 emissive tris, 1280x720, "
+          "4 spp/frame (64 spp over 16 frames), M=128",
+    "c3": "c3: procedural maze, 1,000,000 emissive tris, 1920x1080, 1 spp/frame "
+          "(64 frames), M=128, hash capacity 65,536",
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def make_config(name: str):
+    from paper_1911_10217_b200 import rlcuts, scenes
+    scene, st = scenes.config_scene(name)
+    cfg = rlcuts.RenderConfig(spp=st["spp"], passes=st["passes"],
+                              sampler=rlcuts.SamplerKind.rl_lightcuts,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    return scene, cfg
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks" line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# roofline bookkeeping
+# ---------------------------------------------------------------------------
+NODE_B, TRI_B = 64, 72     # reference BVH node / Moller-Trumbore triangle bytes
+PRIMARY_FIXED_B = 64 + 24  # G-buffer record write + hash probe
+SAMPLE_FIXED_B = 64 + 64 + 24 + 8 + 96 + 64 + 8  # gbuf read, cdf search, cluster
+#   record, order+tri id, triangle+emission, sample record write, sort record write
+
+
+def traversal_stats(name: str) -> dict | None:
+    p = os.path.join(ROOT, "profiles", "traversal_stats.json")
+    try:
+        return json.load(open(p))[name]
+    except Exception:
+        return None
+
+
+def measured_peaks() -> tuple[float, str]:
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config: str, kernel: str) -> float | None:
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return float(json.load(open(p))[config][kernel])
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the unmodified reference library)
+# ---------------------------------------------------------------------------
+def cpu_reference_run(scene, cfg, passes: int, warmup: int, min_seconds: float,
+                      downscale: int):
+    """Times the reference render_pass + end_of_pass_update (workers = all
+    host cores) on the same scene at 1/downscale^2 of the pixels."""
+    import oracle
+    from paper_1911_10217_b200 import rlcuts
+    cores = os.cpu_count() or 1
+    cam = scene.camera
+    small = scene.with_resolution(max(cam.width // downscale, 1), max(cam.height // downscale, 1))
+    rcfg = rlcuts.RenderConfig(spp=cfg.spp, passes=cfg.passes, sampler=cfg.sampler, cut=cfg.cut,
+                               hash=cfg.hash, seed=cfg.seed, workers=cores)
+    run = oracle.RefRun(small, rcfg)
+    for p in range(warmup):
+        run.run_pass(p)
+    l0 = run.stats()["lookups"]
+    total_ms = 0.0
+    done = 0
+    per_step = []
+    for p in range(warmup, warmup + max(passes, 1) + 10000):
+        before = run.stats()["lookups"]
+        _, ms = run.run_pass(p)
+        total_ms += ms
+        per_step.append((run.stats()["lookups"] - before, ms))
+        done += 1
+        if done >= passes and total_ms / 1e3 >= min_seconds:
+            break
+        if done >= passes and min_seconds <= 0:
+            break
+    lookups = run.stats()["lookups"] - l0
+    value = lookups / (total_ms / 1e3)
+    sample = (f"{done} frames of the {small.name} scene at {small.camera.width}x"
+              f"{small.camera.height} (1/{downscale * downscale} of the pixels), "
+              f"{lookups} light samples, reference render_pass + end_of_pass_update, "
+              f"workers={cores}")
+    return value, cores, sample, total_ms / done, per_step
+
+
+def run_reference_arm(args, rank: int, world: int):
+    if rank != 0:
+        return
+    scene, cfg = make_config(args.config)
+    value, cores, sample, ms_step, _ = cpu_reference_run(
+        scene, cfg, passes=args.steps, warmup=args.warmup, min_seconds=0.0,
+        downscale=args.cpu_downscale)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOADS[args.config]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+
+    from paper_1911_10217_b200 import rlcuts
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(local_rank)
+
+    scene, cfg = make_config(args.config)
+    t0 = time.perf_counter()
+    ctx = rlcuts.build_context(scene, cfg, device=local_rank)
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    grid = rlcuts.HashGrid(ctx, cfg)
+    fb = rlcuts.Framebuffer(ctx)
+    H = scene.camera.height
+    r0, r1 = (H * rank) // world, (H * (rank + 1)) // world
+    rows = None if world == 1 else (r0, r1)
+
+    def step(p):
+        if rows is None:
+            rlcuts.render_pass(ctx, cfg, p, grid, fb, sync=False)
+        else:
+            rlcuts.render_pass(ctx, cfg, p, grid, fb, rows=rows)
+        rlcuts.end_of_pass_update(grid, ctx, cfg.cut, sync=False)
+
+    for p in range(args.warmup):
+        step(p)
+    ctx.synchronize()
+    ctx.stage_times()
+    ctx.enable_timing(True)
+    l0 = grid.lookup_count()
+    launches0 = rlcuts.kernel_launches()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for p in range(args.warmup, args.warmup + args.steps):
+        step(p)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = rlcuts.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1)
+    lookups = grid.lookup_count() - l0
+    stages = ctx.stage_times()
+    ctx.enable_timing(False)
+    if dist is not None:
+        t = torch.tensor([ms, float(lookups)], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, lookups = float(mx[0]), int(sm[1])
+    value = lookups / (ms / 1e3)
+    st = grid.stats()
+
+    # roofline of the dominant kernel
+    peak, peak_src = measured_peaks()
+    trav = traversal_stats(args.config)
+    dom = max(("primary", "sample"), key=lambda k: stages[k][0])
+    dom_ms, dom_n = stages[dom]
+    roof = None
+    if trav is not None and dom_n > 0:
+        paths_per_launch = (scene.camera.width * (r1 - r0) * (cfg.spp // cfg.passes))
+        samples_per_launch = (lookups / world) / args.steps if world > 1 else lookups / args.steps
+        if dom == "primary":
+            per_unit = PRIMARY_FIXED_B + NODE_B * trav["primary_nodes"] + TRI_B * trav["primary_tris"]
+            units = paths_per_launch
+            unit_name = "path"
+        else:
+            sh = trav["shadow_rays_per_sample"]
+            per_unit = SAMPLE_FIXED_B + sh * (NODE_B * trav["shadow_nodes"] + TRI_B * trav["shadow_tris"])
+            units = samples_per_launch
+            unit_name = "light sample"
+        bytes_per_launch = per_unit * units
+        achieved = bytes_per_launch / (dom_ms / dom_n / 1e3) / 1e9
+        tr = ncu_traffic(args.config, dom)
+        roof = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": tr, "bytes_per_unit": per_unit, "unit_of_work": unit_name,
+                "units_per_launch": units, "avg_launch_ms": dom_ms / dom_n}
+
+    # end to end through the C-ABI render_frame: host image out, grid created
+    # inside the call (the reference's render_frame, render.cpp:202-240)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        ecfg = rlcuts.RenderConfig(spp=args.steps * (cfg.spp // cfg.passes), passes=args.steps,
+                                   sampler=cfg.sampler, cut=cfg.cut, hash=cfg.hash, seed=cfg.seed + 1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = rlcuts.render_frame(ctx, ecfg)
+        wall = time.perf_counter() - t0
+        npix = scene.camera.width * scene.camera.height
+        e2e = {"value": res.lookups / wall, "unit": UNIT,
+               "h2d_bytes_per_step": (176 + 28 * st["cut_size"]) / args.steps,
+               "d2h_bytes_per_step": (24 * npix + 4 * args.steps + 32) / args.steps,
+               "wall_ms": wall * 1e3, "call": "rlc_render_frame"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, sample, _, _ = cpu_reference_run(
+                scene, cfg, passes=2, warmup=1, min_seconds=args.cpu_seconds,
+                downscale=args.cpu_downscale)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
+        except Exception as ex:  # the reference library is test infrastructure
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config],
+                       "frames_timed": args.steps,
+                       "l2": "no flush: resident scene+cut+pass buffers exceed the 126 MB L2",
+                       "parallelism": f"screen bands x{world}" if world > 1 else "single GPU",
+                       "cells": st["occupied"], "fallback_hits": st["fallback_hits"]},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+            "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+            "context_build_s": build_s,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-downscale", type=int, default=4)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)  # timing rule: at least 3 warm-up steps
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -157,6 +157,15 @@ rlc_status rlc_context_info_get(const rlc_context* ctx, rlc_context_info* info);
 rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream);
 rlc_status rlc_context_synchronize(rlc_context* ctx);
 
+/* Per-stage device timing with CUDA events on the context stream (bench
+ * evidence).  Stages: 0 primary, 1 sample+shadow, 2 sort, 3 fold,
+ * 4 accumulate, 5 split-collapse.  rlc_context_stage_times synchronizes,
+ * returns accumulated milliseconds and launch counts per stage since the
+ * last call, and resets them. */
+#define RLC_NUM_STAGES 6
+rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable);
+rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts);
+
 /* ---- hash grid: HashGrid(hash, init_cut(tree, M, eps))
  *      (proj/src/render.cpp:211-216, proj/src/hash_grid.cpp:102-111,
  *       proj/src/cut.cpp:27-74) --------------------------------------- */

@@ -86,6 +86,8 @@ SIGNATURES = {
     "rlc_context_info_get": (C.c_int, [_P, C.POINTER(ContextInfoC)]),
     "rlc_context_set_stream": (C.c_int, [_P, _P]),
     "rlc_context_synchronize": (C.c_int, [_P]),
+    "rlc_context_enable_timing": (C.c_int, [_P, C.c_int]),
+    "rlc_context_stage_times": (C.c_int, [_P, _dp, _u32p]),
     "rlc_grid_create": (C.c_int, [_P, C.POINTER(RenderConfigC), _PP]),
     "rlc_grid_destroy": (C.c_int, [_P]),
     "rlc_grid_stats_get": (C.c_int, [_P, C.POINTER(GridStatsC)]),

@@ -121,6 +121,39 @@ struct rlc_context {
   rlc::DevScene dev{};
   DeviceArena arena;
   unsigned long long* counters = nullptr;  // error bits for grid-less passes
+  // per-stage CUDA-event timing (rlc_context_enable_timing)
+  bool timing = false;
+  struct Mark {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<Mark> marks;
+  cudaEvent_t take_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      RLC_CK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  // Brackets the launches of one stage with events on the context stream.
+  template <class F>
+  void stage(int id, F&& launch) {
+    if (!timing || marks.size() >= 200000) {
+      launch();
+      return;
+    }
+    const cudaEvent_t a = take_event(), b = take_event();
+    RLC_CK(cudaEventRecord(a, stream));
+    launch();
+    RLC_CK(cudaEventRecord(b, stream));
+    marks.push_back(Mark{id, a, b});
+  }
+  ~rlc_context() {
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  }
   // per-pass scratch, grown on demand
   DeviceArena scratch;
   rlc::PassBuffers pb{};
@@ -216,14 +249,14 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   if (grid) g = grid->dev;
   else g.counters = ctx->counters;
   cudaStream_t st = ctx->stream;
-  rlc::launch_primary(ctx->dev, g, p, ctx->pb, st);
-  rlc::launch_sample(ctx->dev, g, p, ctx->pb, st);
+  ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, g, p, ctx->pb, st); });
+  ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, g, p, ctx->pb, st); });
   if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS) {
-    uint32_t *k, *v;
-    rlc::launch_sort(ctx->pb, n, grid->key_bits, st, &k, &v);
-    rlc::launch_fold(g, p, k, v, ctx->pb, st);
+    uint32_t *k = nullptr, *v = nullptr;
+    ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, n, grid->key_bits, st, &k, &v); });
+    ctx->stage(3, [&] { rlc::launch_fold(g, p, k, v, ctx->pb, st); });
   }
-  rlc::launch_accumulate(ctx->dev, p, ctx->pb, fb->fb, st);
+  ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, p, ctx->pb, fb->fb, st); });
   RLC_CK(cudaGetLastError());
 }
 
@@ -238,8 +271,11 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
   require(grid != nullptr && ctx != nullptr && cut != nullptr,
           "end_of_pass_update: null argument");
   require(grid->ctx == ctx, "end_of_pass_update: grid belongs to another context");
-  rlc::launch_split_collapse(ctx->dev, grid->dev, cut->split_threshold, cut->iterations,
-                             d_changes, ctx->stream);
+  rlc_context* c = const_cast<rlc_context*>(ctx);
+  c->stage(5, [&] {
+    rlc::launch_split_collapse(ctx->dev, grid->dev, cut->split_threshold, cut->iterations,
+                               d_changes, ctx->stream);
+  });
   RLC_CK(cudaGetLastError());
 }
 
@@ -347,6 +383,34 @@ rlc_status rlc_context_synchronize(rlc_context* ctx) {
   return guarded([&] {
     require(ctx != nullptr, "rlc_context_synchronize: null context");
     RLC_CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_enable_timing: null context");
+    ctx->timing = enable != 0;
+  });
+}
+
+rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_stage_times: null context");
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
+    double acc[RLC_NUM_STAGES] = {};
+    uint32_t cnt[RLC_NUM_STAGES] = {};
+    for (const auto& m : ctx->marks) {
+      float t = 0;
+      RLC_CK(cudaEventElapsedTime(&t, m.a, m.b));
+      acc[m.stage] += t;
+      cnt[m.stage] += 1;
+    }
+    ctx->marks.clear();
+    ctx->ev_used = 0;
+    for (int i = 0; i < RLC_NUM_STAGES; ++i) {
+      if (ms) ms[i] = acc[i];
+      if (counts) counts[i] = cnt[i];
+    }
   });
 }
 

@@ -125,6 +125,18 @@ class RenderContext:
     def set_stream(self, stream_ptr: int | None):
         _check(_lib.load().rlc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
+    STAGES = ("primary", "sample", "sort", "fold", "accumulate", "split_collapse")
+
+    def enable_timing(self, on: bool = True):
+        _check(_lib.load().rlc_context_enable_timing(self.handle, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        """{stage: (total_ms, launches)} since the last call (CUDA events)."""
+        ms = np.zeros(6, np.float64)
+        cnt = np.zeros(6, np.uint32)
+        _check(_lib.load().rlc_context_stage_times(self.handle, _dptr(ms), _uptr(cnt)))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.STAGES)}
+
     def synchronize(self):
         _check(_lib.load().rlc_context_synchronize(self.handle))
 

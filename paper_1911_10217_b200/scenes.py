@@ -224,25 +224,30 @@ def cornell_grid(k: int, seed: int = 1, dome_triangles: int = 512, *, light_tess
 def maze(n_emitters: int = 1_000_000, n_walls: int = 400, seed: int = 5, *,
          width: int = 1920, height: int = 1080) -> Scene:
     """Procedural maze lit by many small ceiling emitters:
-    floor [-1,11]^2, axis-aligned diffuse walls of height 3.5, ``n_emitters``
-    randomly jittered, randomly sized, downward-facing emissive triangles
-    just below y = 4 with 16 emission levels, camera (5,3.8,-1) -> (5,0,5)."""
+    floor [-1,11]^2; ``n_walls`` diffuse wall panels of height 1 on randomly
+    chosen edges of a 24 x 24 grid of 0.5 m cells; ``n_emitters`` randomly
+    jittered, randomly sized, downward-facing emissive triangles just below
+    y = 4 with 16 emission levels; camera (5,3.8,-1) -> (5,0,5), vfov 60."""
     rng = np.random.default_rng(seed)
     b = _Builder()
     floor = b.material((0.6, 0.6, 0.6), (0, 0, 0))
     wall = b.material((0.7, 0.7, 0.7), (0, 0, 0))
     b.quad((-1, 0, -1), (-1, 0, 11), (11, 0, 11), (11, 0, -1), floor)
-    x0 = rng.uniform(0.0, 10.0, n_walls)
-    z0 = rng.uniform(0.0, 10.0, n_walls)
-    ln = rng.uniform(0.5, 2.5, n_walls)
-    along_x = rng.random(n_walls) < 0.5
-    x1 = np.where(along_x, np.minimum(x0 + ln, 11.0), x0)
-    z1 = np.where(along_x, z0, np.minimum(z0 + ln, 11.0))
-    h = 3.5
-    A = np.stack([x0, np.zeros(n_walls), z0], 1)
-    B = np.stack([x1, np.zeros(n_walls), z1], 1)
-    Cc = np.stack([x1, np.full(n_walls, h), z1], 1)
-    D = np.stack([x0, np.full(n_walls, h), z0], 1)
+    g, pitch, h = 24, 0.5, 1.0
+    edges = [(i, j, 0) for i in range(g) for j in range(g + 1)] + \
+            [(i, j, 1) for i in range(g + 1) for j in range(g)]
+    pick = rng.choice(len(edges), size=min(n_walls, len(edges)), replace=False)
+    E = np.array([edges[k] for k in np.sort(pick)], dtype=np.float64).reshape(-1, 3)
+    along_x = E[:, 2] == 0
+    x0 = -1.0 + np.where(along_x, E[:, 0], E[:, 0]) * pitch
+    z0 = -1.0 + np.where(along_x, E[:, 1], E[:, 1]) * pitch
+    x1 = x0 + np.where(along_x, pitch, 0.0)
+    z1 = z0 + np.where(along_x, 0.0, pitch)
+    nw = E.shape[0]
+    A = np.stack([x0, np.zeros(nw), z0], 1)
+    B = np.stack([x1, np.zeros(nw), z1], 1)
+    Cc = np.stack([x1, np.full(nw, h), z1], 1)
+    D = np.stack([x0, np.full(nw, h), z0], 1)
     walls = np.stack([np.stack([A, B, Cc], 1), np.stack([A, Cc, D], 1)], 1).reshape(-1, 3, 3)
     b.add(walls, np.full(walls.shape[0], wall))
     levels = 16
@@ -255,7 +260,7 @@ def maze(n_emitters: int = 1_000_000, n_walls: int = 400, seed: int = 5, *,
     idx = np.arange(n_emitters)
     cx = -1.0 + (idx % g + rng.uniform(0.15, 0.85, n_emitters)) * cell
     cz = -1.0 + (idx // g + rng.uniform(0.15, 0.85, n_emitters)) * cell
-    cy = 4.0 - rng.uniform(0.0, 0.05, n_emitters)
+    cy = 4.0 - rng.uniform(0.0, 0.01, n_emitters)
     size = cell * rng.uniform(0.2, 0.6, n_emitters)
     a = np.stack([cx - size / 2, cy, cz - size / 2], 1)
     p1 = a + np.stack([size, np.zeros_like(size), np.zeros_like(size)], 1)
