@@ -158,13 +158,24 @@ rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream);
 rlc_status rlc_context_synchronize(rlc_context* ctx);
 
 /* Per-stage device timing with CUDA events on the context stream (bench
- * evidence).  Stages: 0 primary, 1 sample+shadow, 2 sort, 3 fold,
- * 4 accumulate, 5 split-collapse.  rlc_context_stage_times synchronizes,
+ * evidence).  Stages: 0 primary, 1 sample, 2 sort, 3 fold, 4 accumulate,
+ * 5 split-collapse, 6 shadow (any-hit traversal).  rlc_context_stage_times synchronizes,
  * returns accumulated milliseconds and launch counts per stage since the
  * last call, and resets them. */
-#define RLC_NUM_STAGES 6
+#define RLC_NUM_STAGES 7
 rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable);
 rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts);
+
+/* ---- scene visibility, batched ---------------------------------------- */
+/* occluded (proj/include/rlcuts/bvh.hpp:38-40, proj/src/bvh.cpp:159-188):
+ * a, b [n*3] host arrays, out [n] = 1 iff the open segment is blocked. */
+rlc_status rlc_occluded_batch(const rlc_context* ctx, uint32_t n, const double* a,
+                              const double* b, uint8_t* out);
+/* intersect (bvh.hpp:35-36, bvh.cpp:124-157): closest hit with
+ * t in (t_min, inf); t_out = -1 and tri_out = -1 on a miss. */
+rlc_status rlc_intersect_batch(const rlc_context* ctx, uint32_t n, const double* origins,
+                               const double* dirs, double t_min, double* t_out,
+                               int32_t* tri_out);
 
 /* ---- hash grid: HashGrid(hash, init_cut(tree, M, eps))
  *      (proj/src/render.cpp:211-216, proj/src/hash_grid.cpp:102-111,

@@ -13,6 +13,7 @@
 #include "rlc_build.h"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <deque>
@@ -137,6 +138,91 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
   const V3 ext = V3{nodes[0].hi[0], nodes[0].hi[1], nodes[0].hi[2]} -
                  V3{nodes[0].lo[0], nodes[0].lo[1], nodes[0].lo[2]};
   out.shadow_eps = 1e-4 * length(ext);  // bvh.cpp:120
+}
+
+float round_down(double x) {
+  float f = float(x);
+  if (double(f) > x) f = std::nextafter(f, -HUGE_VALF);
+  return f;
+}
+float round_up(double x) {
+  float f = float(x);
+  if (double(f) < x) f = std::nextafter(f, HUGE_VALF);
+  return f;
+}
+
+double surface(const BvhNode& n) {
+  const double dx = n.hi[0] - n.lo[0], dy = n.hi[1] - n.lo[1], dz = n.hi[2] - n.lo[2];
+  return dx * dy + dy * dz + dz * dx;
+}
+
+// 4-wide tree collapsed from the binary BVH: every wide node stands for one
+// binary internal node and lists up to four of its descendants (children
+// expanded largest-surface-first); child boxes are rounded outward to fp32.
+void build_wide(HostScene& out) {
+  const std::vector<BvhNode>& nodes = out.nodes;
+  out.wide.clear();
+  out.bparent.assign(nodes.size(), -1);
+  out.tri_leaf.assign(out.tris.size(), 0);
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    if (nodes[i].count == 0) {
+      out.bparent[nodes[i].a] = int32_t(i);
+      out.bparent[nodes[i].b] = int32_t(i);
+    } else {
+      for (uint32_t t = nodes[i].a; t < nodes[i].a + nodes[i].count; ++t)
+        out.tri_leaf[t] = uint32_t(i);
+    }
+  }
+  if (nodes.empty() || nodes[0].count > 0) return;
+  if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
+  std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
+  std::vector<std::array<uint32_t, 4>> kids;
+  std::vector<uint32_t> todo{0};
+  std::vector<uint32_t> order;
+  while (!todo.empty()) {
+    const uint32_t b = todo.back();
+    todo.pop_back();
+    wid[b] = uint32_t(order.size());
+    order.push_back(b);
+    std::vector<uint32_t> L{nodes[b].a, nodes[b].b};
+    while (L.size() < 4) {
+      int best = -1;
+      for (size_t k = 0; k < L.size(); ++k)
+        if (nodes[L[k]].count == 0 && (best < 0 || surface(nodes[L[k]]) > surface(nodes[L[size_t(best)]])))
+          best = int(k);
+      if (best < 0) break;
+      const uint32_t x = L[size_t(best)];
+      L[size_t(best)] = nodes[x].a;
+      L.insert(L.begin() + best + 1, nodes[x].b);
+    }
+    std::array<uint32_t, 4> k4{kWideEmpty, kWideEmpty, kWideEmpty, kWideEmpty};
+    for (size_t k = 0; k < L.size(); ++k) k4[k] = L[k];
+    kids.push_back(k4);
+    for (size_t k = L.size(); k-- > 0;)
+      if (nodes[L[k]].count == 0) todo.push_back(L[k]);
+  }
+  out.wide.resize(order.size());
+  for (size_t w = 0; w < order.size(); ++w) {
+    Wide4& n = out.wide[w];
+    std::memset(&n, 0, sizeof(n));
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t b = kids[w][c];
+      if (b == kWideEmpty) {
+        n.child[c] = kWideEmpty;
+        for (int a = 0; a < 3; ++a) {
+          n.lo[a][c] = HUGE_VALF;
+          n.hi[a][c] = -HUGE_VALF;
+        }
+        continue;
+      }
+      const BvhNode& bn = nodes[b];
+      for (int a = 0; a < 3; ++a) {
+        n.lo[a][c] = round_down(bn.lo[a]);
+        n.hi[a][c] = round_up(bn.hi[a]);
+      }
+      n.child[c] = bn.count > 0 ? (kWideLeaf | (bn.count << 28) | bn.a) : wid[b];
+    }
+  }
 }
 
 }  // namespace
@@ -307,6 +393,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   }
 
   build_bvh(d, out);  // render.cpp:145
+  build_wide(out);
 
   // collect_emitters (light_tree.cpp:30-42) over derive_emitters order
   out.lights.clear();

@@ -171,6 +171,8 @@ struct rlc_context {
     pb.keys_alt = scratch.alloc<uint32_t>(cap);
     pb.vals_alt = scratch.alloc<uint32_t>(cap);
     pb.q_before = scratch.alloc<double>(cap);
+    pb.rays = scratch.alloc<rlc::ShadowRay>(cap);
+    pb.ray_count = scratch.alloc<unsigned int>(2);
     pb.sort_hist_cap = ((cap + 4095u) / 4096u + 1u) * 256u;
     pb.sort_hist = scratch.alloc<uint32_t>(pb.sort_hist_cap);
     pb_cap = cap;
@@ -251,6 +253,7 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   cudaStream_t st = ctx->stream;
   ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, g, p, ctx->pb, st); });
   ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, g, p, ctx->pb, st); });
+  ctx->stage(6, [&] { rlc::launch_shadow(ctx->dev, ctx->pb, g.counters, st); });
   if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS) {
     uint32_t *k = nullptr, *v = nullptr;
     ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, n, grid->key_bits, st, &k, &v); });
@@ -325,6 +328,9 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     DeviceArena& A = ctx->arena;
     rlc::DevScene& d = ctx->dev;
     d.nodes = A.upload(h.nodes);
+    d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
+    d.bparent = A.upload(h.bparent);
+    d.tri_leaf = A.upload(h.tri_leaf);
     d.tris = A.upload(h.tris);
     d.mats = A.upload(h.mats);
     d.tri_mat = A.upload(h.tri_mat);
@@ -411,6 +417,50 @@ rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* count
       if (ms) ms[i] = acc[i];
       if (counts) counts[i] = cnt[i];
     }
+  });
+}
+
+rlc_status rlc_occluded_batch(const rlc_context* cctx, uint32_t n, const double* a,
+                              const double* b, uint8_t* out) {
+  return guarded([&] {
+    require(cctx != nullptr && (n == 0 || (a && b && out)), "occluded: null argument");
+    if (n == 0) return;
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    RLC_CK(cudaSetDevice(ctx->device));
+    ctx->ensure_scratch(n);
+    DeviceArena tmp;
+    double* da = tmp.alloc<double>(3 * size_t(n));
+    double* db = tmp.alloc<double>(3 * size_t(n));
+    uint8_t* dout = tmp.alloc<uint8_t>(n);
+    RLC_CK(cudaMemcpyAsync(da, a, 24 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    RLC_CK(cudaMemcpyAsync(db, b, 24 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    rlc::launch_occluded_batch(ctx->dev, n, da, db, ctx->pb, ctx->counters, dout, ctx->stream);
+    RLC_CK(cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, ctx->stream));
+    finish_sync(ctx, nullptr);
+  });
+}
+
+rlc_status rlc_intersect_batch(const rlc_context* cctx, uint32_t n, const double* origins,
+                               const double* dirs, double t_min, double* t_out,
+                               int32_t* tri_out) {
+  return guarded([&] {
+    require(cctx != nullptr && (n == 0 || (origins && dirs && t_out && tri_out)),
+            "intersect: null argument");
+    if (n == 0) return;
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    RLC_CK(cudaSetDevice(ctx->device));
+    DeviceArena tmp;
+    double* dorg = tmp.alloc<double>(3 * size_t(n));
+    double* ddir = tmp.alloc<double>(3 * size_t(n));
+    double* dt = tmp.alloc<double>(n);
+    int32_t* dtri = tmp.alloc<int32_t>(n);
+    RLC_CK(cudaMemcpyAsync(dorg, origins, 24 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    RLC_CK(cudaMemcpyAsync(ddir, dirs, 24 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    rlc::launch_intersect_batch(ctx->dev, n, dorg, ddir, t_min, dt, dtri, ctx->counters,
+                                ctx->stream);
+    RLC_CK(cudaMemcpyAsync(t_out, dt, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    RLC_CK(cudaMemcpyAsync(tri_out, dtri, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    finish_sync(ctx, nullptr);
   });
 }
 

@@ -81,6 +81,21 @@ struct alignas(64) BvhNode {
   uint32_t pad;
 };
 
+// 4-wide node collapsed from the reference binary BVH for the any-hit shadow
+// kernel.  Child boxes are the binary nodes' boxes rounded OUTWARD to fp32,
+// so the fp64 slab test on them passes whenever the reference's test on the
+// exact box passes (rounding is monotone); a triangle hit found through this
+// tree is accepted only after its binary ancestor chain passes the exact
+// fp64 test ("Exact any-hit on a conservative wide BVH").
+constexpr uint32_t kWideLeaf = 0x80000000u;  // child: leaf flag
+constexpr uint32_t kWideEmpty = 0xffffffffu; // child: unused slot
+struct alignas(128) Wide4 {
+  float lo[3][4];      // [axis][child]
+  float hi[3][4];
+  uint32_t child[4];   // internal: Wide4 index; leaf: kWideLeaf | count << 28 | first tri
+  uint32_t pad[4];
+};
+
 // Triangle as the Moller-Trumbore test consumes it (bvh.cpp:44-62): p0 and
 // the two edges, precomputed with the reference's own subtraction.  Stored
 // in BVH leaf order.  80 B.

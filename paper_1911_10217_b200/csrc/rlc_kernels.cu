@@ -14,6 +14,7 @@
 // All FP64 arithmetic keeps the reference's operand order and this file is
 // compiled with --fmad=false: the path is bit-exact with the reference
 // (SURVEY 0 facts 1-6 and Appendix B give the argument).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -30,6 +31,8 @@ constexpr unsigned kFull = 0xffffffffu;
 }  // namespace
 
 uint64_t launches() { return g_launches.load(); }
+
+static inline uint32_t blocks_for(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
 
 // ---------------------------------------------------------------------------
 // geometry helpers
@@ -384,7 +387,9 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
                                                 SampleRec* __restrict__ srec,
                                                 uint32_t* __restrict__ keys,
                                                 uint32_t* __restrict__ vals,
-                                                double* __restrict__ q_before) {
+                                                double* __restrict__ q_before,
+                                                ShadowRay* __restrict__ rays,
+                                                unsigned int* __restrict__ ray_count) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= P.n) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
@@ -480,7 +485,9 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
     const double cos_x = dot(ns, to_light);
     if (!(cos_x <= 0)) {
       const double cos_y = dot(ld3(L.n), -to_light);
-      if (!(cos_y <= 0) && !occluded(sc, pos, point, err)) {
+      if (!(cos_y <= 0)) {
+        // Contribution as if visible; k_shadow zeroes it when the segment
+        // is occluded (occluded(), bvh.cpp:159-188, is q-independent).
         const MatRec& m = sc.mats[gb.flags & kGMatMask];
         const double geometry = cos_x * cos_y / d2;
         const V3 contrib = ld3(m.albedo) * (1.0 / kPi) * ld3(L.emission) * geometry;
@@ -489,13 +496,153 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
         r.c[2] = contrib.z;
         r.flags |= kSNonzero;
         if (P.sampler == 2u) r.v = luminance(contrib) / (r.pin * r.pdf_area);
+        // the shadow segment (pos, point) of occluded(): bvh.cpp:160-167
+        const V3 dd = point - pos;
+        const double len = length(dd);
+        if (!(len <= 2 * sc.shadow_eps)) {
+          const V3 dir = dd / len;
+          namespace cg = cooperative_groups;
+          cg::coalesced_group grp = cg::coalesced_threads();
+          unsigned int base = 0;
+          if (grp.thread_rank() == 0) base = atomicAdd(ray_count, grp.size());
+          base = grp.shfl(base, 0) + grp.thread_rank();
+          ShadowRay ray;
+          ray.o[0] = pos.x;
+          ray.o[1] = pos.y;
+          ray.o[2] = pos.z;
+          ray.d[0] = dir.x;
+          ray.d[1] = dir.y;
+          ray.d[2] = dir.z;
+          ray.tmax = len - sc.shadow_eps;
+          ray.idx = idx;
+          ray.pad = 0;
+          rays[base] = ray;
+        }
       }
     }
   }
-  // update_q's argument check (cut.cpp:78-80); the fallback cut is never updated
-  if (P.sampler == 2u && gb.slot != kFallback && !(r.v >= 0 && isfinite(r.v)))
-    atomicOr(err, kErrBadValue);
   srec[idx] = r;
+}
+
+// ---------------------------------------------------------------------------
+// k_shadow: any-hit traversal of the queued shadow segments.  Persistent
+// warps refill idle lanes from the queue (dynamic ray fetch) so incoherent
+// shadow rays keep the SIMT lanes busy; each traversal step reads one
+// child-pair record and runs both children's slab tests.
+// ---------------------------------------------------------------------------
+constexpr int kShadowThreads = 128;
+constexpr int kShadowStack = 48;
+
+// Exact acceptance of a triangle found through the conservative wide tree:
+// every node on its binary ancestor chain (leaf to root) must pass the
+// reference's fp64 slab test (bvh.cpp:29-40) with the fixed shadow interval.
+__device__ __forceinline__ bool chain_passes(const DevScene& sc, uint32_t leaf, V3 o, V3 inv,
+                                             double tmin, double tmax) {
+  for (int32_t x = int32_t(leaf); x >= 0; x = __ldg(sc.bparent + x))
+    if (!box_hit(load_node(sc.nodes, uint32_t(x)), o, inv, tmin, tmax)) return false;
+  return true;
+}
+
+// fp64 slab test against an fp32 (outward-rounded) box; same operation order
+// as intersect_aabb, so it is monotone in the box and conservative.
+__device__ __forceinline__ bool box_hit_f(float lx, float ly, float lz, float hx, float hy,
+                                          float hz, V3 o, V3 inv, double tmin, double tmax) {
+  if (!slab(double(lx), double(hx), o.x, inv.x, tmin, tmax)) return false;
+  if (!slab(double(ly), double(hy), o.y, inv.y, tmin, tmax)) return false;
+  return slab(double(lz), double(hz), o.z, inv.z, tmin, tmax);
+}
+
+__global__ void __launch_bounds__(kShadowThreads) k_shadow(DevScene sc,
+                                                           const ShadowRay* __restrict__ rays,
+                                                           unsigned int* __restrict__ ray_count,
+                                                           SampleRec* __restrict__ srec,
+                                                           unsigned int* __restrict__ err) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned n = *reinterpret_cast<volatile unsigned*>(ray_count);
+  const double tmin = sc.shadow_eps;
+  bool active = false;
+  bool exhausted = false;
+  V3 o{0, 0, 0}, d{0, 0, 0}, inv{0, 0, 0};
+  double tmax = 0;
+  uint32_t idx = 0;
+  uint32_t stack[kShadowStack];
+  int sp = 0;
+  while (true) {
+    const unsigned need = __ballot_sync(kFull, !active);
+    if (need && !exhausted) {
+      const int leader = __ffs(need) - 1;
+      unsigned base = 0;
+      if (int(lane) == leader) base = atomicAdd(ray_count + 1, unsigned(__popc(need)));
+      base = __shfl_sync(kFull, base, leader);
+      if (base + __popc(need) >= n) exhausted = true;
+      if (!active) {
+        const unsigned my = base + __popc(need & lt_mask);
+        if (my < n) {
+          const ShadowRay r = rays[my];
+          o = V3{r.o[0], r.o[1], r.o[2]};
+          d = V3{r.d[0], r.d[1], r.d[2]};
+          inv = V3{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+          tmax = r.tmax;
+          idx = r.idx;
+          sp = 0;
+          const NodeView root = load_node(sc.nodes, 0);
+          if (box_hit(root, o, inv, tmin, tmax)) {  // the reference tests the root first
+            if (root.count > 0) {  // the whole scene is one leaf
+              stack[sp++] = kWideLeaf | (root.count << 28) | root.a;
+            } else {
+              stack[sp++] = 0;
+            }
+            active = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(kFull, active)) {
+      if (exhausted) break;
+      continue;
+    }
+    for (int step = 0; step < 16 && active; ++step) {
+      const uint32_t e = stack[--sp];
+      bool hit = false;
+      if (e & kWideLeaf) {
+        const uint32_t first = e & 0x0fffffffu, cnt = (e >> 28) & 7u;
+        for (uint32_t i = first; i < first + cnt && !hit; ++i) {
+          double t;
+          hit = tri_hit(sc.tris, i, o, d, tmin, tmax, &t);
+        }
+        if (hit && sc.wide != nullptr)
+          hit = chain_passes(sc, __ldg(sc.tri_leaf + first), o, inv, tmin, tmax);
+      } else {
+        const float4* p = reinterpret_cast<const float4*>(sc.wide + e);
+        const float4 lx = __ldg(p), ly = __ldg(p + 1), lz = __ldg(p + 2);
+        const float4 hx = __ldg(p + 3), hy = __ldg(p + 4), hz = __ldg(p + 5);
+        const uint4 ch = __ldg(reinterpret_cast<const uint4*>(p + 6));
+        const bool h0 = box_hit_f(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, o, inv, tmin, tmax);
+        const bool h1 = box_hit_f(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, o, inv, tmin, tmax);
+        const bool h2 = ch.z != kWideEmpty &&
+                        box_hit_f(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, o, inv, tmin, tmax);
+        const bool h3 = ch.w != kWideEmpty &&
+                        box_hit_f(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, o, inv, tmin, tmax);
+        if (sp + 4 > kShadowStack) {  // deeper than any collapsed 64-level tree
+          atomicOr(err, kErrStackOverflow);
+          active = false;
+          continue;
+        }
+        if (h3) stack[sp++] = ch.w;
+        if (h2) stack[sp++] = ch.z;
+        if (h1) stack[sp++] = ch.y;
+        if (h0) stack[sp++] = ch.x;
+      }
+      if (hit) {
+        srec[idx].v = 0.0;
+        srec[idx].flags &= ~kSNonzero;
+        active = false;
+      } else if (sp == 0) {
+        active = false;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -629,6 +776,8 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
   for (uint32_t j = i; j < P.n && keys[j] == k; ++j) {
     const uint32_t idx = vals[j];
     const double v = srec[idx].v;
+    if (!(v >= 0 && isfinite(v)))  // update_q's argument check, cut.cpp:78-80
+      atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrBadValue);
     q_before[idx] = q;
     const double a = P.harmonic ? 1.0 / (1.0 + double(vis)) : P.alpha;
     q = smax((1.0 - a) * q + a * v, g.eps_q);
@@ -826,6 +975,79 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
   if (lane == 0 && my_changes) atomicAdd(changes_out, my_changes);
 }
 
+// Batch entry points of occluded() / intersect() (bvh.hpp:38-40).
+__global__ void k_segments(DevScene sc, uint32_t n, const double* __restrict__ a,
+                           const double* __restrict__ b, ShadowRay* __restrict__ rays,
+                           unsigned int* __restrict__ ray_count, SampleRec* __restrict__ srec) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const V3 pa = ld3(a + 3 * size_t(i)), pb = ld3(b + 3 * size_t(i));
+  const V3 dd = pb - pa;
+  const double len = length(dd);
+  srec[i].flags = 0;
+  if (len <= 2 * sc.shadow_eps) return;  // bvh.cpp:162
+  srec[i].flags = kSNonzero;
+  const V3 dir = dd / len;
+  const unsigned slot = atomicAdd(ray_count, 1u);
+  ShadowRay r;
+  r.o[0] = pa.x;
+  r.o[1] = pa.y;
+  r.o[2] = pa.z;
+  r.d[0] = dir.x;
+  r.d[1] = dir.y;
+  r.d[2] = dir.z;
+  r.tmax = len - sc.shadow_eps;
+  r.idx = i;
+  r.pad = 0;
+  rays[slot] = r;
+}
+
+__global__ void k_segments_out(uint32_t n, const SampleRec* __restrict__ srec,
+                               const double* __restrict__ a, const double* __restrict__ b,
+                               double eps2, uint8_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const V3 dd = ld3(b + 3 * size_t(i)) - ld3(a + 3 * size_t(i));
+  out[i] = (length(dd) > eps2 && !(srec[i].flags & kSNonzero)) ? 1 : 0;
+}
+
+__global__ void k_intersect_batch(DevScene sc, uint32_t n, const double* __restrict__ org,
+                                  const double* __restrict__ dir, double tmin,
+                                  double* __restrict__ t_out, int32_t* __restrict__ tri_out,
+                                  unsigned int* err) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double t;
+  uint32_t tri;
+  if (intersect(sc, ld3(org + 3 * size_t(i)), ld3(dir + 3 * size_t(i)), tmin, &t, &tri, err)) {
+    t_out[i] = t;
+    tri_out[i] = int32_t(tri);
+  } else {
+    t_out[i] = -1.0;
+    tri_out[i] = -1;
+  }
+}
+
+void launch_occluded_batch(const DevScene& sc, uint32_t n, const double* a, const double* b,
+                           PassBuffers& pb, unsigned long long* counters, uint8_t* out,
+                           cudaStream_t st) {
+  if (n == 0) return;
+  cudaMemsetAsync(pb.ray_count, 0, 2 * sizeof(unsigned int), st);
+  k_segments<<<blocks_for(n, 256), 256, 0, st>>>(sc, n, a, b, pb.rays, pb.ray_count, pb.srec);
+  launch_shadow(sc, pb, counters, st);
+  k_segments_out<<<blocks_for(n, 256), 256, 0, st>>>(n, pb.srec, a, b, 2 * sc.shadow_eps, out);
+  count_launch(2);
+}
+
+void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, const double* dir,
+                            double tmin, double* t_out, int32_t* tri_out,
+                            unsigned long long* counters, cudaStream_t st) {
+  if (n == 0) return;
+  k_intersect_batch<<<blocks_for(n, 128), 128, 0, st>>>(
+      sc, n, org, dir, tmin, t_out, tri_out, reinterpret_cast<unsigned int*>(counters + kCntErr));
+  count_launch();
+}
+
 __global__ void k_resolve(Framebuf fb, uint32_t npix, double* __restrict__ image) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npix) return;
@@ -836,8 +1058,6 @@ __global__ void k_resolve(Framebuf fb, uint32_t npix, double* __restrict__ image
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static inline uint32_t blocks_for(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
-
 void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
                     const PassBuffers& b, cudaStream_t st) {
   if (p.n == 0) return;
@@ -848,8 +1068,24 @@ void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
 void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
                    const PassBuffers& b, cudaStream_t st) {
   if (p.n == 0) return;
+  cudaMemsetAsync(b.ray_count, 0, 2 * sizeof(unsigned int), st);
   k_sample<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.keys, b.vals,
-                                                  b.q_before);
+                                                  b.q_before, b.rays, b.ray_count);
+  count_launch();
+}
+
+void launch_shadow(const DevScene& sc, const PassBuffers& b, unsigned long long* counters,
+                   cudaStream_t st) {
+  static int blocks = 0;
+  if (blocks == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shadow, kShadowThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    blocks = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  }
+  k_shadow<<<blocks, kShadowThreads, 0, st>>>(
+      sc, b.rays, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
   count_launch();
 }
 

@@ -53,8 +53,21 @@ struct alignas(16) SampleRec {  // 64 B per path
   uint32_t flags;
 };
 
+// One shadow segment of nee_estimate (estimators.cpp:95 -> bvh.cpp:159-188),
+// queued by k_sample and traced by k_shadow.  64 B.
+struct alignas(16) ShadowRay {
+  double o[3];
+  double d[3];
+  double tmax;  // len - shadow_eps
+  uint32_t idx; // path index
+  uint32_t pad;
+};
+
 struct DevScene {
   const BvhNode* nodes;
+  const Wide4* wide;        // conservative 4-wide tree (null if the root is a leaf)
+  const int32_t* bparent;   // binary parent per BvhNode
+  const uint32_t* tri_leaf; // binary leaf per leaf-order triangle
   const TriAccel* tris;
   const MatRec* mats;
   const uint32_t* tri_mat;
@@ -119,6 +132,8 @@ struct PassBuffers {
   uint32_t* keys_alt;
   uint32_t* vals_alt;
   double* q_before;
+  ShadowRay* rays;
+  unsigned int* ray_count;  // [0] queued rays, [1] fetch cursor
   uint32_t* sort_hist;
   uint32_t sort_hist_cap;  // entries
 };
@@ -137,6 +152,8 @@ void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
 void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
                    const PassBuffers& b, cudaStream_t st);
 // Sorts (keys, vals) by key; returns which buffer pair holds the result.
+void launch_shadow(const DevScene& sc, const PassBuffers& b, unsigned long long* counters,
+                   cudaStream_t st);
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out);
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
@@ -145,6 +162,12 @@ void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffer
                        const Framebuf& fb, cudaStream_t st);
 void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshold,
                            uint32_t iterations, uint32_t* changes_out, cudaStream_t st);
+void launch_occluded_batch(const DevScene& sc, uint32_t n, const double* a, const double* b,
+                           PassBuffers& pb, unsigned long long* counters, uint8_t* out,
+                           cudaStream_t st);
+void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, const double* dir,
+                            double tmin, double* t_out, int32_t* tri_out,
+                            unsigned long long* counters, cudaStream_t st);
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
 
 }  // namespace rlc

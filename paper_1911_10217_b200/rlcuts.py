@@ -125,17 +125,37 @@ class RenderContext:
     def set_stream(self, stream_ptr: int | None):
         _check(_lib.load().rlc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
-    STAGES = ("primary", "sample", "sort", "fold", "accumulate", "split_collapse")
+    STAGES = ("primary", "sample", "sort", "fold", "accumulate", "split_collapse", "shadow")
 
     def enable_timing(self, on: bool = True):
         _check(_lib.load().rlc_context_enable_timing(self.handle, 1 if on else 0))
 
     def stage_times(self) -> dict:
         """{stage: (total_ms, launches)} since the last call (CUDA events)."""
-        ms = np.zeros(6, np.float64)
-        cnt = np.zeros(6, np.uint32)
+        ms = np.zeros(len(self.STAGES), np.float64)
+        cnt = np.zeros(len(self.STAGES), np.uint32)
         _check(_lib.load().rlc_context_stage_times(self.handle, _dptr(ms), _uptr(cnt)))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.STAGES)}
+
+    def occluded(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        """occluded() (bvh.hpp:38-40) for n segments (n x 3 endpoints)."""
+        a = np.ascontiguousarray(a, np.float64).reshape(-1, 3)
+        b = np.ascontiguousarray(b, np.float64).reshape(-1, 3)
+        out = np.zeros(a.shape[0], np.uint8)
+        _check(_lib.load().rlc_occluded_batch(self.handle, a.shape[0], _dptr(a), _dptr(b),
+                                              out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out.astype(bool)
+
+    def intersect(self, origins: np.ndarray, dirs: np.ndarray, t_min: float = 0.0):
+        """intersect() (bvh.hpp:35-36): (t, triangle id), -1 on a miss."""
+        o = np.ascontiguousarray(origins, np.float64).reshape(-1, 3)
+        d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+        t = np.zeros(o.shape[0], np.float64)
+        tri = np.zeros(o.shape[0], np.int32)
+        _check(_lib.load().rlc_intersect_batch(self.handle, o.shape[0], _dptr(o), _dptr(d),
+                                               t_min, _dptr(t),
+                                               tri.ctypes.data_as(C.POINTER(C.c_int32))))
+        return t, tri
 
     def synchronize(self):
         _check(_lib.load().rlc_context_synchronize(self.handle))
