@@ -205,6 +205,15 @@ static bool mt(const Tri& t, V o, V d, double tmin, double tmax, double* out) {
 // the algorithmic bytes of the visibility kernels.
 struct Trav {
   uint64_t rays = 0, nodes = 0, tris = 0;
+  uint64_t max_nodes = 0, hist[8] = {};  // per-ray node-count histogram (powers of 4)
+  uint64_t cur = 0;
+  void begin() { ++rays; cur = 0; }
+  void end() {
+    max_nodes = cur > max_nodes ? cur : max_nodes;
+    int b = 0;
+    for (uint64_t c = cur; c >= 4 && b < 7; c /= 4) ++b;
+    ++hist[b];
+  }
 };
 
 // bvh.cpp:124-157
@@ -214,11 +223,11 @@ static bool closest(const Scene& s, const Bvh& B, V o, V d, double tmin, double*
   double best = HUGE_VAL;
   int64_t hit = -1;
   std::vector<uint32_t> st{0};
-  if (tv) ++tv->rays;
+  if (tv) tv->begin();
   while (!st.empty()) {
     const Node& n = B.nodes[st.back()];
     st.pop_back();
-    if (tv) ++tv->nodes;
+    if (tv) ++tv->nodes, ++tv->cur;
     if (!slab_test(n.b, o, inv, tmin, best)) continue;
     if (n.count) {
       if (tv) tv->tris += n.count;
@@ -234,6 +243,7 @@ static bool closest(const Scene& s, const Bvh& B, V o, V d, double tmin, double*
       st.push_back(n.r);
     }
   }
+  if (tv) tv->end();
   if (hit < 0) return false;
   *t = best;
   *tri = uint32_t(hit);
@@ -245,7 +255,7 @@ static bool blocked(const Scene& s, const Bvh& B, V a, V b, Trav* tv = nullptr) 
   const V dd = b - a;
   const double L = len(dd);
   if (L <= 2 * B.eps) return false;
-  if (tv) ++tv->rays;
+  if (tv) tv->begin();
   const V d = dd / L;
   const double tmax = L - B.eps;
   const V inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
@@ -253,19 +263,23 @@ static bool blocked(const Scene& s, const Bvh& B, V a, V b, Trav* tv = nullptr) 
   while (!st.empty()) {
     const Node& n = B.nodes[st.back()];
     st.pop_back();
-    if (tv) ++tv->nodes;
+    if (tv) ++tv->nodes, ++tv->cur;
     if (!slab_test(n.b, a, inv, B.eps, tmax)) continue;
     if (n.count) {
       for (uint32_t i = n.begin; i < n.begin + n.count; ++i) {
         double tt;
         if (tv) ++tv->tris;
-        if (mt(s.tris[B.order[i]], a, d, B.eps, tmax, &tt)) return true;
+        if (mt(s.tris[B.order[i]], a, d, B.eps, tmax, &tt)) {
+          if (tv) tv->end();
+          return true;
+        }
       }
     } else {
       st.push_back(n.l);
       st.push_back(n.r);
     }
   }
+  if (tv) tv->end();
   return false;
 }
 
@@ -895,6 +909,14 @@ void orc_run_trav_stats(void* h, uint64_t* out) {
   out[3] = r->shadow.rays;
   out[4] = r->shadow.nodes;
   out[5] = r->shadow.tris;
+}
+
+// shadow rays: max nodes per ray and histogram of node counts in bins
+// [1,4),[4,16),...,[4^7,inf)
+void orc_run_trav_hist(void* h, uint64_t* out) {
+  Run* r = static_cast<Run*>(h);
+  out[0] = r->shadow.max_nodes;
+  for (int i = 0; i < 8; ++i) out[1 + i] = r->shadow.hist[i];
 }
 
 void orc_run_occluded(void* h, uint32_t n, const double* a, const double* b, uint8_t* out) {

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -173,6 +174,8 @@ struct rlc_context {
     pb.q_before = scratch.alloc<double>(cap);
     pb.rays = scratch.alloc<rlc::ShadowRay>(cap);
     pb.ray_count = scratch.alloc<unsigned int>(2);
+    pb.ray_order = scratch.alloc<uint32_t>(cap);
+    pb.block_counts = scratch.alloc<uint32_t>(cap / 2048 + 2);
     pb.sort_hist_cap = ((cap + 4095u) / 4096u + 1u) * 256u;
     pb.sort_hist = scratch.alloc<uint32_t>(pb.sort_hist_cap);
     pb_cap = cap;
@@ -253,12 +256,18 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   cudaStream_t st = ctx->stream;
   ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, g, p, ctx->pb, st); });
   ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, g, p, ctx->pb, st); });
-  ctx->stage(6, [&] { rlc::launch_shadow(ctx->dev, ctx->pb, g.counters, st); });
-  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS) {
-    uint32_t *k = nullptr, *v = nullptr;
+  // Shadow rays are traced in sorted (cell, cluster) order: rays of one cell
+  // toward one cut cluster share most of their BVH path.  The any-hit result
+  // does not depend on the order.
+  uint32_t *k = nullptr, *v = nullptr;
+  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS)
     ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, n, grid->key_bits, st, &k, &v); });
+  ctx->stage(6, [&] {
+    rlc::launch_ray_compact(ctx->pb, v, n, st);
+    rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, g.counters, st);
+  });
+  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS)
     ctx->stage(3, [&] { rlc::launch_fold(g, p, k, v, ctx->pb, st); });
-  }
   ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, p, ctx->pb, fb->fb, st); });
   RLC_CK(cudaGetLastError());
 }
@@ -342,6 +351,9 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     d.emitter_energy = A.upload(h.emitter_energy);
     d.num_lights = uint32_t(h.lights.size());
     d.num_tris = uint32_t(h.tri_mat.size());
+    d.fp32_ok = 1;
+    for (int a = 0; a < 3; ++a)
+      if (!(std::fabs(h.scene_lo[a]) <= 1e8 && std::fabs(h.scene_hi[a]) <= 1e8)) d.fp32_ok = 0;
     d.shadow_eps = h.shadow_eps;
     d.base_tile = h.base_tile;
     for (int k = 0; k <= 16; ++k) d.level_thr[k] = h.level_threshold[k];

@@ -14,7 +14,6 @@
 // All FP64 arithmetic keeps the reference's operand order and this file is
 // compiled with --fmad=false: the path is bit-exact with the reference
 // (SURVEY 0 facts 1-6 and Appendix B give the argument).
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -103,14 +102,8 @@ constexpr int kStack = 64;  // bvh.cpp:134 uses a 64-entry stack too
 // occluded(), proj/src/bvh.cpp:159-188.  The any-hit boolean does not depend
 // on traversal order, so any order over the same tree and slab test gives
 // the reference's answer.
-__device__ bool occluded(const DevScene& sc, V3 a, V3 b, uint32_t* err) {
-  const V3 d = b - a;
-  const double len = length(d);
-  if (len <= 2 * sc.shadow_eps) return false;
-  const V3 dir = d / len;
-  const double tmin = sc.shadow_eps;
-  const double tmax = len - sc.shadow_eps;
-  const V3 inv{1.0 / dir.x, 1.0 / dir.y, 1.0 / dir.z};
+__device__ __noinline__ bool occluded_ray(const DevScene& sc, V3 a, V3 dir, V3 inv, double tmin, double tmax,
+                             uint32_t* err) {
   uint32_t stack[kStack];
   int sp = 0;
   stack[sp++] = 0;
@@ -132,6 +125,15 @@ __device__ bool occluded(const DevScene& sc, V3 a, V3 b, uint32_t* err) {
     }
   }
   return false;
+}
+
+__device__ bool occluded(const DevScene& sc, V3 a, V3 b, uint32_t* err) {
+  const V3 d = b - a;
+  const double len = length(d);
+  if (len <= 2 * sc.shadow_eps) return false;
+  const V3 dir = d / len;
+  const V3 inv{1.0 / dir.x, 1.0 / dir.y, 1.0 / dir.z};
+  return occluded_ray(sc, a, dir, inv, sc.shadow_eps, len - sc.shadow_eps, err);
 }
 
 // intersect(), proj/src/bvh.cpp:124-157: closest hit, exact-t ties go to the
@@ -396,7 +398,10 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
   const GBuf gb = gbuf[idx];
   keys[idx] = kInvalidKey;
   vals[idx] = idx;
-  if (!(gb.flags & kGReflective)) return;
+  if (!(gb.flags & kGReflective)) {
+    srec[idx].flags = 0;  // read by the ray compaction
+    return;
+  }
   const double u1 = rng_draw(gb.rng, kDrawU1);
   const double u2 = rng_draw(gb.rng, kDrawU2);
   const double u3 = rng_draw(gb.rng, kDrawU3);
@@ -501,11 +506,6 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
         const double len = length(dd);
         if (!(len <= 2 * sc.shadow_eps)) {
           const V3 dir = dd / len;
-          namespace cg = cooperative_groups;
-          cg::coalesced_group grp = cg::coalesced_threads();
-          unsigned int base = 0;
-          if (grp.thread_rank() == 0) base = atomicAdd(ray_count, grp.size());
-          base = grp.shfl(base, 0) + grp.thread_rank();
           ShadowRay ray;
           ray.o[0] = pos.x;
           ray.o[1] = pos.y;
@@ -516,7 +516,8 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
           ray.tmax = len - sc.shadow_eps;
           ray.idx = idx;
           ray.pad = 0;
-          rays[base] = ray;
+          rays[idx] = ray;
+          r.flags |= kSRay;
         }
       }
     }
@@ -531,29 +532,102 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
 // child-pair record and runs both children's slab tests.
 // ---------------------------------------------------------------------------
 constexpr int kShadowThreads = 128;
-constexpr int kShadowStack = 48;
+constexpr int kShadowStack = 32;  // 4-wide levels: the 64-deep binary limit / 2
+constexpr uint32_t kDone = 0x7fffffffu;  // traversal finished (no leaf flag)
 
 // Exact acceptance of a triangle found through the conservative wide tree:
 // every node on its binary ancestor chain (leaf to root) must pass the
 // reference's fp64 slab test (bvh.cpp:29-40) with the fixed shadow interval.
-__device__ __forceinline__ bool chain_passes(const DevScene& sc, uint32_t leaf, V3 o, V3 inv,
+__device__ __noinline__ bool chain_passes(const DevScene& sc, uint32_t leaf, V3 o, V3 inv,
                                              double tmin, double tmax) {
   for (int32_t x = int32_t(leaf); x >= 0; x = __ldg(sc.bparent + x))
     if (!box_hit(load_node(sc.nodes, uint32_t(x)), o, inv, tmin, tmax)) return false;
   return true;
 }
 
-// fp64 slab test against an fp32 (outward-rounded) box; same operation order
-// as intersect_aabb, so it is monotone in the box and conservative.
-__device__ __forceinline__ bool box_hit_f(float lx, float ly, float lz, float hx, float hy,
-                                          float hz, V3 o, V3 inv, double tmin, double tmax) {
-  if (!slab(double(lx), double(hx), o.x, inv.x, tmin, tmax)) return false;
-  if (!slab(double(ly), double(hy), o.y, inv.y, tmin, tmax)) return false;
-  return slab(double(lz), double(hz), o.z, inv.z, tmin, tmax);
+// Conservative fp32 slab test of the 4 children of a Wide4 node against one
+// ray.  Per axis the reference computes t = fl64(fl64(c - o) * inv) on the
+// exact box (bvh.cpp:29-40); here t' = fma(c', inv', -o'inv') on the outward-
+// rounded fp32 box, widened by |t'| 2^-20 + |o'||inv'| 2^-21: the box rounding
+// only ever moves t' outward and the margin bounds the fp32 rounding of the
+// origin, inverse and FMA plus the fp64 reference's own rounding, so the
+// interval contains the reference's and the test passes whenever the
+// reference's passes.  NaN terms (zero direction components) are ignored by
+// fmaxf/fminf, which only drops a constraint.  Rays with |inv| > 1e30 (fp32
+// range) take the exact fp64 path instead (ShadowLane::exact).
+struct RayF {
+  float inv[3], b[3], mt[3];
+  uint32_t neg;  // bit a: inv[a] < 0 (near plane is hi)
+  float tmin, tmax;
+};
+
+__device__ __forceinline__ uint32_t box4_f(const float4 lo[3], const float4 hi[3], const RayF& r,
+                                           float near_out[4]) {
+  constexpr float K = 0x1.0p-20f;
+  float nr[4] = {r.tmin, r.tmin, r.tmin, r.tmin};
+  float fr[4] = {r.tmax, r.tmax, r.tmax, r.tmax};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool neg = (r.neg >> a) & 1u;
+    const float4 n4 = neg ? hi[a] : lo[a];
+    const float4 f4 = neg ? lo[a] : hi[a];
+    const float nc[4] = {n4.x, n4.y, n4.z, n4.w};
+    const float fc[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float tn = fmaf(nc[c], r.inv[a], r.b[a]);
+      tn = tn - fmaf(fabsf(tn), K, r.mt[a]);
+      float tf = fmaf(fc[c], r.inv[a], r.b[a]);
+      tf = tf + fmaf(fabsf(tf), K, r.mt[a]);
+      nr[c] = fmaxf(nr[c], tn);
+      fr[c] = fminf(fr[c], tf);
+    }
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    m |= (nr[c] <= fr[c]) ? (1u << c) : 0u;
+    near_out[c] = nr[c];
+  }
+  return m;
 }
 
-__global__ void __launch_bounds__(kShadowThreads) k_shadow(DevScene sc,
+// Branch-free Moller-Trumbore: the reference's expressions (bvh.cpp:44-62)
+// with every early exit folded into one predicate.
+__device__ __forceinline__ bool tri_any(const TriAccel* tris, uint32_t i, V3 o, V3 d, double tmin,
+                                        double tmax) {
+  const double2* p = reinterpret_cast<const double2*>(tris + i);
+  const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), e = __ldg(p + 3),
+                f = __ldg(p + 4);
+  const V3 p0{a.x, a.y, b.x};
+  const V3 e1{b.y, c.x, c.y};
+  const V3 e2{e.x, e.y, f.x};
+  const V3 pv = cross(d, e2);
+  const double det = dot(e1, pv);
+  const double inv_det = 1.0 / det;
+  const V3 tv = o - p0;
+  const double u = dot(tv, pv) * inv_det;
+  const V3 qv = cross(tv, e1);
+  const double v = dot(d, qv) * inv_det;
+  const double t = dot(e2, qv) * inv_det;
+  return !(fabs(det) < 1e-14) & !(u < 0 || u > 1) & !(v < 0 || u + v > 1) &
+         !(t <= tmin || t >= tmax);
+}
+
+__device__ __forceinline__ void mark_occluded(SampleRec* srec, uint32_t idx) {
+  srec[idx].v = 0.0;  // nee_estimate returns the zero result (estimators.cpp:95)
+  srec[idx].flags &= ~kSNonzero;
+}
+
+// Any-hit traversal of the queued shadow segments (occluded(), bvh.cpp:
+// 159-188).  Persistent warps refill idle lanes from the queue after every
+// leaf round.  Node steps and leaf tests are separated ("while-while") and a
+// lane that reaches a leaf postpones it while other lanes still have node
+// steps to do (speculative traversal, Aila & Laine 2009), so both phases run
+// with as many lanes as possible.
+__global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
                                                            const ShadowRay* __restrict__ rays,
+                                                           const uint32_t* __restrict__ order,
                                                            unsigned int* __restrict__ ray_count,
                                                            SampleRec* __restrict__ srec,
                                                            unsigned int* __restrict__ err) {
@@ -564,9 +638,14 @@ __global__ void __launch_bounds__(kShadowThreads) k_shadow(DevScene sc,
   bool active = false;
   bool exhausted = false;
   V3 o{0, 0, 0}, d{0, 0, 0}, inv{0, 0, 0};
+  RayF rf;
   double tmax = 0;
   uint32_t idx = 0;
-  uint32_t stack[kShadowStack];
+  uint32_t leaf = 0;    // postponed leaf entry (0: none)
+  uint32_t cur = kDone; // current entry: Wide4 index, leaf entry, or kDone
+  // per-lane traversal stack in shared memory, [depth][thread]: conflict-free
+  __shared__ uint32_t stack_mem[kShadowStack * kShadowThreads];
+  uint32_t* stack = stack_mem + threadIdx.x;
   int sp = 0;
   while (true) {
     const unsigned need = __ballot_sync(kFull, !active);
@@ -579,21 +658,36 @@ __global__ void __launch_bounds__(kShadowThreads) k_shadow(DevScene sc,
       if (!active) {
         const unsigned my = base + __popc(need & lt_mask);
         if (my < n) {
-          const ShadowRay r = rays[my];
+          const ShadowRay r = rays[order ? __ldg(order + my) : my];
           o = V3{r.o[0], r.o[1], r.o[2]};
           d = V3{r.d[0], r.d[1], r.d[2]};
           inv = V3{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
           tmax = r.tmax;
           idx = r.idx;
           sp = 0;
+          leaf = 0;
           const NodeView root = load_node(sc.nodes, 0);
           if (box_hit(root, o, inv, tmin, tmax)) {  // the reference tests the root first
-            if (root.count > 0) {  // the whole scene is one leaf
-              stack[sp++] = kWideLeaf | (root.count << 28) | root.a;
-            } else {
-              stack[sp++] = 0;
+            const double ia[3] = {inv.x, inv.y, inv.z}, oa[3] = {o.x, o.y, o.z};
+            bool exact = root.count > 0 || !sc.fp32_ok;
+            rf.neg = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              exact |= fabs(ia[a]) > 1e30 && isfinite(ia[a]);
+              const float of = float(oa[a]), fi = float(ia[a]);
+              rf.inv[a] = fi;
+              rf.b[a] = -(of * fi);
+              rf.mt[a] = fmaf(fabsf(of) * fabsf(fi), 0x1.0p-21f, 1e-30f);
+              rf.neg |= (ia[a] < 0 ? 1u : 0u) << a;
             }
-            active = true;
+            rf.tmin = __double2float_rd(tmin);
+            rf.tmax = __double2float_ru(tmax);
+            if (exact) {  // tiny scene or fp32-range ray: the exact fp64 path
+              if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, idx);
+            } else {
+              cur = 0;
+              active = true;
+            }
           }
         }
       }
@@ -602,45 +696,71 @@ __global__ void __launch_bounds__(kShadowThreads) k_shadow(DevScene sc,
       if (exhausted) break;
       continue;
     }
-    for (int step = 0; step < 16 && active; ++step) {
-      const uint32_t e = stack[--sp];
-      bool hit = false;
-      if (e & kWideLeaf) {
-        const uint32_t first = e & 0x0fffffffu, cnt = (e >> 28) & 7u;
-        for (uint32_t i = first; i < first + cnt && !hit; ++i) {
-          double t;
-          hit = tri_hit(sc.tris, i, o, d, tmin, tmax, &t);
-        }
-        if (hit && sc.wide != nullptr)
-          hit = chain_passes(sc, __ldg(sc.tri_leaf + first), o, inv, tmin, tmax);
+    if (!active) continue;
+    // node phase: descend through internal nodes with the current node in a
+    // register; the first leaf met is postponed and traversal continues
+    // while some lane of the warp has not found a leaf yet
+    while (cur != kDone && !(cur & kWideLeaf)) {
+      const float4* p = reinterpret_cast<const float4*>(sc.wide + cur);
+      const float4 lo[3] = {__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+      const float4 hi[3] = {__ldg(p + 3), __ldg(p + 4), __ldg(p + 5)};
+      const uint4 ch = __ldg(reinterpret_cast<const uint4*>(p + 6));
+      float tn[4];
+      uint32_t m = box4_f(lo, hi, rf, tn);
+      if (ch.z == kWideEmpty) m &= ~4u;
+      if (ch.w == kWideEmpty) m &= ~8u;
+      if (sp + 3 > kShadowStack) {
+        atomicOr(err, kErrStackOverflow);
+        m = 0;
+        sp = 0;
+      }
+      // nearest entry first: occluders near the shading point end the ray early
+      uint32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (!(m & (1u << k))) tn[k] = HUGE_VALF;
+#define RLC_CSWAP(i, j)                                   \
+  if (tn[j] < tn[i]) {                                    \
+    const float tt = tn[i]; tn[i] = tn[j]; tn[j] = tt;    \
+    const uint32_t cc = c[i]; c[i] = c[j]; c[j] = cc;     \
+  }
+      RLC_CSWAP(0, 1) RLC_CSWAP(2, 3) RLC_CSWAP(0, 2) RLC_CSWAP(1, 3) RLC_CSWAP(1, 2)
+#undef RLC_CSWAP
+      const int hits = __popc(m);
+      if (hits == 0) {
+        cur = sp > 0 ? stack[(--sp) * kShadowThreads] : kDone;
       } else {
-        const float4* p = reinterpret_cast<const float4*>(sc.wide + e);
-        const float4 lx = __ldg(p), ly = __ldg(p + 1), lz = __ldg(p + 2);
-        const float4 hx = __ldg(p + 3), hy = __ldg(p + 4), hz = __ldg(p + 5);
-        const uint4 ch = __ldg(reinterpret_cast<const uint4*>(p + 6));
-        const bool h0 = box_hit_f(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, o, inv, tmin, tmax);
-        const bool h1 = box_hit_f(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, o, inv, tmin, tmax);
-        const bool h2 = ch.z != kWideEmpty &&
-                        box_hit_f(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, o, inv, tmin, tmax);
-        const bool h3 = ch.w != kWideEmpty &&
-                        box_hit_f(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, o, inv, tmin, tmax);
-        if (sp + 4 > kShadowStack) {  // deeper than any collapsed 64-level tree
-          atomicOr(err, kErrStackOverflow);
-          active = false;
-          continue;
-        }
-        if (h3) stack[sp++] = ch.w;
-        if (h2) stack[sp++] = ch.z;
-        if (h1) stack[sp++] = ch.y;
-        if (h0) stack[sp++] = ch.x;
+        cur = c[0];
+#pragma unroll
+        for (int k = 3; k >= 1; --k)
+          if (k < hits) stack[(sp++) * kShadowThreads] = c[k];
       }
-      if (hit) {
-        srec[idx].v = 0.0;
-        srec[idx].flags &= ~kSNonzero;
-        active = false;
-      } else if (sp == 0) {
-        active = false;
+      if (leaf == 0 && cur != kDone && (cur & kWideLeaf)) {
+        leaf = cur;
+        cur = sp > 0 ? stack[(--sp) * kShadowThreads] : kDone;
       }
+      if (!__any_sync(__activemask(), leaf == 0)) break;
+    }
+    // leaf phase: exact fp64 Moller-Trumbore on the postponed leaf and on
+    // every leaf that follows it directly, then the exact ancestor chain
+    bool hit = false;
+    while (leaf != 0) {
+      const uint32_t first = leaf & 0x0fffffffu, cnt = (leaf >> 28) & 7u;
+      for (uint32_t i = first; i < first + cnt; ++i) hit |= tri_any(sc.tris, i, o, d, tmin, tmax);
+      if (hit) hit = chain_passes(sc, __ldg(sc.tri_leaf + first), o, inv, tmin, tmax);
+      if (hit) break;
+      if (cur != kDone && (cur & kWideLeaf)) {
+        leaf = cur;
+        cur = sp > 0 ? stack[(--sp) * kShadowThreads] : kDone;
+      } else {
+        leaf = 0;
+      }
+    }
+    if (hit) {
+      mark_occluded(srec, idx);
+      active = false;
+    } else if (cur == kDone && leaf == 0) {
+      active = false;
     }
   }
 }
@@ -1034,7 +1154,7 @@ void launch_occluded_batch(const DevScene& sc, uint32_t n, const double* a, cons
   if (n == 0) return;
   cudaMemsetAsync(pb.ray_count, 0, 2 * sizeof(unsigned int), st);
   k_segments<<<blocks_for(n, 256), 256, 0, st>>>(sc, n, a, b, pb.rays, pb.ray_count, pb.srec);
-  launch_shadow(sc, pb, counters, st);
+  launch_shadow(sc, pb, nullptr, counters, st);
   k_segments_out<<<blocks_for(n, 256), 256, 0, st>>>(n, pb.srec, a, b, 2 * sc.shadow_eps, out);
   count_launch(2);
 }
@@ -1074,8 +1194,77 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
   count_launch();
 }
 
-void launch_shadow(const DevScene& sc, const PassBuffers& b, unsigned long long* counters,
-                   cudaStream_t st) {
+// ---- stable compaction of ray-bearing paths -------------------------------
+constexpr int kCmpThreads = 256, kCmpItems = 8, kCmpTile = kCmpThreads * kCmpItems;
+
+__device__ __forceinline__ bool has_ray(const SampleRec* srec, const uint32_t* order, uint32_t j) {
+  const uint32_t i = order ? order[j] : j;
+  return i != kNoSlot && (srec[i].flags & kSRay);
+}
+
+__global__ void __launch_bounds__(kCmpThreads) k_cmp_count(const SampleRec* __restrict__ srec,
+                                                           const uint32_t* __restrict__ order,
+                                                           uint32_t n, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t ws[kCmpThreads / 32];
+  uint32_t c = 0;
+  for (int k = 0; k < kCmpItems; ++k) {
+    const uint32_t j = blockIdx.x * kCmpTile + k * kCmpThreads + threadIdx.x;
+    if (j < n && has_ray(srec, order, j)) ++c;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kCmpThreads / 32; ++w) t += ws[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+// counts[] holds exclusive block offsets (rs_scan) on entry.
+__global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const SampleRec* __restrict__ srec,
+                                                             const uint32_t* __restrict__ order,
+                                                             uint32_t n, const uint32_t* __restrict__ offs,
+                                                             uint32_t* __restrict__ out,
+                                                             unsigned int* __restrict__ ray_count) {
+  __shared__ uint32_t wsum[kCmpThreads / 32];
+  __shared__ uint32_t base;
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = offs[blockIdx.x];
+  __syncthreads();
+  for (int k = 0; k < kCmpItems; ++k) {
+    const uint32_t j = blockIdx.x * kCmpTile + k * kCmpThreads + threadIdx.x;
+    const bool f = j < n && has_ray(srec, order, j);
+    const unsigned b = __ballot_sync(kFull, f);
+    if (lane == 0) wsum[w] = __popc(b);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t q = 0; q < kCmpThreads / 32; ++q) {
+      before += q < w ? wsum[q] : 0u;
+      total += wsum[q];
+    }
+    if (f) out[base + before + __popc(b & ((1u << lane) - 1u))] = order ? order[j] : j;
+    __syncthreads();
+    if (threadIdx.x == 0) base += total;
+    __syncthreads();
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    ray_count[0] = base;
+    ray_count[1] = 0;
+  }
+}
+
+void launch_ray_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, cudaStream_t st) {
+  const uint32_t nb = blocks_for(n > 0 ? n : 1, kCmpTile);
+  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, b.block_counts);
+  rs_scan<<<1, 1024, 0, st>>>(b.block_counts, nb);
+  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, b.block_counts, b.ray_order,
+                                            b.ray_count);
+  count_launch(3);
+}
+
+void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* order,
+                   unsigned long long* counters, cudaStream_t st) {
   static int blocks = 0;
   if (blocks == 0) {
     int per_sm = 0, dev = 0, sms = 0;
@@ -1085,7 +1274,7 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, unsigned long long*
     blocks = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
   }
   k_shadow<<<blocks, kShadowThreads, 0, st>>>(
-      sc, b.rays, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
+      sc, b.rays, order, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
   count_launch();
 }
 

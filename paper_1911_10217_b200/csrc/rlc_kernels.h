@@ -20,7 +20,7 @@ enum : uint32_t {
   kGMatMask = (1u << 29) - 1,
 };
 // Sample-record flags
-enum : uint32_t { kSNonzero = 1u, kSLearned = 2u };
+enum : uint32_t { kSNonzero = 1u, kSLearned = 2u, kSRay = 4u };  // kSRay: rays[idx] valid
 
 // Device error bits (mapped to the reference's exceptions by the host).
 enum : uint32_t {
@@ -79,6 +79,7 @@ struct DevScene {
   const double* emitter_energy;
   uint32_t num_lights;
   uint32_t num_tris;
+  uint32_t fp32_ok;  // scene coordinates within 1e8: the fp32 shadow pre-test is valid
   double shadow_eps;
   double base_tile;
   double level_thr[17];
@@ -134,6 +135,8 @@ struct PassBuffers {
   double* q_before;
   ShadowRay* rays;
   unsigned int* ray_count;  // [0] queued rays, [1] fetch cursor
+  uint32_t* ray_order;      // path indices with a shadow ray, in trace order
+  uint32_t* block_counts;   // compaction scratch
   uint32_t* sort_hist;
   uint32_t sort_hist_cap;  // entries
 };
@@ -152,8 +155,11 @@ void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
 void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
                    const PassBuffers& b, cudaStream_t st);
 // Sorts (keys, vals) by key; returns which buffer pair holds the result.
-void launch_shadow(const DevScene& sc, const PassBuffers& b, unsigned long long* counters,
-                   cudaStream_t st);
+// Stable compaction of the paths that carry a shadow ray, in the order of
+// `order` (sorted update records) or canonical order when it is null.
+void launch_ray_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, cudaStream_t st);
+void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* order,
+                   unsigned long long* counters, cudaStream_t st);
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out);
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
