@@ -1,0 +1,186 @@
+// rlcuts_b200_shim.cpp -- implementation of rlcuts_b200_shim.hpp over the
+// C-ABI.  Builds against the reference headers (proj/include) and
+// include/rlcuts_b200.h; no reference source is needed.
+#include "rlcuts_b200_shim.hpp"
+
+#include <chrono>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rlcuts_b200.h"
+
+namespace rlcuts::b200 {
+
+namespace {
+
+// Maps an rlc_status back to the reference's exception types.
+void check(rlc_status st) {
+  if (st == RLC_OK) return;
+  const std::string msg = rlc_last_error();
+  if (st == RLC_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (st == RLC_ERR_OUT_OF_RANGE) throw std::out_of_range(msg);
+  throw std::runtime_error(msg);
+}
+
+rlc_render_config to_c(const RenderConfig& c) {
+  rlc_render_config r;
+  check(rlc_render_config_default(&r));
+  r.spp = c.spp;
+  r.passes = c.passes;
+  r.max_depth = c.max_depth;
+  r.sampler = uint32_t(c.sampler);
+  r.cut.cut_size = c.cut.cut_size;
+  r.cut.alpha = c.cut.alpha;
+  r.cut.split_threshold = c.cut.split_threshold;
+  r.cut.eps_q = c.cut.eps_q;
+  r.cut.iterations = c.cut.iterations;
+  r.cut.alpha_schedule = uint32_t(c.cut.alpha_schedule);
+  r.hash.capacity = c.hash.capacity;
+  r.hash.base_tile = c.hash.base_tile;
+  r.hash.probe_limit = c.hash.probe_limit;
+  r.hash.normal_bits = c.hash.normal_bits;
+  r.hash.jitter_scale = c.hash.jitter_scale;
+  r.seed = c.seed;
+  r.workers = c.workers;
+  return r;
+}
+
+// Flattened rlcuts::Scene (scene.hpp:53-67) kept alive for the descriptor.
+struct SceneArrays {
+  std::vector<double> vertices, materials;
+  std::vector<uint32_t> material_ids;
+  rlc_scene_desc desc{};
+
+  explicit SceneArrays(const Scene& s) {
+    for (const Triangle& t : s.triangles) {
+      for (const Vec3* p : {&t.p0, &t.p1, &t.p2}) {
+        vertices.push_back(p->x);
+        vertices.push_back(p->y);
+        vertices.push_back(p->z);
+      }
+      material_ids.push_back(t.material_id);
+    }
+    for (const Material& m : s.materials) {
+      for (double v : {m.albedo.x, m.albedo.y, m.albedo.z, m.emission.x, m.emission.y,
+                       m.emission.z})
+        materials.push_back(v);
+    }
+    desc.num_triangles = uint32_t(s.triangles.size());
+    desc.num_materials = uint32_t(s.materials.size());
+    desc.vertices = vertices.data();
+    desc.material_ids = material_ids.data();
+    desc.materials = materials.data();
+    const Camera& c = s.camera;
+    const Vec3* cam[3] = {&c.origin, &c.look_at, &c.up};
+    double* dst[3] = {desc.cam_origin, desc.cam_look_at, desc.cam_up};
+    for (int k = 0; k < 3; ++k) {
+      dst[k][0] = cam[k]->x;
+      dst[k][1] = cam[k]->y;
+      dst[k][2] = cam[k]->z;
+    }
+    desc.vfov_degrees = c.vfov_degrees;
+    desc.width = c.width;
+    desc.height = c.height;
+  }
+};
+
+}  // namespace
+
+struct Session::Impl {
+  const RenderContext* ctx = nullptr;
+  rlc_render_config cfg{};
+  rlc_context* c = nullptr;
+  rlc_grid* g = nullptr;
+  rlc_framebuffer* fb = nullptr;
+
+  ~Impl() {
+    rlc_framebuffer_destroy(fb);
+    rlc_grid_destroy(g);
+    rlc_context_destroy(c);
+  }
+};
+
+Session::Session(const RenderContext& ctx, const RenderConfig& config, int device)
+    : impl_(std::make_unique<Impl>()) {
+  if (ctx.scene == nullptr) throw std::invalid_argument("Session: context without a scene");
+  impl_->ctx = &ctx;
+  impl_->cfg = to_c(config);
+  impl_->cfg.hash.base_tile = ctx.base_tile;  // resolved by build_context (render.cpp:153-155)
+  SceneArrays arrays(*ctx.scene);
+  check(rlc_context_create(&arrays.desc, &impl_->cfg, device, &impl_->c));
+  if (config.sampler == SamplerKind::rl_lightcuts)
+    check(rlc_grid_create(impl_->c, &impl_->cfg, &impl_->g));
+  check(rlc_framebuffer_create(impl_->c, ctx.scene->camera.width, ctx.scene->camera.height,
+                               &impl_->fb));
+}
+
+Session::~Session() = default;
+
+void Session::render_pass(uint32_t pass_index) {
+  check(rlc_render_pass(impl_->c, &impl_->cfg, pass_index, impl_->g, impl_->fb));
+}
+
+uint32_t Session::end_of_pass_update() {
+  if (impl_->g == nullptr) return 0;
+  uint32_t changes = 0;
+  check(rlc_end_of_pass_update(impl_->g, impl_->c, &impl_->cfg.cut, &changes));
+  return changes;
+}
+
+void Session::framebuffer(Framebuffer& out) const {
+  const size_t n = size_t(out.width) * size_t(out.height);
+  std::vector<double> sum(3 * n);
+  std::vector<uint64_t> count(n);
+  check(rlc_framebuffer_download(impl_->fb, sum.data(), count.data()));
+  for (size_t i = 0; i < n; ++i) {
+    out.sum[i] = Vec3{sum[3 * i], sum[3 * i + 1], sum[3 * i + 2]};
+    out.count[i] = count[i];
+  }
+}
+
+uint32_t Session::occupied_count() const {
+  rlc_grid_stats s{};
+  if (impl_->g) check(rlc_grid_stats_get(impl_->g, &s));
+  return s.occupied;
+}
+
+uint64_t Session::lookup_count() const {
+  rlc_grid_stats s{};
+  if (impl_->g) check(rlc_grid_stats_get(impl_->g, &s));
+  return s.lookups;
+}
+
+uint64_t Session::fallback_hits() const {
+  rlc_grid_stats s{};
+  if (impl_->g) check(rlc_grid_stats_get(impl_->g, &s));
+  return s.fallback_hits;
+}
+
+RenderResult render_frame(const RenderContext& ctx, const RenderConfig& config,
+                          const Image* reference) {
+  if (config.passes == 0 || config.spp == 0 || config.spp % config.passes != 0)
+    throw std::invalid_argument("render_frame: spp must be divisible by passes");
+  const auto t0 = std::chrono::steady_clock::now();
+  Session s(ctx, config);
+  Framebuffer fb(ctx.scene->camera.width, ctx.scene->camera.height);
+  RenderResult result;
+  for (uint32_t pass = 0; pass < config.passes; ++pass) {
+    s.render_pass(pass);
+    result.sc_changes.push_back(s.end_of_pass_update());
+    if (reference != nullptr) {  // per-pass MSE needs the running image on the host
+      s.framebuffer(fb);
+      result.pass_mse.push_back(mse(fb.resolve(), *reference));
+    }
+  }
+  s.framebuffer(fb);
+  result.image = fb.resolve();
+  result.occupied_cells = s.occupied_count();
+  result.lookups = s.lookup_count();
+  result.fallback_hits = s.fallback_hits();
+  result.wall_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return result;
+}
+
+}  // namespace rlcuts::b200
