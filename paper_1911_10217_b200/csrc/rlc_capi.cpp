@@ -176,7 +176,7 @@ struct rlc_context {
     pb.ray_count = scratch.alloc<unsigned int>(2);
     pb.ray_order = scratch.alloc<uint32_t>(cap);
     pb.block_counts = scratch.alloc<uint32_t>(cap / 2048 + 2);
-    pb.sort_hist_cap = ((cap + 4095u) / 4096u + 1u) * 256u;
+    pb.sort_hist_cap = ((cap + 4095u) / 4096u + 2u) * 256u;  // rows + digit totals
     pb.sort_hist = scratch.alloc<uint32_t>(pb.sort_hist_cap);
     pb_cap = cap;
   }

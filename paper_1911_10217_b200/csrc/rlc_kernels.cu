@@ -823,17 +823,61 @@ __global__ void __launch_bounds__(1024) rs_scan(uint32_t* __restrict__ hist, uin
   }
 }
 
+// Exclusive scan of one digit's row of per-block counts (hist[d][0..nb)) in
+// place; the digit total goes to totals[d].  One block per digit.
+__global__ void __launch_bounds__(256) rs_scan_rows(uint32_t* __restrict__ hist, uint32_t nb,
+                                                    uint32_t* __restrict__ totals) {
+  __shared__ uint32_t ws[8];
+  uint32_t* row = hist + size_t(blockIdx.x) * nb;
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nb; base += 256) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < nb ? row[i] : 0u;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= uint32_t(o)) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t q = 0; q < 8; ++q) {
+      before += q < w ? ws[q] : 0u;
+      total += ws[q];
+    }
+    if (i < nb) row[i] = carry + before + x - v;
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
 __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin,
                                                          uint32_t* __restrict__ kout,
                                                          uint32_t* __restrict__ vout,
                                                          uint32_t n, int shift,
-                                                         const uint32_t* __restrict__ offs) {
+                                                         const uint32_t* __restrict__ offs,
+                                                         const uint32_t* __restrict__ totals) {
   __shared__ uint32_t wh[kRsWarps][256];
   __shared__ uint32_t base_off[256];
+  __shared__ uint32_t dsum[kRsWarps];
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
   for (int d = lane; d < 256; d += 32) wh[w][d] = 0;
-  base_off[threadIdx.x] = offs[threadIdx.x * gridDim.x + blockIdx.x];
+  {  // digit base = exclusive prefix of the digit totals, + this block's row offset
+    const uint32_t t = totals[threadIdx.x];
+    uint32_t x = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= uint32_t(o)) x += y;
+    }
+    if (lane == 31) dsum[w] = x;
+    __syncthreads();
+    uint32_t before = 0;
+    for (uint32_t q = 0; q < w; ++q) before += dsum[q];
+    base_off[threadIdx.x] = before + x - t + offs[threadIdx.x * gridDim.x + blockIdx.x];
+  }
   __syncwarp();
   const uint32_t base = blockIdx.x * kRsTile + w * kRsWarpSpan;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -1288,8 +1332,9 @@ void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
     const uint32_t nb = blocks_for(n, kRsTile);
     for (uint32_t shift = 0; shift < key_bits; shift += 8) {
       rs_hist<<<nb, kRsThreads, 0, st>>>(ka, n, int(shift), b.sort_hist);
-      rs_scan<<<1, 1024, 0, st>>>(b.sort_hist, nb * 256u);
-      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, int(shift), b.sort_hist);
+      uint32_t* totals = b.sort_hist + size_t(nb) * 256u;
+      rs_scan_rows<<<256, 256, 0, st>>>(b.sort_hist, nb, totals);
+      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, int(shift), b.sort_hist, totals);
       count_launch(3);
       uint32_t* t = ka;
       ka = kb;
