@@ -222,6 +222,30 @@ rlc_status rlc_render_pass_async(const rlc_context* ctx, const rlc_render_config
 rlc_status rlc_end_of_pass_update_async(rlc_grid* grid, const rlc_context* ctx,
                                         const rlc_cut_config* cut);
 rlc_status rlc_grid_last_changes(const rlc_grid* grid, uint32_t* changes);
+/* ---- screen-band sharding with an exact exchange --
+ * One learned update (the update_q call of render.cpp:111-117) as exchanged
+ * between ranks: the cell key, the cluster and the feedback value.  32 B. */
+typedef struct rlc_update_record {
+  int32_t qx, qy, qz;
+  uint32_t qn, level, cluster;
+  double v;
+} rlc_update_record;
+/* Traces rows [row_begin, row_end) of pass `pass_index` (primary rays, cut
+ * samples, shadow rays) without applying updates.  *records receives a
+ * device pointer to the band's update records in canonical order and
+ * *count their number; valid until the next call on this context. */
+rlc_status rlc_pass_trace(const rlc_context* ctx, const rlc_render_config* config,
+                          uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
+                          uint32_t row_end, const void** records, uint64_t* count);
+/* Folds the update records of all ranks (device memory: rank k's counts[k]
+ * records at all_records + k*stride, ranks owning consecutive row bands in
+ * rank order), inserting foreign cells, then accumulates this rank's band
+ * (traced by the preceding rlc_pass_trace) into fb.  Every rank ends with
+ * the learned state a single render_pass over all rows produces. */
+rlc_status rlc_pass_fold(const rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
+                         rlc_framebuffer* fb, const void* all_records, const uint64_t* counts,
+                         uint32_t nranks, uint32_t rank, uint64_t stride);
+
 /* render_frame (proj/src/render.cpp:202-240): image_out [h*w*3] host,
  * resolved; result may be NULL. */
 rlc_status rlc_render_frame(const rlc_context* ctx, const rlc_render_config* config,

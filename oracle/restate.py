@@ -35,6 +35,10 @@ _SIGS = {
                                     _dp, _u32p]),
     "orc_run_samples": (C.c_uint32, [_P, C.c_uint32, _u32p, _dp]),
     "orc_run_trav_stats": (None, [_P, _u64p]),
+    "orc_run_trace": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint32]),
+    "orc_run_records": (None, [_P, _P]),
+    "orc_run_fold": (C.c_int, [_P, _P, _u64p, C.c_uint32, C.c_uint32, C.c_uint64]),
+    "orc_run_end_of_pass": (C.c_int64, [_P]),
     "orc_run_occluded": (None, [_P, C.c_uint32, _dp, _dp, C.POINTER(C.c_uint8)]),
     "orc_light_tree": (C.c_uint32, [C.c_uint32, _dp, _dp, _u32p, _i32p, _dp]),
     "orc_init_cut": (C.c_uint32, [C.c_uint32, _dp, _dp, C.c_uint32, C.c_double, _u32p, _u32p, _dp,
@@ -137,6 +141,31 @@ class OracleRun:
         return {"pixel": u[:n, 0], "cluster": u[:n, 1], "emitter": u[:n, 2],
                 "fallback": u[:n, 3].astype(bool), "q_before": f[:n, 0], "v": f[:n, 1],
                 "radiance": f[:n, 2:5], "total": f[:n, 5]}
+
+    # ---- sharded pass (CPU model of rlc_pass_trace / rlc_pass_fold) ----
+    def trace(self, pass_index: int, rows: tuple) -> int:
+        r = oracle_lib().orc_run_trace(self.h, pass_index, rows[0], rows[1])
+        if r < 0:
+            _raise(-r)
+        self._n = int(r)
+        return self._n
+
+    def records(self) -> np.ndarray:
+        from paper_1911_10217_b200.rlcuts import RECORD_DTYPE
+        out = np.zeros(self._n, RECORD_DTYPE)
+        oracle_lib().orc_run_records(self.h, out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def fold(self, all_records: np.ndarray, counts, rank: int, stride: int):
+        c = np.ascontiguousarray(counts, np.uint64)
+        buf = np.ascontiguousarray(all_records)
+        st = oracle_lib().orc_run_fold(self.h, buf.ctypes.data_as(C.c_void_p),
+                                       c.ctypes.data_as(_u64p), len(c), rank, stride)
+        if st:
+            _raise(st)
+
+    def end_of_pass(self) -> int:
+        return int(oracle_lib().orc_run_end_of_pass(self.h))
 
     def trav_stats(self) -> dict:
         """Mean nodes / triangles tested per primary and per shadow ray so far

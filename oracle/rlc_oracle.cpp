@@ -591,10 +591,33 @@ struct Run {
     return UINT32_MAX;
   }
 
+  // lookup_or_insert without the lookup counter (keys received from other ranks)
+  uint32_t insert(const Key& k) {
+    const uint64_t l0 = lookups, f0 = fallbacks;
+    const uint32_t slot = lookup(k);
+    lookups = l0;
+    fallbacks = f0;
+    return slot;
+  }
+
   const Cut& cut_of(uint32_t slot) const { return slot == UINT32_MAX ? tmpl : cuts[slot]; }
 
   // render_pass, proj/src/render.cpp:59-138 and 159-183, as a deferred fold
+  // Current band of the pass being traced: rows [r0, r1).
+  std::vector<Sample> cur;
+  std::vector<V> emitted;
+  std::vector<int64_t> sample_of;
+  uint32_t band_r0 = 0, band_spp = 1;
+
+  // render_pass (render.cpp:159-183) = trace + fold_local.
   void pass(uint32_t pass_index) {
+    trace(pass_index, 0, uint32_t(s.h));
+    fold_local();
+  }
+
+  // PassRenderer::trace up to the light sample and its NEE (render.cpp:59-
+  // 117 without update_q) for every path of rows [r0, r1), canonical order.
+  void trace(uint32_t pass_index, uint32_t r0, uint32_t r1) {
     if (cfg.passes == 0 || cfg.spp % cfg.passes != 0)
       throw std::invalid_argument("render_pass: spp must be divisible by passes");
     if (cfg.max_depth != 1) throw std::invalid_argument("oracle: max_depth must be 1");
@@ -604,13 +627,17 @@ struct Run {
     const double tan_half = std::tan(0.5 * s.vfov * 3.14159265358979323846 / 180.0);
     const double aspect = double(s.w) / double(s.h);
     const uint32_t n_em = uint32_t(em_tri.size());
-    std::vector<Sample> samples;
-    std::vector<V> emitted(size_t(s.w) * s.h * spp_pp);
-    std::vector<int64_t> sample_of(emitted.size(), -1);
-    for (uint32_t py = 0; py < uint32_t(s.h); ++py)
+    if (r1 > uint32_t(s.h) || r0 > r1) throw std::invalid_argument("oracle: bad row band");
+    std::vector<Sample>& samples = cur;
+    samples.clear();
+    band_r0 = r0;
+    band_spp = spp_pp;
+    emitted.assign(size_t(s.w) * (r1 - r0) * spp_pp, V{});
+    sample_of.assign(emitted.size(), -1);
+    for (uint32_t py = r0; py < r1; ++py)
       for (uint32_t px = 0; px < uint32_t(s.w); ++px)
         for (uint32_t k = 0; k < spp_pp; ++k) {
-          const uint64_t canon = (uint64_t(py) * s.w + px) * spp_pp + k;
+          const uint64_t canon = (uint64_t(py - r0) * s.w + px) * spp_pp + k;
           Rng rng(cfg.seed, uint64_t(py) * s.w + px, uint64_t(pass_index) * spp_pp + k, 0);
           const double jx = rng.next(), jy = rng.next();
           const double sx = (2.0 * (double(px) + jx) / s.w - 1.0) * tan_half * aspect;
@@ -650,7 +677,6 @@ struct Run {
             e = tree.order[b + std::min(sm.size - 1, uint32_t(frac * double(sm.size)))];
             sm.cluster = sidx;
             sm.total = c.cdf.back();
-            if (sm.slot != UINT32_MAX) touched[sm.slot] = 1;
           } else if (cfg.sampler == RLC_SAMPLER_UNIFORM) {
             e = std::min(n_em - 1, uint32_t(u1 * double(n_em)));
             pdf_sel_base = 1.0 / double(n_em);
@@ -687,6 +713,12 @@ struct Run {
           sample_of[canon] = int64_t(samples.size());
           samples.push_back(sm);
         }
+  }
+
+  // The deferred fold of the band's own update records.
+  void fold_local() {
+    std::vector<Sample>& samples = cur;
+    const bool rl = cfg.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
     if (rl) {
       // deferred fold: stable order by (fallback, slot, cluster, canonical id)
       std::vector<uint32_t> idx(samples.size());
@@ -705,19 +737,85 @@ struct Run {
           const double pdf_sel = (sm.q_before / sm.total) * (1.0 / double(sm.size));
           sm.radiance = sm.contrib / (pdf_sel * sm.pdf_area);
         }
-        if (!fb) update(c, sm.cluster, sm.v, cfg.cut.alpha,
-                        cfg.cut.alpha_schedule == RLC_ALPHA_HARMONIC);
+        if (!fb) {
+          update(c, sm.cluster, sm.v, cfg.cut.alpha, cfg.cut.alpha_schedule == RLC_ALPHA_HARMONIC);
+          touched[sm.slot] = 1;
+        }
       }
     }
-    // Framebuffer::add_sample in canonical order (image.hpp:56-60)
+    accumulate();
+  }
+
+  // Framebuffer::add_sample in canonical order (image.hpp:56-60)
+  void accumulate() {
+    std::vector<Sample>& samples = cur;
     for (size_t canon = 0; canon < emitted.size(); ++canon) {
       V L = emitted[canon];
       if (sample_of[canon] >= 0) L = L + V{1, 1, 1} * samples[size_t(sample_of[canon])].radiance;
-      const size_t pix = canon / spp_pp;
+      const size_t pix = size_t(band_r0) * s.w + canon / band_spp;
       sum[pix] = sum[pix] + L;
       count[pix] += 1;
     }
-    last = std::move(samples);
+    last = samples;
+  }
+
+  // This band's update records in canonical order (sharded passes).
+  std::vector<rlc_update_record> records() const {
+    std::vector<rlc_update_record> out;
+    if (cfg.sampler != RLC_SAMPLER_RL_LIGHTCUTS) return out;
+    for (const Sample& sm : cur) {
+      if (sm.slot == UINT32_MAX) continue;
+      const Key& k = keys[sm.slot];
+      out.push_back(rlc_update_record{k.qx, k.qy, k.qz, k.qn, k.level, sm.cluster, sm.v});
+    }
+    return out;
+  }
+
+  // Sharded pass: folds the records of all ranks (rank-major, which is
+  // canonical order because ranks own consecutive row bands), then forms the
+  // radiance of this band's samples from their q_before and accumulates it.
+  void fold_records(const rlc_update_record* all, const uint64_t* counts, uint32_t nranks,
+                    uint32_t rank, uint64_t stride) {
+    struct R {
+      uint32_t slot, cluster;
+      double v;
+    };
+    std::vector<R> recs;
+    uint64_t own_offset = 0;
+    for (uint32_t r = 0; r < nranks; ++r) {
+      if (r < rank) own_offset += counts[r];
+      for (uint64_t k = 0; k < counts[r]; ++k) {
+        const rlc_update_record& u = all[r * stride + k];
+        const Key key{u.qx, u.qy, u.qz, u.qn, u.level};
+        const uint32_t slot = insert(key);
+        if (slot == UINT32_MAX) throw std::runtime_error("oracle: sharded key overflow");
+        recs.push_back(R{slot, u.cluster, u.v});
+      }
+    }
+    std::vector<uint32_t> idx(recs.size());
+    std::iota(idx.begin(), idx.end(), 0u);
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
+      if (recs[a].slot != recs[b].slot) return recs[a].slot < recs[b].slot;
+      return recs[a].cluster < recs[b].cluster;
+    });
+    std::vector<double> qb(recs.size());
+    for (uint32_t i : idx) {
+      Cut& c = cuts[recs[i].slot];
+      qb[i] = c.q[recs[i].cluster];
+      update(c, recs[i].cluster, recs[i].v, cfg.cut.alpha,
+             cfg.cut.alpha_schedule == RLC_ALPHA_HARMONIC);
+      touched[recs[i].slot] = 1;
+    }
+    uint64_t k = own_offset;
+    for (Sample& sm : cur) {
+      if (sm.slot == UINT32_MAX) sm.q_before = tmpl.q[sm.cluster];
+      else sm.q_before = qb[k++];
+      if (sm.nonzero) {
+        const double pdf_sel = (sm.q_before / sm.total) * (1.0 / double(sm.size));
+        sm.radiance = sm.contrib / (pdf_sel * sm.pdf_area);
+      }
+    }
+    accumulate();
   }
 
   // end_of_pass_update, proj/src/render.cpp:185-200
@@ -840,6 +938,35 @@ int64_t orc_run_pass(void* h, uint32_t pass_index) {
     return -int64_t(fail(e));
   }
 }
+
+// Sharded pass (oracle model of rlc_pass_trace / rlc_pass_fold).
+int64_t orc_run_trace(void* h, uint32_t pass_index, uint32_t r0, uint32_t r1) {
+  Run* r = static_cast<Run*>(h);
+  try {
+    r->trace(pass_index, r0, r1);
+    return int64_t(r->records().size());
+  } catch (const std::exception& e) {
+    return -int64_t(fail(e));
+  }
+}
+
+void orc_run_records(void* h, rlc_update_record* out) {
+  const std::vector<rlc_update_record> v = static_cast<Run*>(h)->records();
+  std::copy(v.begin(), v.end(), out);
+}
+
+int orc_run_fold(void* h, const rlc_update_record* all, const uint64_t* counts, uint32_t nranks,
+                 uint32_t rank, uint64_t stride) {
+  Run* r = static_cast<Run*>(h);
+  try {
+    r->fold_records(all, counts, nranks, rank, stride);
+    return RLC_OK;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int64_t orc_run_end_of_pass(void* h) { return static_cast<Run*>(h)->end_of_pass(); }
 
 void orc_run_framebuffer(void* h, double* sum, uint64_t* count) {
   Run* r = static_cast<Run*>(h);

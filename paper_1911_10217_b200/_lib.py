@@ -109,6 +109,10 @@ SIGNATURES = {
     "rlc_render_pass_async": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, _P]),
     "rlc_end_of_pass_update_async": (C.c_int, [_P, _P, C.POINTER(CutConfigC)]),
     "rlc_grid_last_changes": (C.c_int, [_P, _u32p]),
+    "rlc_pass_trace": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, C.c_uint32,
+                                 C.c_uint32, C.POINTER(C.c_void_p), _u64p]),
+    "rlc_pass_fold": (C.c_int, [_P, C.POINTER(RenderConfigC), _P, _P, _P, _u64p, C.c_uint32,
+                                C.c_uint32, C.c_uint64]),
     "rlc_render_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.POINTER(RenderResultC)]),
 }
 

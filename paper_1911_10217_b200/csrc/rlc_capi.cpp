@@ -114,6 +114,14 @@ const char* device_error_message(uint32_t bits) {
 
 }  // namespace
 
+struct PassParamsHolder {
+  rlc::PassParams p{};
+  rlc::DevGrid g{};
+  uint32_t n = 0;
+  const rlc_grid* grid = nullptr;
+  bool valid = false;
+};
+
 struct rlc_context {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -155,10 +163,35 @@ struct rlc_context {
   ~rlc_context() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
   }
+  // sharded pass state (rlc_pass_trace -> rlc_pass_fold)
+  PassParamsHolder shard;
+  DeviceArena xarena;
+  rlc::ExchangeBuffers xb{};
+  unsigned long long* d_counts = nullptr;
+  uint32_t d_counts_cap = 0;
+  void ensure_exchange(uint32_t total, uint32_t nranks) {
+    if (total <= xb.cap && nranks <= d_counts_cap) return;
+    RLC_CK(cudaStreamSynchronize(stream));
+    xarena.release();
+    const uint32_t cap = total > xb.cap ? total : xb.cap;
+    const uint32_t nr = nranks > d_counts_cap ? nranks : d_counts_cap;
+    xb.contig = xarena.alloc<rlc::UpdateRecord>(cap);
+    xb.slots = xarena.alloc<uint32_t>(cap);
+    xb.keys = xarena.alloc<uint32_t>(cap);
+    xb.vals = xarena.alloc<uint32_t>(cap);
+    xb.keys_alt = xarena.alloc<uint32_t>(cap);
+    xb.vals_alt = xarena.alloc<uint32_t>(cap);
+    xb.hist = xarena.alloc<uint32_t>((size_t(cap) / 4096 + 2) * 256);
+    xb.q_rec = xarena.alloc<double>(cap);
+    xb.cap = cap;
+    d_counts = xarena.alloc<unsigned long long>(nr);
+    d_counts_cap = nr;
+  }
   // per-pass scratch, grown on demand
   DeviceArena scratch;
   rlc::PassBuffers pb{};
   uint32_t pb_cap = 0;
+  rlc::UpdateRecord* rec_out = nullptr;  // this rank's exported update records
 
   void ensure_scratch(uint32_t n) {
     if (n <= pb_cap) return;
@@ -175,6 +208,9 @@ struct rlc_context {
     pb.rays = scratch.alloc<rlc::ShadowRay>(cap);
     pb.ray_count = scratch.alloc<unsigned int>(2);
     pb.ray_order = scratch.alloc<uint32_t>(cap);
+    pb.rec_path = scratch.alloc<uint32_t>(cap);
+    pb.rec_count = scratch.alloc<unsigned int>(2);
+    rec_out = scratch.alloc<rlc::UpdateRecord>(cap);
     pb.block_counts = scratch.alloc<uint32_t>(cap / 2048 + 2);
     pb.sort_hist_cap = ((cap + 4095u) / 4096u + 2u) * 256u;  // rows + digit totals
     pb.sort_hist = scratch.alloc<uint32_t>(pb.sort_hist_cap);
@@ -216,10 +252,15 @@ void throw_device_error(uint32_t bits) {
   throw rlc::InvalidArgument(device_error_message(bits));
 }
 
-// render_pass body (proj/src/render.cpp:159-183) for rows [r0, r1).
-void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_t pass_index,
-                  rlc_grid* grid, rlc_framebuffer* fb, uint32_t r0, uint32_t r1) {
-  rlc_context* ctx = const_cast<rlc_context*>(cctx);
+// Validated launch parameters of one pass over rows [r0, r1).
+struct PassSetup {
+  rlc::PassParams p{};
+  rlc::DevGrid g{};
+  uint32_t n = 0;
+};
+
+PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pass_index,
+                     rlc_grid* grid, rlc_framebuffer* fb, bool need_fb, uint32_t r0, uint32_t r1) {
   require(cfg->passes != 0 && cfg->spp % cfg->passes == 0,
           "render_pass: spp must be divisible by passes");
   require(!(cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && grid == nullptr),
@@ -227,48 +268,65 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   require(cfg->sampler <= RLC_SAMPLER_RL_LIGHTCUTS, "render_pass: unknown sampler");
   require(cfg->max_depth == 1,
           "render_pass: the device path implements max_depth == 1 (direct lighting)");
-  require(fb != nullptr && fb->width == ctx->host.cam.width && fb->height == ctx->host.cam.height,
+  require(!need_fb || (fb != nullptr && fb->width == ctx->host.cam.width &&
+                       fb->height == ctx->host.cam.height),
           "render_pass: framebuffer size must match the camera");
   require(r0 <= r1 && r1 <= uint32_t(ctx->host.cam.height), "render_pass: bad row range");
-  require(grid == nullptr || grid->ctx == cctx, "render_pass: grid belongs to another context");
+  require(grid == nullptr || grid->ctx == ctx, "render_pass: grid belongs to another context");
+  PassSetup S;
   const uint32_t spp_pp = cfg->spp / cfg->passes;
   const uint64_t n64 = uint64_t(r1 - r0) * uint64_t(ctx->host.cam.width) * spp_pp;
   require(n64 < (1ull << 31), "render_pass: too many paths for one launch");
-  const uint32_t n = uint32_t(n64);
-  if (n == 0) return;
-  ctx->ensure_scratch(n);
+  S.n = uint32_t(n64);
+  S.p.width = uint32_t(ctx->host.cam.width);
+  S.p.row_begin = r0;
+  S.p.spp_pp = spp_pp;
+  S.p.pass_index = pass_index;
+  S.p.n = S.n;
+  S.p.sampler = cfg->sampler;
+  S.p.seed_mixed = rlc::mix64(cfg->seed);
+  S.p.zero_mixed = rlc::mix64(0);
+  S.p.alpha = grid ? grid->alpha : cfg->cut.alpha;
+  S.p.harmonic = grid ? grid->harmonic : 0u;
+  if (grid) S.g = grid->dev;
+  else S.g.counters = ctx->counters;
+  if (S.n > 0) ctx->ensure_scratch(S.n);
+  return S;
+}
 
-  rlc::PassParams p{};
-  p.width = uint32_t(ctx->host.cam.width);
-  p.row_begin = r0;
-  p.spp_pp = spp_pp;
-  p.pass_index = pass_index;
-  p.n = n;
-  p.sampler = cfg->sampler;
-  p.seed_mixed = rlc::mix64(cfg->seed);
-  p.zero_mixed = rlc::mix64(0);
-  p.alpha = grid ? grid->alpha : cfg->cut.alpha;
-  p.harmonic = grid ? grid->harmonic : 0u;
-
-  rlc::DevGrid g{};
-  if (grid) g = grid->dev;
-  else g.counters = ctx->counters;
+// Primary rays, cut samples and shadow rays of one pass (render.cpp:59-99,
+// estimators.cpp:28-106).  Returns the update records sorted by
+// (cell, cluster) in *k / *v for the learned sampler.
+void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_t** k,
+                   uint32_t** v) {
   cudaStream_t st = ctx->stream;
-  ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, g, p, ctx->pb, st); });
-  ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, g, p, ctx->pb, st); });
+  ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, st); });
+  ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, S.g, S.p, ctx->pb, st); });
   // Shadow rays are traced in sorted (cell, cluster) order: rays of one cell
   // toward one cut cluster share most of their BVH path.  The any-hit result
   // does not depend on the order.
-  uint32_t *k = nullptr, *v = nullptr;
-  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS)
-    ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, n, grid->key_bits, st, &k, &v); });
+  *k = nullptr;
+  *v = nullptr;
+  if (S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS)
+    ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, S.n, grid->key_bits, st, k, v); });
   ctx->stage(6, [&] {
-    rlc::launch_ray_compact(ctx->pb, v, n, st);
-    rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, g.counters, st);
+    rlc::launch_ray_compact(ctx->pb, *v, S.n, st);
+    rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, S.g.counters, st);
   });
+}
+
+// render_pass body (proj/src/render.cpp:159-183) for rows [r0, r1).
+void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_t pass_index,
+                  rlc_grid* grid, rlc_framebuffer* fb, uint32_t r0, uint32_t r1) {
+  rlc_context* ctx = const_cast<rlc_context*>(cctx);
+  const PassSetup S = setup_pass(ctx, cfg, pass_index, grid, fb, true, r0, r1);
+  if (S.n == 0) return;
+  uint32_t *k, *v;
+  enqueue_trace(ctx, S, grid, &k, &v);
+  cudaStream_t st = ctx->stream;
   if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS)
-    ctx->stage(3, [&] { rlc::launch_fold(g, p, k, v, ctx->pb, st); });
-  ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, p, ctx->pb, fb->fb, st); });
+    ctx->stage(3, [&] { rlc::launch_fold(S.g, S.p, k, v, ctx->pb, st); });
+  ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
   RLC_CK(cudaGetLastError());
 }
 
@@ -679,6 +737,70 @@ rlc_status rlc_render_pass_async(const rlc_context* ctx, const rlc_render_config
   return guarded([&] {
     require(ctx != nullptr && config != nullptr, "render_pass: null argument");
     enqueue_pass(ctx, config, pass_index, grid, fb, 0, uint32_t(ctx->host.cam.height));
+  });
+}
+
+rlc_status rlc_pass_trace(const rlc_context* cctx, const rlc_render_config* config,
+                          uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
+                          uint32_t row_end, const void** records, uint64_t* count) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr && records != nullptr && count != nullptr,
+            "rlc_pass_trace: null argument");
+    require(config->sampler == RLC_SAMPLER_RL_LIGHTCUTS && grid != nullptr,
+            "rlc_pass_trace: the sharded pass is the learned sampler's");
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    RLC_CK(cudaSetDevice(ctx->device));
+    const PassSetup S = setup_pass(ctx, config, pass_index, grid, nullptr, false, row_begin,
+                                   row_end);
+    ctx->shard = PassParamsHolder{S.p, S.g, S.n, grid, true};
+    *records = ctx->rec_out;
+    *count = 0;
+    if (S.n == 0) return;
+    uint32_t *k, *v;
+    enqueue_trace(ctx, S, grid, &k, &v);
+    rlc::launch_export_records(S.g, ctx->pb, S.n, ctx->rec_out, ctx->stream);
+    unsigned int c = 0;
+    RLC_CK(cudaMemcpyAsync(&c, ctx->pb.rec_count, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    finish_sync(ctx, grid);
+    *count = c;
+  });
+}
+
+rlc_status rlc_pass_fold(const rlc_context* cctx, const rlc_render_config* config,
+                         rlc_grid* grid, rlc_framebuffer* fb, const void* all_records,
+                         const uint64_t* counts, uint32_t nranks, uint32_t rank,
+                         uint64_t stride) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr && counts != nullptr && nranks > 0 &&
+                rank < nranks, "rlc_pass_fold: bad argument");
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    require(ctx->shard.valid && ctx->shard.grid == grid,
+            "rlc_pass_fold: no matching rlc_pass_trace on this grid");
+    require(fb != nullptr && fb->width == ctx->host.cam.width && fb->height == ctx->host.cam.height,
+            "render_pass: framebuffer size must match the camera");
+    RLC_CK(cudaSetDevice(ctx->device));
+    uint64_t total = 0, own_offset = 0;
+    for (uint32_t r = 0; r < nranks; ++r) {
+      require(counts[r] <= stride, "rlc_pass_fold: count exceeds the per-rank stride");
+      if (r < rank) own_offset += counts[r];
+      total += counts[r];
+    }
+    require(total < (1ull << 31), "rlc_pass_fold: too many records");
+    require(total == 0 || all_records != nullptr, "rlc_pass_fold: null records");
+    const PassParamsHolder S = ctx->shard;
+    ctx->shard.valid = false;
+    ctx->ensure_exchange(uint32_t(total) > 0 ? uint32_t(total) : 1u, nranks);
+    cudaStream_t st = ctx->stream;
+    RLC_CK(cudaMemcpyAsync(ctx->d_counts, counts, 8 * size_t(nranks), cudaMemcpyHostToDevice, st));
+    ctx->stage(3, [&] {
+      rlc::launch_fold_records(S.g, S.p, ctx->pb,
+                               static_cast<const rlc::UpdateRecord*>(all_records), ctx->d_counts,
+                               nranks, stride, uint32_t(total), own_offset, grid->key_bits, ctx->xb,
+                               S.n, st);
+    });
+    if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
+    RLC_CK(cudaGetLastError());
+    finish_sync(ctx, grid);
   });
 }
 

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstddef>
 #include <cstdio>
 
 #include "rlc_kernels.h"
@@ -446,6 +447,7 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
       q_before[idx] = g.t_q[s];  // the fallback cut is never updated
     } else {
       keys[idx] = cell * g.M + s;
+      r.flags |= kSRecord;  // carries an update_q record (render.cpp:111-117)
     }
   } else if (P.sampler == 0u) {
     const uint32_t n = sc.num_lights;
@@ -923,10 +925,12 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restr
 // k_fold: update_q (cut.cpp:76-86) applied per (cell, cluster) segment in
 // canonical order; q_before feeds the deferred radiance.
 // ---------------------------------------------------------------------------
+// v of record `idx` is at vbase + idx * vstride (sample records or exchanged
+// update records); q_before is written per record index.
 __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
                                               const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ vals,
-                                              const SampleRec* __restrict__ srec,
+                                              const char* __restrict__ vbase, uint32_t vstride,
                                               double* __restrict__ q_before) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.n) return;
@@ -939,7 +943,7 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
   uint32_t vis = g.visits[at];
   for (uint32_t j = i; j < P.n && keys[j] == k; ++j) {
     const uint32_t idx = vals[j];
-    const double v = srec[idx].v;
+    const double v = *reinterpret_cast<const double*>(vbase + size_t(idx) * vstride);
     if (!(v >= 0 && isfinite(v)))  // update_q's argument check, cut.cpp:78-80
       atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrBadValue);
     q_before[idx] = q;
@@ -1212,6 +1216,133 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
   count_launch();
 }
 
+static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, uint32_t mask,
+                           uint32_t* out, unsigned int* count_out, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Screen-band sharding with an exact exchange: every
+// rank folds the update records of all ranks in canonical order, so the
+// learned state stays identical on every rank and to a single-GPU run.
+// ---------------------------------------------------------------------------
+__global__ void k_write_records(DevGrid g, const GBuf* __restrict__ gbuf,
+                                const SampleRec* __restrict__ srec,
+                                const uint32_t* __restrict__ rec_path,
+                                const unsigned int* __restrict__ count, uint32_t n,
+                                UpdateRecord* __restrict__ out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || k >= *count) return;
+  const uint32_t idx = rec_path[k];
+  const uint32_t* ck = g.cell_key + size_t(5) * g.slot_cell[gbuf[idx].slot];
+  UpdateRecord r;
+  r.qx = int32_t(ck[0]);
+  r.qy = int32_t(ck[1]);
+  r.qz = int32_t(ck[2]);
+  r.qn = ck[3];
+  r.level = ck[4];
+  r.cluster = srec[idx].s;
+  r.v = srec[idx].v;
+  out[k] = r;
+}
+
+// Gathers all ranks' records (rank-major = canonical order, ranks own
+// contiguous row bands) into one array and inserts their keys.
+__global__ void __launch_bounds__(128) k_insert_records(DevGrid g, const UpdateRecord* __restrict__ all,
+                                                        const unsigned long long* __restrict__ counts,
+                                                        uint32_t nranks, unsigned long long stride,
+                                                        uint32_t total,
+                                                        UpdateRecord* __restrict__ contig,
+                                                        uint32_t* __restrict__ slots) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u;
+  bool need = t < total;
+  Key key{};
+  uint64_t h = 0;
+  if (need) {
+    unsigned long long off = 0, k = t;
+    uint32_t rank = 0;
+    for (; rank < nranks; ++rank) {
+      if (t < off + counts[rank]) {
+        k = t - off;
+        break;
+      }
+      off += counts[rank];
+    }
+    const UpdateRecord r = all[rank * stride + k];
+    contig[t] = r;
+    key = Key{r.qx, r.qy, r.qz, r.qn, r.level};
+    h = hash_key(key);
+  }
+  const unsigned need_mask = __ballot_sync(kFull, need);
+  if (!need) return;
+  const unsigned peers = __match_any_sync(need_mask, h) & need_mask;
+  const int leader = __ffs(peers) - 1;
+  uint32_t slot = 0;
+  if (int(lane) == leader) slot = probe_insert(g, key, h);
+  slot = __shfl_sync(peers, slot, leader);
+  const int lqx = __shfl_sync(peers, key.qx, leader);
+  const int lqy = __shfl_sync(peers, key.qy, leader);
+  const int lqz = __shfl_sync(peers, key.qz, leader);
+  const uint32_t lqn = __shfl_sync(peers, key.qn, leader);
+  const uint32_t llv = __shfl_sync(peers, key.level, leader);
+  if (lqx != key.qx || lqy != key.qy || lqz != key.qz || lqn != key.qn || llv != key.level)
+    slot = probe_insert(g, key, h);
+  if (slot == kFallback)  // a key another rank could insert does not fit here
+    atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrShardOverflow);
+  slots[t] = slot;
+}
+
+__global__ void k_record_keys(DevGrid g, const UpdateRecord* __restrict__ contig,
+                              const uint32_t* __restrict__ slots, uint32_t total,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const uint32_t slot = slots[t];
+  keys[t] = slot == kFallback ? kInvalidKey : g.slot_cell[slot] * g.M + contig[t].cluster;
+  vals[t] = t;
+}
+
+__global__ void k_scatter_qbefore(const double* __restrict__ q_rec, uint64_t own_offset,
+                                  const uint32_t* __restrict__ rec_path,
+                                  const unsigned int* __restrict__ count, uint32_t n,
+                                  double* __restrict__ q_before) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || k >= *count) return;
+  q_before[rec_path[k]] = q_rec[own_offset + k];
+}
+
+void launch_export_records(const DevGrid& g, const PassBuffers& b, uint32_t n,
+                           UpdateRecord* out, cudaStream_t st) {
+  launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);
+  k_write_records<<<blocks_for(n, 256), 256, 0, st>>>(g, b.gbuf, b.srec, b.rec_path, b.rec_count,
+                                                      n, out);
+  count_launch();
+}
+
+void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const PassBuffers& b,
+                         const UpdateRecord* all, const unsigned long long* d_counts,
+                         uint32_t nranks, unsigned long long stride, uint32_t total,
+                         unsigned long long own_offset, uint32_t key_bits, ExchangeBuffers& x,
+                         uint32_t local_n, cudaStream_t st) {
+  if (total > 0) {
+    k_insert_records<<<blocks_for(total, 128), 128, 0, st>>>(g, all, d_counts, nranks, stride,
+                                                             total, x.contig, x.slots);
+    k_record_keys<<<blocks_for(total, 256), 256, 0, st>>>(g, x.contig, x.slots, total, x.keys,
+                                                          x.vals);
+    count_launch(2);
+    uint32_t *k = nullptr, *v = nullptr;
+    launch_sort_buffers(x.keys, x.vals, x.keys_alt, x.vals_alt, x.hist, total, key_bits, st, &k, &v);
+    PassParams p = fold_params;
+    p.n = total;
+    k_fold<<<blocks_for(total, 256), 256, 0, st>>>(
+        g, p, k, v, reinterpret_cast<const char*>(x.contig) + offsetof(UpdateRecord, v),
+        uint32_t(sizeof(UpdateRecord)), x.q_rec);
+    count_launch();
+  }
+  k_scatter_qbefore<<<blocks_for(local_n, 256), 256, 0, st>>>(x.q_rec, own_offset, b.rec_path,
+                                                              b.rec_count, local_n, b.q_before);
+  count_launch();
+}
+
 __global__ void k_resolve(Framebuf fb, uint32_t npix, double* __restrict__ image) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npix) return;
@@ -1241,19 +1372,21 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
 // ---- stable compaction of ray-bearing paths -------------------------------
 constexpr int kCmpThreads = 256, kCmpItems = 8, kCmpTile = kCmpThreads * kCmpItems;
 
-__device__ __forceinline__ bool has_ray(const SampleRec* srec, const uint32_t* order, uint32_t j) {
+__device__ __forceinline__ bool has_flag(const SampleRec* srec, const uint32_t* order, uint32_t j,
+                                         uint32_t mask) {
   const uint32_t i = order ? order[j] : j;
-  return i != kNoSlot && (srec[i].flags & kSRay);
+  return i != kNoSlot && (srec[i].flags & mask);
 }
 
 __global__ void __launch_bounds__(kCmpThreads) k_cmp_count(const SampleRec* __restrict__ srec,
                                                            const uint32_t* __restrict__ order,
-                                                           uint32_t n, uint32_t* __restrict__ counts) {
+                                                           uint32_t n, uint32_t mask,
+                                                           uint32_t* __restrict__ counts) {
   __shared__ uint32_t ws[kCmpThreads / 32];
   uint32_t c = 0;
   for (int k = 0; k < kCmpItems; ++k) {
     const uint32_t j = blockIdx.x * kCmpTile + k * kCmpThreads + threadIdx.x;
-    if (j < n && has_ray(srec, order, j)) ++c;
+    if (j < n && has_flag(srec, order, j, mask)) ++c;
   }
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
@@ -1268,9 +1401,10 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_count(const SampleRec* __re
 // counts[] holds exclusive block offsets (rs_scan) on entry.
 __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const SampleRec* __restrict__ srec,
                                                              const uint32_t* __restrict__ order,
-                                                             uint32_t n, const uint32_t* __restrict__ offs,
+                                                             uint32_t n, uint32_t mask,
+                                                             const uint32_t* __restrict__ offs,
                                                              uint32_t* __restrict__ out,
-                                                             unsigned int* __restrict__ ray_count) {
+                                                             unsigned int* __restrict__ count_out) {
   __shared__ uint32_t wsum[kCmpThreads / 32];
   __shared__ uint32_t base;
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
@@ -1278,7 +1412,7 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const SampleRec* __
   __syncthreads();
   for (int k = 0; k < kCmpItems; ++k) {
     const uint32_t j = blockIdx.x * kCmpTile + k * kCmpThreads + threadIdx.x;
-    const bool f = j < n && has_ray(srec, order, j);
+    const bool f = j < n && has_flag(srec, order, j, mask);
     const unsigned b = __ballot_sync(kFull, f);
     if (lane == 0) wsum[w] = __popc(b);
     __syncthreads();
@@ -1293,18 +1427,23 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const SampleRec* __
     __syncthreads();
   }
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-    ray_count[0] = base;
-    ray_count[1] = 0;
+    count_out[0] = base;
+    count_out[1] = 0;  // fetch cursor of the persistent consumer
   }
 }
 
-void launch_ray_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, cudaStream_t st) {
+static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, uint32_t mask,
+                           uint32_t* out, unsigned int* count_out, cudaStream_t st) {
   const uint32_t nb = blocks_for(n > 0 ? n : 1, kCmpTile);
-  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, b.block_counts);
+  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, mask, b.block_counts);
   rs_scan<<<1, 1024, 0, st>>>(b.block_counts, nb);
-  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, b.block_counts, b.ray_order,
-                                            b.ray_count);
+  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, mask, b.block_counts, out,
+                                            count_out);
   count_launch(3);
+}
+
+void launch_ray_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, cudaStream_t st) {
+  launch_compact(b, order, n, kSRay, b.ray_order, b.ray_count, st);
 }
 
 void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* order,
@@ -1322,19 +1461,16 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   count_launch();
 }
 
-void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
-                 uint32_t** keys_out, uint32_t** vals_out) {
-  uint32_t* ka = b.keys;
-  uint32_t* va = b.vals;
-  uint32_t* kb = b.keys_alt;
-  uint32_t* vb = b.vals_alt;
+void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
+                         uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
+                         uint32_t** vals_out) {
   if (n > 1) {
     const uint32_t nb = blocks_for(n, kRsTile);
     for (uint32_t shift = 0; shift < key_bits; shift += 8) {
-      rs_hist<<<nb, kRsThreads, 0, st>>>(ka, n, int(shift), b.sort_hist);
-      uint32_t* totals = b.sort_hist + size_t(nb) * 256u;
-      rs_scan_rows<<<256, 256, 0, st>>>(b.sort_hist, nb, totals);
-      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, int(shift), b.sort_hist, totals);
+      rs_hist<<<nb, kRsThreads, 0, st>>>(ka, n, int(shift), hist);
+      uint32_t* totals = hist + size_t(nb) * 256u;
+      rs_scan_rows<<<256, 256, 0, st>>>(hist, nb, totals);
+      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, int(shift), hist, totals);
       count_launch(3);
       uint32_t* t = ka;
       ka = kb;
@@ -1348,10 +1484,18 @@ void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
   *vals_out = va;
 }
 
+void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
+                 uint32_t** keys_out, uint32_t** vals_out) {
+  launch_sort_buffers(b.keys, b.vals, b.keys_alt, b.vals_alt, b.sort_hist, n, key_bits, st,
+                      keys_out, vals_out);
+}
+
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
                  const uint32_t* vals, const PassBuffers& b, cudaStream_t st) {
   if (p.n == 0) return;
-  k_fold<<<blocks_for(p.n, 256), 256, 0, st>>>(g, p, keys, vals, b.srec, b.q_before);
+  k_fold<<<blocks_for(p.n, 256), 256, 0, st>>>(
+      g, p, keys, vals, reinterpret_cast<const char*>(b.srec) + offsetof(SampleRec, v),
+      uint32_t(sizeof(SampleRec)), b.q_before);
   count_launch();
 }
 

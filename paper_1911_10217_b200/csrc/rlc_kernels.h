@@ -20,7 +20,8 @@ enum : uint32_t {
   kGMatMask = (1u << 29) - 1,
 };
 // Sample-record flags
-enum : uint32_t { kSNonzero = 1u, kSLearned = 2u, kSRay = 4u };  // kSRay: rays[idx] valid
+// kSRay: rays[idx] valid; kSRecord: the sample carries an update_q record
+enum : uint32_t { kSNonzero = 1u, kSLearned = 2u, kSRay = 4u, kSRecord = 8u };
 
 // Device error bits (mapped to the reference's exceptions by the host).
 enum : uint32_t {
@@ -29,6 +30,7 @@ enum : uint32_t {
   kErrDegenerateLight = 4u,   // sample_triangle_point, scene.cpp:50-51
   kErrBadAreaPdf = 8u,        // level_for_footprint, hash_grid.cpp:35-37
   kErrStackOverflow = 16u,    // BVH deeper than the traversal stack
+  kErrShardOverflow = 32u,    // sharded fold: a foreign key overflowed the hash table
 };
 
 // Counters block (u64 each).
@@ -61,6 +63,13 @@ struct alignas(16) ShadowRay {
   double tmax;  // len - shadow_eps
   uint32_t idx; // path index
   uint32_t pad;
+};
+
+// One update_q record exchanged between ranks (== rlc_update_record).
+struct alignas(16) UpdateRecord {
+  int32_t qx, qy, qz;
+  uint32_t qn, level, cluster;
+  double v;
 };
 
 struct DevScene {
@@ -136,9 +145,24 @@ struct PassBuffers {
   ShadowRay* rays;
   unsigned int* ray_count;  // [0] queued rays, [1] fetch cursor
   uint32_t* ray_order;      // path indices with a shadow ray, in trace order
+  uint32_t* rec_path;       // path index of each update record (canonical order)
+  unsigned int* rec_count;  // [0] update records of the pass
   uint32_t* block_counts;   // compaction scratch
   uint32_t* sort_hist;
   uint32_t sort_hist_cap;  // entries
+};
+
+// Buffers of the sharded fold, sized for the records of all ranks.
+struct ExchangeBuffers {
+  UpdateRecord* contig;
+  uint32_t* slots;
+  uint32_t* keys;
+  uint32_t* vals;
+  uint32_t* keys_alt;
+  uint32_t* vals_alt;
+  uint32_t* hist;
+  double* q_rec;
+  uint32_t cap;
 };
 
 struct Framebuf {
@@ -162,6 +186,16 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
                    unsigned long long* counters, cudaStream_t st);
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out);
+void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
+                         uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
+                         uint32_t** vals_out);
+void launch_export_records(const DevGrid& g, const PassBuffers& b, uint32_t n,
+                           UpdateRecord* out, cudaStream_t st);
+void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const PassBuffers& b,
+                         const UpdateRecord* all, const unsigned long long* d_counts,
+                         uint32_t nranks, unsigned long long stride, uint32_t total,
+                         unsigned long long own_offset, uint32_t key_bits, ExchangeBuffers& x,
+                         uint32_t local_n, cudaStream_t st);
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
                  const uint32_t* vals, const PassBuffers& b, cudaStream_t st);
 void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffers& b,

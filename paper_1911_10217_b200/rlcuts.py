@@ -314,6 +314,33 @@ def end_of_pass_update(grid: HashGrid, ctx: RenderContext, config: CutConfig,
     return ch.value
 
 
+RECORD_DTYPE = np.dtype([("qx", "<i4"), ("qy", "<i4"), ("qz", "<i4"), ("qn", "<u4"),
+                         ("level", "<u4"), ("cluster", "<u4"), ("v", "<f8")])  # rlc_update_record
+
+
+def pass_trace(ctx: RenderContext, config: RenderConfig, pass_index: int, grid: HashGrid,
+               rows: tuple) -> tuple[int, int]:
+    """rlc_pass_trace: trace a band without applying updates.  Returns
+    (device pointer, count) of the band's update records (32 B each)."""
+    cfg = config.c()
+    ptr = C.c_void_p()
+    n = C.c_uint64()
+    _check(_lib.load().rlc_pass_trace(ctx.handle, C.byref(cfg), pass_index, grid.handle,
+                                      rows[0], rows[1], C.byref(ptr), C.byref(n)))
+    return int(ptr.value or 0), int(n.value)
+
+
+def pass_fold(ctx: RenderContext, config: RenderConfig, grid: HashGrid, framebuffer: Framebuffer,
+              all_records_ptr: int, counts, rank: int, stride: int):
+    """rlc_pass_fold: fold every rank's records (device memory, rank-major,
+    `stride` records per rank) and accumulate this rank's band."""
+    cfg = config.c()
+    c = np.ascontiguousarray(counts, np.uint64)
+    _check(_lib.load().rlc_pass_fold(ctx.handle, C.byref(cfg), grid.handle, framebuffer.handle,
+                                     C.c_void_p(all_records_ptr), c.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                     len(c), rank, stride))
+
+
 @dataclass
 class RenderResult:  # render.hpp:56-64
     image: np.ndarray
