@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librlcuts_b200.so")
+LIB_PATH = os.environ.get("RLC_LIB_PATH") or os.path.join(HERE, "librlcuts_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "rlcuts_b200.h")
 
 RLC_OK = 0

@@ -220,7 +220,7 @@ void build_wide(HostScene& out) {
         n.lo[a][c] = round_down(bn.lo[a]);
         n.hi[a][c] = round_up(bn.hi[a]);
       }
-      n.child[c] = bn.count > 0 ? (kWideLeaf | (bn.count << 28) | bn.a) : wid[b];
+      n.child[c] = bn.count > 0 ? (kWideLeaf | ((bn.count - 1) << 28) | bn.a) : wid[b];
     }
   }
 }
@@ -394,6 +394,23 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
 
   build_bvh(d, out);  // render.cpp:145
   build_wide(out);
+  out.nodes_f.resize(out.nodes.size());
+  for (size_t i = 0; i < out.nodes.size(); ++i) {
+    const BvhNode& n = out.nodes[i];
+    BvhNodeF& f = out.nodes_f[i];
+    for (int a = 0; a < 3; ++a) {
+      f.lo[a] = round_down(n.lo[a]);
+      f.hi[a] = round_up(n.hi[a]);
+    }
+    if (n.count > 0) {
+      f.a = kNodeLeaf | n.a;
+      f.b = n.count;
+    } else {
+      if (n.b != n.a + 1) throw std::runtime_error("build_scene_bvh: siblings must be adjacent");
+      f.a = n.a;
+      f.b = 0;
+    }
+  }
 
   // collect_emitters (light_tree.cpp:30-42) over derive_emitters order
   out.lights.clear();

@@ -130,6 +130,16 @@ struct rlc_context {
   rlc::DevScene dev{};
   DeviceArena arena;
   unsigned long long* counters = nullptr;  // error bits for grid-less passes
+  // primary rays of the next pass overlap the tail of the current one: they
+  // run on `pstream` into the other G-buffer slot
+  cudaStream_t pstream = nullptr;
+  cudaEvent_t ev_prim_done = nullptr;
+  cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
+  rlc::GBuf* gslot[2] = {nullptr, nullptr};
+  void sync_all() {
+    RLC_CK(cudaStreamSynchronize(stream));
+    if (pstream) RLC_CK(cudaStreamSynchronize(pstream));
+  }
   // per-stage CUDA-event timing (rlc_context_enable_timing)
   bool timing = false;
   struct Mark {
@@ -139,7 +149,7 @@ struct rlc_context {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<Mark> marks;
-  cudaEvent_t take_event() {
+  cudaEvent_t take_event() {  // pooled timing events
     if (ev_used == ev_pool.size()) {
       cudaEvent_t e;
       RLC_CK(cudaEventCreate(&e));
@@ -147,21 +157,29 @@ struct rlc_context {
     }
     return ev_pool[ev_used++];
   }
-  // Brackets the launches of one stage with events on the context stream.
+  // Brackets the launches of one stage with events on the stream they use.
   template <class F>
-  void stage(int id, F&& launch) {
+  void stage_on(cudaStream_t s, int id, F&& launch) {
     if (!timing || marks.size() >= 200000) {
       launch();
       return;
     }
     const cudaEvent_t a = take_event(), b = take_event();
-    RLC_CK(cudaEventRecord(a, stream));
+    RLC_CK(cudaEventRecord(a, s));
     launch();
-    RLC_CK(cudaEventRecord(b, stream));
+    RLC_CK(cudaEventRecord(b, s));
     marks.push_back(Mark{id, a, b});
+  }
+  template <class F>
+  void stage(int id, F&& launch) {
+    stage_on(stream, id, static_cast<F&&>(launch));
   }
   ~rlc_context() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    if (ev_prim_done) cudaEventDestroy(ev_prim_done);
+    for (cudaEvent_t e : ev_gbuf_free)
+      if (e) cudaEventDestroy(e);
+    if (pstream) cudaStreamDestroy(pstream);
   }
   // sharded pass state (rlc_pass_trace -> rlc_pass_fold)
   PassParamsHolder shard;
@@ -195,10 +213,12 @@ struct rlc_context {
 
   void ensure_scratch(uint32_t n) {
     if (n <= pb_cap) return;
-    RLC_CK(cudaStreamSynchronize(stream));
+    sync_all();
     scratch.release();
     const uint32_t cap = n;
-    pb.gbuf = scratch.alloc<rlc::GBuf>(cap);
+    gslot[0] = scratch.alloc<rlc::GBuf>(cap);
+    gslot[1] = scratch.alloc<rlc::GBuf>(cap);
+    pb.gbuf = gslot[0];
     pb.srec = scratch.alloc<rlc::SampleRec>(cap);
     pb.keys = scratch.alloc<uint32_t>(cap);
     pb.vals = scratch.alloc<uint32_t>(cap);
@@ -300,7 +320,17 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
 void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_t** k,
                    uint32_t** v) {
   cudaStream_t st = ctx->stream;
-  ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, st); });
+  // Primary rays do not read the learned state, only the hash table's keys
+  // (new cells get fresh ids with touched = 0, which the running
+  // split-collapse skips), so they run on the side stream as soon as their
+  // G-buffer slot is free and overlap the previous pass's tail.
+  const int slot = int(S.p.pass_index & 1u);
+  ctx->pb.gbuf = ctx->gslot[slot];
+  RLC_CK(cudaStreamWaitEvent(ctx->pstream, ctx->ev_gbuf_free[slot], 0));
+  ctx->stage_on(ctx->pstream, 0,
+                [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, ctx->pstream); });
+  RLC_CK(cudaEventRecord(ctx->ev_prim_done, ctx->pstream));
+  RLC_CK(cudaStreamWaitEvent(st, ctx->ev_prim_done, 0));
   ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, S.g, S.p, ctx->pb, st); });
   // Shadow rays are traced in sorted (cell, cluster) order: rays of one cell
   // toward one cut cluster share most of their BVH path.  The any-hit result
@@ -327,6 +357,7 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS)
     ctx->stage(3, [&] { rlc::launch_fold(S.g, S.p, k, v, ctx->pb, st); });
   ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
+  RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));  // last G-buffer reader
   RLC_CK(cudaGetLastError());
 }
 
@@ -395,6 +426,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     DeviceArena& A = ctx->arena;
     rlc::DevScene& d = ctx->dev;
     d.nodes = A.upload(h.nodes);
+    d.nodes_f = A.upload(h.nodes_f);
     d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
     d.bparent = A.upload(h.bparent);
     d.tri_leaf = A.upload(h.tri_leaf);
@@ -420,6 +452,12 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     RLC_CK(cudaMemset(ctx->counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
+    RLC_CK(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking));
+    RLC_CK(cudaEventCreateWithFlags(&ctx->ev_prim_done, cudaEventDisableTiming));
+    for (cudaEvent_t& e : ctx->ev_gbuf_free) {
+      RLC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      RLC_CK(cudaEventRecord(e, ctx->stream));
+    }
     *out = ctx.release();
   });
 }
@@ -429,6 +467,7 @@ rlc_status rlc_context_destroy(rlc_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -450,7 +489,7 @@ rlc_status rlc_context_info_get(const rlc_context* ctx, rlc_context_info* info) 
 rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream) {
   return guarded([&] {
     require(ctx != nullptr, "rlc_context_set_stream: null context");
-    RLC_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->sync_all();
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
   });
 }
@@ -458,7 +497,7 @@ rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream) {
 rlc_status rlc_context_synchronize(rlc_context* ctx) {
   return guarded([&] {
     require(ctx != nullptr, "rlc_context_synchronize: null context");
-    RLC_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->sync_all();
   });
 }
 
@@ -472,7 +511,7 @@ rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable) {
 rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts) {
   return guarded([&] {
     require(ctx != nullptr, "rlc_context_stage_times: null context");
-    RLC_CK(cudaStreamSynchronize(ctx->stream));
+    ctx->sync_all();
     double acc[RLC_NUM_STAGES] = {};
     uint32_t cnt[RLC_NUM_STAGES] = {};
     for (const auto& m : ctx->marks) {
@@ -602,7 +641,7 @@ rlc_status rlc_grid_stats_get(const rlc_grid* grid, rlc_grid_stats* stats) {
   return guarded([&] {
     require(grid != nullptr && stats != nullptr, "rlc_grid_stats_get: null argument");
     unsigned long long c[rlc::kCntNum];
-    RLC_CK(cudaStreamSynchronize(grid->ctx->stream));
+    const_cast<rlc_context*>(grid->ctx)->sync_all();
     RLC_CK(cudaMemcpy(c, grid->dev.counters, sizeof(c), cudaMemcpyDeviceToHost));
     stats->occupied = uint32_t(c[rlc::kCntCells]);
     stats->cut_size = grid->dev.M;
@@ -616,7 +655,7 @@ rlc_status rlc_grid_export(const rlc_grid* grid, uint32_t max_cells, rlc_cell_ke
                            uint32_t* visits, uint32_t* num_cells) {
   return guarded([&] {
     require(grid != nullptr, "rlc_grid_export: null grid");
-    RLC_CK(cudaStreamSynchronize(grid->ctx->stream));
+    const_cast<rlc_context*>(grid->ctx)->sync_all();
     unsigned long long nc = 0;
     RLC_CK(cudaMemcpy(&nc, grid->dev.counters + rlc::kCntCells, 8, cudaMemcpyDeviceToHost));
     if (num_cells) *num_cells = uint32_t(nc);
@@ -799,6 +838,7 @@ rlc_status rlc_pass_fold(const rlc_context* cctx, const rlc_render_config* confi
                                S.n, st);
     });
     if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
+    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));
     RLC_CK(cudaGetLastError());
     finish_sync(ctx, grid);
   });

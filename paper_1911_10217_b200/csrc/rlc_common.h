@@ -81,6 +81,17 @@ struct alignas(64) BvhNode {
   uint32_t pad;
 };
 
+// The same binary node with its box rounded outward to fp32 for the
+// closest-hit traversal's fp32 decision tests (exact fp64 only in the rare
+// ambiguous band).  32 B: two siblings share one 64-byte line.
+constexpr uint32_t kNodeLeaf = 0x80000000u;
+struct alignas(32) BvhNodeF {
+  float lo[3];
+  float hi[3];
+  uint32_t a;  // internal: left child (right = a + 1); leaf: kNodeLeaf | first tri
+  uint32_t b;  // leaf: triangle count
+};
+
 // 4-wide node collapsed from the reference binary BVH for the any-hit shadow
 // kernel.  Child boxes are the binary nodes' boxes rounded OUTWARD to fp32,
 // so the fp64 slab test on them passes whenever the reference's test on the
@@ -92,7 +103,7 @@ constexpr uint32_t kWideEmpty = 0xffffffffu; // child: unused slot
 struct alignas(128) Wide4 {
   float lo[3][4];      // [axis][child]
   float hi[3][4];
-  uint32_t child[4];   // internal: Wide4 index; leaf: kWideLeaf | count << 28 | first tri
+  uint32_t child[4];   // internal: Wide4 index; leaf: kWideLeaf | (count - 1) << 28 | first tri
   uint32_t pad[4];
 };
 

@@ -19,6 +19,7 @@
 #include <atomic>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 
 #include "rlc_kernels.h"
 
@@ -137,25 +138,97 @@ __device__ bool occluded(const DevScene& sc, V3 a, V3 b, uint32_t* err) {
   return occluded_ray(sc, a, dir, inv, sc.shadow_eps, len - sc.shadow_eps, err);
 }
 
-// intersect(), proj/src/bvh.cpp:124-157: closest hit, exact-t ties go to the
-// first triangle tested in the reference traversal order (right child first).
+// fp32 decision test of one binary node against the reference's fp64 slab
+// test (bvh.cpp:29-40), both sides bounded:
+//   outer: box rounded outward and the interval widened by the rounding
+//          bound -> if it fails, the reference test fails;
+//   inner: the interval narrowed by the rounding bound plus the box rounding
+//          (|c| |inv| 2^-22) -> if it passes, the reference test passes.
+// Returns 0 (fail), 1 (pass) or 2 (ambiguous: run the exact fp64 test).  The
+// inner test is only used when every |inv| is finite and <= 1e30 (ray.fast),
+// where no fp32 term can be NaN or overflow.
+struct RayDecide {
+  float inv[3], b[3], mt[3], mb[3];
+  uint32_t neg;
+  bool fast;
+};
+
+__device__ __forceinline__ RayDecide make_ray_decide(V3 o, V3 inv) {
+  RayDecide r;
+  const double oa[3] = {o.x, o.y, o.z}, ia[3] = {inv.x, inv.y, inv.z};
+  r.neg = 0;
+  r.fast = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float of = float(oa[a]), fi = float(ia[a]);
+    r.inv[a] = fi;
+    r.b[a] = -(of * fi);
+    r.mt[a] = fmaf(fabsf(of) * fabsf(fi), 0x1.0p-21f, 1e-30f);
+    r.mb[a] = fabsf(fi) * 0x1.0p-22f;
+    r.neg |= (ia[a] < 0 ? 1u : 0u) << a;
+    r.fast &= fabs(ia[a]) <= 1e30;
+  }
+  return r;
+}
+
+__device__ __forceinline__ int box_decide(const float4& q0, const float4& q1, const RayDecide& r,
+                                          float tmin_dn, float tmin_up, float tmax_dn,
+                                          float tmax_up) {
+  constexpr float K = 0x1.0p-20f;
+  const float lo[3] = {q0.x, q0.y, q0.z}, hi[3] = {q0.w, q1.x, q1.y};
+  float no = tmin_dn, fo = tmax_up, ni = tmin_up, fi = tmax_dn;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool neg = (r.neg >> a) & 1u;
+    const float nc = neg ? hi[a] : lo[a];
+    const float fc = neg ? lo[a] : hi[a];
+    const float tn = fmaf(nc, r.inv[a], r.b[a]);
+    const float tf = fmaf(fc, r.inv[a], r.b[a]);
+    const float en = fmaf(fabsf(tn), K, r.mt[a]);
+    const float ef = fmaf(fabsf(tf), K, r.mt[a]);
+    no = fmaxf(no, tn - en);
+    fo = fminf(fo, tf + ef);
+    ni = fmaxf(ni, tn + en + fmaf(fabsf(nc), r.mb[a], 1e-37f));
+    fi = fminf(fi, tf - ef - fmaf(fabsf(fc), r.mb[a], 1e-37f));
+  }
+  if (!(no <= fo)) return 0;
+  if (r.fast && ni <= fi) return 1;
+  return 2;
+}
+
+// intersect(), proj/src/bvh.cpp:124-157: closest hit in the reference's
+// traversal order (pop the right child first), so exact-t ties go to the same
+// triangle.  Every box decision equals the reference's (box_decide, exact
+// fp64 test in the ambiguous band); triangle tests are the exact fp64
+// Moller-Trumbore.
 __device__ bool intersect(const DevScene& sc, V3 o, V3 d, double tmin, double* t_out,
                           uint32_t* tri_out, uint32_t* err) {
   const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+  const RayDecide rd = make_ray_decide(o, inv);
+  const float tmin_dn = __double2float_rd(tmin), tmin_up = __double2float_ru(tmin);
   double closest = HUGE_VAL;
+  float tmax_dn = HUGE_VALF, tmax_up = HUGE_VALF;
   uint32_t hit = kNoSlot;
   uint32_t stack[kStack];
   int sp = 0;
   stack[sp++] = 0;
   while (sp > 0) {
-    const NodeView n = load_node(sc.nodes, stack[--sp]);
-    if (!box_hit(n, o, inv, tmin, closest)) continue;
-    if (n.count > 0) {
-      for (uint32_t i = n.a; i < n.a + n.count; ++i) {
+    const uint32_t i = stack[--sp];
+    const float4* np = reinterpret_cast<const float4*>(sc.nodes_f + i);
+    const float4 q0 = __ldg(np), q1 = __ldg(np + 1);
+    int dcs = box_decide(q0, q1, rd, tmin_dn, tmin_up, tmax_dn, tmax_up);
+    if (dcs == 2) dcs = box_hit(load_node(sc.nodes, i), o, inv, tmin, closest) ? 1 : 0;
+    if (dcs == 0) continue;
+    const uint32_t a = __float_as_uint(q1.z), cnt = __float_as_uint(q1.w);
+    if (a & kNodeLeaf) {
+      const uint32_t first = a & ~kNodeLeaf;
+      for (uint32_t k = first; k < first + cnt; ++k) {
         double t;
-        if (tri_hit(sc.tris, i, o, d, tmin, closest, &t)) {
+        if (tri_hit(sc.tris, k, o, d, tmin, closest, &t)) {
           closest = t;
-          hit = i;
+          hit = k;
+          tmax_dn = __double2float_rd(closest);
+          tmax_up = __double2float_ru(closest);
         }
       }
     } else {
@@ -163,8 +236,8 @@ __device__ bool intersect(const DevScene& sc, V3 o, V3 d, double tmin, double* t
         atomicOr(err, kErrStackOverflow);
         break;
       }
-      stack[sp++] = n.a;
-      stack[sp++] = n.b;
+      stack[sp++] = a;      // left
+      stack[sp++] = a + 1;  // right, popped first (bvh.cpp:147-148)
     }
   }
   if (hit == kNoSlot) return false;
@@ -537,14 +610,23 @@ constexpr int kShadowThreads = 128;
 constexpr int kShadowStack = 32;  // 4-wide levels: the 64-deep binary limit / 2
 constexpr uint32_t kDone = 0x7fffffffu;  // traversal finished (no leaf flag)
 
-// Exact acceptance of a triangle found through the conservative wide tree:
-// every node on its binary ancestor chain (leaf to root) must pass the
-// reference's fp64 slab test (bvh.cpp:29-40) with the fixed shadow interval.
-__device__ __noinline__ bool chain_passes(const DevScene& sc, uint32_t leaf, V3 o, V3 inv,
+// Leaf entries: kWideLeaf | kLeafVerified? | (count - 1) << 28 | first tri.
+constexpr uint32_t kLeafVerified = 0x40000000u;
+__device__ __forceinline__ uint32_t leaf_first(uint32_t e) { return e & 0x0fffffffu; }
+__device__ __forceinline__ uint32_t leaf_count(uint32_t e) { return ((e >> 28) & 3u) + 1u; }
+
+// Exact acceptance of a triangle found through the conservative wide tree.
+// The reference reaches a leaf iff every node on its ancestor chain passes
+// the fp64 slab test (bvh.cpp:29-40).  That test is monotone under box
+// inclusion (a larger box only lowers the entry and raises the exit, and
+// rounding is monotone) and every binary parent's box contains its
+// children's (exact min/max over a superset of triangles), so the chain
+// passes iff the leaf's own box passes: one exact test, skipped entirely
+// when the fp32 inner test already proved it (kLeafVerified).
+__device__ __forceinline__ bool leaf_reached(const DevScene& sc, uint32_t e, V3 o, V3 inv,
                                              double tmin, double tmax) {
-  for (int32_t x = int32_t(leaf); x >= 0; x = __ldg(sc.bparent + x))
-    if (!box_hit(load_node(sc.nodes, uint32_t(x)), o, inv, tmin, tmax)) return false;
-  return true;
+  if (e & kLeafVerified) return true;
+  return box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf + leaf_first(e))), o, inv, tmin, tmax);
 }
 
 // Conservative fp32 slab test of the 4 children of a Wide4 node against one
@@ -558,16 +640,23 @@ __device__ __noinline__ bool chain_passes(const DevScene& sc, uint32_t leaf, V3 
 // fmaxf/fminf, which only drops a constraint.  Rays with |inv| > 1e30 (fp32
 // range) take the exact fp64 path instead (ShadowLane::exact).
 struct RayF {
-  float inv[3], b[3], mt[3];
+  float inv[3], b[3], mt[3], mb[3];
   uint32_t neg;  // bit a: inv[a] < 0 (near plane is hi)
-  float tmin, tmax;
+  float tmin, tmax;        // outward-rounded interval (outer test)
+  float tmin_in, tmax_in;  // inward-rounded interval (inner test)
+  bool fast;               // every |inv| finite and <= 1e30: the inner test is valid
 };
 
+// Also returns in *inner the children whose fp32 inner test passes (the
+// interval narrowed by the rounding bound and the box rounding |c||inv|2^-22),
+// i.e. the children whose exact fp64 test certainly passes (see box_decide).
 __device__ __forceinline__ uint32_t box4_f(const float4 lo[3], const float4 hi[3], const RayF& r,
-                                           float near_out[4]) {
+                                           float near_out[4], uint32_t* inner) {
   constexpr float K = 0x1.0p-20f;
   float nr[4] = {r.tmin, r.tmin, r.tmin, r.tmin};
   float fr[4] = {r.tmax, r.tmax, r.tmax, r.tmax};
+  float ni[4] = {r.tmin_in, r.tmin_in, r.tmin_in, r.tmin_in};
+  float fi[4] = {r.tmax_in, r.tmax_in, r.tmax_in, r.tmax_in};
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const bool neg = (r.neg >> a) & 1u;
@@ -577,20 +666,24 @@ __device__ __forceinline__ uint32_t box4_f(const float4 lo[3], const float4 hi[3
     const float fc[4] = {f4.x, f4.y, f4.z, f4.w};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      float tn = fmaf(nc[c], r.inv[a], r.b[a]);
-      tn = tn - fmaf(fabsf(tn), K, r.mt[a]);
-      float tf = fmaf(fc[c], r.inv[a], r.b[a]);
-      tf = tf + fmaf(fabsf(tf), K, r.mt[a]);
-      nr[c] = fmaxf(nr[c], tn);
-      fr[c] = fminf(fr[c], tf);
+      const float tn = fmaf(nc[c], r.inv[a], r.b[a]);
+      const float tf = fmaf(fc[c], r.inv[a], r.b[a]);
+      const float en = fmaf(fabsf(tn), K, r.mt[a]);
+      const float ef = fmaf(fabsf(tf), K, r.mt[a]);
+      nr[c] = fmaxf(nr[c], tn - en);
+      fr[c] = fminf(fr[c], tf + ef);
+      ni[c] = fmaxf(ni[c], tn + en + fmaf(fabsf(nc[c]), r.mb[a], 1e-37f));
+      fi[c] = fminf(fi[c], tf - ef - fmaf(fabsf(fc[c]), r.mb[a], 1e-37f));
     }
   }
-  uint32_t m = 0;
+  uint32_t m = 0, mi = 0;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     m |= (nr[c] <= fr[c]) ? (1u << c) : 0u;
+    mi |= (ni[c] <= fi[c]) ? (1u << c) : 0u;
     near_out[c] = nr[c];
   }
+  *inner = r.fast ? (mi & m) : 0u;
   return m;
 }
 
@@ -680,10 +773,14 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
               rf.inv[a] = fi;
               rf.b[a] = -(of * fi);
               rf.mt[a] = fmaf(fabsf(of) * fabsf(fi), 0x1.0p-21f, 1e-30f);
+              rf.mb[a] = fabsf(fi) * 0x1.0p-22f;
               rf.neg |= (ia[a] < 0 ? 1u : 0u) << a;
             }
+            rf.fast = fabs(ia[0]) <= 1e30 && fabs(ia[1]) <= 1e30 && fabs(ia[2]) <= 1e30;
             rf.tmin = __double2float_rd(tmin);
             rf.tmax = __double2float_ru(tmax);
+            rf.tmin_in = __double2float_ru(tmin);
+            rf.tmax_in = __double2float_rd(tmax);
             if (exact) {  // tiny scene or fp32-range ray: the exact fp64 path
               if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, idx);
             } else {
@@ -708,7 +805,8 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
       const float4 hi[3] = {__ldg(p + 3), __ldg(p + 4), __ldg(p + 5)};
       const uint4 ch = __ldg(reinterpret_cast<const uint4*>(p + 6));
       float tn[4];
-      uint32_t m = box4_f(lo, hi, rf, tn);
+      uint32_t mi;
+      uint32_t m = box4_f(lo, hi, rf, tn, &mi);
       if (ch.z == kWideEmpty) m &= ~4u;
       if (ch.w == kWideEmpty) m &= ~8u;
       if (sp + 3 > kShadowStack) {
@@ -718,6 +816,9 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
       }
       // nearest entry first: occluders near the shading point end the ray early
       uint32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)  // leaf children the inner test proved reached
+        if ((mi >> k) & (c[k] >> 31)) c[k] |= kLeafVerified;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (!(m & (1u << k))) tn[k] = HUGE_VALF;
@@ -747,9 +848,9 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
     // every leaf that follows it directly, then the exact ancestor chain
     bool hit = false;
     while (leaf != 0) {
-      const uint32_t first = leaf & 0x0fffffffu, cnt = (leaf >> 28) & 7u;
+      const uint32_t first = leaf_first(leaf), cnt = leaf_count(leaf);
       for (uint32_t i = first; i < first + cnt; ++i) hit |= tri_any(sc.tris, i, o, d, tmin, tmax);
-      if (hit) hit = chain_passes(sc, __ldg(sc.tri_leaf + first), o, inv, tmin, tmax);
+      if (hit) hit = leaf_reached(sc, leaf, o, inv, tmin, tmax);
       if (hit) break;
       if (cur != kDone && (cur & kWideLeaf)) {
         leaf = cur;
@@ -1452,6 +1553,8 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   if (blocks == 0) {
     int per_sm = 0, dev = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shadow, kShadowThreads, 0);
+    if (const char* e = getenv("RLC_SHADOW_BLOCKS_PER_SM"))  // tuning knob (co-residency)
+      if (atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     blocks = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
