@@ -18,6 +18,8 @@
 #include <cstring>
 #include <deque>
 #include <numeric>
+#include <cstdlib>
+#include <string>
 
 namespace rlc {
 
@@ -156,24 +158,142 @@ double surface(const BvhNode& n) {
   return dx * dy + dy * dz + dz * dx;
 }
 
-// 4-wide tree collapsed from the binary BVH: every wide node stands for one
-// binary internal node and lists up to four of its descendants (children
-// expanded largest-surface-first); child boxes are rounded outward to fp32.
-void build_wide(HostScene& out) {
-  const std::vector<BvhNode>& nodes = out.nodes;
-  out.wide.clear();
-  out.bparent.assign(nodes.size(), -1);
-  out.tri_leaf.assign(out.tris.size(), 0);
-  for (size_t i = 0; i < nodes.size(); ++i) {
-    if (nodes[i].count == 0) {
-      out.bparent[nodes[i].a] = int32_t(i);
-      out.bparent[nodes[i].b] = int32_t(i);
+// Binned-SAH binary tree whose leaves are exactly the reference BVH's leaves
+// (same triangle ranges, same exact boxes).  Every node box is the exact
+// union of the leaf boxes below it, so it contains them: traversing this
+// tree with a conservative test reaches every leaf whose exact slab test
+// passes, which is all the exact any-hit acceptance needs.
+std::vector<BvhNode> sah_over_leaves(const std::vector<BvhNode>& ref) {
+  struct Prim {
+    Box b;
+    V3 c;
+    uint32_t node;
+  };
+  std::vector<Prim> prims;
+  for (uint32_t i = 0; i < ref.size(); ++i) {
+    if (ref[i].count == 0) continue;
+    Box b;
+    b.lo = V3{ref[i].lo[0], ref[i].lo[1], ref[i].lo[2]};
+    b.hi = V3{ref[i].hi[0], ref[i].hi[1], ref[i].hi[2]};
+    prims.push_back(Prim{b, b.center(), i});
+  }
+  auto area = [](const Box& b) {
+    const V3 e = b.extent();
+    return e.x * e.y + e.y * e.z + e.z * e.x;
+  };
+  std::vector<BvhNode> out;
+  out.reserve(2 * prims.size());
+  out.push_back(BvhNode{});
+  struct Todo {
+    uint32_t node, begin, end;
+  };
+  std::vector<Todo> todo{{0, 0, uint32_t(prims.size())}};
+  constexpr int kBins = 16;
+  while (!todo.empty()) {
+    const Todo t = todo.back();
+    todo.pop_back();
+    Box bounds, cb;
+    for (uint32_t i = t.begin; i < t.end; ++i) {
+      bounds.grow(prims[i].b);
+      cb.grow(prims[i].c);
+    }
+    BvhNode& nd = out[t.node];
+    put3(nd.lo, bounds.lo);
+    put3(nd.hi, bounds.hi);
+    if (t.end - t.begin == 1) {
+      const BvhNode& leaf = ref[prims[t.begin].node];
+      nd.a = leaf.a;
+      nd.b = 0;
+      nd.count = leaf.count;
+      continue;
+    }
+    int best_axis = -1, best_split = 0;
+    double best_cost = HUGE_VAL;
+    for (int a = 0; a < 3; ++a) {
+      const double lo = comp(cb.lo, a), ext = comp(cb.hi, a) - lo;
+      if (!(ext > 0)) continue;
+      Box bb[kBins];
+      uint32_t cnt[kBins] = {};
+      for (uint32_t i = t.begin; i < t.end; ++i) {
+        int k = int((comp(prims[i].c, a) - lo) / ext * kBins);
+        k = k < 0 ? 0 : (k >= kBins ? kBins - 1 : k);
+        bb[k].grow(prims[i].b);
+        ++cnt[k];
+      }
+      Box right[kBins];
+      uint32_t rc[kBins] = {};
+      Box acc;
+      uint32_t n = 0;
+      for (int k = kBins - 1; k > 0; --k) {
+        acc.grow(bb[k]);
+        n += cnt[k];
+        right[k] = acc;
+        rc[k] = n;
+      }
+      Box left;
+      uint32_t nl = 0;
+      for (int k = 1; k < kBins; ++k) {
+        left.grow(bb[k - 1]);
+        nl += cnt[k - 1];
+        if (nl == 0 || rc[k] == 0) continue;
+        const double cost = area(left) * nl + area(right[k]) * rc[k];
+        if (cost < best_cost) {
+          best_cost = cost;
+          best_axis = a;
+          best_split = k;
+        }
+      }
+    }
+    uint32_t mid;
+    if (best_axis < 0) {
+      mid = t.begin + (t.end - t.begin) / 2;
     } else {
-      for (uint32_t t = nodes[i].a; t < nodes[i].a + nodes[i].count; ++t)
+      const double lo = comp(cb.lo, best_axis), ext = comp(cb.hi, best_axis) - lo;
+      const auto it = std::partition(prims.begin() + t.begin, prims.begin() + t.end,
+                                     [&](const Prim& p) {
+                                       int k = int((comp(p.c, best_axis) - lo) / ext * kBins);
+                                       k = k < 0 ? 0 : (k >= kBins ? kBins - 1 : k);
+                                       return k < best_split;
+                                     });
+      mid = uint32_t(it - prims.begin());
+      if (mid == t.begin || mid == t.end) mid = t.begin + (t.end - t.begin) / 2;
+    }
+    const uint32_t child = uint32_t(out.size());
+    out.push_back(BvhNode{});
+    out.push_back(BvhNode{});
+    out[t.node].a = child;
+    out[t.node].b = child + 1;
+    out[t.node].count = 0;
+    todo.push_back({child, t.begin, mid});
+    todo.push_back({child + 1, mid, t.end});
+  }
+  return out;
+}
+
+// 4-wide tree for the any-hit shadow kernel, collapsed from a binary tree
+// over the reference leaves: every wide node stands for one binary internal
+// node and lists up to four of its descendants (children expanded
+// largest-surface-first); child boxes are rounded outward to fp32.  The
+// binary tree is a binned-SAH tree over the reference's leaves (default) or
+// the reference tree itself (RLC_SHADOW_TREE=reference).
+void build_wide(HostScene& out) {
+  out.wide.clear();
+  out.bparent.assign(out.nodes.size(), -1);
+  out.tri_leaf.assign(out.tris.size(), 0);
+  for (size_t i = 0; i < out.nodes.size(); ++i) {
+    if (out.nodes[i].count == 0) {
+      out.bparent[out.nodes[i].a] = int32_t(i);
+      out.bparent[out.nodes[i].b] = int32_t(i);
+    } else {
+      for (uint32_t t = out.nodes[i].a; t < out.nodes[i].a + out.nodes[i].count; ++t)
         out.tri_leaf[t] = uint32_t(i);
     }
   }
-  if (nodes.empty() || nodes[0].count > 0) return;
+  if (out.nodes.empty() || out.nodes[0].count > 0) return;
+  const char* mode = std::getenv("RLC_SHADOW_TREE");
+  const bool use_ref = mode != nullptr && std::string(mode) == "reference";
+  const std::vector<BvhNode> sah = use_ref ? std::vector<BvhNode>() : sah_over_leaves(out.nodes);
+  const std::vector<BvhNode>& nodes = use_ref ? out.nodes : sah;
   if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
   std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
   std::vector<std::array<uint32_t, 4>> kids;
