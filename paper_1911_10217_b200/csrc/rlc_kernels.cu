@@ -356,10 +356,37 @@ __device__ uint32_t probe_insert(const DevGrid& g, const Key& k, uint64_t h) {
 // ---------------------------------------------------------------------------
 // k_primary: PassRenderer::trace up to the cell lookup (render.cpp:59-99)
 // ---------------------------------------------------------------------------
+// Thread -> path mapping: with one sample per pixel and pass, each warp
+// takes an 8 x 4 pixel tile (coherent camera rays for the packet traversal);
+// otherwise consecutive canonical indices.  Results land at the canonical
+// index either way.
+__device__ __forceinline__ bool path_of_thread(const PassParams& P, uint32_t rows, uint32_t* idx,
+                                               uint32_t* px, uint32_t* py, uint32_t* s) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (P.spp_pp == 1) {
+    const uint32_t warp = t >> 5, lane = t & 31u;
+    const uint32_t tiles_x = (P.width + 7u) / 8u;
+    const uint32_t tx = warp % tiles_x, ty = warp / tiles_x;
+    const uint32_t x = tx * 8u + (lane & 7u), y = ty * 4u + (lane >> 3);
+    *s = 0;
+    *px = x;
+    *py = P.row_begin + y;
+    *idx = y * P.width + x;
+    return x < P.width && y < rows;
+  }
+  *idx = t;
+  *s = t % P.spp_pp;
+  const uint32_t pix = t / P.spp_pp;
+  *px = pix % P.width;
+  *py = P.row_begin + pix / P.width;
+  return t < P.n;
+}
+
 __global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassParams P,
                                                  GBuf* __restrict__ gbuf) {
-  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = idx < P.n;
+  const uint32_t rows = P.n / (P.width * P.spp_pp);
+  uint32_t idx, px, py, s;
+  const bool active = path_of_thread(P, rows, &idx, &px, &py, &s);
   const uint32_t lane = threadIdx.x & 31u;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
 
@@ -369,15 +396,12 @@ __global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassPar
   GBuf out;
   out.slot = kNoSlot;
   out.flags = 0;
+  V3 org{0, 0, 0}, dir{0, 0, 1};
+  uint64_t rk = 0;
   if (active) {
-    const uint32_t s = idx % P.spp_pp;
-    const uint32_t pix = idx / P.spp_pp;
-    const uint32_t px = pix % P.width;
-    const uint32_t py = P.row_begin + pix / P.width;
     const uint64_t pixel_index = uint64_t(py) * uint64_t(P.width) + px;
     const uint64_t sample_index = uint64_t(P.pass_index) * P.spp_pp + s;
-    const uint64_t rk = rng_key(P.seed_mixed, pixel_index, sample_index, P.zero_mixed);
-    out.rng = rk;
+    rk = rng_key(P.seed_mixed, pixel_index, sample_index, P.zero_mixed);
     const double jx = rng_draw(rk, kDrawJx);
     const double jy = rng_draw(rk, kDrawJy);
     // camera_ray, scene.cpp:10-23
@@ -386,11 +410,16 @@ __global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassPar
     const double fy = double(py) + jy;
     const double sx = (2.0 * fx / c.width_d - 1.0) * c.tan_half * c.aspect;
     const double sy = (1.0 - 2.0 * fy / c.height_d) * c.tan_half;
-    const V3 dir = normalize(ld3(c.u) * sx + ld3(c.v) * sy - ld3(c.w));
-    const V3 org = ld3(c.origin);
-    double t;
-    uint32_t tri;
-    if (intersect(sc, org, dir, 0.0, &t, &tri, err)) {
+    dir = normalize(ld3(c.u) * sx + ld3(c.v) * sy - ld3(c.w));
+    org = ld3(c.origin);
+  }
+  out.rng = rk;
+  double t = 0;
+  uint32_t tri = 0;
+  const bool got = active && intersect(sc, org, dir, 0.0, &t, &tri, err);
+  if (active) {
+    const CameraConst& c = sc.cam;
+    if (got) {
       const V3 pos = org + dir * t;
       const V3 ng = ld3(sc.tri_normal + size_t(3) * tri);
       const V3 wo = -dir;
@@ -1457,7 +1486,13 @@ __global__ void k_resolve(Framebuf fb, uint32_t npix, double* __restrict__ image
 void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
                     const PassBuffers& b, cudaStream_t st) {
   if (p.n == 0) return;
-  k_primary<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, b.gbuf);
+  uint32_t blocks = blocks_for(p.n, 128);
+  if (p.spp_pp == 1) {  // 8 x 4 pixel tiles per warp (path_of_thread)
+    const uint32_t rows = p.n / p.width;
+    const uint32_t warps = ((p.width + 7u) / 8u) * ((rows + 3u) / 4u);
+    blocks = (warps + 3u) / 4u;
+  }
+  k_primary<<<blocks, 128, 0, st>>>(sc, g, p, b.gbuf);
   count_launch();
 }
 
