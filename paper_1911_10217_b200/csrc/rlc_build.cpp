@@ -600,6 +600,16 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   cam.pdf_omega = 1.0 / ((plane_w / d.width) * (plane_h / d.height));
 
   level_thresholds(out.level_threshold);
+
+  // Camera-relative copy for the primary rays, whose origin is exactly the
+  // camera origin O: the reference's per-axis term fl64(c - O) rounded
+  // outward to fp32, so every fp32 error of the decision test is relative.
+  out.nodes_cam = out.nodes_f;
+  for (size_t i = 0; i < out.nodes.size(); ++i)
+    for (int a = 0; a < 3; ++a) {
+      out.nodes_cam[i].lo[a] = round_down(out.nodes[i].lo[a] - cam.origin[a]);
+      out.nodes_cam[i].hi[a] = round_up(out.nodes[i].hi[a] - cam.origin[a]);
+    }
 }
 
 }  // namespace rlc

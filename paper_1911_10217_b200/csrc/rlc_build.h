@@ -26,6 +26,7 @@ struct HostScene {
   // scene BVH (reference topology, bvh.cpp:64-122)
   std::vector<BvhNode> nodes;
   std::vector<BvhNodeF> nodes_f;  // same topology, fp32 outward-rounded boxes
+  std::vector<BvhNodeF> nodes_cam; // same, boxes relative to the camera origin (fl64(c - O))
   std::vector<TriAccel> tris;  // BVH leaf order
   std::vector<Wide4> wide;       // 4-wide conservative tree, DFS order (empty: root is a leaf)
   std::vector<int32_t> bparent;  // binary BVH parent per node (-1 at the root)

@@ -427,6 +427,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     rlc::DevScene& d = ctx->dev;
     d.nodes = A.upload(h.nodes);
     d.nodes_f = A.upload(h.nodes_f);
+    d.nodes_cam = A.upload(h.nodes_cam);
     d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
     d.bparent = A.upload(h.bparent);
     d.tri_leaf = A.upload(h.tri_leaf);

@@ -246,6 +246,90 @@ __device__ bool intersect(const DevScene& sc, V3 o, V3 d, double tmin, double* t
   return true;
 }
 
+// Camera rays: origin == the camera origin O, so the node boxes can be
+// stored as fp32(fl64(c - O)) rounded outward (nodes_cam) and every error of
+// the fp32 decision test is relative to the per-axis t (inverse and product
+// rounding, box rounding, the reference's own fp64 rounding: < 4 u32 in
+// total; K = 8 u32).  Same three outcomes as box_decide; the 1e-30 slack
+// covers underflow.
+__device__ __forceinline__ int box_decide_cam(const float4& q0, const float4& q1,
+                                              const float inv[3], uint32_t neg, bool fast,
+                                              float tmin_dn, float tmin_up, float tmax_dn,
+                                              float tmax_up) {
+  constexpr float K = 0x1.0p-21f;
+  const float lo[3] = {q0.x, q0.y, q0.z}, hi[3] = {q0.w, q1.x, q1.y};
+  float no = tmin_dn, fo = tmax_up, ni = tmin_up, fi = tmax_dn;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool ng = (neg >> a) & 1u;
+    const float tn = (ng ? hi[a] : lo[a]) * inv[a];
+    const float tf = (ng ? lo[a] : hi[a]) * inv[a];
+    no = fmaxf(no, fmaf(fabsf(tn), -K, tn));
+    ni = fmaxf(ni, fmaf(fabsf(tn), K, tn));
+    fo = fminf(fo, fmaf(fabsf(tf), K, tf));
+    fi = fminf(fi, fmaf(fabsf(tf), -K, tf));
+  }
+  if (!(no <= fo + 1e-30f)) return 0;
+  if (fast && ni + 1e-30f <= fi) return 1;
+  return 2;
+}
+
+// intersect() for camera rays: the reference order and decisions, with the
+// camera-relative decision test.
+__device__ bool intersect_camera(const DevScene& sc, V3 o, V3 d, double* t_out,
+                                 uint32_t* tri_out, uint32_t* err) {
+  const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+  const double ia[3] = {inv.x, inv.y, inv.z};
+  float finv[3];
+  uint32_t neg = 0;
+  bool fast = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    finv[a] = float(ia[a]);
+    neg |= (ia[a] < 0 ? 1u : 0u) << a;
+    fast &= fabs(ia[a]) <= 1e30;
+  }
+  const double tmin = 0.0;
+  double closest = HUGE_VAL;
+  float tmax_dn = HUGE_VALF, tmax_up = HUGE_VALF;
+  uint32_t hit = kNoSlot;
+  uint32_t stack[kStack];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp > 0) {
+    const uint32_t i = stack[--sp];
+    const float4* np = reinterpret_cast<const float4*>(sc.nodes_cam + i);
+    const float4 q0 = __ldg(np), q1 = __ldg(np + 1);
+    int dcs = box_decide_cam(q0, q1, finv, neg, fast, 0.f, 0.f, tmax_dn, tmax_up);
+    if (dcs == 2) dcs = box_hit(load_node(sc.nodes, i), o, inv, tmin, closest) ? 1 : 0;
+    if (dcs == 0) continue;
+    const uint32_t a = __float_as_uint(q1.z), cnt = __float_as_uint(q1.w);
+    if (a & kNodeLeaf) {
+      const uint32_t first = a & ~kNodeLeaf;
+      for (uint32_t k = first; k < first + cnt; ++k) {
+        double t;
+        if (tri_hit(sc.tris, k, o, d, tmin, closest, &t)) {
+          closest = t;
+          hit = k;
+          tmax_dn = __double2float_rd(closest);
+          tmax_up = __double2float_ru(closest);
+        }
+      }
+    } else {
+      if (sp + 2 > kStack) {
+        atomicOr(err, kErrStackOverflow);
+        break;
+      }
+      stack[sp++] = a;      // left
+      stack[sp++] = a + 1;  // right, popped first (bvh.cpp:147-148)
+    }
+  }
+  if (hit == kNoSlot) return false;
+  *t_out = closest;
+  *tri_out = sc.tris[hit].tri_id;
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // hash-grid key (proj/src/hash_grid.cpp:27-100)
 // ---------------------------------------------------------------------------
@@ -416,7 +500,8 @@ __global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassPar
   out.rng = rk;
   double t = 0;
   uint32_t tri = 0;
-  const bool got = active && intersect(sc, org, dir, 0.0, &t, &tri, err);
+  const bool got = active && (sc.fp32_ok ? intersect_camera(sc, org, dir, &t, &tri, err)
+                                         : intersect(sc, org, dir, 0.0, &t, &tri, err));
   if (active) {
     const CameraConst& c = sc.cam;
     if (got) {
