@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -133,6 +134,7 @@ struct rlc_context {
   // primary rays of the next pass overlap the tail of the current one: they
   // run on `pstream` into the other G-buffer slot
   cudaStream_t pstream = nullptr;
+  bool overlap = false;  // RLC_OVERLAP=1: primary rays of the next pass on a side stream
   cudaEvent_t ev_prim_done = nullptr;
   cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
   rlc::GBuf* gslot[2] = {nullptr, nullptr};
@@ -326,11 +328,15 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   // G-buffer slot is free and overlap the previous pass's tail.
   const int slot = int(S.p.pass_index & 1u);
   ctx->pb.gbuf = ctx->gslot[slot];
-  RLC_CK(cudaStreamWaitEvent(ctx->pstream, ctx->ev_gbuf_free[slot], 0));
-  ctx->stage_on(ctx->pstream, 0,
-                [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, ctx->pstream); });
-  RLC_CK(cudaEventRecord(ctx->ev_prim_done, ctx->pstream));
-  RLC_CK(cudaStreamWaitEvent(st, ctx->ev_prim_done, 0));
+  if (ctx->overlap) {
+    RLC_CK(cudaStreamWaitEvent(ctx->pstream, ctx->ev_gbuf_free[slot], 0));
+    ctx->stage_on(ctx->pstream, 0,
+                  [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, ctx->pstream); });
+    RLC_CK(cudaEventRecord(ctx->ev_prim_done, ctx->pstream));
+    RLC_CK(cudaStreamWaitEvent(st, ctx->ev_prim_done, 0));
+  } else {
+    ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, st); });
+  }
   ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, S.g, S.p, ctx->pb, st); });
   // Shadow rays are traced in sorted (cell, cluster) order: rays of one cell
   // toward one cut cluster share most of their BVH path.  The any-hit result
@@ -454,6 +460,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     RLC_CK(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking));
+    if (const char* e = std::getenv("RLC_OVERLAP")) ctx->overlap = std::string(e) == "1";
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_prim_done, cudaEventDisableTiming));
     for (cudaEvent_t& e : ctx->ev_gbuf_free) {
       RLC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
