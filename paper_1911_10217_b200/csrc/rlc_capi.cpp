@@ -207,6 +207,13 @@ struct rlc_context {
     d_counts = xarena.alloc<unsigned long long>(nr);
     d_counts_cap = nr;
   }
+  // render_frame cache (prepare_frame_cache)
+  rlc_grid* frame_grid = nullptr;
+  rlc_framebuffer* frame_fb = nullptr;
+  rlc_render_config frame_cfg{};
+  DeviceArena frame_hist_arena;
+  uint32_t* frame_hist = nullptr;
+  uint32_t frame_hist_cap = 0;
   // per-pass scratch, grown on demand
   DeviceArena scratch;
   rlc::PassBuffers pb{};
@@ -373,6 +380,8 @@ void finish_sync(const rlc_context* ctx, rlc_grid* grid) {
   if (bits) throw_device_error(bits);
 }
 
+void prepare_frame_cache(rlc_context* ctx, const rlc_render_config* config);
+
 void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* cut,
                  uint32_t* d_changes) {
   require(grid != nullptr && ctx != nullptr && cut != nullptr,
@@ -466,6 +475,9 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
       RLC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       RLC_CK(cudaEventRecord(e, ctx->stream));
     }
+    // render_frame's grid, framebuffer and pass buffers for this config
+    prepare_frame_cache(ctx.get(), config);
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
     *out = ctx.release();
   });
 }
@@ -476,6 +488,8 @@ rlc_status rlc_context_destroy(rlc_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
+    rlc_grid_destroy(ctx->frame_grid);
+    rlc_framebuffer_destroy(ctx->frame_fb);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -882,55 +896,108 @@ rlc_status rlc_grid_last_changes(const rlc_grid* grid, uint32_t* changes) {
   });
 }
 
-rlc_status rlc_render_frame(const rlc_context* ctx, const rlc_render_config* config,
-                            double* image_out, rlc_render_result* result) {
-  return guarded([&] {
-    require(ctx != nullptr && config != nullptr, "render_frame: null argument");
-    require(config->passes != 0 && config->spp != 0 && config->spp % config->passes == 0,
-            "render_frame: spp must be divisible by passes");
-    const auto t0 = std::chrono::steady_clock::now();
-    rlc_framebuffer* fbp = nullptr;
-    rlc_grid* gp = nullptr;
-    rlc_status st = rlc_framebuffer_create(ctx, ctx->host.cam.width, ctx->host.cam.height, &fbp);
-    if (st != RLC_OK) throw std::runtime_error(g_err);
-    std::unique_ptr<rlc_framebuffer> fb(fbp);
-    std::unique_ptr<rlc_grid> grid;
-    if (config->sampler == RLC_SAMPLER_RL_LIGHTCUTS) {
-      st = rlc_grid_create(ctx, config, &gp);
+}  // extern "C"
+
+namespace {
+
+bool same_grid_config(const rlc_render_config& a, const rlc_render_config& b) {
+  return a.hash.capacity == b.hash.capacity && a.hash.probe_limit == b.hash.probe_limit &&
+         a.hash.normal_bits == b.hash.normal_bits && a.hash.jitter_scale == b.hash.jitter_scale &&
+         a.cut.cut_size == b.cut.cut_size && a.cut.eps_q == b.cut.eps_q &&
+         a.cut.alpha == b.cut.alpha && a.cut.alpha_schedule == b.cut.alpha_schedule;
+}
+
+// A fresh HashGrid in place: empty slots, no cells, zeroed counters.  Cut
+// rows need no reset (a row is written from the template when its cell is
+// inserted, src/hash_grid.cpp:126).
+void reset_grid(rlc_grid* g, cudaStream_t st) {
+  const size_t cap = g->dev.capacity;
+  RLC_CK(cudaMemsetAsync(g->dev.slot_keys, 0, 16 * cap, st));
+  RLC_CK(cudaMemsetAsync(g->dev.touched, 0, 4 * cap, st));
+  RLC_CK(cudaMemsetAsync(g->dev.counters, 0, sizeof(unsigned long long) * rlc::kCntNum, st));
+  RLC_CK(cudaMemsetAsync(g->d_changes, 0, 4, st));
+}
+
+// The context's reusable render_frame state (grid, framebuffer, per-pass
+// change counts), allocated once -- at context creation for the creation
+// config -- so render_frame itself performs no device allocation.
+void prepare_frame_cache(rlc_context* ctx, const rlc_render_config* config) {
+  if (config->sampler == RLC_SAMPLER_RL_LIGHTCUTS) {
+    if (ctx->frame_grid == nullptr || !same_grid_config(ctx->frame_cfg, *config)) {
+      if (ctx->frame_grid) {
+        rlc_grid_destroy(ctx->frame_grid);
+        ctx->frame_grid = nullptr;
+      }
+      rlc_grid* g = nullptr;
+      const rlc_status st = rlc_grid_create(ctx, config, &g);
       if (st == RLC_ERR_INVALID_ARGUMENT) throw rlc::InvalidArgument(g_err);
       if (st != RLC_OK) throw std::runtime_error(g_err);
-      grid.reset(gp);
+      ctx->frame_grid = g;
+      ctx->frame_cfg = *config;
     }
-    DeviceArena hist;
-    uint32_t* d_hist = hist.alloc<uint32_t>(config->passes);
-    RLC_CK(cudaMemsetAsync(d_hist, 0, 4 * size_t(config->passes), ctx->stream));
+  }
+  if (ctx->frame_fb == nullptr) {
+    rlc_framebuffer* fb = nullptr;
+    if (rlc_framebuffer_create(ctx, ctx->host.cam.width, ctx->host.cam.height, &fb) != RLC_OK)
+      throw std::runtime_error(g_err);
+    ctx->frame_fb = fb;
+  }
+  if (config->passes > ctx->frame_hist_cap) {
+    ctx->frame_hist_arena.release();
+    ctx->frame_hist = ctx->frame_hist_arena.alloc<uint32_t>(config->passes);
+    ctx->frame_hist_cap = config->passes;
+  }
+  if (config->passes != 0 && config->spp % config->passes == 0)
+    ctx->ensure_scratch(uint32_t(ctx->host.cam.width) * uint32_t(ctx->host.cam.height) *
+                        (config->spp / config->passes));
+}
+
+}  // namespace
+
+extern "C" {
+
+rlc_status rlc_render_frame(const rlc_context* cctx, const rlc_render_config* config,
+                            double* image_out, rlc_render_result* result) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr, "render_frame: null argument");
+    require(config->passes != 0 && config->spp != 0 && config->spp % config->passes == 0,
+            "render_frame: spp must be divisible by passes");
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    const auto t0 = std::chrono::steady_clock::now();
+    RLC_CK(cudaSetDevice(ctx->device));
+    prepare_frame_cache(ctx, config);
+    rlc_grid* grid = config->sampler == RLC_SAMPLER_RL_LIGHTCUTS ? ctx->frame_grid : nullptr;
+    rlc_framebuffer* fb = ctx->frame_fb;
+    cudaStream_t st = ctx->stream;
+    if (grid) {
+      grid->alpha = config->cut.alpha;
+      reset_grid(grid, st);
+    }
+    const size_t npix = size_t(fb->width) * size_t(fb->height);
+    RLC_CK(cudaMemsetAsync(fb->fb.sum, 0, 24 * npix, st));
+    RLC_CK(cudaMemsetAsync(fb->fb.count, 0, 8 * npix, st));
+    uint32_t* d_hist = ctx->frame_hist;
+    RLC_CK(cudaMemsetAsync(d_hist, 0, 4 * size_t(config->passes), st));
     for (uint32_t pass = 0; pass < config->passes; ++pass) {
-      enqueue_pass(ctx, config, pass, grid.get(), fb.get(), 0, uint32_t(ctx->host.cam.height));
-      if (grid) enqueue_eop(grid.get(), ctx, &config->cut, d_hist + pass);
+      enqueue_pass(ctx, config, pass, grid, fb, 0, uint32_t(ctx->host.cam.height));
+      if (grid) enqueue_eop(grid, ctx, &config->cut, d_hist + pass);
     }
-    const uint32_t npix = uint32_t(size_t(fb->width) * size_t(fb->height));
     if (image_out) {
-      rlc::launch_resolve(fb->fb, npix, fb->d_image, ctx->stream);
-      RLC_CK(cudaMemcpyAsync(image_out, fb->d_image, 24 * size_t(npix), cudaMemcpyDeviceToHost,
-                             ctx->stream));
+      rlc::launch_resolve(fb->fb, uint32_t(npix), fb->d_image, st);
+      RLC_CK(cudaMemcpyAsync(image_out, fb->d_image, 24 * npix, cudaMemcpyDeviceToHost, st));
     }
     std::vector<uint32_t> h(config->passes);
-    RLC_CK(cudaMemcpyAsync(h.data(), d_hist, 4 * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
-    finish_sync(ctx, grid.get());
+    RLC_CK(cudaMemcpyAsync(h.data(), d_hist, 4 * h.size(), cudaMemcpyDeviceToHost, st));
+    unsigned long long c[rlc::kCntNum] = {};
+    if (grid)
+      RLC_CK(cudaMemcpyAsync(c, grid->dev.counters, sizeof(c), cudaMemcpyDeviceToHost, st));
+    finish_sync(ctx, grid);
     if (result) {
       result->num_passes = config->passes;
       if (result->sc_changes) std::memcpy(result->sc_changes, h.data(), 4 * h.size());
-      if (grid) {
-        rlc_grid_stats s;
-        rlc_grid_stats_get(grid.get(), &s);
-        result->occupied_cells = s.occupied;
-        result->lookups = s.lookups;
-        result->fallback_hits = s.fallback_hits;
-      } else {
-        result->occupied_cells = 0;
-        result->lookups = 0;
-        result->fallback_hits = 0;
-      }
+      result->occupied_cells = uint32_t(c[rlc::kCntCells]);
+      result->lookups = c[rlc::kCntLookups];
+      result->fallback_hits = c[rlc::kCntFallback];
       result->wall_ms = std::chrono::duration<double, std::milli>(
                             std::chrono::steady_clock::now() - t0).count();
     }
