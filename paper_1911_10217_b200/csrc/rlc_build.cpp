@@ -296,7 +296,7 @@ void build_wide(HostScene& out) {
   const std::vector<BvhNode>& nodes = use_ref ? out.nodes : sah;
   if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
   std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
-  std::vector<std::array<uint32_t, 4>> kids;
+  std::vector<std::array<uint32_t, kWide>> kids;
   std::vector<uint32_t> todo{0};
   std::vector<uint32_t> order;
   while (!todo.empty()) {
@@ -305,7 +305,7 @@ void build_wide(HostScene& out) {
     wid[b] = uint32_t(order.size());
     order.push_back(b);
     std::vector<uint32_t> L{nodes[b].a, nodes[b].b};
-    while (L.size() < 4) {
+    while (L.size() < size_t(kWide)) {
       int best = -1;
       for (size_t k = 0; k < L.size(); ++k)
         if (nodes[L[k]].count == 0 && (best < 0 || surface(nodes[L[k]]) > surface(nodes[L[size_t(best)]])))
@@ -315,7 +315,8 @@ void build_wide(HostScene& out) {
       L[size_t(best)] = nodes[x].a;
       L.insert(L.begin() + best + 1, nodes[x].b);
     }
-    std::array<uint32_t, 4> k4{kWideEmpty, kWideEmpty, kWideEmpty, kWideEmpty};
+    std::array<uint32_t, kWide> k4;
+    k4.fill(kWideEmpty);
     for (size_t k = 0; k < L.size(); ++k) k4[k] = L[k];
     kids.push_back(k4);
     for (size_t k = L.size(); k-- > 0;)
@@ -325,7 +326,7 @@ void build_wide(HostScene& out) {
   for (size_t w = 0; w < order.size(); ++w) {
     Wide4& n = out.wide[w];
     std::memset(&n, 0, sizeof(n));
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < kWide; ++c) {
       const uint32_t b = kids[w][c];
       if (b == kWideEmpty) {
         n.child[c] = kWideEmpty;

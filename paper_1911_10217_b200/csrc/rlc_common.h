@@ -100,12 +100,17 @@ struct alignas(32) BvhNodeF {
 // fp64 test ("Exact any-hit on a conservative wide BVH").
 constexpr uint32_t kWideLeaf = 0x80000000u;  // child: leaf flag
 constexpr uint32_t kWideEmpty = 0xffffffffu; // child: unused slot
+#ifndef RLC_WIDE
+#define RLC_WIDE 4
+#endif
+constexpr int kWide = RLC_WIDE;  // children per node (4 or 8)
 struct alignas(128) Wide4 {
-  float lo[3][4];      // [axis][child]
-  float hi[3][4];
-  uint32_t child[4];   // internal: Wide4 index; leaf: kWideLeaf | (count - 1) << 28 | first tri
-  uint32_t pad[4];
+  float lo[3][kWide];  // [axis][child]
+  float hi[3][kWide];
+  uint32_t child[kWide];  // internal: node index; leaf: kWideLeaf | (count - 1) << 28 | first tri
+  uint32_t pad[kWide == 8 ? 8 : 4];
 };
+static_assert(sizeof(Wide4) % 128 == 0, "wide nodes are whole 128-byte lines");
 
 // Triangle as the Moller-Trumbore test consumes it (bvh.cpp:44-62): p0 and
 // the two edges, precomputed with the reference's own subtraction.  Stored

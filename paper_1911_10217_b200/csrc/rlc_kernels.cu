@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
 // child-pair record and runs both children's slab tests.
 // ---------------------------------------------------------------------------
 constexpr int kShadowThreads = 128;
-constexpr int kShadowStack = 32;  // 4-wide levels: the 64-deep binary limit / 2
+constexpr int kShadowStack = kWide == 8 ? 64 : 32;  // per-lane stack entries (shared memory)
 constexpr uint32_t kDone = 0x7fffffffu;  // traversal finished (no leaf flag)
 
 // Leaf entries: kWideLeaf | kLeafVerified? | (count - 1) << 28 | first tri.
@@ -764,35 +764,38 @@ struct RayF {
 // Also returns in *inner the children whose fp32 inner test passes (the
 // interval narrowed by the rounding bound and the box rounding |c||inv|2^-22),
 // i.e. the children whose exact fp64 test certainly passes (see box_decide).
-__device__ __forceinline__ uint32_t box4_f(const float4 lo[3], const float4 hi[3], const RayF& r,
-                                           float near_out[4], uint32_t* inner) {
+__device__ __forceinline__ uint32_t boxw_f(const float (&lo)[3][kWide],
+                                           const float (&hi)[3][kWide], const RayF& r,
+                                           float (&near_out)[kWide], uint32_t* inner) {
   constexpr float K = 0x1.0p-20f;
-  float nr[4] = {r.tmin, r.tmin, r.tmin, r.tmin};
-  float fr[4] = {r.tmax, r.tmax, r.tmax, r.tmax};
-  float ni[4] = {r.tmin_in, r.tmin_in, r.tmin_in, r.tmin_in};
-  float fi[4] = {r.tmax_in, r.tmax_in, r.tmax_in, r.tmax_in};
+  float nr[kWide], fr[kWide], ni[kWide], fi[kWide];
+#pragma unroll
+  for (int c = 0; c < kWide; ++c) {
+    nr[c] = r.tmin;
+    fr[c] = r.tmax;
+    ni[c] = r.tmin_in;
+    fi[c] = r.tmax_in;
+  }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const bool neg = (r.neg >> a) & 1u;
-    const float4 n4 = neg ? hi[a] : lo[a];
-    const float4 f4 = neg ? lo[a] : hi[a];
-    const float nc[4] = {n4.x, n4.y, n4.z, n4.w};
-    const float fc[4] = {f4.x, f4.y, f4.z, f4.w};
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float tn = fmaf(nc[c], r.inv[a], r.b[a]);
-      const float tf = fmaf(fc[c], r.inv[a], r.b[a]);
+    for (int c = 0; c < kWide; ++c) {
+      const float nc = neg ? hi[a][c] : lo[a][c];
+      const float fc = neg ? lo[a][c] : hi[a][c];
+      const float tn = fmaf(nc, r.inv[a], r.b[a]);
+      const float tf = fmaf(fc, r.inv[a], r.b[a]);
       const float en = fmaf(fabsf(tn), K, r.mt[a]);
       const float ef = fmaf(fabsf(tf), K, r.mt[a]);
       nr[c] = fmaxf(nr[c], tn - en);
       fr[c] = fminf(fr[c], tf + ef);
-      ni[c] = fmaxf(ni[c], tn + en + fmaf(fabsf(nc[c]), r.mb[a], 1e-37f));
-      fi[c] = fminf(fi[c], tf - ef - fmaf(fabsf(fc[c]), r.mb[a], 1e-37f));
+      ni[c] = fmaxf(ni[c], tn + en + fmaf(fabsf(nc), r.mb[a], 1e-37f));
+      fi[c] = fminf(fi[c], tf - ef - fmaf(fabsf(fc), r.mb[a], 1e-37f));
     }
   }
   uint32_t m = 0, mi = 0;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < kWide; ++c) {
     m |= (nr[c] <= fr[c]) ? (1u << c) : 0u;
     mi |= (ni[c] <= fi[c]) ? (1u << c) : 0u;
     near_out[c] = nr[c];
@@ -914,34 +917,54 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
     // register; the first leaf met is postponed and traversal continues
     // while some lane of the warp has not found a leaf yet
     while (cur != kDone && !(cur & kWideLeaf)) {
+      constexpr int Q = kWide / 4;  // float4 per [axis] row
       const float4* p = reinterpret_cast<const float4*>(sc.wide + cur);
-      const float4 lo[3] = {__ldg(p), __ldg(p + 1), __ldg(p + 2)};
-      const float4 hi[3] = {__ldg(p + 3), __ldg(p + 4), __ldg(p + 5)};
-      const uint4 ch = __ldg(reinterpret_cast<const uint4*>(p + 6));
-      float tn[4];
+      float lo[3][kWide], hi[3][kWide];
+      uint32_t c[kWide];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const float4 vl = __ldg(p + a * Q + q), vh = __ldg(p + (3 + a) * Q + q);
+          lo[a][4 * q] = vl.x, lo[a][4 * q + 1] = vl.y, lo[a][4 * q + 2] = vl.z, lo[a][4 * q + 3] = vl.w;
+          hi[a][4 * q] = vh.x, hi[a][4 * q + 1] = vh.y, hi[a][4 * q + 2] = vh.z, hi[a][4 * q + 3] = vh.w;
+        }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + 6 * Q + q));
+        c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+      }
+      float tn[kWide];
       uint32_t mi;
-      uint32_t m = box4_f(lo, hi, rf, tn, &mi);
-      if (ch.z == kWideEmpty) m &= ~4u;
-      if (ch.w == kWideEmpty) m &= ~8u;
-      if (sp + 3 > kShadowStack) {
+      uint32_t m = boxw_f(lo, hi, rf, tn, &mi);
+#pragma unroll
+      for (int k = 0; k < kWide; ++k) {
+        if (c[k] == kWideEmpty) m &= ~(1u << k);
+        if ((mi >> k) & (c[k] >> 31)) c[k] |= kLeafVerified;  // leaf proven reached
+        if (!(m & (1u << k))) tn[k] = HUGE_VALF;
+      }
+      if (sp + kWide - 1 > kShadowStack) {
         atomicOr(err, kErrStackOverflow);
         m = 0;
         sp = 0;
       }
       // nearest entry first: occluders near the shading point end the ray early
-      uint32_t c[4] = {ch.x, ch.y, ch.z, ch.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k)  // leaf children the inner test proved reached
-        if ((mi >> k) & (c[k] >> 31)) c[k] |= kLeafVerified;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (!(m & (1u << k))) tn[k] = HUGE_VALF;
 #define RLC_CSWAP(i, j)                                   \
   if (tn[j] < tn[i]) {                                    \
     const float tt = tn[i]; tn[i] = tn[j]; tn[j] = tt;    \
     const uint32_t cc = c[i]; c[i] = c[j]; c[j] = cc;     \
   }
-      RLC_CSWAP(0, 1) RLC_CSWAP(2, 3) RLC_CSWAP(0, 2) RLC_CSWAP(1, 3) RLC_CSWAP(1, 2)
+      if constexpr (kWide == 4) {
+        RLC_CSWAP(0, 1) RLC_CSWAP(2, 3) RLC_CSWAP(0, 2) RLC_CSWAP(1, 3) RLC_CSWAP(1, 2)
+      } else {  // Batcher's 8-input network, 19 comparators
+        RLC_CSWAP(0, 1) RLC_CSWAP(2, 3) RLC_CSWAP(4, 5) RLC_CSWAP(6, 7)
+        RLC_CSWAP(0, 2) RLC_CSWAP(1, 3) RLC_CSWAP(4, 6) RLC_CSWAP(5, 7)
+        RLC_CSWAP(1, 2) RLC_CSWAP(5, 6) RLC_CSWAP(0, 4) RLC_CSWAP(3, 7)
+        RLC_CSWAP(1, 5) RLC_CSWAP(2, 6)
+        RLC_CSWAP(1, 4) RLC_CSWAP(3, 6)
+        RLC_CSWAP(2, 4) RLC_CSWAP(3, 5)
+        RLC_CSWAP(3, 4)
+      }
 #undef RLC_CSWAP
       const int hits = __popc(m);
       if (hits == 0) {
@@ -949,7 +972,7 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
       } else {
         cur = c[0];
 #pragma unroll
-        for (int k = 3; k >= 1; --k)
+        for (int k = kWide - 1; k >= 1; --k)
           if (k < hits) stack[(sp++) * kShadowThreads] = c[k];
       }
       if (leaf == 0 && cur != kDone && (cur & kWideLeaf)) {
