@@ -278,17 +278,10 @@ std::vector<BvhNode> sah_over_leaves(const std::vector<BvhNode>& ref) {
 // the reference tree itself (RLC_SHADOW_TREE=reference).
 void build_wide(HostScene& out) {
   out.wide.clear();
-  out.bparent.assign(out.nodes.size(), -1);
   out.tri_leaf.assign(out.tris.size(), 0);
-  for (size_t i = 0; i < out.nodes.size(); ++i) {
-    if (out.nodes[i].count == 0) {
-      out.bparent[out.nodes[i].a] = int32_t(i);
-      out.bparent[out.nodes[i].b] = int32_t(i);
-    } else {
-      for (uint32_t t = out.nodes[i].a; t < out.nodes[i].a + out.nodes[i].count; ++t)
-        out.tri_leaf[t] = uint32_t(i);
-    }
-  }
+  for (size_t i = 0; i < out.nodes.size(); ++i)
+    for (uint32_t t = out.nodes[i].a; out.nodes[i].count > 0 && t < out.nodes[i].a + out.nodes[i].count; ++t)
+      out.tri_leaf[t] = uint32_t(i);
   if (out.nodes.empty() || out.nodes[0].count > 0) return;
   const char* mode = std::getenv("RLC_SHADOW_TREE");
   const bool use_ref = mode != nullptr && std::string(mode) == "reference";

@@ -29,7 +29,6 @@ struct HostScene {
   std::vector<BvhNodeF> nodes_cam; // same, boxes relative to the camera origin (fl64(c - O))
   std::vector<TriAccel> tris;  // BVH leaf order
   std::vector<Wide4> wide;       // 4-wide conservative tree, DFS order (empty: root is a leaf)
-  std::vector<int32_t> bparent;  // binary BVH parent per node (-1 at the root)
   std::vector<uint32_t> tri_leaf; // binary leaf node per leaf-order triangle
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;

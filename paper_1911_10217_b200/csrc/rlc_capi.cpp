@@ -444,7 +444,6 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     d.nodes_f = A.upload(h.nodes_f);
     d.nodes_cam = A.upload(h.nodes_cam);
     d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
-    d.bparent = A.upload(h.bparent);
     d.tri_leaf = A.upload(h.tri_leaf);
     d.tris = A.upload(h.tris);
     d.mats = A.upload(h.mats);
@@ -475,8 +474,13 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
       RLC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       RLC_CK(cudaEventRecord(e, ctx->stream));
     }
-    // render_frame's grid, framebuffer and pass buffers for this config
-    prepare_frame_cache(ctx.get(), config);
+    // render_frame's grid, framebuffer and pass buffers for this config;
+    // best effort: build_context does not validate the hash/cut config
+    // (render.cpp:143-157), render_frame reports it
+    try {
+      prepare_frame_cache(ctx.get(), config);
+    } catch (const std::invalid_argument&) {
+    }
     RLC_CK(cudaStreamSynchronize(ctx->stream));
     *out = ctx.release();
   });

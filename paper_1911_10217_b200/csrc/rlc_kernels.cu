@@ -20,6 +20,7 @@
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "rlc_kernels.h"
 
@@ -129,14 +130,6 @@ __device__ __noinline__ bool occluded_ray(const DevScene& sc, V3 a, V3 dir, V3 i
   return false;
 }
 
-__device__ bool occluded(const DevScene& sc, V3 a, V3 b, uint32_t* err) {
-  const V3 d = b - a;
-  const double len = length(d);
-  if (len <= 2 * sc.shadow_eps) return false;
-  const V3 dir = d / len;
-  const V3 inv{1.0 / dir.x, 1.0 / dir.y, 1.0 / dir.z};
-  return occluded_ray(sc, a, dir, inv, sc.shadow_eps, len - sc.shadow_eps, err);
-}
 
 // fp32 decision test of one binary node against the reference's fp64 slab
 // test (bvh.cpp:29-40), both sides bounded:
@@ -1179,15 +1172,40 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
   const size_t at = size_t(k);
   double q = g.q[at];
   uint32_t vis = g.visits[at];
-  for (uint32_t j = i; j < P.n && keys[j] == k; ++j) {
-    const uint32_t idx = vals[j];
-    const double v = *reinterpret_cast<const double*>(vbase + size_t(idx) * vstride);
-    if (!(v >= 0 && isfinite(v)))  // update_q's argument check, cut.cpp:78-80
-      atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrBadValue);
-    q_before[idx] = q;
-    const double a = P.harmonic ? 1.0 / (1.0 + double(vis)) : P.alpha;
-    q = smax((1.0 - a) * q + a * v, g.eps_q);
-    ++vis;
+  // The update chain is sequential (bit-exact order); the record loads are
+  // not, so they are issued kBatch at a time ahead of the arithmetic.
+  constexpr int kBatch = 8;
+  uint32_t j = i;
+  while (true) {
+    uint32_t ids[kBatch];
+    int cnt = 0;
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const uint32_t jj = j + b;
+      const bool in = cnt == b && jj < P.n && keys[jj] == k;
+      if (in) {
+        ids[b] = vals[jj];
+        ++cnt;
+      }
+    }
+    if (cnt == 0) break;
+    double vb[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b)
+      if (b < cnt) vb[b] = *reinterpret_cast<const double*>(vbase + size_t(ids[b]) * vstride);
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      if (b >= cnt) break;
+      const double v = vb[b];
+      if (!(v >= 0 && isfinite(v)))  // update_q's argument check, cut.cpp:78-80
+        atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrBadValue);
+      q_before[ids[b]] = q;
+      const double a = P.harmonic ? 1.0 / (1.0 + double(vis)) : P.alpha;
+      q = smax((1.0 - a) * q + a * v, g.eps_q);
+      ++vis;
+    }
+    j += uint32_t(cnt);
+    if (cnt < kBatch) break;
   }
   g.q[at] = q;
   g.visits[at] = vis;

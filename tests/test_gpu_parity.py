@@ -90,15 +90,21 @@ def test_baseline_samplers_bit_exact(ref, sampler):
 
 
 def test_render_frame_matches_reference(ref):
+    """render_frame reuses the context's grid/framebuffer cache: repeated
+    calls, and calls with another config, must each equal a fresh reference
+    render_frame (render.cpp:202-240)."""
     scene = scenes.cornell_grid(2, 1, dome_triangles=32, width=32, height=32)
     cfg = rlcuts.RenderConfig(spp=4, passes=2, sampler=RL)
+    cfg2 = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL, seed=4,
+                               cut=rlcuts.CutConfig(cut_size=16))
     ctx = rlcuts.build_context(scene, cfg)
-    res = rlcuts.render_frame(ctx, cfg)
-    rres = ref.ref_render_frame(scene, cfg)
-    assert np.array_equal(res.image, rres["image"])
-    assert res.sc_changes == rres["sc_changes"]
-    assert (res.occupied_cells, res.lookups, res.fallback_hits) == (
-        rres["occupied"], rres["lookups"], rres["fallback_hits"])
+    for c in (cfg, cfg, cfg2, cfg):
+        res = rlcuts.render_frame(ctx, c)
+        rres = ref.ref_render_frame(scene, c)
+        assert np.array_equal(res.image, rres["image"])
+        assert res.sc_changes == rres["sc_changes"]
+        assert (res.occupied_cells, res.lookups, res.fallback_hits) == (
+            rres["occupied"], rres["lookups"], rres["fallback_hits"])
 
 
 def test_errors_match_reference_exceptions(ref):
