@@ -225,12 +225,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_1911_10217_b200 import rlcuts
 
     dist = None
+    # one process per GPU; with fewer GPUs than ranks (--dist-backend gloo
+    # functional runs only) ranks share devices round-robin
+    local_rank = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    else:
-        torch.cuda.set_device(local_rank)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
 
     scene, cfg = make_config(args.config)
     t0 = time.perf_counter()
@@ -254,7 +258,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ctx.set_stream(stream.cuda_stream)
         frame = rdist.ShardedFrame(rdist.GpuEngine(ctx, grid, fb, cfg,
                                                    torch.device("cuda", local_rank)),
-                                   H, rank, world)
+                                   H, rank, world, host_staging=args.dist_backend == "gloo")
         r0, r1 = frame.rows
 
         def step(p):
@@ -289,7 +293,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     stages = ctx.stage_times()
     ctx.enable_timing(False)
     if dist is not None:
-        t = torch.tensor([ms, float(lookups)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, float(lookups)], dtype=torch.float64,
+                         device="cuda" if args.dist_backend == "nccl" else "cpu")
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = t.clone()
@@ -363,7 +368,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "frames_timed": args.steps,
                        "l2": "no flush: resident scene+cut+pass buffers exceed the 126 MB L2",
                        "parallelism": (f"screen bands x{world}, exact update-record all-gather "
-                                       "over NCCL" if world > 1 else "single GPU"),
+                                       f"over {args.dist_backend}" if world > 1 else "single GPU"),
                        "cells": st["occupied"], "fallback_hits": st["fallback_hits"]},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
@@ -386,6 +391,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-downscale", type=int, default=4)
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo stages the record exchange through host memory (functional "
+                         "multi-rank runs with fewer GPUs than ranks)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 warm-up steps
     rank = env_int("RANK", 0)

@@ -86,13 +86,16 @@ class OracleEngine:
 class ShardedFrame:
     """One rank's share of a sharded frame."""
 
-    def __init__(self, engine, height: int, rank: int, world: int, group=None):
+    def __init__(self, engine, height: int, rank: int, world: int, group=None,
+                 host_staging: bool = False):
         self.engine, self.rank, self.world, self.group = engine, rank, world, group
         self.rows = band(height, rank, world)
         self.last_counts = [0] * world
+        # gloo cannot all-gather device tensors: stage through host memory
+        self.host_staging = host_staging
 
     def exchange(self, n: int) -> tuple[torch.Tensor, list, int]:
-        dev = self.engine.device
+        dev = torch.device("cpu") if self.host_staging else self.engine.device
         cnt = torch.tensor([n], dtype=torch.int64, device=dev)
         counts_t = [torch.zeros_like(cnt) for _ in range(self.world)]
         dist.all_gather(counts_t, cnt, group=self.group)
@@ -100,10 +103,10 @@ class ShardedFrame:
         stride = max(max(counts), 1)
         send = torch.zeros(stride * RECORD_BYTES, dtype=torch.uint8, device=dev)
         if n:
-            send[: n * RECORD_BYTES] = self.engine.records()
+            send[: n * RECORD_BYTES] = self.engine.records().to(dev)
         parts = [torch.empty_like(send) for _ in range(self.world)]
         dist.all_gather(parts, send, group=self.group)
-        return torch.cat(parts), counts, stride
+        return torch.cat(parts).to(self.engine.device), counts, stride
 
     def step(self, pass_index: int) -> int:
         """render_pass + end_of_pass_update for this rank's band; returns the
