@@ -159,7 +159,8 @@ rlc_status rlc_context_synchronize(rlc_context* ctx);
 
 /* Per-stage device timing with CUDA events on the context stream (bench
  * evidence).  Stages: 0 primary, 1 sample, 2 sort, 3 fold, 4 accumulate,
- * 5 split-collapse, 6 shadow (any-hit traversal).  rlc_context_stage_times synchronizes,
+ * 5 split-collapse, 6 shadow (any-hit traversal).  Stage 0 includes the
+ * bounce rays of max_depth > 1.  rlc_context_stage_times synchronizes,
  * returns accumulated milliseconds and launch counts per stage since the
  * last call, and resets them. */
 #define RLC_NUM_STAGES 7
@@ -176,6 +177,20 @@ rlc_status rlc_occluded_batch(const rlc_context* ctx, uint32_t n, const double* 
 rlc_status rlc_intersect_batch(const rlc_context* ctx, uint32_t n, const double* origins,
                                const double* dirs, double t_min, double* t_out,
                                int32_t* tri_out);
+
+/* ---- bounce sampler trigonometry ---------------------------------------
+ * sample_cosine_hemisphere (proj/include/rlcuts/math.hpp:101-107) calls
+ * std::cos / std::sin, which glibc does not round correctly; the device
+ * restates the host libm's build exactly (paper_1911_10217_b200/csrc/
+ * rlc_libm.h).  rlc_libm_variant: 1 = glibc FMA build, 0 = SSE2 build,
+ * -1 = unrecognised (max_depth > 1 then fails with RLC_ERR_INTERNAL).
+ * rlc_libm_sincos runs the device restatement on host arrays (parity tests);
+ * rlc_libm_sincos_host runs the same code on the host (no device needed). */
+rlc_status rlc_libm_variant(int32_t* variant);
+rlc_status rlc_libm_sincos(const rlc_context* ctx, uint32_t n, const double* x, double* s,
+                           double* c);
+rlc_status rlc_libm_sincos_host(int32_t variant, uint64_t n, const double* x, double* s,
+                                double* c);
 
 /* ---- hash grid: HashGrid(hash, init_cut(tree, M, eps))
  *      (proj/src/render.cpp:211-216, proj/src/hash_grid.cpp:102-111,

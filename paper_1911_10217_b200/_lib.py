@@ -89,6 +89,9 @@ SIGNATURES = {
     "rlc_context_enable_timing": (C.c_int, [_P, C.c_int]),
     "rlc_context_stage_times": (C.c_int, [_P, _dp, _u32p]),
     "rlc_occluded_batch": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.POINTER(C.c_uint8)]),
+    "rlc_libm_variant": (C.c_int, [C.POINTER(C.c_int32)]),
+    "rlc_libm_sincos": (C.c_int, [_P, C.c_uint32, _dp, _dp, _dp]),
+    "rlc_libm_sincos_host": (C.c_int, [C.c_int32, C.c_uint64, _dp, _dp, _dp]),
     "rlc_intersect_batch": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp,
                                       C.POINTER(C.c_int32)]),
     "rlc_grid_create": (C.c_int, [_P, C.POINTER(RenderConfigC), _PP]),

@@ -15,6 +15,8 @@
 
 #include "rlc_build.h"
 #include "rlc_kernels.h"
+#include "rlc_libm.h"
+#include "rlc_sincostab.h"
 #include "rlcuts_b200.h"
 
 namespace {
@@ -104,6 +106,40 @@ void check_device(int device) {
   RLC_CK(cudaSetDevice(device));
 }
 
+const double kSinCosTabHost[440] = RLC_SINCOSTAB_INIT;
+
+// The x86-64 glibc build of sin/cos the host libm dispatches to (rlc_libm.h):
+// the host restatement of each build is compared with std::sin / std::cos on
+// angles that separate the two builds and on 4096 sampler angles 2 pi u.
+// kUnknown if neither matches everywhere (then bounce directions cannot be
+// reproduced and max_depth > 1 is refused).
+int probe_libm_variant() {
+  static const int variant = [] {
+    std::vector<double> xs = {0x1.47750e7b60563p+0, 0x1.de8813a4f28cap+0, 0x1.2ce0bf964b8acp+1,
+                              0x1.68e5b478ea497p+0};
+    uint64_t st = 0x243f6a8885a308d3ull;
+    for (int i = 0; i < 4096; ++i) {
+      st = rlc::mix64(st + 0x9e3779b97f4a7c15ull);
+      xs.push_back(2.0 * rlc::kPi * (double(st >> 11) * 0x1.0p-53));
+    }
+    for (const int cand : {rlc::libm::kFma, rlc::libm::kSse2}) {
+      const rlc::libm::Ctx c{kSinCosTabHost, cand == rlc::libm::kFma};
+      bool ok = true;
+      for (const double x : xs) {
+        volatile double vx = x;  // a runtime libm call, never a compile-time fold
+        const double hs = std::sin(vx), hc = std::cos(vx);
+        if (hs != rlc::libm::sin(c, x) || hc != rlc::libm::cos(c, x)) {
+          ok = false;
+          break;
+        }
+      }
+      if (ok) return cand;
+    }
+    return int(rlc::libm::kUnknown);
+  }();
+  return variant;
+}
+
 const char* device_error_message(uint32_t bits) {
   if (bits & rlc::kErrNonUnitNormal) return "make_key: normal must be unit length";
   if (bits & rlc::kErrBadValue) return "update_q: value must be finite and non-negative";
@@ -119,6 +155,7 @@ struct PassParamsHolder {
   rlc::PassParams p{};
   rlc::DevGrid g{};
   uint32_t n = 0;
+  uint32_t nv = 0;
   const rlc_grid* grid = nullptr;
   bool valid = false;
 };
@@ -285,7 +322,8 @@ void throw_device_error(uint32_t bits) {
 struct PassSetup {
   rlc::PassParams p{};
   rlc::DevGrid g{};
-  uint32_t n = 0;
+  uint32_t n = 0;   // paths
+  uint32_t nv = 0;  // path vertices n * max_depth
 };
 
 PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pass_index,
@@ -295,8 +333,10 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
   require(!(cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && grid == nullptr),
           "render_pass: learned sampler needs a hash grid");
   require(cfg->sampler <= RLC_SAMPLER_RL_LIGHTCUTS, "render_pass: unknown sampler");
-  require(cfg->max_depth == 1,
-          "render_pass: the device path implements max_depth == 1 (direct lighting)");
+  if (cfg->max_depth > 1 && probe_libm_variant() == rlc::libm::kUnknown)
+    throw std::runtime_error(
+        "render_pass: max_depth > 1 needs the host libm's sin/cos, which this build does not "
+        "reproduce (rlc_libm.h)");
   require(!need_fb || (fb != nullptr && fb->width == ctx->host.cam.width &&
                        fb->height == ctx->host.cam.height),
           "render_pass: framebuffer size must match the camera");
@@ -305,13 +345,16 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
   PassSetup S;
   const uint32_t spp_pp = cfg->spp / cfg->passes;
   const uint64_t n64 = uint64_t(r1 - r0) * uint64_t(ctx->host.cam.width) * spp_pp;
-  require(n64 < (1ull << 31), "render_pass: too many paths for one launch");
+  require(n64 * cfg->max_depth < (1ull << 31), "render_pass: too many path vertices for one launch");
   S.n = uint32_t(n64);
+  S.nv = uint32_t(n64 * cfg->max_depth);
   S.p.width = uint32_t(ctx->host.cam.width);
   S.p.row_begin = r0;
   S.p.spp_pp = spp_pp;
   S.p.pass_index = pass_index;
   S.p.n = S.n;
+  S.p.depth = cfg->max_depth;
+  S.p.nv = S.nv;
   S.p.sampler = cfg->sampler;
   S.p.seed_mixed = rlc::mix64(cfg->seed);
   S.p.zero_mixed = rlc::mix64(0);
@@ -319,7 +362,7 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
   S.p.harmonic = grid ? grid->harmonic : 0u;
   if (grid) S.g = grid->dev;
   else S.g.counters = ctx->counters;
-  if (S.n > 0) ctx->ensure_scratch(S.n);
+  if (S.nv > 0) ctx->ensure_scratch(S.nv);
   return S;
 }
 
@@ -344,6 +387,11 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   } else {
     ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, st); });
   }
+  // Multi-bounce paths (max_depth > 1): one launch per further vertex; the
+  // vertices of all depths then share the sample / sort / shadow / fold
+  // launches below, in canonical (path, depth) order.
+  for (uint32_t d = 2; d <= S.p.depth; ++d)
+    ctx->stage(0, [&] { rlc::launch_bounce(ctx->dev, S.g, S.p, d, ctx->pb, st); });
   ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, S.g, S.p, ctx->pb, st); });
   // Shadow rays are traced in sorted (cell, cluster) order: rays of one cell
   // toward one cut cluster share most of their BVH path.  The any-hit result
@@ -351,9 +399,9 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   *k = nullptr;
   *v = nullptr;
   if (S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS)
-    ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, S.n, grid->key_bits, st, k, v); });
+    ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, S.nv, grid->key_bits, st, k, v); });
   ctx->stage(6, [&] {
-    rlc::launch_ray_compact(ctx->pb, *v, S.n, st);
+    rlc::launch_ray_compact(ctx->pb, *v, S.nv, st);
     rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, S.g.counters, st);
   });
 }
@@ -364,10 +412,10 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   rlc_context* ctx = const_cast<rlc_context*>(cctx);
   const PassSetup S = setup_pass(ctx, cfg, pass_index, grid, fb, true, r0, r1);
   if (S.n == 0) return;
-  uint32_t *k, *v;
-  enqueue_trace(ctx, S, grid, &k, &v);
+  uint32_t *k = nullptr, *v = nullptr;
+  if (S.nv > 0) enqueue_trace(ctx, S, grid, &k, &v);  // max_depth 0: empty paths
   cudaStream_t st = ctx->stream;
-  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS)
+  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && S.nv > 0)
     ctx->stage(3, [&] { rlc::launch_fold(S.g, S.p, k, v, ctx->pb, st); });
   ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
   RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));  // last G-buffer reader
@@ -460,6 +508,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     for (int a = 0; a < 3; ++a)
       if (!(std::fabs(h.scene_lo[a]) <= 1e8 && std::fabs(h.scene_hi[a]) <= 1e8)) d.fp32_ok = 0;
     d.shadow_eps = h.shadow_eps;
+    d.libm_fma = probe_libm_variant() == rlc::libm::kFma ? 1u : 0u;
     d.base_tile = h.base_tile;
     for (int k = 0; k <= 16; ++k) d.level_thr[k] = h.level_threshold[k];
     d.cam = h.cam;
@@ -552,6 +601,47 @@ rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* count
       if (ms) ms[i] = acc[i];
       if (counts) counts[i] = cnt[i];
     }
+  });
+}
+
+rlc_status rlc_libm_variant(int32_t* variant) {
+  return guarded([&] {
+    require(variant != nullptr, "rlc_libm_variant: null argument");
+    *variant = probe_libm_variant();
+  });
+}
+
+rlc_status rlc_libm_sincos_host(int32_t variant, uint64_t n, const double* x, double* s,
+                                double* c) {
+  return guarded([&] {
+    require(variant == rlc::libm::kFma || variant == rlc::libm::kSse2,
+            "rlc_libm_sincos_host: unknown variant");
+    require(n == 0 || (x && s && c), "rlc_libm_sincos_host: null argument");
+    const rlc::libm::Ctx lc{kSinCosTabHost, variant == rlc::libm::kFma};
+    for (uint64_t i = 0; i < n; ++i) {
+      s[i] = rlc::libm::sin(lc, x[i]);
+      c[i] = rlc::libm::cos(lc, x[i]);
+    }
+  });
+}
+
+rlc_status rlc_libm_sincos(const rlc_context* cctx, uint32_t n, const double* x, double* s,
+                           double* c) {
+  return guarded([&] {
+    require(cctx != nullptr && (n == 0 || (x && s && c)), "rlc_libm_sincos: null argument");
+    if (n == 0) return;
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    RLC_CK(cudaSetDevice(ctx->device));
+    DeviceArena tmp;
+    double* dx = tmp.alloc<double>(n);
+    double* ds = tmp.alloc<double>(n);
+    double* dc = tmp.alloc<double>(n);
+    RLC_CK(cudaMemcpyAsync(dx, x, 8 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    rlc::launch_libm_sincos(ctx->dev, n, dx, ds, dc, ctx->stream);
+    RLC_CK(cudaGetLastError());
+    RLC_CK(cudaMemcpyAsync(s, ds, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    RLC_CK(cudaMemcpyAsync(c, dc, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -817,13 +907,13 @@ rlc_status rlc_pass_trace(const rlc_context* cctx, const rlc_render_config* conf
     RLC_CK(cudaSetDevice(ctx->device));
     const PassSetup S = setup_pass(ctx, config, pass_index, grid, nullptr, false, row_begin,
                                    row_end);
-    ctx->shard = PassParamsHolder{S.p, S.g, S.n, grid, true};
+    ctx->shard = PassParamsHolder{S.p, S.g, S.n, S.nv, grid, true};
     *records = ctx->rec_out;
     *count = 0;
-    if (S.n == 0) return;
+    if (S.nv == 0) return;
     uint32_t *k, *v;
     enqueue_trace(ctx, S, grid, &k, &v);
-    rlc::launch_export_records(S.g, ctx->pb, S.n, ctx->rec_out, ctx->stream);
+    rlc::launch_export_records(S.g, ctx->pb, S.nv, ctx->rec_out, ctx->stream);
     unsigned int c = 0;
     RLC_CK(cudaMemcpyAsync(&c, ctx->pb.rec_count, 4, cudaMemcpyDeviceToHost, ctx->stream));
     finish_sync(ctx, grid);
@@ -861,7 +951,7 @@ rlc_status rlc_pass_fold(const rlc_context* cctx, const rlc_render_config* confi
       rlc::launch_fold_records(S.g, S.p, ctx->pb,
                                static_cast<const rlc::UpdateRecord*>(all_records), ctx->d_counts,
                                nranks, stride, uint32_t(total), own_offset, grid->key_bits, ctx->xb,
-                               S.n, st);
+                               S.nv, st);
     });
     if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
     RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));

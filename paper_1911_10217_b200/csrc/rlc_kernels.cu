@@ -23,6 +23,8 @@
 #include <string>
 
 #include "rlc_kernels.h"
+#include "rlc_libm.h"
+#include "rlc_sincostab.h"
 
 namespace rlc {
 
@@ -459,6 +461,84 @@ __device__ __forceinline__ bool path_of_thread(const PassParams& P, uint32_t row
   return t < P.n;
 }
 
+// First RNG dimension of the draws at path vertex `depth` (1-based):
+// RandomSequence::next() order of PassRenderer::trace (render.cpp:63-133):
+// jx, jy, then per vertex u1 u2 u3 [ju1 ju2 learned] b1 b2.
+__device__ __forceinline__ uint32_t draw_base(const PassParams& P, uint32_t depth) {
+  return kDrawU1 + (depth - 1u) * (P.sampler == 2u ? 7u : 5u);
+}
+
+// Shading of a closest hit at vertex `depth` (render.cpp:74-99, up to the
+// cell lookup): G-buffer entry plus the cell key of a learned vertex.
+__device__ __forceinline__ void shade_vertex(const DevScene& sc, const DevGrid& g,
+                                             const PassParams& P, uint32_t depth, V3 org, V3 dir,
+                                             double t, uint32_t tri, double pdf_omega, GBuf& out,
+                                             bool& need, Key& key, uint64_t& h, uint32_t* err) {
+  const V3 pos = org + dir * t;
+  const V3 ng = ld3(sc.tri_normal + size_t(3) * tri);
+  const V3 wo = -dir;
+  const double cos_facing = dot(ng, wo);
+  const uint32_t mat = sc.tri_mat[tri];
+  const MatRec& m = sc.mats[mat];
+  uint32_t flags = kGHit | mat;
+  if (depth == 1 && m.is_emitter && cos_facing > 0) flags |= kGEmit;
+  const V3 ns = dot(ng, wo) < 0 ? -ng : ng;  // faceforward, math.hpp:59-61
+  out.pos[0] = pos.x;
+  out.pos[1] = pos.y;
+  out.pos[2] = pos.z;
+  out.ns[0] = ns.x;
+  out.ns[1] = ns.y;
+  out.ns[2] = ns.z;
+  if (m.reflective) {
+    flags |= kGReflective;
+    if (P.sampler == 2u) {
+      const double cos_in = fabs(cos_facing);
+      const double area_pdf =
+          smax(pdf_omega * cos_in / smax(t * t, 1e-24), 1e-12);  // render.cpp:86-88
+      if (!(area_pdf > 0)) atomicOr(err, kErrBadAreaPdf);
+      // level_for_footprint (hash_grid.cpp:34-44) via host-derived thresholds
+      const double r = 1.0 / sqrt(area_pdf) / sc.base_tile;
+      uint32_t level = 0;
+#pragma unroll
+      for (int k = 1; k <= 16; ++k) level += (r >= sc.level_thr[k]) ? 1u : 0u;
+      if (fabs(length(ns) - 1.0) > 1e-4) atomicOr(err, kErrNonUnitNormal);
+      const uint32_t base = draw_base(P, depth);
+      const double ju1 = rng_draw(out.rng, base + 3u);
+      const double ju2 = rng_draw(out.rng, base + 4u);
+      key = make_key(pos, ns, level, ju1, ju2, sc.base_tile, g.normal_bits, g.jitter_scale);
+      h = hash_key(key);
+      need = true;
+    }
+  }
+  out.flags = flags;
+}
+
+// Warp-cooperative lookup_or_insert: one probe per distinct hash in the
+// warp (all 32 lanes must call).
+__device__ __forceinline__ void warp_lookup(const DevGrid& g, bool need, const Key& key,
+                                            uint64_t h, uint32_t lane, uint32_t* slot_out) {
+  const unsigned need_mask = __ballot_sync(kFull, need);
+  if (!need) return;
+  const unsigned peers = __match_any_sync(need_mask, h) & need_mask;
+  const int leader = __ffs(peers) - 1;
+  uint32_t slot = 0;
+  if (int(lane) == leader) slot = probe_insert(g, key, h);
+  slot = __shfl_sync(peers, slot, leader);
+  const int lqx = __shfl_sync(peers, key.qx, leader);
+  const int lqy = __shfl_sync(peers, key.qy, leader);
+  const int lqz = __shfl_sync(peers, key.qz, leader);
+  const uint32_t lqn = __shfl_sync(peers, key.qn, leader);
+  const uint32_t llv = __shfl_sync(peers, key.level, leader);
+  if (lqx != key.qx || lqy != key.qy || lqz != key.qz || lqn != key.qn || llv != key.level)
+    slot = probe_insert(g, key, h);  // 64-bit hash collision inside the warp
+  *slot_out = slot;
+  const unsigned fb = __ballot_sync(need_mask, slot == kFallback);
+  if (int(lane) == __ffs(need_mask) - 1) {
+    atomicAdd(g.counters + kCntLookups, (unsigned long long)__popc(need_mask));
+    if (fb) atomicAdd(g.counters + kCntFallback, (unsigned long long)__popc(fb));
+  }
+}
+
 __global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassParams P,
                                                  GBuf* __restrict__ gbuf) {
   const uint32_t rows = P.n / (P.width * P.spp_pp);
@@ -495,71 +575,73 @@ __global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassPar
   uint32_t tri = 0;
   const bool got = active && (sc.fp32_ok ? intersect_camera(sc, org, dir, &t, &tri, err)
                                          : intersect(sc, org, dir, 0.0, &t, &tri, err));
-  if (active) {
-    const CameraConst& c = sc.cam;
-    if (got) {
-      const V3 pos = org + dir * t;
-      const V3 ng = ld3(sc.tri_normal + size_t(3) * tri);
-      const V3 wo = -dir;
-      const double cos_facing = dot(ng, wo);
-      const uint32_t mat = sc.tri_mat[tri];
-      const MatRec& m = sc.mats[mat];
-      uint32_t flags = kGHit | mat;
-      if (m.is_emitter && cos_facing > 0) flags |= kGEmit;
-      const V3 ns = dot(ng, wo) < 0 ? -ng : ng;  // faceforward, math.hpp:59-61
-      out.pos[0] = pos.x;
-      out.pos[1] = pos.y;
-      out.pos[2] = pos.z;
-      out.ns[0] = ns.x;
-      out.ns[1] = ns.y;
-      out.ns[2] = ns.z;
-      if (m.reflective) {
-        flags |= kGReflective;
-        if (P.sampler == 2u) {
-          const double cos_in = fabs(cos_facing);
-          const double area_pdf =
-              smax(c.pdf_omega * cos_in / smax(t * t, 1e-24), 1e-12);  // render.cpp:86-88
-          if (!(area_pdf > 0)) atomicOr(err, kErrBadAreaPdf);
-          // level_for_footprint (hash_grid.cpp:34-44) via host-derived thresholds
-          const double r = 1.0 / sqrt(area_pdf) / sc.base_tile;
-          uint32_t level = 0;
-#pragma unroll
-          for (int k = 1; k <= 16; ++k) level += (r >= sc.level_thr[k]) ? 1u : 0u;
-          if (fabs(length(ns) - 1.0) > 1e-4) atomicOr(err, kErrNonUnitNormal);
-          const double ju1 = rng_draw(rk, kDrawJu1);
-          const double ju2 = rng_draw(rk, kDrawJu2);
-          key = make_key(pos, ns, level, ju1, ju2, sc.base_tile, g.normal_bits, g.jitter_scale);
-          h = hash_key(key);
-          need = true;
-        }
-      }
-      out.flags = flags;
-    }
-  }
+  if (got) shade_vertex(sc, g, P, 1u, org, dir, t, tri, sc.cam.pdf_omega, out, need, key, h, err);
+  warp_lookup(g, need, key, h, lane, &out.slot);
+  if (active) gbuf[size_t(idx) * P.depth] = out;
+}
 
-  // Warp-cooperative lookup: one probe per distinct hash in the warp.
-  const unsigned need_mask = __ballot_sync(kFull, need);
-  if (need) {
-    const unsigned peers = __match_any_sync(need_mask, h) & need_mask;
-    const int leader = __ffs(peers) - 1;
-    uint32_t slot = 0;
-    if (int(lane) == leader) slot = probe_insert(g, key, h);
-    slot = __shfl_sync(peers, slot, leader);
-    const int lqx = __shfl_sync(peers, key.qx, leader);
-    const int lqy = __shfl_sync(peers, key.qy, leader);
-    const int lqz = __shfl_sync(peers, key.qz, leader);
-    const uint32_t lqn = __shfl_sync(peers, key.qn, leader);
-    const uint32_t llv = __shfl_sync(peers, key.level, leader);
-    if (lqx != key.qx || lqy != key.qy || lqz != key.qz || lqn != key.qn || llv != key.level)
-      slot = probe_insert(g, key, h);  // 64-bit hash collision inside the warp
-    out.slot = slot;
-    const unsigned fb = __ballot_sync(need_mask, slot == kFallback);
-    if (int(lane) == __ffs(need_mask) - 1) {
-      atomicAdd(g.counters + kCntLookups, (unsigned long long)__popc(need_mask));
-      if (fb) atomicAdd(g.counters + kCntFallback, (unsigned long long)__popc(fb));
+// ---------------------------------------------------------------------------
+// k_bounce: the continuation of PassRenderer::trace from vertex depth-1 to
+// vertex depth (render.cpp:127-135, then 71-99 for the new hit):
+// sample_cosine_hemisphere (math.hpp:101-107) with the host libm's exact
+// sin/cos (rlc_libm.h), the closest hit from t_min = shadow_eps in the
+// reference traversal order, and the cell lookup of the new vertex.
+// ---------------------------------------------------------------------------
+__device__ const double kSinCosTab[440] = RLC_SINCOSTAB_INIT;
+
+__device__ __forceinline__ V3 cosine_hemisphere(const DevScene& sc, V3 n, double u1, double u2) {
+  const libm::Ctx lc{kSinCosTab, sc.libm_fma != 0};
+  const double r = sqrt(u1);
+  const double phi = 2.0 * kPi * u2;
+  const V3 local{r * libm::cos(lc, phi), r * libm::sin(lc, phi), sqrt(smax(0.0, 1.0 - u1))};
+  // Frame (math.hpp:85-99): Duff et al. branchless basis
+  const double sign = copysign(1.0, n.z);
+  const double a = -1.0 / (sign + n.z);
+  const double bb = n.x * n.y * a;
+  const V3 t{1.0 + sign * n.x * n.x * a, sign * bb, -sign * n.x};
+  const V3 b{bb, sign + n.y * n.y * a, -n.y};
+  return t * local.x + b * local.y + n * local.z;
+}
+
+__global__ void __launch_bounds__(128) k_bounce(DevScene sc, DevGrid g, PassParams P,
+                                                uint32_t depth, GBuf* __restrict__ gbuf) {
+  const uint32_t path = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = path < P.n;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
+  bool need = false;
+  Key key{};
+  uint64_t h = 0;
+  GBuf out;
+  out.slot = kNoSlot;
+  out.flags = 0;
+  out.rng = 0;
+  bool go = false;
+  V3 org{0, 0, 0}, dir{0, 0, 1};
+  double pdf_omega = 0;
+  if (active) {
+    const GBuf prev = gbuf[size_t(path) * P.depth + depth - 2u];
+    out.rng = prev.rng;
+    if (prev.flags & kGReflective) {  // render.cpp:127: non-reflective vertices end the path
+      const uint32_t base = draw_base(P, depth - 1u) + (P.sampler == 2u ? 5u : 3u);
+      const double b1 = rng_draw(prev.rng, base);
+      const double b2 = rng_draw(prev.rng, base + 1u);
+      const V3 ns = ld3(prev.ns);
+      dir = cosine_hemisphere(sc, ns, b1, b2);
+      const double cos_theta = dot(ns, dir);
+      if (!(cos_theta <= 0)) {
+        go = true;
+        pdf_omega = cos_theta / kPi;
+        org = ld3(prev.pos);
+      }
     }
   }
-  if (active) gbuf[idx] = out;
+  double t = 0;
+  uint32_t tri = 0;
+  const bool got = go && intersect(sc, org, dir, sc.shadow_eps, &t, &tri, err);
+  if (got) shade_vertex(sc, g, P, depth, org, dir, t, tri, pdf_omega, out, need, key, h, err);
+  warp_lookup(g, need, key, h, lane, &out.slot);
+  if (active) gbuf[size_t(path) * P.depth + depth - 1u] = out;
 }
 
 // ---------------------------------------------------------------------------
@@ -573,8 +655,8 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
                                                 double* __restrict__ q_before,
                                                 ShadowRay* __restrict__ rays,
                                                 unsigned int* __restrict__ ray_count) {
-  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= P.n) return;
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // path vertex
+  if (idx >= P.nv) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
   const GBuf gb = gbuf[idx];
   keys[idx] = kInvalidKey;
@@ -583,9 +665,10 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
     srec[idx].flags = 0;  // read by the ray compaction
     return;
   }
-  const double u1 = rng_draw(gb.rng, kDrawU1);
-  const double u2 = rng_draw(gb.rng, kDrawU2);
-  const double u3 = rng_draw(gb.rng, kDrawU3);
+  const uint32_t base = draw_base(P, idx % P.depth + 1u);
+  const double u1 = rng_draw(gb.rng, base);
+  const double u2 = rng_draw(gb.rng, base + 1u);
+  const double u3 = rng_draw(gb.rng, base + 2u);
 
   SampleRec r;
   r.flags = 0;
@@ -1231,11 +1314,18 @@ __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
   V3 sum = ld3(fb.sum + 3 * fi);
   unsigned long long cnt = fb.count[fi];
   for (uint32_t s = 0; s < P.spp_pp; ++s) {
-    const uint32_t idx = pix * P.spp_pp + s;
-    const uint32_t flags = gbuf[idx].flags;
+    // radiance of PassRenderer::trace (render.cpp:64-137): emission of the
+    // primary hit, then throughput-weighted NEE of every reflective vertex
     V3 L{0.0, 0.0, 0.0};
-    if (flags & kGEmit) L = L + ld3(sc.mats[flags & kGMatMask].emission);
-    if (flags & kGReflective) {
+    V3 T{1.0, 1.0, 1.0};
+    const size_t v0 = size_t(pix * P.spp_pp + s) * P.depth;
+    for (uint32_t d = 0; d < P.depth; ++d) {
+      const size_t idx = v0 + d;
+      const uint32_t flags = gbuf[idx].flags;
+      if (!(flags & kGHit)) break;
+      const MatRec& m = sc.mats[flags & kGMatMask];
+      if (flags & kGEmit) L = L + ld3(m.emission);
+      if (!(flags & kGReflective)) break;
       const SampleRec& r = srec[idx];
       V3 rad{0.0, 0.0, 0.0};
       if (r.flags & kSNonzero) {
@@ -1249,7 +1339,8 @@ __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
         const double den = pdf_sel * r.pdf_area;
         rad = V3{r.c[0], r.c[1], r.c[2]} / den;
       }
-      L = L + V3{1.0, 1.0, 1.0} * rad;
+      L = L + T * rad;
+      T = T * ld3(m.albedo);  // used only if vertex d + 1 exists (render.cpp:133)
     }
     sum = sum + L;
     cnt += 1;
@@ -1594,6 +1685,7 @@ void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const 
         uint32_t(sizeof(UpdateRecord)), x.q_rec);
     count_launch();
   }
+  if (local_n == 0) return;
   k_scatter_qbefore<<<blocks_for(local_n, 256), 256, 0, st>>>(x.q_rec, own_offset, b.rec_path,
                                                               b.rec_count, local_n, b.q_before);
   count_launch();
@@ -1622,11 +1714,18 @@ void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
   count_launch();
 }
 
-void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
+void launch_bounce(const DevScene& sc, const DevGrid& g, const PassParams& p, uint32_t depth,
                    const PassBuffers& b, cudaStream_t st) {
   if (p.n == 0) return;
+  k_bounce<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, depth, b.gbuf);
+  count_launch();
+}
+
+void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
+                   const PassBuffers& b, cudaStream_t st) {
+  if (p.nv == 0) return;
   cudaMemsetAsync(b.ray_count, 0, 2 * sizeof(unsigned int), st);
-  k_sample<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.keys, b.vals,
+  k_sample<<<blocks_for(p.nv, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.keys, b.vals,
                                                   b.q_before, b.rays, b.ray_count);
   count_launch();
 }
@@ -1756,9 +1855,11 @@ void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
 
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
                  const uint32_t* vals, const PassBuffers& b, cudaStream_t st) {
-  if (p.n == 0) return;
-  k_fold<<<blocks_for(p.n, 256), 256, 0, st>>>(
-      g, p, keys, vals, reinterpret_cast<const char*>(b.srec) + offsetof(SampleRec, v),
+  if (p.nv == 0) return;
+  PassParams q = p;
+  q.n = p.nv;  // k_fold runs over the update records of all path vertices
+  k_fold<<<blocks_for(q.n, 256), 256, 0, st>>>(
+      g, q, keys, vals, reinterpret_cast<const char*>(b.srec) + offsetof(SampleRec, v),
       uint32_t(sizeof(SampleRec)), b.q_before);
   count_launch();
 }
@@ -1784,6 +1885,22 @@ void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshol
     configured = true;
   }
   k_split<<<148 * 4, wpb * 32, smem, st>>>(sc, g, threshold, iterations, changes_out);
+  count_launch();
+}
+
+__global__ void k_libm_sincos(DevScene sc, uint32_t n, const double* __restrict__ x,
+                              double* __restrict__ s, double* __restrict__ c) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const libm::Ctx lc{kSinCosTab, sc.libm_fma != 0};
+  s[i] = libm::sin(lc, x[i]);
+  c[i] = libm::cos(lc, x[i]);
+}
+
+void launch_libm_sincos(const DevScene& sc, uint32_t n, const double* x, double* s, double* c,
+                        cudaStream_t st) {
+  if (n == 0) return;
+  k_libm_sincos<<<blocks_for(n, 256), 256, 0, st>>>(sc, n, x, s, c);
   count_launch();
 }
 

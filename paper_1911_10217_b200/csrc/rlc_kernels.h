@@ -37,7 +37,7 @@ enum : uint32_t {
 enum : uint32_t { kCntCells = 0, kCntLookups = 1, kCntFallback = 2, kCntChanges = 3,
                   kCntErr = 4, kCntNum = 8 };
 
-struct alignas(16) GBuf {  // 64 B per path
+struct alignas(16) GBuf {  // 64 B per path vertex
   double pos[3];
   double ns[3];
   uint64_t rng;
@@ -90,6 +90,7 @@ struct DevScene {
   uint32_t num_lights;
   uint32_t num_tris;
   uint32_t fp32_ok;  // scene coordinates within 1e8: the fp32 shadow pre-test is valid
+  uint32_t libm_fma; // host libm build whose sin/cos the bounce sampler restates (rlc_libm.h)
   double shadow_eps;
   double base_tile;
   double level_thr[17];
@@ -128,6 +129,8 @@ struct PassParams {
   uint32_t spp_pp;
   uint32_t pass_index;
   uint32_t n;           // paths in this launch: rows * width * spp_pp
+  uint32_t depth;       // max_depth D: path vertices per path
+  uint32_t nv;          // vertices n * D; vertex (path, d) is path * D + d - 1
   uint32_t sampler;
   uint64_t seed_mixed;  // mix64(seed)
   uint64_t zero_mixed;  // mix64(0): the c component of the RNG key
@@ -177,6 +180,10 @@ uint64_t launches();
 
 void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
                     const PassBuffers& b, cudaStream_t st);
+// Bounce to vertex `depth` (2..D) of every path: cosine-hemisphere
+// direction, closest hit, cell lookup (render.cpp:127-135 then 71-99).
+void launch_bounce(const DevScene& sc, const DevGrid& g, const PassParams& p, uint32_t depth,
+                   const PassBuffers& b, cudaStream_t st);
 void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
                    const PassBuffers& b, cudaStream_t st);
 // Sorts (keys, vals) by key; returns which buffer pair holds the result.
@@ -210,5 +217,8 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
                             double tmin, double* t_out, int32_t* tri_out,
                             unsigned long long* counters, cudaStream_t st);
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
+// Device sin/cos of the bounce sampler (rlc_libm.h) for the parity tests.
+void launch_libm_sincos(const DevScene& sc, uint32_t n, const double* x, double* s, double* c,
+                        cudaStream_t st);
 
 }  // namespace rlc

@@ -137,6 +137,13 @@ class RenderContext:
         _check(_lib.load().rlc_context_stage_times(self.handle, _dptr(ms), _uptr(cnt)))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.STAGES)}
 
+    def libm_sincos(self, x: np.ndarray):
+        """The bounce sampler's sin/cos on the device (rlc_libm.h)."""
+        x = np.ascontiguousarray(x, np.float64).ravel()
+        s, c = np.empty_like(x), np.empty_like(x)
+        _check(_lib.load().rlc_libm_sincos(self.handle, x.size, _dptr(x), _dptr(s), _dptr(c)))
+        return s, c
+
     def occluded(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
         """occluded() (bvh.hpp:38-40) for n segments (n x 3 endpoints)."""
         a = np.ascontiguousarray(a, np.float64).reshape(-1, 3)
@@ -362,6 +369,21 @@ def render_frame(ctx: RenderContext, config: RenderConfig) -> RenderResult:
     _check(_lib.load().rlc_render_frame(ctx.handle, C.byref(cfg), _dptr(img), C.byref(res)))
     return RenderResult(img, res.wall_ms, res.occupied_cells, res.lookups, res.fallback_hits,
                         list(changes)[:config.passes])
+
+
+def libm_variant() -> int:
+    """Host libm build the bounce sampler restates: 1 glibc FMA, 0 SSE2, -1 unknown."""
+    v = C.c_int32()
+    _check(_lib.load().rlc_libm_variant(C.byref(v)))
+    return v.value
+
+
+def libm_sincos_host(x: np.ndarray, variant: int):
+    """Host run of the restated libm sin/cos (no device needed)."""
+    x = np.ascontiguousarray(x, np.float64).ravel()
+    s, c = np.empty_like(x), np.empty_like(x)
+    _check(_lib.load().rlc_libm_sincos_host(variant, x.size, _dptr(x), _dptr(s), _dptr(c)))
+    return s, c
 
 
 def kernel_launches() -> int:

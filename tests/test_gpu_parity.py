@@ -89,6 +89,36 @@ def test_baseline_samplers_bit_exact(ref, sampler):
     assert_same_state(grid, fb, rr)
 
 
+@pytest.mark.parametrize("depth,sampler", [(2, RL), (3, RL), (5, RL),
+                                           (2, rlcuts.SamplerKind.uniform),
+                                           (3, rlcuts.SamplerKind.energy)])
+def test_multi_bounce_bit_exact(ref, depth, sampler):
+    """max_depth > 1 (render.cpp:71-136): cosine-hemisphere bounces with the
+    host libm's sin/cos, closest hits from t_min = shadow_eps, NEE and
+    update_q records at every vertex, throughput-weighted radiance."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=40, height=32)
+    cfg = rlcuts.RenderConfig(spp=4, passes=2, max_depth=depth, sampler=sampler)
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+
+
+def test_multi_bounce_c1_analog_learns(ref):
+    scene, st = scenes.config_scene("c1")
+    scene = scene.with_resolution(48, 48)
+    cfg = rlcuts.RenderConfig(spp=4, passes=4, max_depth=3, sampler=RL,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+    assert grid.lookup_count() > 48 * 48 * 4 * 1.5  # the bounces reached learned vertices
+
+
+def test_zero_depth_adds_empty_samples(ref):
+    scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=16, height=16)
+    cfg = rlcuts.RenderConfig(spp=2, passes=2, max_depth=0, sampler=RL)
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+
+
 def test_render_frame_matches_reference(ref):
     """render_frame reuses the context's grid/framebuffer cache: repeated
     calls, and calls with another config, must each equal a fresh reference
@@ -97,8 +127,9 @@ def test_render_frame_matches_reference(ref):
     cfg = rlcuts.RenderConfig(spp=4, passes=2, sampler=RL)
     cfg2 = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL, seed=4,
                                cut=rlcuts.CutConfig(cut_size=16))
+    cfg3 = rlcuts.RenderConfig(spp=4, passes=2, sampler=RL, max_depth=3)
     ctx = rlcuts.build_context(scene, cfg)
-    for c in (cfg, cfg, cfg2, cfg):
+    for c in (cfg, cfg, cfg2, cfg3, cfg):
         res = rlcuts.render_frame(ctx, c)
         rres = ref.ref_render_frame(scene, c)
         assert np.array_equal(res.image, rres["image"])

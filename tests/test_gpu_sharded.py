@@ -13,10 +13,10 @@ pytestmark = pytest.mark.gpu
 RL = rlcuts.SamplerKind.rl_lightcuts
 
 
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_sharded_gpu_matches_single(ref, world):
+@pytest.mark.parametrize("world,depth", [(1, 1), (2, 1), (3, 1), (2, 3)])
+def test_sharded_gpu_matches_single(ref, world, depth):
     scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
-    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL, max_depth=depth,
                               cut=rlcuts.CutConfig(cut_size=64, split_threshold=2.0))
     dev = torch.device("cuda", 0)
     engines = []
