@@ -538,7 +538,7 @@ static Key make_key(V p, V n, uint32_t level, double j1, double j2, double base,
 }
 
 // ---- one oracle run ------------------------------------------------------
-struct Sample {  // one light sample of the pass (max_depth = 1)
+struct Sample {  // one light sample of the pass (one per reflective path vertex)
   uint64_t canon;    // (py*W + px)*spp_pp + s
   uint32_t pixel;
   uint32_t slot;     // UINT32_MAX: fallback
@@ -547,6 +547,7 @@ struct Sample {  // one light sample of the pass (max_depth = 1)
   uint32_t size;
   double total, pdf_area, v, q_before;
   V contrib, radiance;
+  V thr;             // path throughput at the vertex (render.cpp:110, 133)
   bool nonzero;
 };
 
@@ -606,7 +607,7 @@ struct Run {
   // Current band of the pass being traced: rows [r0, r1).
   std::vector<Sample> cur;
   std::vector<V> emitted;
-  std::vector<int64_t> sample_of;
+  std::vector<size_t> first_of;  // samples of path canon: [first_of[canon], first_of[canon + 1])
   uint32_t band_r0 = 0, band_spp = 1;
 
   // render_pass (render.cpp:159-183) = trace + fold_local.
@@ -615,12 +616,12 @@ struct Run {
     fold_local();
   }
 
-  // PassRenderer::trace up to the light sample and its NEE (render.cpp:59-
-  // 117 without update_q) for every path of rows [r0, r1), canonical order.
+  // PassRenderer::trace (render.cpp:59-137) without update_q for every path
+  // of rows [r0, r1), canonical order: light samples of all path vertices in
+  // (path, depth) order, each with the path throughput it is weighted by.
   void trace(uint32_t pass_index, uint32_t r0, uint32_t r1) {
     if (cfg.passes == 0 || cfg.spp % cfg.passes != 0)
       throw std::invalid_argument("render_pass: spp must be divisible by passes");
-    if (cfg.max_depth != 1) throw std::invalid_argument("oracle: max_depth must be 1");
     const uint32_t spp_pp = cfg.spp / cfg.passes;
     const bool rl = cfg.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
     const V w = unit(s.org - s.look), u = unit(cross(s.up, w)), vv = cross(w, u);
@@ -633,86 +634,113 @@ struct Run {
     band_r0 = r0;
     band_spp = spp_pp;
     emitted.assign(size_t(s.w) * (r1 - r0) * spp_pp, V{});
-    sample_of.assign(emitted.size(), -1);
+    first_of.assign(emitted.size() + 1, 0);
     for (uint32_t py = r0; py < r1; ++py)
       for (uint32_t px = 0; px < uint32_t(s.w); ++px)
         for (uint32_t k = 0; k < spp_pp; ++k) {
           const uint64_t canon = (uint64_t(py - r0) * s.w + px) * spp_pp + k;
+          first_of[canon] = samples.size();
           Rng rng(cfg.seed, uint64_t(py) * s.w + px, uint64_t(pass_index) * spp_pp + k, 0);
           const double jx = rng.next(), jy = rng.next();
           const double sx = (2.0 * (double(px) + jx) / s.w - 1.0) * tan_half * aspect;
           const double sy = (1.0 - 2.0 * (double(py) + jy) / s.h) * tan_half;
-          const V dir = unit(u * sx + vv * sy - w);
-          double t;
-          uint32_t tri;
-          if (!closest(s, bvh, s.org, dir, 0.0, &t, &tri, &prim)) continue;
-          const V pos = s.org + dir * t;
-          const Tri& T = s.tris[tri];
-          const V ng = unit(cross(T.p1 - T.p0, T.p2 - T.p0));
-          const V wo = -dir;
-          const double cf = dot(ng, wo);
-          const Mat& m = s.mats[T.mat];
-          if (lum(m.emission) > 0 && cf > 0) emitted[canon] = V{} + m.emission;
-          const V ns = dot(ng, wo) < 0 ? -ng : ng;
-          if (!(lum(m.albedo) > 0)) continue;
-          const double area_pdf = std::max(pdf_omega * std::abs(cf) / std::max(t * t, 1e-24), 1e-12);
-          const double u1 = rng.next(), u2 = rng.next(), u3 = rng.next();
-          Sample sm{};
-          sm.canon = canon;
-          sm.pixel = py * s.w + px;
-          uint32_t e = 0;
-          double pdf_sel_base = 0;
-          if (rl) {
-            const double j1 = rng.next(), j2 = rng.next();
-            const Key key = make_key(pos, ns, level_of(area_pdf, base), j1, j2, base,
-                                     cfg.hash.normal_bits, cfg.hash.jitter_scale);
-            sm.slot = lookup(key);
-            const Cut& c = cut_of(sm.slot);  // cdf and ends are frozen for the pass
-            const uint32_t sidx = pick_cluster(c, u1);
-            const uint32_t b = sidx == 0 ? 0 : c.ends[sidx - 1];
-            sm.size = c.ends[sidx] - b;
-            const double lo = sidx == 0 ? 0.0 : c.cdf[sidx - 1];
-            const double span = c.cdf[sidx] - lo;
-            const double frac = span > 0 ? std::clamp((u1 * c.cdf.back() - lo) / span, 0.0, 1.0) : 0.0;
-            e = tree.order[b + std::min(sm.size - 1, uint32_t(frac * double(sm.size)))];
-            sm.cluster = sidx;
-            sm.total = c.cdf.back();
-          } else if (cfg.sampler == RLC_SAMPLER_UNIFORM) {
-            e = std::min(n_em - 1, uint32_t(u1 * double(n_em)));
-            pdf_sel_base = 1.0 / double(n_em);
-          } else {
-            const double target = u1 * energy_cdf.back();
-            const auto it = std::upper_bound(energy_cdf.begin(), energy_cdf.end(), target);
-            e = it == energy_cdf.end() ? n_em - 1 : uint32_t(it - energy_cdf.begin());
-            pdf_sel_base = em_energy[e] / energy_cdf.back();
-          }
-          sm.emitter = e;
-          // sample_triangle_point, scene.cpp:49-59
-          const Tri& L = s.tris[em_tri[e]];
-          const double area = 0.5 * len(cross(L.p1 - L.p0, L.p2 - L.p0));
-          if (area <= 0) throw std::invalid_argument("sample_triangle_point: degenerate triangle");
-          const double su = std::sqrt(u2), b0 = 1.0 - su, b1 = u3 * su;
-          const V pt = L.p0 * b0 + L.p1 * b1 + L.p2 * (1.0 - b0 - b1);
-          sm.pdf_area = 1.0 / area;
-          const double pin = rl ? 1.0 / double(sm.size) : 1.0;
-          // nee_estimate, estimators.cpp:82-106 (radiance deferred)
-          V tl = pt - pos;
-          const double d2 = dot(tl, tl);
-          if (!(d2 < 1e-24)) {
-            tl = tl / std::sqrt(d2);
-            const double cx = dot(ns, tl);
-            const double cy = dot(unit(cross(L.p1 - L.p0, L.p2 - L.p0)), -tl);
-            if (!(cx <= 0) && !(cy <= 0) && !blocked(s, bvh, pos, pt, &shadow)) {
-              sm.contrib = m.albedo * (1.0 / 3.14159265358979323846) * s.mats[L.mat].emission *
-                           (cx * cy / d2);
-              sm.nonzero = true;
-              sm.v = lum(sm.contrib) / (pin * sm.pdf_area);
+          V org = s.org, dir = unit(u * sx + vv * sy - w);
+          double tmin = 0.0, pdf_om = pdf_omega;
+          V thr{1, 1, 1};
+          for (uint32_t depth = 1; depth <= cfg.max_depth; ++depth) {
+            double t;
+            uint32_t tri;
+            if (!closest(s, bvh, org, dir, tmin, &t, &tri, depth == 1 ? &prim : nullptr)) break;
+            const V pos = org + dir * t;
+            const Tri& T = s.tris[tri];
+            const V ng = unit(cross(T.p1 - T.p0, T.p2 - T.p0));
+            const V wo = -dir;
+            const double cf = dot(ng, wo);
+            const Mat& m = s.mats[T.mat];
+            if (depth == 1 && lum(m.emission) > 0 && cf > 0) emitted[canon] = V{} + m.emission;
+            const V ns = dot(ng, wo) < 0 ? -ng : ng;
+            if (!(lum(m.albedo) > 0)) break;
+            const double area_pdf =
+                std::max(pdf_om * std::abs(cf) / std::max(t * t, 1e-24), 1e-12);
+            const double u1 = rng.next(), u2 = rng.next(), u3 = rng.next();
+            Sample sm{};
+            sm.canon = canon;
+            sm.pixel = py * s.w + px;
+            sm.thr = thr;
+            uint32_t e = 0;
+            double pdf_sel_base = 0;
+            if (rl) {
+              const double j1 = rng.next(), j2 = rng.next();
+              const Key key = make_key(pos, ns, level_of(area_pdf, base), j1, j2, base,
+                                       cfg.hash.normal_bits, cfg.hash.jitter_scale);
+              sm.slot = lookup(key);
+              const Cut& c = cut_of(sm.slot);  // cdf and ends are frozen for the pass
+              const uint32_t sidx = pick_cluster(c, u1);
+              const uint32_t b = sidx == 0 ? 0 : c.ends[sidx - 1];
+              sm.size = c.ends[sidx] - b;
+              const double lo = sidx == 0 ? 0.0 : c.cdf[sidx - 1];
+              const double span = c.cdf[sidx] - lo;
+              const double frac =
+                  span > 0 ? std::clamp((u1 * c.cdf.back() - lo) / span, 0.0, 1.0) : 0.0;
+              e = tree.order[b + std::min(sm.size - 1, uint32_t(frac * double(sm.size)))];
+              sm.cluster = sidx;
+              sm.total = c.cdf.back();
+            } else if (cfg.sampler == RLC_SAMPLER_UNIFORM) {
+              e = std::min(n_em - 1, uint32_t(u1 * double(n_em)));
+              pdf_sel_base = 1.0 / double(n_em);
+            } else {
+              const double target = u1 * energy_cdf.back();
+              const auto it = std::upper_bound(energy_cdf.begin(), energy_cdf.end(), target);
+              e = it == energy_cdf.end() ? n_em - 1 : uint32_t(it - energy_cdf.begin());
+              pdf_sel_base = em_energy[e] / energy_cdf.back();
             }
+            sm.emitter = e;
+            // sample_triangle_point, scene.cpp:49-59
+            const Tri& L = s.tris[em_tri[e]];
+            const double area = 0.5 * len(cross(L.p1 - L.p0, L.p2 - L.p0));
+            if (area <= 0) throw std::invalid_argument("sample_triangle_point: degenerate triangle");
+            const double su = std::sqrt(u2), b0 = 1.0 - su, b1 = u3 * su;
+            const V pt = L.p0 * b0 + L.p1 * b1 + L.p2 * (1.0 - b0 - b1);
+            sm.pdf_area = 1.0 / area;
+            const double pin = rl ? 1.0 / double(sm.size) : 1.0;
+            // nee_estimate, estimators.cpp:82-106 (radiance deferred)
+            V tl = pt - pos;
+            const double d2 = dot(tl, tl);
+            if (!(d2 < 1e-24)) {
+              tl = tl / std::sqrt(d2);
+              const double cx = dot(ns, tl);
+              const double cy = dot(unit(cross(L.p1 - L.p0, L.p2 - L.p0)), -tl);
+              if (!(cx <= 0) && !(cy <= 0) && !blocked(s, bvh, pos, pt, &shadow)) {
+                sm.contrib = m.albedo * (1.0 / 3.14159265358979323846) * s.mats[L.mat].emission *
+                             (cx * cy / d2);
+                sm.nonzero = true;
+                sm.v = lum(sm.contrib) / (pin * sm.pdf_area);
+              }
+            }
+            if (!rl && sm.nonzero) sm.radiance = sm.contrib / (pdf_sel_base * sm.pdf_area);
+            samples.push_back(sm);
+            if (depth == cfg.max_depth) break;
+            // the bounce, render.cpp:128-135: sample_cosine_hemisphere
+            // (math.hpp:101-107) with the host libm's std::cos / std::sin
+            const double b1u = rng.next(), b2u = rng.next();
+            const double r = std::sqrt(b1u), phi = 2.0 * 3.14159265358979323846 * b2u;
+            const V local{r * std::cos(phi), r * std::sin(phi), std::sqrt(std::max(0.0, 1.0 - b1u))};
+            const double sign = std::copysign(1.0, ns.z);  // Frame, math.hpp:85-99
+            const double a = -1.0 / (sign + ns.z);
+            const double bb = ns.x * ns.y * a;
+            const V tx{1.0 + sign * ns.x * ns.x * a, sign * bb, -sign * ns.x};
+            const V by{bb, sign + ns.y * ns.y * a, -ns.y};
+            const V nd = tx * local.x + by * local.y + ns * local.z;
+            const double cos_theta = dot(ns, nd);
+            if (cos_theta <= 0) break;
+            thr = thr * m.albedo;
+            pdf_om = cos_theta / 3.14159265358979323846;
+            org = pos;
+            dir = nd;
+            tmin = bvh.eps;
           }
-          if (!rl && sm.nonzero) sm.radiance = sm.contrib / (pdf_sel_base * sm.pdf_area);
-          sample_of[canon] = int64_t(samples.size());
-          samples.push_back(sm);
         }
+    first_of[emitted.size()] = samples.size();
   }
 
   // The deferred fold of the band's own update records.
@@ -751,7 +779,8 @@ struct Run {
     std::vector<Sample>& samples = cur;
     for (size_t canon = 0; canon < emitted.size(); ++canon) {
       V L = emitted[canon];
-      if (sample_of[canon] >= 0) L = L + V{1, 1, 1} * samples[size_t(sample_of[canon])].radiance;
+      for (size_t i = first_of[canon]; i < first_of[canon + 1]; ++i)
+        L = L + samples[i].thr * samples[i].radiance;
       const size_t pix = size_t(band_r0) * s.w + canon / band_spp;
       sum[pix] = sum[pix] + L;
       count[pix] += 1;

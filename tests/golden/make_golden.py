@@ -112,6 +112,11 @@ def runs():
                                              alpha_schedule=rlcuts.AlphaSchedule.harmonic))),
         "energy": (scenes.cornell_grid(2, 1, dome_triangles=32, width=32, height=24),
                    rlcuts.RenderConfig(spp=2, passes=1, sampler=rlcuts.SamplerKind.energy)),
+        "bounce3": (scenes.cornell_grid(2, 1, dome_triangles=32, width=32, height=24),
+                    rlcuts.RenderConfig(spp=4, passes=2, sampler=RL, max_depth=3)),
+        "bounce2u": (scenes.cornell_grid(1, 2, dome_triangles=32, width=24, height=24),
+                     rlcuts.RenderConfig(spp=2, passes=1, max_depth=2,
+                                         sampler=rlcuts.SamplerKind.uniform)),
     }
     for name, (scene, cfg) in cases.items():
         r = RefRun(scene, cfg)
