@@ -19,9 +19,9 @@ from paper_1911_10217_b200 import rlcuts, scenes
 RL = rlcuts.SamplerKind.rl_lightcuts
 
 
-def _case():
+def _case(depth=1):
     scene = scenes.cornell_grid(2, 1, dome_triangles=32, width=36, height=27)
-    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL, max_depth=depth,
                               cut=rlcuts.CutConfig(cut_size=32, split_threshold=2.0))
     return scene, cfg
 
@@ -32,10 +32,10 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank: int, world: int, port: int, outdir: str):
+def _worker(rank: int, world: int, port: int, outdir: str, depth: int):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
-    scene, cfg = _case()
+    scene, cfg = _case(depth)
     run = OracleRun(scene, cfg)
     frame = rdist.ShardedFrame(rdist.OracleEngine(run), scene.camera.height, rank, world)
     changes = [frame.step(p) for p in range(cfg.passes)]
@@ -46,10 +46,10 @@ def _worker(rank: int, world: int, port: int, outdir: str):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_oracle_matches_single_process(tmp_path, world):
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    scene, cfg = _case()
+@pytest.mark.parametrize("world,depth", [(2, 1), (3, 1), (2, 3)])
+def test_sharded_oracle_matches_single_process(tmp_path, world, depth):
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), depth), nprocs=world, join=True)
+    scene, cfg = _case(depth)
     single = OracleRun(scene, cfg)
     ref_changes = [single.run_pass(p) for p in range(cfg.passes)]
     ref_sum, ref_count = single.framebuffer()
