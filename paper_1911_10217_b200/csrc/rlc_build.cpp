@@ -270,24 +270,14 @@ std::vector<BvhNode> sah_over_leaves(const std::vector<BvhNode>& ref) {
   return out;
 }
 
-// 4-wide tree for the any-hit shadow kernel, collapsed from a binary tree
-// over the reference leaves: every wide node stands for one binary internal
-// node and lists up to four of its descendants (children expanded
-// largest-surface-first); child boxes are rounded outward to fp32.  The
-// binary tree is a binned-SAH tree over the reference's leaves (default) or
-// the reference tree itself (RLC_SHADOW_TREE=reference).
-void build_wide(HostScene& out) {
-  out.wide.clear();
-  out.tri_leaf.assign(out.tris.size(), 0);
-  for (size_t i = 0; i < out.nodes.size(); ++i)
-    for (uint32_t t = out.nodes[i].a; out.nodes[i].count > 0 && t < out.nodes[i].a + out.nodes[i].count; ++t)
-      out.tri_leaf[t] = uint32_t(i);
-  if (out.nodes.empty() || out.nodes[0].count > 0) return;
-  const char* mode = std::getenv("RLC_SHADOW_TREE");
-  const bool use_ref = mode != nullptr && std::string(mode) == "reference";
-  const std::vector<BvhNode> sah = use_ref ? std::vector<BvhNode>() : sah_over_leaves(out.nodes);
-  const std::vector<BvhNode>& nodes = use_ref ? out.nodes : sah;
-  if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
+// Collapses a binary tree to 4-wide nodes: every wide node stands for one
+// binary internal node and lists up to four of its descendants (children
+// expanded largest-surface-first, in place, so the list keeps the binary
+// tree's left-to-right order); child boxes are rounded outward to fp32, taken
+// relative to `origin` when given (x = fl64(c - O)) and then enlarged by
+// |x| * grow before the outward rounding.
+std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double* origin,
+                                 double grow = 0.0) {
   std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
   std::vector<std::array<uint32_t, kWide>> kids;
   std::vector<uint32_t> todo{0};
@@ -315,9 +305,9 @@ void build_wide(HostScene& out) {
     for (size_t k = L.size(); k-- > 0;)
       if (nodes[L[k]].count == 0) todo.push_back(L[k]);
   }
-  out.wide.resize(order.size());
+  std::vector<Wide4> wide(order.size());
   for (size_t w = 0; w < order.size(); ++w) {
-    Wide4& n = out.wide[w];
+    Wide4& n = wide[w];
     std::memset(&n, 0, sizeof(n));
     for (int c = 0; c < kWide; ++c) {
       const uint32_t b = kids[w][c];
@@ -331,12 +321,38 @@ void build_wide(HostScene& out) {
       }
       const BvhNode& bn = nodes[b];
       for (int a = 0; a < 3; ++a) {
-        n.lo[a][c] = round_down(bn.lo[a]);
-        n.hi[a][c] = round_up(bn.hi[a]);
+        const double lo = origin ? bn.lo[a] - origin[a] : bn.lo[a];
+        const double hi = origin ? bn.hi[a] - origin[a] : bn.hi[a];
+        n.lo[a][c] = round_down(lo - std::fabs(lo) * grow);
+        n.hi[a][c] = round_up(hi + std::fabs(hi) * grow);
       }
       n.child[c] = bn.count > 0 ? (kWideLeaf | ((bn.count - 1) << 28) | bn.a) : wid[b];
     }
   }
+  return wide;
+}
+
+// The wide trees of the traversal kernels:
+//  * `wide`: any-hit shadow rays -- a binned-SAH tree over the reference
+//    BVH's leaves (default) or the reference tree itself
+//    (RLC_SHADOW_TREE=reference), collapsed;
+//  * `wide_ref`: closest-hit rays -- the reference tree collapsed with its
+//    children in left-to-right order, so the reference's leaf order (right
+//    subtree first) is a plain stack traversal; `wide_cam` (camera-relative
+//    boxes) is filled in with the camera constants.
+void build_wide(HostScene& out) {
+  out.wide.clear();
+  out.wide_ref.clear();
+  out.tri_leaf.assign(out.tris.size(), 0);
+  for (size_t i = 0; i < out.nodes.size(); ++i)
+    for (uint32_t t = out.nodes[i].a; out.nodes[i].count > 0 && t < out.nodes[i].a + out.nodes[i].count; ++t)
+      out.tri_leaf[t] = uint32_t(i);
+  if (out.nodes.empty() || out.nodes[0].count > 0) return;
+  if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
+  const char* mode = std::getenv("RLC_SHADOW_TREE");
+  const bool use_ref = mode != nullptr && std::string(mode) == "reference";
+  out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr);
+  out.wide_ref = collapse_wide(out.nodes, nullptr);
 }
 
 }  // namespace
@@ -604,6 +620,12 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
       out.nodes_cam[i].lo[a] = round_down(out.nodes[i].lo[a] - cam.origin[a]);
       out.nodes_cam[i].hi[a] = round_up(out.nodes[i].hi[a] - cam.origin[a]);
     }
+  // The wide copy for camera rays is enlarged by 2^-21 |x| per coordinate,
+  // more than the whole relative gap between fl32(x' * fl32(inv)) and the
+  // reference's fl64(x * inv) (< 2^-23): its plain slab test is conservative
+  // (DESIGN.md 5.4).
+  out.wide_cam.clear();
+  if (!out.wide_ref.empty()) out.wide_cam = collapse_wide(out.nodes, cam.origin, 0x1.0p-21);
 }
 
 }  // namespace rlc

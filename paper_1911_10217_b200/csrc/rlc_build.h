@@ -29,6 +29,8 @@ struct HostScene {
   std::vector<BvhNodeF> nodes_cam; // same, boxes relative to the camera origin (fl64(c - O))
   std::vector<TriAccel> tris;  // BVH leaf order
   std::vector<Wide4> wide;       // 4-wide conservative tree, DFS order (empty: root is a leaf)
+  std::vector<Wide4> wide_ref;   // the reference tree collapsed, children left to right
+  std::vector<Wide4> wide_cam;   // wide_ref with camera-relative boxes
   std::vector<uint32_t> tri_leaf; // binary leaf node per leaf-order triangle
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;

@@ -492,6 +492,8 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     d.nodes_f = A.upload(h.nodes_f);
     d.nodes_cam = A.upload(h.nodes_cam);
     d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
+    d.wide_ref = h.wide_ref.empty() ? nullptr : A.upload(h.wide_ref);
+    d.wide_cam = h.wide_cam.empty() ? nullptr : A.upload(h.wide_cam);
     d.tri_leaf = A.upload(h.tri_leaf);
     d.tris = A.upload(h.tris);
     d.mats = A.upload(h.mats);

@@ -191,6 +191,11 @@ __device__ __forceinline__ int box_decide(const float4& q0, const float4& q1, co
   return 2;
 }
 
+// Closest hit through the collapsed reference tree (defined with the wide
+// traversal helpers below); false in *used when the ray needs the binary path.
+__device__ bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool camera,
+                               bool* used, double* t_out, uint32_t* tri_out, uint32_t* err);
+
 // intersect(), proj/src/bvh.cpp:124-157: closest hit in the reference's
 // traversal order (pop the right child first), so exact-t ties go to the same
 // triangle.  Every box decision equals the reference's (box_decide, exact
@@ -198,6 +203,9 @@ __device__ __forceinline__ int box_decide(const float4& q0, const float4& q1, co
 // Moller-Trumbore.
 __device__ bool intersect(const DevScene& sc, V3 o, V3 d, double tmin, double* t_out,
                           uint32_t* tri_out, uint32_t* err) {
+  bool used;
+  const bool got = intersect_wide(sc, o, d, tmin, false, &used, t_out, tri_out, err);
+  if (used) return got;
   const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
   const RayDecide rd = make_ray_decide(o, inv);
   const float tmin_dn = __double2float_rd(tmin), tmin_up = __double2float_ru(tmin);
@@ -273,6 +281,9 @@ __device__ __forceinline__ int box_decide_cam(const float4& q0, const float4& q1
 // camera-relative decision test.
 __device__ bool intersect_camera(const DevScene& sc, V3 o, V3 d, double* t_out,
                                  uint32_t* tri_out, uint32_t* err) {
+  bool used;
+  const bool got = intersect_wide(sc, o, d, 0.0, true, &used, t_out, tri_out, err);
+  if (used) return got;
   const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
   const double ia[3] = {inv.x, inv.y, inv.z};
   float finv[3];
@@ -882,6 +893,174 @@ __device__ __forceinline__ uint32_t boxw_f(const float (&lo)[3][kWide],
 
 // Branch-free Moller-Trumbore: the reference's expressions (bvh.cpp:44-62)
 // with every early exit folded into one predicate.
+// ---------------------------------------------------------------------------
+// Closest hit on the collapsed reference tree.  The
+// reference's closest hit equals a scan of its leaves in DFS order (right
+// subtree first) in which a leaf's triangles are tested iff the leaf's own
+// box passes the slab test against the running `closest`: every ancestor was
+// tested earlier with a `closest` at least as large, on a box containing the
+// leaf's, so it passed whenever the leaf passes (the slab test is monotone in
+// both).  wide_ref keeps the binary left-to-right order in every node, so
+// pushing the passing children left to right pops them in the reference's
+// leaf order.  Internal children are culled conservatively with the `closest`
+// of the moment (a failing box fails later too).  A leaf is decided when it
+// is popped: by the fp32 inner test made at push time if `closest` has not
+// changed since (the stack watermark `fresh`), else by the exact fp64 test
+// of its reference box.  Triangle tests are the exact fp64 Moller-Trumbore.
+// ---------------------------------------------------------------------------
+// Camera rays on wide_cam: every stored coordinate is x' = fl32 outward of
+// x -/+ 2^-21 |x| (x = fl64(c - O)), so fl32(x' * fl32(inv)) bounds the
+// reference's fl64(x * inv) from outside on every axis and the plain slab
+// test is the outer test.  The reference's per-axis t exceeds ours by less
+// than 2^-20 |t|, and t -> t + |t| kappa is monotone, so the inner test
+// (the exact test certainly passes) needs only the per-child near/far
+// moved in by kappa = 2^-19.  t_min = 0; 1e-30 covers underflow.
+__device__ __forceinline__ uint32_t boxw_cam(const float (&lo)[3][kWide],
+                                             const float (&hi)[3][kWide], const float (&inv)[3],
+                                             uint32_t neg, float tmax_up, float tmax_dn,
+                                             uint32_t* inner) {
+  constexpr float kappa = 0x1.0p-19f;
+  float nb[kWide], fb[kWide];
+#pragma unroll
+  for (int c = 0; c < kWide; ++c) {
+    nb[c] = 0.f;
+    fb[c] = HUGE_VALF;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool ng = (neg >> a) & 1u;
+#pragma unroll
+    for (int c = 0; c < kWide; ++c) {
+      const float n = ng ? hi[a][c] : lo[a][c];
+      const float f = ng ? lo[a][c] : hi[a][c];
+      nb[c] = fmaxf(nb[c], n * inv[a]);
+      fb[c] = fminf(fb[c], f * inv[a]);
+    }
+  }
+  uint32_t m = 0, mi = 0;
+#pragma unroll
+  for (int c = 0; c < kWide; ++c) {
+    m |= (nb[c] <= fminf(fb[c], tmax_up) + 1e-30f) ? (1u << c) : 0u;
+    const float ni = fmaf(fabsf(nb[c]), kappa, nb[c]) + 1e-30f;
+    const float fi = fminf(fmaf(-fabsf(fb[c]), kappa, fb[c]) - 1e-30f, tmax_dn);
+    mi |= (ni <= fi) ? (1u << c) : 0u;
+  }
+  *inner = mi & m;
+  return m;
+}
+
+template <bool CAM>
+__device__ __forceinline__ bool closest_wide(const DevScene& sc, const Wide4* __restrict__ wn,
+                                             RayF rf, V3 o, V3 d, V3 inv, double tmin,
+                                             double* t_out, uint32_t* tri_out, uint32_t* err) {
+  double closest = HUGE_VAL;
+  uint32_t hit = kNoSlot;
+  uint32_t stack[kStack];
+  int sp = 0, fresh = 0;
+  // the reference tests the root box first (bvh.cpp:130-134)
+  if (!box_hit(load_node(sc.nodes, 0), o, inv, tmin, closest)) return false;
+  uint32_t cur = 0;
+  bool stale = false;
+  while (true) {
+    if (cur & kWideLeaf) {
+      bool reach = true;
+      if (stale || !(cur & kLeafVerified))
+        reach = box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf + leaf_first(cur))), o, inv, tmin,
+                        closest);
+      if (reach) {
+        const uint32_t first = leaf_first(cur), cnt = leaf_count(cur);
+        for (uint32_t k = first; k < first + cnt; ++k) {
+          double t;
+          if (tri_hit(sc.tris, k, o, d, tmin, closest, &t)) {
+            closest = t;
+            hit = k;
+            rf.tmax = __double2float_ru(closest);
+            rf.tmax_in = __double2float_rd(closest);
+            fresh = sp;  // the leaves on the stack were decided with the old closest
+          }
+        }
+      }
+    } else {
+      const float4* p = reinterpret_cast<const float4*>(wn + cur);
+      float lo[3][kWide], hi[3][kWide];
+      uint32_t c[kWide];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float4 vl = __ldg(p + a), vh = __ldg(p + 3 + a);
+        lo[a][0] = vl.x, lo[a][1] = vl.y, lo[a][2] = vl.z, lo[a][3] = vl.w;
+        hi[a][0] = vh.x, hi[a][1] = vh.y, hi[a][2] = vh.z, hi[a][3] = vh.w;
+      }
+      {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + 6));
+        c[0] = v.x, c[1] = v.y, c[2] = v.z, c[3] = v.w;
+      }
+      uint32_t mi, m;
+      if (CAM) {
+        m = boxw_cam(lo, hi, rf.inv, rf.neg, rf.tmax, rf.tmax_in, &mi);
+      } else {
+        float tn[kWide];
+        m = boxw_f(lo, hi, rf, tn, &mi);
+      }
+      if (sp + kWide > kStack) {
+        atomicOr(err, kErrStackOverflow);
+        break;
+      }
+#pragma unroll
+      for (int k = 0; k < kWide; ++k) {  // left to right: the rightmost is popped first
+        if (!((m >> k) & 1u) || c[k] == kWideEmpty) continue;
+        uint32_t e = c[k];
+        if ((e & kWideLeaf) && ((mi >> k) & 1u)) e |= kLeafVerified;
+        stack[sp++] = e;
+      }
+    }
+    if (sp == 0) break;
+    const int p = --sp;
+    cur = stack[p];
+    stale = p < fresh;
+    if (stale) fresh = p;
+  }
+  if (hit == kNoSlot) return false;
+  *t_out = closest;
+  *tri_out = sc.tris[hit].tri_id;
+  return true;
+}
+
+__device__ bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool camera,
+                               bool* used, double* t_out, uint32_t* tri_out, uint32_t* err) {
+  static_assert(kWide == 4, "closest_wide loads 4-wide nodes");
+  const Wide4* wn = camera ? sc.wide_cam : sc.wide_ref;
+  const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+  const double ia[3] = {inv.x, inv.y, inv.z}, oa[3] = {o.x, o.y, o.z};
+  bool ok = wn != nullptr && sc.fp32_ok;
+  RayF rf;
+  rf.neg = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ok &= fabs(ia[a]) <= 1e30;  // fp32-representable inverse: the decision bounds hold
+    const float fi = float(ia[a]);
+    rf.inv[a] = fi;
+    if (camera) {  // camera-relative boxes: purely relative errors (box_decide_cam)
+      rf.b[a] = 0.f;
+      rf.mt[a] = 1e-30f;
+    } else {
+      const float of = float(oa[a]);
+      rf.b[a] = -(of * fi);
+      rf.mt[a] = fmaf(fabsf(of) * fabsf(fi), 0x1.0p-21f, 1e-30f);
+    }
+    rf.mb[a] = fabsf(fi) * 0x1.0p-22f;
+    rf.neg |= (ia[a] < 0 ? 1u : 0u) << a;
+  }
+  *used = ok;
+  if (!ok) return false;
+  rf.fast = true;
+  rf.tmin = __double2float_rd(tmin);
+  rf.tmin_in = __double2float_ru(tmin);
+  rf.tmax = HUGE_VALF;
+  rf.tmax_in = HUGE_VALF;
+  return camera ? closest_wide<true>(sc, wn, rf, o, d, inv, tmin, t_out, tri_out, err)
+                : closest_wide<false>(sc, wn, rf, o, d, inv, tmin, t_out, tri_out, err);
+}
+
 __device__ __forceinline__ bool tri_any(const TriAccel* tris, uint32_t i, V3 o, V3 d, double tmin,
                                         double tmax) {
   const double2* p = reinterpret_cast<const double2*>(tris + i);
