@@ -275,9 +275,9 @@ std::vector<BvhNode> sah_over_leaves(const std::vector<BvhNode>& ref) {
 // expanded largest-surface-first, in place, so the list keeps the binary
 // tree's left-to-right order); child boxes are rounded outward to fp32, taken
 // relative to `origin` when given (x = fl64(c - O)) and then enlarged by
-// |x| * grow before the outward rounding.
+// |x| * grow + pad before the outward rounding.
 std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double* origin,
-                                 double grow = 0.0) {
+                                 double grow = 0.0, double pad = 0.0) {
   std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
   std::vector<std::array<uint32_t, kWide>> kids;
   std::vector<uint32_t> todo{0};
@@ -323,8 +323,8 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
       for (int a = 0; a < 3; ++a) {
         const double lo = origin ? bn.lo[a] - origin[a] : bn.lo[a];
         const double hi = origin ? bn.hi[a] - origin[a] : bn.hi[a];
-        n.lo[a][c] = round_down(lo - std::fabs(lo) * grow);
-        n.hi[a][c] = round_up(hi + std::fabs(hi) * grow);
+        n.lo[a][c] = round_down(lo - std::fabs(lo) * grow - pad);
+        n.hi[a][c] = round_up(hi + std::fabs(hi) * grow + pad);
       }
       n.child[c] = bn.count > 0 ? (kWideLeaf | ((bn.count - 1) << 28) | bn.a) : wid[b];
     }
@@ -351,7 +351,15 @@ void build_wide(HostScene& out) {
   if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
   const char* mode = std::getenv("RLC_SHADOW_TREE");
   const bool use_ref = mode != nullptr && std::string(mode) == "reference";
-  out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr);
+  // Shadow-tree boxes are padded by S 2^-21 (S = the largest |coordinate| of
+  // the scene): more than the fp32 error of t = fma(c, inv, -(o inv)) for any
+  // origin within S, so k_shadow's plain slab test is conservative.
+  double S = 0;
+  for (int a = 0; a < 3; ++a)
+    S = std::max(S, std::max(std::fabs(out.nodes[0].lo[a]), std::fabs(out.nodes[0].hi[a])));
+  out.coord_bound = S;
+  out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
+                           S * 0x1.0p-21);
   out.wide_ref = collapse_wide(out.nodes, nullptr);
 }
 

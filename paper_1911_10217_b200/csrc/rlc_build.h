@@ -31,6 +31,7 @@ struct HostScene {
   std::vector<Wide4> wide;       // 4-wide conservative tree, DFS order (empty: root is a leaf)
   std::vector<Wide4> wide_ref;   // the reference tree collapsed, children left to right
   std::vector<Wide4> wide_cam;   // wide_ref with camera-relative boxes
+  double coord_bound = 0;        // S: largest |coordinate| of the scene (shadow-tree padding)
   std::vector<uint32_t> tri_leaf; // binary leaf node per leaf-order triangle
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;

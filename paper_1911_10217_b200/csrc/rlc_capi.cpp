@@ -510,6 +510,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     for (int a = 0; a < 3; ++a)
       if (!(std::fabs(h.scene_lo[a]) <= 1e8 && std::fabs(h.scene_hi[a]) <= 1e8)) d.fp32_ok = 0;
     d.shadow_eps = h.shadow_eps;
+    d.coord_bound = h.coord_bound;
     d.libm_fma = probe_libm_variant() == rlc::libm::kFma ? 1u : 0u;
     d.base_tile = h.base_tile;
     for (int k = 0; k <= 16; ++k) d.level_thr[k] = h.level_threshold[k];

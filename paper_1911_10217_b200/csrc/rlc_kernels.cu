@@ -846,7 +846,49 @@ struct RayF {
   float tmin, tmax;        // outward-rounded interval (outer test)
   float tmin_in, tmax_in;  // inward-rounded interval (inner test)
   bool fast;               // every |inv| finite and <= 1e30: the inner test is valid
+  float margin;            // boxw_s inner margin S max|inv| 2^-19
 };
+
+// Shadow rays on the padded shadow tree (boxes grown by S 2^-21, S the
+// largest |coordinate| of the scene; rlc_build.cpp build_wide).  For an
+// origin within S the fp32 t = fma(c, inv, -(o inv)) differs from
+// (c - o) inv by at most 6 S |inv| 2^-24 < S |inv| 2^-21, less than the
+// padding moves the planes, so the plain slab test is the outer test.  The
+// reference's t lies within S |inv_a| 2^-20 of ours on every axis, so the
+// inner test shrinks the per-child interval by the ray constant
+// margin = S max|inv| 2^-19 (infinite or NaN, i.e. no inner test, for
+// axis-parallel rays, whose NaN slab terms fmaxf/fminf ignore).
+__device__ __forceinline__ uint32_t boxw_s(const float (&lo)[3][kWide],
+                                           const float (&hi)[3][kWide], const RayF& r,
+                                           float (&near_out)[kWide], uint32_t* inner) {
+  float nb[kWide], fb[kWide];
+#pragma unroll
+  for (int c = 0; c < kWide; ++c) {
+    nb[c] = r.tmin;
+    fb[c] = r.tmax;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool neg = (r.neg >> a) & 1u;
+#pragma unroll
+    for (int c = 0; c < kWide; ++c) {
+      const float n = neg ? hi[a][c] : lo[a][c];
+      const float f = neg ? lo[a][c] : hi[a][c];
+      nb[c] = fmaxf(nb[c], fmaf(n, r.inv[a], r.b[a]));
+      fb[c] = fminf(fb[c], fmaf(f, r.inv[a], r.b[a]));
+    }
+  }
+  uint32_t m = 0, mi = 0;
+#pragma unroll
+  for (int c = 0; c < kWide; ++c) {
+    m |= (nb[c] <= fb[c]) ? (1u << c) : 0u;
+    mi |= (fmaxf(nb[c] + r.margin, r.tmin_in) <= fminf(fb[c] - r.margin, r.tmax_in)) ? (1u << c)
+                                                                                      : 0u;
+    near_out[c] = nb[c];
+  }
+  *inner = mi & m;
+  return m;
+}
 
 // Also returns in *inner the children whose fp32 inner test passes (the
 // interval narrowed by the rounding bound and the box rounding |c||inv|2^-22),
@@ -1137,18 +1179,19 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
           if (box_hit(root, o, inv, tmin, tmax)) {  // the reference tests the root first
             const double ia[3] = {inv.x, inv.y, inv.z}, oa[3] = {o.x, o.y, o.z};
             bool exact = root.count > 0 || !sc.fp32_ok;
+            double maxinv = 0;
             rf.neg = 0;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
               exact |= fabs(ia[a]) > 1e30 && isfinite(ia[a]);
+              exact |= !(fabs(oa[a]) <= sc.coord_bound);  // origin outside the padding bound
               const float of = float(oa[a]), fi = float(ia[a]);
               rf.inv[a] = fi;
               rf.b[a] = -(of * fi);
-              rf.mt[a] = fmaf(fabsf(of) * fabsf(fi), 0x1.0p-21f, 1e-30f);
-              rf.mb[a] = fabsf(fi) * 0x1.0p-22f;
               rf.neg |= (ia[a] < 0 ? 1u : 0u) << a;
+              maxinv = fmax(maxinv, fabs(ia[a]));
             }
-            rf.fast = fabs(ia[0]) <= 1e30 && fabs(ia[1]) <= 1e30 && fabs(ia[2]) <= 1e30;
+            rf.margin = __double2float_ru(sc.coord_bound * maxinv * 0x1.0p-19) + 1e-30f;
             rf.tmin = __double2float_rd(tmin);
             rf.tmax = __double2float_ru(tmax);
             rf.tmin_in = __double2float_ru(tmin);
@@ -1191,7 +1234,7 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
       }
       float tn[kWide];
       uint32_t mi;
-      uint32_t m = boxw_f(lo, hi, rf, tn, &mi);
+      uint32_t m = boxw_s(lo, hi, rf, tn, &mi);
 #pragma unroll
       for (int k = 0; k < kWide; ++k) {
         if (c[k] == kWideEmpty) m &= ~(1u << k);

@@ -94,6 +94,7 @@ struct DevScene {
   uint32_t fp32_ok;  // scene coordinates within 1e8: the fp32 shadow pre-test is valid
   uint32_t libm_fma; // host libm build whose sin/cos the bounce sampler restates (rlc_libm.h)
   double shadow_eps;
+  double coord_bound;  // S: k_shadow's lean test holds for ray origins within S
   double base_tile;
   double level_thr[17];
   CameraConst cam;
