@@ -270,6 +270,133 @@ std::vector<BvhNode> sah_over_leaves(const std::vector<BvhNode>& ref) {
   return out;
 }
 
+// Binned-SAH binary tree over single triangles for the any-hit shadow rays
+// (DESIGN.md 5.3).  Prims are the leaf-order triangles (positions of
+// out.tris) with their exact vertex boxes; a leaf holds at most 4 triangles
+// of ONE reference leaf, so its exact box lies inside that reference leaf's
+// box and a passing (inner) test on it proves the reference leaf test.  The
+// returned leaves index `perm` (a permutation of leaf-order positions).
+std::vector<BvhNode> sah_over_tris(const rlc_scene_desc& d, const HostScene& hs,
+                                   std::vector<uint32_t>& perm) {
+  const uint32_t n = uint32_t(hs.tris.size());
+  std::vector<Box> tb(n);
+  std::vector<V3> cen(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t id = hs.tris[i].tri_id;
+    Box b;
+    b.grow(vert(d, id, 0));
+    b.grow(vert(d, id, 1));
+    b.grow(vert(d, id, 2));
+    tb[i] = b;
+    cen[i] = b.center();
+  }
+  perm.resize(n);
+  std::iota(perm.begin(), perm.end(), 0u);
+  auto area = [](const Box& b) {
+    const V3 e = b.extent();
+    return e.x * e.y + e.y * e.z + e.z * e.x;
+  };
+  std::vector<BvhNode> out;
+  out.reserve(size_t(2) * n);
+  out.push_back(BvhNode{});
+  struct Todo {
+    uint32_t node, begin, end;
+  };
+  std::vector<Todo> todo{{0, 0, n}};
+  constexpr int kBins = 16;
+  while (!todo.empty()) {
+    const Todo t = todo.back();
+    todo.pop_back();
+    Box bounds, cb;
+    for (uint32_t i = t.begin; i < t.end; ++i) {
+      bounds.grow(tb[perm[i]]);
+      cb.grow(cen[perm[i]]);
+    }
+    BvhNode& nd = out[t.node];
+    put3(nd.lo, bounds.lo);
+    put3(nd.hi, bounds.hi);
+    const uint32_t count = t.end - t.begin;
+    bool pure = true;
+    for (uint32_t i = t.begin + 1; i < t.end; ++i)
+      pure &= hs.tri_leaf[perm[i]] == hs.tri_leaf[perm[t.begin]];
+    int best_axis = -1, best_split = 0;
+    double best_cost = HUGE_VAL;
+    if (count > 1) {
+      for (int a = 0; a < 3; ++a) {
+        const double lo = comp(cb.lo, a), ext = comp(cb.hi, a) - lo;
+        if (!(ext > 0)) continue;
+        Box bb[kBins];
+        uint32_t cnt[kBins] = {};
+        for (uint32_t i = t.begin; i < t.end; ++i) {
+          int k = int((comp(cen[perm[i]], a) - lo) / ext * kBins);
+          k = k < 0 ? 0 : (k >= kBins ? kBins - 1 : k);
+          bb[k].grow(tb[perm[i]]);
+          ++cnt[k];
+        }
+        Box right[kBins];
+        uint32_t rc[kBins] = {};
+        Box acc;
+        uint32_t m = 0;
+        for (int k = kBins - 1; k > 0; --k) {
+          acc.grow(bb[k]);
+          m += cnt[k];
+          right[k] = acc;
+          rc[k] = m;
+        }
+        Box left;
+        uint32_t nl = 0;
+        for (int k = 1; k < kBins; ++k) {
+          left.grow(bb[k - 1]);
+          nl += cnt[k - 1];
+          if (nl == 0 || rc[k] == 0) continue;
+          const double cost = area(left) * nl + area(right[k]) * rc[k];
+          if (cost < best_cost) {
+            best_cost = cost;
+            best_axis = a;
+            best_split = k;
+          }
+        }
+      }
+    }
+    // leaf: one triangle, or up to 4 of one reference leaf when splitting
+    // does not pay (SAH, traversal cost 1 per box against 1 per triangle)
+    const double a_node = area(bounds);
+    const bool can_leaf = count == 1 || (count <= 4 && pure);
+    if (can_leaf && (best_axis < 0 || !(a_node > 0) ||
+                     double(count) <= 1.0 + best_cost / a_node)) {
+      nd.a = t.begin;
+      nd.b = 0;
+      nd.count = count;
+      continue;
+    }
+    uint32_t mid;
+    if (best_axis < 0) {  // coincident centroids: split the list (keeps leaves pure)
+      std::stable_sort(perm.begin() + t.begin, perm.begin() + t.end,
+                       [&](uint32_t x, uint32_t y) { return hs.tri_leaf[x] < hs.tri_leaf[y]; });
+      mid = t.begin + count / 2;
+    } else {
+      const double lo = comp(cb.lo, best_axis), ext = comp(cb.hi, best_axis) - lo;
+      const auto it = std::partition(perm.begin() + t.begin, perm.begin() + t.end,
+                                     [&](uint32_t x) {
+                                       int k = int((comp(cen[x], best_axis) - lo) / ext * kBins);
+                                       k = k < 0 ? 0 : (k >= kBins ? kBins - 1 : k);
+                                       return k < best_split;
+                                     });
+      mid = uint32_t(it - perm.begin());
+      if (mid == t.begin || mid == t.end) mid = t.begin + count / 2;
+    }
+    const uint32_t child = uint32_t(out.size());
+    out.push_back(BvhNode{});
+    out.push_back(BvhNode{});
+    out[t.node].a = child;
+    out[t.node].b = child + 1;
+    out[t.node].count = 0;
+    todo.push_back({child, t.begin, mid});
+    todo.push_back({child + 1, mid, t.end});
+  }
+  return out;
+}
+
 // Collapses a binary tree to 4-wide nodes: every wide node stands for one
 // binary internal node and lists up to four of its descendants (children
 // expanded largest-surface-first, in place, so the list keeps the binary
@@ -340,17 +467,22 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
 //    children in left-to-right order, so the reference's leaf order (right
 //    subtree first) is a plain stack traversal; `wide_cam` (camera-relative
 //    boxes) is filled in with the camera constants.
-void build_wide(HostScene& out) {
+void build_wide(const rlc_scene_desc& d, HostScene& out) {
   out.wide.clear();
   out.wide_ref.clear();
   out.tri_leaf.assign(out.tris.size(), 0);
   for (size_t i = 0; i < out.nodes.size(); ++i)
     for (uint32_t t = out.nodes[i].a; out.nodes[i].count > 0 && t < out.nodes[i].a + out.nodes[i].count; ++t)
       out.tri_leaf[t] = uint32_t(i);
+  out.tris_s = out.tris;
+  out.tri_leaf_s = out.tri_leaf;
   if (out.nodes.empty() || out.nodes[0].count > 0) return;
   if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
-  const char* mode = std::getenv("RLC_SHADOW_TREE");
-  const bool use_ref = mode != nullptr && std::string(mode) == "reference";
+  // shadow tree: SAH over triangles (default), over the reference leaves
+  // (RLC_SHADOW_TREE=leaves) or the reference tree (=reference)
+  const char* env = std::getenv("RLC_SHADOW_TREE");
+  const std::string mode = env ? env : "tris";
+  const bool use_ref = mode == "reference";
   // Shadow-tree boxes are padded by S 2^-21 (S = the largest |coordinate| of
   // the scene): more than the fp32 error of t = fma(c, inv, -(o inv)) for any
   // origin within S, so k_shadow's plain slab test is conservative.
@@ -358,8 +490,18 @@ void build_wide(HostScene& out) {
   for (int a = 0; a < 3; ++a)
     S = std::max(S, std::max(std::fabs(out.nodes[0].lo[a]), std::fabs(out.nodes[0].hi[a])));
   out.coord_bound = S;
-  out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
-                           S * 0x1.0p-21);
+  if (mode == "reference" || mode == "leaves") {
+    out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
+                             S * 0x1.0p-21);
+  } else {
+    std::vector<uint32_t> perm;
+    const std::vector<BvhNode> st = sah_over_tris(d, out, perm);
+    for (size_t i = 0; i < perm.size(); ++i) {
+      out.tris_s[i] = out.tris[perm[i]];
+      out.tri_leaf_s[i] = out.tri_leaf[perm[i]];
+    }
+    out.wide = collapse_wide(st, nullptr, 0.0, S * 0x1.0p-21);
+  }
   out.wide_ref = collapse_wide(out.nodes, nullptr);
 }
 
@@ -531,7 +673,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   }
 
   build_bvh(d, out);  // render.cpp:145
-  build_wide(out);
+  build_wide(d, out);
   out.nodes_f.resize(out.nodes.size());
   for (size_t i = 0; i < out.nodes.size(); ++i) {
     const BvhNode& n = out.nodes[i];

@@ -33,6 +33,8 @@ struct HostScene {
   std::vector<Wide4> wide_cam;   // wide_ref with camera-relative boxes
   double coord_bound = 0;        // S: largest |coordinate| of the scene (shadow-tree padding)
   std::vector<uint32_t> tri_leaf; // binary leaf node per leaf-order triangle
+  std::vector<TriAccel> tris_s;   // triangles in the shadow tree's leaf order
+  std::vector<uint32_t> tri_leaf_s; // reference leaf node per tris_s entry
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;
   // materials / triangles

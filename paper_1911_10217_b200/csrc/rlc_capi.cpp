@@ -495,6 +495,8 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     d.wide_ref = h.wide_ref.empty() ? nullptr : A.upload(h.wide_ref);
     d.wide_cam = h.wide_cam.empty() ? nullptr : A.upload(h.wide_cam);
     d.tri_leaf = A.upload(h.tri_leaf);
+    d.tris_s = A.upload(h.tris_s);
+    d.tri_leaf_s = A.upload(h.tri_leaf_s);
     d.tris = A.upload(h.tris);
     d.mats = A.upload(h.mats);
     d.tri_mat = A.upload(h.tri_mat);

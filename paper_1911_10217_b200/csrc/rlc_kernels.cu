@@ -827,7 +827,7 @@ __device__ __forceinline__ uint32_t leaf_count(uint32_t e) { return ((e >> 28) &
 __device__ __forceinline__ bool leaf_reached(const DevScene& sc, uint32_t e, V3 o, V3 inv,
                                              double tmin, double tmax) {
   if (e & kLeafVerified) return true;
-  return box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf + leaf_first(e))), o, inv, tmin, tmax);
+  return box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf_s + leaf_first(e))), o, inv, tmin, tmax);
 }
 
 // Conservative fp32 slab test of the 4 children of a Wide4 node against one
@@ -1284,7 +1284,7 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
     bool hit = false;
     while (leaf != 0) {
       const uint32_t first = leaf_first(leaf), cnt = leaf_count(leaf);
-      for (uint32_t i = first; i < first + cnt; ++i) hit |= tri_any(sc.tris, i, o, d, tmin, tmax);
+      for (uint32_t i = first; i < first + cnt; ++i) hit |= tri_any(sc.tris_s, i, o, d, tmin, tmax);
       if (hit) hit = leaf_reached(sc, leaf, o, inv, tmin, tmax);
       if (hit) break;
       if (cur != kDone && (cur & kWideLeaf)) {

@@ -80,6 +80,8 @@ struct DevScene {
   const Wide4* wide_ref;    // reference tree collapsed in its leaf order (closest hit)
   const Wide4* wide_cam;    // same, camera-relative boxes (primary rays)
   const uint32_t* tri_leaf; // binary leaf per leaf-order triangle
+  const TriAccel* tris_s;   // triangles in the shadow tree's leaf order
+  const uint32_t* tri_leaf_s; // reference leaf per tris_s entry
   const TriAccel* tris;
   const MatRec* mats;
   const uint32_t* tri_mat;

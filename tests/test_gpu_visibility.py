@@ -27,10 +27,11 @@ def random_soup(count, seed, extent, tri_size):
                  scenes.Camera((0, 0, -5), (0, 0, 0), (0, 1, 0), 45, 8, 8), "soup")
 
 
-@pytest.fixture(params=["sah", "reference"], autouse=True)
+@pytest.fixture(params=["tris", "leaves", "reference"], autouse=True)
 def shadow_tree(request, monkeypatch):
-    """Both shadow-ray trees: the SAH tree over the reference leaves
-    (default) and the reference tree collapsed to 4-wide."""
+    """All shadow-ray trees: the SAH tree over single triangles (default),
+    the SAH tree over the reference leaves, and the reference tree collapsed
+    to 4-wide."""
     monkeypatch.setenv("RLC_SHADOW_TREE", request.param)
     return request.param
 
