@@ -41,7 +41,9 @@ typedef enum rlc_status {
   RLC_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range in the reference */
   RLC_ERR_CUDA = 3,             /* CUDA runtime / kernel failure */
   RLC_ERR_NO_DEVICE = 4,        /* no sm_100 device: there is no CPU fallback */
-  RLC_ERR_INTERNAL = 5
+  RLC_ERR_INTERNAL = 5,
+  RLC_ERR_IO = 6,               /* ImageIoError io_error (image.hpp:15-28) */
+  RLC_ERR_PARSE = 7             /* ImageIoError parse_error */
 } rlc_status;
 
 /* proj/include/rlcuts/estimators.hpp:16-20 (SamplerKind) */
@@ -265,6 +267,35 @@ rlc_status rlc_pass_fold(const rlc_context* ctx, const rlc_render_config* config
  * resolved; result may be NULL. */
 rlc_status rlc_render_frame(const rlc_context* ctx, const rlc_render_config* config,
                             double* image_out, rlc_render_result* result);
+/* render_frame with a reference image (render.cpp:226-228): reference
+ * [ref_height*ref_width*3] host, linear RGB, top row first; pass_mse [passes]
+ * receives mse(framebuffer.resolve(), reference) after every pass, identical
+ * to the reference's sequential sum (per-pixel terms on the device, the
+ * ordered sum on the host while the next pass runs).  Dimensions other than
+ * the camera's fail like mse (RLC_ERR_INVALID_ARGUMENT). */
+rlc_status rlc_render_frame_scored(const rlc_context* ctx, const rlc_render_config* config,
+                                   const double* reference, int32_t ref_width,
+                                   int32_t ref_height, double* image_out,
+                                   rlc_render_result* result, double* pass_mse);
+
+/* ---- image module (proj/include/rlcuts/image.hpp:65-78,
+ *      proj/src/image.cpp:43-136); host code, images are [h*w*3] doubles,
+ *      linear RGB, top row first ----------------------------------------- */
+/* write_pfm: float32 RGB, little-endian (scale -1), bottom row first. */
+rlc_status rlc_image_write_pfm(const double* pixels, int32_t width, int32_t height,
+                               const char* path);
+/* read_pfm: *width / *height always set; pixels filled when max_pixels
+ * >= width * height (pixels may be NULL to query the size). */
+rlc_status rlc_image_read_pfm(const char* path, double* pixels, uint64_t max_pixels,
+                              int32_t* width, int32_t* height);
+/* write_ppm: 8-bit gamma-2.2 preview. */
+rlc_status rlc_image_write_ppm(const double* pixels, int32_t width, int32_t height,
+                               const char* path);
+/* mse / relative_mse (b is the reference). */
+rlc_status rlc_image_mse(const double* a, int32_t wa, int32_t ha, const double* b, int32_t wb,
+                         int32_t hb, double* out);
+rlc_status rlc_image_relative_mse(const double* a, int32_t wa, int32_t ha, const double* b,
+                                  int32_t wb, int32_t hb, double* out);
 
 #ifdef __cplusplus
 }

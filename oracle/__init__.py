@@ -13,4 +13,5 @@ Two CPU checkers live here, neither of which the product may call:
 Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline /
 ``--impl reference`` legs import this package.
 """
-from .ref import (RefRun, ref_available, ref_lib, ref_render_frame)  # noqa: F401
+from .ref import (RefRun, ref_available, ref_lib, ref_mse, ref_read_pfm,  # noqa: F401
+                  ref_render_frame, ref_write_pfm, ref_write_ppm)

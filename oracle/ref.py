@@ -39,7 +39,12 @@ _SIGS = {
     "ref_run_occluded": (None, [_P, C.c_uint32, _dp, _dp, C.POINTER(C.c_uint8)]),
     "ref_run_intersect": (None, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp, _i32p]),
     "ref_render_frame": (C.c_double, [C.POINTER(_lib.SceneDescC), C.POINTER(_lib.RenderConfigC),
-                                      _dp, _u64p, _u32p]),
+                                      _dp, _u64p, _u32p, _dp, _dp]),
+    "ref_image_write_pfm": (C.c_int, [_dp, C.c_int, C.c_int, C.c_char_p]),
+    "ref_image_read_pfm": (C.c_int, [C.c_char_p, _dp, C.c_uint64, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]),
+    "ref_image_write_ppm": (C.c_int, [_dp, C.c_int, C.c_int, C.c_char_p]),
+    "ref_image_mse": (C.c_int, [_dp, C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_int, _dp]),
     "ref_light_tree": (C.c_uint32, [C.c_uint32, _dp, _dp, _u32p, _i32p, _dp]),
     "ref_init_cut": (C.c_uint32, [C.c_uint32, _dp, _dp, C.c_uint32, C.c_double, _u32p, _u32p, _dp,
                                   _dp, _u32p, _dp]),
@@ -179,17 +184,57 @@ class RefRun:
             pass
 
 
-def ref_render_frame(scene: Scene, config: RenderConfig):
-    """The stock reference render_frame (render.cpp:202-240)."""
+def ref_render_frame(scene: Scene, config: RenderConfig, reference=None):
+    """The stock reference render_frame (render.cpp:202-240), optionally
+    scored against `reference` (h x w x 3) after every pass."""
     cam = scene.camera
     img = np.zeros((cam.height, cam.width, 3), np.float64)
     stats = np.zeros(3, np.uint64)
     ch = np.zeros(max(config.passes, 1), np.uint32)
+    pm = np.zeros(max(config.passes, 1))
     desc = scene.desc()
     cfg = config.c()
+    ref = None if reference is None else np.ascontiguousarray(reference, np.float64)
     ms = ref_lib().ref_render_frame(C.byref(desc), C.byref(cfg), dp(img),
-                                    stats.ctypes.data_as(_u64p), up(ch))
+                                    stats.ctypes.data_as(_u64p), up(ch),
+                                    None if ref is None else dp(ref),
+                                    None if ref is None else dp(pm))
     if ms < 0:
         raise RuntimeError(ref_lib().ref_last_error().decode())
     return {"image": img, "wall_ms": ms, "occupied": int(stats[0]), "lookups": int(stats[1]),
-            "fallback_hits": int(stats[2]), "sc_changes": ch[:config.passes].tolist()}
+            "fallback_hits": int(stats[2]), "sc_changes": ch[:config.passes].tolist(),
+            "pass_mse": pm[:config.passes].tolist() if ref is not None else []}
+
+
+def _img_status(r: int):
+    if r:
+        raise RuntimeError(f"reference image call failed ({r}): "
+                           + ref_lib().ref_last_error().decode())
+
+
+def ref_write_pfm(image, path):
+    im = np.ascontiguousarray(image, np.float64)
+    _img_status(ref_lib().ref_image_write_pfm(dp(im), im.shape[1], im.shape[0], str(path).encode()))
+
+
+def ref_read_pfm(path):
+    w, h = C.c_int(), C.c_int()
+    _img_status(ref_lib().ref_image_read_pfm(str(path).encode(), None, 0, C.byref(w), C.byref(h)))
+    img = np.zeros((h.value, w.value, 3))
+    _img_status(ref_lib().ref_image_read_pfm(str(path).encode(), dp(img), w.value * h.value,
+                                             C.byref(w), C.byref(h)))
+    return img
+
+
+def ref_write_ppm(image, path):
+    im = np.ascontiguousarray(image, np.float64)
+    _img_status(ref_lib().ref_image_write_ppm(dp(im), im.shape[1], im.shape[0], str(path).encode()))
+
+
+def ref_mse(a, b, relative=False):
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    out = C.c_double()
+    _img_status(ref_lib().ref_image_mse(dp(a), a.shape[1], a.shape[0], dp(b), b.shape[1],
+                                        b.shape[0], int(relative), C.byref(out)))
+    return out.value

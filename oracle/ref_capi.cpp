@@ -39,7 +39,16 @@ int fail(const std::exception& e) {
   g_err = e.what();
   if (dynamic_cast<const std::invalid_argument*>(&e)) return RLC_ERR_INVALID_ARGUMENT;
   if (dynamic_cast<const std::out_of_range*>(&e)) return RLC_ERR_OUT_OF_RANGE;
+  if (const auto* io = dynamic_cast<const ImageIoError*>(&e))
+    return io->code() == ImageIoErrc::io_error ? RLC_ERR_IO : RLC_ERR_PARSE;
   return RLC_ERR_INTERNAL;
+}
+
+Image to_image(const double* px, int w, int h) {
+  Image im(w, h);
+  for (size_t i = 0; i < im.pixels.size(); ++i)
+    im.pixels[i] = Vec3{px[3 * i], px[3 * i + 1], px[3 * i + 2]};
+  return im;
 }
 
 Scene to_scene(const rlc_scene_desc* d) {
@@ -282,13 +291,19 @@ void ref_run_intersect(void* h, uint32_t n, const double* org, const double* dir
 
 // The stock render_frame (render.cpp:202-240) -- the CPU baseline arm.
 // stats: occupied, lookups, fallback_hits.  Returns wall_ms (< 0 on error).
+// With `reference` ([h*w*3], the camera's size) pass_mse[passes] is filled.
 double ref_render_frame(const rlc_scene_desc* desc, const rlc_render_config* config,
-                        double* image, uint64_t* stats, uint32_t* sc_changes) {
+                        double* image, uint64_t* stats, uint32_t* sc_changes,
+                        const double* reference, double* pass_mse) {
   try {
     Scene scene = to_scene(desc);
     const RenderConfig cfg = to_config(config);
     const RenderContext ctx = build_context(scene, cfg);
-    const RenderResult res = render_frame(ctx, cfg);
+    Image ref_img;
+    if (reference) ref_img = to_image(reference, desc->width, desc->height);
+    const RenderResult res = render_frame(ctx, cfg, reference ? &ref_img : nullptr);
+    if (pass_mse)
+      for (size_t i = 0; i < res.pass_mse.size(); ++i) pass_mse[i] = res.pass_mse[i];
     if (image)
       for (size_t i = 0; i < res.image.pixels.size(); ++i) {
         image[3 * i] = res.image.pixels[i].x;
@@ -448,6 +463,53 @@ void ref_octa_encode(uint32_t n, const double* nrm, double* uv) {
     const Vec2 e = octa_encode({nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]});
     uv[2 * i] = e.x;
     uv[2 * i + 1] = e.y;
+  }
+}
+
+// image module (image.cpp:43-136) through the reference's own functions
+int ref_image_write_pfm(const double* px, int w, int h, const char* path) {
+  try {
+    write_pfm(to_image(px, w, h), path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_image_read_pfm(const char* path, double* px, uint64_t cap, int* w, int* h) {
+  try {
+    const Image im = read_pfm(path);
+    *w = im.width;
+    *h = im.height;
+    if (px && cap >= im.pixels.size())
+      for (size_t i = 0; i < im.pixels.size(); ++i) {
+        px[3 * i] = im.pixels[i].x;
+        px[3 * i + 1] = im.pixels[i].y;
+        px[3 * i + 2] = im.pixels[i].z;
+      }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_image_write_ppm(const double* px, int w, int h, const char* path) {
+  try {
+    write_ppm(to_image(px, w, h), path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_image_mse(const double* a, int wa, int ha, const double* b, int wb, int hb, int relative,
+                  double* out) {
+  try {
+    const Image ia = to_image(a, wa, ha), ib = to_image(b, wb, hb);
+    *out = relative ? relative_mse(ia, ib) : mse(ia, ib);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
   }
 }
 

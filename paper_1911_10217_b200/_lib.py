@@ -18,6 +18,8 @@ RLC_ERR_OUT_OF_RANGE = 2
 RLC_ERR_CUDA = 3
 RLC_ERR_NO_DEVICE = 4
 RLC_ERR_INTERNAL = 5
+RLC_ERR_IO = 6
+RLC_ERR_PARSE = 7
 
 
 class CutConfigC(C.Structure):
@@ -117,6 +119,15 @@ SIGNATURES = {
     "rlc_pass_fold": (C.c_int, [_P, C.POINTER(RenderConfigC), _P, _P, _P, _u64p, C.c_uint32,
                                 C.c_uint32, C.c_uint64]),
     "rlc_render_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.POINTER(RenderResultC)]),
+    "rlc_render_frame_scored": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.c_int32, C.c_int32,
+                                          _dp, C.POINTER(RenderResultC), _dp]),
+    "rlc_image_write_pfm": (C.c_int, [_dp, C.c_int32, C.c_int32, C.c_char_p]),
+    "rlc_image_read_pfm": (C.c_int, [C.c_char_p, _dp, C.c_uint64, C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32)]),
+    "rlc_image_write_ppm": (C.c_int, [_dp, C.c_int32, C.c_int32, C.c_char_p]),
+    "rlc_image_mse": (C.c_int, [_dp, C.c_int32, C.c_int32, _dp, C.c_int32, C.c_int32, _dp]),
+    "rlc_image_relative_mse": (C.c_int, [_dp, C.c_int32, C.c_int32, _dp, C.c_int32, C.c_int32,
+                                         _dp]),
 }
 
 _lib = None

@@ -81,4 +81,21 @@ HostCut make_template_cut(const std::vector<LtNode>& nodes, const std::vector<ui
 // level_for_footprint (hash_grid.cpp:34-44) without its own log2.
 void level_thresholds(double out[kMaxLevel + 1]);
 
+// ---- image module (rlc_image.cpp; proj/src/image.cpp:43-136) -------------
+// ImageIoError (image.hpp:15-28): code is RLC_ERR_IO or RLC_ERR_PARSE.
+struct ImageIoError : std::runtime_error {
+  ImageIoError(int code, const std::string& msg);
+  int code() const { return code_; }
+
+ private:
+  int code_;
+};
+void write_pfm(const double* px, int32_t w, int32_t h, const std::string& path);
+void read_pfm(const std::string& path, double* px, uint64_t cap_pixels, int32_t* w, int32_t* h);
+void write_ppm(const double* px, int32_t w, int32_t h, const std::string& path);
+double mse(const double* a, const double* b, uint64_t npix);
+double relative_mse(const double* a, const double* b, uint64_t npix);
+// mse's sequential sum over per-pixel terms computed elsewhere (device).
+double sum_terms(const double* e, uint64_t n);
+
 }  // namespace rlc

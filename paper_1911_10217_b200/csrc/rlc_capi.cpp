@@ -45,6 +45,9 @@ rlc_status guarded(F&& f) {
   } catch (const NoDevice& e) {
     g_err = e.what();
     return RLC_ERR_NO_DEVICE;
+  } catch (const rlc::ImageIoError& e) {
+    g_err = e.what();
+    return rlc_status(e.code());
   } catch (const CudaError& e) {
     g_err = e.what();
     return RLC_ERR_CUDA;
@@ -1055,51 +1058,173 @@ void prepare_frame_cache(rlc_context* ctx, const rlc_render_config* config) {
 
 extern "C" {
 
+namespace {
+
+// Pinned host staging for the per-pixel error terms of render_frame_scored.
+struct PinnedBuf {
+  double* p = nullptr;
+  explicit PinnedBuf(size_t n) { RLC_CK(cudaMallocHost(&p, n * sizeof(double))); }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// render_frame (render.cpp:202-240), optionally scored against a reference
+// image after every pass (render.cpp:226-228).
+void render_frame_impl(rlc_context* ctx, const rlc_render_config* config, const double* reference,
+                       double* image_out, rlc_render_result* result, double* pass_mse) {
+  require(config->passes != 0 && config->spp != 0 && config->spp % config->passes == 0,
+          "render_frame: spp must be divisible by passes");
+  const auto t0 = std::chrono::steady_clock::now();
+  RLC_CK(cudaSetDevice(ctx->device));
+  prepare_frame_cache(ctx, config);
+  rlc_grid* grid = config->sampler == RLC_SAMPLER_RL_LIGHTCUTS ? ctx->frame_grid : nullptr;
+  rlc_framebuffer* fb = ctx->frame_fb;
+  cudaStream_t st = ctx->stream;
+  if (grid) {
+    grid->alpha = config->cut.alpha;
+    reset_grid(grid, st);
+  }
+  const size_t npix = size_t(fb->width) * size_t(fb->height);
+  RLC_CK(cudaMemsetAsync(fb->fb.sum, 0, 24 * npix, st));
+  RLC_CK(cudaMemsetAsync(fb->fb.count, 0, 8 * npix, st));
+  uint32_t* d_hist = ctx->frame_hist;
+  RLC_CK(cudaMemsetAsync(d_hist, 0, 4 * size_t(config->passes), st));
+  // scoring: the reference on the device, per-pixel terms double-buffered to
+  // pinned host memory, the ordered sum of pass p - 1 while pass p runs
+  DeviceArena tmp;
+  std::unique_ptr<PinnedBuf> h_err[2];
+  double* d_ref = nullptr;
+  double* d_err[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int k = 0; k < 2; ++k)
+        if (e[k]) cudaEventDestroy(e[k]);
+    }
+  } ev_guard{ev};
+  if (reference) {
+    d_ref = tmp.alloc<double>(3 * npix);
+    RLC_CK(cudaMemcpyAsync(d_ref, reference, 24 * npix, cudaMemcpyHostToDevice, st));
+    for (int k = 0; k < 2; ++k) {
+      d_err[k] = tmp.alloc<double>(npix);
+      h_err[k] = std::make_unique<PinnedBuf>(npix);
+      RLC_CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    }
+  }
+  auto score = [&](uint32_t pass) {
+    const int k = int(pass & 1u);
+    RLC_CK(cudaEventSynchronize(ev[k]));
+    pass_mse[pass] = rlc::sum_terms(h_err[k]->p, npix) / (3.0 * double(npix));
+  };
+  for (uint32_t pass = 0; pass < config->passes; ++pass) {
+    enqueue_pass(ctx, config, pass, grid, fb, 0, uint32_t(ctx->host.cam.height));
+    if (grid) enqueue_eop(grid, ctx, &config->cut, d_hist + pass);
+    if (reference) {
+      const int k = int(pass & 1u);
+      rlc::launch_pixel_err(fb->fb, uint32_t(npix), d_ref, d_err[k], st);
+      RLC_CK(cudaMemcpyAsync(h_err[k]->p, d_err[k], 8 * npix, cudaMemcpyDeviceToHost, st));
+      RLC_CK(cudaEventRecord(ev[k], st));
+      if (pass > 0) score(pass - 1);
+    }
+  }
+  if (reference) score(config->passes - 1);
+  if (image_out) {
+    rlc::launch_resolve(fb->fb, uint32_t(npix), fb->d_image, st);
+    RLC_CK(cudaMemcpyAsync(image_out, fb->d_image, 24 * npix, cudaMemcpyDeviceToHost, st));
+  }
+  std::vector<uint32_t> h(config->passes);
+  RLC_CK(cudaMemcpyAsync(h.data(), d_hist, 4 * h.size(), cudaMemcpyDeviceToHost, st));
+  unsigned long long c[rlc::kCntNum] = {};
+  if (grid)
+    RLC_CK(cudaMemcpyAsync(c, grid->dev.counters, sizeof(c), cudaMemcpyDeviceToHost, st));
+  finish_sync(ctx, grid);
+  if (result) {
+    result->num_passes = config->passes;
+    if (result->sc_changes) std::memcpy(result->sc_changes, h.data(), 4 * h.size());
+    result->occupied_cells = uint32_t(c[rlc::kCntCells]);
+    result->lookups = c[rlc::kCntLookups];
+    result->fallback_hits = c[rlc::kCntFallback];
+    result->wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+}
+
+void check_image(const double* px, int32_t w, int32_t h, const char* what) {
+  require(px != nullptr && w > 0 && h > 0, what);
+}
+
+}  // namespace
+
 rlc_status rlc_render_frame(const rlc_context* cctx, const rlc_render_config* config,
                             double* image_out, rlc_render_result* result) {
   return guarded([&] {
     require(cctx != nullptr && config != nullptr, "render_frame: null argument");
-    require(config->passes != 0 && config->spp != 0 && config->spp % config->passes == 0,
-            "render_frame: spp must be divisible by passes");
-    rlc_context* ctx = const_cast<rlc_context*>(cctx);
-    const auto t0 = std::chrono::steady_clock::now();
-    RLC_CK(cudaSetDevice(ctx->device));
-    prepare_frame_cache(ctx, config);
-    rlc_grid* grid = config->sampler == RLC_SAMPLER_RL_LIGHTCUTS ? ctx->frame_grid : nullptr;
-    rlc_framebuffer* fb = ctx->frame_fb;
-    cudaStream_t st = ctx->stream;
-    if (grid) {
-      grid->alpha = config->cut.alpha;
-      reset_grid(grid, st);
-    }
-    const size_t npix = size_t(fb->width) * size_t(fb->height);
-    RLC_CK(cudaMemsetAsync(fb->fb.sum, 0, 24 * npix, st));
-    RLC_CK(cudaMemsetAsync(fb->fb.count, 0, 8 * npix, st));
-    uint32_t* d_hist = ctx->frame_hist;
-    RLC_CK(cudaMemsetAsync(d_hist, 0, 4 * size_t(config->passes), st));
-    for (uint32_t pass = 0; pass < config->passes; ++pass) {
-      enqueue_pass(ctx, config, pass, grid, fb, 0, uint32_t(ctx->host.cam.height));
-      if (grid) enqueue_eop(grid, ctx, &config->cut, d_hist + pass);
-    }
-    if (image_out) {
-      rlc::launch_resolve(fb->fb, uint32_t(npix), fb->d_image, st);
-      RLC_CK(cudaMemcpyAsync(image_out, fb->d_image, 24 * npix, cudaMemcpyDeviceToHost, st));
-    }
-    std::vector<uint32_t> h(config->passes);
-    RLC_CK(cudaMemcpyAsync(h.data(), d_hist, 4 * h.size(), cudaMemcpyDeviceToHost, st));
-    unsigned long long c[rlc::kCntNum] = {};
-    if (grid)
-      RLC_CK(cudaMemcpyAsync(c, grid->dev.counters, sizeof(c), cudaMemcpyDeviceToHost, st));
-    finish_sync(ctx, grid);
-    if (result) {
-      result->num_passes = config->passes;
-      if (result->sc_changes) std::memcpy(result->sc_changes, h.data(), 4 * h.size());
-      result->occupied_cells = uint32_t(c[rlc::kCntCells]);
-      result->lookups = c[rlc::kCntLookups];
-      result->fallback_hits = c[rlc::kCntFallback];
-      result->wall_ms = std::chrono::duration<double, std::milli>(
-                            std::chrono::steady_clock::now() - t0).count();
-    }
+    render_frame_impl(const_cast<rlc_context*>(cctx), config, nullptr, image_out, result, nullptr);
+  });
+}
+
+rlc_status rlc_render_frame_scored(const rlc_context* cctx, const rlc_render_config* config,
+                                   const double* reference, int32_t ref_width,
+                                   int32_t ref_height, double* image_out,
+                                   rlc_render_result* result, double* pass_mse) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr, "render_frame: null argument");
+    require(reference == nullptr || pass_mse != nullptr, "render_frame: null pass_mse");
+    if (reference)
+      require(ref_width == cctx->host.cam.width && ref_height == cctx->host.cam.height,
+              "mse: image dimensions disagree");
+    render_frame_impl(const_cast<rlc_context*>(cctx), config, reference, image_out, result,
+                      pass_mse);
+  });
+}
+
+rlc_status rlc_image_write_pfm(const double* pixels, int32_t width, int32_t height,
+                               const char* path) {
+  return guarded([&] {
+    require(path != nullptr, "write_pfm: null path");
+    check_image(pixels, width, height, "write_pfm: bad image");
+    rlc::write_pfm(pixels, width, height, path);
+  });
+}
+
+rlc_status rlc_image_read_pfm(const char* path, double* pixels, uint64_t max_pixels,
+                              int32_t* width, int32_t* height) {
+  return guarded([&] {
+    require(path != nullptr && width != nullptr && height != nullptr, "read_pfm: null argument");
+    rlc::read_pfm(path, pixels, max_pixels, width, height);
+  });
+}
+
+rlc_status rlc_image_write_ppm(const double* pixels, int32_t width, int32_t height,
+                               const char* path) {
+  return guarded([&] {
+    require(path != nullptr, "write_ppm: null path");
+    check_image(pixels, width, height, "write_ppm: bad image");
+    rlc::write_ppm(pixels, width, height, path);
+  });
+}
+
+rlc_status rlc_image_mse(const double* a, int32_t wa, int32_t ha, const double* b, int32_t wb,
+                         int32_t hb, double* out) {
+  return guarded([&] {
+    require(out != nullptr, "mse: null output");
+    require(wa == wb && ha == hb, "mse: image dimensions disagree");
+    check_image(a, wa, ha, "mse: bad image");
+    check_image(b, wb, hb, "mse: bad image");
+    *out = rlc::mse(a, b, uint64_t(wa) * uint64_t(ha));
+  });
+}
+
+rlc_status rlc_image_relative_mse(const double* a, int32_t wa, int32_t ha, const double* b,
+                                  int32_t wb, int32_t hb, double* out) {
+  return guarded([&] {
+    require(out != nullptr, "relative_mse: null output");
+    require(wa == wb && ha == hb, "mse: image dimensions disagree");
+    check_image(a, wa, ha, "mse: bad image");
+    check_image(b, wb, hb, "mse: bad image");
+    *out = rlc::relative_mse(a, b, uint64_t(wa) * uint64_t(ha));
   });
 }
 

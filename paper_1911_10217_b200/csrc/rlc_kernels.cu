@@ -2126,6 +2126,25 @@ void launch_libm_sincos(const DevScene& sc, uint32_t n, const double* x, double*
   count_launch();
 }
 
+// d = resolve() - ref per pixel (image.cpp:35-41, 117-121)
+__global__ void k_pixel_err(Framebuf fb, uint32_t npix, const double* __restrict__ ref,
+                            double* __restrict__ err) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  const unsigned long long c = fb.count[i];
+  double a[3];
+  for (int k = 0; k < 3; ++k) a[k] = c > 0 ? fb.sum[3 * i + k] / double(c) : 0.0;
+  const double dx = a[0] - ref[3 * i], dy = a[1] - ref[3 * i + 1], dz = a[2] - ref[3 * i + 2];
+  err[i] = dx * dx + dy * dy + dz * dz;
+}
+
+void launch_pixel_err(const Framebuf& fb, uint32_t npix, const double* ref, double* err,
+                      cudaStream_t st) {
+  if (npix == 0) return;
+  k_pixel_err<<<blocks_for(npix, 256), 256, 0, st>>>(fb, npix, ref, err);
+  count_launch();
+}
+
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st) {
   if (npix == 0) return;
   k_resolve<<<blocks_for(npix, 256), 256, 0, st>>>(fb, npix, image);

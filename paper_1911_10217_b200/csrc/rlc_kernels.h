@@ -222,6 +222,10 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
                             double tmin, double* t_out, int32_t* tri_out,
                             unsigned long long* counters, cudaStream_t st);
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
+// Per-pixel squared error of the resolved framebuffer against `ref`
+// (mse's summand, image.cpp:119-121), for the ordered host sum.
+void launch_pixel_err(const Framebuf& fb, uint32_t npix, const double* ref, double* err,
+                      cudaStream_t st);
 // Device sin/cos of the bounce sampler (rlc_libm.h) for the parity tests.
 void launch_libm_sincos(const DevScene& sc, uint32_t n, const double* x, double* s, double* c,
                         cudaStream_t st);

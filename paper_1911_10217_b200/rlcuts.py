@@ -26,6 +26,14 @@ class DeviceError(RuntimeError):
     pass
 
 
+class ImageIoError(RuntimeError):
+    """ImageIoError (image.hpp:15-28); .code is "io_error" or "parse_error"."""
+
+    def __init__(self, msg: str, code: str):
+        super().__init__(msg)
+        self.code = code
+
+
 def _check(status: int):
     if status == _lib.RLC_OK:
         return
@@ -36,6 +44,8 @@ def _check(status: int):
         raise IndexError(msg)
     if status == _lib.RLC_ERR_NO_DEVICE:
         raise NoDeviceError(msg)
+    if status in (_lib.RLC_ERR_IO, _lib.RLC_ERR_PARSE):
+        raise ImageIoError(msg, "io_error" if status == _lib.RLC_ERR_IO else "parse_error")
     raise DeviceError(msg)
 
 
@@ -356,19 +366,133 @@ class RenderResult:  # render.hpp:56-64
     lookups: int
     fallback_hits: int
     sc_changes: list
+    pass_mse: list = field(default_factory=list)  # vs the reference image; empty without one
 
 
-def render_frame(ctx: RenderContext, config: RenderConfig) -> RenderResult:
-    """render_frame (proj/src/render.cpp:202-240)."""
+def render_frame(ctx: RenderContext, config: RenderConfig,
+                 reference: np.ndarray | None = None) -> RenderResult:
+    """render_frame (proj/src/render.cpp:202-240); with `reference` (h x w x 3
+    linear RGB) the accumulated image is scored after every pass."""
     cam = ctx.scene.camera
     img = np.zeros((cam.height, cam.width, 3), np.float64)
     changes = (C.c_uint32 * max(config.passes, 1))()
     res = _lib.RenderResultC()
     res.sc_changes = C.cast(changes, C.POINTER(C.c_uint32))
     cfg = config.c()
-    _check(_lib.load().rlc_render_frame(ctx.handle, C.byref(cfg), _dptr(img), C.byref(res)))
+    if reference is None:
+        _check(_lib.load().rlc_render_frame(ctx.handle, C.byref(cfg), _dptr(img), C.byref(res)))
+        pm = []
+    else:
+        ref = np.ascontiguousarray(reference, np.float64)
+        if ref.ndim != 3 or ref.shape[2] != 3:
+            raise ValueError("mse: image dimensions disagree")
+        out = np.zeros(max(config.passes, 1))
+        _check(_lib.load().rlc_render_frame_scored(ctx.handle, C.byref(cfg), _dptr(ref),
+                                                   ref.shape[1], ref.shape[0], _dptr(img),
+                                                   C.byref(res), _dptr(out)))
+        pm = out[:config.passes].tolist()
     return RenderResult(img, res.wall_ms, res.occupied_cells, res.lookups, res.fallback_hits,
-                        list(changes)[:config.passes])
+                        list(changes)[:config.passes], pm)
+
+
+# ---- image module (proj/include/rlcuts/image.hpp:65-78) -------------------
+def _img(a: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, np.float64)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError("image must be h x w x 3")
+    return a
+
+
+def write_pfm(image: np.ndarray, path: str) -> None:
+    """write_pfm (image.cpp:43-60): float32 RGB, little-endian, bottom row first."""
+    im = _img(image)
+    _check(_lib.load().rlc_image_write_pfm(_dptr(im), im.shape[1], im.shape[0],
+                                           str(path).encode()))
+
+
+def read_pfm(path: str) -> np.ndarray:
+    """read_pfm (image.cpp:62-94)."""
+    w, h = C.c_int32(), C.c_int32()
+    lib = _lib.load()
+    _check(lib.rlc_image_read_pfm(str(path).encode(), None, 0, C.byref(w), C.byref(h)))
+    img = np.zeros((h.value, w.value, 3), np.float64)
+    _check(lib.rlc_image_read_pfm(str(path).encode(), _dptr(img), img.shape[0] * img.shape[1],
+                                  C.byref(w), C.byref(h)))
+    return img
+
+
+def write_ppm(image: np.ndarray, path: str) -> None:
+    """write_ppm (image.cpp:96-112): 8-bit gamma-2.2 preview."""
+    im = _img(image)
+    _check(_lib.load().rlc_image_write_ppm(_dptr(im), im.shape[1], im.shape[0],
+                                           str(path).encode()))
+
+
+def mse(a: np.ndarray, b: np.ndarray) -> float:
+    """mse (image.cpp:114-124), the reference's sequential sum."""
+    a, b = _img(a), _img(b)
+    out = C.c_double()
+    _check(_lib.load().rlc_image_mse(_dptr(a), a.shape[1], a.shape[0], _dptr(b), b.shape[1],
+                                     b.shape[0], C.byref(out)))
+    return out.value
+
+
+def relative_mse(a: np.ndarray, b: np.ndarray) -> float:
+    """relative_mse (image.cpp:126-136); b is the reference."""
+    a, b = _img(a), _img(b)
+    out = C.c_double()
+    _check(_lib.load().rlc_image_relative_mse(_dptr(a), a.shape[1], a.shape[0], _dptr(b),
+                                              b.shape[1], b.shape[0], C.byref(out)))
+    return out.value
+
+
+# ---- the stats CSV of the reference CLI (tools/main.cpp:224-258) ----------
+STATS_HEADER = (
+    "scene,sampler,spp,passes,width,height,seed,depth,workers,cut_size,alpha,"
+    "threshold_T,eps_q,iterations,base_tile,capacity,probe_limit,normal_bits,"
+    "jitter_scale,alpha_schedule,wall_ms,mse,relative_mse,pass_mse_series,"
+    "sc_changes_per_pass,occupied_cells,lookups,fallback_hits,fallback_rate,error")
+
+_SAMPLER_NAMES = {0: "uniform", 1: "energy", 2: "rl"}
+
+
+def _g(v: float, prec: int = 6) -> str:
+    """std::ostream << double at precision `prec` (%g-style, no trailing zeros)."""
+    return f"{v:.{prec}g}"
+
+
+def csv_escape(field_: str) -> str:
+    if not any(c in field_ for c in ',"\n\r'):
+        return field_
+    return '"' + field_.replace('"', '""') + '"'
+
+
+def stats_row(scene_id: str, config: RenderConfig, width: int, height: int, base_tile: float,
+              result: RenderResult | None = None, error_mse: float | None = None,
+              error_rel: float | None = None, error_message: str = "") -> str:
+    """write_stats_row (tools/main.cpp:230-258): one CSV row, newline-terminated.
+    `config` carries the CLI flags (RenderConfig fields); `base_tile` is the
+    resolved one (RenderContext.base_tile)."""
+    c = config
+    schedule = "harmonic" if int(c.cut.alpha_schedule) == 1 else "fixed"
+    parts = [csv_escape(scene_id), _SAMPLER_NAMES[int(c.sampler)], str(c.spp), str(c.passes),
+             str(width), str(height), str(c.seed), str(c.max_depth), str(c.workers),
+             str(c.cut.cut_size), _g(c.cut.alpha), _g(c.cut.split_threshold), _g(c.cut.eps_q),
+             str(c.cut.iterations), _g(base_tile), str(c.hash.capacity), str(c.hash.probe_limit),
+             str(c.hash.normal_bits), _g(c.hash.jitter_scale), schedule]
+    if result is not None:
+        rate = result.fallback_hits / result.lookups if result.lookups > 0 else 0.0
+        parts += [_g(result.wall_ms, 17),
+                  _g(error_mse, 17) if error_mse is not None else "",
+                  _g(error_rel, 17) if error_rel is not None else "",
+                  csv_escape(";".join(_g(v, 17) for v in result.pass_mse)),
+                  csv_escape(";".join(str(v) for v in result.sc_changes)),
+                  str(result.occupied_cells), str(result.lookups), str(result.fallback_hits),
+                  _g(rate, 17)]
+    else:
+        parts += [""] * 9
+    parts.append(csv_escape(error_message))
+    return ",".join(parts) + "\n"
 
 
 def libm_variant() -> int:
