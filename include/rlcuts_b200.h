@@ -154,6 +154,16 @@ rlc_status rlc_render_config_default(rlc_render_config* config);
 rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_config* config,
                               int device, rlc_context** out);
 rlc_status rlc_context_destroy(rlc_context* ctx);
+/* Dynamic emitters (the reference has no such call):
+ * after this call the context renders `scene` exactly as
+ *     ctx' = build_context(scene, creation config); ctx'.tree = ctx.tree;
+ * would (render.cpp:143-157) -- a fresh scene BVH, emitter records and
+ * energy cdf, but the light tree of the context's creation (emitter order,
+ * topology and node energies), so the learned cuts of every hash grid of
+ * this context stay valid across frames.  Vertices and the camera pose may
+ * change; the triangle count, material ids, materials and the camera
+ * resolution must not (RLC_ERR_INVALID_ARGUMENT).  Synchronizes. */
+rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scene);
 rlc_status rlc_context_info_get(const rlc_context* ctx, rlc_context_info* info);
 /* Issue device work on `stream` (a cudaStream_t); NULL = the context's own. */
 rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream);

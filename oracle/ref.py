@@ -40,6 +40,7 @@ _SIGS = {
     "ref_run_intersect": (None, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp, _i32p]),
     "ref_render_frame": (C.c_double, [C.POINTER(_lib.SceneDescC), C.POINTER(_lib.RenderConfigC),
                                       _dp, _u64p, _u32p, _dp, _dp]),
+    "ref_run_update_scene": (C.c_int, [_P, C.POINTER(_lib.SceneDescC)]),
     "ref_image_write_pfm": (C.c_int, [_dp, C.c_int, C.c_int, C.c_char_p]),
     "ref_image_read_pfm": (C.c_int, [C.c_char_p, _dp, C.c_uint64, C.POINTER(C.c_int),
                                      C.POINTER(C.c_int)]),
@@ -109,6 +110,15 @@ class RefRun:
         self.h = lib.ref_run_create(C.byref(self._desc), C.byref(self._cfg), C.byref(st))
         if not self.h:
             raise_ref(st.value)
+
+    def update_scene(self, scene: Scene):
+        """ctx' = build_context(scene, cfg) with the creation light tree
+        (the semantics of rlc_context_update_scene)."""
+        desc = scene.desc()
+        st = ref_lib().ref_run_update_scene(self.h, C.byref(desc))
+        if st:
+            raise_ref(st)
+        self.scene, self._desc = scene, desc
 
     def run_pass(self, pass_index: int) -> tuple[int, float]:
         ms = C.c_double()

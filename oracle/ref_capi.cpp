@@ -171,6 +171,24 @@ void* ref_run_create(const rlc_scene_desc* desc, const rlc_render_config* config
 
 void ref_run_destroy(void* h) { delete static_cast<RefRun*>(h); }
 
+// The dynamic-emitter semantics of rlc_context_update_scene, through the
+// reference's public API: ctx' = build_context(scene', cfg) with the light
+// tree of the run's creation; the HashGrid and the Framebuffer carry over.
+int ref_run_update_scene(void* h, const rlc_scene_desc* desc) {
+  RefRun* run = static_cast<RefRun*>(h);
+  try {
+    LightTree tree0 = run->ctx.tree;
+    run->scene = to_scene(desc);
+    run->ctx = build_context(run->scene, run->cfg);
+    run->ctx.scene = &run->scene;
+    run->ctx.accel.scene = &run->scene;
+    run->ctx.tree = std::move(tree0);
+    return RLC_OK;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // render_pass + end_of_pass_update (render.cpp:219-224).  Returns the
 // split-collapse change count, or -status on error.
 int64_t ref_run_pass(void* h, uint32_t pass_index, double* wall_ms) {

@@ -119,6 +119,7 @@ SIGNATURES = {
     "rlc_pass_fold": (C.c_int, [_P, C.POINTER(RenderConfigC), _P, _P, _P, _u64p, C.c_uint32,
                                 C.c_uint32, C.c_uint64]),
     "rlc_render_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.POINTER(RenderResultC)]),
+    "rlc_context_update_scene": (C.c_int, [_P, C.POINTER(SceneDescC)]),
     "rlc_render_frame_scored": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.c_int32, C.c_int32,
                                           _dp, C.POINTER(RenderResultC), _dp]),
     "rlc_image_write_pfm": (C.c_int, [_dp, C.c_int32, C.c_int32, C.c_char_p]),

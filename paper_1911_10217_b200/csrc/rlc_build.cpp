@@ -654,6 +654,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
     if (d.material_ids[t] >= d.num_materials)
       throw OutOfRange("build_context: material id out of range");
 
+  out.mat_values.assign(d.materials, d.materials + size_t(d.num_materials) * 6);
   out.mats.resize(d.num_materials);
   for (uint32_t m = 0; m < d.num_materials; ++m) {
     const double* v = d.materials + size_t(m) * 6;

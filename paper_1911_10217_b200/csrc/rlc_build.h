@@ -33,6 +33,7 @@ struct HostScene {
   std::vector<Wide4> wide_cam;   // wide_ref with camera-relative boxes
   double coord_bound = 0;        // S: largest |coordinate| of the scene (shadow-tree padding)
   std::vector<uint32_t> tri_leaf; // binary leaf node per leaf-order triangle
+  std::vector<double> mat_values; // the scene's materials [m*6] (albedo, emission)
   std::vector<TriAccel> tris_s;   // triangles in the shadow tree's leaf order
   std::vector<uint32_t> tri_leaf_s; // reference leaf node per tris_s entry
   double scene_lo[3], scene_hi[3];

@@ -169,6 +169,7 @@ struct rlc_context {
   cudaStream_t stream = nullptr;
   rlc::HostScene host;
   rlc::DevScene dev{};
+  rlc_render_config create_cfg{};  // build_context's config (rlc_context_update_scene)
   DeviceArena arena;
   unsigned long long* counters = nullptr;  // error bits for grid-less passes
   // primary rays of the next pass overlap the tail of the current one: they
@@ -446,6 +447,39 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
   RLC_CK(cudaGetLastError());
 }
 
+// Uploads the device view of a host scene into arena A.
+void upload_scene(const rlc::HostScene& h, DeviceArena& A, rlc::DevScene& d) {
+  d.nodes = A.upload(h.nodes);
+  d.nodes_f = A.upload(h.nodes_f);
+  d.nodes_cam = A.upload(h.nodes_cam);
+  d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
+  d.wide_ref = h.wide_ref.empty() ? nullptr : A.upload(h.wide_ref);
+  d.wide_cam = h.wide_cam.empty() ? nullptr : A.upload(h.wide_cam);
+  d.tri_leaf = A.upload(h.tri_leaf);
+  d.tris_s = A.upload(h.tris_s);
+  d.tri_leaf_s = A.upload(h.tri_leaf_s);
+  d.tris = A.upload(h.tris);
+  d.mats = A.upload(h.mats);
+  d.tri_mat = A.upload(h.tri_mat);
+  d.tri_normal = A.upload(h.tri_normal);
+  d.lights = A.upload(h.lights);
+  d.order = A.upload(h.order);
+  d.lt = A.upload(h.lt_nodes);
+  d.energy_cdf = A.upload(h.energy_cdf);
+  d.emitter_energy = A.upload(h.emitter_energy);
+  d.num_lights = uint32_t(h.lights.size());
+  d.num_tris = uint32_t(h.tri_mat.size());
+  d.fp32_ok = 1;
+  for (int a = 0; a < 3; ++a)
+    if (!(std::fabs(h.scene_lo[a]) <= 1e8 && std::fabs(h.scene_hi[a]) <= 1e8)) d.fp32_ok = 0;
+  d.shadow_eps = h.shadow_eps;
+  d.coord_bound = h.coord_bound;
+  d.libm_fma = probe_libm_variant() == rlc::libm::kFma ? 1u : 0u;
+  d.base_tile = h.base_tile;
+  for (int k = 0; k <= 16; ++k) d.level_thr[k] = h.level_threshold[k];
+  d.cam = h.cam;
+}
+
 }  // namespace
 
 extern "C" {
@@ -487,40 +521,10 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     check_device(device);
     auto ctx = std::make_unique<rlc_context>();
     ctx->device = device;
+    ctx->create_cfg = *config;
     rlc::build_host_scene(*scene, *config, ctx->host);
-    const rlc::HostScene& h = ctx->host;
-    DeviceArena& A = ctx->arena;
-    rlc::DevScene& d = ctx->dev;
-    d.nodes = A.upload(h.nodes);
-    d.nodes_f = A.upload(h.nodes_f);
-    d.nodes_cam = A.upload(h.nodes_cam);
-    d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
-    d.wide_ref = h.wide_ref.empty() ? nullptr : A.upload(h.wide_ref);
-    d.wide_cam = h.wide_cam.empty() ? nullptr : A.upload(h.wide_cam);
-    d.tri_leaf = A.upload(h.tri_leaf);
-    d.tris_s = A.upload(h.tris_s);
-    d.tri_leaf_s = A.upload(h.tri_leaf_s);
-    d.tris = A.upload(h.tris);
-    d.mats = A.upload(h.mats);
-    d.tri_mat = A.upload(h.tri_mat);
-    d.tri_normal = A.upload(h.tri_normal);
-    d.lights = A.upload(h.lights);
-    d.order = A.upload(h.order);
-    d.lt = A.upload(h.lt_nodes);
-    d.energy_cdf = A.upload(h.energy_cdf);
-    d.emitter_energy = A.upload(h.emitter_energy);
-    d.num_lights = uint32_t(h.lights.size());
-    d.num_tris = uint32_t(h.tri_mat.size());
-    d.fp32_ok = 1;
-    for (int a = 0; a < 3; ++a)
-      if (!(std::fabs(h.scene_lo[a]) <= 1e8 && std::fabs(h.scene_hi[a]) <= 1e8)) d.fp32_ok = 0;
-    d.shadow_eps = h.shadow_eps;
-    d.coord_bound = h.coord_bound;
-    d.libm_fma = probe_libm_variant() == rlc::libm::kFma ? 1u : 0u;
-    d.base_tile = h.base_tile;
-    for (int k = 0; k <= 16; ++k) d.level_thr[k] = h.level_threshold[k];
-    d.cam = h.cam;
-    ctx->counters = A.alloc<unsigned long long>(rlc::kCntNum);
+    upload_scene(ctx->host, ctx->arena, ctx->dev);
+    ctx->counters = ctx->arena.alloc<unsigned long long>(rlc::kCntNum);
     RLC_CK(cudaMemset(ctx->counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
@@ -540,6 +544,43 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     }
     RLC_CK(cudaStreamSynchronize(ctx->stream));
     *out = ctx.release();
+  });
+}
+
+rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scene) {
+  return guarded([&] {
+    require(ctx != nullptr && scene != nullptr, "rlc_context_update_scene: null argument");
+    const rlc::HostScene& old = ctx->host;
+    require(scene->num_triangles == old.tri_mat.size() &&
+                scene->num_materials * 6 == old.mat_values.size() &&
+                scene->width == old.cam.width && scene->height == old.cam.height,
+            "rlc_context_update_scene: triangle count, materials and resolution must not change");
+    for (uint32_t t = 0; t < scene->num_triangles; ++t)
+      require(scene->material_ids[t] == old.tri_mat[t],
+              "rlc_context_update_scene: material ids must not change");
+    for (size_t i = 0; i < old.mat_values.size(); ++i)
+      require(scene->materials[i] == old.mat_values[i],
+              "rlc_context_update_scene: materials must not change");
+    RLC_CK(cudaSetDevice(ctx->device));
+    // build_context(scene) (render.cpp:143-157) with the light tree of the
+    // context's creation: same emitter order, topology and node energies
+    rlc::HostScene h;
+    rlc::build_host_scene(*scene, ctx->create_cfg, h);
+    h.order = old.order;
+    h.lt_nodes = old.lt_nodes;
+    h.lt_begin = old.lt_begin;
+    h.lt_energy = old.lt_energy;
+    DeviceArena A;
+    rlc::DevScene d{};
+    upload_scene(h, A, d);
+    unsigned long long* counters = A.alloc<unsigned long long>(rlc::kCntNum);
+    RLC_CK(cudaMemset(counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
+    ctx->sync_all();
+    std::swap(ctx->arena.ptrs, A.ptrs);
+    std::swap(ctx->arena.bytes, A.bytes);
+    ctx->dev = d;
+    ctx->counters = counters;
+    ctx->host = std::move(h);
   });
 }
 

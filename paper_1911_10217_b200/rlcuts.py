@@ -128,6 +128,14 @@ class RenderContext:
         _check(_lib.load().rlc_context_info_get(self.handle, C.byref(i)))
         return {k: getattr(i, k) for k, _ in _lib.ContextInfoC._fields_}
 
+    def update_scene(self, scene: Scene):
+        """Dynamic emitters (rlc_context_update_scene): render `scene` from now
+        on with the light tree of this context's creation, so the learned cuts
+        of its hash grids stay valid.  Vertices and camera pose may change."""
+        desc = scene.desc()
+        _check(_lib.load().rlc_context_update_scene(self.handle, C.byref(desc)))
+        self.scene, self._desc = scene, desc
+
     @property
     def base_tile(self) -> float:
         return self.info()["base_tile"]

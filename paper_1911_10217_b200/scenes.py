@@ -271,6 +271,35 @@ def maze(n_emitters: int = 1_000_000, n_walls: int = 400, seed: int = 5, *,
     return b.scene(cam, f"maze_{n_emitters}")
 
 
+def _mix64_np(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finalizer on uint64 arrays (wrapping arithmetic)."""
+    x = x + np.uint64(0x9E3779B97F4A7C15)
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def displace_emitters(scene: Scene, frame: int, seed: int = 7, amplitude: float = 0.02) -> Scene:
+    """C4's moving emitters: every emissive triangle of `scene`
+    translated in x and z by amplitude * (u - 1/2), u a counter hash of
+    (seed, frame, emitter index, axis); frame 0 is the scene itself.  Same
+    triangle order, materials and camera, so the result is a valid
+    rlc_context_update_scene input."""
+    if frame == 0:
+        return scene
+    emissive = (scene.materials[:, 3:] @ np.array([0.2126, 0.7152, 0.0722])) > 0
+    idx = np.nonzero(emissive[scene.material_ids])[0]
+    v = scene.vertices.copy()
+    with np.errstate(over="ignore"):
+        base = _mix64_np(np.array([seed], np.uint64))[0] ^ _mix64_np(np.array([frame], np.uint64))[0]
+        key = _mix64_np(np.uint64(base) ^ _mix64_np(np.arange(len(idx), dtype=np.uint64)))
+        ux = (_mix64_np(key ^ np.uint64(1)) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+        uz = (_mix64_np(key ^ np.uint64(2)) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    v[idx, :, 0] += (amplitude * (ux - 0.5))[:, None]
+    v[idx, :, 2] += (amplitude * (uz - 0.5))[:, None]
+    return Scene(v, scene.material_ids, scene.materials, scene.camera, f"{scene.name}_f{frame}")
+
+
 # ---- BASELINE.json configurations (SURVEY 8(d)) ---------------------------
 
 def config_scene(name: str) -> tuple[Scene, dict]:
