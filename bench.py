@@ -42,7 +42,11 @@ WORKLOADS = {
           "4 spp/frame (64 spp over 16 frames), M=128",
     "c3": "c3: procedural maze, 1,000,000 emissive tris, 1920x1080, 1 spp/frame "
           "(64 frames), M=128, hash capacity 65,536",
+    "c4": "c4: maze, 65,536 emissive tris displaced every frame (seeded x/z jitter, "
+          "scenes.displace_emitters) via rlc_context_update_scene (fresh scene BVH and "
+          "emitter records, frozen light tree), 1920x1080, 1 spp/frame, M=128",
 }
+DYNAMIC = {"c4"}  # workloads whose emitters move every frame
 
 
 def env_int(k, d):
@@ -161,18 +165,30 @@ def ncu_traffic(config: str, kernel: str) -> float | None:
 # CPU reference (oracle/_ref: the unmodified reference library)
 # ---------------------------------------------------------------------------
 def cpu_reference_run(scene, cfg, passes: int, warmup: int, min_seconds: float,
-                      downscale: int):
+                      downscale: int, dynamic: bool = False):
     """Times the reference render_pass + end_of_pass_update (workers = all
-    host cores) on the same scene at 1/downscale^2 of the pixels."""
+    host cores) on the same scene at 1/downscale^2 of the pixels; for the
+    dynamic workloads also the per-frame context rebuild (build_context with
+    the frozen light tree, the semantics of rlc_context_update_scene)."""
     import oracle
-    from paper_1911_10217_b200 import rlcuts
+    from paper_1911_10217_b200 import rlcuts, scenes
     cores = os.cpu_count() or 1
     cam = scene.camera
     small = scene.with_resolution(max(cam.width // downscale, 1), max(cam.height // downscale, 1))
     rcfg = rlcuts.RenderConfig(spp=cfg.spp, passes=cfg.passes, sampler=cfg.sampler, cut=cfg.cut,
                                hash=cfg.hash, seed=cfg.seed, workers=cores)
     run = oracle.RefRun(small, rcfg)
+
+    def update(p):
+        if not dynamic or p == 0:
+            return 0.0
+        s = scenes.displace_emitters(small, p)
+        t0 = time.perf_counter()
+        run.update_scene(s)
+        return (time.perf_counter() - t0) * 1e3
+
     for p in range(warmup):
+        update(p)
         run.run_pass(p)
     l0 = run.stats()["lookups"]
     total_ms = 0.0
@@ -180,7 +196,9 @@ def cpu_reference_run(scene, cfg, passes: int, warmup: int, min_seconds: float,
     per_step = []
     for p in range(warmup, warmup + max(passes, 1) + 10000):
         before = run.stats()["lookups"]
+        ums = update(p)
         _, ms = run.run_pass(p)
+        ms += ums
         total_ms += ms
         per_step.append((run.stats()["lookups"] - before, ms))
         done += 1
@@ -203,7 +221,7 @@ def run_reference_arm(args, rank: int, world: int):
     scene, cfg = make_config(args.config)
     value, cores, sample, ms_step, _ = cpu_reference_run(
         scene, cfg, passes=args.steps, warmup=args.warmup, min_seconds=0.0,
-        downscale=args.cpu_downscale)
+        downscale=args.cpu_downscale, dynamic=args.config in DYNAMIC)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -243,12 +261,26 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     grid = rlcuts.HashGrid(ctx, cfg)
     fb = rlcuts.Framebuffer(ctx)
     H = scene.camera.height
+    # dynamic workloads: the per-frame scenes are inputs, built before timing
+    dynamic = args.config in DYNAMIC
+    from paper_1911_10217_b200 import scenes as scn
+    frames = ([scn.displace_emitters(scene, p) for p in range(args.warmup + args.steps)]
+              if dynamic else None)
+    update_ms = [0.0]
+
+    def update(p):
+        if dynamic and p > 0:
+            t = time.perf_counter()
+            ctx.update_scene(frames[p % len(frames)])
+            update_ms[0] += (time.perf_counter() - t) * 1e3
+
     if world == 1:
         r0, r1 = 0, H
         stream = torch.cuda.Stream()
         ctx.set_stream(stream.cuda_stream)
 
         def step(p):
+            update(p)
             rlcuts.render_pass(ctx, cfg, p, grid, fb, sync=False)
             rlcuts.end_of_pass_update(grid, ctx, cfg.cut, sync=False)
     else:
@@ -262,10 +294,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         r0, r1 = frame.rows
 
         def step(p):
+            update(p)
             frame.step(p)
 
     for p in range(args.warmup):
         step(p)
+    update_ms[0] = 0.0
     ctx.synchronize()
     ctx.stage_times()
     ctx.enable_timing(True)
@@ -335,7 +369,26 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # end to end through the C-ABI render_frame: host image out, grid created
     # inside the call (the reference's render_frame, render.cpp:202-240)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and world == 1 and dynamic:
+        # the public API per frame: update_scene (the frame's scene, host ->
+        # device), render_pass, end_of_pass_update, the frame's light-sample
+        # count read back (device -> host)
+        g2, f2 = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+        ctx.set_stream(None)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for p in range(args.steps):
+            ctx.update_scene(frames[p % len(frames)])
+            rlcuts.render_pass(ctx, cfg, p, g2, f2, sync=False)
+            rlcuts.end_of_pass_update(g2, ctx, cfg.cut, sync=False)
+            n_done = g2.lookup_count()
+        wall = time.perf_counter() - t0
+        ntri = scene.num_triangles
+        e2e = {"value": n_done / wall, "unit": UNIT,
+               "h2d_bytes_per_step": 76 * ntri + 48 * scene.materials.shape[0] + 128,
+               "d2h_bytes_per_step": 8, "wall_ms": wall * 1e3,
+               "call": "rlc_context_update_scene + rlc_render_pass + rlc_end_of_pass_update"}
+    elif not args.no_e2e and world == 1:
         ecfg = rlcuts.RenderConfig(spp=args.steps * (cfg.spp // cfg.passes), passes=args.steps,
                                    sampler=cfg.sampler, cut=cfg.cut, hash=cfg.hash, seed=cfg.seed + 1)
         torch.cuda.synchronize()
@@ -353,7 +406,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         try:
             v, cores, sample, _, _ = cpu_reference_run(
                 scene, cfg, passes=2, warmup=1, min_seconds=args.cpu_seconds,
-                downscale=args.cpu_downscale)
+                downscale=args.cpu_downscale, dynamic=args.config in DYNAMIC)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
         except Exception as ex:  # the reference library is test infrastructure
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
@@ -373,6 +426,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
             "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+            "scene_update_ms_per_step": update_ms[0] / args.steps if dynamic else None,
             "context_build_s": build_s,
         }
         print(json.dumps(line), flush=True)

@@ -13,15 +13,19 @@ from paper_1911_10217_b200 import rlcuts, scenes
 from oracle.restate import OracleRun
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-DOWNSCALE = {"c1": 1, "c2": 2, "c3": 4}
+DOWNSCALE = {"c1": 1, "c2": 2, "c3": 4, "c4": 4}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--passes", type=int, default=4)
+    ap.add_argument("--only", nargs="*", default=None, help="configurations to (re)measure")
     args = ap.parse_args()
-    out = {}
+    path = os.path.join(ROOT, "profiles", "traversal_stats.json")
+    out = json.load(open(path)) if args.only and os.path.exists(path) else {}
     for name, ds in DOWNSCALE.items():
+        if args.only and name not in args.only:
+            continue
         scene, st = scenes.config_scene(name)
         scene = scene.with_resolution(scene.camera.width // ds, scene.camera.height // ds)
         spp_pp = st["spp"] // st["passes"]
@@ -39,7 +43,6 @@ def main():
         t["measured_at"] = f"{scene.camera.width}x{scene.camera.height}, {args.passes} passes"
         out[name] = t
         print(name, t)
-    path = os.path.join(ROOT, "profiles", "traversal_stats.json")
     json.dump(out, open(path, "w"), indent=1, sort_keys=True)
     print("wrote", path)
 

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <future>
 #include <numeric>
 #include <cstdlib>
 #include <string>
@@ -403,10 +404,14 @@ std::vector<BvhNode> sah_over_tris(const rlc_scene_desc& d, const HostScene& hs,
 // tree's left-to-right order); child boxes are rounded outward to fp32, taken
 // relative to `origin` when given (x = fl64(c - O)) and then enlarged by
 // |x| * grow + pad before the outward rounding.
+// Leaves get kLeafPure when all their triangles lie in one reference leaf
+// (leaf_of[i]: reference leaf of triangle position i; null: always).
 std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double* origin,
-                                 double grow = 0.0, double pad = 0.0) {
+                                 double grow = 0.0, double pad = 0.0,
+                                 const std::vector<uint32_t>* leaf_of = nullptr) {
   std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
   std::vector<std::array<uint32_t, kWide>> kids;
+  kids.reserve(nodes.size() / 2 + 1);
   std::vector<uint32_t> todo{0};
   std::vector<uint32_t> order;
   while (!todo.empty()) {
@@ -414,22 +419,25 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
     todo.pop_back();
     wid[b] = uint32_t(order.size());
     order.push_back(b);
-    std::vector<uint32_t> L{nodes[b].a, nodes[b].b};
-    while (L.size() < size_t(kWide)) {
+    std::array<uint32_t, kWide> L;
+    L.fill(kWideEmpty);
+    L[0] = nodes[b].a;
+    L[1] = nodes[b].b;
+    int nl = 2;
+    while (nl < kWide) {
       int best = -1;
-      for (size_t k = 0; k < L.size(); ++k)
-        if (nodes[L[k]].count == 0 && (best < 0 || surface(nodes[L[k]]) > surface(nodes[L[size_t(best)]])))
-          best = int(k);
+      for (int k = 0; k < nl; ++k)
+        if (nodes[L[k]].count == 0 && (best < 0 || surface(nodes[L[k]]) > surface(nodes[L[best]])))
+          best = k;
       if (best < 0) break;
-      const uint32_t x = L[size_t(best)];
-      L[size_t(best)] = nodes[x].a;
-      L.insert(L.begin() + best + 1, nodes[x].b);
+      const uint32_t x = L[best];
+      for (int k = nl; k > best + 1; --k) L[k] = L[k - 1];  // keep left-to-right order
+      L[best] = nodes[x].a;
+      L[best + 1] = nodes[x].b;
+      ++nl;
     }
-    std::array<uint32_t, kWide> k4;
-    k4.fill(kWideEmpty);
-    for (size_t k = 0; k < L.size(); ++k) k4[k] = L[k];
-    kids.push_back(k4);
-    for (size_t k = L.size(); k-- > 0;)
+    kids.push_back(L);
+    for (int k = nl; k-- > 0;)
       if (nodes[L[k]].count == 0) todo.push_back(L[k]);
   }
   std::vector<Wide4> wide(order.size());
@@ -453,7 +461,12 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
         n.lo[a][c] = round_down(lo - std::fabs(lo) * grow - pad);
         n.hi[a][c] = round_up(hi + std::fabs(hi) * grow + pad);
       }
-      n.child[c] = bn.count > 0 ? (kWideLeaf | ((bn.count - 1) << 28) | bn.a) : wid[b];
+      bool pure = true;
+      if (bn.count > 0 && leaf_of)
+        for (uint32_t k = 1; k < bn.count; ++k) pure &= (*leaf_of)[bn.a + k] == (*leaf_of)[bn.a];
+      n.child[c] = bn.count > 0 ? (kWideLeaf | ((bn.count - 1) << 28) | (pure ? kLeafPure : 0u) |
+                                   bn.a)
+                                : wid[b];
     }
   }
   return wide;
@@ -467,7 +480,7 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
 //    children in left-to-right order, so the reference's leaf order (right
 //    subtree first) is a plain stack traversal; `wide_cam` (camera-relative
 //    boxes) is filled in with the camera constants.
-void build_wide(const rlc_scene_desc& d, HostScene& out) {
+void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) {
   out.wide.clear();
   out.wide_ref.clear();
   out.tri_leaf.assign(out.tris.size(), 0);
@@ -477,7 +490,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out) {
   out.tris_s = out.tris;
   out.tri_leaf_s = out.tri_leaf;
   if (out.nodes.empty() || out.nodes[0].count > 0) return;
-  if (out.tris.size() >= (1u << 28)) throw InvalidArgument("build_scene_bvh: too many triangles");
+  if (out.tris.size() >= (1u << 27)) throw InvalidArgument("build_scene_bvh: too many triangles");
   // shadow tree: SAH over triangles (default), over the reference leaves
   // (RLC_SHADOW_TREE=leaves) or the reference tree (=reference)
   const char* env = std::getenv("RLC_SHADOW_TREE");
@@ -493,14 +506,51 @@ void build_wide(const rlc_scene_desc& d, HostScene& out) {
   if (mode == "reference" || mode == "leaves") {
     out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
                              S * 0x1.0p-21);
+  } else if (keep != nullptr && !keep->shadow_bin.empty()) {
+    // dynamic update: the creation SAH topology refitted to the moved
+    // triangles (any conservative tree is exact); leaves whose
+    // triangles now lie in different reference leaves lose kLeafPure
+    std::vector<uint32_t> leaf_of_id(out.tris.size());
+    for (size_t j = 0; j < out.tris.size(); ++j) leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j];
+    out.tris_s = keep->tris_s;
+    std::vector<Box> tb(out.tris_s.size());
+    for (size_t i = 0; i < out.tris_s.size(); ++i) {
+      TriAccel& ta = out.tris_s[i];
+      const uint32_t id = ta.tri_id;
+      const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
+      put3(ta.p0, p0);
+      put3(ta.e1, p1 - p0);
+      put3(ta.e2, p2 - p0);
+      out.tri_leaf_s[i] = leaf_of_id[id];
+      tb[i].grow(p0);
+      tb[i].grow(p1);
+      tb[i].grow(p2);
+    }
+    out.shadow_bin = keep->shadow_bin;
+    for (size_t k = out.shadow_bin.size(); k-- > 0;) {  // children follow their parent
+      BvhNode& nd = out.shadow_bin[k];
+      Box b;
+      if (nd.count > 0) {
+        for (uint32_t i = nd.a; i < nd.a + nd.count; ++i) b.grow(tb[i]);
+      } else {
+        const BvhNode &l = out.shadow_bin[nd.a], &r = out.shadow_bin[nd.b];
+        b.grow(V3{l.lo[0], l.lo[1], l.lo[2]});
+        b.grow(V3{l.hi[0], l.hi[1], l.hi[2]});
+        b.grow(V3{r.lo[0], r.lo[1], r.lo[2]});
+        b.grow(V3{r.hi[0], r.hi[1], r.hi[2]});
+      }
+      put3(nd.lo, b.lo);
+      put3(nd.hi, b.hi);
+    }
+    out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s);
   } else {
     std::vector<uint32_t> perm;
-    const std::vector<BvhNode> st = sah_over_tris(d, out, perm);
+    out.shadow_bin = sah_over_tris(d, out, perm);
     for (size_t i = 0; i < perm.size(); ++i) {
       out.tris_s[i] = out.tris[perm[i]];
       out.tri_leaf_s[i] = out.tri_leaf[perm[i]];
     }
-    out.wide = collapse_wide(st, nullptr, 0.0, S * 0x1.0p-21);
+    out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s);
   }
   out.wide_ref = collapse_wide(out.nodes, nullptr);
 }
@@ -644,7 +694,8 @@ void level_thresholds(double out[kMaxLevel + 1]) {
   }
 }
 
-void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, HostScene& out) {
+void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, HostScene& out,
+                      const HostScene* keep) {
   if (d.num_triangles == 0 || d.vertices == nullptr || d.material_ids == nullptr)
     throw InvalidArgument("build_scene_bvh: empty scene");
   if (d.num_materials == 0 || d.materials == nullptr)
@@ -674,66 +725,78 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   }
 
   build_bvh(d, out);  // render.cpp:145
-  build_wide(d, out);
-  out.nodes_f.resize(out.nodes.size());
-  for (size_t i = 0; i < out.nodes.size(); ++i) {
-    const BvhNode& n = out.nodes[i];
-    BvhNodeF& f = out.nodes_f[i];
-    for (int a = 0; a < 3; ++a) {
-      f.lo[a] = round_down(n.lo[a]);
-      f.hi[a] = round_up(n.hi[a]);
+  // The rest depends only on the scene and the reference BVH and writes
+  // disjoint parts of `out`: the traversal trees, the emitters and light
+  // tree, and the camera-relative copies run concurrently.
+  auto f_wide = std::async(std::launch::async, [&] { build_wide(d, out, keep); });
+  auto f_emit = std::async(std::launch::async, [&] {
+    out.nodes_f.resize(out.nodes.size());
+    for (size_t i = 0; i < out.nodes.size(); ++i) {
+      const BvhNode& n = out.nodes[i];
+      BvhNodeF& f = out.nodes_f[i];
+      for (int a = 0; a < 3; ++a) {
+        f.lo[a] = round_down(n.lo[a]);
+        f.hi[a] = round_up(n.hi[a]);
+      }
+      if (n.count > 0) {
+        f.a = kNodeLeaf | n.a;
+        f.b = n.count;
+      } else {
+        if (n.b != n.a + 1) throw std::runtime_error("build_scene_bvh: siblings must be adjacent");
+        f.a = n.a;
+        f.b = 0;
+      }
     }
-    if (n.count > 0) {
-      f.a = kNodeLeaf | n.a;
-      f.b = n.count;
+
+    // collect_emitters (light_tree.cpp:30-42) over derive_emitters order
+    out.lights.clear();
+    out.emitter_tri.clear();
+    out.emitter_energy.clear();
+    out.emitter_centroid.clear();
+    for (uint32_t t = 0; t < d.num_triangles; ++t) {
+      const MatRec& m = out.mats[d.material_ids[t]];
+      if (!m.is_emitter) continue;
+      const V3 p0 = vert(d, t, 0), p1 = vert(d, t, 1), p2 = vert(d, t, 2);
+      const V3 cr = cross(p1 - p0, p2 - p0);
+      const double area = 0.5 * length(cr);
+      const V3 c = (p0 + p1 + p2) / 3.0;
+      LightRec lr{};
+      put3(lr.p0, p0);
+      put3(lr.p1, p1);
+      put3(lr.p2, p2);
+      put3(lr.n, normalize(cr));
+      for (int a = 0; a < 3; ++a) lr.emission[a] = m.emission[a];
+      // sample_triangle_point throws on area <= 0 (scene.cpp:50-51); the
+      // device checks pdf_area <= 0 and raises the same error when drawn.
+      lr.pdf_area = area > 0 ? 1.0 / area : 0.0;
+      out.lights.push_back(lr);
+      out.emitter_tri.push_back(t);
+      out.emitter_energy.push_back(luminance(V3{m.emission[0], m.emission[1], m.emission[2]}) * area);
+      out.emitter_centroid.push_back(c.x);
+      out.emitter_centroid.push_back(c.y);
+      out.emitter_centroid.push_back(c.z);
+    }
+    if (out.lights.empty()) throw InvalidArgument("build_context: scene has no emitters");
+    if (keep) {  // dynamic update: the light tree of the context's creation
+      out.order = keep->order;
+      out.lt_nodes = keep->lt_nodes;
+      out.lt_begin = keep->lt_begin;
+      out.lt_energy = keep->lt_energy;
     } else {
-      if (n.b != n.a + 1) throw std::runtime_error("build_scene_bvh: siblings must be adjacent");
-      f.a = n.a;
-      f.b = 0;
+      build_light_tree(out.emitter_centroid, out.emitter_energy, out.order, out.lt_nodes,
+                       out.lt_begin, out.lt_energy);
     }
-  }
 
-  // collect_emitters (light_tree.cpp:30-42) over derive_emitters order
-  out.lights.clear();
-  out.emitter_tri.clear();
-  out.emitter_energy.clear();
-  out.emitter_centroid.clear();
-  for (uint32_t t = 0; t < d.num_triangles; ++t) {
-    const MatRec& m = out.mats[d.material_ids[t]];
-    if (!m.is_emitter) continue;
-    const V3 p0 = vert(d, t, 0), p1 = vert(d, t, 1), p2 = vert(d, t, 2);
-    const V3 cr = cross(p1 - p0, p2 - p0);
-    const double area = 0.5 * length(cr);
-    const V3 c = (p0 + p1 + p2) / 3.0;
-    LightRec lr{};
-    put3(lr.p0, p0);
-    put3(lr.p1, p1);
-    put3(lr.p2, p2);
-    put3(lr.n, normalize(cr));
-    for (int a = 0; a < 3; ++a) lr.emission[a] = m.emission[a];
-    // sample_triangle_point throws on area <= 0 (scene.cpp:50-51); the
-    // device checks pdf_area <= 0 and raises the same error when drawn.
-    lr.pdf_area = area > 0 ? 1.0 / area : 0.0;
-    out.lights.push_back(lr);
-    out.emitter_tri.push_back(t);
-    out.emitter_energy.push_back(luminance(V3{m.emission[0], m.emission[1], m.emission[2]}) * area);
-    out.emitter_centroid.push_back(c.x);
-    out.emitter_centroid.push_back(c.y);
-    out.emitter_centroid.push_back(c.z);
-  }
-  if (out.lights.empty()) throw InvalidArgument("build_context: scene has no emitters");
-  build_light_tree(out.emitter_centroid, out.emitter_energy, out.order, out.lt_nodes,
-                   out.lt_begin, out.lt_energy);
+    out.energy_cdf.resize(out.emitter_energy.size());  // estimators.cpp:12-26
+    double run = 0;
+    for (size_t i = 0; i < out.emitter_energy.size(); ++i) {
+      run += out.emitter_energy[i];
+      out.energy_cdf[i] = run;
+    }
+    if (!(out.energy_cdf.back() > 0))
+      throw InvalidArgument("build_energy_cdf: total emitter energy must be positive");
 
-  out.energy_cdf.resize(out.emitter_energy.size());  // estimators.cpp:12-26
-  double run = 0;
-  for (size_t i = 0; i < out.emitter_energy.size(); ++i) {
-    run += out.emitter_energy[i];
-    out.energy_cdf[i] = run;
-  }
-  if (!(out.energy_cdf.back() > 0))
-    throw InvalidArgument("build_energy_cdf: total emitter energy must be positive");
-
+  });
   const V3 ext = V3{out.scene_hi[0], out.scene_hi[1], out.scene_hi[2]} -
                  V3{out.scene_lo[0], out.scene_lo[1], out.scene_lo[2]};
   out.base_tile = cfg.hash.base_tile > 0 ? cfg.hash.base_tile : length(ext) / 256.0;
@@ -765,18 +828,25 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   // Camera-relative copy for the primary rays, whose origin is exactly the
   // camera origin O: the reference's per-axis term fl64(c - O) rounded
   // outward to fp32, so every fp32 error of the decision test is relative.
-  out.nodes_cam = out.nodes_f;
-  for (size_t i = 0; i < out.nodes.size(); ++i)
+  out.nodes_cam.resize(out.nodes.size());
+  for (size_t i = 0; i < out.nodes.size(); ++i) {
+    const BvhNode& n = out.nodes[i];
+    BvhNodeF& f = out.nodes_cam[i];
     for (int a = 0; a < 3; ++a) {
-      out.nodes_cam[i].lo[a] = round_down(out.nodes[i].lo[a] - cam.origin[a]);
-      out.nodes_cam[i].hi[a] = round_up(out.nodes[i].hi[a] - cam.origin[a]);
+      f.lo[a] = round_down(n.lo[a] - cam.origin[a]);
+      f.hi[a] = round_up(n.hi[a] - cam.origin[a]);
     }
+    f.a = n.count > 0 ? (kNodeLeaf | n.a) : n.a;
+    f.b = n.count > 0 ? n.count : 0;
+  }
   // The wide copy for camera rays is enlarged by 2^-21 |x| per coordinate,
   // more than the whole relative gap between fl32(x' * fl32(inv)) and the
   // reference's fl64(x * inv) (< 2^-23): its plain slab test is conservative
   // (DESIGN.md 5.4).
   out.wide_cam.clear();
-  if (!out.wide_ref.empty()) out.wide_cam = collapse_wide(out.nodes, cam.origin, 0x1.0p-21);
+  if (out.nodes[0].count == 0) out.wide_cam = collapse_wide(out.nodes, cam.origin, 0x1.0p-21);
+  f_wide.get();
+  f_emit.get();
 }
 
 }  // namespace rlc

@@ -36,6 +36,7 @@ struct HostScene {
   std::vector<double> mat_values; // the scene's materials [m*6] (albedo, emission)
   std::vector<TriAccel> tris_s;   // triangles in the shadow tree's leaf order
   std::vector<uint32_t> tri_leaf_s; // reference leaf node per tris_s entry
+  std::vector<BvhNode> shadow_bin;  // binary SAH tree behind `wide` (leaves: tris_s ranges)
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;
   // materials / triangles
@@ -59,7 +60,10 @@ struct HostScene {
 
 // Whole-context build (proj/src/render.cpp:143-157).  Throws InvalidArgument
 // with the reference's messages for empty scenes / no emitters.
-void build_host_scene(const rlc_scene_desc& desc, const rlc_render_config& cfg, HostScene& out);
+// With `keep` (rlc_context_update_scene): the light tree is copied from it
+// and the shadow tree's topology refitted instead of rebuilt.
+void build_host_scene(const rlc_scene_desc& desc, const rlc_render_config& cfg, HostScene& out,
+                      const HostScene* keep = nullptr);
 
 // Light tree alone over emitter centroids/energies (light_tree.cpp:56-119),
 // exposed for the unit-level entry points.

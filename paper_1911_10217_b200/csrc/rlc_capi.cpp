@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -94,6 +95,42 @@ struct DeviceArena {
   ~DeviceArena() { release(); }
 };
 
+// The scene arrays of a context: one device buffer per array, in the fixed
+// order of upload_scene, reused by rlc_context_update_scene while the new
+// contents fit (a frame's arrays have nearly the same sizes), so a scene
+// update is a copy, not a reallocation.
+struct SceneBuffers {
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  std::vector<Buf> bufs;
+  size_t next = 0;
+  uint64_t bytes = 0;
+  void begin() { next = 0; }
+  template <class T>
+  T* put(const std::vector<T>& v) {
+    if (next == bufs.size()) bufs.emplace_back();
+    Buf& b = bufs[next++];
+    const size_t need = v.size() * sizeof(T) > 0 ? v.size() * sizeof(T) : 16;
+    if (need > b.cap) {
+      if (b.p) RLC_CK(cudaFree(b.p));
+      b.p = nullptr;
+      bytes -= b.cap;
+      const size_t cap = need + need / 8;  // headroom for the next frame
+      RLC_CK(cudaMalloc(&b.p, cap));
+      b.cap = cap;
+      bytes += cap;
+    }
+    if (!v.empty()) RLC_CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return static_cast<T*>(b.p);
+  }
+  ~SceneBuffers() {
+    for (Buf& b : bufs)
+      if (b.p) cudaFree(b.p);
+  }
+};
+
 void check_device(int device) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -170,6 +207,7 @@ struct rlc_context {
   rlc::HostScene host;
   rlc::DevScene dev{};
   rlc_render_config create_cfg{};  // build_context's config (rlc_context_update_scene)
+  SceneBuffers scene_bufs;  // the device scene (upload_scene)
   DeviceArena arena;
   unsigned long long* counters = nullptr;  // error bits for grid-less passes
   // primary rays of the next pass overlap the tail of the current one: they
@@ -448,25 +486,29 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
 }
 
 // Uploads the device view of a host scene into arena A.
-void upload_scene(const rlc::HostScene& h, DeviceArena& A, rlc::DevScene& d) {
-  d.nodes = A.upload(h.nodes);
-  d.nodes_f = A.upload(h.nodes_f);
-  d.nodes_cam = A.upload(h.nodes_cam);
-  d.wide = h.wide.empty() ? nullptr : A.upload(h.wide);
-  d.wide_ref = h.wide_ref.empty() ? nullptr : A.upload(h.wide_ref);
-  d.wide_cam = h.wide_cam.empty() ? nullptr : A.upload(h.wide_cam);
-  d.tri_leaf = A.upload(h.tri_leaf);
-  d.tris_s = A.upload(h.tris_s);
-  d.tri_leaf_s = A.upload(h.tri_leaf_s);
-  d.tris = A.upload(h.tris);
-  d.mats = A.upload(h.mats);
-  d.tri_mat = A.upload(h.tri_mat);
-  d.tri_normal = A.upload(h.tri_normal);
-  d.lights = A.upload(h.lights);
-  d.order = A.upload(h.order);
-  d.lt = A.upload(h.lt_nodes);
-  d.energy_cdf = A.upload(h.energy_cdf);
-  d.emitter_energy = A.upload(h.emitter_energy);
+void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d) {
+  A.begin();
+  d.nodes = A.put(h.nodes);
+  d.nodes_f = A.put(h.nodes_f);
+  d.nodes_cam = A.put(h.nodes_cam);
+  d.wide = A.put(h.wide);
+  d.wide_ref = A.put(h.wide_ref);
+  d.wide_cam = A.put(h.wide_cam);
+  if (h.wide.empty()) d.wide = nullptr;
+  if (h.wide_ref.empty()) d.wide_ref = nullptr;
+  if (h.wide_cam.empty()) d.wide_cam = nullptr;
+  d.tri_leaf = A.put(h.tri_leaf);
+  d.tris_s = A.put(h.tris_s);
+  d.tri_leaf_s = A.put(h.tri_leaf_s);
+  d.tris = A.put(h.tris);
+  d.mats = A.put(h.mats);
+  d.tri_mat = A.put(h.tri_mat);
+  d.tri_normal = A.put(h.tri_normal);
+  d.lights = A.put(h.lights);
+  d.order = A.put(h.order);
+  d.lt = A.put(h.lt_nodes);
+  d.energy_cdf = A.put(h.energy_cdf);
+  d.emitter_energy = A.put(h.emitter_energy);
   d.num_lights = uint32_t(h.lights.size());
   d.num_tris = uint32_t(h.tri_mat.size());
   d.fp32_ok = 1;
@@ -523,7 +565,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     ctx->device = device;
     ctx->create_cfg = *config;
     rlc::build_host_scene(*scene, *config, ctx->host);
-    upload_scene(ctx->host, ctx->arena, ctx->dev);
+    upload_scene(ctx->host, ctx->scene_bufs, ctx->dev);
     ctx->counters = ctx->arena.alloc<unsigned long long>(rlc::kCntNum);
     RLC_CK(cudaMemset(ctx->counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
@@ -562,25 +604,27 @@ rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scen
       require(scene->materials[i] == old.mat_values[i],
               "rlc_context_update_scene: materials must not change");
     RLC_CK(cudaSetDevice(ctx->device));
+    const bool report = std::getenv("RLC_UPDATE_TIMING") != nullptr;
+    auto t = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!report) return;
+      const auto n = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "update_scene %s %.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(n - t).count());
+      t = n;
+    };
     // build_context(scene) (render.cpp:143-157) with the light tree of the
     // context's creation: same emitter order, topology and node energies
     rlc::HostScene h;
-    rlc::build_host_scene(*scene, ctx->create_cfg, h);
-    h.order = old.order;
-    h.lt_nodes = old.lt_nodes;
-    h.lt_begin = old.lt_begin;
-    h.lt_energy = old.lt_energy;
-    DeviceArena A;
+    rlc::build_host_scene(*scene, ctx->create_cfg, h, &old);
+    lap("host build");
+    ctx->sync_all();  // the previous frame's kernels read the buffers
+    lap("sync");
     rlc::DevScene d{};
-    upload_scene(h, A, d);
-    unsigned long long* counters = A.alloc<unsigned long long>(rlc::kCntNum);
-    RLC_CK(cudaMemset(counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
-    ctx->sync_all();
-    std::swap(ctx->arena.ptrs, A.ptrs);
-    std::swap(ctx->arena.bytes, A.bytes);
+    upload_scene(h, ctx->scene_bufs, d);
     ctx->dev = d;
-    ctx->counters = counters;
     ctx->host = std::move(h);
+    lap("upload");
   });
 }
 
@@ -606,7 +650,7 @@ rlc_status rlc_context_info_get(const rlc_context* ctx, rlc_context_info* info) 
     info->light_tree_nodes = uint32_t(ctx->host.lt_nodes.size());
     info->base_tile = ctx->host.base_tile;
     info->shadow_eps = ctx->host.shadow_eps;
-    info->device_bytes = ctx->arena.bytes + ctx->scratch.bytes;
+    info->device_bytes = ctx->arena.bytes + ctx->scene_bufs.bytes + ctx->scratch.bytes;
   });
 }
 

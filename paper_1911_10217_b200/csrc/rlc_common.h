@@ -100,6 +100,7 @@ struct alignas(32) BvhNodeF {
 // fp64 test ("Exact any-hit on a conservative wide BVH").
 constexpr uint32_t kWideLeaf = 0x80000000u;  // child: leaf flag
 constexpr uint32_t kWideEmpty = 0xffffffffu; // child: unused slot
+constexpr uint32_t kLeafPure = 0x08000000u;  // leaf: all triangles in one reference leaf
 #ifndef RLC_WIDE
 #define RLC_WIDE 4
 #endif
@@ -107,7 +108,8 @@ constexpr int kWide = RLC_WIDE;  // children per node (4 or 8)
 struct alignas(128) Wide4 {
   float lo[3][kWide];  // [axis][child]
   float hi[3][kWide];
-  uint32_t child[kWide];  // internal: node index; leaf: kWideLeaf | (count - 1) << 28 | first tri
+  uint32_t child[kWide];  // internal: node index; leaf: kWideLeaf | (count - 1) << 28 |
+                          // kLeafPure? | first tri (27 bits)
   uint32_t pad[kWide == 8 ? 8 : 4];
 };
 static_assert(sizeof(Wide4) % 128 == 0, "wide nodes are whole 128-byte lines");

@@ -811,9 +811,11 @@ constexpr int kShadowThreads = 128;
 constexpr int kShadowStack = kWide == 8 ? 64 : 32;  // per-lane stack entries (shared memory)
 constexpr uint32_t kDone = 0x7fffffffu;  // traversal finished (no leaf flag)
 
-// Leaf entries: kWideLeaf | kLeafVerified? | (count - 1) << 28 | first tri.
+// Leaf entries: kWideLeaf | kLeafVerified? | (count - 1) << 28 | kLeafPure? |
+// first tri (27 bits).  kLeafVerified (set during traversal) is only ever set
+// on pure leaves, whose box lies inside their reference leaf's box.
 constexpr uint32_t kLeafVerified = 0x40000000u;
-__device__ __forceinline__ uint32_t leaf_first(uint32_t e) { return e & 0x0fffffffu; }
+__device__ __forceinline__ uint32_t leaf_first(uint32_t e) { return e & 0x07ffffffu; }
 __device__ __forceinline__ uint32_t leaf_count(uint32_t e) { return ((e >> 28) & 3u) + 1u; }
 
 // Exact acceptance of a triangle found through the conservative wide tree.
@@ -1051,7 +1053,7 @@ __device__ __forceinline__ bool closest_wide(const DevScene& sc, const Wide4* __
       for (int k = 0; k < kWide; ++k) {  // left to right: the rightmost is popped first
         if (!((m >> k) & 1u) || c[k] == kWideEmpty) continue;
         uint32_t e = c[k];
-        if ((e & kWideLeaf) && ((mi >> k) & 1u)) e |= kLeafVerified;
+        if ((e & kWideLeaf) && (e & kLeafPure) && ((mi >> k) & 1u)) e |= kLeafVerified;
         stack[sp++] = e;
       }
     }
@@ -1238,7 +1240,8 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
 #pragma unroll
       for (int k = 0; k < kWide; ++k) {
         if (c[k] == kWideEmpty) m &= ~(1u << k);
-        if ((mi >> k) & (c[k] >> 31)) c[k] |= kLeafVerified;  // leaf proven reached
+        if (((mi >> k) & (c[k] >> 31)) && (c[k] & kLeafPure))
+          c[k] |= kLeafVerified;  // leaf proven reached
         if (!(m & (1u << k))) tn[k] = HUGE_VALF;
       }
       if (sp + kWide - 1 > kShadowStack) {
@@ -1284,8 +1287,15 @@ __global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
     bool hit = false;
     while (leaf != 0) {
       const uint32_t first = leaf_first(leaf), cnt = leaf_count(leaf);
-      for (uint32_t i = first; i < first + cnt; ++i) hit |= tri_any(sc.tris_s, i, o, d, tmin, tmax);
-      if (hit) hit = leaf_reached(sc, leaf, o, inv, tmin, tmax);
+      if (leaf & kLeafPure) {  // one reference leaf: one exact test for the leaf
+        for (uint32_t i = first; i < first + cnt; ++i)
+          hit |= tri_any(sc.tris_s, i, o, d, tmin, tmax);
+        if (hit) hit = leaf_reached(sc, leaf, o, inv, tmin, tmax);
+      } else {  // a refitted leaf spanning reference leaves: test each hit's own
+        for (uint32_t i = first; i < first + cnt && !hit; ++i)
+          hit = tri_any(sc.tris_s, i, o, d, tmin, tmax) &&
+                box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf_s + i)), o, inv, tmin, tmax);
+      }
       if (hit) break;
       if (cur != kDone && (cur & kWideLeaf)) {
         leaf = cur;
