@@ -550,7 +550,10 @@ __device__ __forceinline__ void warp_lookup(const DevGrid& g, bool need, const K
   }
 }
 
-__global__ void __launch_bounds__(128) k_primary(DevScene sc, DevGrid g, PassParams P,
+#ifndef RLC_PRIMARY_BLOCKS
+#define RLC_PRIMARY_BLOCKS 8  // blocks per SM (64 registers): measured best on c3
+#endif
+__global__ void __launch_bounds__(128, RLC_PRIMARY_BLOCKS) k_primary(DevScene sc, DevGrid g, PassParams P,
                                                  GBuf* __restrict__ gbuf) {
   const uint32_t rows = P.n / (P.width * P.spp_pp);
   uint32_t idx, px, py, s;
