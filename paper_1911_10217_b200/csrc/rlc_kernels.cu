@@ -1139,7 +1139,10 @@ __device__ __forceinline__ void mark_occluded(SampleRec* srec, uint32_t idx) {
 // lane that reaches a leaf postpones it while other lanes still have node
 // steps to do (speculative traversal, Aila & Laine 2009), so both phases run
 // with as many lanes as possible.
-__global__ void __launch_bounds__(kShadowThreads, 7) k_shadow(DevScene sc,
+#ifndef RLC_SHADOW_BLOCKS
+#define RLC_SHADOW_BLOCKS 7  // minimum resident blocks per SM (register budget)
+#endif
+__global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(DevScene sc,
                                                            const ShadowRay* __restrict__ rays,
                                                            const uint32_t* __restrict__ order,
                                                            unsigned int* __restrict__ ray_count,
