@@ -121,6 +121,11 @@ void Session::render_pass(uint32_t pass_index) {
   check(rlc_render_pass(impl_->c, &impl_->cfg, pass_index, impl_->g, impl_->fb));
 }
 
+void Session::update_scene(const Scene& scene) {
+  SceneArrays arrays(scene);
+  check(rlc_context_update_scene(impl_->c, &arrays.desc));
+}
+
 uint32_t Session::end_of_pass_update() {
   if (impl_->g == nullptr) return 0;
   uint32_t changes = 0;
@@ -161,25 +166,45 @@ RenderResult render_frame(const RenderContext& ctx, const RenderConfig& config,
                           const Image* reference) {
   if (config.passes == 0 || config.spp == 0 || config.spp % config.passes != 0)
     throw std::invalid_argument("render_frame: spp must be divisible by passes");
-  const auto t0 = std::chrono::steady_clock::now();
-  Session s(ctx, config);
-  Framebuffer fb(ctx.scene->camera.width, ctx.scene->camera.height);
-  RenderResult result;
-  for (uint32_t pass = 0; pass < config.passes; ++pass) {
-    s.render_pass(pass);
-    result.sc_changes.push_back(s.end_of_pass_update());
-    if (reference != nullptr) {  // per-pass MSE needs the running image on the host
-      s.framebuffer(fb);
-      result.pass_mse.push_back(mse(fb.resolve(), *reference));
+  if (ctx.scene == nullptr) throw std::invalid_argument("render_frame: context without a scene");
+  rlc_render_config cfg = to_c(config);
+  cfg.hash.base_tile = ctx.base_tile;  // resolved by build_context (render.cpp:153-155)
+  SceneArrays arrays(*ctx.scene);
+  rlc_context* c = nullptr;
+  check(rlc_context_create(&arrays.desc, &cfg, 0, &c));
+  struct Guard {
+    rlc_context* c;
+    ~Guard() { rlc_context_destroy(c); }
+  } guard{c};
+  const int w = ctx.scene->camera.width, h = ctx.scene->camera.height;
+  std::vector<double> img(size_t(w) * size_t(h) * 3);
+  std::vector<uint32_t> changes(config.passes);
+  std::vector<double> pass_mse(config.passes);
+  rlc_render_result r{};
+  r.sc_changes = changes.data();
+  if (reference != nullptr) {  // scored after every pass on the device path
+    std::vector<double> ref;
+    ref.reserve(reference->pixels.size() * 3);
+    for (const Vec3& p : reference->pixels) {
+      ref.push_back(p.x);
+      ref.push_back(p.y);
+      ref.push_back(p.z);
     }
+    check(rlc_render_frame_scored(c, &cfg, ref.data(), reference->width, reference->height,
+                                  img.data(), &r, pass_mse.data()));
+  } else {
+    check(rlc_render_frame(c, &cfg, img.data(), &r));
   }
-  s.framebuffer(fb);
-  result.image = fb.resolve();
-  result.occupied_cells = s.occupied_count();
-  result.lookups = s.lookup_count();
-  result.fallback_hits = s.fallback_hits();
-  result.wall_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  RenderResult result;
+  result.image = Image(w, h);
+  for (size_t i = 0; i < result.image.pixels.size(); ++i)
+    result.image.pixels[i] = Vec3{img[3 * i], img[3 * i + 1], img[3 * i + 2]};
+  result.wall_ms = r.wall_ms;
+  result.occupied_cells = r.occupied_cells;
+  result.lookups = r.lookups;
+  result.fallback_hits = r.fallback_hits;
+  result.sc_changes = changes;
+  if (reference != nullptr) result.pass_mse = pass_mse;
   return result;
 }
 

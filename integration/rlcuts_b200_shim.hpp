@@ -33,6 +33,10 @@ class Session {
 
   void render_pass(uint32_t pass_index);   // render_pass
   uint32_t end_of_pass_update();           // end_of_pass_update
+  // Dynamic emitters (rlc_context_update_scene): render `scene` from now on
+  // as build_context(scene) would, keeping the light tree of the session's
+  // creation so the learned cuts stay valid.  Same triangles and materials.
+  void update_scene(const Scene& scene);
   void framebuffer(Framebuffer& out) const;
   uint32_t occupied_count() const;
   uint64_t lookup_count() const;
