@@ -213,6 +213,8 @@ struct rlc_context {
   // primary rays of the next pass overlap the tail of the current one: they
   // run on `pstream` into the other G-buffer slot
   cudaStream_t pstream = nullptr;
+  cudaStream_t sstream = nullptr;  // the update-record sort beside the shadow rays
+  cudaEvent_t ev_sample_done = nullptr, ev_sort_done = nullptr;
   bool overlap = false;  // RLC_OVERLAP=1: primary rays of the next pass on a side stream
   cudaEvent_t ev_prim_done = nullptr;
   cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
@@ -220,6 +222,7 @@ struct rlc_context {
   void sync_all() {
     RLC_CK(cudaStreamSynchronize(stream));
     if (pstream) RLC_CK(cudaStreamSynchronize(pstream));
+    if (sstream) RLC_CK(cudaStreamSynchronize(sstream));
   }
   // per-stage CUDA-event timing (rlc_context_enable_timing)
   bool timing = false;
@@ -258,6 +261,9 @@ struct rlc_context {
   ~rlc_context() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (ev_prim_done) cudaEventDestroy(ev_prim_done);
+    if (ev_sample_done) cudaEventDestroy(ev_sample_done);
+    if (ev_sort_done) cudaEventDestroy(ev_sort_done);
+    if (sstream) cudaStreamDestroy(sstream);
     for (cudaEvent_t e : ev_gbuf_free)
       if (e) cudaEventDestroy(e);
     if (pstream) cudaStreamDestroy(pstream);
@@ -308,6 +314,7 @@ struct rlc_context {
     gslot[1] = scratch.alloc<rlc::GBuf>(cap);
     pb.gbuf = gslot[0];
     pb.srec = scratch.alloc<rlc::SampleRec>(cap);
+    pb.rflag = scratch.alloc<uint8_t>(cap);
     pb.keys = scratch.alloc<uint32_t>(cap);
     pb.vals = scratch.alloc<uint32_t>(cap);
     pb.keys_alt = scratch.alloc<uint32_t>(cap);
@@ -435,17 +442,27 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   for (uint32_t d = 2; d <= S.p.depth; ++d)
     ctx->stage(0, [&] { rlc::launch_bounce(ctx->dev, S.g, S.p, d, ctx->pb, st); });
   ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, S.g, S.p, ctx->pb, st); });
-  // Shadow rays are traced in sorted (cell, cluster) order: rays of one cell
-  // toward one cut cluster share most of their BVH path.  The any-hit result
-  // does not depend on the order.
+  // The update records are sorted by (cell, cluster) for the fold on the
+  // side stream while the shadow rays are traced, in canonical (pixel)
+  // order: neighbouring pixels give coherent origins, and on the
+  // triangle-level shadow tree that beats the sorted order (0.55 vs 0.62 ms
+  // on c3).  The any-hit result does not depend on the order.
   *k = nullptr;
   *v = nullptr;
-  if (S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS)
-    ctx->stage(2, [&] { rlc::launch_sort(ctx->pb, S.nv, grid->key_bits, st, k, v); });
+  const bool rl = S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
+  if (rl) {
+    RLC_CK(cudaEventRecord(ctx->ev_sample_done, st));
+    RLC_CK(cudaStreamWaitEvent(ctx->sstream, ctx->ev_sample_done, 0));
+    ctx->stage_on(ctx->sstream, 2, [&] {
+      rlc::launch_sort(ctx->pb, S.nv, grid->key_bits, ctx->sstream, k, v);
+    });
+    RLC_CK(cudaEventRecord(ctx->ev_sort_done, ctx->sstream));
+  }
   ctx->stage(6, [&] {
-    rlc::launch_ray_compact(ctx->pb, *v, S.nv, st);
-    rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, S.g.counters, st);
+    rlc::launch_ray_compact(ctx->pb, nullptr, S.nv, st);
+    rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, S.g.counters, st, rl);
   });
+  if (rl) RLC_CK(cudaStreamWaitEvent(st, ctx->ev_sort_done, 0));
 }
 
 // render_pass body (proj/src/render.cpp:159-183) for rows [r0, r1).
@@ -573,6 +590,9 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     RLC_CK(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking));
     if (const char* e = std::getenv("RLC_OVERLAP")) ctx->overlap = std::string(e) == "1";
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_prim_done, cudaEventDisableTiming));
+    RLC_CK(cudaStreamCreateWithFlags(&ctx->sstream, cudaStreamNonBlocking));
+    RLC_CK(cudaEventCreateWithFlags(&ctx->ev_sample_done, cudaEventDisableTiming));
+    RLC_CK(cudaEventCreateWithFlags(&ctx->ev_sort_done, cudaEventDisableTiming));
     for (cudaEvent_t& e : ctx->ev_gbuf_free) {
       RLC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       RLC_CK(cudaEventRecord(e, ctx->stream));
@@ -634,6 +654,7 @@ rlc_status rlc_context_destroy(rlc_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
+    if (ctx->sstream) cudaStreamSynchronize(ctx->sstream);
     rlc_grid_destroy(ctx->frame_grid);
     rlc_framebuffer_destroy(ctx->frame_fb);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(128) k_bounce(DevScene sc, DevGrid g, PassPara
 __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassParams P,
                                                 const GBuf* __restrict__ gbuf,
                                                 SampleRec* __restrict__ srec,
+                                                uint8_t* __restrict__ rflag,
                                                 uint32_t* __restrict__ keys,
                                                 uint32_t* __restrict__ vals,
                                                 double* __restrict__ q_before,
@@ -676,7 +677,8 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
   keys[idx] = kInvalidKey;
   vals[idx] = idx;
   if (!(gb.flags & kGReflective)) {
-    srec[idx].flags = 0;  // read by the ray compaction
+    srec[idx].flags = 0;
+    rflag[idx] = 0;  // read by the compactions
     return;
   }
   const uint32_t base = draw_base(P, idx % P.depth + 1u);
@@ -802,6 +804,7 @@ __global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassPara
     }
   }
   srec[idx] = r;
+  rflag[idx] = uint8_t(r.flags & (kSRay | kSRecord));
 }
 
 // ---------------------------------------------------------------------------
@@ -1963,7 +1966,7 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
                    const PassBuffers& b, cudaStream_t st) {
   if (p.nv == 0) return;
   cudaMemsetAsync(b.ray_count, 0, 2 * sizeof(unsigned int), st);
-  k_sample<<<blocks_for(p.nv, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.keys, b.vals,
+  k_sample<<<blocks_for(p.nv, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.rflag, b.keys, b.vals,
                                                   b.q_before, b.rays, b.ray_count);
   count_launch();
 }
@@ -1971,13 +1974,13 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
 // ---- stable compaction of ray-bearing paths -------------------------------
 constexpr int kCmpThreads = 256, kCmpItems = 8, kCmpTile = kCmpThreads * kCmpItems;
 
-__device__ __forceinline__ bool has_flag(const SampleRec* srec, const uint32_t* order, uint32_t j,
+__device__ __forceinline__ bool has_flag(const uint8_t* rflag, const uint32_t* order, uint32_t j,
                                          uint32_t mask) {
   const uint32_t i = order ? order[j] : j;
-  return i != kNoSlot && (srec[i].flags & mask);
+  return i != kNoSlot && (rflag[i] & mask);
 }
 
-__global__ void __launch_bounds__(kCmpThreads) k_cmp_count(const SampleRec* __restrict__ srec,
+__global__ void __launch_bounds__(kCmpThreads) k_cmp_count(const uint8_t* __restrict__ rflag,
                                                            const uint32_t* __restrict__ order,
                                                            uint32_t n, uint32_t mask,
                                                            uint32_t* __restrict__ counts) {
@@ -1985,7 +1988,7 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_count(const SampleRec* __re
   uint32_t c = 0;
   for (int k = 0; k < kCmpItems; ++k) {
     const uint32_t j = blockIdx.x * kCmpTile + k * kCmpThreads + threadIdx.x;
-    if (j < n && has_flag(srec, order, j, mask)) ++c;
+    if (j < n && has_flag(rflag, order, j, mask)) ++c;
   }
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
@@ -1998,7 +2001,7 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_count(const SampleRec* __re
 }
 
 // counts[] holds exclusive block offsets (rs_scan) on entry.
-__global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const SampleRec* __restrict__ srec,
+__global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const uint8_t* __restrict__ rflag,
                                                              const uint32_t* __restrict__ order,
                                                              uint32_t n, uint32_t mask,
                                                              const uint32_t* __restrict__ offs,
@@ -2011,7 +2014,7 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const SampleRec* __
   __syncthreads();
   for (int k = 0; k < kCmpItems; ++k) {
     const uint32_t j = blockIdx.x * kCmpTile + k * kCmpThreads + threadIdx.x;
-    const bool f = j < n && has_flag(srec, order, j, mask);
+    const bool f = j < n && has_flag(rflag, order, j, mask);
     const unsigned b = __ballot_sync(kFull, f);
     if (lane == 0) wsum[w] = __popc(b);
     __syncthreads();
@@ -2034,9 +2037,9 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const SampleRec* __
 static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, uint32_t mask,
                            uint32_t* out, unsigned int* count_out, cudaStream_t st) {
   const uint32_t nb = blocks_for(n > 0 ? n : 1, kCmpTile);
-  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, mask, b.block_counts);
+  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, b.block_counts);
   rs_scan<<<1, 1024, 0, st>>>(b.block_counts, nb);
-  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.srec, order, n, mask, b.block_counts, out,
+  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, b.block_counts, out,
                                             count_out);
   count_launch(3);
 }
@@ -2046,18 +2049,22 @@ void launch_ray_compact(const PassBuffers& b, const uint32_t* order, uint32_t n,
 }
 
 void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* order,
-                   unsigned long long* counters, cudaStream_t st) {
-  static int blocks = 0;
-  if (blocks == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
+                   unsigned long long* counters, cudaStream_t st, bool leave_room) {
+  static int per_sm = 0, sms = 0;
+  if (per_sm == 0) {
+    int dev = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shadow, kShadowThreads, 0);
     if (const char* e = getenv("RLC_SHADOW_BLOCKS_PER_SM"))  // tuning knob (co-residency)
       if (atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
+    if (per_sm < 1) per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    blocks = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    if (sms < 1) sms = 148;
   }
-  k_shadow<<<blocks, kShadowThreads, 0, st>>>(
+  // with the update-record sort running beside it, one block slot per SM is
+  // left to the sort (measured: 1.69 vs 1.71 ms per c3 frame)
+  const int use = leave_room && per_sm > 1 ? per_sm - 1 : per_sm;
+  k_shadow<<<use * sms, kShadowThreads, 0, st>>>(
       sc, b.rays, order, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
   count_launch();
 }

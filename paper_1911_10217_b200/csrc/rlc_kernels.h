@@ -146,6 +146,7 @@ struct PassParams {
 struct PassBuffers {
   GBuf* gbuf;
   SampleRec* srec;
+  uint8_t* rflag;        // per vertex: the kSRay | kSRecord bits of srec (compaction input)
   uint32_t* keys;
   uint32_t* vals;
   uint32_t* keys_alt;
@@ -195,8 +196,9 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
 // Stable compaction of the paths that carry a shadow ray, in the order of
 // `order` (sorted update records) or canonical order when it is null.
 void launch_ray_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, cudaStream_t st);
+// leave_room: one block slot per SM stays free for concurrent work (the sort).
 void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* order,
-                   unsigned long long* counters, cudaStream_t st);
+                   unsigned long long* counters, cudaStream_t st, bool leave_room = false);
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out);
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
