@@ -363,8 +363,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "bytes_per_unit": pk["bytes_per_unit"], "unit_of_work": pk["unit_of_work"],
                 "units_per_launch": pk["units_per_launch"], "avg_launch_ms": pk["avg_launch_ms"],
                 "per_kernel": per_kernel,
-                "note": "algorithmic bytes use the reference BVH traversal counts; most are "
-                        "served by L1/L2, so frac > 1 is possible (BASELINE.md 3)"}
+                "note": "achieved = algorithmic bytes with the reference BVH's node/triangle "
+                        "counts per ray (SURVEY 8(d)); our trees serve them mostly from L1/L2 "
+                        "or skip them, so frac > 1; dram_achieved = ncu DRAM bytes per launch "
+                        "(traffic) / live launch time (profiles/r01_ncu_summary.md)"}
+        tr = roof["traffic"]
+        if tr:
+            roof["dram_achieved"] = tr / (pk["avg_launch_ms"] / 1e3) / 1e9
+            roof["dram_frac"] = roof["dram_achieved"] / peak
 
     # end to end through the C-ABI render_frame: host image out, grid created
     # inside the call (the reference's render_frame, render.cpp:202-240)
