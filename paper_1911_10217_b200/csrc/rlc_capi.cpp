@@ -213,8 +213,18 @@ struct rlc_context {
   // primary rays of the next pass overlap the tail of the current one: they
   // run on `pstream` into the other G-buffer slot
   cudaStream_t pstream = nullptr;
-  cudaStream_t sstream = nullptr;  // the update-record sort beside the shadow rays
+  cudaStream_t sstream = nullptr;  // the record sort beside the shadow rays, the
+                                   // framebuffer accumulation beside split-collapse
   cudaEvent_t ev_sample_done = nullptr, ev_sort_done = nullptr;
+  cudaEvent_t ev_fold_done = nullptr, ev_acc_done = nullptr;
+  bool acc_pending = false;  // an accumulation on sstream the main stream has not joined
+  // Orders every later main-stream operation after the side-stream
+  // accumulation (framebuffer and pass-buffer readers/writers call this).
+  void join_acc() {
+    if (!acc_pending) return;
+    RLC_CK(cudaStreamWaitEvent(stream, ev_acc_done, 0));
+    acc_pending = false;
+  }
   bool overlap = false;  // RLC_OVERLAP=1: primary rays of the next pass on a side stream
   cudaEvent_t ev_prim_done = nullptr;
   cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
@@ -223,6 +233,7 @@ struct rlc_context {
     RLC_CK(cudaStreamSynchronize(stream));
     if (pstream) RLC_CK(cudaStreamSynchronize(pstream));
     if (sstream) RLC_CK(cudaStreamSynchronize(sstream));
+    acc_pending = false;
   }
   // per-stage CUDA-event timing (rlc_context_enable_timing)
   bool timing = false;
@@ -262,6 +273,8 @@ struct rlc_context {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (ev_prim_done) cudaEventDestroy(ev_prim_done);
     if (ev_sample_done) cudaEventDestroy(ev_sample_done);
+    if (ev_fold_done) cudaEventDestroy(ev_fold_done);
+    if (ev_acc_done) cudaEventDestroy(ev_acc_done);
     if (ev_sort_done) cudaEventDestroy(ev_sort_done);
     if (sstream) cudaStreamDestroy(sstream);
     for (cudaEvent_t e : ev_gbuf_free)
@@ -391,6 +404,7 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
           "render_pass: framebuffer size must match the camera");
   require(r0 <= r1 && r1 <= uint32_t(ctx->host.cam.height), "render_pass: bad row range");
   require(grid == nullptr || grid->ctx == ctx, "render_pass: grid belongs to another context");
+  ctx->join_acc();  // the pass buffers and the framebuffer are free again
   PassSetup S;
   const uint32_t spp_pp = cfg->spp / cfg->passes;
   const uint64_t n64 = uint64_t(r1 - r0) * uint64_t(ctx->host.cam.width) * spp_pp;
@@ -474,14 +488,29 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   uint32_t *k = nullptr, *v = nullptr;
   if (S.nv > 0) enqueue_trace(ctx, S, grid, &k, &v);  // max_depth 0: empty paths
   cudaStream_t st = ctx->stream;
-  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && S.nv > 0)
+  if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && S.nv > 0) {
     ctx->stage(3, [&] { rlc::launch_fold(S.g, S.p, k, v, ctx->pb, st); });
-  ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
-  RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));  // last G-buffer reader
+    // The framebuffer accumulation reads only pass buffers; the
+    // end_of_pass_update that follows touches only cut rows: run the former
+    // on the side stream beside the latter, joined by the next reader.
+    RLC_CK(cudaEventRecord(ctx->ev_fold_done, st));
+    RLC_CK(cudaStreamWaitEvent(ctx->sstream, ctx->ev_fold_done, 0));
+    ctx->stage_on(ctx->sstream, 4, [&] {
+      rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, ctx->sstream);
+    });
+    RLC_CK(cudaEventRecord(ctx->ev_acc_done, ctx->sstream));
+    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], ctx->sstream));
+    ctx->acc_pending = true;
+  } else {
+    ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
+    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));  // last G-buffer reader
+  }
   RLC_CK(cudaGetLastError());
 }
 
-void finish_sync(const rlc_context* ctx, rlc_grid* grid) {
+void finish_sync(const rlc_context* cctx, rlc_grid* grid) {
+  rlc_context* ctx = const_cast<rlc_context*>(cctx);
+  ctx->join_acc();
   const uint32_t bits =
       read_and_clear_err(ctx->stream, grid ? grid->dev.counters : ctx->counters);
   if (bits) throw_device_error(bits);
@@ -499,6 +528,7 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
     rlc::launch_split_collapse(ctx->dev, grid->dev, cut->split_threshold, cut->iterations,
                                d_changes, ctx->stream);
   });
+  c->join_acc();  // the pass's accumulation ran beside split-collapse; the frame ends here
   RLC_CK(cudaGetLastError());
 }
 
@@ -592,6 +622,8 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_prim_done, cudaEventDisableTiming));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->sstream, cudaStreamNonBlocking));
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_sample_done, cudaEventDisableTiming));
+    RLC_CK(cudaEventCreateWithFlags(&ctx->ev_fold_done, cudaEventDisableTiming));
+    RLC_CK(cudaEventCreateWithFlags(&ctx->ev_acc_done, cudaEventDisableTiming));
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_sort_done, cudaEventDisableTiming));
     for (cudaEvent_t& e : ctx->ev_gbuf_free) {
       RLC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -948,6 +980,7 @@ rlc_status rlc_framebuffer_destroy(rlc_framebuffer* fb) {
   return guarded([&] {
     if (!fb) return;
     cudaStreamSynchronize(fb->ctx->stream);
+    if (fb->ctx->sstream) cudaStreamSynchronize(fb->ctx->sstream);  // a pending accumulation
     delete fb;
   });
 }
@@ -955,6 +988,7 @@ rlc_status rlc_framebuffer_destroy(rlc_framebuffer* fb) {
 rlc_status rlc_framebuffer_clear(rlc_framebuffer* fb) {
   return guarded([&] {
     require(fb != nullptr, "rlc_framebuffer_clear: null framebuffer");
+    const_cast<rlc_context*>(fb->ctx)->join_acc();
     const size_t npix = size_t(fb->width) * size_t(fb->height);
     RLC_CK(cudaMemsetAsync(fb->fb.sum, 0, 24 * npix, fb->ctx->stream));
     RLC_CK(cudaMemsetAsync(fb->fb.count, 0, 8 * npix, fb->ctx->stream));
@@ -964,6 +998,7 @@ rlc_status rlc_framebuffer_clear(rlc_framebuffer* fb) {
 rlc_status rlc_framebuffer_download(const rlc_framebuffer* fb, double* sum, uint64_t* count) {
   return guarded([&] {
     require(fb != nullptr, "rlc_framebuffer_download: null framebuffer");
+    const_cast<rlc_context*>(fb->ctx)->join_acc();
     const size_t npix = size_t(fb->width) * size_t(fb->height);
     RLC_CK(cudaStreamSynchronize(fb->ctx->stream));
     if (sum) RLC_CK(cudaMemcpy(sum, fb->fb.sum, 24 * npix, cudaMemcpyDeviceToHost));
@@ -974,6 +1009,7 @@ rlc_status rlc_framebuffer_download(const rlc_framebuffer* fb, double* sum, uint
 rlc_status rlc_framebuffer_resolve(const rlc_framebuffer* fb, double* image) {
   return guarded([&] {
     require(fb != nullptr && image != nullptr, "rlc_framebuffer_resolve: null argument");
+    const_cast<rlc_context*>(fb->ctx)->join_acc();
     const uint32_t npix = uint32_t(size_t(fb->width) * size_t(fb->height));
     rlc::launch_resolve(fb->fb, npix, fb->d_image, fb->ctx->stream);
     RLC_CK(cudaMemcpyAsync(image, fb->d_image, 24 * size_t(npix), cudaMemcpyDeviceToHost,
@@ -1229,6 +1265,7 @@ void render_frame_impl(rlc_context* ctx, const rlc_render_config* config, const 
     if (grid) enqueue_eop(grid, ctx, &config->cut, d_hist + pass);
     if (reference) {
       const int k = int(pass & 1u);
+      ctx->join_acc();
       rlc::launch_pixel_err(fb->fb, uint32_t(npix), d_ref, d_err[k], st);
       RLC_CK(cudaMemcpyAsync(h_err[k]->p, d_err[k], 8 * npix, cudaMemcpyDeviceToHost, st));
       RLC_CK(cudaEventRecord(ev[k], st));
@@ -1236,6 +1273,7 @@ void render_frame_impl(rlc_context* ctx, const rlc_render_config* config, const 
     }
   }
   if (reference) score(config->passes - 1);
+  ctx->join_acc();
   if (image_out) {
     rlc::launch_resolve(fb->fb, uint32_t(npix), fb->d_image, st);
     RLC_CK(cudaMemcpyAsync(image_out, fb->d_image, 24 * npix, cudaMemcpyDeviceToHost, st));

@@ -661,7 +661,10 @@ __global__ void __launch_bounds__(128) k_bounce(DevScene sc, DevGrid g, PassPara
 // ---------------------------------------------------------------------------
 // k_sample: sample_light + nee_estimate (estimators.cpp:28-106)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_sample(DevScene sc, DevGrid g, PassParams P,
+#ifndef RLC_SAMPLE_BLOCKS
+#define RLC_SAMPLE_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, DevGrid g, PassParams P,
                                                 const GBuf* __restrict__ gbuf,
                                                 SampleRec* __restrict__ srec,
                                                 uint8_t* __restrict__ rflag,
