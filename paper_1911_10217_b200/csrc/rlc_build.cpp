@@ -472,6 +472,55 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
   return wide;
 }
 
+// Quantizes wide nodes to WideQ (rlc_common.h): per node and axis the origin
+// is the smallest child bound and the scale the smallest power of two that
+// spans the node in 250 steps; each bound is then moved outward until the
+// exact plane origin + q * scale encloses the fp32 bound.
+std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
+  std::vector<WideQ> out(w.size());
+  for (size_t i = 0; i < w.size(); ++i) {
+    const Wide4& n = w[i];
+    WideQ& q = out[i];
+    std::memset(&q, 0, sizeof(q));
+    for (int c = 0; c < 4; ++c) q.child[c] = n.child[c];
+    for (int a = 0; a < 3; ++a) {
+      float lo = HUGE_VALF, hi = -HUGE_VALF;
+      for (int c = 0; c < 4; ++c)
+        if (n.child[c] != kWideEmpty) {
+          lo = std::min(lo, n.lo[a][c]);
+          hi = std::max(hi, n.hi[a][c]);
+        }
+      if (!(lo <= hi)) lo = hi = 0.f;  // no children
+      q.origin[a] = lo;
+      const double ext = double(hi) - double(lo);
+      int e = -126;  // scale 2^e, smallest with ext / scale <= 250
+      while (e < 127 && std::ldexp(250.0, e) < ext) ++e;
+      q.ex[a] = uint8_t(e + 127);
+      const float scale = std::ldexp(1.0f, e);
+      for (int c = 0; c < 4; ++c) {
+        if (n.child[c] == kWideEmpty) {
+          q.qlo[a][c] = 255;
+          q.qhi[a][c] = 0;
+          continue;
+        }
+        // the device evaluates the exact plane origin + q * scale (k_shadow)
+        auto plane = [&](int qv) { return double(lo) + double(qv) * double(scale); };
+        int ql = int(std::floor((double(n.lo[a][c]) - double(lo)) / double(scale)));
+        ql = std::max(0, std::min(255, ql));
+        while (ql > 0 && plane(ql) > double(n.lo[a][c])) --ql;
+        int qh = int(std::ceil((double(n.hi[a][c]) - double(lo)) / double(scale)));
+        qh = std::max(0, std::min(255, qh));
+        while (qh < 255 && plane(qh) < double(n.hi[a][c])) ++qh;
+        if (plane(ql) > double(n.lo[a][c]) || plane(qh) < double(n.hi[a][c]))
+          throw std::runtime_error("quantize_wide: bound not representable");
+        q.qlo[a][c] = uint8_t(ql);
+        q.qhi[a][c] = uint8_t(qh);
+      }
+    }
+  }
+  return out;
+}
+
 // The wide trees of the traversal kernels:
 //  * `wide`: any-hit shadow rays -- a binned-SAH tree over the reference
 //    BVH's leaves (default) or the reference tree itself
@@ -553,6 +602,9 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s);
   }
   out.wide_ref = collapse_wide(out.nodes, nullptr);
+  const char* q = std::getenv("RLC_SHADOW_QUANT");
+  out.wide_q.clear();
+  if (!(q && std::string(q) == "0")) out.wide_q = quantize_wide(out.wide);
 }
 
 }  // namespace

@@ -29,6 +29,7 @@ struct HostScene {
   std::vector<BvhNodeF> nodes_cam; // same, boxes relative to the camera origin (fl64(c - O))
   std::vector<TriAccel> tris;  // BVH leaf order
   std::vector<Wide4> wide;       // 4-wide conservative tree, DFS order (empty: root is a leaf)
+  std::vector<WideQ> wide_q;     // `wide` quantized to 64-byte nodes (RLC_SHADOW_QUANT=0: none)
   std::vector<Wide4> wide_ref;   // the reference tree collapsed, children left to right
   std::vector<Wide4> wide_cam;   // wide_ref with camera-relative boxes
   double coord_bound = 0;        // S: largest |coordinate| of the scene (shadow-tree padding)

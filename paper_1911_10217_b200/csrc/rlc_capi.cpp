@@ -539,9 +539,11 @@ void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d) {
   d.nodes_f = A.put(h.nodes_f);
   d.nodes_cam = A.put(h.nodes_cam);
   d.wide = A.put(h.wide);
+  d.wide_q = A.put(h.wide_q);
   d.wide_ref = A.put(h.wide_ref);
   d.wide_cam = A.put(h.wide_cam);
   if (h.wide.empty()) d.wide = nullptr;
+  if (h.wide_q.empty()) d.wide_q = nullptr;
   if (h.wide_ref.empty()) d.wide_ref = nullptr;
   if (h.wide_cam.empty()) d.wide_cam = nullptr;
   d.tri_leaf = A.put(h.tri_leaf);

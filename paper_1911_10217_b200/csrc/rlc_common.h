@@ -114,6 +114,22 @@ struct alignas(128) Wide4 {
 };
 static_assert(sizeof(Wide4) % 128 == 0, "wide nodes are whole 128-byte lines");
 
+// The shadow tree's 4-wide node quantized to 64 bytes: child box planes are
+// origin + q * 2^(e - 127) per axis (q 8-bit).  The host chooses every q so
+// the plane lies OUTSIDE the Wide4 node's (already outward-rounded, padded)
+// fp32 bound, so a quantized box contains the exact one; k_shadow evaluates
+// t = fma(q, 2^e inv, fma(origin, inv, -o inv)) per plane.
+struct alignas(64) WideQ {
+  float origin[3];
+  uint8_t ex[3];          // per-axis scale exponent: scale = 2^(ex - 127)
+  uint8_t pad0;
+  uint8_t qlo[3][4];      // [axis][child]
+  uint8_t qhi[3][4];
+  uint32_t child[4];      // as Wide4::child
+  uint32_t pad1[2];
+};
+static_assert(sizeof(WideQ) == 64, "quantized wide nodes are 64 bytes");
+
 // Triangle as the Moller-Trumbore test consumes it (bvh.cpp:44-62): p0 and
 // the two edges, precomputed with the reference's own subtraction.  Stored
 // in BVH leaf order.  80 B.

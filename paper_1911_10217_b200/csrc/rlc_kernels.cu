@@ -1229,26 +1229,60 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
     // register; the first leaf met is postponed and traversal continues
     // while some lane of the warp has not found a leaf yet
     while (cur != kDone && !(cur & kWideLeaf)) {
-      constexpr int Q = kWide / 4;  // float4 per [axis] row
-      const float4* p = reinterpret_cast<const float4*>(sc.wide + cur);
-      float lo[3][kWide], hi[3][kWide];
+      float tn[kWide];
+      uint32_t mi, m;
       uint32_t c[kWide];
+      if (sc.wide_q) {  // 64-byte quantized node: no inner test (leaves checked exactly)
+        const uint4* p = reinterpret_cast<const uint4*>(sc.wide_q + cur);
+        const uint4 w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2), w3 = __ldg(p + 3);
+        const uint32_t ql[3] = {w1.x, w1.y, w1.z}, qh[3] = {w1.w, w2.x, w2.y};
+        const float org[3] = {__uint_as_float(w0.x), __uint_as_float(w0.y), __uint_as_float(w0.z)};
+        c[0] = w2.z, c[1] = w2.w, c[2] = w3.x, c[3] = w3.y;
+        float nb[kWide], fb[kWide];
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const float4 vl = __ldg(p + a * Q + q), vh = __ldg(p + (3 + a) * Q + q);
-          lo[a][4 * q] = vl.x, lo[a][4 * q + 1] = vl.y, lo[a][4 * q + 2] = vl.z, lo[a][4 * q + 3] = vl.w;
-          hi[a][4 * q] = vh.x, hi[a][4 * q + 1] = vh.y, hi[a][4 * q + 2] = vh.z, hi[a][4 * q + 3] = vh.w;
+        for (int k = 0; k < kWide; ++k) {
+          nb[k] = rf.tmin;
+          fb[k] = rf.tmax;
         }
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + 6 * Q + q));
-        c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+        for (int a = 0; a < 3; ++a) {
+          const bool ng = (rf.neg >> a) & 1u;
+          const uint32_t nw = ng ? qh[a] : ql[a], fw = ng ? ql[a] : qh[a];
+          const float A = __uint_as_float(((w0.w >> (8 * a)) & 255u) << 23) * rf.inv[a];
+          const float B = fmaf(org[a], rf.inv[a], rf.b[a]);
+#pragma unroll
+          for (int k = 0; k < kWide; ++k) {
+            const float qn = float((nw >> (8 * k)) & 255u), qf = float((fw >> (8 * k)) & 255u);
+            nb[k] = fmaxf(nb[k], fmaf(qn, A, B));
+            fb[k] = fminf(fb[k], fmaf(qf, A, B));
+          }
+        }
+        m = 0;
+#pragma unroll
+        for (int k = 0; k < kWide; ++k) {
+          m |= (nb[k] <= fb[k]) ? (1u << k) : 0u;
+          tn[k] = nb[k];
+        }
+        mi = 0;
+      } else {
+        constexpr int Q = kWide / 4;  // float4 per [axis] row
+        const float4* p = reinterpret_cast<const float4*>(sc.wide + cur);
+        float lo[3][kWide], hi[3][kWide];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const float4 vl = __ldg(p + a * Q + q), vh = __ldg(p + (3 + a) * Q + q);
+            lo[a][4 * q] = vl.x, lo[a][4 * q + 1] = vl.y, lo[a][4 * q + 2] = vl.z, lo[a][4 * q + 3] = vl.w;
+            hi[a][4 * q] = vh.x, hi[a][4 * q + 1] = vh.y, hi[a][4 * q + 2] = vh.z, hi[a][4 * q + 3] = vh.w;
+          }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + 6 * Q + q));
+          c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+        }
+        m = boxw_s(lo, hi, rf, tn, &mi);
       }
-      float tn[kWide];
-      uint32_t mi;
-      uint32_t m = boxw_s(lo, hi, rf, tn, &mi);
 #pragma unroll
       for (int k = 0; k < kWide; ++k) {
         if (c[k] == kWideEmpty) m &= ~(1u << k);

@@ -77,6 +77,7 @@ struct DevScene {
   const BvhNodeF* nodes_f;  // fp32 outward-rounded copy for the decision tests
   const BvhNodeF* nodes_cam; // camera-relative fp32 copy (primary rays)
   const Wide4* wide;        // conservative 4-wide tree (null if the root is a leaf)
+  const WideQ* wide_q;      // the same tree quantized (null: k_shadow reads `wide`)
   const Wide4* wide_ref;    // reference tree collapsed in its leaf order (closest hit)
   const Wide4* wide_cam;    // same, camera-relative boxes (primary rays)
   const uint32_t* tri_leaf; // binary leaf per leaf-order triangle
