@@ -412,11 +412,14 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
   std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
   std::vector<std::array<uint32_t, kWide>> kids;
   kids.reserve(nodes.size() / 2 + 1);
+  // breadth-first numbering: the internal children of a node get consecutive
+  // indices, so siblings share cache lines (two 64-byte quantized nodes per
+  // 128-byte line)
   std::vector<uint32_t> todo{0};
+  todo.reserve(nodes.size() / 2 + 1);
   std::vector<uint32_t> order;
-  while (!todo.empty()) {
-    const uint32_t b = todo.back();
-    todo.pop_back();
+  for (size_t head = 0; head < todo.size(); ++head) {
+    const uint32_t b = todo[head];
     wid[b] = uint32_t(order.size());
     order.push_back(b);
     std::array<uint32_t, kWide> L;
@@ -437,7 +440,7 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
       ++nl;
     }
     kids.push_back(L);
-    for (int k = nl; k-- > 0;)
+    for (int k = 0; k < nl; ++k)
       if (nodes[L[k]].count == 0) todo.push_back(L[k]);
   }
   std::vector<Wide4> wide(order.size());
