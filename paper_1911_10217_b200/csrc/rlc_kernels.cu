@@ -961,6 +961,19 @@ __device__ __forceinline__ uint32_t boxw_f(const float (&lo)[3][kWide],
 // changed since (the stack watermark `fresh`), else by the exact fp64 test
 // of its reference box.  Triangle tests are the exact fp64 Moller-Trumbore.
 // ---------------------------------------------------------------------------
+// Three-input fp32 min / max (sm_100 FMNMX3); like fminf / fmaxf, a NaN
+// operand is ignored.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 // Camera rays on wide_cam: every stored coordinate is x' = fl32 outward of
 // x -/+ 2^-21 |x| (x = fl64(c - O)), so fl32(x' * fl32(inv)) bounds the
 // reference's fl64(x * inv) from outside on every axis and the plain slab
@@ -976,19 +989,15 @@ __device__ __forceinline__ uint32_t boxw_cam(const float (&lo)[3][kWide],
   float nb[kWide], fb[kWide];
 #pragma unroll
   for (int c = 0; c < kWide; ++c) {
-    nb[c] = 0.f;
-    fb[c] = HUGE_VALF;
-  }
+    float tn[3], tf[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const bool ng = (neg >> a) & 1u;
-#pragma unroll
-    for (int c = 0; c < kWide; ++c) {
-      const float n = ng ? hi[a][c] : lo[a][c];
-      const float f = ng ? lo[a][c] : hi[a][c];
-      nb[c] = fmaxf(nb[c], n * inv[a]);
-      fb[c] = fminf(fb[c], f * inv[a]);
+    for (int a = 0; a < 3; ++a) {
+      const bool ng = (neg >> a) & 1u;
+      tn[a] = (ng ? hi[a][c] : lo[a][c]) * inv[a];
+      tf[a] = (ng ? lo[a][c] : hi[a][c]) * inv[a];
     }
+    nb[c] = fmaxf(fmax3(0.f, tn[0], tn[1]), tn[2]);  // t_min = 0
+    fb[c] = fmin3(tf[0], tf[1], tf[2]);
   }
   uint32_t m = 0, mi = 0;
 #pragma unroll
@@ -1238,24 +1247,27 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
         const uint32_t ql[3] = {w1.x, w1.y, w1.z}, qh[3] = {w1.w, w2.x, w2.y};
         const float org[3] = {__uint_as_float(w0.x), __uint_as_float(w0.y), __uint_as_float(w0.z)};
         c[0] = w2.z, c[1] = w2.w, c[2] = w3.x, c[3] = w3.y;
-        float nb[kWide], fb[kWide];
-#pragma unroll
-        for (int k = 0; k < kWide; ++k) {
-          nb[k] = rf.tmin;
-          fb[k] = rf.tmax;
-        }
+        float A[3], B[3];
+        uint32_t nw[3], fw[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           const bool ng = (rf.neg >> a) & 1u;
-          const uint32_t nw = ng ? qh[a] : ql[a], fw = ng ? ql[a] : qh[a];
-          const float A = __uint_as_float(((w0.w >> (8 * a)) & 255u) << 23) * rf.inv[a];
-          const float B = fmaf(org[a], rf.inv[a], rf.b[a]);
+          nw[a] = ng ? qh[a] : ql[a];
+          fw[a] = ng ? ql[a] : qh[a];
+          A[a] = __uint_as_float(((w0.w >> (8 * a)) & 255u) << 23) * rf.inv[a];
+          B[a] = fmaf(org[a], rf.inv[a], rf.b[a]);
+        }
+        float nb[kWide], fb[kWide];
 #pragma unroll
-          for (int k = 0; k < kWide; ++k) {
-            const float qn = float((nw >> (8 * k)) & 255u), qf = float((fw >> (8 * k)) & 255u);
-            nb[k] = fmaxf(nb[k], fmaf(qn, A, B));
-            fb[k] = fminf(fb[k], fmaf(qf, A, B));
+        for (int k = 0; k < kWide; ++k) {
+          float tn[3], tf[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            tn[a] = fmaf(float((nw[a] >> (8 * k)) & 255u), A[a], B[a]);
+            tf[a] = fmaf(float((fw[a] >> (8 * k)) & 255u), A[a], B[a]);
           }
+          nb[k] = fmaxf(fmax3(rf.tmin, tn[0], tn[1]), tn[2]);
+          fb[k] = fminf(fmin3(rf.tmax, tf[0], tf[1]), tf[2]);
         }
         m = 0;
 #pragma unroll
