@@ -56,13 +56,18 @@ def env_int(k, d):
         return d
 
 
-def make_config(name: str):
+def make_config(name: str, max_depth: int = 1):
     from paper_1911_10217_b200 import rlcuts, scenes
     scene, st = scenes.config_scene(name)
-    cfg = rlcuts.RenderConfig(spp=st["spp"], passes=st["passes"],
+    cfg = rlcuts.RenderConfig(spp=st["spp"], passes=st["passes"], max_depth=max_depth,
                               sampler=rlcuts.SamplerKind.rl_lightcuts,
                               hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
     return scene, cfg
+
+
+def workload(args) -> str:
+    w = WORKLOADS[args.config]
+    return w if args.max_depth == 1 else w + f", max_depth {args.max_depth} (multi-bounce paths)"
 
 
 # ---------------------------------------------------------------------------
@@ -176,7 +181,8 @@ def cpu_reference_run(scene, cfg, passes: int, warmup: int, min_seconds: float,
     cam = scene.camera
     small = scene.with_resolution(max(cam.width // downscale, 1), max(cam.height // downscale, 1))
     rcfg = rlcuts.RenderConfig(spp=cfg.spp, passes=cfg.passes, sampler=cfg.sampler, cut=cfg.cut,
-                               hash=cfg.hash, seed=cfg.seed, workers=cores)
+                               hash=cfg.hash, seed=cfg.seed, workers=cores,
+                               max_depth=cfg.max_depth)
     run = oracle.RefRun(small, rcfg)
 
     def update(p):
@@ -218,14 +224,14 @@ def cpu_reference_run(scene, cfg, passes: int, warmup: int, min_seconds: float,
 def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
-    scene, cfg = make_config(args.config)
+    scene, cfg = make_config(args.config, args.max_depth)
     value, cores, sample, ms_step, _ = cpu_reference_run(
         scene, cfg, passes=args.steps, warmup=args.warmup, min_seconds=0.0,
         downscale=args.cpu_downscale, dynamic=args.config in DYNAMIC)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOADS[args.config]},
+            "data": "synthetic", "config": {"workload": workload(args)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -254,7 +260,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         else:
             dist.init_process_group("gloo")
 
-    scene, cfg = make_config(args.config)
+    scene, cfg = make_config(args.config, args.max_depth)
     t0 = time.perf_counter()
     ctx = rlcuts.build_context(scene, cfg, device=local_rank)
     build_s = time.perf_counter() - t0
@@ -396,7 +402,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "call": "rlc_context_update_scene + rlc_render_pass + rlc_end_of_pass_update"}
     elif not args.no_e2e and world == 1:
         ecfg = rlcuts.RenderConfig(spp=args.steps * (cfg.spp // cfg.passes), passes=args.steps,
-                                   sampler=cfg.sampler, cut=cfg.cut, hash=cfg.hash, seed=cfg.seed + 1)
+                                   sampler=cfg.sampler, cut=cfg.cut, hash=cfg.hash,
+                                   seed=cfg.seed + 1, max_depth=cfg.max_depth)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = rlcuts.render_frame(ctx, ecfg)
@@ -423,7 +430,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config],
+            "config": {"workload": workload(args),
                        "frames_timed": args.steps,
                        "l2": "no flush: resident scene+cut+pass buffers exceed the 126 MB L2",
                        "parallelism": (f"screen bands x{world}, exact update-record all-gather "
@@ -447,6 +454,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--max-depth", type=int, default=1,
+                    help="path vertices per sample (render.hpp:20); 1 = the headline direct lighting")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
