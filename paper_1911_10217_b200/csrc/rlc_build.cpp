@@ -496,8 +496,14 @@ std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
       if (!(lo <= hi)) lo = hi = 0.f;  // no children
       q.origin[a] = lo;
       const double ext = double(hi) - double(lo);
-      int e = -126;  // scale 2^e, smallest with ext / scale <= 250
-      while (e < 127 && std::ldexp(250.0, e) < ext) ++e;
+      // scale 2^e: the smallest with ext / scale <= 250
+      int e = -126;
+      if (ext > 0) {
+        std::frexp(ext / 250.0, &e);  // ext / 250 < 2^e
+        while (e > -126 && std::ldexp(250.0, e - 1) >= ext) --e;
+        while (e < 127 && std::ldexp(250.0, e) < ext) ++e;
+        e = std::max(-126, std::min(127, e));
+      }
       q.ex[a] = uint8_t(e + 127);
       const float scale = std::ldexp(1.0f, e);
       for (int c = 0; c < 4; ++c) {
