@@ -1069,7 +1069,9 @@ __device__ __forceinline__ bool closest_wide(const DevScene& sc, const Wide4* __
       }
 #pragma unroll
       for (int k = 0; k < kWide; ++k) {  // left to right: the rightmost is popped first
-        if (!((m >> k) & 1u) || c[k] == kWideEmpty) continue;
+        // an empty slot's box (+inf, -inf) never passes the camera test; the
+        // general test's error terms can turn it into NaN, which passes
+        if (!((m >> k) & 1u) || (!CAM && c[k] == kWideEmpty)) continue;
         uint32_t e = c[k];
         if ((e & kWideLeaf) && (e & kLeafPure) && ((mi >> k) & 1u)) e |= kLeafVerified;
         stack[sp++] = e;
