@@ -46,6 +46,8 @@ WORKLOADS = {
           "scenes.displace_emitters) via rlc_context_update_scene (fresh scene BVH and "
           "emitter records, frozen light tree), 1920x1080, 1 spp/frame, M=128",
 }
+WORKLOADS["c5"] = ("c5: maze, 4,000,000 emissive tris, 3840x2160, 64 spp in 16 passes "
+                   "(4 spp per pass), M=128 (BASELINE's 8-GPU offline case, here on one GPU)")
 DYNAMIC = {"c4"}  # workloads whose emitters move every frame
 
 
