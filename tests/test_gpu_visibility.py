@@ -27,12 +27,14 @@ def random_soup(count, seed, extent, tri_size):
                  scenes.Camera((0, 0, -5), (0, 0, 0), (0, 1, 0), 45, 8, 8), "soup")
 
 
-@pytest.fixture(params=["tris", "leaves", "reference"], autouse=True)
+@pytest.fixture(params=["tris", "tris-128B", "leaves", "reference"], autouse=True)
 def shadow_tree(request, monkeypatch):
-    """All shadow-ray trees: the SAH tree over single triangles (default),
-    the SAH tree over the reference leaves, and the reference tree collapsed
-    to 4-wide."""
-    monkeypatch.setenv("RLC_SHADOW_TREE", request.param)
+    """All shadow-ray trees: the SAH tree over single triangles (default,
+    64-byte quantized nodes; "-128B": the unquantized nodes), the SAH tree over
+    the reference leaves, and the reference tree collapsed to 4-wide."""
+    tree, _, variant = request.param.partition("-")
+    monkeypatch.setenv("RLC_SHADOW_TREE", tree)
+    monkeypatch.setenv("RLC_SHADOW_QUANT", "0" if variant == "128B" else "1")
     return request.param
 
 
