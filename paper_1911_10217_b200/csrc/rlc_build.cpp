@@ -17,7 +17,10 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <thread>
+#include <atomic>
 #include <future>
+#include <limits>
 #include <numeric>
 #include <cstdlib>
 #include <string>
@@ -68,7 +71,13 @@ uint32_t spread10(uint32_t x) {  // 10 bits -> every third bit
   return x;
 }
 
-// Scene BVH over all triangles; returns the leaf order.
+// Scene BVH over all triangles (build_scene_bvh, bvh.cpp:64-122): median
+// split on the longest centroid axis with libstdc++ std::nth_element, leaves
+// of <= 4 triangles.  A node's split depends only on the index range it owns,
+// so subtrees below n/64 triangles are built concurrently into private node
+// arrays and spliced in afterwards: the topology, left/right order, leaf
+// membership and triangle order are those of the sequential build (only the
+// internal node numbering differs; siblings stay adjacent).
 void build_bvh(const rlc_scene_desc& d, HostScene& out) {
   const uint32_t n = d.num_triangles;
   std::vector<Box> tb(n);
@@ -87,41 +96,85 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
   struct Todo {
     uint32_t node, begin, end;
   };
+  // Builds the subtree of `root` (already allocated in `nodes`) over
+  // perm[begin, end); new nodes are appended to `nodes`.
+  auto build = [&](std::vector<BvhNode>& nodes, uint32_t root, uint32_t begin, uint32_t end,
+                   uint32_t defer_below, std::vector<Todo>* deferred) {
+    std::vector<Todo> todo{{root, begin, end}};
+    while (!todo.empty()) {
+      const Todo t = todo.back();
+      todo.pop_back();
+      const uint32_t count = t.end - t.begin;
+      if (deferred && count < defer_below && count > 4) {
+        deferred->push_back(t);
+        continue;
+      }
+      Box bounds, cb;
+      for (uint32_t i = t.begin; i < t.end; ++i) {
+        bounds.grow(tb[perm[i]]);
+        cb.grow(cen[perm[i]]);
+      }
+      BvhNode& nd = nodes[t.node];
+      put3(nd.lo, bounds.lo);
+      put3(nd.hi, bounds.hi);
+      if (count <= 4) {
+        nd.a = t.begin;
+        nd.b = 0;
+        nd.count = count;
+        continue;
+      }
+      const int axis = cb.longest_axis();
+      const uint32_t mid = t.begin + count / 2;
+      std::nth_element(perm.begin() + t.begin, perm.begin() + mid, perm.begin() + t.end,
+                       [&](uint32_t x, uint32_t y) { return comp(cen[x], axis) < comp(cen[y], axis); });
+      const uint32_t child = uint32_t(nodes.size());
+      nodes.push_back(BvhNode{});
+      nodes.push_back(BvhNode{});
+      nodes[t.node].a = child;
+      nodes[t.node].b = child + 1;
+      nodes[t.node].count = 0;
+      todo.push_back({child, t.begin, mid});
+      todo.push_back({child + 1, mid, t.end});
+    }
+  };
   std::vector<BvhNode>& nodes = out.nodes;
   nodes.clear();
   nodes.reserve(size_t(2) * n);
   nodes.push_back(BvhNode{});
-  std::vector<Todo> todo{{0, 0, n}};
-  while (!todo.empty()) {
-    const Todo t = todo.back();
-    todo.pop_back();
-    Box bounds, cb;
-    for (uint32_t i = t.begin; i < t.end; ++i) {
-      bounds.grow(tb[perm[i]]);
-      cb.grow(cen[perm[i]]);
+  std::vector<Todo> deferred;
+  const uint32_t cut = std::max<uint32_t>(n / 16, 2048);
+  build(nodes, 0, 0, n, cut, &deferred);
+  if (!deferred.empty()) {
+    // subtrees in parallel, each into a private array whose element 0 is the
+    // subtree root (a node already allocated in `nodes`)
+    std::vector<std::vector<BvhNode>> local(deferred.size());
+    std::vector<std::future<void>> jobs;
+    std::atomic<size_t> next{0};
+    const unsigned nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (unsigned w = 0; w < nthreads; ++w)
+      jobs.push_back(std::async(std::launch::async, [&] {
+        for (size_t k; (k = next.fetch_add(1)) < deferred.size();) {
+          std::vector<BvhNode>& L = local[k];
+          L.reserve(size_t(2) * (deferred[k].end - deferred[k].begin));
+          L.push_back(BvhNode{});
+          build(L, 0, deferred[k].begin, deferred[k].end, 0, nullptr);
+        }
+      }));
+    for (auto& j : jobs) j.get();
+    for (size_t k = 0; k < deferred.size(); ++k) {
+      const std::vector<BvhNode>& L = local[k];
+      const uint32_t base = uint32_t(nodes.size()) - 1;  // local index i >= 1 -> base + i
+      auto remap = [&](const BvhNode& y) {
+        BvhNode x = y;
+        if (x.count == 0) {
+          x.a += base;
+          x.b += base;
+        }
+        return x;
+      };
+      nodes[deferred[k].node] = remap(L[0]);
+      for (size_t i = 1; i < L.size(); ++i) nodes.push_back(remap(L[i]));
     }
-    BvhNode& nd = nodes[t.node];
-    put3(nd.lo, bounds.lo);
-    put3(nd.hi, bounds.hi);
-    const uint32_t count = t.end - t.begin;
-    if (count <= 4) {
-      nd.a = t.begin;
-      nd.b = 0;
-      nd.count = count;
-      continue;
-    }
-    const int axis = cb.longest_axis();
-    const uint32_t mid = t.begin + count / 2;
-    std::nth_element(perm.begin() + t.begin, perm.begin() + mid, perm.begin() + t.end,
-                     [&](uint32_t x, uint32_t y) { return comp(cen[x], axis) < comp(cen[y], axis); });
-    const uint32_t child = uint32_t(nodes.size());
-    nodes.push_back(BvhNode{});
-    nodes.push_back(BvhNode{});
-    nodes[t.node].a = child;
-    nodes[t.node].b = child + 1;
-    nodes[t.node].count = 0;
-    todo.push_back({child, t.begin, mid});
-    todo.push_back({child + 1, mid, t.end});
   }
   out.tris.resize(n);
   for (uint32_t i = 0; i < n; ++i) {
@@ -143,14 +196,27 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
   out.shadow_eps = 1e-4 * length(ext);  // bvh.cpp:120
 }
 
+// The next float toward -inf / +inf (bit stepping; std::nextafter's libm
+// call dominated the tree collapses).
+inline float float_down(float f) {
+  if (f != f || f == -HUGE_VALF) return f;
+  if (f == 0.0f) return -std::numeric_limits<float>::denorm_min();
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u = f > 0 ? u - 1 : u + 1;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+inline float float_up(float f) { return -float_down(-f); }
+
 float round_down(double x) {
   float f = float(x);
-  if (double(f) > x) f = std::nextafter(f, -HUGE_VALF);
+  if (double(f) > x) f = float_down(f);
   return f;
 }
 float round_up(double x) {
   float f = float(x);
-  if (double(f) < x) f = std::nextafter(f, HUGE_VALF);
+  if (double(f) < x) f = float_up(f);
   return f;
 }
 
@@ -545,10 +611,16 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
   for (size_t i = 0; i < out.nodes.size(); ++i)
     for (uint32_t t = out.nodes[i].a; out.nodes[i].count > 0 && t < out.nodes[i].a + out.nodes[i].count; ++t)
       out.tri_leaf[t] = uint32_t(i);
-  out.tris_s = out.tris;
-  out.tri_leaf_s = out.tri_leaf;
-  if (out.nodes.empty() || out.nodes[0].count > 0) return;
+  if (out.nodes.empty() || out.nodes[0].count > 0) {  // a leaf root: exact paths only
+    out.tris_s = out.tris;
+    out.tri_leaf_s = out.tri_leaf;
+    return;
+  }
   if (out.tris.size() >= (1u << 27)) throw InvalidArgument("build_scene_bvh: too many triangles");
+  // the closest-hit trees depend only on the reference BVH: built beside the shadow tree
+  auto f_ref = std::async(std::launch::async, [&] {
+    out.wide_ref = collapse_wide(out.nodes, nullptr);
+  });
   // shadow tree: SAH over triangles (default), over the reference leaves
   // (RLC_SHADOW_TREE=leaves) or the reference tree (=reference)
   const char* env = std::getenv("RLC_SHADOW_TREE");
@@ -562,6 +634,8 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     S = std::max(S, std::max(std::fabs(out.nodes[0].lo[a]), std::fabs(out.nodes[0].hi[a])));
   out.coord_bound = S;
   if (mode == "reference" || mode == "leaves") {
+    out.tris_s = out.tris;
+    out.tri_leaf_s = out.tri_leaf;
     out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
                              S * 0x1.0p-21);
   } else if (keep != nullptr && !keep->shadow_bin.empty()) {
@@ -571,6 +645,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     std::vector<uint32_t> leaf_of_id(out.tris.size());
     for (size_t j = 0; j < out.tris.size(); ++j) leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j];
     out.tris_s = keep->tris_s;
+    out.tri_leaf_s.resize(out.tris_s.size());
     std::vector<Box> tb(out.tris_s.size());
     for (size_t i = 0; i < out.tris_s.size(); ++i) {
       TriAccel& ta = out.tris_s[i];
@@ -603,6 +678,8 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s);
   } else {
     std::vector<uint32_t> perm;
+    out.tris_s.resize(out.tris.size());
+    out.tri_leaf_s.resize(out.tris.size());
     out.shadow_bin = sah_over_tris(d, out, perm);
     for (size_t i = 0; i < perm.size(); ++i) {
       out.tris_s[i] = out.tris[perm[i]];
@@ -610,7 +687,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     }
     out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s);
   }
-  out.wide_ref = collapse_wide(out.nodes, nullptr);
+  f_ref.get();
   const char* q = std::getenv("RLC_SHADOW_QUANT");
   out.wide_q.clear();
   if (!(q && std::string(q) == "0")) out.wide_q = quantize_wide(out.wide);
