@@ -29,6 +29,26 @@ namespace rlc {
 
 namespace {
 
+// Runs fn(i) for i in [0, n) on up to 16 threads in contiguous chunks.  The
+// iterations must write disjoint data; exceptions propagate to the caller.
+template <class F>
+void parallel_for(size_t n, const F& fn, size_t min_chunk = 2048) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t chunks = std::min<size_t>(hw, (n + min_chunk - 1) / min_chunk);
+  if (chunks <= 1) {
+    for (size_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::future<void>> jobs;
+  for (size_t c = 0; c < chunks; ++c) {
+    const size_t b = n * c / chunks, e = n * (c + 1) / chunks;
+    jobs.push_back(std::async(std::launch::async, [&fn, b, e] {
+      for (size_t i = b; i < e; ++i) fn(i);
+    }));
+  }
+  for (auto& j : jobs) j.get();
+}
+
 struct Box {
   V3 lo{HUGE_VAL, HUGE_VAL, HUGE_VAL};
   V3 hi{-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
@@ -82,14 +102,14 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
   const uint32_t n = d.num_triangles;
   std::vector<Box> tb(n);
   std::vector<V3> cen(n);
-  for (uint32_t i = 0; i < n; ++i) {
+  parallel_for(n, [&](size_t i) {
     Box b;
-    b.grow(vert(d, i, 0));
-    b.grow(vert(d, i, 1));
-    b.grow(vert(d, i, 2));
+    b.grow(vert(d, uint32_t(i), 0));
+    b.grow(vert(d, uint32_t(i), 1));
+    b.grow(vert(d, uint32_t(i), 2));
     tb[i] = b;
     cen[i] = b.center();
-  }
+  });
   std::vector<uint32_t> perm(n);
   std::iota(perm.begin(), perm.end(), 0u);
 
@@ -510,7 +530,7 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
       if (nodes[L[k]].count == 0) todo.push_back(L[k]);
   }
   std::vector<Wide4> wide(order.size());
-  for (size_t w = 0; w < order.size(); ++w) {
+  parallel_for(order.size(), [&](size_t w) {
     Wide4& n = wide[w];
     std::memset(&n, 0, sizeof(n));
     for (int c = 0; c < kWide; ++c) {
@@ -537,7 +557,7 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
                                    bn.a)
                                 : wid[b];
     }
-  }
+  });
   return wide;
 }
 
@@ -547,7 +567,7 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
 // exact plane origin + q * scale encloses the fp32 bound.
 std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
   std::vector<WideQ> out(w.size());
-  for (size_t i = 0; i < w.size(); ++i) {
+  parallel_for(w.size(), [&](size_t i) {
     const Wide4& n = w[i];
     WideQ& q = out[i];
     std::memset(&q, 0, sizeof(q));
@@ -592,7 +612,7 @@ std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
         q.qhi[a][c] = uint8_t(qh);
       }
     }
-  }
+  });
   return out;
 }
 
@@ -608,9 +628,10 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
   out.wide.clear();
   out.wide_ref.clear();
   out.tri_leaf.assign(out.tris.size(), 0);
-  for (size_t i = 0; i < out.nodes.size(); ++i)
+  parallel_for(out.nodes.size(), [&](size_t i) {
     for (uint32_t t = out.nodes[i].a; out.nodes[i].count > 0 && t < out.nodes[i].a + out.nodes[i].count; ++t)
       out.tri_leaf[t] = uint32_t(i);
+  });
   if (out.nodes.empty() || out.nodes[0].count > 0) {  // a leaf root: exact paths only
     out.tris_s = out.tris;
     out.tri_leaf_s = out.tri_leaf;
@@ -647,7 +668,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     out.tris_s = keep->tris_s;
     out.tri_leaf_s.resize(out.tris_s.size());
     std::vector<Box> tb(out.tris_s.size());
-    for (size_t i = 0; i < out.tris_s.size(); ++i) {
+    parallel_for(out.tris_s.size(), [&](size_t i) {
       TriAccel& ta = out.tris_s[i];
       const uint32_t id = ta.tri_id;
       const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
@@ -658,7 +679,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
       tb[i].grow(p0);
       tb[i].grow(p1);
       tb[i].grow(p2);
-    }
+    });
     out.shadow_bin = keep->shadow_bin;
     for (size_t k = out.shadow_bin.size(); k-- > 0;) {  // children follow their parent
       BvhNode& nd = out.shadow_bin[k];
@@ -967,7 +988,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   // camera origin O: the reference's per-axis term fl64(c - O) rounded
   // outward to fp32, so every fp32 error of the decision test is relative.
   out.nodes_cam.resize(out.nodes.size());
-  for (size_t i = 0; i < out.nodes.size(); ++i) {
+  parallel_for(out.nodes.size(), [&](size_t i) {
     const BvhNode& n = out.nodes[i];
     BvhNodeF& f = out.nodes_cam[i];
     for (int a = 0; a < 3; ++a) {
@@ -976,7 +997,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
     }
     f.a = n.count > 0 ? (kNodeLeaf | n.a) : n.a;
     f.b = n.count > 0 ? n.count : 0;
-  }
+  });
   // The wide copy for camera rays is enlarged by 2^-21 |x| per coordinate,
   // more than the whole relative gap between fl32(x' * fl32(inv)) and the
   // reference's fl64(x * inv) (< 2^-23): its plain slab test is conservative
