@@ -876,6 +876,10 @@ rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg,
     d.visits = A.alloc<uint32_t>(cap * M);
     d.cell_key = A.alloc<uint32_t>(5 * cap);
     d.touched = A.alloc<uint32_t>(cap);
+    // cuts too large for k_split's shared-memory rows work in global scratch
+    d.split_scratch = size_t(M) * 32 > rlc::kSplitSmemMax
+                          ? A.alloc<unsigned char>(size_t(rlc::kSplitGlobalWarps) * 32 * M)
+                          : nullptr;
     RLC_CK(cudaMemset(d.touched, 0, 4 * cap));
     d.t_node = A.upload(g->tmpl.node_ids);
     d.t_ends = A.upload(g->tmpl.ends);

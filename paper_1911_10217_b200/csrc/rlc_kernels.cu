@@ -1685,11 +1685,17 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
   const uint32_t wib = threadIdx.x >> 5;
   const uint32_t wpb = blockDim.x >> 5;
   const uint32_t M = g.M;
-  // per warp: qA, qB (double), nA, nB, vA, vB (u32)
-  double* qA = reinterpret_cast<double*>(smem) + size_t(wib) * 2 * M;
+  // per warp: qA, qB (double), nA, nB, vA, vB (u32) -- in shared memory, or
+  // for cuts too large for it in the grid's global scratch (same arithmetic)
+  unsigned char* base = g.split_scratch
+                            ? g.split_scratch + size_t(blockIdx.x * wpb + wib) * 32 * size_t(M)
+                            : smem + size_t(wib) * 16 * size_t(M);
+  double* qA = reinterpret_cast<double*>(base);
   double* qB = qA + M;
-  uint32_t* nA = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(smem) + size_t(wpb) * 2 * M) +
-                 size_t(wib) * 4 * M;
+  uint32_t* nA = g.split_scratch
+                     ? reinterpret_cast<uint32_t*>(qB + M)
+                     : reinterpret_cast<uint32_t*>(smem + size_t(wpb) * 16 * size_t(M)) +
+                           size_t(wib) * 4 * M;
   uint32_t* nB = nA + M;
   uint32_t* vA = nB + M;
   uint32_t* vB = vA + M;
@@ -2170,16 +2176,21 @@ void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffer
 
 void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshold,
                            uint32_t iterations, uint32_t* changes_out, cudaStream_t st) {
-  const size_t per_warp = size_t(g.M) * 32;  // 2 doubles + 4 u32 per entry
-  uint32_t wpb = uint32_t(96 * 1024 / per_warp);
-  if (wpb > 8) wpb = 8;
-  if (wpb < 1) wpb = 1;
-  const size_t smem = per_warp * wpb;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
+  const size_t per_warp = size_t(g.M) * 32;  // 2 doubles + 4 u32 per entry
+  if (g.split_scratch) {  // rows in global memory: kSplitGlobalWarps warps
+    k_split<<<kSplitGlobalWarps / 4, 128, 0, st>>>(sc, g, threshold, iterations, changes_out);
+    count_launch();
+    return;
+  }
+  uint32_t wpb = uint32_t(96 * 1024 / per_warp);
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1) wpb = 1;
+  const size_t smem = per_warp * wpb;
   k_split<<<148 * 4, wpb * 32, smem, st>>>(sc, g, threshold, iterations, changes_out);
   count_launch();
 }

@@ -127,6 +127,8 @@ struct DevGrid {
   const uint32_t* t_visits;
   double eps_q;
   unsigned long long* counters;   // kCnt*
+  unsigned char* split_scratch;   // k_split rows in global memory for cuts too large
+                                  // for shared memory (kSplitGlobalWarps * 32 M bytes)
 };
 
 struct PassParams {
@@ -216,6 +218,10 @@ void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
                  const uint32_t* vals, const PassBuffers& b, cudaStream_t st);
 void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffers& b,
                        const Framebuf& fb, cudaStream_t st);
+// Cut sizes whose k_split rows (32 M bytes per warp) exceed this stage in
+// global memory (DevGrid::split_scratch, kSplitGlobalWarps warps).
+constexpr size_t kSplitSmemMax = 200 * 1024;
+constexpr uint32_t kSplitGlobalWarps = 148 * 8;
 void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshold,
                            uint32_t iterations, uint32_t* changes_out, cudaStream_t st);
 void launch_occluded_batch(const DevScene& sc, uint32_t n, const double* a, const double* b,

@@ -159,6 +159,17 @@ def test_async_passes_bit_exact(ref, depth):
     assert_same_state(grid, fb, rr)
 
 
+@pytest.mark.parametrize("m", [4096, 8192])
+def test_large_cuts_bit_exact(ref, m):
+    """Cut sizes whose split-collapse rows no longer fit in shared memory
+    (32 M bytes per warp > 200 KB) take k_split's global-memory rows."""
+    scene = scenes.maze(16384, seed=3, width=40, height=32)
+    cfg = rlcuts.RenderConfig(spp=2, passes=2, sampler=RL, cut=rlcuts.CutConfig(cut_size=m),
+                              hash=rlcuts.HashConfig(capacity=4096, base_tile=0.1))
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+
+
 def test_errors_match_reference_exceptions(ref):
     scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=8, height=8)
     cfg = rlcuts.RenderConfig(spp=3, passes=2, sampler=RL)
