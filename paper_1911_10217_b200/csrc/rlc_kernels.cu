@@ -186,7 +186,9 @@ __device__ __forceinline__ int box_decide(const float4& q0, const float4& q1, co
     ni = fmaxf(ni, tn + en + fmaf(fabsf(nc), r.mb[a], 1e-37f));
     fi = fminf(fi, tf - ef - fmaf(fabsf(fc), r.mb[a], 1e-37f));
   }
-  if (!(no <= fo)) return 0;
+  // reject only when certain: NaN terms (a NaN closest after a NaN-direction
+  // "hit", which the reference's !(tmax < tmin) keeps) go to the exact test
+  if (no > fo) return 0;
   if (r.fast && ni <= fi) return 1;
   return 2;
 }
@@ -272,7 +274,7 @@ __device__ __forceinline__ int box_decide_cam(const float4& q0, const float4& q1
     fo = fminf(fo, fmaf(fabsf(tf), K, tf));
     fi = fminf(fi, fmaf(fabsf(tf), -K, tf));
   }
-  if (!(no <= fo + 1e-30f)) return 0;
+  if (no > fo + 1e-30f) return 0;  // NaN: the exact test decides
   if (fast && ni + 1e-30f <= fi) return 1;
   return 2;
 }
@@ -1678,6 +1680,7 @@ __device__ __forceinline__ WarpArg warp_argmin(WarpArg a) {
   return a;
 }
 
+template <bool GLOBAL_ROWS>
 __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t iterations,
                         uint32_t* changes_out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1687,12 +1690,13 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
   const uint32_t M = g.M;
   // per warp: qA, qB (double), nA, nB, vA, vB (u32) -- in shared memory, or
   // for cuts too large for it in the grid's global scratch (same arithmetic)
-  unsigned char* base = g.split_scratch
+  // (a compile-time choice, so shared-memory rows use shared-memory accesses)
+  unsigned char* base = GLOBAL_ROWS
                             ? g.split_scratch + size_t(blockIdx.x * wpb + wib) * 32 * size_t(M)
                             : smem + size_t(wib) * 16 * size_t(M);
   double* qA = reinterpret_cast<double*>(base);
   double* qB = qA + M;
-  uint32_t* nA = g.split_scratch
+  uint32_t* nA = GLOBAL_ROWS
                      ? reinterpret_cast<uint32_t*>(qB + M)
                      : reinterpret_cast<uint32_t*>(smem + size_t(wpb) * 16 * size_t(M)) +
                            size_t(wib) * 4 * M;
@@ -2178,12 +2182,13 @@ void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshol
                            uint32_t iterations, uint32_t* changes_out, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_split<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   const size_t per_warp = size_t(g.M) * 32;  // 2 doubles + 4 u32 per entry
   if (g.split_scratch) {  // rows in global memory: kSplitGlobalWarps warps
-    k_split<<<kSplitGlobalWarps / 4, 128, 0, st>>>(sc, g, threshold, iterations, changes_out);
+    k_split<true><<<kSplitGlobalWarps / 4, 128, 0, st>>>(sc, g, threshold, iterations,
+                                                        changes_out);
     count_launch();
     return;
   }
@@ -2191,7 +2196,7 @@ void launch_split_collapse(const DevScene& sc, const DevGrid& g, double threshol
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
   const size_t smem = per_warp * wpb;
-  k_split<<<148 * 4, wpb * 32, smem, st>>>(sc, g, threshold, iterations, changes_out);
+  k_split<false><<<148 * 4, wpb * 32, smem, st>>>(sc, g, threshold, iterations, changes_out);
   count_launch();
 }
 

@@ -170,6 +170,50 @@ def test_large_cuts_bit_exact(ref, m):
     assert_same_state(grid, fb, rr)
 
 
+@pytest.mark.parametrize("case", ["looks_away", "one_pixel", "odd_raster"])
+def test_degenerate_frames_bit_exact(ref, case):
+    """No hits at all (every stage runs on empty work), a 1x1 image and an
+    odd raster that fills no 8x4 tile completely."""
+    scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=21, height=13)
+    cam = scene.camera
+    if case == "looks_away":
+        scene = scenes.Scene(scene.vertices, scene.material_ids, scene.materials,
+                             scenes.Camera((0.5, 0.5, -50.0), (0.5, 0.5, -100.0), (0.0, 1.0, 0.0),
+                                           cam.vfov_degrees, 16, 16))
+    elif case == "one_pixel":
+        scene = scene.with_resolution(1, 1)
+    cfg = rlcuts.RenderConfig(spp=3, passes=3, sampler=RL, max_depth=2)
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+    if case == "looks_away":
+        assert grid.occupied_count() == 0
+
+
+def test_nan_rays_follow_the_reference(ref):
+    """A camera whose up vector is parallel to the view direction makes every
+    camera ray NaN.  The reference's slab and Moller-Trumbore tests pass NaN,
+    so it reports NaN-distance hits and then level_for_footprint rejects the
+    NaN area pdf; the device path must do the same (and the batch intersect
+    must return the reference's last-tested triangle)."""
+    scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=21, height=13)
+    cam = scene.camera
+    scene = scenes.Scene(scene.vertices, scene.material_ids, scene.materials,
+                         scenes.Camera((0.5, 0.5, -50.0), (0.5, 0.5, -100.0), cam.up,
+                                       cam.vfov_degrees, 16, 16))
+    cfg = rlcuts.RenderConfig(spp=1, passes=1, sampler=RL)
+    ctx = rlcuts.build_context(scene, cfg)
+    rr = ref.RefRun(scene, cfg)
+    o = np.array([[0.5, 0.5, -50.0]] * 2)
+    d = np.array([[np.nan, np.nan, np.nan], [np.nan, 0.2, -1.0]])
+    t, tri = ctx.intersect(o, d)
+    rt, rtri = rr.intersect(o, d)
+    assert np.array_equal(tri, rtri) and np.array_equal(np.isnan(t), np.isnan(rt))
+    with pytest.raises(ValueError, match="area pdf must be positive"):
+        rr.run_pass(0)
+    with pytest.raises(ValueError, match="area pdf must be positive"):
+        rlcuts.render_pass(ctx, cfg, 0, rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx))
+
+
 def test_errors_match_reference_exceptions(ref):
     scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=8, height=8)
     cfg = rlcuts.RenderConfig(spp=3, passes=2, sampler=RL)
