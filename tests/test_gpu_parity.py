@@ -214,6 +214,21 @@ def test_nan_rays_follow_the_reference(ref):
         rlcuts.render_pass(ctx, cfg, 0, rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx))
 
 
+@pytest.mark.parametrize("scale,offset", [(3e8, 0.0), (1.0, 2e8), (1e-12, 0.0)])
+def test_extreme_coordinates_bit_exact(ref, scale, offset):
+    """Coordinates beyond the fp32 decision range (|x| > 1e8: the exact fp64
+    traversals run) and a tiny scene (fp32 terms near their underflow slack)."""
+    base = scenes.cornell_grid(2, 1, dome_triangles=32, width=32, height=24)
+    cam = base.camera
+    sc = scenes.Scene(base.vertices * scale + offset, base.material_ids, base.materials,
+                      scenes.Camera(tuple(np.array(cam.origin) * scale + offset),
+                                    tuple(np.array(cam.look_at) * scale + offset), cam.up,
+                                    cam.vfov_degrees, cam.width, cam.height))
+    cfg = rlcuts.RenderConfig(spp=2, passes=2, sampler=RL, max_depth=2)
+    _, grid, fb, rr = run_both(ref, sc, cfg)
+    assert_same_state(grid, fb, rr)
+
+
 def test_errors_match_reference_exceptions(ref):
     scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=8, height=8)
     cfg = rlcuts.RenderConfig(spp=3, passes=2, sampler=RL)
