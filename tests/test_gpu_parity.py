@@ -229,6 +229,24 @@ def test_extreme_coordinates_bit_exact(ref, scale, offset):
     assert_same_state(grid, fb, rr)
 
 
+def test_degenerate_emitter_raises_like_the_reference(ref):
+    """A zero-area emissive triangle: sample_triangle_point (scene.cpp:49-51)
+    throws when it is drawn; the device path reports the same error."""
+    base = scenes.cornell_grid(1, 1, dome_triangles=8, width=16, height=16)
+    v = base.vertices.copy()
+    emissive = np.nonzero((base.materials[:, 3:].sum(axis=1) > 0)[base.material_ids])[0]
+    v[emissive[0], 2] = v[emissive[0], 1]  # collapse one emitter to a segment
+    sc = scenes.Scene(v, base.material_ids, base.materials, base.camera)
+    cfg = rlcuts.RenderConfig(spp=8, passes=1, sampler=rlcuts.SamplerKind.uniform)
+    ctx = rlcuts.build_context(sc, cfg)
+    rr = ref.RefRun(sc, cfg)
+    with pytest.raises(ValueError) as want:
+        rr.run_pass(0)
+    with pytest.raises(ValueError) as got:
+        rlcuts.render_pass(ctx, cfg, 0, None, rlcuts.Framebuffer(ctx))
+    assert str(got.value) == str(want.value)
+
+
 def test_errors_match_reference_exceptions(ref):
     scene = scenes.cornell_grid(1, 1, dome_triangles=8, width=8, height=8)
     cfg = rlcuts.RenderConfig(spp=3, passes=2, sampler=RL)
