@@ -4,6 +4,7 @@
 // sm_100 device every create call fails with RLC_ERR_NO_DEVICE.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -201,6 +202,11 @@ struct PassParamsHolder {
 };
 
 struct rlc_context {
+  // Grids and framebuffers keep their context alive: the caller's reference
+  // plus one per live child, so destroying the context before its children
+  // (any order a garbage collector picks) defers the teardown to the last
+  // child.  The render_frame cache's own grid/framebuffer hold no reference.
+  std::atomic<int> refs{1};
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
@@ -348,6 +354,7 @@ struct rlc_context {
 
 struct rlc_grid {
   const rlc_context* ctx = nullptr;
+  bool holds_ref = false;  // false for the context's own render_frame cache
   rlc::DevGrid dev{};
   rlc::HostCut tmpl;
   uint32_t key_bits = 0;
@@ -359,6 +366,7 @@ struct rlc_grid {
 
 struct rlc_framebuffer {
   const rlc_context* ctx = nullptr;
+  bool holds_ref = false;  // false for the context's own render_frame cache
   int32_t width = 0, height = 0;
   DeviceArena arena;
   rlc::Framebuf fb{};
@@ -683,17 +691,25 @@ rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scen
   });
 }
 
+namespace {
+void context_release(const rlc_context* cctx) {
+  rlc_context* ctx = const_cast<rlc_context*>(cctx);
+  if (ctx->refs.fetch_sub(1) != 1) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
+  if (ctx->sstream) cudaStreamSynchronize(ctx->sstream);
+  rlc_grid_destroy(ctx->frame_grid);
+  rlc_framebuffer_destroy(ctx->frame_fb);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+}  // namespace
+
 rlc_status rlc_context_destroy(rlc_context* ctx) {
   return guarded([&] {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
-    if (ctx->sstream) cudaStreamSynchronize(ctx->sstream);
-    rlc_grid_destroy(ctx->frame_grid);
-    rlc_framebuffer_destroy(ctx->frame_fb);
-    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
-    delete ctx;
+    context_release(ctx);
   });
 }
 
@@ -893,6 +909,8 @@ rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg,
     RLC_CK(cudaMemset(g->d_changes, 0, 4));
     g->alpha = cfg->cut.alpha;
     g->harmonic = cfg->cut.alpha_schedule == RLC_ALPHA_HARMONIC ? 1u : 0u;
+    g->holds_ref = true;
+    const_cast<rlc_context*>(ctx)->refs.fetch_add(1);
     *out = g.release();
   });
 }
@@ -900,9 +918,12 @@ rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg,
 rlc_status rlc_grid_destroy(rlc_grid* grid) {
   return guarded([&] {
     if (!grid) return;
-    cudaSetDevice(grid->ctx->device);
-    cudaStreamSynchronize(grid->ctx->stream);
+    const rlc_context* ctx = grid->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    const bool release = grid->holds_ref;
     delete grid;
+    if (release) context_release(ctx);
   });
 }
 
@@ -979,6 +1000,8 @@ rlc_status rlc_framebuffer_create(const rlc_context* ctx, int32_t width, int32_t
     fb->d_image = fb->arena.alloc<double>(3 * npix);
     RLC_CK(cudaMemset(fb->fb.sum, 0, 24 * npix));
     RLC_CK(cudaMemset(fb->fb.count, 0, 8 * npix));
+    fb->holds_ref = true;
+    const_cast<rlc_context*>(ctx)->refs.fetch_add(1);
     *out = fb.release();
   });
 }
@@ -986,9 +1009,13 @@ rlc_status rlc_framebuffer_create(const rlc_context* ctx, int32_t width, int32_t
 rlc_status rlc_framebuffer_destroy(rlc_framebuffer* fb) {
   return guarded([&] {
     if (!fb) return;
-    cudaStreamSynchronize(fb->ctx->stream);
-    if (fb->ctx->sstream) cudaStreamSynchronize(fb->ctx->sstream);  // a pending accumulation
+    const rlc_context* ctx = fb->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->sstream) cudaStreamSynchronize(ctx->sstream);  // a pending accumulation
+    const bool release = fb->holds_ref;
     delete fb;
+    if (release) context_release(ctx);
   });
 }
 
@@ -1183,6 +1210,8 @@ void prepare_frame_cache(rlc_context* ctx, const rlc_render_config* config) {
       const rlc_status st = rlc_grid_create(ctx, config, &g);
       if (st == RLC_ERR_INVALID_ARGUMENT) throw rlc::InvalidArgument(g_err);
       if (st != RLC_OK) throw std::runtime_error(g_err);
+      g->holds_ref = false;  // owned by the context itself
+      ctx->refs.fetch_sub(1);
       ctx->frame_grid = g;
       ctx->frame_cfg = *config;
     }
@@ -1191,6 +1220,8 @@ void prepare_frame_cache(rlc_context* ctx, const rlc_render_config* config) {
     rlc_framebuffer* fb = nullptr;
     if (rlc_framebuffer_create(ctx, ctx->host.cam.width, ctx->host.cam.height, &fb) != RLC_OK)
       throw std::runtime_error(g_err);
+    fb->holds_ref = false;  // owned by the context itself
+    ctx->refs.fetch_sub(1);
     ctx->frame_fb = fb;
   }
   if (config->passes > ctx->frame_hist_cap) {
