@@ -189,6 +189,13 @@ rlc_status rlc_occluded_batch(const rlc_context* ctx, uint32_t n, const double* 
 rlc_status rlc_intersect_batch(const rlc_context* ctx, uint32_t n, const double* origins,
                                const double* dirs, double t_min, double* t_out,
                                int32_t* tri_out);
+/* Diagnostic (parity tests): the closest-hit decision of the SAH tree alone
+ * (DESIGN.md 5.4): as rlc_intersect_batch, but tri_out = -2 where the SAH
+ * traversal defers to the reference-order traversal (exact tie, or the hit's
+ * reference leaf fails the exact slab test, or a ray outside its bounds). */
+rlc_status rlc_intersect_batch_sah(const rlc_context* ctx, uint32_t n, const double* origins,
+                                   const double* dirs, double t_min, double* t_out,
+                                   int32_t* tri_out);
 
 /* ---- bounce sampler trigonometry ---------------------------------------
  * sample_cosine_hemisphere (proj/include/rlcuts/math.hpp:101-107) calls

@@ -571,6 +571,7 @@ void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d) {
   d.fp32_ok = 1;
   for (int a = 0; a < 3; ++a)
     if (!(std::fabs(h.scene_lo[a]) <= 1e8 && std::fabs(h.scene_hi[a]) <= 1e8)) d.fp32_ok = 0;
+  d.nodes_root_leaf = h.nodes.empty() || h.nodes[0].count > 0 ? 1u : 0u;
   d.shadow_eps = h.shadow_eps;
   d.coord_bound = h.coord_bound;
   d.libm_fma = probe_libm_variant() == rlc::libm::kFma ? 1u : 0u;
@@ -830,10 +831,10 @@ rlc_status rlc_occluded_batch(const rlc_context* cctx, uint32_t n, const double*
   });
 }
 
-rlc_status rlc_intersect_batch(const rlc_context* cctx, uint32_t n, const double* origins,
-                               const double* dirs, double t_min, double* t_out,
-                               int32_t* tri_out) {
-  return guarded([&] {
+namespace {
+void intersect_batch(const rlc_context* cctx, uint32_t n, const double* origins,
+                     const double* dirs, double t_min, double* t_out, int32_t* tri_out,
+                     bool sah_only) {
     require(cctx != nullptr && (n == 0 || (origins && dirs && t_out && tri_out)),
             "intersect: null argument");
     if (n == 0) return;
@@ -847,11 +848,23 @@ rlc_status rlc_intersect_batch(const rlc_context* cctx, uint32_t n, const double
     RLC_CK(cudaMemcpyAsync(dorg, origins, 24 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
     RLC_CK(cudaMemcpyAsync(ddir, dirs, 24 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
     rlc::launch_intersect_batch(ctx->dev, n, dorg, ddir, t_min, dt, dtri, ctx->counters,
-                                ctx->stream);
+                                ctx->stream, sah_only);
     RLC_CK(cudaMemcpyAsync(t_out, dt, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     RLC_CK(cudaMemcpyAsync(tri_out, dtri, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     finish_sync(ctx, nullptr);
-  });
+}
+}  // namespace
+
+rlc_status rlc_intersect_batch(const rlc_context* ctx, uint32_t n, const double* origins,
+                               const double* dirs, double t_min, double* t_out,
+                               int32_t* tri_out) {
+  return guarded([&] { intersect_batch(ctx, n, origins, dirs, t_min, t_out, tri_out, false); });
+}
+
+rlc_status rlc_intersect_batch_sah(const rlc_context* ctx, uint32_t n, const double* origins,
+                                   const double* dirs, double t_min, double* t_out,
+                                   int32_t* tri_out) {
+  return guarded([&] { intersect_batch(ctx, n, origins, dirs, t_min, t_out, tri_out, true); });
 }
 
 rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg, rlc_grid** out) {

@@ -198,6 +198,11 @@ __device__ __forceinline__ int box_decide(const float4& q0, const float4& q1, co
 __device__ bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool camera,
                                bool* used, double* t_out, uint32_t* tri_out, uint32_t* err);
 
+// Closest hit on the quantized SAH tree (defined below): 0 miss, 1 hit,
+// 2 undecided (the caller runs the reference-order traversal).
+__device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* t_out,
+                           uint32_t* tri_out);
+
 // intersect(), proj/src/bvh.cpp:124-157: closest hit in the reference's
 // traversal order (pop the right child first), so exact-t ties go to the same
 // triangle.  Every box decision equals the reference's (box_decide, exact
@@ -205,6 +210,8 @@ __device__ bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool
 // Moller-Trumbore.
 __device__ bool intersect(const DevScene& sc, V3 o, V3 d, double tmin, double* t_out,
                           uint32_t* tri_out, uint32_t* err) {
+  const int sah = closest_sah(sc, o, d, tmin, t_out, tri_out);
+  if (sah != 2) return sah == 1;
   bool used;
   const bool got = intersect_wide(sc, o, d, tmin, false, &used, t_out, tri_out, err);
   if (used) return got;
@@ -283,6 +290,8 @@ __device__ __forceinline__ int box_decide_cam(const float4& q0, const float4& q1
 // camera-relative decision test.
 __device__ bool intersect_camera(const DevScene& sc, V3 o, V3 d, double* t_out,
                                  uint32_t* tri_out, uint32_t* err) {
+  const int sah = closest_sah(sc, o, d, 0.0, t_out, tri_out);
+  if (sah != 2) return sah == 1;
   bool used;
   const bool got = intersect_wide(sc, o, d, 0.0, true, &used, t_out, tri_out, err);
   if (used) return got;
@@ -1127,6 +1136,161 @@ __device__ bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool
                 : closest_wide<false>(sc, wn, rf, o, d, inv, tmin, t_out, tri_out, err);
 }
 
+// ---------------------------------------------------------------------------
+// Closest hit on the quantized triangle-level SAH tree.  The
+// reference's answer is the first triangle, in its leaf scan order, whose
+// Moller-Trumbore t is smallest among the triangles its traversal reaches
+// (leaf box passes the slab test against the running `closest`).  Let T1 be
+// the triangle with the smallest MT t (t1) over ALL triangles, found here by
+// any conservative traversal (every triangle with an MT hit below the
+// running closest is reached: the same property k_shadow relies on), and
+// assume no other triangle's MT t equals t1.  If T1's reference leaf passes
+// the exact slab test against t1, then when the reference reaches that leaf
+// its `closest` is > t1 (no tie), the test passes (monotone in t_max, and
+// the ancestors passed earlier on larger boxes with a larger closest), T1 is
+// accepted, and nothing after it can beat t1: the reference returns T1.
+// Otherwise (the leaf test fails, or an exact tie) the answer depends on the
+// reference's order and the caller runs the ordered traversal.  Nodes are
+// culled against fl32_ru(closest); a triangle at t <= closest has a
+// conservative box entry <= t, so ties are always seen.
+// ---------------------------------------------------------------------------
+#ifndef RLC_CLOSEST_SAH
+#define RLC_CLOSEST_SAH 1
+#endif
+constexpr int kSahStack = 32;
+
+__device__ __forceinline__ bool tri_t(const TriAccel* tris, uint32_t i, V3 o, V3 d, double* tout) {
+  const double2* p = reinterpret_cast<const double2*>(tris + i);
+  const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), e = __ldg(p + 3),
+                f = __ldg(p + 4);
+  const V3 p0{a.x, a.y, b.x};
+  const V3 e1{b.y, c.x, c.y};
+  const V3 e2{e.x, e.y, f.x};
+  const V3 pv = cross(d, e2);
+  const double det = dot(e1, pv);
+  const double inv_det = 1.0 / det;
+  const V3 tv = o - p0;
+  const double u = dot(tv, pv) * inv_det;
+  const V3 qv = cross(tv, e1);
+  const double v = dot(d, qv) * inv_det;
+  *tout = dot(e2, qv) * inv_det;
+  return !(fabs(det) < 1e-14) & !(u < 0 || u > 1) & !(v < 0 || u + v > 1);
+}
+
+__device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* t_out,
+                           uint32_t* tri_out) {
+  if (!RLC_CLOSEST_SAH || sc.wide_q == nullptr || !sc.fp32_ok || sc.nodes_root_leaf) return 2;
+  const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+  const double ia[3] = {inv.x, inv.y, inv.z}, oa[3] = {o.x, o.y, o.z};
+  float finv[3], fb0[3];
+  uint32_t neg = 0;
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ok &= fabs(ia[a]) <= 1e30;              // finite fp32 inverse (NaN, axis-parallel: no)
+    ok &= fabs(oa[a]) <= sc.coord_bound;   // the padding bound of the shadow tree
+    finv[a] = float(ia[a]);
+    fb0[a] = -(float(oa[a]) * finv[a]);
+    neg |= (ia[a] < 0 ? 1u : 0u) << a;
+  }
+  if (!ok) return 2;
+  const float tmin_f = __double2float_rd(tmin);
+  double closest = HUGE_VAL;
+  float tmax_f = HUGE_VALF;
+  uint32_t hit = kNoSlot;
+  bool tie = false;
+  uint32_t stk_e[kSahStack];
+  float stk_t[kSahStack];
+  int sp = 0;
+  uint32_t cur = 0;
+  while (true) {
+    if (!(cur & kWideLeaf)) {
+      const uint4* p = reinterpret_cast<const uint4*>(sc.wide_q + cur);
+      const uint4 w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2), w3 = __ldg(p + 3);
+      const uint32_t ql[3] = {w1.x, w1.y, w1.z}, qh[3] = {w1.w, w2.x, w2.y};
+      const float org[3] = {__uint_as_float(w0.x), __uint_as_float(w0.y), __uint_as_float(w0.z)};
+      uint32_t c[kWide] = {w2.z, w2.w, w3.x, w3.y};
+      float A[3], B[3];
+      uint32_t nw[3], fw[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const bool ng = (neg >> a) & 1u;
+        nw[a] = ng ? qh[a] : ql[a];
+        fw[a] = ng ? ql[a] : qh[a];
+        A[a] = __uint_as_float(((w0.w >> (8 * a)) & 255u) << 23) * finv[a];
+        B[a] = fmaf(org[a], finv[a], fb0[a]);
+      }
+      float tn[kWide];
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < kWide; ++k) {
+        float n3[3], f3[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          n3[a] = fmaf(float((nw[a] >> (8 * k)) & 255u), A[a], B[a]);
+          f3[a] = fmaf(float((fw[a] >> (8 * k)) & 255u), A[a], B[a]);
+        }
+        tn[k] = fmaxf(fmax3(tmin_f, n3[0], n3[1]), n3[2]);
+        const float fk = fminf(fmin3(tmax_f, f3[0], f3[1]), f3[2]);
+        const bool pass = tn[k] <= fk && c[k] != kWideEmpty;
+        m |= pass ? (1u << k) : 0u;
+        if (!pass) tn[k] = HUGE_VALF;
+      }
+#define RLC_CSWAP(i, j)                                   \
+  if (tn[j] < tn[i]) {                                    \
+    const float tt = tn[i]; tn[i] = tn[j]; tn[j] = tt;    \
+    const uint32_t cc = c[i]; c[i] = c[j]; c[j] = cc;     \
+  }
+      RLC_CSWAP(0, 1) RLC_CSWAP(2, 3) RLC_CSWAP(0, 2) RLC_CSWAP(1, 3) RLC_CSWAP(1, 2)
+#undef RLC_CSWAP
+      const int hits = __popc(m);
+      if (hits > 0) {
+        if (sp + hits - 1 > kSahStack) return 2;
+#pragma unroll
+        for (int k = kWide - 1; k >= 1; --k)
+          if (k < hits) {
+            stk_e[sp] = c[k];
+            stk_t[sp] = tn[k];
+            ++sp;
+          }
+        cur = c[0];
+        continue;
+      }
+    } else {
+      const uint32_t first = leaf_first(cur), cnt = leaf_count(cur);
+      for (uint32_t i = first; i < first + cnt; ++i) {
+        double t;
+        if (tri_t(sc.tris_s, i, o, d, &t) && !(t <= tmin)) {
+          if (t < closest) {
+            closest = t;
+            hit = i;
+            tie = false;
+            tmax_f = __double2float_ru(closest);
+          } else if (!(t > closest)) {
+            tie = true;  // an exact tie (or NaN): the reference's order decides
+          }
+        }
+      }
+    }
+    bool found = false;
+    while (sp > 0) {
+      --sp;
+      if (stk_t[sp] <= tmax_f) {
+        cur = stk_e[sp];
+        found = true;
+        break;
+      }
+    }
+    if (!found) break;
+  }
+  if (hit == kNoSlot) return 0;
+  if (tie) return 2;
+  if (!box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf_s + hit)), o, inv, tmin, closest)) return 2;
+  *t_out = closest;
+  *tri_out = sc.tris_s[hit].tri_id;
+  return 1;
+}
+
 __device__ __forceinline__ bool tri_any(const TriAccel* tris, uint32_t i, V3 o, V3 d, double tmin,
                                         double tmax) {
   const double2* p = reinterpret_cast<const double2*>(tris + i);
@@ -1831,11 +1995,17 @@ __global__ void k_segments_out(uint32_t n, const SampleRec* __restrict__ srec,
 __global__ void k_intersect_batch(DevScene sc, uint32_t n, const double* __restrict__ org,
                                   const double* __restrict__ dir, double tmin,
                                   double* __restrict__ t_out, int32_t* __restrict__ tri_out,
-                                  unsigned int* err) {
+                                  unsigned int* err, uint32_t sah_only) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double t;
   uint32_t tri;
+  if (sah_only) {  // diagnostic: the SAH decision alone, -2 when it defers to the ordered path
+    const int r = closest_sah(sc, ld3(org + 3 * size_t(i)), ld3(dir + 3 * size_t(i)), tmin, &t, &tri);
+    t_out[i] = r == 1 ? t : -1.0;
+    tri_out[i] = r == 1 ? int32_t(tri) : (r == 0 ? -1 : -2);
+    return;
+  }
   if (intersect(sc, ld3(org + 3 * size_t(i)), ld3(dir + 3 * size_t(i)), tmin, &t, &tri, err)) {
     t_out[i] = t;
     tri_out[i] = int32_t(tri);
@@ -1858,10 +2028,11 @@ void launch_occluded_batch(const DevScene& sc, uint32_t n, const double* a, cons
 
 void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, const double* dir,
                             double tmin, double* t_out, int32_t* tri_out,
-                            unsigned long long* counters, cudaStream_t st) {
+                            unsigned long long* counters, cudaStream_t st, bool sah_only) {
   if (n == 0) return;
   k_intersect_batch<<<blocks_for(n, 128), 128, 0, st>>>(
-      sc, n, org, dir, tmin, t_out, tri_out, reinterpret_cast<unsigned int*>(counters + kCntErr));
+      sc, n, org, dir, tmin, t_out, tri_out, reinterpret_cast<unsigned int*>(counters + kCntErr),
+      sah_only ? 1u : 0u);
   count_launch();
 }
 

@@ -95,6 +95,7 @@ struct DevScene {
   uint32_t num_lights;
   uint32_t num_tris;
   uint32_t fp32_ok;  // scene coordinates within 1e8: the fp32 shadow pre-test is valid
+  uint32_t nodes_root_leaf;  // the reference BVH is a single leaf (no wide trees apply)
   uint32_t libm_fma; // host libm build whose sin/cos the bounce sampler restates (rlc_libm.h)
   double shadow_eps;
   double coord_bound;  // S: k_shadow's lean test holds for ray origins within S
@@ -229,7 +230,7 @@ void launch_occluded_batch(const DevScene& sc, uint32_t n, const double* a, cons
                            cudaStream_t st);
 void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, const double* dir,
                             double tmin, double* t_out, int32_t* tri_out,
-                            unsigned long long* counters, cudaStream_t st);
+                            unsigned long long* counters, cudaStream_t st, bool sah_only = false);
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
 // Per-pixel squared error of the resolved framebuffer against `ref`
 // (mse's summand, image.cpp:119-121), for the ordered host sum.

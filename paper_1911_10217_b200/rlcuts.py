@@ -171,13 +171,17 @@ class RenderContext:
                                               out.ctypes.data_as(C.POINTER(C.c_uint8))))
         return out.astype(bool)
 
-    def intersect(self, origins: np.ndarray, dirs: np.ndarray, t_min: float = 0.0):
-        """intersect() (bvh.hpp:35-36): (t, triangle id), -1 on a miss."""
+    def intersect(self, origins: np.ndarray, dirs: np.ndarray, t_min: float = 0.0,
+                  sah_only: bool = False):
+        """intersect() (bvh.hpp:35-36): (t, triangle id), -1 on a miss.  With
+        sah_only, the SAH tree's decision alone (-2: deferred to the ordered
+        traversal)."""
         o = np.ascontiguousarray(origins, np.float64).reshape(-1, 3)
         d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
         t = np.zeros(o.shape[0], np.float64)
         tri = np.zeros(o.shape[0], np.int32)
-        _check(_lib.load().rlc_intersect_batch(self.handle, o.shape[0], _dptr(o), _dptr(d),
+        fn = _lib.load().rlc_intersect_batch_sah if sah_only else _lib.load().rlc_intersect_batch
+        _check(fn(self.handle, o.shape[0], _dptr(o), _dptr(d),
                                                t_min, _dptr(t),
                                                tri.ctypes.data_as(C.POINTER(C.c_int32))))
         return t, tri

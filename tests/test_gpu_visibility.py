@@ -98,3 +98,52 @@ def test_occluded_many_emitter_maze(ref):
     got, want = ctx.occluded(a, b), rr.occluded(a, b)
     assert np.array_equal(got, want)
     assert 0 < want.sum() < n
+
+
+def _check_sah(ctx, rr, o, d, t_min=0.0):
+    """Full intersect and the SAH decision alone against the reference: every
+    decided ray (tri != -2) must already be the reference's answer."""
+    t, tri = ctx.intersect(o, d, t_min)
+    rt, rtri = rr.intersect(o, d, t_min)
+    assert np.array_equal(tri, rtri) and np.array_equal(t, rt)
+    st, stri = ctx.intersect(o, d, t_min, sah_only=True)
+    dec = stri != -2
+    assert np.array_equal(stri[dec], rtri[dec]) and np.array_equal(st[dec], rt[dec])
+    return dec, rtri
+
+
+def test_intersect_sah_decisions_and_tmin(ref, shadow_tree):
+    """Bounce-like queries: origins on the soup's triangles, t_min > 0."""
+    scene = random_soup(6000, 17, 8.0, 0.7)
+    ctx, rr = both(ref, scene)
+    rng = np.random.default_rng(11)
+    v = scene.vertices
+    pick = rng.integers(0, v.shape[0], 8000)
+    u = rng.random((8000, 2))
+    u = np.where(u.sum(1, keepdims=True) > 1, 1 - u, u)
+    o = v[pick, 0] + u[:, :1] * (v[pick, 1] - v[pick, 0]) + u[:, 1:] * (v[pick, 2] - v[pick, 0])
+    d = rng.normal(size=(8000, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    dec, rtri = _check_sah(ctx, rr, o, d, t_min=1e-3)
+    assert (rtri >= 0).sum() > 3000
+    # the SAH closest hit runs on the quantized tree (absent with the 128-byte nodes)
+    assert dec.mean() > 0.9 if shadow_tree != "tris-128B" else not dec.any()
+
+
+def test_intersect_exact_ties_defer_to_reference_order(ref):
+    """Every triangle twice (identical Moller-Trumbore t): the reference keeps
+    the first one its leaf scan meets; the SAH traversal must defer."""
+    base = random_soup(3000, 23, 8.0, 0.8)
+    v = base.vertices
+    mats_idx = np.arange(2 * v.shape[0]) % 2
+    scene = Scene(np.concatenate([v, v[::-1]]), mats_idx.astype(np.uint32),
+                  np.array([[0.5, 0.5, 0.5, 0, 0, 0], [0, 0, 0, 1, 1, 1]], float),
+                  scenes.Camera((0, 0, -5), (0, 0, 0), (0, 1, 0), 45, 8, 8), "dup")
+    ctx, rr = both(ref, scene)
+    rng = np.random.default_rng(12)
+    o = rng.uniform(0, 8, (6000, 3))
+    d = rng.normal(size=(6000, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    dec, rtri = _check_sah(ctx, rr, o, d)
+    hits = rtri >= 0
+    assert hits.sum() > 1000 and not dec[hits].any()  # every hit is a tie
