@@ -195,7 +195,17 @@ __device__ __forceinline__ int box_decide(const float4& q0, const float4& q1, co
 
 // Closest hit through the collapsed reference tree (defined with the wide
 // traversal helpers below); false in *used when the ray needs the binary path.
-__device__ bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool camera,
+// RLC_COLD_NOINLINE=1 moves it out of line (the rare path after the SAH
+// closest hit); measured slower: the call spills more registers.
+#ifndef RLC_COLD_NOINLINE
+#define RLC_COLD_NOINLINE 0  // measured: noinline spills more and is 8% slower on c3
+#endif
+#if RLC_COLD_NOINLINE
+#define RLC_COLD __noinline__
+#else
+#define RLC_COLD
+#endif
+__device__ RLC_COLD bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool camera,
                                bool* used, double* t_out, uint32_t* tri_out, uint32_t* err);
 
 // Closest hit on the quantized SAH tree (defined below): 0 miss, 1 hit,
@@ -1100,8 +1110,9 @@ __device__ __forceinline__ bool closest_wide(const DevScene& sc, const Wide4* __
   return true;
 }
 
-__device__ bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool camera,
-                               bool* used, double* t_out, uint32_t* tri_out, uint32_t* err) {
+__device__ RLC_COLD bool intersect_wide(const DevScene& sc, V3 o, V3 d, double tmin, bool camera,
+                                        bool* used, double* t_out, uint32_t* tri_out,
+                                        uint32_t* err) {
   static_assert(kWide == 4, "closest_wide loads 4-wide nodes");
   const Wide4* wn = camera ? sc.wide_cam : sc.wide_ref;
   const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
