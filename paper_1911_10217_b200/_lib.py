@@ -96,6 +96,7 @@ SIGNATURES = {
     "rlc_libm_sincos_host": (C.c_int, [C.c_int32, C.c_uint64, _dp, _dp, _dp]),
     "rlc_intersect_batch": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp,
                                       C.POINTER(C.c_int32)]),
+    "rlc_debug_trav_stats": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
     "rlc_intersect_batch_sah": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp,
                                           C.POINTER(C.c_int32)]),
     "rlc_grid_create": (C.c_int, [_P, C.POINTER(RenderConfigC), _PP]),

@@ -571,7 +571,10 @@ std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
     const Wide4& n = w[i];
     WideQ& q = out[i];
     std::memset(&q, 0, sizeof(q));
-    for (int c = 0; c < 4; ++c) q.child[c] = n.child[c];
+    for (int c = 0; c < 4; ++c) {
+      q.child[c] = n.child[c];
+      if (n.child[c] != kWideEmpty) q.valid |= 1u << c;
+    }
     for (int a = 0; a < 3; ++a) {
       float lo = HUGE_VALF, hi = -HUGE_VALF;
       for (int c = 0; c < 4; ++c)

@@ -770,6 +770,13 @@ rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* count
   });
 }
 
+rlc_status rlc_debug_trav_stats(int32_t reset, uint64_t* out8) {
+  return guarded([&] {
+    require(out8 != nullptr, "rlc_debug_trav_stats: null argument");
+    rlc::trav_stats(out8, reset != 0);
+  });
+}
+
 rlc_status rlc_libm_variant(int32_t* variant) {
   return guarded([&] {
     require(variant != nullptr, "rlc_libm_variant: null argument");

@@ -126,7 +126,8 @@ struct alignas(64) WideQ {
   uint8_t qlo[3][4];      // [axis][child]
   uint8_t qhi[3][4];
   uint32_t child[4];      // as Wide4::child
-  uint32_t pad1[2];
+  uint32_t valid;         // bit c: child[c] is not kWideEmpty
+  uint32_t pad1;
 };
 static_assert(sizeof(WideQ) == 64, "quantized wide nodes are 64 bytes");
 

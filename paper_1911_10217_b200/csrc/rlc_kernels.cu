@@ -36,6 +36,23 @@ constexpr unsigned kFull = 0xffffffffu;
 
 uint64_t launches() { return g_launches.load(); }
 
+// Opt-in traversal statistics (build with EXTRA=-DRLC_TRAV_STATS): per-ray
+// node steps and triangle tests of k_shadow [0..2] and closest_sah [3..5]
+// (rays, nodes, triangles).  Diagnostics only; zero in the product build.
+__device__ unsigned long long g_trav[8];
+#ifdef RLC_TRAV_STATS
+#define RLC_STAT(i, v) atomicAdd(&g_trav[i], (unsigned long long)(v))
+#else
+#define RLC_STAT(i, v) ((void)0)
+#endif
+void trav_stats(uint64_t out[8], bool reset) {
+  cudaMemcpyFromSymbol(out, g_trav, sizeof(uint64_t) * 8);
+  if (reset) {
+    const unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_trav, z, sizeof(z));
+  }
+}
+
 static inline uint32_t blocks_for(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
 
 // ---------------------------------------------------------------------------
@@ -1222,8 +1239,10 @@ __device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* 
   float stk_t[kSahStack];
   int sp = 0;
   uint32_t cur = 0;
+  uint32_t st_nodes = 0, st_tris = 0;
   while (true) {
     if (!(cur & kWideLeaf)) {
+      ++st_nodes;
       const uint4* p = reinterpret_cast<const uint4*>(sc.wide_q + cur);
       const uint4 w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2), w3 = __ldg(p + 3);
       const uint32_t ql[3] = {w1.x, w1.y, w1.z}, qh[3] = {w1.w, w2.x, w2.y};
@@ -1251,7 +1270,7 @@ __device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* 
         }
         tn[k] = fmaxf(fmax3(tmin_f, n3[0], n3[1]), n3[2]);
         const float fk = fminf(fmin3(tmax_f, f3[0], f3[1]), f3[2]);
-        const bool pass = tn[k] <= fk && c[k] != kWideEmpty;
+        const bool pass = tn[k] <= fk && ((w3.z >> k) & 1u);  // w3.z: non-empty children
         m |= pass ? (1u << k) : 0u;
         if (!pass) tn[k] = HUGE_VALF;
       }
@@ -1277,6 +1296,7 @@ __device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* 
       }
     } else {
       const uint32_t first = leaf_first(cur), cnt = leaf_count(cur);
+      st_tris += cnt;
       for (uint32_t i = first; i < first + cnt; ++i) {
         double t;
         if (tri_t(sc.tris_s, i, o, d, &t) && !(t <= tmin)) {
@@ -1302,6 +1322,9 @@ __device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* 
     }
     if (!found) break;
   }
+  RLC_STAT(3, 1);
+  RLC_STAT(4, st_nodes);
+  RLC_STAT(5, st_tris);
   if (hit == kNoSlot) return 0;
   if (tie) return 2;
   if (!box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf_s + hit)), o, inv, tmin, closest)) return 2;
@@ -1344,6 +1367,7 @@ __device__ __forceinline__ void mark_occluded(SampleRec* srec, uint32_t idx) {
 #ifndef RLC_SHADOW_BLOCKS
 #define RLC_SHADOW_BLOCKS 7  // minimum resident blocks per SM (register budget)
 #endif
+template <bool QUANT>
 __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(DevScene sc,
                                                            const ShadowRay* __restrict__ rays,
                                                            const uint32_t* __restrict__ order,
@@ -1411,6 +1435,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
             } else {
               cur = 0;
               active = true;
+              RLC_STAT(0, 1);
             }
           }
         }
@@ -1425,10 +1450,11 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
     // register; the first leaf met is postponed and traversal continues
     // while some lane of the warp has not found a leaf yet
     while (cur != kDone && !(cur & kWideLeaf)) {
+      RLC_STAT(1, 1);
       float tn[kWide];
       uint32_t mi, m;
       uint32_t c[kWide];
-      if (sc.wide_q) {  // 64-byte quantized node: no inner test (leaves checked exactly)
+      if constexpr (QUANT) {  // 64-byte quantized node: no inner test (leaves checked exactly)
         const uint4* p = reinterpret_cast<const uint4*>(sc.wide_q + cur);
         const uint4 w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2), w3 = __ldg(p + 3);
         const uint32_t ql[3] = {w1.x, w1.y, w1.z}, qh[3] = {w1.w, w2.x, w2.y};
@@ -1459,9 +1485,11 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
         m = 0;
 #pragma unroll
         for (int k = 0; k < kWide; ++k) {
-          m |= (nb[k] <= fb[k]) ? (1u << k) : 0u;
-          tn[k] = nb[k];
+          const bool pass = nb[k] <= fb[k];
+          m |= pass ? (1u << k) : 0u;
+          tn[k] = pass ? nb[k] : HUGE_VALF;
         }
+        m &= w3.z;  // non-empty children
         mi = 0;
       } else {
         constexpr int Q = kWide / 4;  // float4 per [axis] row
@@ -1482,12 +1510,14 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
         }
         m = boxw_s(lo, hi, rf, tn, &mi);
       }
+      if constexpr (!QUANT) {
 #pragma unroll
-      for (int k = 0; k < kWide; ++k) {
-        if (c[k] == kWideEmpty) m &= ~(1u << k);
-        if (((mi >> k) & (c[k] >> 31)) && (c[k] & kLeafPure))
-          c[k] |= kLeafVerified;  // leaf proven reached
-        if (!(m & (1u << k))) tn[k] = HUGE_VALF;
+        for (int k = 0; k < kWide; ++k) {
+          if (c[k] == kWideEmpty) m &= ~(1u << k);
+          if (((mi >> k) & (c[k] >> 31)) && (c[k] & kLeafPure))
+            c[k] |= kLeafVerified;  // leaf proven reached
+          if (!(m & (1u << k))) tn[k] = HUGE_VALF;
+        }
       }
       if (sp + kWide - 1 > kShadowStack) {
         atomicOr(err, kErrStackOverflow);
@@ -1532,6 +1562,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
     bool hit = false;
     while (leaf != 0) {
       const uint32_t first = leaf_first(leaf), cnt = leaf_count(leaf);
+      RLC_STAT(2, cnt);
       if (leaf & kLeafPure) {  // one reference leaf: one exact test for the leaf
         for (uint32_t i = first; i < first + cnt; ++i)
           hit |= tri_any(sc.tris_s, i, o, d, tmin, tmax);
@@ -2304,7 +2335,7 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   static int per_sm = 0, sms = 0;
   if (per_sm == 0) {
     int dev = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shadow, kShadowThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shadow<true>, kShadowThreads, 0);
     if (const char* e = getenv("RLC_SHADOW_BLOCKS_PER_SM"))  // tuning knob (co-residency)
       if (atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
     if (per_sm < 1) per_sm = 1;
@@ -2315,7 +2346,8 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   // with the update-record sort running beside it, one block slot per SM is
   // left to the sort (measured: 1.69 vs 1.71 ms per c3 frame)
   const int use = leave_room && per_sm > 1 ? per_sm - 1 : per_sm;
-  k_shadow<<<use * sms, kShadowThreads, 0, st>>>(
+  auto kern = sc.wide_q ? k_shadow<true> : k_shadow<false>;
+  kern<<<use * sms, kShadowThreads, 0, st>>>(
       sc, b.rays, order, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
   count_launch();
 }

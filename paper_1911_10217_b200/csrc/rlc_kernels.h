@@ -187,6 +187,7 @@ struct Framebuf {
 
 // Each launcher adds its kernel launches to a process-wide counter.
 uint64_t launches();
+void trav_stats(uint64_t out[8], bool reset);
 
 void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
                     const PassBuffers& b, cudaStream_t st);

@@ -524,3 +524,12 @@ def libm_sincos_host(x: np.ndarray, variant: int):
 
 def kernel_launches() -> int:
     return int(_lib.load().rlc_kernel_launches())
+
+
+def trav_stats(reset: bool = True) -> dict:
+    """Traversal counters of a -DRLC_TRAV_STATS build (zeros otherwise)."""
+    out = (C.c_uint64 * 8)()
+    _check(_lib.load().rlc_debug_trav_stats(1 if reset else 0, out))
+    v = list(out)
+    return {"shadow_rays": v[0], "shadow_nodes": v[1], "shadow_tris": v[2],
+            "closest_rays": v[3], "closest_nodes": v[4], "closest_tris": v[5]}
