@@ -13,6 +13,8 @@
 #include "rlc_build.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -75,6 +77,18 @@ V3 vert(const rlc_scene_desc& d, uint32_t t, int k) {
   const double* p = d.vertices + size_t(t) * 9 + size_t(k) * 3;
   return V3{p[0], p[1], p[2]};
 }
+
+// RLC_BUILD_TIMING=1: per-phase host build times on stderr (diagnostics).
+struct PhaseTimer {
+  bool on = std::getenv("RLC_BUILD_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "build %-16s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t0).count());
+  }
+};
 
 void put3(double* dst, V3 v) {
   dst[0] = v.x;
@@ -494,7 +508,8 @@ std::vector<BvhNode> sah_over_tris(const rlc_scene_desc& d, const HostScene& hs,
 // (leaf_of[i]: reference leaf of triangle position i; null: always).
 std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double* origin,
                                  double grow = 0.0, double pad = 0.0,
-                                 const std::vector<uint32_t>* leaf_of = nullptr) {
+                                 const std::vector<uint32_t>* leaf_of = nullptr,
+                                 std::vector<std::array<uint32_t, kWide>>* kids_out = nullptr) {
   std::vector<uint32_t> wid(nodes.size(), kWideEmpty);
   std::vector<std::array<uint32_t, kWide>> kids;
   kids.reserve(nodes.size() / 2 + 1);
@@ -558,6 +573,7 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
                                 : wid[b];
     }
   });
+  if (kids_out) *kids_out = std::move(kids);
   return wide;
 }
 
@@ -627,7 +643,26 @@ std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
 //    children in left-to-right order, so the reference's leaf order (right
 //    subtree first) is a plain stack traversal; `wide_cam` (camera-relative
 //    boxes) is filled in with the camera constants.
-void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) {
+// Per binary node of a tree whose leaves are [a, a + count) ranges in DFS
+// order (children after their parent): the [first, end) range it covers.
+void node_ranges(const std::vector<BvhNode>& bin, std::vector<uint32_t>& first,
+                 std::vector<uint32_t>& end) {
+  first.assign(bin.size(), 0);
+  end.assign(bin.size(), 0);
+  for (size_t k = bin.size(); k-- > 0;) {
+    const BvhNode& nd = bin[k];
+    if (nd.count > 0) {
+      first[k] = nd.a;
+      end[k] = nd.a + nd.count;
+    } else {
+      first[k] = std::min(first[nd.a], first[nd.b]);
+      end[k] = std::max(end[nd.a], end[nd.b]);
+    }
+  }
+}
+
+void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
+  PhaseTimer pt;
   out.wide.clear();
   out.wide_ref.clear();
   out.tri_leaf.assign(out.tris.size(), 0);
@@ -635,6 +670,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     for (uint32_t t = out.nodes[i].a; out.nodes[i].count > 0 && t < out.nodes[i].a + out.nodes[i].count; ++t)
       out.tri_leaf[t] = uint32_t(i);
   });
+  pt.lap("tri_leaf");
   if (out.nodes.empty() || out.nodes[0].count > 0) {  // a leaf root: exact paths only
     out.tris_s = out.tris;
     out.tri_leaf_s = out.tri_leaf;
@@ -643,7 +679,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
   if (out.tris.size() >= (1u << 27)) throw InvalidArgument("build_scene_bvh: too many triangles");
   // the closest-hit trees depend only on the reference BVH: built beside the shadow tree
   auto f_ref = std::async(std::launch::async, [&] {
-    out.wide_ref = collapse_wide(out.nodes, nullptr);
+    if (keep == nullptr) out.wide_ref = collapse_wide(out.nodes, nullptr);
   });
   // shadow tree: SAH over triangles (default), over the reference leaves
   // (RLC_SHADOW_TREE=leaves) or the reference tree (=reference)
@@ -662,17 +698,21 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
     out.tri_leaf_s = out.tri_leaf;
     out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
                              S * 0x1.0p-21);
-  } else if (keep != nullptr && !keep->shadow_bin.empty()) {
+  } else if (keep != nullptr && !keep->shadow_bin.empty() && !keep->wide_kids.empty()) {
     // dynamic update: the creation SAH topology refitted to the moved
-    // triangles (any conservative tree is exact); leaves whose
-    // triangles now lie in different reference leaves lose kLeafPure
+    // triangles (any conservative tree is exact): every wide
+    // child box is the union of its moved triangles' boxes (its tris_s
+    // range); leaves whose triangles now lie in different reference leaves
+    // lose kLeafPure
     std::vector<uint32_t> leaf_of_id(out.tris.size());
-    for (size_t j = 0; j < out.tris.size(); ++j) leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j];
-    out.tris_s = keep->tris_s;
-    out.tri_leaf_s.resize(out.tris_s.size());
-    std::vector<Box> tb(out.tris_s.size());
-    parallel_for(out.tris_s.size(), [&](size_t i) {
+    parallel_for(out.tris.size(), [&](size_t j) { leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j]; });
+    const size_t nt = keep->tris_s.size();
+    out.tris_s.resize(nt);
+    out.tri_leaf_s.resize(nt);
+    std::vector<Box> tb(nt);
+    parallel_for(nt, [&](size_t i) {
       TriAccel& ta = out.tris_s[i];
+      ta = keep->tris_s[i];
       const uint32_t id = ta.tri_id;
       const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
       put3(ta.p0, p0);
@@ -683,23 +723,42 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
       tb[i].grow(p1);
       tb[i].grow(p2);
     });
-    out.shadow_bin = keep->shadow_bin;
-    for (size_t k = out.shadow_bin.size(); k-- > 0;) {  // children follow their parent
-      BvhNode& nd = out.shadow_bin[k];
-      Box b;
-      if (nd.count > 0) {
-        for (uint32_t i = nd.a; i < nd.a + nd.count; ++i) b.grow(tb[i]);
-      } else {
-        const BvhNode &l = out.shadow_bin[nd.a], &r = out.shadow_bin[nd.b];
-        b.grow(V3{l.lo[0], l.lo[1], l.lo[2]});
-        b.grow(V3{l.hi[0], l.hi[1], l.hi[2]});
-        b.grow(V3{r.lo[0], r.lo[1], r.lo[2]});
-        b.grow(V3{r.hi[0], r.hi[1], r.hi[2]});
+    pt.lap("refit tris");
+    const auto& kids = keep->wide_kids;
+    const auto& bin = keep->shadow_bin;
+    const double pad = S * 0x1.0p-21;
+    out.wide.resize(kids.size());
+    parallel_for(kids.size(), [&](size_t w) {
+      Wide4& n = out.wide[w];
+      std::memset(&n, 0, sizeof(n));
+      for (int c = 0; c < kWide; ++c) {
+        const uint32_t b = kids[w][c];
+        if (b == kWideEmpty) {
+          n.child[c] = kWideEmpty;
+          for (int a = 0; a < 3; ++a) {
+            n.lo[a][c] = HUGE_VALF;
+            n.hi[a][c] = -HUGE_VALF;
+          }
+          continue;
+        }
+        Box bx;
+        for (uint32_t i = keep->bin_first[b]; i < keep->bin_end[b]; ++i) bx.grow(tb[i]);
+        for (int a = 0; a < 3; ++a) {  // as collapse_wide (no origin, no growth)
+          n.lo[a][c] = round_down(comp(bx.lo, a) - pad);
+          n.hi[a][c] = round_up(comp(bx.hi, a) + pad);
+        }
+        const BvhNode& bn = bin[b];
+        if (bn.count > 0) {
+          bool pure = true;
+          for (uint32_t k = 1; k < bn.count; ++k)
+            pure &= out.tri_leaf_s[bn.a + k] == out.tri_leaf_s[bn.a];
+          n.child[c] = kWideLeaf | ((bn.count - 1) << 28) | (pure ? kLeafPure : 0u) | bn.a;
+        } else {
+          n.child[c] = keep->wide[w].child[c];  // internal: the creation numbering
+        }
       }
-      put3(nd.lo, b.lo);
-      put3(nd.hi, b.hi);
-    }
-    out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s);
+    }, 64);
+    pt.lap("wide refit");
   } else {
     std::vector<uint32_t> perm;
     out.tris_s.resize(out.tris.size());
@@ -709,12 +768,16 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep) 
       out.tris_s[i] = out.tris[perm[i]];
       out.tri_leaf_s[i] = out.tri_leaf[perm[i]];
     }
-    out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s);
+    out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s,
+                             &out.wide_kids);
+    node_ranges(out.shadow_bin, out.bin_first, out.bin_end);
   }
   f_ref.get();
+  pt.lap("wide_ref");
   const char* q = std::getenv("RLC_SHADOW_QUANT");
   out.wide_q.clear();
   if (!(q && std::string(q) == "0")) out.wide_q = quantize_wide(out.wide);
+  pt.lap("quantize");
 }
 
 }  // namespace
@@ -857,7 +920,8 @@ void level_thresholds(double out[kMaxLevel + 1]) {
 }
 
 void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, HostScene& out,
-                      const HostScene* keep) {
+                      HostScene* keep) {
+  PhaseTimer pt;
   if (d.num_triangles == 0 || d.vertices == nullptr || d.material_ids == nullptr)
     throw InvalidArgument("build_scene_bvh: empty scene");
   if (d.num_materials == 0 || d.materials == nullptr)
@@ -881,48 +945,49 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   }
   out.tri_mat.assign(d.material_ids, d.material_ids + d.num_triangles);
   out.tri_normal.resize(size_t(3) * d.num_triangles);
-  for (uint32_t t = 0; t < d.num_triangles; ++t) {
-    const V3 p0 = vert(d, t, 0);
-    put3(&out.tri_normal[size_t(3) * t], normalize(cross(vert(d, t, 1) - p0, vert(d, t, 2) - p0)));
-  }
-
+  parallel_for(d.num_triangles, [&](size_t t) {
+    const V3 p0 = vert(d, uint32_t(t), 0);
+    put3(&out.tri_normal[3 * t],
+         normalize(cross(vert(d, uint32_t(t), 1) - p0, vert(d, uint32_t(t), 2) - p0)));
+  });
+  pt.lap("normals");
   build_bvh(d, out);  // render.cpp:145
+  pt.lap("reference bvh");
   // The rest depends only on the scene and the reference BVH and writes
   // disjoint parts of `out`: the traversal trees, the emitters and light
   // tree, and the camera-relative copies run concurrently.
   auto f_wide = std::async(std::launch::async, [&] { build_wide(d, out, keep); });
   auto f_emit = std::async(std::launch::async, [&] {
-    out.nodes_f.resize(out.nodes.size());
-    for (size_t i = 0; i < out.nodes.size(); ++i) {
-      const BvhNode& n = out.nodes[i];
-      BvhNodeF& f = out.nodes_f[i];
-      for (int a = 0; a < 3; ++a) {
-        f.lo[a] = round_down(n.lo[a]);
-        f.hi[a] = round_up(n.hi[a]);
-      }
-      if (n.count > 0) {
-        f.a = kNodeLeaf | n.a;
-        f.b = n.count;
-      } else {
-        if (n.b != n.a + 1) throw std::runtime_error("build_scene_bvh: siblings must be adjacent");
-        f.a = n.a;
-        f.b = 0;
+    if (keep == nullptr) {  // fp32 reference-tree copy: deferred closest-hit rays only
+      out.nodes_f.resize(out.nodes.size());
+      for (size_t i = 0; i < out.nodes.size(); ++i) {
+        const BvhNode& n = out.nodes[i];
+        BvhNodeF& f = out.nodes_f[i];
+        for (int a = 0; a < 3; ++a) {
+          f.lo[a] = round_down(n.lo[a]);
+          f.hi[a] = round_up(n.hi[a]);
+        }
+        if (n.count > 0) {
+          f.a = kNodeLeaf | n.a;
+          f.b = n.count;
+        } else {
+          if (n.b != n.a + 1) throw std::runtime_error("build_scene_bvh: siblings must be adjacent");
+          f.a = n.a;
+          f.b = 0;
+        }
       }
     }
 
-    // collect_emitters (light_tree.cpp:30-42) over derive_emitters order
-    out.lights.clear();
-    out.emitter_tri.clear();
-    out.emitter_energy.clear();
-    out.emitter_centroid.clear();
-    for (uint32_t t = 0; t < d.num_triangles; ++t) {
+    // collect_emitters (light_tree.cpp:30-42) over derive_emitters order;
+    // a dynamic update keeps the materials, hence the emitter list
+    auto emitter = [&](uint32_t t, size_t k) {
       const MatRec& m = out.mats[d.material_ids[t]];
-      if (!m.is_emitter) continue;
       const V3 p0 = vert(d, t, 0), p1 = vert(d, t, 1), p2 = vert(d, t, 2);
       const V3 cr = cross(p1 - p0, p2 - p0);
       const double area = 0.5 * length(cr);
       const V3 c = (p0 + p1 + p2) / 3.0;
-      LightRec lr{};
+      LightRec& lr = out.lights[k];
+      lr = LightRec{};
       put3(lr.p0, p0);
       put3(lr.p1, p1);
       put3(lr.p2, p2);
@@ -931,20 +996,25 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
       // sample_triangle_point throws on area <= 0 (scene.cpp:50-51); the
       // device checks pdf_area <= 0 and raises the same error when drawn.
       lr.pdf_area = area > 0 ? 1.0 / area : 0.0;
-      out.lights.push_back(lr);
-      out.emitter_tri.push_back(t);
-      out.emitter_energy.push_back(luminance(V3{m.emission[0], m.emission[1], m.emission[2]}) * area);
-      out.emitter_centroid.push_back(c.x);
-      out.emitter_centroid.push_back(c.y);
-      out.emitter_centroid.push_back(c.z);
-    }
-    if (out.lights.empty()) throw InvalidArgument("build_context: scene has no emitters");
-    if (keep) {  // dynamic update: the light tree of the context's creation
-      out.order = keep->order;
-      out.lt_nodes = keep->lt_nodes;
-      out.lt_begin = keep->lt_begin;
-      out.lt_energy = keep->lt_energy;
+      out.emitter_energy[k] = luminance(V3{m.emission[0], m.emission[1], m.emission[2]}) * area;
+      out.emitter_centroid[3 * k] = c.x;
+      out.emitter_centroid[3 * k + 1] = c.y;
+      out.emitter_centroid[3 * k + 2] = c.z;
+    };
+    if (keep != nullptr) {
+      out.emitter_tri = keep->emitter_tri;
     } else {
+      out.emitter_tri.clear();
+      for (uint32_t t = 0; t < d.num_triangles; ++t)
+        if (out.mats[d.material_ids[t]].is_emitter) out.emitter_tri.push_back(t);
+    }
+    const size_t ne = out.emitter_tri.size();
+    out.lights.resize(ne);
+    out.emitter_energy.resize(ne);
+    out.emitter_centroid.resize(3 * ne);
+    parallel_for(ne, [&](size_t k) { emitter(out.emitter_tri[k], k); });
+    if (out.lights.empty()) throw InvalidArgument("build_context: scene has no emitters");
+    if (!keep) {  // (a dynamic update moves the creation light tree over at the end)
       build_light_tree(out.emitter_centroid, out.emitter_energy, out.order, out.lt_nodes,
                        out.lt_begin, out.lt_energy);
     }
@@ -957,6 +1027,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
     }
     if (!(out.energy_cdf.back() > 0))
       throw InvalidArgument("build_energy_cdf: total emitter energy must be positive");
+    pt.lap("emitters");
 
   });
   const V3 ext = V3{out.scene_hi[0], out.scene_hi[1], out.scene_hi[2]} -
@@ -990,8 +1061,8 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   // Camera-relative copy for the primary rays, whose origin is exactly the
   // camera origin O: the reference's per-axis term fl64(c - O) rounded
   // outward to fp32, so every fp32 error of the decision test is relative.
-  out.nodes_cam.resize(out.nodes.size());
-  parallel_for(out.nodes.size(), [&](size_t i) {
+  if (keep == nullptr) out.nodes_cam.resize(out.nodes.size());
+  if (keep == nullptr) parallel_for(out.nodes.size(), [&](size_t i) {
     const BvhNode& n = out.nodes[i];
     BvhNodeF& f = out.nodes_cam[i];
     for (int a = 0; a < 3; ++a) {
@@ -1006,9 +1077,25 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   // reference's fl64(x * inv) (< 2^-23): its plain slab test is conservative
   // (DESIGN.md 5.4).
   out.wide_cam.clear();
-  if (out.nodes[0].count == 0) out.wide_cam = collapse_wide(out.nodes, cam.origin, 0x1.0p-21);
+  if (out.nodes[0].count == 0 && keep == nullptr)
+    out.wide_cam = collapse_wide(out.nodes, cam.origin, 0x1.0p-21);
+  pt.lap("camera copies");
   f_wide.get();
+  pt.lap("wide join");
   f_emit.get();
+  pt.lap("emit join");
+  if (keep != nullptr) {  // the creation light tree and shadow topology, moved on
+    out.order = std::move(keep->order);
+    out.lt_nodes = std::move(keep->lt_nodes);
+    out.lt_begin = std::move(keep->lt_begin);
+    out.lt_energy = std::move(keep->lt_energy);
+    if (out.wide_kids.empty() && !keep->wide_kids.empty()) {  // refitted, not rebuilt
+      out.shadow_bin = std::move(keep->shadow_bin);
+      out.wide_kids = std::move(keep->wide_kids);
+      out.bin_first = std::move(keep->bin_first);
+      out.bin_end = std::move(keep->bin_end);
+    }
+  }
 }
 
 }  // namespace rlc

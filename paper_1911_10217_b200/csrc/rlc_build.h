@@ -6,6 +6,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "rlc_common.h"
@@ -38,6 +39,11 @@ struct HostScene {
   std::vector<TriAccel> tris_s;   // triangles in the shadow tree's leaf order
   std::vector<uint32_t> tri_leaf_s; // reference leaf node per tris_s entry
   std::vector<BvhNode> shadow_bin;  // binary SAH tree behind `wide` (leaves: tris_s ranges)
+  // per `wide` node, the shadow_bin node behind each child (kWideEmpty: none),
+  // and per shadow_bin node its tris_s range: a dynamic update recomputes the
+  // wide boxes straight from the moved triangles
+  std::vector<std::array<uint32_t, kWide>> wide_kids;
+  std::vector<uint32_t> bin_first, bin_end;
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;
   // materials / triangles
@@ -61,10 +67,13 @@ struct HostScene {
 
 // Whole-context build (proj/src/render.cpp:143-157).  Throws InvalidArgument
 // with the reference's messages for empty scenes / no emitters.
-// With `keep` (rlc_context_update_scene): the light tree is copied from it
-// and the shadow tree's topology refitted instead of rebuilt.
+// With `keep` (rlc_context_update_scene): the light tree and the shadow
+// tree's topology are taken from it (moved: `keep` is the scene being
+// replaced) and the shadow tree refitted instead of rebuilt; the fp32 copies
+// of the reference tree that only deferred closest-hit rays use are not
+// built (the device then runs those rays on the fp64 reference tree).
 void build_host_scene(const rlc_scene_desc& desc, const rlc_render_config& cfg, HostScene& out,
-                      const HostScene* keep = nullptr);
+                      HostScene* keep = nullptr);
 
 // Light tree alone over emitter centroids/energies (light_tree.cpp:56-119),
 // exposed for the unit-level entry points.

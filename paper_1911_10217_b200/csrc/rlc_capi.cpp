@@ -109,12 +109,15 @@ struct SceneBuffers {
   size_t next = 0;
   uint64_t bytes = 0;
   void begin() { next = 0; }
+  // copy = false: the contents are known unchanged since the last upload
+  // into this slot (a dynamic scene update's frozen arrays)
   template <class T>
-  T* put(const std::vector<T>& v) {
+  T* put(const std::vector<T>& v, bool copy = true) {
     if (next == bufs.size()) bufs.emplace_back();
     Buf& b = bufs[next++];
     const size_t need = v.size() * sizeof(T) > 0 ? v.size() * sizeof(T) : 16;
     if (need > b.cap) {
+      copy = true;
       if (b.p) RLC_CK(cudaFree(b.p));
       b.p = nullptr;
       bytes -= b.cap;
@@ -123,7 +126,8 @@ struct SceneBuffers {
       b.cap = cap;
       bytes += cap;
     }
-    if (!v.empty()) RLC_CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (copy && !v.empty())
+      RLC_CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
     return static_cast<T*>(b.p);
   }
   ~SceneBuffers() {
@@ -541,16 +545,22 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
 }
 
 // Uploads the device view of a host scene into arena A.
-void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d) {
+// update = true: a dynamic scene update (rlc_context_update_scene), whose
+// materials, material ids and light tree are those of the previous upload.
+void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d, bool update = false) {
   A.begin();
   d.nodes = A.put(h.nodes);
   d.nodes_f = A.put(h.nodes_f);
   d.nodes_cam = A.put(h.nodes_cam);
-  d.wide = A.put(h.wide);
+  // the unquantized shadow tree is read only when there is no quantized one
+  static const std::vector<rlc::Wide4> kNoWide;
+  d.wide = A.put(h.wide_q.empty() ? h.wide : kNoWide);
   d.wide_q = A.put(h.wide_q);
   d.wide_ref = A.put(h.wide_ref);
   d.wide_cam = A.put(h.wide_cam);
-  if (h.wide.empty()) d.wide = nullptr;
+  if (h.nodes_f.empty()) d.nodes_f = nullptr;
+  if (h.nodes_cam.empty()) d.nodes_cam = nullptr;
+  if (h.wide.empty() || !h.wide_q.empty()) d.wide = nullptr;
   if (h.wide_q.empty()) d.wide_q = nullptr;
   if (h.wide_ref.empty()) d.wide_ref = nullptr;
   if (h.wide_cam.empty()) d.wide_cam = nullptr;
@@ -558,12 +568,12 @@ void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d) {
   d.tris_s = A.put(h.tris_s);
   d.tri_leaf_s = A.put(h.tri_leaf_s);
   d.tris = A.put(h.tris);
-  d.mats = A.put(h.mats);
-  d.tri_mat = A.put(h.tri_mat);
+  d.mats = A.put(h.mats, !update);
+  d.tri_mat = A.put(h.tri_mat, !update);
   d.tri_normal = A.put(h.tri_normal);
   d.lights = A.put(h.lights);
-  d.order = A.put(h.order);
-  d.lt = A.put(h.lt_nodes);
+  d.order = A.put(h.order, !update);
+  d.lt = A.put(h.lt_nodes, !update);
   d.energy_cdf = A.put(h.energy_cdf);
   d.emitter_energy = A.put(h.emitter_energy);
   d.num_lights = uint32_t(h.lights.size());
@@ -656,7 +666,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
 rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scene) {
   return guarded([&] {
     require(ctx != nullptr && scene != nullptr, "rlc_context_update_scene: null argument");
-    const rlc::HostScene& old = ctx->host;
+    rlc::HostScene& old = ctx->host;
     require(scene->num_triangles == old.tri_mat.size() &&
                 scene->num_materials * 6 == old.mat_values.size() &&
                 scene->width == old.cam.width && scene->height == old.cam.height,
@@ -685,7 +695,7 @@ rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scen
     ctx->sync_all();  // the previous frame's kernels read the buffers
     lap("sync");
     rlc::DevScene d{};
-    upload_scene(h, ctx->scene_bufs, d);
+    upload_scene(h, ctx->scene_bufs, d, true);
     ctx->dev = d;
     ctx->host = std::move(h);
     lap("upload");

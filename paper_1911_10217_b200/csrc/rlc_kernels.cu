@@ -230,6 +230,44 @@ __device__ RLC_COLD bool intersect_wide(const DevScene& sc, V3 o, V3 d, double t
 __device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* t_out,
                            uint32_t* tri_out);
 
+// intersect() exactly as the reference runs it (bvh.cpp:124-157): binary
+// tree, fp64 slab tests, right child first.  The path of last resort for
+// deferred rays when the context carries no fp32 copies of the reference
+// tree (dynamic scene updates build none).
+__device__ __noinline__ bool intersect_exact(const DevScene& sc, V3 o, V3 d, double tmin,
+                                             double* t_out, uint32_t* tri_out, uint32_t* err) {
+  const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
+  double closest = HUGE_VAL;
+  uint32_t hit = kNoSlot;
+  uint32_t stack[kStack];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp > 0) {
+    const NodeView n = load_node(sc.nodes, stack[--sp]);
+    if (!box_hit(n, o, inv, tmin, closest)) continue;
+    if (n.count > 0) {
+      for (uint32_t k = n.a; k < n.a + n.count; ++k) {
+        double t;
+        if (tri_hit(sc.tris, k, o, d, tmin, closest, &t)) {
+          closest = t;
+          hit = k;
+        }
+      }
+    } else {
+      if (sp + 2 > kStack) {
+        atomicOr(err, kErrStackOverflow);
+        break;
+      }
+      stack[sp++] = n.a;
+      stack[sp++] = n.b;
+    }
+  }
+  if (hit == kNoSlot) return false;
+  *t_out = closest;
+  *tri_out = sc.tris[hit].tri_id;
+  return true;
+}
+
 // intersect(), proj/src/bvh.cpp:124-157: closest hit in the reference's
 // traversal order (pop the right child first), so exact-t ties go to the same
 // triangle.  Every box decision equals the reference's (box_decide, exact
@@ -242,6 +280,7 @@ __device__ bool intersect(const DevScene& sc, V3 o, V3 d, double tmin, double* t
   bool used;
   const bool got = intersect_wide(sc, o, d, tmin, false, &used, t_out, tri_out, err);
   if (used) return got;
+  if (sc.nodes_f == nullptr) return intersect_exact(sc, o, d, tmin, t_out, tri_out, err);
   const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
   const RayDecide rd = make_ray_decide(o, inv);
   const float tmin_dn = __double2float_rd(tmin), tmin_up = __double2float_ru(tmin);
@@ -322,6 +361,7 @@ __device__ bool intersect_camera(const DevScene& sc, V3 o, V3 d, double* t_out,
   bool used;
   const bool got = intersect_wide(sc, o, d, 0.0, true, &used, t_out, tri_out, err);
   if (used) return got;
+  if (sc.nodes_cam == nullptr) return intersect_exact(sc, o, d, 0.0, t_out, tri_out, err);
   const V3 inv{1.0 / d.x, 1.0 / d.y, 1.0 / d.z};
   const double ia[3] = {inv.x, inv.y, inv.z};
   float finv[3];
