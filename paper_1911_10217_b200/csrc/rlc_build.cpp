@@ -176,8 +176,57 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
   nodes.reserve(size_t(2) * n);
   nodes.push_back(BvhNode{});
   std::vector<Todo> deferred;
-  const uint32_t cut = std::max<uint32_t>(n / 16, 2048);
-  build(nodes, 0, 0, n, cut, &deferred);
+  const uint32_t cut = std::max<uint32_t>(n / 64, 2048);
+  // The top levels breadth first, the nodes of a level split concurrently
+  // (disjoint perm ranges; children numbered in level order afterwards), so
+  // the sequential nth_element work on the critical path is ~2n instead of
+  // n per level.  Below `cut` whole subtrees are built in parallel.
+  {
+    std::vector<Todo> level{{0, 0, n}};
+    while (!level.empty()) {
+      std::vector<std::array<uint32_t, 3>> split(level.size());  // mid, leaf?, count
+      parallel_for(level.size(), [&](size_t k) {
+        const Todo t = level[k];
+        const uint32_t count = t.end - t.begin;
+        Box bounds, cb;
+        for (uint32_t i = t.begin; i < t.end; ++i) {
+          bounds.grow(tb[perm[i]]);
+          cb.grow(cen[perm[i]]);
+        }
+        BvhNode& nd = nodes[t.node];
+        put3(nd.lo, bounds.lo);
+        put3(nd.hi, bounds.hi);
+        if (count <= 4) {
+          nd.a = t.begin;
+          nd.b = 0;
+          nd.count = count;
+          split[k] = {0u, 1u, count};
+          return;
+        }
+        const int axis = cb.longest_axis();
+        const uint32_t mid = t.begin + count / 2;
+        std::nth_element(perm.begin() + t.begin, perm.begin() + mid, perm.begin() + t.end,
+                         [&](uint32_t x, uint32_t y) { return comp(cen[x], axis) < comp(cen[y], axis); });
+        split[k] = {mid, 0u, count};
+      }, 1);
+      std::vector<Todo> next;
+      for (size_t k = 0; k < level.size(); ++k) {
+        if (split[k][1]) continue;
+        const Todo t = level[k];
+        const uint32_t child = uint32_t(nodes.size());
+        nodes.push_back(BvhNode{});
+        nodes.push_back(BvhNode{});
+        nodes[t.node].a = child;
+        nodes[t.node].b = child + 1;
+        nodes[t.node].count = 0;
+        for (const Todo c : {Todo{child, t.begin, split[k][0]}, Todo{child + 1, split[k][0], t.end}}) {
+          if (c.end - c.begin < cut && c.end - c.begin > 4) deferred.push_back(c);
+          else next.push_back(c);
+        }
+      }
+      level.swap(next);
+    }
+  }
   if (!deferred.empty()) {
     // subtrees in parallel, each into a private array whose element 0 is the
     // subtree root (a node already allocated in `nodes`)
@@ -211,7 +260,7 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
     }
   }
   out.tris.resize(n);
-  for (uint32_t i = 0; i < n; ++i) {
+  parallel_for(n, [&](size_t i) {
     const uint32_t id = perm[i];
     const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
     TriAccel& ta = out.tris[i];
@@ -220,7 +269,7 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
     put3(ta.e2, p2 - p0);
     ta.tri_id = id;
     ta.pad = 0;
-  }
+  });
   for (int a = 0; a < 3; ++a) {
     out.scene_lo[a] = nodes[0].lo[a];
     out.scene_hi[a] = nodes[0].hi[a];
