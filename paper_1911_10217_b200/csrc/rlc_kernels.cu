@@ -1969,6 +1969,7 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
       vA[i] = g.visits[row + i];
     }
     __syncwarp();
+    const uint32_t changes_before = my_changes;
     for (uint32_t it = 0; it < iterations; ++it) {
       WarpArg sp{0.0, kNoSlot};
       for (uint32_t i = lane; i < M; i += 32) {
@@ -2026,12 +2027,15 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
       __syncwarp();
       ++my_changes;
     }
-    // write back node ids, q, visits, ends; serial cdf (cut.cpp:88-95)
-    for (uint32_t i = lane; i < M; i += 32) {
-      g.q[row + i] = qA[i];
-      g.node_ids[row + i] = nA[i];
-      g.visits[row + i] = vA[i];
-      g.ends[row + i] = sc.lt[nA[i]].range_end;
+    // write back node ids, q, visits, ends when the cut changed (k_fold
+    // already stored the folded q); serial cdf (cut.cpp:88-95) always
+    if (my_changes != changes_before) {  // warp-uniform
+      for (uint32_t i = lane; i < M; i += 32) {
+        g.q[row + i] = qA[i];
+        g.node_ids[row + i] = nA[i];
+        g.visits[row + i] = vA[i];
+        g.ends[row + i] = sc.lt[nA[i]].range_end;
+      }
     }
     if (lane == 0) {
       double run = 0;
