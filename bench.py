@@ -310,7 +310,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     update_ms[0] = 0.0
     ctx.synchronize()
     ctx.stage_times()
-    ctx.enable_timing(True)
+    # single GPU, static scene: the timed frames are one render_passes call
+    # (render_frame's pass loop; CUDA-graph replays for launch-bound frames),
+    # the per-kernel CUDA-event times come from a separate untimed run below
+    batch = world == 1 and not dynamic
+    ctx.enable_timing(not batch)
     l0 = grid.lookup_count()
     launches0 = rlcuts.kernel_launches()
     clocks = ClockSampler(local_rank)
@@ -322,8 +326,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for p in range(args.warmup, args.warmup + args.steps):
-        step(p)
+    if batch:
+        rlcuts.render_passes(ctx, cfg, args.warmup, args.steps, grid, fb)
+    else:
+        for p in range(args.warmup, args.warmup + args.steps):
+            step(p)
     e1.record(stream)
     torch.cuda.synchronize()
     if dist is not None:
@@ -332,6 +339,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     launches = rlcuts.kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
     lookups = grid.lookup_count() - l0
+    stage_frames = args.steps
+    if batch:  # per-kernel times: a few more frames with CUDA events around every stage
+        stage_frames = min(args.steps, 20)
+        ctx.stage_times()
+        ctx.enable_timing(True)
+        for p in range(args.warmup + args.steps, args.warmup + args.steps + stage_frames):
+            step(p)
+        ctx.synchronize()
     stages = ctx.stage_times()
     ctx.enable_timing(False)
     if dist is not None:
@@ -440,7 +455,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "cells": st["occupied"], "fallback_hits": st["fallback_hits"]},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
-            "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+            "stage_ms_per_step": {k: v[0] / stage_frames for k, v in stages.items()},
+            "stage_source": ("CUDA events around every stage in %d further frames" % stage_frames
+                             if batch else "CUDA events around every stage in the timed frames"),
             "scene_update_ms_per_step": update_ms[0] / args.steps if dynamic else None,
             "context_build_s": build_s,
         }

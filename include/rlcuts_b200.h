@@ -258,6 +258,14 @@ rlc_status rlc_end_of_pass_update(rlc_grid* grid, const rlc_context* ctx,
  * change count stays on the device (read it with rlc_grid_last_changes). */
 rlc_status rlc_render_pass_async(const rlc_context* ctx, const rlc_render_config* config,
                                  uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb);
+/* Passes [first_pass, first_pass + count) of render_frame's loop
+ * (render.cpp:218-224): for each, render_pass and -- with the learned
+ * sampler -- end_of_pass_update, enqueued without synchronizing (errors
+ * surface at the next synchronizing call).  Launch-bound frames (at most 2^19
+ * paths per pass) replay one captured CUDA graph per pass. */
+rlc_status rlc_render_passes_async(const rlc_context* ctx, const rlc_render_config* config,
+                                   uint32_t first_pass, uint32_t count, rlc_grid* grid,
+                                   rlc_framebuffer* fb);
 rlc_status rlc_end_of_pass_update_async(rlc_grid* grid, const rlc_context* ctx,
                                         const rlc_cut_config* cut);
 rlc_status rlc_grid_last_changes(const rlc_grid* grid, uint32_t* changes);

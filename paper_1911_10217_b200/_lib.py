@@ -97,6 +97,8 @@ SIGNATURES = {
     "rlc_intersect_batch": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp,
                                       C.POINTER(C.c_int32)]),
     "rlc_debug_trav_stats": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
+    "rlc_render_passes_async": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, C.c_uint32,
+                                          _P, _P]),
     "rlc_intersect_batch_sah": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp,
                                           C.POINTER(C.c_int32)]),
     "rlc_grid_create": (C.c_int, [_P, C.POINTER(RenderConfigC), _PP]),

@@ -35,6 +35,7 @@ constexpr unsigned kFull = 0xffffffffu;
 }  // namespace
 
 uint64_t launches() { return g_launches.load(); }
+void add_launches(uint64_t k) { count_launch(k); }
 
 // Opt-in traversal statistics (build with EXTRA=-DRLC_TRAV_STATS): per-ray
 // node steps and triangle tests of k_shadow [0..2] and closest_sah [3..5]
@@ -649,7 +650,10 @@ __global__ void __launch_bounds__(128, RLC_PRIMARY_BLOCKS) k_primary(DevScene sc
   uint64_t rk = 0;
   if (active) {
     const uint64_t pixel_index = uint64_t(py) * uint64_t(P.width) + px;
-    const uint64_t sample_index = uint64_t(P.pass_index) * P.spp_pp + s;
+    // graph replays: the replay's first pass index in device memory, plus
+    // this pass's position in the graph
+    const uint32_t pass = P.pass_dev ? *P.pass_dev + P.pass_index : P.pass_index;
+    const uint64_t sample_index = uint64_t(pass) * P.spp_pp + s;
     rk = rng_key(P.seed_mixed, pixel_index, sample_index, P.zero_mixed);
     const double jx = rng_draw(rk, kDrawJx);
     const double jy = rng_draw(rk, kDrawJy);
@@ -2255,6 +2259,30 @@ void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const 
   if (local_n == 0) return;
   k_scatter_qbefore<<<blocks_for(local_n, 256), 256, 0, st>>>(x.q_rec, own_offset, b.rec_path,
                                                               b.rec_count, local_n, b.q_before);
+  count_launch();
+}
+
+__global__ void k_end_pass(const uint32_t* pass_dev, uint32_t offset, uint32_t* changes,
+                           uint32_t* hist) {
+  if (hist) hist[*pass_dev + offset] = *changes;
+  *changes = 0;
+}
+
+__global__ void k_add_u32(uint32_t* p, uint32_t v, uint32_t set) { *p = set ? v : *p + v; }
+
+void launch_end_pass(const uint32_t* pass_dev, uint32_t offset, uint32_t* changes, uint32_t* hist,
+                     cudaStream_t st) {
+  k_end_pass<<<1, 1, 0, st>>>(pass_dev, offset, changes, hist);
+  count_launch();
+}
+
+void launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t st) {
+  k_add_u32<<<1, 1, 0, st>>>(p, v, 1u);
+  count_launch();
+}
+
+void launch_add_u32(uint32_t* p, uint32_t v, cudaStream_t st) {
+  k_add_u32<<<1, 1, 0, st>>>(p, v, 0u);
   count_launch();
 }
 

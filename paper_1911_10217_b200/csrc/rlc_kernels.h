@@ -145,6 +145,7 @@ struct PassParams {
   uint64_t zero_mixed;  // mix64(0): the c component of the RNG key
   double alpha;
   uint32_t harmonic;
+  const uint32_t* pass_dev;  // non-null (CUDA-graph replays): the pass index is read here
 };
 
 struct PassBuffers {
@@ -187,6 +188,13 @@ struct Framebuf {
 
 // Each launcher adds its kernel launches to a process-wide counter.
 uint64_t launches();
+void add_launches(uint64_t k);
+// End of pass `offset` of a graph replay: hist[*pass_dev + offset] = *changes
+// (hist may be null), *changes = 0.
+void launch_end_pass(const uint32_t* pass_dev, uint32_t offset, uint32_t* changes, uint32_t* hist,
+                     cudaStream_t st);
+void launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t st);  // *p = v
+void launch_add_u32(uint32_t* p, uint32_t v, cudaStream_t st);  // *p += v
 void trav_stats(uint64_t out[8], bool reset);
 
 void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,

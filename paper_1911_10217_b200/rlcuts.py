@@ -330,6 +330,18 @@ def render_pass(ctx: RenderContext, config: RenderConfig, pass_index: int,
                                          framebuffer.handle))
 
 
+def render_passes(ctx: RenderContext, config: RenderConfig, first_pass: int, count: int,
+                  grid: HashGrid | None, framebuffer: Framebuffer):
+    """render_frame's pass loop (proj/src/render.cpp:218-224) for passes
+    [first_pass, first_pass + count): render_pass and, with the learned
+    sampler, end_of_pass_update per pass, enqueued asynchronously (CUDA-graph
+    replays for launch-bound frames).  ctx.synchronize() waits for it."""
+    cfg = config.c()
+    _check(_lib.load().rlc_render_passes_async(ctx.handle, C.byref(cfg), first_pass, count,
+                                               grid.handle if grid is not None else None,
+                                               framebuffer.handle))
+
+
 def end_of_pass_update(grid: HashGrid, ctx: RenderContext, config: CutConfig,
                        sync: bool = True) -> int | None:
     """end_of_pass_update (proj/src/render.cpp:185-200); returns the change count."""
