@@ -19,6 +19,10 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <mutex>
+#include <memory>
+#include <functional>
+#include <condition_variable>
 #include <thread>
 #include <atomic>
 #include <future>
@@ -31,24 +35,107 @@ namespace rlc {
 
 namespace {
 
-// Runs fn(i) for i in [0, n) on up to 16 threads in contiguous chunks.  The
+// A process-wide pool of hardware_concurrency - 1 persistent workers (host
+// builds run many short parallel loops, several of them concurrently from
+// the build's own tasks: thread creation per loop and oversubscription cost
+// more than the loops).  A submitter works on its own batch too, so nested
+// and concurrent submissions cannot deadlock.
+class WorkerPool {
+ public:
+  static WorkerPool& get() {
+    static WorkerPool pool;
+    return pool;
+  }
+  unsigned threads() const { return unsigned(workers_.size()) + 1; }
+  // Runs job(c) for c in [0, chunks); returns when all are done.
+  void run(size_t chunks, const std::function<void(size_t)>& job) {
+    auto batch = std::make_shared<Batch>();
+    batch->job = &job;
+    batch->chunks = chunks;
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      queue_.push_back(batch);
+    }
+    cv_.notify_all();
+    work(*batch);  // the submitter takes chunks too
+    std::unique_lock<std::mutex> lk(batch->m);
+    batch->cv.wait(lk, [&] { return batch->done == batch->chunks; });
+    if (batch->error) std::rethrow_exception(batch->error);
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (std::thread& t : workers_) t.join();
+  }
+
+ private:
+  struct Batch {
+    const std::function<void(size_t)>* job = nullptr;
+    size_t chunks = 0;
+    std::atomic<size_t> next{0};
+    size_t done = 0;  // under m
+    std::exception_ptr error;
+    std::mutex m;
+    std::condition_variable cv;
+  };
+  WorkerPool() {
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    for (unsigned i = 0; i + 1 < hw; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  static void work(Batch& b) {
+    for (size_t c; (c = b.next.fetch_add(1)) < b.chunks;) {
+      std::exception_ptr err;
+      try {
+        (*b.job)(c);
+      } catch (...) {
+        err = std::current_exception();
+      }
+      std::lock_guard<std::mutex> lk(b.m);
+      if (err && !b.error) b.error = err;
+      if (++b.done == b.chunks) b.cv.notify_all();
+    }
+  }
+  void loop() {
+    while (true) {
+      std::shared_ptr<Batch> b;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || !queue_.empty(); });
+        if (stop_) return;
+        b = queue_.front();
+        if (b->next.load() >= b->chunks) {  // fully claimed: retire it
+          queue_.pop_front();
+          continue;
+        }
+      }
+      work(*b);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::deque<std::shared_ptr<Batch>> queue_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+};
+
+// Runs fn(i) for i in [0, n) on the worker pool in contiguous chunks.  The
 // iterations must write disjoint data; exceptions propagate to the caller.
 template <class F>
 void parallel_for(size_t n, const F& fn, size_t min_chunk = 2048) {
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const size_t chunks = std::min<size_t>(hw, (n + min_chunk - 1) / min_chunk);
+  WorkerPool& pool = WorkerPool::get();
+  const size_t chunks = std::min<size_t>(pool.threads(), (n + min_chunk - 1) / min_chunk);
   if (chunks <= 1) {
     for (size_t i = 0; i < n; ++i) fn(i);
     return;
   }
-  std::vector<std::future<void>> jobs;
-  for (size_t c = 0; c < chunks; ++c) {
+  const std::function<void(size_t)> job = [&](size_t c) {
     const size_t b = n * c / chunks, e = n * (c + 1) / chunks;
-    jobs.push_back(std::async(std::launch::async, [&fn, b, e] {
-      for (size_t i = b; i < e; ++i) fn(i);
-    }));
-  }
-  for (auto& j : jobs) j.get();
+    for (size_t i = b; i < e; ++i) fn(i);
+  };
+  pool.run(chunks, job);
 }
 
 struct Box {
@@ -630,8 +717,8 @@ std::vector<Wide4> collapse_wide(const std::vector<BvhNode>& nodes, const double
 // is the smallest child bound and the scale the smallest power of two that
 // spans the node in 250 steps; each bound is then moved outward until the
 // exact plane origin + q * scale encloses the fp32 bound.
-std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
-  std::vector<WideQ> out(w.size());
+void quantize_wide(const std::vector<Wide4>& w, std::vector<WideQ>& out) {
+  out.resize(w.size());
   parallel_for(w.size(), [&](size_t i) {
     const Wide4& n = w[i];
     WideQ& q = out[i];
@@ -681,7 +768,6 @@ std::vector<WideQ> quantize_wide(const std::vector<Wide4>& w) {
       }
     }
   });
-  return out;
 }
 
 // The wide trees of the traversal kernels:
@@ -756,12 +842,11 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
     std::vector<uint32_t> leaf_of_id(out.tris.size());
     parallel_for(out.tris.size(), [&](size_t j) { leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j]; });
     const size_t nt = keep->tris_s.size();
-    out.tris_s.resize(nt);
-    out.tri_leaf_s.resize(nt);
+    out.tris_s = std::move(keep->tris_s);  // positions and triangle ids kept; the
+    out.tri_leaf_s.resize(nt);             // vertices are rewritten below
     std::vector<Box> tb(nt);
     parallel_for(nt, [&](size_t i) {
       TriAccel& ta = out.tris_s[i];
-      ta = keep->tris_s[i];
       const uint32_t id = ta.tri_id;
       const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
       put3(ta.p0, p0);
@@ -776,10 +861,9 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
     const auto& kids = keep->wide_kids;
     const auto& bin = keep->shadow_bin;
     const double pad = S * 0x1.0p-21;
-    out.wide.resize(kids.size());
+    out.wide = std::move(keep->wide);  // rewritten in place: boxes and leaf bits
     parallel_for(kids.size(), [&](size_t w) {
       Wide4& n = out.wide[w];
-      std::memset(&n, 0, sizeof(n));
       for (int c = 0; c < kWide; ++c) {
         const uint32_t b = kids[w][c];
         if (b == kWideEmpty) {
@@ -803,7 +887,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
             pure &= out.tri_leaf_s[bn.a + k] == out.tri_leaf_s[bn.a];
           n.child[c] = kWideLeaf | ((bn.count - 1) << 28) | (pure ? kLeafPure : 0u) | bn.a;
         } else {
-          n.child[c] = keep->wide[w].child[c];  // internal: the creation numbering
+          // internal: the creation numbering, already in place
         }
       }
     }, 64);
@@ -824,8 +908,8 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
   f_ref.get();
   pt.lap("wide_ref");
   const char* q = std::getenv("RLC_SHADOW_QUANT");
-  out.wide_q.clear();
-  if (!(q && std::string(q) == "0")) out.wide_q = quantize_wide(out.wide);
+  if (q && std::string(q) == "0") out.wide_q.clear();
+  if (!(q && std::string(q) == "0")) quantize_wide(out.wide, out.wide_q);
   pt.lap("quantize");
 }
 
@@ -980,6 +1064,18 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
     if (d.material_ids[t] >= d.num_materials)
       throw OutOfRange("build_context: material id out of range");
 
+  if (keep != nullptr) {  // the replaced scene's output buffers: no fresh pages per update
+    out.nodes = std::move(keep->nodes);
+    out.tris = std::move(keep->tris);
+    out.wide_q = std::move(keep->wide_q);
+    out.tri_leaf = std::move(keep->tri_leaf);
+    out.tri_leaf_s = std::move(keep->tri_leaf_s);
+    out.tri_normal = std::move(keep->tri_normal);
+    out.lights = std::move(keep->lights);
+    out.emitter_energy = std::move(keep->emitter_energy);
+    out.emitter_centroid = std::move(keep->emitter_centroid);
+    out.energy_cdf = std::move(keep->energy_cdf);
+  }
   out.mat_values.assign(d.materials, d.materials + size_t(d.num_materials) * 6);
   out.mats.resize(d.num_materials);
   for (uint32_t m = 0; m < d.num_materials; ++m) {
