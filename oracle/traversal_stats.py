@@ -13,7 +13,7 @@ from paper_1911_10217_b200 import rlcuts, scenes
 from oracle.restate import OracleRun
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-DOWNSCALE = {"c1": 1, "c2": 2, "c3": 4, "c4": 4}
+DOWNSCALE = {"c1": 1, "c2": 2, "c3": 4, "c4": 4, "c5": 8}
 
 
 def main():
