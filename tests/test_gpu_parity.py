@@ -262,3 +262,46 @@ def test_errors_match_reference_exceptions(ref):
         rlcuts.HashGrid(ctx, rlcuts.RenderConfig(sampler=RL, hash=rlcuts.HashConfig(capacity=0)))
     with pytest.raises(ValueError, match="cut size"):
         rlcuts.HashGrid(ctx, rlcuts.RenderConfig(sampler=RL, cut=rlcuts.CutConfig(cut_size=0)))
+
+
+@pytest.mark.parametrize("name,res,passes", [("c3", (192, 108), 3), ("c5", (96, 54), 2)])
+def test_full_size_scene_bit_exact(ref, name, res, passes):
+    """The bench scenes themselves (1M / 4M emitters: full-size traversal
+    trees, light tree and cuts) at a reduced raster, against the reference."""
+    scene, st = scenes.config_scene(name)
+    scene = scene.with_resolution(*res)
+    spp_pp = st["spp"] // st["passes"]
+    cfg = rlcuts.RenderConfig(spp=spp_pp * passes, passes=passes, sampler=RL,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+    assert grid.fallback_hits() == 0 and grid.lookup_count() > 0.5 * res[0] * res[1] * spp_pp
+
+
+def test_full_resolution_c3_properties():
+    """c3 at its bench size (1920x1080, 1M emitters), where the reference is too
+    slow to run in a test: size-independent invariants of the learned state
+    after a few frames -- every pixel sampled once per frame, light samples
+    counted once each, cdf rows exact prefix sums of q, cut leaves a
+    partition of the emitter range, no fallback cells."""
+    scene, st = scenes.config_scene("c3")
+    cfg = rlcuts.RenderConfig(spp=4, passes=4, sampler=RL,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    ctx = rlcuts.build_context(scene, cfg)
+    grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+    rlcuts.render_passes(ctx, cfg, 0, cfg.passes, grid, fb)
+    ctx.synchronize()
+    s, c = fb.download()
+    assert (c == cfg.passes).all()
+    assert np.isfinite(s).all() and (s >= 0).all()
+    stats = grid.stats()
+    assert stats["fallback_hits"] == 0 and stats["occupied"] > 1000
+    n_emit = ctx.info()["num_emitters"]
+    cells = grid.export()
+    rng = np.random.default_rng(0)
+    for k in rng.choice(len(cells), size=200, replace=False):
+        v = list(cells.values())[k]
+        q, cdf, ends = v["q"], v["cdf"], v["ends"]
+        assert np.array_equal(cdf, np.cumsum(q))  # serial left-to-right sum, as rebuild_cdf
+        assert (np.diff(ends.astype(np.int64)) > 0).all() and ends[-1] == n_emit
+        assert (q > 0).all() and (v["visits"] >= 1).all()
