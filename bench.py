@@ -160,6 +160,21 @@ def measured_peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def frame_hbm(config: str, value: float, peak: float) -> dict | None:
+    """Whole-frame HBM traffic (BASELINE's "HBM GB/s"): the DRAM bytes of
+    every launch of one steady-state frame per light sample, measured once
+    with ncu (profiles/r01_frame_dram_c3.txt), times the live sample rate."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        b = float(json.load(open(p))[config]["frame_bytes_per_sample"])
+    except Exception:
+        return None
+    gbs = value * b / 1e9
+    return {"bytes_per_sample": b, "achieved_gbs": gbs, "frac": gbs / peak,
+            "source": "ncu DRAM read+write of one frame's launches / its light samples "
+                      "(profiles/r01_frame_dram_c3.txt) x this run's light samples/s"}
+
+
 def ncu_traffic(config: str, kernel: str) -> float | None:
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -390,6 +405,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                         "counts per ray (SURVEY 8(d)); our trees serve them mostly from L1/L2 "
                         "or skip them, so frac > 1; dram_achieved = ncu DRAM bytes per launch "
                         "(traffic) / live launch time (profiles/r01_ncu_summary.md)"}
+        fh = frame_hbm(args.config, value, peak)
+        if fh:
+            roof["frame_hbm"] = fh
         tr = roof["traffic"]
         if tr:
             roof["dram_achieved"] = tr / (pk["avg_launch_ms"] / 1e3) / 1e9
