@@ -1243,4 +1243,13 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   }
 }
 
+void parallel_copy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kChunk = size_t(1) << 20;
+  const size_t n = (bytes + kChunk - 1) / kChunk;
+  parallel_for(n, [&](size_t i) {
+    const size_t b = i * kChunk, e = std::min(bytes, b + kChunk);
+    std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+  }, 1);
+}
+
 }  // namespace rlc

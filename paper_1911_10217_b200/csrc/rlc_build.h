@@ -75,6 +75,10 @@ struct HostScene {
 void build_host_scene(const rlc_scene_desc& desc, const rlc_render_config& cfg, HostScene& out,
                       HostScene* keep = nullptr);
 
+// memcpy on the host build's worker pool (1 MB chunks): moves large device
+// downloads out of pinned staging at host memory bandwidth.
+void parallel_copy(void* dst, const void* src, size_t bytes);
+
 // Light tree alone over emitter centroids/energies (light_tree.cpp:56-119),
 // exposed for the unit-level entry points.
 void build_light_tree(const std::vector<double>& centroids, const std::vector<double>& energy,

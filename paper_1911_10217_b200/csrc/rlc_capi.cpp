@@ -280,6 +280,7 @@ struct rlc_context {
     stage_on(stream, id, static_cast<F&&>(launch));
   }
   ~rlc_context() {
+    if (h_stage) cudaFreeHost(h_stage);
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (ev_prim_done) cudaEventDestroy(ev_prim_done);
@@ -343,6 +344,9 @@ struct rlc_context {
   uint32_t scene_gen = 0;       // bumped by rlc_context_update_scene
   const uint32_t* graph_pass_dev = nullptr;  // set while capturing: setup_pass reads it
   uint32_t* d_pass = nullptr;     // device pass index of graph replays
+  // pinned staging for large downloads (download_to_host)
+  void* h_stage = nullptr;
+  size_t h_stage_cap = 0;
   uint32_t* d_changes = nullptr;  // device change count of graph replays
   rlc::UpdateRecord* rec_out = nullptr;  // this rank's exported update records
 
@@ -1274,6 +1278,16 @@ void prepare_frame_cache(rlc_context* ctx, const rlc_render_config* config) {
     fb->holds_ref = false;  // owned by the context itself
     ctx->refs.fetch_sub(1);
     ctx->frame_fb = fb;
+    // render_frame's image download staging (download_to_host), allocated
+    // with the rest of the frame cache so render_frame allocates nothing
+    const size_t img = size_t(24) * size_t(fb->width) * size_t(fb->height);
+    if (img >= (size_t(4) << 20) && ctx->h_stage_cap < img) {
+      if (ctx->h_stage) RLC_CK(cudaFreeHost(ctx->h_stage));
+      ctx->h_stage = nullptr;
+      ctx->h_stage_cap = 0;
+      RLC_CK(cudaMallocHost(&ctx->h_stage, img));
+      ctx->h_stage_cap = img;
+    }
   }
   if (config->passes > ctx->frame_hist_cap) {
     ctx->frame_hist_arena.release();
@@ -1292,6 +1306,29 @@ extern "C" {
 namespace {
 
 // Pinned host staging for the per-pixel error terms of render_frame_scored.
+// Device -> caller host memory, synchronously on stream st: large copies go
+// through the context's pinned staging buffer (full-rate DMA) and are fanned
+// out to the caller's pageable memory by the worker pool; a pageable
+// cudaMemcpy is staged by the driver at a fraction of that rate.
+void download_to_host(rlc_context* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes < (size_t(4) << 20)) {
+    RLC_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    RLC_CK(cudaStreamSynchronize(st));
+    return;
+  }
+  if (bytes > ctx->h_stage_cap) {
+    RLC_CK(cudaStreamSynchronize(st));
+    if (ctx->h_stage) RLC_CK(cudaFreeHost(ctx->h_stage));
+    ctx->h_stage = nullptr;
+    ctx->h_stage_cap = 0;
+    RLC_CK(cudaMallocHost(&ctx->h_stage, bytes));
+    ctx->h_stage_cap = bytes;
+  }
+  RLC_CK(cudaMemcpyAsync(ctx->h_stage, src, bytes, cudaMemcpyDeviceToHost, st));
+  RLC_CK(cudaStreamSynchronize(st));
+  rlc::parallel_copy(dst, ctx->h_stage, bytes);
+}
+
 struct PinnedBuf {
   double* p = nullptr;
   explicit PinnedBuf(size_t n) { RLC_CK(cudaMallocHost(&p, n * sizeof(double))); }
@@ -1459,7 +1496,7 @@ void render_frame_impl(rlc_context* ctx, const rlc_render_config* config, const 
   ctx->join_acc();
   if (image_out) {
     rlc::launch_resolve(fb->fb, uint32_t(npix), fb->d_image, st);
-    RLC_CK(cudaMemcpyAsync(image_out, fb->d_image, 24 * npix, cudaMemcpyDeviceToHost, st));
+    download_to_host(ctx, image_out, fb->d_image, 24 * npix, st);
   }
   std::vector<uint32_t> h(config->passes);
   RLC_CK(cudaMemcpyAsync(h.data(), d_hist, 4 * h.size(), cudaMemcpyDeviceToHost, st));
