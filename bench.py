@@ -405,7 +405,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                         "counts per ray (SURVEY 8(d)); our trees serve them mostly from L1/L2 "
                         "or skip them, so frac > 1; dram_achieved = ncu DRAM bytes per launch "
                         "(traffic) / live launch time (profiles/r01_ncu_summary.md)"}
-        fh = frame_hbm(args.config, value, peak)
+        fh = frame_hbm(args.config, value, peak) if args.max_depth == 1 else None
         if fh:
             roof["frame_hbm"] = fh
         tr = roof["traffic"]
