@@ -596,11 +596,16 @@ std::vector<BvhNode> sah_over_tris(const rlc_scene_desc& d, const HostScene& hs,
       }
     }
     // leaf: one triangle, or up to 4 of one reference leaf when splitting
-    // does not pay (SAH, traversal cost 1 per box against 1 per triangle)
+    // does not pay (SAH, traversal cost 1 per box against tri_cost per
+    // triangle; RLC_SAH_TRI_COST, default 1)
+    static const double tri_cost = [] {
+      const char* e = std::getenv("RLC_SAH_TRI_COST");
+      return e ? std::atof(e) : 1.0;
+    }();
     const double a_node = area(bounds);
     const bool can_leaf = count == 1 || (count <= 4 && pure);
     if (can_leaf && (best_axis < 0 || !(a_node > 0) ||
-                     double(count) <= 1.0 + best_cost / a_node)) {
+                     tri_cost * double(count) <= 1.0 + tri_cost * best_cost / a_node)) {
       nd.a = t.begin;
       nd.b = 0;
       nd.count = count;
