@@ -226,6 +226,14 @@ rlc_status rlc_grid_stats_get(const rlc_grid* grid, rlc_grid_stats* stats);
 /* Parity export keyed by CellKey (slot ids are insertion-order dependent,
  * SURVEY 0 fact 9).  Arrays are [max_cells] / [max_cells * cut_size]; any
  * pointer may be NULL.  *num_cells receives the occupied count. */
+/* HashGrid's slot view (hash_grid.hpp:87-110: key_of, touched_slots,
+ * dump_stats, memory_records are built on it by the mirrors): the occupied
+ * slots in slot order with their dense cell, CellKey and touched flag (set by
+ * render_pass, cleared by end_of_pass_update).  *count_out = occupied slots;
+ * at most max_slots entries are written, every output array optional. */
+rlc_status rlc_grid_slots(const rlc_grid* grid, uint32_t max_slots, uint32_t* slot_out,
+                          uint32_t* cell_out, rlc_cell_key* key_out, uint8_t* touched_out,
+                          uint32_t* count_out);
 rlc_status rlc_grid_export(const rlc_grid* grid, uint32_t max_cells, rlc_cell_key* keys,
                            uint32_t* node_ids, uint32_t* ends, double* q, double* cdf,
                            uint32_t* visits, uint32_t* num_cells);

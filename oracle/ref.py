@@ -58,6 +58,8 @@ _SIGS = {
     "ref_make_key": (C.c_int, [C.c_uint32, _dp, _dp, _u32p, _dp, _dp, C.c_double, C.c_uint32,
                                C.c_double, C.POINTER(_lib.CellKeyC), _u64p]),
     "ref_octa_encode": (None, [C.c_uint32, _dp, _dp]),
+    "ref_run_grid_views": (C.c_uint32, [C.c_void_p, C.c_char_p, C.c_uint32, _u64p, _u32p,
+                                        C.c_uint32]),
 }
 
 
@@ -146,6 +148,26 @@ class RefRun:
         ref_lib().ref_run_info(self.h, dp(d), up(u))
         return {"base_tile": d[0], "shadow_eps": d[1], "num_triangles": int(u[0]),
                 "num_emitters": int(u[1]), "bvh_nodes": int(u[2]), "light_tree_nodes": int(u[3])}
+
+    def render_only(self, pass_index: int):
+        """render_pass alone (no end_of_pass_update): the touched slots stay set."""
+        st = ref_lib().ref_run_render_only(self.h, pass_index)
+        if st:
+            raise_ref(st)
+
+    def grid_views(self) -> tuple[str, int, list]:
+        """HashGrid::dump_stats text, memory_records and the CellKeys of
+        touched_slots() in slot order."""
+        buf = C.create_string_buffer(1 << 16)
+        mem = np.zeros(1, np.uint64)
+        cap = max(self.stats()["occupied"], 1)
+        keys = np.zeros(5 * cap, np.uint32)
+        n = ref_lib().ref_run_grid_views(self.h, buf, len(buf), mem.ctypes.data_as(_u64p),
+                                         up(keys), cap)
+        k = keys.view(np.int32).reshape(-1, 5)
+        touched = [(int(k[i, 0]), int(k[i, 1]), int(k[i, 2]), int(keys[5 * i + 3]),
+                    int(keys[5 * i + 4])) for i in range(min(n, cap))]
+        return buf.value.decode(), int(mem[0]), touched
 
     def export(self) -> dict:
         st = self.stats()

@@ -11,6 +11,8 @@
 // Nothing here re-implements reference logic: each function marshals arrays
 // into rlcuts:: types and calls the reference function named in its comment.
 
+#include <algorithm>
+#include <sstream>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -242,6 +244,34 @@ void ref_run_stats(void* h, uint64_t* out) {
   out[1] = run->grid->lookup_count();
   out[2] = run->grid->fallback_hits();
   out[3] = run->grid->fallback_cut().size();
+}
+
+// HashGrid::dump_stats text (into out, NUL-terminated, truncated to cap),
+// memory_records, and the keys of touched_slots() in slot order (5 u32 per
+// key; returns their count).
+uint32_t ref_run_grid_views(void* h, char* out, uint32_t cap, uint64_t* mem_records,
+                            uint32_t* touched_keys, uint32_t max_keys) {
+  RefRun* run = static_cast<RefRun*>(h);
+  if (!run->grid) return 0;
+  std::ostringstream os;
+  run->grid->dump_stats(os);
+  const std::string s = os.str();
+  if (out && cap > 0) {
+    const size_t n = std::min<size_t>(s.size(), cap - 1);
+    std::memcpy(out, s.data(), n);
+    out[n] = 0;
+  }
+  if (mem_records) *mem_records = run->grid->memory_records();
+  const std::vector<uint32_t> t = run->grid->touched_slots();
+  for (size_t i = 0; i < t.size() && i < max_keys; ++i) {
+    const CellKey& k = run->grid->key_of(t[i]);
+    touched_keys[5 * i] = uint32_t(k.qx);
+    touched_keys[5 * i + 1] = uint32_t(k.qy);
+    touched_keys[5 * i + 2] = uint32_t(k.qz);
+    touched_keys[5 * i + 3] = k.qn;
+    touched_keys[5 * i + 4] = k.level;
+  }
+  return uint32_t(t.size());
 }
 
 // dout: base_tile, shadow_eps;  uout: triangles, emitters, bvh nodes, tree nodes

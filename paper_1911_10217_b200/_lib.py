@@ -99,6 +99,8 @@ SIGNATURES = {
     "rlc_debug_trav_stats": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
     "rlc_render_passes_async": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, C.c_uint32,
                                           _P, _P]),
+    "rlc_grid_slots": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                 C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32)]),
     "rlc_intersect_batch_sah": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp,
                                           C.POINTER(C.c_int32)]),
     "rlc_grid_create": (C.c_int, [_P, C.POINTER(RenderConfigC), _PP]),

@@ -1022,6 +1022,43 @@ rlc_status rlc_grid_export(const rlc_grid* grid, uint32_t max_cells, rlc_cell_ke
   });
 }
 
+rlc_status rlc_grid_slots(const rlc_grid* grid, uint32_t max_slots, uint32_t* slot_out,
+                          uint32_t* cell_out, rlc_cell_key* key_out, uint8_t* touched_out,
+                          uint32_t* count_out) {
+  return guarded([&] {
+    require(grid != nullptr && count_out != nullptr, "rlc_grid_slots: null argument");
+    const_cast<rlc_context*>(grid->ctx)->sync_all();
+    const rlc::DevGrid& g = grid->dev;
+    const size_t cap = g.capacity;
+    unsigned long long nc = 0;
+    RLC_CK(cudaMemcpy(&nc, g.counters + rlc::kCntCells, 8, cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> sk(2 * cap);
+    std::vector<uint32_t> sc(cap), ck(5 * static_cast<size_t>(nc)), tch(static_cast<size_t>(nc));
+    RLC_CK(cudaMemcpy(sk.data(), g.slot_keys, 16 * cap, cudaMemcpyDeviceToHost));
+    RLC_CK(cudaMemcpy(sc.data(), g.slot_cell, 4 * cap, cudaMemcpyDeviceToHost));
+    if (nc > 0) {
+      RLC_CK(cudaMemcpy(ck.data(), g.cell_key, 20 * size_t(nc), cudaMemcpyDeviceToHost));
+      RLC_CK(cudaMemcpy(tch.data(), g.touched, 4 * size_t(nc), cudaMemcpyDeviceToHost));
+    }
+    uint32_t n = 0;
+    for (size_t s = 0; s < cap; ++s) {
+      if (sk[2 * s] == 0 && sk[2 * s + 1] == 0) continue;  // empty slot
+      const uint32_t c = sc[s];
+      if (c >= nc) continue;  // (cannot happen between calls: claims publish their cell)
+      if (n < max_slots) {
+        if (slot_out) slot_out[n] = uint32_t(s);
+        if (cell_out) cell_out[n] = c;
+        if (key_out)
+          key_out[n] = rlc_cell_key{int32_t(ck[5 * c]), int32_t(ck[5 * c + 1]),
+                                    int32_t(ck[5 * c + 2]), ck[5 * c + 3], ck[5 * c + 4]};
+        if (touched_out) touched_out[n] = tch[c] ? 1 : 0;
+      }
+      ++n;
+    }
+    *count_out = n;
+  });
+}
+
 rlc_status rlc_grid_template(const rlc_grid* grid, uint32_t* node_ids, uint32_t* ends, double* q,
                              double* cdf, uint32_t* visits, double* eps_q) {
   return guarded([&] {

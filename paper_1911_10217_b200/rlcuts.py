@@ -250,6 +250,57 @@ class HashGrid:
                 "node_ids": node[i], "ends": ends[i], "q": q[i], "cdf": cdf[i], "visits": vis[i]}
         return out
 
+    def slots(self) -> list:
+        """Occupied slots in slot order: (slot, dense cell, CellKey, touched)."""
+        lib = _lib.load()
+        n = C.c_uint32()
+        _check(lib.rlc_grid_slots(self.handle, 0, None, None, None, None, C.byref(n)))
+        m = max(n.value, 1)
+        slot = np.zeros(m, np.uint32)
+        cell = np.zeros(m, np.uint32)
+        touched = np.zeros(m, np.uint8)
+        keys = (_lib.CellKeyC * m)()
+        _check(lib.rlc_grid_slots(self.handle, m, _uptr(slot), _uptr(cell), keys,
+                                  touched.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(n)))
+        return [(int(slot[i]), int(cell[i]),
+                 (keys[i].qx, keys[i].qy, keys[i].qz, keys[i].qn, keys[i].level), bool(touched[i]))
+                for i in range(min(n.value, m))]
+
+    def key_of(self, slot: int):
+        """HashGrid::key_of (hash_grid.hpp:90): the CellKey in `slot` (None: empty)."""
+        for s, _, k, _ in self.slots():
+            if s == slot:
+                return k
+        return None
+
+    def touched_slots(self) -> list:
+        """HashGrid::touched_slots (hash_grid.cpp:157-170): ready and touched
+        slots in slot order (between render_pass and end_of_pass_update)."""
+        return [s for s, _, _, t in self.slots() if t]
+
+    def memory_records(self) -> int:
+        """HashGrid::memory_records (hash_grid.cpp:179-187): the sum of cut
+        sizes over occupied slots (every cut keeps the template's size)."""
+        st = self.stats()
+        return st["occupied"] * st["cut_size"]
+
+    def dump_stats(self) -> str:
+        """HashGrid::dump_stats (hash_grid.cpp:189-202): CSV header and value
+        rows -- occupancy, lookups, fallback hits, per-level occupied counts."""
+        st = self.stats()
+        hist = [0] * 17
+        for _, _, k, _ in self.slots():
+            hist[min(k[4], 16)] += 1
+        head = "occupied,lookups,fallback_hits" + "".join(f",level_{l}" for l in range(17))
+        row = f"{st['occupied']},{st['lookups']},{st['fallback_hits']}" + \
+            "".join(f",{h}" for h in hist)
+        return head + "\n" + row + "\n"
+
+    def fallback_cut(self) -> dict:
+        """HashGrid::fallback_cut: the template cut, sampled on overflow and
+        never adapted (hash_grid.cpp:102-111, 136-140)."""
+        return self.template()
+
     def template(self) -> dict:
         m = self.stats()["cut_size"]
         node = np.zeros(m, np.uint32)

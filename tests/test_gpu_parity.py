@@ -305,3 +305,32 @@ def test_full_resolution_c3_properties():
         assert np.array_equal(cdf, np.cumsum(q))  # serial left-to-right sum, as rebuild_cdf
         assert (np.diff(ends.astype(np.int64)) > 0).all() and ends[-1] == n_emit
         assert (q > 0).all() and (v["visits"] >= 1).all()
+
+
+def test_hash_grid_host_views_match_reference(ref):
+    """HashGrid's host accessors (hash_grid.hpp:87-110) served from the device
+    grid: dump_stats text, memory_records, the touched slots between
+    render_pass and end_of_pass_update (compared by CellKey: slot positions
+    depend on insertion order under probing), key_of, fallback_cut."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=64, width=48, height=36)
+    cfg = rlcuts.RenderConfig(spp=3, passes=3, sampler=RL,
+                              cut=rlcuts.CutConfig(cut_size=32))
+    ctx = rlcuts.build_context(scene, cfg)
+    grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+    rr = ref.RefRun(scene, cfg)
+    for p in range(2):
+        rlcuts.render_pass(ctx, cfg, p, grid, fb)
+        rlcuts.end_of_pass_update(grid, ctx, cfg.cut)
+        rr.run_pass(p)
+    rlcuts.render_pass(ctx, cfg, 2, grid, fb)  # touched slots set, not yet cleared
+    rr.render_only(2)
+    text, mem, touched = rr.grid_views()
+    assert grid.dump_stats() == text
+    assert grid.memory_records() == mem
+    got = [grid.key_of(s) for s in grid.touched_slots()]
+    assert sorted(got) == sorted(touched) and len(got) > 50
+    assert grid.key_of(2**31) is None
+    tmpl = grid.fallback_cut()
+    assert tmpl["q"].shape == (32,) and tmpl["visits"].min() == 1
+    rlcuts.end_of_pass_update(grid, ctx, cfg.cut)
+    assert grid.touched_slots() == []
