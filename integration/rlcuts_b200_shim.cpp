@@ -3,6 +3,9 @@
 // include/rlcuts_b200.h; no reference source is needed.
 #include "rlcuts_b200_shim.hpp"
 
+#include <algorithm>
+#include <ostream>
+
 #include <chrono>
 #include <stdexcept>
 #include <string>
@@ -160,6 +163,63 @@ uint64_t Session::fallback_hits() const {
   rlc_grid_stats s{};
   if (impl_->g) check(rlc_grid_stats_get(impl_->g, &s));
   return s.fallback_hits;
+}
+
+namespace {
+struct SlotView {
+  std::vector<uint32_t> slot;
+  std::vector<rlc_cell_key> key;
+  std::vector<uint8_t> touched;
+};
+
+SlotView slot_view(rlc_grid* g) {
+  SlotView v;
+  if (!g) return v;
+  uint32_t n = 0;
+  check(rlc_grid_slots(g, 0, nullptr, nullptr, nullptr, nullptr, &n));
+  v.slot.resize(n);
+  v.key.resize(n);
+  v.touched.resize(n);
+  check(rlc_grid_slots(g, n, v.slot.data(), nullptr, v.key.data(), v.touched.data(), &n));
+  return v;
+}
+}  // namespace
+
+CellKey Session::key_of(uint32_t slot) const {
+  const SlotView v = slot_view(impl_->g);
+  for (size_t i = 0; i < v.slot.size(); ++i)
+    if (v.slot[i] == slot) {
+      const rlc_cell_key& k = v.key[i];
+      return CellKey{k.qx, k.qy, k.qz, k.qn, k.level};
+    }
+  return CellKey{};  // an empty slot holds a default key
+}
+
+std::vector<uint32_t> Session::touched_slots() const {
+  const SlotView v = slot_view(impl_->g);
+  std::vector<uint32_t> out;
+  for (size_t i = 0; i < v.slot.size(); ++i)
+    if (v.touched[i]) out.push_back(v.slot[i]);
+  return out;
+}
+
+uint64_t Session::memory_records() const {
+  rlc_grid_stats s{};
+  if (impl_->g) check(rlc_grid_stats_get(impl_->g, &s));
+  return uint64_t(s.occupied) * s.cut_size;  // every cut keeps the template's size
+}
+
+void Session::dump_stats(std::ostream& out) const {  // hash_grid.cpp:189-202
+  rlc_grid_stats s{};
+  if (impl_->g) check(rlc_grid_stats_get(impl_->g, &s));
+  uint64_t histogram[17] = {};
+  for (const rlc_cell_key& k : slot_view(impl_->g).key) ++histogram[std::min<uint32_t>(k.level, 16)];
+  out << "occupied,lookups,fallback_hits";
+  for (uint32_t level = 0; level <= 16; ++level) out << ",level_" << level;
+  out << "\n";
+  out << s.occupied << ',' << s.lookups << ',' << s.fallback_hits;
+  for (uint32_t level = 0; level <= 16; ++level) out << ',' << histogram[level];
+  out << "\n";
 }
 
 RenderResult render_frame(const RenderContext& ctx, const RenderConfig& config,

@@ -7,7 +7,10 @@
 
 #include <cstdint>
 #include <memory>
+#include <ostream>
+#include <vector>
 
+#include "rlcuts/hash_grid.hpp"
 #include "rlcuts/image.hpp"
 #include "rlcuts/render.hpp"
 
@@ -41,6 +44,13 @@ class Session {
   uint32_t occupied_count() const;
   uint64_t lookup_count() const;
   uint64_t fallback_hits() const;
+  // HashGrid's host accessors (hash_grid.hpp:87-110) over the device grid:
+  // key_of / touched_slots index the device table's slots (positions can
+  // differ from a CPU grid's, whose insertion order differs under probing).
+  CellKey key_of(uint32_t slot) const;
+  std::vector<uint32_t> touched_slots() const;
+  uint64_t memory_records() const;
+  void dump_stats(std::ostream& out) const;
 
  private:
   struct Impl;

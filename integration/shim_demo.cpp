@@ -3,17 +3,69 @@
 // rlcuts::b200::render_frame (this repo, via the C-ABI) and compares them.
 // Prints "MATCH <lookups> <cells>" when image, statistics, per-pass
 // split-collapse counts and per-pass mse against a reference image are
-// identical.
+// identical.  `shim_demo session`: rlcuts::b200::Session driven pass by pass
+// beside the reference's own HashGrid; its HashGrid accessors (dump_stats,
+// memory_records, the keys of touched_slots) must agree.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <sstream>
+#include <tuple>
+#include <vector>
 
 #include "rlcuts/render.hpp"
 #include "rlcuts/scene_gen.hpp"
 #include "rlcuts_b200_shim.hpp"
 
+static int session_demo() {
+  rlcuts::Scene scene = rlcuts::gen_cornell_grid(2, 1, 64);
+  scene.camera.width = 48;
+  scene.camera.height = 36;
+  rlcuts::RenderConfig cfg;
+  cfg.spp = 3;
+  cfg.passes = 3;
+  cfg.sampler = rlcuts::SamplerKind::rl_lightcuts;
+  cfg.cut.cut_size = 32;
+  const rlcuts::RenderContext ctx = rlcuts::build_context(scene, cfg);
+  rlcuts::HashConfig hash = cfg.hash;
+  hash.base_tile = ctx.base_tile;
+  rlcuts::HashGrid grid(hash, rlcuts::init_cut(ctx.tree, cfg.cut.cut_size, cfg.cut.eps_q));
+  rlcuts::Framebuffer fb(scene.camera.width, scene.camera.height);
+  rlcuts::b200::Session gpu(ctx, cfg);
+  for (uint32_t p = 0; p < 2; ++p) {
+    rlcuts::render_pass(ctx, cfg, p, &grid, fb);
+    rlcuts::end_of_pass_update(grid, ctx.tree, cfg.cut, cfg.workers);
+    gpu.render_pass(p);
+    gpu.end_of_pass_update();
+  }
+  rlcuts::render_pass(ctx, cfg, 2, &grid, fb);  // touched slots set, not yet cleared
+  gpu.render_pass(2);
+  std::ostringstream a, b;
+  grid.dump_stats(a);
+  gpu.dump_stats(b);
+  using K = std::tuple<int32_t, int32_t, int32_t, uint32_t, uint32_t>;
+  auto keys = [](auto&& slots, auto&& key_of) {
+    std::vector<K> v;
+    for (uint32_t s : slots) {
+      const rlcuts::CellKey k = key_of(s);
+      v.emplace_back(k.qx, k.qy, k.qz, k.qn, k.level);
+    }
+    std::sort(v.begin(), v.end());
+    return v;
+  };
+  const auto kc = keys(grid.touched_slots(), [&](uint32_t s) { return grid.key_of(s); });
+  const auto kg = keys(gpu.touched_slots(), [&](uint32_t s) { return gpu.key_of(s); });
+  const bool same = a.str() == b.str() && grid.memory_records() == gpu.memory_records() &&
+                    kc == kg && !kc.empty();
+  std::printf("%s touched=%zu records=%llu\n", same ? "MATCH" : "DIFFER", kg.size(),
+              (unsigned long long)gpu.memory_records());
+  return same ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
   try {
+    if (argc > 1 && std::strcmp(argv[1], "session") == 0) return session_demo();
     const int k = argc > 1 ? std::atoi(argv[1]) : 2;
     rlcuts::Scene scene = rlcuts::gen_cornell_grid(k, 1, 128);
     scene.camera.width = 64;

@@ -31,6 +31,6 @@ def test_shim_reports_missing_device():
 def test_shim_matches_reference_render_frame():
     if not os.path.exists(DEMO):
         pytest.skip("integration/shim_demo not built")
-    for k in ("1", "2"):
+    for k in ("1", "2", "session"):
         r = subprocess.run([DEMO, k], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0 and r.stdout.startswith("MATCH"), r.stdout + r.stderr
