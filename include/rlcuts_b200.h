@@ -192,7 +192,8 @@ rlc_status rlc_intersect_batch(const rlc_context* ctx, uint32_t n, const double*
 /* Diagnostic: traversal counters of a build with -DRLC_TRAV_STATS (zeros
  * otherwise): out8[0..2] shadow rays / node steps / triangle tests of
  * k_shadow, out8[3..5] rays / node steps / triangle tests of the SAH closest
- * hit.  reset != 0 clears them after reading. */
+ * hit, out8[6] shadow rays finished on the exact path after a stack
+ * overflow.  reset != 0 clears them after reading. */
 rlc_status rlc_debug_trav_stats(int32_t reset, uint64_t* out8);
 /* Diagnostic (parity tests): the closest-hit decision of the SAH tree alone
  * (DESIGN.md 5.4): as rlc_intersect_batch, but tri_out = -2 where the SAH

@@ -606,6 +606,8 @@ void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d, bo
   for (int a = 0; a < 3; ++a)
     if (!(std::fabs(h.scene_lo[a]) <= 1e8 && std::fabs(h.scene_hi[a]) <= 1e8)) d.fp32_ok = 0;
   d.nodes_root_leaf = h.nodes.empty() || h.nodes[0].count > 0 ? 1u : 0u;
+  d.shadow_stack_limit = 0;
+  if (const char* e = std::getenv("RLC_SHADOW_STACK_LIMIT")) d.shadow_stack_limit = uint32_t(std::atoi(e));
   d.shadow_eps = h.shadow_eps;
   d.coord_bound = h.coord_bound;
   d.libm_fma = probe_libm_variant() == rlc::libm::kFma ? 1u : 0u;

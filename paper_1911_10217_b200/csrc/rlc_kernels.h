@@ -96,6 +96,7 @@ struct DevScene {
   uint32_t num_tris;
   uint32_t fp32_ok;  // scene coordinates within 1e8: the fp32 shadow pre-test is valid
   uint32_t nodes_root_leaf;  // the reference BVH is a single leaf (no wide trees apply)
+  uint32_t shadow_stack_limit;  // test knob RLC_SHADOW_STACK_LIMIT: a smaller k_shadow stack (0: full)
   uint32_t libm_fma; // host libm build whose sin/cos the bounce sampler restates (rlc_libm.h)
   double shadow_eps;
   double coord_bound;  // S: k_shadow's lean test holds for ray origins within S

@@ -595,4 +595,5 @@ def trav_stats(reset: bool = True) -> dict:
     _check(_lib.load().rlc_debug_trav_stats(1 if reset else 0, out))
     v = list(out)
     return {"shadow_rays": v[0], "shadow_nodes": v[1], "shadow_tris": v[2],
-            "closest_rays": v[3], "closest_nodes": v[4], "closest_tris": v[5]}
+            "closest_rays": v[3], "closest_nodes": v[4], "closest_tris": v[5],
+            "shadow_overflows": v[6]}

@@ -147,3 +147,18 @@ def test_intersect_exact_ties_defer_to_reference_order(ref):
     dec, rtri = _check_sah(ctx, rr, o, d)
     hits = rtri >= 0
     assert hits.sum() > 1000 and not dec[hits].any()  # every hit is a tie
+
+
+@pytest.mark.parametrize("limit", ["3", "5"])
+def test_occluded_stack_overflow_finishes_exactly(ref, monkeypatch, limit):
+    """A shadow ray that would overflow k_shadow's shared-memory stack is
+    finished on the exact fp64 path: forced here with a tiny stack."""
+    monkeypatch.setenv("RLC_SHADOW_STACK_LIMIT", limit)
+    scene = random_soup(3000, 21, 6.0, 0.8)
+    ctx, rr = both(ref, scene)
+    rng = np.random.default_rng(79)
+    a = rng.uniform(0, 6, (20000, 3))
+    b = rng.uniform(0, 6, (20000, 3))
+    got, want = ctx.occluded(a, b), rr.occluded(a, b)
+    assert np.array_equal(got, want)
+    assert 100 < want.sum() < len(want)
