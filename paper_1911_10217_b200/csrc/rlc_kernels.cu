@@ -1246,7 +1246,10 @@ __device__ RLC_COLD bool intersect_wide(const DevScene& sc, V3 o, V3 d, double t
 #ifndef RLC_CLOSEST_SAH
 #define RLC_CLOSEST_SAH 1
 #endif
-constexpr int kSahStack = 32;
+#ifndef RLC_SAH_STACK
+#define RLC_SAH_STACK 32
+#endif
+constexpr int kSahStack = RLC_SAH_STACK;  // overflow: the ray is deferred to the ordered path
 
 __device__ __forceinline__ bool tri_t(const TriAccel* tris, uint32_t i, V3 o, V3 d, double* tout) {
   const double2* p = reinterpret_cast<const double2*>(tris + i);
@@ -1418,7 +1421,7 @@ __device__ __forceinline__ void mark_occluded(SampleRec* srec, uint32_t idx) {
 // steps to do (speculative traversal, Aila & Laine 2009), so both phases run
 // with as many lanes as possible.
 #ifndef RLC_SHADOW_BLOCKS
-#define RLC_SHADOW_BLOCKS 7  // minimum resident blocks per SM (register budget)
+#define RLC_SHADOW_BLOCKS 8  // blocks per SM (64 registers) with the 12-entry stack: c3 1.058 -> 1.045 ms (c5: 16.4 -> 16.8 ms; 7 was best with 32 entries)
 #endif
 template <bool QUANT>
 __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(DevScene sc,
