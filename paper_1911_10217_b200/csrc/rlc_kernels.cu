@@ -2438,7 +2438,11 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   }
   // with the update-record sort running beside it, one block slot per SM is
   // left to the sort (measured: 1.69 vs 1.71 ms per c3 frame)
-  const int use = leave_room && per_sm > 1 ? per_sm - 1 : per_sm;
+  static const int room = [] {  // RLC_SHADOW_ROOM: block slots per SM left to the sort
+    const char* e = getenv("RLC_SHADOW_ROOM");
+    return e ? atoi(e) : 1;
+  }();
+  const int use = leave_room && per_sm > room ? per_sm - room : per_sm;
   auto kern = sc.wide_q ? k_shadow<true> : k_shadow<false>;
   kern<<<use * sms, kShadowThreads, 0, st>>>(
       sc, b.rays, order, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
