@@ -104,11 +104,27 @@ struct SceneBuffers {
   struct Buf {
     void* p = nullptr;
     size_t cap = 0;
+    const void* host = nullptr;  // page-locked host source (cudaHostRegister), if any
+    size_t host_bytes = 0;
   };
   std::vector<Buf> bufs;
   size_t next = 0;
   uint64_t bytes = 0;
-  void begin() { next = 0; }
+  // Dynamic scene updates reuse the replaced scene's host buffers, so their
+  // addresses are stable from one update to the next: large ones are
+  // page-locked once (cudaHostRegister) and then DMA'd at full rate instead of
+  // being staged by the driver.
+  bool pin = false;
+  void begin(bool pin_sources = false) {
+    next = 0;
+    pin = pin_sources;
+  }
+  void unpin(Buf& b) {
+    if (b.host) cudaHostUnregister(const_cast<void*>(b.host));
+    cudaGetLastError();  // an already-freed source: nothing to undo
+    b.host = nullptr;
+    b.host_bytes = 0;
+  }
   // copy = false: the contents are known unchanged since the last upload
   // into this slot (a dynamic scene update's frozen arrays)
   template <class T>
@@ -126,13 +142,26 @@ struct SceneBuffers {
       b.cap = cap;
       bytes += cap;
     }
-    if (copy && !v.empty())
-      RLC_CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (copy && !v.empty()) {
+      const size_t n = v.size() * sizeof(T);
+      if (pin && n >= (size_t(1) << 20) && (b.host != v.data() || b.host_bytes != n)) {
+        unpin(b);
+        if (cudaHostRegister(const_cast<T*>(v.data()), n, cudaHostRegisterDefault) == cudaSuccess) {
+          b.host = v.data();
+          b.host_bytes = n;
+        } else {
+          cudaGetLastError();  // not pinnable: the pageable copy below still works
+        }
+      }
+      RLC_CK(cudaMemcpy(b.p, v.data(), n, cudaMemcpyHostToDevice));
+    }
     return static_cast<T*>(b.p);
   }
   ~SceneBuffers() {
-    for (Buf& b : bufs)
+    for (Buf& b : bufs) {
+      unpin(b);
       if (b.p) cudaFree(b.p);
+    }
   }
 };
 
@@ -572,7 +601,7 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
 // update = true: a dynamic scene update (rlc_context_update_scene), whose
 // materials, material ids and light tree are those of the previous upload.
 void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d, bool update = false) {
-  A.begin();
+  A.begin(update);
   d.nodes = A.put(h.nodes);
   d.nodes_f = A.put(h.nodes_f);
   d.nodes_cam = A.put(h.nodes_cam);
