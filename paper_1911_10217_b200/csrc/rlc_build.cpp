@@ -801,6 +801,25 @@ void node_ranges(const std::vector<BvhNode>& bin, std::vector<uint32_t>& first,
   }
 }
 
+// shadow_bin's nodes grouped by depth, deepest first (children after their
+// parent in the array, so depths come from one forward pass).
+void bin_levels(const std::vector<BvhNode>& bin, std::vector<uint32_t>& order,
+                std::vector<uint32_t>& level_start) {
+  std::vector<uint32_t> depth(bin.size(), 0);
+  uint32_t maxd = 0;
+  for (size_t k = 0; k < bin.size(); ++k) {
+    maxd = std::max(maxd, depth[k]);
+    if (bin[k].count == 0) depth[bin[k].a] = depth[bin[k].b] = depth[k] + 1;
+  }
+  std::vector<uint32_t> cnt(maxd + 2, 0);
+  for (uint32_t dd : depth) ++cnt[maxd - dd + 1];
+  level_start.assign(maxd + 2, 0);
+  for (uint32_t l = 1; l < maxd + 2; ++l) level_start[l] = level_start[l - 1] + cnt[l];
+  order.assign(bin.size(), 0);
+  std::vector<uint32_t> at(level_start.begin(), level_start.end() - 1);
+  for (size_t k = 0; k < bin.size(); ++k) order[at[maxd - depth[k]]++] = uint32_t(k);
+}
+
 void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
   PhaseTimer pt;
   out.wide.clear();
@@ -844,12 +863,13 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
     // child box is the union of its moved triangles' boxes (its tris_s
     // range); leaves whose triangles now lie in different reference leaves
     // lose kLeafPure
-    std::vector<uint32_t> leaf_of_id(out.tris.size());
+    std::vector<uint32_t>& leaf_of_id = out.refit_leaf;  // scratch reused across updates
+    leaf_of_id = std::move(keep->refit_leaf);
+    leaf_of_id.resize(out.tris.size());
     parallel_for(out.tris.size(), [&](size_t j) { leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j]; });
     const size_t nt = keep->tris_s.size();
     out.tris_s = std::move(keep->tris_s);  // positions and triangle ids kept; the
     out.tri_leaf_s.resize(nt);             // vertices are rewritten below
-    std::vector<Box> tb(nt);
     parallel_for(nt, [&](size_t i) {
       TriAccel& ta = out.tris_s[i];
       const uint32_t id = ta.tri_id;
@@ -858,13 +878,42 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
       put3(ta.e1, p1 - p0);
       put3(ta.e2, p2 - p0);
       out.tri_leaf_s[i] = leaf_of_id[id];
-      tb[i].grow(p0);
-      tb[i].grow(p1);
-      tb[i].grow(p2);
     });
     pt.lap("refit tris");
     const auto& kids = keep->wide_kids;
     const auto& bin = keep->shadow_bin;
+    // binary node boxes bottom up, one level at a time (leaves from their
+    // triangles' vertices, internal nodes from their children): O(n) work
+    std::vector<double>& nb = out.refit_box;
+    nb = std::move(keep->refit_box);
+    nb.resize(6 * bin.size());
+    const auto& order = keep->bin_order;
+    const auto& lstart = keep->bin_level_start;
+    for (size_t l = 0; l + 1 < lstart.size(); ++l) {
+      const uint32_t l0 = lstart[l], l1 = lstart[l + 1];
+      parallel_for(l1 - l0, [&](size_t q) {
+        const uint32_t k = order[l0 + q];
+        const BvhNode& nd = bin[k];
+        Box bx;
+        if (nd.count > 0) {
+          for (uint32_t i = nd.a; i < nd.a + nd.count; ++i) {
+            const uint32_t id = out.tris_s[i].tri_id;
+            bx.grow(vert(d, id, 0));
+            bx.grow(vert(d, id, 1));
+            bx.grow(vert(d, id, 2));
+          }
+        } else {
+          for (const uint32_t ch : {nd.a, nd.b}) {
+            const double* c = &nb[6 * size_t(ch)];
+            bx.grow(V3{c[0], c[1], c[2]});
+            bx.grow(V3{c[3], c[4], c[5]});
+          }
+        }
+        double* o = &nb[6 * size_t(k)];
+        o[0] = bx.lo.x, o[1] = bx.lo.y, o[2] = bx.lo.z, o[3] = bx.hi.x, o[4] = bx.hi.y, o[5] = bx.hi.z;
+      }, 512);
+    }
+    pt.lap("refit boxes");
     const double pad = S * 0x1.0p-21;
     out.wide = std::move(keep->wide);  // rewritten in place: boxes and leaf bits
     parallel_for(kids.size(), [&](size_t w) {
@@ -879,11 +928,10 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
           }
           continue;
         }
-        Box bx;
-        for (uint32_t i = keep->bin_first[b]; i < keep->bin_end[b]; ++i) bx.grow(tb[i]);
+        const double* bx = &nb[6 * size_t(b)];
         for (int a = 0; a < 3; ++a) {  // as collapse_wide (no origin, no growth)
-          n.lo[a][c] = round_down(comp(bx.lo, a) - pad);
-          n.hi[a][c] = round_up(comp(bx.hi, a) + pad);
+          n.lo[a][c] = round_down(bx[a] - pad);
+          n.hi[a][c] = round_up(bx[3 + a] + pad);
         }
         const BvhNode& bn = bin[b];
         if (bn.count > 0) {
@@ -891,11 +939,9 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
           for (uint32_t k = 1; k < bn.count; ++k)
             pure &= out.tri_leaf_s[bn.a + k] == out.tri_leaf_s[bn.a];
           n.child[c] = kWideLeaf | ((bn.count - 1) << 28) | (pure ? kLeafPure : 0u) | bn.a;
-        } else {
-          // internal: the creation numbering, already in place
-        }
+        }  // internal: the creation numbering, already in place
       }
-    }, 64);
+    }, 512);
     pt.lap("wide refit");
   } else {
     std::vector<uint32_t> perm;
@@ -909,6 +955,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
     out.wide = collapse_wide(out.shadow_bin, nullptr, 0.0, S * 0x1.0p-21, &out.tri_leaf_s,
                              &out.wide_kids);
     node_ranges(out.shadow_bin, out.bin_first, out.bin_end);
+    bin_levels(out.shadow_bin, out.bin_order, out.bin_level_start);
   }
   f_ref.get();
   pt.lap("wide_ref");
@@ -1244,6 +1291,8 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
       out.wide_kids = std::move(keep->wide_kids);
       out.bin_first = std::move(keep->bin_first);
       out.bin_end = std::move(keep->bin_end);
+      out.bin_order = std::move(keep->bin_order);
+      out.bin_level_start = std::move(keep->bin_level_start);
     }
   }
 }

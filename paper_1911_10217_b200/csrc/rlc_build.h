@@ -44,6 +44,11 @@ struct HostScene {
   // wide boxes straight from the moved triangles
   std::vector<std::array<uint32_t, kWide>> wide_kids;
   std::vector<uint32_t> bin_first, bin_end;
+  // shadow_bin nodes deepest level first, and each level's start in it (the
+  // refit's bottom-up order); refit scratch reused from update to update
+  std::vector<uint32_t> bin_order, bin_level_start;
+  std::vector<double> refit_box;    // [6] per shadow_bin node
+  std::vector<uint32_t> refit_leaf; // reference leaf per triangle id
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;
   // materials / triangles
