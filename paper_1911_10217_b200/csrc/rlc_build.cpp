@@ -276,9 +276,26 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
         const Todo t = level[k];
         const uint32_t count = t.end - t.begin;
         Box bounds, cb;
-        for (uint32_t i = t.begin; i < t.end; ++i) {
-          bounds.grow(tb[perm[i]]);
-          cb.grow(cen[perm[i]]);
+        if (count >= 32768) {  // min/max: chunked in parallel, exactly the same boxes
+          constexpr uint32_t kChunk = 4096;
+          const uint32_t nc = (count + kChunk - 1) / kChunk;
+          std::vector<Box> pb(nc), pc(nc);
+          parallel_for(nc, [&](size_t c) {
+            const uint32_t b0 = t.begin + uint32_t(c) * kChunk, b1 = std::min(t.end, b0 + kChunk);
+            for (uint32_t i = b0; i < b1; ++i) {
+              pb[c].grow(tb[perm[i]]);
+              pc[c].grow(cen[perm[i]]);
+            }
+          }, 1);
+          for (uint32_t c = 0; c < nc; ++c) {
+            bounds.grow(pb[c]);
+            cb.grow(pc[c]);
+          }
+        } else {
+          for (uint32_t i = t.begin; i < t.end; ++i) {
+            bounds.grow(tb[perm[i]]);
+            cb.grow(cen[perm[i]]);
+          }
         }
         BvhNode& nd = nodes[t.node];
         put3(nd.lo, bounds.lo);
