@@ -488,6 +488,9 @@ __device__ __forceinline__ void cas128(unsigned long long* addr, uint64_t new_lo
 // capacity, at most min(probe_limit, capacity) slots, CAS-claim of an empty
 // slot; the claimer takes a dense cell id and copies the template cut in.
 // The dense id is published to other paths at the kernel boundary.
+#ifndef RLC_PROBE_LOAD_FIRST
+#define RLC_PROBE_LOAD_FIRST 1
+#endif
 __device__ uint32_t probe_insert(const DevGrid& g, const Key& k, uint64_t h) {
   uint64_t lo, hi;
   pack_key(k, lo, hi);
@@ -495,6 +498,16 @@ __device__ uint32_t probe_insert(const DevGrid& g, const Key& k, uint64_t h) {
   uint32_t slot = uint32_t(h % uint64_t(g.capacity));
   for (uint32_t i = 0; i < probes; ++i) {
     uint64_t olo, ohi;
+#if RLC_PROBE_LOAD_FIRST
+    // a claimed slot never changes: a plain L2 read settles every slot but an
+    // empty one (a stale "empty" only costs the CAS below, which is exact)
+    const ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(g.slot_keys + 2 * size_t(slot)));
+    if (cur.x == lo && cur.y == hi) return slot;
+    if (cur.x != 0 || cur.y != 0) {
+      slot = slot + 1 == g.capacity ? 0 : slot + 1;
+      continue;
+    }
+#endif
     cas128(g.slot_keys + 2 * size_t(slot), lo, hi, olo, ohi);
     if (olo == 0 && ohi == 0) {  // claimed: new cell
       const uint32_t cid = uint32_t(atomicAdd(g.counters + kCntCells, 1ull));
