@@ -331,6 +331,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     batch = world == 1 and not dynamic
     ctx.enable_timing(not batch)
     l0 = grid.lookup_count()
+    ins0 = grid.insertion_stats()
     launches0 = rlcuts.kernel_launches()
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -354,6 +355,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     launches = rlcuts.kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
     lookups = grid.lookup_count() - l0
+    ins1 = grid.insertion_stats()
+    grid_insert_stats = {f"{k}_per_frame": (ins1[k] - ins0[k]) / args.steps for k in ins1}
     stage_frames = args.steps
     if batch:  # per-kernel times: a few more frames with CUDA events around every stage
         stage_frames = min(args.steps, 20)
@@ -470,7 +473,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "l2": "no flush: resident scene+cut+pass buffers exceed the 126 MB L2",
                        "parallelism": (f"screen bands x{world}, exact update-record all-gather "
                                        f"over {args.dist_backend}" if world > 1 else "single GPU"),
-                       "cells": st["occupied"], "fallback_hits": st["fallback_hits"]},
+                       "cells": st["occupied"], "fallback_hits": st["fallback_hits"],
+                       **grid_insert_stats},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
             "stage_ms_per_step": {k: v[0] / stage_frames for k, v in stages.items()},

@@ -126,6 +126,11 @@ typedef struct rlc_grid_stats {
   uint32_t cut_size;
   uint64_t lookups;
   uint64_t fallback_hits;
+  /* lookups whose key was not in the table when their pass began, and the
+   * distinct such keys (each inserted, or refused by a full probe window,
+   * in canonical order after the pass's lookups) */
+  uint64_t pending_lookups;
+  uint64_t new_keys;
 } rlc_grid_stats;
 
 typedef struct rlc_context_info {
@@ -171,11 +176,12 @@ rlc_status rlc_context_synchronize(rlc_context* ctx);
 
 /* Per-stage device timing with CUDA events on the context stream (bench
  * evidence).  Stages: 0 primary, 1 sample, 2 sort, 3 fold, 4 accumulate,
- * 5 split-collapse, 6 shadow (any-hit traversal).  Stage 0 includes the
+ * 5 split-collapse, 6 shadow (any-hit traversal), 7 insert (the pass's new
+ * hash-grid keys, in canonical order).  Stage 0 includes the
  * bounce rays of max_depth > 1.  rlc_context_stage_times synchronizes,
  * returns accumulated milliseconds and launch counts per stage since the
  * last call, and resets them. */
-#define RLC_NUM_STAGES 7
+#define RLC_NUM_STAGES 8
 rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable);
 rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts);
 
@@ -301,6 +307,40 @@ rlc_status rlc_pass_trace(const rlc_context* ctx, const rlc_render_config* confi
 rlc_status rlc_pass_fold(const rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
                          rlc_framebuffer* fb, const void* all_records, const uint64_t* counts,
                          uint32_t nranks, uint32_t rank, uint64_t stride);
+
+/* ---- per-sample parity export (SURVEY 8(b) "opt-in per-sample record
+ * dump") ---------------------------------------------------------------
+ * One record per path vertex of the context's last render_pass / sharded
+ * pass (rows of that call, canonical order: pixel, sample, depth).  A vertex
+ * that drew a light sample (sample_light, proj/src/estimators.cpp:28-80)
+ * has RLC_SAMPLE_VALID; `emitter` is the selected emitter index (the
+ * north star's bit-exact light selection), `cluster` the cut entry
+ * (sample_cluster, proj/src/cut.cpp:97-106), `q_before` the live q the
+ * reference's pdf reads (cut.cpp:105), `v` the update_q value
+ * (estimators.cpp:103-104, 0 when occluded), `total` the frozen cdf total,
+ * `radiance` nee_estimate's radiance (estimators.cpp:100-101).  Emitter
+ * indices are filed only while rlc_context_enable_sample_export is on. */
+enum {
+  RLC_SAMPLE_VALID = 1,      /* a light sample was drawn at this vertex */
+  RLC_SAMPLE_FALLBACK = 2,   /* the cell lookup fell back (hash_grid.cpp:140) */
+  RLC_SAMPLE_RAY = 4,        /* a shadow segment was traced (bvh.cpp:159-188) */
+  RLC_SAMPLE_NONZERO = 8,    /* unoccluded, front-facing: nonzero contribution */
+  RLC_SAMPLE_LEARNED = 16    /* drawn from a cut (rl_lightcuts) */
+};
+typedef struct rlc_sample_record {
+  uint32_t vertex;  /* canonical index within the pass's rows */
+  uint32_t cluster;
+  uint32_t emitter;
+  uint32_t flags;   /* RLC_SAMPLE_* */
+  double q_before;
+  double v;
+  double total;
+  double radiance[3];
+} rlc_sample_record;
+rlc_status rlc_context_enable_sample_export(rlc_context* ctx, int enable);
+/* out [max_n] may be NULL (count only); *n_out = path vertices of the pass. */
+rlc_status rlc_pass_samples(const rlc_context* ctx, uint64_t max_n, rlc_sample_record* out,
+                            uint64_t* n_out);
 
 /* render_frame (proj/src/render.cpp:202-240): image_out [h*w*3] host,
  * resolved; result may be NULL. */

@@ -58,6 +58,7 @@ _SIGS = {
     "ref_make_key": (C.c_int, [C.c_uint32, _dp, _dp, _u32p, _dp, _dp, C.c_double, C.c_uint32,
                                C.c_double, C.POINTER(_lib.CellKeyC), _u64p]),
     "ref_octa_encode": (None, [C.c_uint32, _dp, _dp]),
+    "ref_run_slots": (C.c_uint32, [_P, C.c_uint32, _u32p, _u32p]),
     "ref_run_grid_views": (C.c_uint32, [C.c_void_p, C.c_char_p, C.c_uint32, _u64p, _u32p,
                                         C.c_uint32]),
 }
@@ -168,6 +169,16 @@ class RefRun:
         touched = [(int(k[i, 0]), int(k[i, 1]), int(k[i, 2]), int(keys[5 * i + 3]),
                     int(keys[5 * i + 4])) for i in range(min(n, cap))]
         return buf.value.decode(), int(mem[0]), touched
+
+    def slots(self) -> list:
+        """Occupied slots in slot order: (slot, CellKey)."""
+        n = max(self.stats()["occupied"], 1)
+        slot = np.zeros(n, np.uint32)
+        keys = np.zeros(5 * n, np.uint32)
+        got = ref_lib().ref_run_slots(self.h, n, up(slot), up(keys))
+        k = keys.view(np.int32).reshape(-1, 5)
+        return [(int(slot[i]), (int(k[i, 0]), int(k[i, 1]), int(k[i, 2]), int(keys[5 * i + 3]),
+                                int(keys[5 * i + 4]))) for i in range(min(got, n))]
 
     def export(self) -> dict:
         st = self.stats()

@@ -274,6 +274,29 @@ uint32_t ref_run_grid_views(void* h, char* out, uint32_t cap, uint64_t* mem_reco
   return uint32_t(t.size());
 }
 
+// Occupied slots in slot order (HashGrid::key_of per slot, hash_grid.hpp:90):
+// slot index and 5 u32 of its CellKey.  Returns the number of occupied slots.
+uint32_t ref_run_slots(void* h, uint32_t max_n, uint32_t* slot_out, uint32_t* key_out) {
+  RefRun* run = static_cast<RefRun*>(h);
+  if (!run->grid) return 0;
+  const HashGrid& g = *run->grid;
+  uint32_t n = 0;
+  for (uint32_t slot = 0; slot < g.config().capacity; ++slot) {
+    if (g.cut(CellHandle{slot}).size() == 0) continue;
+    if (n < max_n) {
+      const CellKey& k = g.key_of(slot);
+      slot_out[n] = slot;
+      key_out[5 * n] = uint32_t(k.qx);
+      key_out[5 * n + 1] = uint32_t(k.qy);
+      key_out[5 * n + 2] = uint32_t(k.qz);
+      key_out[5 * n + 3] = k.qn;
+      key_out[5 * n + 4] = k.level;
+    }
+    ++n;
+  }
+  return n;
+}
+
 // dout: base_tile, shadow_eps;  uout: triangles, emitters, bvh nodes, tree nodes
 void ref_run_info(void* h, double* dout, uint32_t* uout) {
   RefRun* run = static_cast<RefRun*>(h);

@@ -61,7 +61,8 @@ class RenderResultC(C.Structure):
 
 class GridStatsC(C.Structure):
     _fields_ = [("occupied", C.c_uint32), ("cut_size", C.c_uint32), ("lookups", C.c_uint64),
-                ("fallback_hits", C.c_uint64)]
+                ("fallback_hits", C.c_uint64), ("pending_lookups", C.c_uint64),
+                ("new_keys", C.c_uint64)]
 
 
 class ContextInfoC(C.Structure):
@@ -126,6 +127,8 @@ SIGNATURES = {
     "rlc_pass_fold": (C.c_int, [_P, C.POINTER(RenderConfigC), _P, _P, _P, _u64p, C.c_uint32,
                                 C.c_uint32, C.c_uint64]),
     "rlc_render_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.POINTER(RenderResultC)]),
+    "rlc_context_enable_sample_export": (C.c_int, [_P, C.c_int]),
+    "rlc_pass_samples": (C.c_int, [_P, C.c_uint64, C.c_void_p, _u64p]),
     "rlc_context_update_scene": (C.c_int, [_P, C.POINTER(SceneDescC)]),
     "rlc_render_frame_scored": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.c_int32, C.c_int32,
                                           _dp, C.POINTER(RenderResultC), _dp]),

@@ -82,10 +82,12 @@ struct DeviceArena {
     bytes += b;
     return static_cast<T*>(p);
   }
+  // ordered on stream st; the caller synchronizes st before freeing v
   template <class T>
-  T* upload(const std::vector<T>& v) {
+  T* upload(const std::vector<T>& v, cudaStream_t st) {
     T* p = alloc<T>(v.size());
-    if (!v.empty()) RLC_CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!v.empty())
+      RLC_CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     return p;
   }
   void release() {
@@ -95,6 +97,23 @@ struct DeviceArena {
   }
   ~DeviceArena() { release(); }
 };
+
+// A pass's new-key table (rlc::NewKeys) for up to n lookups: 2^k >= 2n
+// entries, cleared once here and then by k_commit after every pass.
+rlc::NewKeys alloc_new_keys(DeviceArena& A, uint64_t n, cudaStream_t st) {
+  uint64_t cap = 1024;
+  while (cap < 2 * n) cap <<= 1;
+  rlc::NewKeys nk{};
+  nk.keys = A.alloc<unsigned long long>(2 * cap);
+  nk.id = A.alloc<uint32_t>(cap);
+  nk.list = A.alloc<uint32_t>(cap);
+  nk.count = A.alloc<unsigned int>(1);
+  nk.mask = uint32_t(cap - 1);
+  RLC_CK(cudaMemsetAsync(nk.keys, 0, 16 * cap, st));
+  RLC_CK(cudaMemsetAsync(nk.id, 0xff, 4 * cap, st));
+  RLC_CK(cudaMemsetAsync(nk.count, 0, 4, st));
+  return nk;
+}
 
 // The scene arrays of a context: one device buffer per array, in the fixed
 // order of upload_scene, reused by rlc_context_update_scene while the new
@@ -115,8 +134,10 @@ struct SceneBuffers {
   // page-locked once (cudaHostRegister) and then DMA'd at full rate instead of
   // being staged by the driver.
   bool pin = false;
-  void begin(bool pin_sources = false) {
+  cudaStream_t stream = nullptr;  // the context stream the copies are ordered on
+  void begin(cudaStream_t st, bool pin_sources = false) {
     next = 0;
+    stream = st;
     pin = pin_sources;
   }
   void unpin(Buf& b) {
@@ -153,7 +174,7 @@ struct SceneBuffers {
           cudaGetLastError();  // not pinnable: the pageable copy below still works
         }
       }
-      RLC_CK(cudaMemcpy(b.p, v.data(), n, cudaMemcpyHostToDevice));
+      RLC_CK(cudaMemcpyAsync(b.p, v.data(), n, cudaMemcpyHostToDevice, stream));
     }
     return static_cast<T*>(b.p);
   }
@@ -220,6 +241,7 @@ const char* device_error_message(uint32_t bits) {
   if (bits & rlc::kErrDegenerateLight) return "sample_triangle_point: degenerate triangle";
   if (bits & rlc::kErrBadAreaPdf) return "level_for_footprint: area pdf must be positive";
   if (bits & rlc::kErrStackOverflow) return "scene BVH deeper than the 64-entry traversal stack";
+  if (bits & rlc::kErrNewKeyOverflow) return "hash grid: new-key table of the pass overflowed";
   return "device error";
 }
 
@@ -266,8 +288,20 @@ struct rlc_context {
   }
   bool overlap = true;  // primary rays of the next pass on a side stream (RLC_OVERLAP=0: off)
   cudaEvent_t ev_prim_done = nullptr;
+  // Orders all later side-stream work after everything enqueued on the main
+  // stream so far.  The next pass's primary rays wait only for their G-buffer
+  // slot, so a main-stream write they read (a grid reset, a fresh grid's
+  // slots, a scene upload) must be followed by this fence.
+  cudaEvent_t ev_main_fence = nullptr;
+  cudaEvent_t ev_commit = nullptr;  // the last pass's new keys are in the table
+  void fence_side() {
+    RLC_CK(cudaEventRecord(ev_main_fence, stream));
+    if (pstream) RLC_CK(cudaStreamWaitEvent(pstream, ev_main_fence, 0));
+    if (sstream) RLC_CK(cudaStreamWaitEvent(sstream, ev_main_fence, 0));
+  }
   cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
   rlc::GBuf* gslot[2] = {nullptr, nullptr};
+  unsigned long long* pkey_slot[2] = {nullptr, nullptr};  // pending keys, per G-buffer slot
   void sync_all() {
     RLC_CK(cudaStreamSynchronize(stream));
     if (pstream) RLC_CK(cudaStreamSynchronize(pstream));
@@ -313,6 +347,8 @@ struct rlc_context {
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (ev_prim_done) cudaEventDestroy(ev_prim_done);
+    if (ev_main_fence) cudaEventDestroy(ev_main_fence);
+    if (ev_commit) cudaEventDestroy(ev_commit);
     if (ev_sample_done) cudaEventDestroy(ev_sample_done);
     if (ev_fold_done) cudaEventDestroy(ev_fold_done);
     if (ev_acc_done) cudaEventDestroy(ev_acc_done);
@@ -342,6 +378,7 @@ struct rlc_context {
     xb.vals_alt = xarena.alloc<uint32_t>(cap);
     xb.hist = xarena.alloc<uint32_t>((size_t(cap) / 4096 + 2) * 256);
     xb.q_rec = xarena.alloc<double>(cap);
+    xb.nk = alloc_new_keys(xarena, cap, stream);
     xb.cap = cap;
     d_counts = xarena.alloc<unsigned long long>(nr);
     d_counts_cap = nr;
@@ -378,6 +415,10 @@ struct rlc_context {
   size_t h_stage_cap = 0;
   uint32_t* d_changes = nullptr;  // device change count of graph replays
   rlc::UpdateRecord* rec_out = nullptr;  // this rank's exported update records
+  // rlc_pass_samples: the last pass's parameters and G-buffer slot
+  bool export_samples = false;
+  rlc::PassParams last_pass{};
+  rlc::GBuf* last_gbuf = nullptr;
 
   void ensure_scratch(uint32_t n) {
     if (n <= pb_cap) return;
@@ -388,6 +429,11 @@ struct rlc_context {
     gslot[0] = scratch.alloc<rlc::GBuf>(cap);
     gslot[1] = scratch.alloc<rlc::GBuf>(cap);
     pb.gbuf = gslot[0];
+    pkey_slot[0] = scratch.alloc<unsigned long long>(2 * size_t(cap));
+    pkey_slot[1] = scratch.alloc<unsigned long long>(2 * size_t(cap));
+    pb.pkey = pkey_slot[0];
+    pb.nk = alloc_new_keys(scratch, cap, stream);
+    pb.emit = scratch.alloc<uint32_t>(cap);
     pb.srec = scratch.alloc<rlc::SampleRec>(cap);
     pb.rflag = scratch.alloc<uint8_t>(cap);
     pb.keys = scratch.alloc<uint32_t>(cap);
@@ -440,7 +486,8 @@ uint32_t read_and_clear_err(cudaStream_t st, unsigned long long* counters) {
 }
 
 void throw_device_error(uint32_t bits) {
-  if (bits & rlc::kErrStackOverflow) throw std::runtime_error(device_error_message(bits));
+  if (bits & (rlc::kErrStackOverflow | rlc::kErrNewKeyOverflow))
+    throw std::runtime_error(device_error_message(bits));
   throw rlc::InvalidArgument(device_error_message(bits));
 }
 
@@ -488,6 +535,7 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
   S.p.alpha = grid ? grid->alpha : cfg->cut.alpha;
   S.p.harmonic = grid ? grid->harmonic : 0u;
   S.p.pass_dev = ctx->graph_pass_dev;
+  S.p.export_samples = ctx->export_samples ? 1u : 0u;
   if (grid) S.g = grid->dev;
   else S.g.counters = ctx->counters;
   if (S.nv > 0) ctx->ensure_scratch(S.nv);
@@ -506,20 +554,42 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   // G-buffer slot is free and overlap the previous pass's tail.
   const int slot = int(S.p.pass_index & 1u);
   ctx->pb.gbuf = ctx->gslot[slot];
+  ctx->pb.pkey = ctx->pkey_slot[slot];
+  const bool rl = S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
+  // The pass's new keys go in after all its lookups, in canonical order
+  // (k_insert / k_commit, the reference's sequential insertion), right behind
+  // the primary rays (one vertex per path) or behind the last bounce; k_sample
+  // then finds them.  Side-stream placements that keep the two small launches
+  // off the critical path (a resolve kernel ahead of the record sort) measured
+  // slower: the sort, already level with the shadow rays, then waits for them
+  // (c3 1.108 vs 1.042 ms per frame, same box).
+  const bool insert = rl && !S.p.defer_insert;
+  const cudaStream_t ps = ctx->overlap ? ctx->pstream : st;
+  auto insert_new_keys = [&](cudaStream_t s) {
+    ctx->stage_on(s, 7, [&] { rlc::launch_insert_new_keys(S.g, ctx->pb.nk, s); });
+  };
+  if (ctx->overlap) RLC_CK(cudaStreamWaitEvent(ps, ctx->ev_gbuf_free[slot], 0));
+  if (rl) RLC_CK(cudaMemsetAsync(ctx->pb.nk.count, 0, sizeof(unsigned int), ps));
+  ctx->stage_on(ps, 0, [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, ps); });
+  if (insert && S.p.depth == 1) insert_new_keys(ps);
   if (ctx->overlap) {
-    RLC_CK(cudaStreamWaitEvent(ctx->pstream, ctx->ev_gbuf_free[slot], 0));
-    ctx->stage_on(ctx->pstream, 0,
-                  [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, ctx->pstream); });
-    RLC_CK(cudaEventRecord(ctx->ev_prim_done, ctx->pstream));
+    RLC_CK(cudaEventRecord(ctx->ev_prim_done, ps));
     RLC_CK(cudaStreamWaitEvent(st, ctx->ev_prim_done, 0));
-  } else {
-    ctx->stage(0, [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, st); });
   }
   // Multi-bounce paths (max_depth > 1): one launch per further vertex; the
   // vertices of all depths then share the sample / sort / shadow / fold
   // launches below, in canonical (path, depth) order.
   for (uint32_t d = 2; d <= S.p.depth; ++d)
     ctx->stage(0, [&] { rlc::launch_bounce(ctx->dev, S.g, S.p, d, ctx->pb, st); });
+  if (insert && S.p.depth > 1) {
+    insert_new_keys(st);
+    // the next pass's lookups (primary stream) read the table and reuse the
+    // new-key table
+    if (ps != st) {
+      RLC_CK(cudaEventRecord(ctx->ev_commit, st));
+      RLC_CK(cudaStreamWaitEvent(ps, ctx->ev_commit, 0));
+    }
+  }
   ctx->stage(1, [&] { rlc::launch_sample(ctx->dev, S.g, S.p, ctx->pb, st); });
   // The update records are sorted by (cell, cluster) for the fold on the
   // side stream while the shadow rays are traced, in canonical (pixel)
@@ -528,7 +598,6 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   // on c3).  The any-hit result does not depend on the order.
   *k = nullptr;
   *v = nullptr;
-  const bool rl = S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
   if (rl) {
     RLC_CK(cudaEventRecord(ctx->ev_sample_done, st));
     RLC_CK(cudaStreamWaitEvent(ctx->sstream, ctx->ev_sample_done, 0));
@@ -552,6 +621,8 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   if (S.n == 0) return;
   uint32_t *k = nullptr, *v = nullptr;
   if (S.nv > 0) enqueue_trace(ctx, S, grid, &k, &v);  // max_depth 0: empty paths
+  ctx->last_pass = S.p;
+  ctx->last_gbuf = ctx->pb.gbuf;
   cudaStream_t st = ctx->stream;
   if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && S.nv > 0) {
     ctx->stage(3, [&] { rlc::launch_fold(S.g, S.p, k, v, ctx->pb, st); });
@@ -600,8 +671,9 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
 // Uploads the device view of a host scene into arena A.
 // update = true: a dynamic scene update (rlc_context_update_scene), whose
 // materials, material ids and light tree are those of the previous upload.
-void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d, bool update = false) {
-  A.begin(update);
+void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d, cudaStream_t st,
+                  bool update = false) {
+  A.begin(st, update);
   d.nodes = A.put(h.nodes);
   d.nodes_f = A.put(h.nodes_f);
   d.nodes_cam = A.put(h.nodes_cam);
@@ -688,15 +760,17 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     ctx->device = device;
     ctx->create_cfg = *config;
     rlc::build_host_scene(*scene, *config, ctx->host);
-    upload_scene(ctx->host, ctx->scene_bufs, ctx->dev);
-    ctx->counters = ctx->arena.alloc<unsigned long long>(rlc::kCntNum);
-    RLC_CK(cudaMemset(ctx->counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
+    upload_scene(ctx->host, ctx->scene_bufs, ctx->dev, ctx->stream);
+    ctx->counters = ctx->arena.alloc<unsigned long long>(rlc::kCntNum);
+    RLC_CK(cudaMemsetAsync(ctx->counters, 0, sizeof(unsigned long long) * rlc::kCntNum, ctx->stream));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking));
     ctx->overlap = true;  // measured faster on c3 (1.51 vs 1.56 ms per frame)
     if (const char* e = std::getenv("RLC_OVERLAP")) ctx->overlap = std::string(e) != "0";
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_prim_done, cudaEventDisableTiming));
+    RLC_CK(cudaEventCreateWithFlags(&ctx->ev_main_fence, cudaEventDisableTiming));
+    RLC_CK(cudaEventCreateWithFlags(&ctx->ev_commit, cudaEventDisableTiming));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->sstream, cudaStreamNonBlocking));
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_sample_done, cudaEventDisableTiming));
     RLC_CK(cudaEventCreateWithFlags(&ctx->ev_fold_done, cudaEventDisableTiming));
@@ -750,7 +824,10 @@ rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scen
     ctx->sync_all();  // the previous frame's kernels read the buffers
     lap("sync");
     rlc::DevScene d{};
-    upload_scene(h, ctx->scene_bufs, d, true);
+    upload_scene(h, ctx->scene_bufs, d, ctx->stream, true);
+    // the copies complete before the host buffers are reused or freed and
+    // before any stream reads the new scene
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
     ctx->dev = d;
     ctx->host = std::move(h);
     ++ctx->scene_gen;  // captured pass graphs hold the old scene's pointers
@@ -963,8 +1040,9 @@ rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg,
     g->key_bits = bits;
     DeviceArena& A = g->arena;
     rlc::DevGrid& d = g->dev;
+    const cudaStream_t st = ctx->stream;
     d.slot_keys = A.alloc<unsigned long long>(2 * cap);
-    RLC_CK(cudaMemset(d.slot_keys, 0, 16 * cap));
+    RLC_CK(cudaMemsetAsync(d.slot_keys, 0, 16 * cap, st));
     d.slot_cell = A.alloc<uint32_t>(cap);
     d.capacity = uint32_t(cap);
     d.probe_limit = cfg->hash.probe_limit;
@@ -982,17 +1060,21 @@ rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg,
     d.split_scratch = size_t(M) * 32 > rlc::kSplitSmemMax
                           ? A.alloc<unsigned char>(size_t(rlc::kSplitGlobalWarps) * 32 * M)
                           : nullptr;
-    RLC_CK(cudaMemset(d.touched, 0, 4 * cap));
-    d.t_node = A.upload(g->tmpl.node_ids);
-    d.t_ends = A.upload(g->tmpl.ends);
-    d.t_q = A.upload(g->tmpl.q);
-    d.t_cdf = A.upload(g->tmpl.cdf);
-    d.t_visits = A.upload(g->tmpl.visits);
+    RLC_CK(cudaMemsetAsync(d.touched, 0, 4 * cap, st));
+    d.t_node = A.upload(g->tmpl.node_ids, st);
+    d.t_ends = A.upload(g->tmpl.ends, st);
+    d.t_q = A.upload(g->tmpl.q, st);
+    d.t_cdf = A.upload(g->tmpl.cdf, st);
+    d.t_visits = A.upload(g->tmpl.visits, st);
     d.eps_q = g->tmpl.eps_q;
     d.counters = A.alloc<unsigned long long>(rlc::kCntNum);
-    RLC_CK(cudaMemset(d.counters, 0, sizeof(unsigned long long) * rlc::kCntNum));
+    RLC_CK(cudaMemsetAsync(d.counters, 0, sizeof(unsigned long long) * rlc::kCntNum, st));
+    d.claim = A.alloc<unsigned long long>(cap);
+    RLC_CK(cudaMemsetAsync(d.claim, 0xff, 8 * cap, st));
     g->d_changes = A.alloc<uint32_t>(1);
-    RLC_CK(cudaMemset(g->d_changes, 0, 4));
+    RLC_CK(cudaMemsetAsync(g->d_changes, 0, 4, st));
+    // initialised before this call returns: any stream of the context may use it
+    RLC_CK(cudaStreamSynchronize(st));
     g->alpha = cfg->cut.alpha;
     g->harmonic = cfg->cut.alpha_schedule == RLC_ALPHA_HARMONIC ? 1u : 0u;
     g->holds_ref = true;
@@ -1023,6 +1105,8 @@ rlc_status rlc_grid_stats_get(const rlc_grid* grid, rlc_grid_stats* stats) {
     stats->cut_size = grid->dev.M;
     stats->lookups = c[rlc::kCntLookups];
     stats->fallback_hits = c[rlc::kCntFallback];
+    stats->pending_lookups = c[rlc::kCntPending];
+    stats->new_keys = c[rlc::kCntNewKeys];
   });
 }
 
@@ -1121,8 +1205,9 @@ rlc_status rlc_framebuffer_create(const rlc_context* ctx, int32_t width, int32_t
     fb->fb.count = fb->arena.alloc<unsigned long long>(npix);
     fb->fb.width = uint32_t(width);
     fb->d_image = fb->arena.alloc<double>(3 * npix);
-    RLC_CK(cudaMemset(fb->fb.sum, 0, 24 * npix));
-    RLC_CK(cudaMemset(fb->fb.count, 0, 8 * npix));
+    RLC_CK(cudaMemsetAsync(fb->fb.sum, 0, 24 * npix, ctx->stream));
+    RLC_CK(cudaMemsetAsync(fb->fb.count, 0, 8 * npix, ctx->stream));
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
     fb->holds_ref = true;
     const_cast<rlc_context*>(ctx)->refs.fetch_add(1);
     *out = fb.release();
@@ -1212,14 +1297,16 @@ rlc_status rlc_pass_trace(const rlc_context* cctx, const rlc_render_config* conf
             "rlc_pass_trace: the sharded pass is the learned sampler's");
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     RLC_CK(cudaSetDevice(ctx->device));
-    const PassSetup S = setup_pass(ctx, config, pass_index, grid, nullptr, false, row_begin,
-                                   row_end);
+    PassSetup S = setup_pass(ctx, config, pass_index, grid, nullptr, false, row_begin, row_end);
+    S.p.defer_insert = 1;  // new keys go in with all ranks' records (rlc_pass_fold)
     ctx->shard = PassParamsHolder{S.p, S.g, S.n, S.nv, grid, true};
     *records = ctx->rec_out;
     *count = 0;
     if (S.nv == 0) return;
     uint32_t *k, *v;
     enqueue_trace(ctx, S, grid, &k, &v);
+    ctx->last_pass = S.p;
+    ctx->last_gbuf = ctx->pb.gbuf;
     rlc::launch_export_records(S.g, ctx->pb, S.nv, ctx->rec_out, ctx->stream);
     unsigned int c = 0;
     RLC_CK(cudaMemcpyAsync(&c, ctx->pb.rec_count, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1257,13 +1344,44 @@ rlc_status rlc_pass_fold(const rlc_context* cctx, const rlc_render_config* confi
     ctx->stage(3, [&] {
       rlc::launch_fold_records(S.g, S.p, ctx->pb,
                                static_cast<const rlc::UpdateRecord*>(all_records), ctx->d_counts,
-                               nranks, stride, uint32_t(total), own_offset, grid->key_bits, ctx->xb,
-                               S.nv, st);
+                               nranks, stride, uint32_t(total), own_offset, counts[rank],
+                               grid->key_bits, ctx->xb, S.nv, st);
     });
     if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
     RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));
     RLC_CK(cudaGetLastError());
     finish_sync(ctx, grid);
+  });
+}
+
+rlc_status rlc_context_enable_sample_export(rlc_context* ctx, int enable) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_enable_sample_export: null context");
+    ctx->export_samples = enable != 0;
+  });
+}
+
+rlc_status rlc_pass_samples(const rlc_context* cctx, uint64_t max_n, rlc_sample_record* out,
+                            uint64_t* n_out) {
+  return guarded([&] {
+    require(cctx != nullptr && n_out != nullptr, "rlc_pass_samples: null argument");
+    static_assert(sizeof(rlc_sample_record) == sizeof(rlc::SampleExport), "record layout");
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    const rlc::PassParams& p = ctx->last_pass;
+    *n_out = p.nv;
+    if (out == nullptr || max_n == 0 || p.nv == 0 || ctx->last_gbuf == nullptr) return;
+    RLC_CK(cudaSetDevice(ctx->device));
+    ctx->sync_all();
+    const uint64_t n = std::min<uint64_t>(max_n, p.nv);
+    DeviceArena tmp;
+    rlc::SampleExport* d = tmp.alloc<rlc::SampleExport>(p.nv);
+    rlc::PassBuffers b = ctx->pb;
+    b.gbuf = ctx->last_gbuf;
+    rlc::launch_export_samples(p, b, d, ctx->stream);
+    RLC_CK(cudaGetLastError());
+    RLC_CK(cudaMemcpyAsync(out, d, n * sizeof(rlc_sample_record), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    RLC_CK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -1314,6 +1432,7 @@ bool same_grid_config(const rlc_render_config& a, const rlc_render_config& b) {
 void reset_grid(rlc_grid* g, cudaStream_t st) {
   const size_t cap = g->dev.capacity;
   RLC_CK(cudaMemsetAsync(g->dev.slot_keys, 0, 16 * cap, st));
+  RLC_CK(cudaMemsetAsync(g->dev.claim, 0xff, 8 * cap, st));
   RLC_CK(cudaMemsetAsync(g->dev.touched, 0, 4 * cap, st));
   RLC_CK(cudaMemsetAsync(g->dev.counters, 0, sizeof(unsigned long long) * rlc::kCntNum, st));
   RLC_CK(cudaMemsetAsync(g->d_changes, 0, 4, st));
@@ -1519,6 +1638,8 @@ void render_frame_impl(rlc_context* ctx, const rlc_render_config* config, const 
   RLC_CK(cudaMemsetAsync(fb->fb.count, 0, 8 * npix, st));
   uint32_t* d_hist = ctx->frame_hist;
   RLC_CK(cudaMemsetAsync(d_hist, 0, 4 * size_t(config->passes), st));
+  // the first pass's primary rays (side stream) insert into the reset table
+  ctx->fence_side();
   // scoring: the reference on the device, per-pixel terms double-buffered to
   // pinned host memory, the ordered sum of pass p - 1 while pass p runs
   DeviceArena tmp;

@@ -484,55 +484,180 @@ __device__ __forceinline__ void cas128(unsigned long long* addr, uint64_t new_lo
       : "memory");
 }
 
-// lookup_or_insert (hash_grid.cpp:113-141): linear probing from hash %
-// capacity, at most min(probe_limit, capacity) slots, CAS-claim of an empty
-// slot; the claimer takes a dense cell id and copies the template cut in.
-// The dense id is published to other paths at the kernel boundary.
-#ifndef RLC_PROBE_LOAD_FIRST
-#define RLC_PROBE_LOAD_FIRST 1
-#endif
-__device__ uint32_t probe_insert(const DevGrid& g, const Key& k, uint64_t h) {
-  uint64_t lo, hi;
-  pack_key(k, lo, hi);
+__device__ __forceinline__ Key unpack_key(uint64_t lo, uint64_t hi) {
+  return Key{int32_t(uint32_t(lo)), int32_t(uint32_t(lo >> 32)), int32_t(uint32_t(hi)),
+             uint32_t(hi >> 32) & 0x3ffffffu, uint32_t(hi >> 58) & 0x1fu};
+}
+
+// lookup_or_insert (hash_grid.cpp:113-141) is split in two so that the table
+// the reference builds -- keys inserted one by one in canonical lookup order
+// -- comes out slot for slot, whatever order the threads run in:
+//  * during a pass every lookup only reads the table as it stood when the
+//    pass began (probe_find); nothing writes it, so plain loads are exact;
+//  * keys not found (kPending) are collected once each with the smallest
+//    canonical id that looked them up (nk_register), inserted after the
+//    lookups in that order (k_insert), and published (k_commit).
+// Linear probing from hash % capacity over min(probe_limit, capacity) slots.
+// kPending: an empty slot ends the probe (the key is new); kFallback: the
+// window is full of other keys (the table only grows, so the reference's
+// lookup exhausts it too, hash_grid.cpp:140).
+// Slot i of the probe sequence of hash h: (h + i) % capacity in uint64
+// arithmetic, as the reference computes it (the sum wraps for h within
+// probe_limit of 2^64).
+__device__ __forceinline__ uint32_t probe_slot(uint64_t h, uint32_t i, uint64_t cap) {
+  return uint32_t((h + i) % cap);
+}
+
+__device__ __forceinline__ uint32_t probe_find(const DevGrid& g, uint64_t lo, uint64_t hi,
+                                               uint64_t h) {
   const uint32_t probes = min(g.probe_limit, g.capacity);
+  const bool wraps = h > ~0ull - probes;
   uint32_t slot = uint32_t(h % uint64_t(g.capacity));
   for (uint32_t i = 0; i < probes; ++i) {
-    uint64_t olo, ohi;
-#if RLC_PROBE_LOAD_FIRST
-    // a claimed slot never changes: a plain L2 read settles every slot but an
-    // empty one (a stale "empty" only costs the CAS below, which is exact)
+    if (wraps) slot = probe_slot(h, i, g.capacity);
     const ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(g.slot_keys + 2 * size_t(slot)));
     if (cur.x == lo && cur.y == hi) return slot;
-    if (cur.x != 0 || cur.y != 0) {
-      slot = slot + 1 == g.capacity ? 0 : slot + 1;
-      continue;
+    if (cur.y == 0) return kPending;  // empty (an occupied word has the valid bit in hi)
+    slot = slot + 1 == g.capacity ? 0 : slot + 1;
+  }
+  return kFallback;
+}
+
+// Files a pending key with canonical id `id` in the pass's new-key table
+// (128-bit CAS claim, smallest id kept).
+__device__ __forceinline__ void nk_register(const NewKeys& nk, uint64_t lo, uint64_t hi, uint64_t h,
+                                            uint32_t id, uint32_t* err) {
+  uint32_t e = uint32_t(h ^ (h >> 31)) & nk.mask;
+  for (uint32_t i = 0; i <= nk.mask; ++i) {
+    uint64_t olo, ohi;
+    cas128(nk.keys + 2 * size_t(e), lo, hi, olo, ohi);
+    if (olo == 0 && ohi == 0) {
+      const uint32_t d = atomicAdd(nk.count, 1u);
+      nk.list[d] = e;
+      atomicMin(nk.id + e, id);
+      return;
     }
-#endif
-    cas128(g.slot_keys + 2 * size_t(slot), lo, hi, olo, ohi);
-    if (olo == 0 && ohi == 0) {  // claimed: new cell
-      const uint32_t cid = uint32_t(atomicAdd(g.counters + kCntCells, 1ull));
+    if (olo == lo && ohi == hi) {
+      atomicMin(nk.id + e, id);
+      return;
+    }
+    e = (e + 1) & nk.mask;
+  }
+  atomicOr(err, kErrNewKeyOverflow);
+}
+
+// k_insert: the pending keys of the pass into the table as if inserted one
+// by one in order of their smallest canonical id.  Ordered linear probing
+// (Amble & Knuth): along its probe window a key passes occupied slots and
+// slots claimed by earlier keys, claims the first other slot with atomicMin
+// on (id << 32 | d), and a later key it displaces carries on from there.  At
+// the fixpoint every key sits on the first slot of its window not held by an
+// earlier key -- exactly the reference's sequential insertion -- or, if its
+// whole window is held by earlier keys, has none (the fallback cut).
+__global__ void __launch_bounds__(128) k_insert(DevGrid g, NewKeys nk) {
+  const uint32_t n = *nk.count;
+  const uint32_t probes = min(g.probe_limit, g.capacity);
+  const uint64_t cap = g.capacity;
+  for (uint32_t d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    uint32_t e = nk.list[d];
+    uint64_t v = (uint64_t(nk.id[e]) << 32) | d;
+    uint64_t h = hash_key(unpack_key(nk.keys[2 * size_t(e)], nk.keys[2 * size_t(e) + 1]));
+    uint32_t i = 0;
+    while (i < probes) {
+      const uint64_t s = probe_slot(h, i, cap);
+      if (__ldcg(g.slot_keys + 2 * s + 1) != 0) {  // a key of an earlier pass
+        ++i;
+        continue;
+      }
+      const uint64_t old = atomicMin(g.claim + s, v);
+      if (old == ~0ull) break;  // the slot was free: placed
+      if (old < v) {            // held by an earlier key
+        ++i;
+        continue;
+      }
+      // displaced a later key: it continues behind this slot
+      v = old;
+      e = nk.list[uint32_t(old)];
+      h = hash_key(unpack_key(nk.keys[2 * size_t(e)], nk.keys[2 * size_t(e) + 1]));
+      uint32_t j = 0;  // its position in its own window (it held slot s)
+      while (j + 1 < probes && probe_slot(h, j, cap) != uint32_t(s)) ++j;
+      i = j + 1u;
+    }
+  }
+}
+
+// k_commit: one warp per new key finds its claimed slot (if any), publishes
+// the key and a fresh cell holding the template cut (hash_grid.cpp:121-127),
+// and clears the new-key entry for the next pass.
+__global__ void __launch_bounds__(256) k_commit(DevGrid g, NewKeys nk) {
+  const uint32_t n = *nk.count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(g.counters + kCntNewKeys, (unsigned long long)n);
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t probes = min(g.probe_limit, g.capacity);
+  const uint64_t cap = g.capacity;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); d < n; d += warps) {
+    const uint32_t e = nk.list[d];
+    const uint64_t lo = nk.keys[2 * size_t(e)], hi = nk.keys[2 * size_t(e) + 1];
+    const uint64_t v = (uint64_t(nk.id[e]) << 32) | d;
+    const uint64_t h = hash_key(unpack_key(lo, hi));
+    uint32_t slot = kFallback;
+    for (uint32_t i0 = 0; i0 < probes && slot == kFallback; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      bool mine = false;
+      uint64_t s = 0;
+      if (i < probes) {
+        s = probe_slot(h, i, cap);
+        // slots of earlier passes keep stale-free claims (cleared below), but
+        // the key check first keeps a numerically equal old claim out
+        mine = __ldcg(g.slot_keys + 2 * s + 1) == 0 && __ldcg(g.claim + s) == v;
+      }
+      const unsigned m = __ballot_sync(kFull, mine);
+      if (m) slot = probe_slot(h, i0 + uint32_t(__ffs(m) - 1), cap);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      nk.keys[2 * size_t(e)] = 0;
+      nk.keys[2 * size_t(e) + 1] = 0;
+      nk.id[e] = 0xffffffffu;
+    }
+    if (slot == kFallback) continue;
+    uint32_t cid = 0;
+    if (lane == 0) {
+      cid = uint32_t(atomicAdd(g.counters + kCntCells, 1ull));
+      g.claim[slot] = ~0ull;
+      g.slot_keys[2 * size_t(slot)] = lo;
+      g.slot_keys[2 * size_t(slot) + 1] = hi;
       g.slot_cell[slot] = cid;
+      const Key k = unpack_key(lo, hi);
       uint32_t* ck = g.cell_key + size_t(5) * cid;
       ck[0] = uint32_t(k.qx);
       ck[1] = uint32_t(k.qy);
       ck[2] = uint32_t(k.qz);
       ck[3] = k.qn;
       ck[4] = k.level;
-      const size_t row = size_t(cid) * g.M;
-      for (uint32_t j = 0; j < g.M; ++j) {
-        g.node_ids[row + j] = g.t_node[j];
-        g.ends[row + j] = g.t_ends[j];
-        g.q[row + j] = g.t_q[j];
-        g.cdf[row + j] = g.t_cdf[j];
-        g.visits[row + j] = g.t_visits[j];
-      }
       g.touched[cid] = 0;
-      return slot;
     }
-    if (olo == lo && ohi == hi) return slot;
-    slot = slot + 1 == g.capacity ? 0 : slot + 1;
+    cid = __shfl_sync(kFull, cid, 0);
+    const size_t row = size_t(cid) * g.M;
+    for (uint32_t j = lane; j < g.M; j += 32) {
+      g.node_ids[row + j] = g.t_node[j];
+      g.ends[row + j] = g.t_ends[j];
+      g.q[row + j] = g.t_q[j];
+      g.cdf[row + j] = g.t_cdf[j];
+      g.visits[row + j] = g.t_visits[j];
+    }
   }
-  return kFallback;
+}
+
+void launch_insert_new_keys(const DevGrid& g, const NewKeys& nk, cudaStream_t st) {
+  static const uint32_t blocks = [] {
+    const char* e = std::getenv("RLC_INSERT_BLOCKS");
+    return e ? uint32_t(std::max(1, std::atoi(e))) : 2u * 148u;
+  }();
+  k_insert<<<blocks, 128, 0, st>>>(g, nk);
+  k_commit<<<blocks, 256, 0, st>>>(g, nk);
+  count_launch(2);
 }
 
 // ---------------------------------------------------------------------------
@@ -616,24 +741,46 @@ __device__ __forceinline__ void shade_vertex(const DevScene& sc, const DevGrid& 
   out.flags = flags;
 }
 
-// Warp-cooperative lookup_or_insert: one probe per distinct hash in the
-// warp (all 32 lanes must call).
-__device__ __forceinline__ void warp_lookup(const DevGrid& g, bool need, const Key& key,
-                                            uint64_t h, uint32_t lane, uint32_t* slot_out) {
+// Warp-cooperative lookup (hash_grid.cpp:113-141 up to the insertion): one
+// probe per distinct hash in the warp (all 32 lanes must call).  A key the
+// table lacks is filed once with the smallest vertex id of the lanes that
+// hold it; the vertex keeps its packed key for the resolution after k_commit.
+__device__ __forceinline__ void warp_lookup(const DevGrid& g, const NewKeys& nk,
+                                            unsigned long long* __restrict__ pkey, bool need,
+                                            const Key& key, uint64_t h, uint32_t vid,
+                                            uint32_t lane, uint32_t* slot_out, uint32_t* err,
+                                            bool file_new) {
   const unsigned need_mask = __ballot_sync(kFull, need);
   if (!need) return;
+  uint64_t lo, hi;
+  pack_key(key, lo, hi);
   const unsigned peers = __match_any_sync(need_mask, h) & need_mask;
   const int leader = __ffs(peers) - 1;
   uint32_t slot = 0;
-  if (int(lane) == leader) slot = probe_insert(g, key, h);
+  if (int(lane) == leader) slot = probe_find(g, lo, hi, h);
   slot = __shfl_sync(peers, slot, leader);
-  const int lqx = __shfl_sync(peers, key.qx, leader);
-  const int lqy = __shfl_sync(peers, key.qy, leader);
-  const int lqz = __shfl_sync(peers, key.qz, leader);
-  const uint32_t lqn = __shfl_sync(peers, key.qn, leader);
-  const uint32_t llv = __shfl_sync(peers, key.level, leader);
-  if (lqx != key.qx || lqy != key.qy || lqz != key.qz || lqn != key.qn || llv != key.level)
-    slot = probe_insert(g, key, h);  // 64-bit hash collision inside the warp
+  const uint64_t llo = __shfl_sync(peers, lo, leader);
+  const uint64_t lhi = __shfl_sync(peers, hi, leader);
+  const bool same = llo == lo && lhi == hi;
+  const unsigned same_mask = __ballot_sync(peers, same);
+  if (same) {
+    if (slot == kPending && file_new) {
+      const uint32_t first = __reduce_min_sync(same_mask, vid);
+      if (int(lane) == leader) nk_register(nk, lo, hi, h, first, err);
+    }
+  } else {  // 64-bit hash collision inside the warp
+    slot = probe_find(g, lo, hi, h);
+    if (slot == kPending && file_new) nk_register(nk, lo, hi, h, vid, err);
+  }
+  if (slot == kPending) {
+    pkey[2 * size_t(vid)] = lo;
+    pkey[2 * size_t(vid) + 1] = hi;
+  }
+  if (file_new) {
+    const unsigned pm = __ballot_sync(need_mask, slot == kPending);
+    if (pm && int(lane) == __ffs(pm) - 1)
+      atomicAdd(g.counters + kCntPending, (unsigned long long)__popc(pm));
+  }
   *slot_out = slot;
   const unsigned fb = __ballot_sync(need_mask, slot == kFallback);
   if (int(lane) == __ffs(need_mask) - 1) {
@@ -646,7 +793,8 @@ __device__ __forceinline__ void warp_lookup(const DevGrid& g, bool need, const K
 #define RLC_PRIMARY_BLOCKS 8  // blocks per SM (64 registers): measured best on c3
 #endif
 __global__ void __launch_bounds__(128, RLC_PRIMARY_BLOCKS) k_primary(DevScene sc, DevGrid g, PassParams P,
-                                                 GBuf* __restrict__ gbuf) {
+                                                 GBuf* __restrict__ gbuf, NewKeys nk,
+                                                 unsigned long long* __restrict__ pkey) {
   const uint32_t rows = P.n / (P.width * P.spp_pp);
   uint32_t idx, px, py, s;
   const bool active = path_of_thread(P, rows, &idx, &px, &py, &s);
@@ -685,7 +833,8 @@ __global__ void __launch_bounds__(128, RLC_PRIMARY_BLOCKS) k_primary(DevScene sc
   const bool got = active && (sc.fp32_ok ? intersect_camera(sc, org, dir, &t, &tri, err)
                                          : intersect(sc, org, dir, 0.0, &t, &tri, err));
   if (got) shade_vertex(sc, g, P, 1u, org, dir, t, tri, sc.cam.pdf_omega, out, need, key, h, err);
-  warp_lookup(g, need, key, h, lane, &out.slot);
+  warp_lookup(g, nk, pkey, need, key, h, idx * P.depth, lane, &out.slot, err,
+              !P.defer_insert);
   if (active) gbuf[size_t(idx) * P.depth] = out;
 }
 
@@ -716,7 +865,8 @@ __device__ __forceinline__ V3 cosine_hemisphere(const DevScene& sc, V3 n, double
 #define RLC_BOUNCE_BLOCKS 6  // blocks per SM (80 registers): c3 depth 3 5.07 -> 4.75 ms per frame
 #endif
 __global__ void __launch_bounds__(128, RLC_BOUNCE_BLOCKS) k_bounce(DevScene sc, DevGrid g, PassParams P,
-                                                uint32_t depth, GBuf* __restrict__ gbuf) {
+                                                uint32_t depth, GBuf* __restrict__ gbuf,
+                                                NewKeys nk, unsigned long long* __restrict__ pkey) {
   const uint32_t path = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = path < P.n;
   const uint32_t lane = threadIdx.x & 31u;
@@ -752,7 +902,8 @@ __global__ void __launch_bounds__(128, RLC_BOUNCE_BLOCKS) k_bounce(DevScene sc, 
   uint32_t tri = 0;
   const bool got = go && intersect(sc, org, dir, sc.shadow_eps, &t, &tri, err);
   if (got) shade_vertex(sc, g, P, depth, org, dir, t, tri, pdf_omega, out, need, key, h, err);
-  warp_lookup(g, need, key, h, lane, &out.slot);
+  warp_lookup(g, nk, pkey, need, key, h, path * P.depth + depth - 1u, lane, &out.slot, err,
+              !P.defer_insert);
   if (active) gbuf[size_t(path) * P.depth + depth - 1u] = out;
 }
 
@@ -788,7 +939,9 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
                                                 uint32_t* __restrict__ vals,
                                                 double* __restrict__ q_before,
                                                 ShadowRay* __restrict__ rays,
-                                                unsigned int* __restrict__ ray_count) {
+                                                unsigned int* __restrict__ ray_count,
+                                                const unsigned long long* __restrict__ pkey,
+                                                uint32_t* __restrict__ emit) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // path vertex
   if (idx >= P.nv) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
@@ -811,11 +964,28 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   r.total = 0;
   uint32_t e;
   if (P.sampler == 2u) {
-    const bool fallback = gb.slot == kFallback;
-    const uint32_t cell = fallback ? 0u : g.slot_cell[gb.slot];
-    const size_t row = fallback ? 0 : size_t(cell) * g.M;
-    const double* cdf = fallback ? g.t_cdf : g.cdf + row;
-    const uint32_t* ends = fallback ? g.t_ends : g.ends + row;
+    // A key new this pass (kPending) has been inserted in canonical order
+    // since the lookups (k_insert / k_commit) or refused (fallback); either
+    // way its cut is still the template (a new cell starts as a copy, the
+    // fallback cut never changes), so the selection reads the template.
+    // Sharded traces (defer_insert) leave the insertion to the fold of all
+    // ranks' records.
+    uint32_t slot = gb.slot;
+    const bool fresh = slot == kPending;
+    if (fresh && !P.defer_insert) {
+      const uint64_t lo = pkey[2 * size_t(idx)], hi = pkey[2 * size_t(idx) + 1];
+      slot = probe_find(g, lo, hi, hash_key(unpack_key(lo, hi)));
+      if (slot >= kPending) {
+        slot = kFallback;
+        atomicAdd(g.counters + kCntFallback, 1ull);
+      }
+    }
+    const bool fallback = slot == kFallback;
+    const bool tmpl = fallback || fresh;
+    const uint32_t cell = tmpl ? 0u : g.slot_cell[slot];
+    const size_t row = tmpl ? 0 : size_t(cell) * g.M;
+    const double* cdf = tmpl ? g.t_cdf : g.cdf + row;
+    const uint32_t* ends = tmpl ? g.t_ends : g.ends + row;
     // sample_cluster (cut.cpp:97-106): upper_bound of u1 * total
     const double total = cdf[g.M - 1];
     const double target = u1 * total;
@@ -827,6 +997,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
     const double frac = span > 0 ? clampd((u1 * total - clo) / span, 0.0, 1.0) : 0.0;
     const uint32_t offset = min(size - 1, uint32_t(frac * double(size)));
     e = sc.order[begin + offset];
+    if (P.export_samples) emit[idx] = e;
     r.pin = 1.0 / double(size);
     r.total = total;
     r.s = s;
@@ -834,12 +1005,16 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
     if (fallback) {
       q_before[idx] = g.t_q[s];  // the fallback cut is never updated
     } else {
-      keys[idx] = cell * g.M + s;
-      r.flags |= kSRecord;  // carries an update_q record (render.cpp:111-117)
+      // carries an update_q record (render.cpp:111-117); a deferred new key
+      // is sorted by the sharded fold
+      if (!fresh) keys[idx] = cell * g.M + s;
+      else if (slot < kPending) keys[idx] = g.slot_cell[slot] * g.M + s;
+      r.flags |= kSRecord;
     }
   } else if (P.sampler == 0u) {
     const uint32_t n = sc.num_lights;
     e = min(n - 1, uint32_t(u1 * double(n)));
+    if (P.export_samples) emit[idx] = e;
     r.pin = 1.0 / double(n);
   } else {
     const uint32_t n = sc.num_lights;
@@ -856,6 +1031,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
       }
     }
     e = lo == n ? n - 1 : lo;
+    if (P.export_samples) emit[idx] = e;
     r.pin = sc.emitter_energy[e] / back;
   }
 
@@ -890,7 +1066,8 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
         r.c[1] = contrib.y;
         r.c[2] = contrib.z;
         r.flags |= kSNonzero;
-        if (P.sampler == 2u) r.v = luminance(contrib) / (r.pin * r.pdf_area);
+        // estimators.cpp:103-104; pdf_in_cluster is 1 for the baselines
+        r.v = luminance(contrib) / ((P.sampler == 2u ? r.pin : 1.0) * r.pdf_area);
         // the shadow segment (pos, point) of occluded(): bvh.cpp:160-167
         const V3 dd = point - pos;
         const double len = length(dd);
@@ -2180,35 +2357,48 @@ __global__ void k_write_records(DevGrid g, const GBuf* __restrict__ gbuf,
                                 const SampleRec* __restrict__ srec,
                                 const uint32_t* __restrict__ rec_path,
                                 const unsigned int* __restrict__ count, uint32_t n,
+                                const unsigned long long* __restrict__ pkey,
                                 UpdateRecord* __restrict__ out) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n || k >= *count) return;
   const uint32_t idx = rec_path[k];
-  const uint32_t* ck = g.cell_key + size_t(5) * g.slot_cell[gbuf[idx].slot];
+  const uint32_t slot = gbuf[idx].slot;
   UpdateRecord r;
-  r.qx = int32_t(ck[0]);
-  r.qy = int32_t(ck[1]);
-  r.qz = int32_t(ck[2]);
-  r.qn = ck[3];
-  r.level = ck[4];
+  if (slot == kPending) {  // new this pass: inserted by the fold of all ranks
+    const Key key = unpack_key(pkey[2 * size_t(idx)], pkey[2 * size_t(idx) + 1]);
+    r.qx = key.qx;
+    r.qy = key.qy;
+    r.qz = key.qz;
+    r.qn = key.qn;
+    r.level = key.level;
+  } else {
+    const uint32_t* ck = g.cell_key + size_t(5) * g.slot_cell[slot];
+    r.qx = int32_t(ck[0]);
+    r.qy = int32_t(ck[1]);
+    r.qz = int32_t(ck[2]);
+    r.qn = ck[3];
+    r.level = ck[4];
+  }
   r.cluster = srec[idx].s;
   r.v = srec[idx].v;
   out[k] = r;
 }
 
 // Gathers all ranks' records (rank-major = canonical order, ranks own
-// contiguous row bands) into one array and inserts their keys.
-__global__ void __launch_bounds__(128) k_insert_records(DevGrid g, const UpdateRecord* __restrict__ all,
+// contiguous row bands) into one array and looks their keys up; keys new
+// this pass are filed with their smallest record index, the canonical order
+// in which the single-GPU reference inserts them.
+__global__ void __launch_bounds__(128) k_gather_records(DevGrid g, const UpdateRecord* __restrict__ all,
                                                         const unsigned long long* __restrict__ counts,
                                                         uint32_t nranks, unsigned long long stride,
-                                                        uint32_t total,
+                                                        uint32_t total, NewKeys nk,
                                                         UpdateRecord* __restrict__ contig,
                                                         uint32_t* __restrict__ slots) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t lane = threadIdx.x & 31u;
   bool need = t < total;
   Key key{};
-  uint64_t h = 0;
+  uint64_t lo = 0, hi = 0, h = 0;
   if (need) {
     unsigned long long off = 0, k = t;
     uint32_t rank = 0;
@@ -2222,35 +2412,61 @@ __global__ void __launch_bounds__(128) k_insert_records(DevGrid g, const UpdateR
     const UpdateRecord r = all[rank * stride + k];
     contig[t] = r;
     key = Key{r.qx, r.qy, r.qz, r.qn, r.level};
+    pack_key(key, lo, hi);
     h = hash_key(key);
   }
   const unsigned need_mask = __ballot_sync(kFull, need);
   if (!need) return;
+  uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
   const unsigned peers = __match_any_sync(need_mask, h) & need_mask;
   const int leader = __ffs(peers) - 1;
   uint32_t slot = 0;
-  if (int(lane) == leader) slot = probe_insert(g, key, h);
+  if (int(lane) == leader) slot = probe_find(g, lo, hi, h);
   slot = __shfl_sync(peers, slot, leader);
-  const int lqx = __shfl_sync(peers, key.qx, leader);
-  const int lqy = __shfl_sync(peers, key.qy, leader);
-  const int lqz = __shfl_sync(peers, key.qz, leader);
-  const uint32_t lqn = __shfl_sync(peers, key.qn, leader);
-  const uint32_t llv = __shfl_sync(peers, key.level, leader);
-  if (lqx != key.qx || lqy != key.qy || lqz != key.qz || lqn != key.qn || llv != key.level)
-    slot = probe_insert(g, key, h);
-  if (slot == kFallback)  // a key another rank could insert does not fit here
-    atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrShardOverflow);
+  const uint64_t llo = __shfl_sync(peers, lo, leader);
+  const uint64_t lhi = __shfl_sync(peers, hi, leader);
+  const bool same = llo == lo && lhi == hi;
+  const unsigned same_mask = __ballot_sync(peers, same);
+  if (same) {
+    if (slot == kPending) {
+      const uint32_t first = __reduce_min_sync(same_mask, t);
+      if (int(lane) == leader) nk_register(nk, lo, hi, h, first, err);
+    }
+  } else {
+    slot = probe_find(g, lo, hi, h);
+    if (slot == kPending) nk_register(nk, lo, hi, h, t, err);
+  }
   slots[t] = slot;
 }
 
+// Sort keys of the gathered records once the new keys are in: a record whose
+// key was refused has no update (the fallback cut, never updated): its
+// q_before is the template's.  Fallback hits of this rank's own records are
+// counted here.
 __global__ void k_record_keys(DevGrid g, const UpdateRecord* __restrict__ contig,
-                              const uint32_t* __restrict__ slots, uint32_t total,
-                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                              uint32_t* __restrict__ slots, uint32_t total,
+                              unsigned long long own_begin, unsigned long long own_end,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                              double* __restrict__ q_rec) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const uint32_t slot = slots[t];
-  keys[t] = slot == kFallback ? kInvalidKey : g.slot_cell[slot] * g.M + contig[t].cluster;
+  uint32_t slot = slots[t];
+  const UpdateRecord r = contig[t];
+  if (slot == kPending) {
+    uint64_t lo, hi;
+    pack_key(Key{r.qx, r.qy, r.qz, r.qn, r.level}, lo, hi);
+    slot = probe_find(g, lo, hi, hash_key(Key{r.qx, r.qy, r.qz, r.qn, r.level}));
+    if (slot == kPending) slot = kFallback;
+    if (slot == kFallback && t >= own_begin && t < own_end)
+      atomicAdd(g.counters + kCntFallback, 1ull);
+  }
   vals[t] = t;
+  if (slot == kFallback) {
+    keys[t] = kInvalidKey;
+    q_rec[t] = g.t_q[r.cluster];
+  } else {
+    keys[t] = g.slot_cell[slot] * g.M + r.cluster;
+  }
 }
 
 __global__ void k_scatter_qbefore(const double* __restrict__ q_rec, uint64_t own_offset,
@@ -2266,21 +2482,25 @@ void launch_export_records(const DevGrid& g, const PassBuffers& b, uint32_t n,
                            UpdateRecord* out, cudaStream_t st) {
   launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);
   k_write_records<<<blocks_for(n, 256), 256, 0, st>>>(g, b.gbuf, b.srec, b.rec_path, b.rec_count,
-                                                      n, out);
+                                                      n, b.pkey, out);
   count_launch();
 }
 
 void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const PassBuffers& b,
                          const UpdateRecord* all, const unsigned long long* d_counts,
                          uint32_t nranks, unsigned long long stride, uint32_t total,
-                         unsigned long long own_offset, uint32_t key_bits, ExchangeBuffers& x,
-                         uint32_t local_n, cudaStream_t st) {
+                         unsigned long long own_offset, unsigned long long local_records,
+                         uint32_t key_bits, ExchangeBuffers& x, uint32_t local_n, cudaStream_t st) {
   if (total > 0) {
-    k_insert_records<<<blocks_for(total, 128), 128, 0, st>>>(g, all, d_counts, nranks, stride,
-                                                             total, x.contig, x.slots);
-    k_record_keys<<<blocks_for(total, 256), 256, 0, st>>>(g, x.contig, x.slots, total, x.keys,
-                                                          x.vals);
-    count_launch(2);
+    cudaMemsetAsync(x.nk.count, 0, sizeof(unsigned int), st);
+    k_gather_records<<<blocks_for(total, 128), 128, 0, st>>>(g, all, d_counts, nranks, stride,
+                                                             total, x.nk, x.contig, x.slots);
+    count_launch();
+    launch_insert_new_keys(g, x.nk, st);
+    k_record_keys<<<blocks_for(total, 256), 256, 0, st>>>(g, x.contig, x.slots, total, own_offset,
+                                                          own_offset + local_records, x.keys,
+                                                          x.vals, x.q_rec);
+    count_launch();
     uint32_t *k = nullptr, *v = nullptr;
     launch_sort_buffers(x.keys, x.vals, x.keys_alt, x.vals_alt, x.hist, total, key_bits, st, &k, &v);
     PassParams p = fold_params;
@@ -2320,6 +2540,44 @@ void launch_add_u32(uint32_t* p, uint32_t v, cudaStream_t st) {
   count_launch();
 }
 
+// rlc_pass_samples: one record per path vertex; radiance as k_accumulate
+// forms it (estimators.cpp:100-101 with the live q_before, cut.cpp:105).
+__global__ void k_export_samples(PassParams P, const GBuf* __restrict__ gbuf,
+                                 const SampleRec* __restrict__ srec,
+                                 const double* __restrict__ q_before,
+                                 const uint32_t* __restrict__ emit, SampleExport* __restrict__ out) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= P.nv) return;
+  SampleExport e{};
+  e.vertex = idx;
+  if (gbuf[idx].flags & kGReflective) {
+    const SampleRec r = srec[idx];
+    const bool learned = r.flags & kSLearned;
+    e.flags = 1u | (learned && !(r.flags & kSRecord) ? 2u : 0u) | (r.flags & kSRay ? 4u : 0u) |
+              (r.flags & kSNonzero ? 8u : 0u) | (learned ? 16u : 0u);
+    e.cluster = learned ? r.s : 0u;
+    e.emitter = P.export_samples ? emit[idx] : 0xffffffffu;
+    e.v = r.v;
+    e.total = r.total;
+    if (learned) e.q_before = q_before[idx];
+    if (r.flags & kSNonzero) {
+      const double pdf_sel = learned ? (e.q_before / r.total) * r.pin : r.pin;
+      const double den = pdf_sel * r.pdf_area;
+      e.radiance[0] = r.c[0] / den;
+      e.radiance[1] = r.c[1] / den;
+      e.radiance[2] = r.c[2] / den;
+    }
+  }
+  out[idx] = e;
+}
+
+void launch_export_samples(const PassParams& p, const PassBuffers& b, SampleExport* out,
+                           cudaStream_t st) {
+  if (p.nv == 0) return;
+  k_export_samples<<<blocks_for(p.nv, 256), 256, 0, st>>>(p, b.gbuf, b.srec, b.q_before, b.emit, out);
+  count_launch();
+}
+
 __global__ void k_resolve(Framebuf fb, uint32_t npix, double* __restrict__ image) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npix) return;
@@ -2339,14 +2597,14 @@ void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
     const uint32_t warps = ((p.width + 7u) / 8u) * ((rows + 3u) / 4u);
     blocks = (warps + 3u) / 4u;
   }
-  k_primary<<<blocks, 128, 0, st>>>(sc, g, p, b.gbuf);
+  k_primary<<<blocks, 128, 0, st>>>(sc, g, p, b.gbuf, b.nk, b.pkey);
   count_launch();
 }
 
 void launch_bounce(const DevScene& sc, const DevGrid& g, const PassParams& p, uint32_t depth,
                    const PassBuffers& b, cudaStream_t st) {
   if (p.n == 0) return;
-  k_bounce<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, depth, b.gbuf);
+  k_bounce<<<blocks_for(p.n, 128), 128, 0, st>>>(sc, g, p, depth, b.gbuf, b.nk, b.pkey);
   count_launch();
 }
 
@@ -2355,7 +2613,8 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
   if (p.nv == 0) return;
   cudaMemsetAsync(b.ray_count, 0, 2 * sizeof(unsigned int), st);
   k_sample<<<blocks_for(p.nv, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.rflag, b.keys, b.vals,
-                                                  b.q_before, b.rays, b.ray_count);
+                                                  b.q_before, b.rays, b.ray_count, b.pkey,
+                                                  b.emit);
   count_launch();
 }
 

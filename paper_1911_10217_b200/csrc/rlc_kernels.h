@@ -10,6 +10,10 @@ namespace rlc {
 
 constexpr uint32_t kNoSlot = 0xffffffffu;    // path without an RL lookup
 constexpr uint32_t kFallback = 0xfffffffeu;  // probe exhaustion -> fallback cut
+// a key not in the table when the pass started, inserted (or refused) in
+// canonical order after the lookups (k_insert / k_commit); its cut is the
+// template until then
+constexpr uint32_t kPending = 0xfffffffdu;
 constexpr uint32_t kInvalidKey = 0xffffffffu;
 
 // G-buffer flags (per path)
@@ -30,12 +34,12 @@ enum : uint32_t {
   kErrDegenerateLight = 4u,   // sample_triangle_point, scene.cpp:50-51
   kErrBadAreaPdf = 8u,        // level_for_footprint, hash_grid.cpp:35-37
   kErrStackOverflow = 16u,    // BVH deeper than the traversal stack
-  kErrShardOverflow = 32u,    // sharded fold: a foreign key overflowed the hash table
+  kErrNewKeyOverflow = 32u,   // more distinct new keys in one pass than the dedup table holds
 };
 
 // Counters block (u64 each).
 enum : uint32_t { kCntCells = 0, kCntLookups = 1, kCntFallback = 2, kCntChanges = 3,
-                  kCntErr = 4, kCntNum = 8 };
+                  kCntErr = 4, kCntPending = 5, kCntNewKeys = 6, kCntNum = 8 };
 
 struct alignas(16) GBuf {  // 64 B per path vertex
   double pos[3];
@@ -129,6 +133,9 @@ struct DevGrid {
   const uint32_t* t_visits;
   double eps_q;
   unsigned long long* counters;   // kCnt*
+  // insertion claims [capacity]: (canonical id << 32 | new-key index) of the
+  // pending key holding an empty slot during k_insert; ~0 = none
+  unsigned long long* claim;
   unsigned char* split_scratch;   // k_split rows in global memory for cuts too large
                                   // for shared memory (kSplitGlobalWarps * 32 M bytes)
 };
@@ -147,10 +154,27 @@ struct PassParams {
   double alpha;
   uint32_t harmonic;
   const uint32_t* pass_dev;  // non-null (CUDA-graph replays): the pass index is read here
+  uint32_t defer_insert;     // sharded trace: new keys are inserted by the fold of all ranks
+  uint32_t export_samples;   // k_sample files each vertex's emitter index (rlc_pass_samples)
+};
+
+// The distinct keys missing from the table in one pass, each with the
+// smallest canonical id that looked it up (the reference's insertion order,
+// hash_grid.cpp:113-141): an open-addressing table of 2^k entries, cleared
+// entry by entry by k_commit after use.
+struct NewKeys {
+  unsigned long long* keys;  // [cap][2] packed CellKey, 0 = empty
+  uint32_t* id;              // [cap] smallest canonical id, ~0 = empty
+  uint32_t* list;            // [cap] entry index of the d-th distinct key
+  unsigned int* count;       // distinct keys this pass
+  uint32_t mask;             // cap - 1
 };
 
 struct PassBuffers {
   GBuf* gbuf;
+  unsigned long long* pkey;  // [vertex][2] packed key of a kPending lookup (per G-buffer slot)
+  NewKeys nk;
+  uint32_t* emit;            // [vertex] emitter index (P.export_samples)
   SampleRec* srec;
   uint8_t* rflag;        // per vertex: the kSRay | kSRecord bits of srec (compaction input)
   uint32_t* keys;
@@ -178,7 +202,15 @@ struct ExchangeBuffers {
   uint32_t* vals_alt;
   uint32_t* hist;
   double* q_rec;
+  NewKeys nk;
   uint32_t cap;
+};
+
+// == rlc_sample_record (include/rlcuts_b200.h)
+struct alignas(8) SampleExport {
+  uint32_t vertex, cluster, emitter, flags;
+  double q_before, v, total;
+  double radiance[3];
 };
 
 struct Framebuf {
@@ -206,6 +238,9 @@ void launch_bounce(const DevScene& sc, const DevGrid& g, const PassParams& p, ui
                    const PassBuffers& b, cudaStream_t st);
 void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
                    const PassBuffers& b, cudaStream_t st);
+// The pass's new keys into the table in canonical order (k_insert), then
+// published with fresh cells holding the template cut (k_commit).
+void launch_insert_new_keys(const DevGrid& g, const NewKeys& nk, cudaStream_t st);
 // Sorts (keys, vals) by key; returns which buffer pair holds the result.
 // Stable compaction of the paths that carry a shadow ray, in the order of
 // `order` (sorted update records) or canonical order when it is null.
@@ -223,8 +258,8 @@ void launch_export_records(const DevGrid& g, const PassBuffers& b, uint32_t n,
 void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const PassBuffers& b,
                          const UpdateRecord* all, const unsigned long long* d_counts,
                          uint32_t nranks, unsigned long long stride, uint32_t total,
-                         unsigned long long own_offset, uint32_t key_bits, ExchangeBuffers& x,
-                         uint32_t local_n, cudaStream_t st);
+                         unsigned long long own_offset, unsigned long long local_records,
+                         uint32_t key_bits, ExchangeBuffers& x, uint32_t local_n, cudaStream_t st);
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
                  const uint32_t* vals, const PassBuffers& b, cudaStream_t st);
 void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffers& b,
@@ -242,6 +277,9 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
                             double tmin, double* t_out, int32_t* tri_out,
                             unsigned long long* counters, cudaStream_t st, bool sah_only = false);
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
+// Per-vertex parity records of the pass in `p` (rlc_pass_samples).
+void launch_export_samples(const PassParams& p, const PassBuffers& b, SampleExport* out,
+                           cudaStream_t st);
 // Per-pixel squared error of the resolved framebuffer against `ref`
 // (mse's summand, image.cpp:119-121), for the ordered host sum.
 void launch_pixel_err(const Framebuf& fb, uint32_t npix, const double* ref, double* err,

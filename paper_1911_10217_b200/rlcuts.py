@@ -143,7 +143,8 @@ class RenderContext:
     def set_stream(self, stream_ptr: int | None):
         _check(_lib.load().rlc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
-    STAGES = ("primary", "sample", "sort", "fold", "accumulate", "split_collapse", "shadow")
+    STAGES = ("primary", "sample", "sort", "fold", "accumulate", "split_collapse", "shadow",
+              "insert")
 
     def enable_timing(self, on: bool = True):
         _check(_lib.load().rlc_context_enable_timing(self.handle, 1 if on else 0))
@@ -220,6 +221,13 @@ class HashGrid:
         _check(_lib.load().rlc_grid_stats_get(self.handle, C.byref(s)))
         return {"occupied": s.occupied, "cut_size": s.cut_size, "lookups": s.lookups,
                 "fallback_hits": s.fallback_hits}
+
+    def insertion_stats(self) -> dict:
+        """Lookups that missed the table at the start of their pass, and the
+        distinct keys among them (inserted in canonical order or refused)."""
+        s = _lib.GridStatsC()
+        _check(_lib.load().rlc_grid_stats_get(self.handle, C.byref(s)))
+        return {"pending_lookups": s.pending_lookups, "new_keys": s.new_keys}
 
     def occupied_count(self) -> int:
         return self.stats()["occupied"]
@@ -408,6 +416,39 @@ def end_of_pass_update(grid: HashGrid, ctx: RenderContext, config: CutConfig,
 
 RECORD_DTYPE = np.dtype([("qx", "<i4"), ("qy", "<i4"), ("qz", "<i4"), ("qn", "<u4"),
                          ("level", "<u4"), ("cluster", "<u4"), ("v", "<f8")])  # rlc_update_record
+
+
+SAMPLE_DTYPE = np.dtype([("vertex", "<u4"), ("cluster", "<u4"), ("emitter", "<u4"),
+                         ("flags", "<u4"), ("q_before", "<f8"), ("v", "<f8"), ("total", "<f8"),
+                         ("radiance", "<f8", (3,))])  # rlc_sample_record
+SAMPLE_VALID, SAMPLE_FALLBACK, SAMPLE_RAY, SAMPLE_NONZERO, SAMPLE_LEARNED = 1, 2, 4, 8, 16
+
+
+def enable_sample_export(ctx: RenderContext, enable: bool = True) -> None:
+    """File the selected emitter index of every light sample from now on
+    (rlc_context_enable_sample_export; needed by pass_samples)."""
+    _check(_lib.load().rlc_context_enable_sample_export(ctx.handle, int(bool(enable))))
+
+
+def pass_samples(ctx: RenderContext, config: RenderConfig, row_begin: int = 0) -> dict:
+    """The light samples of the context's last pass in canonical order
+    (pixel, sample, depth) -- sample_light's selection (cluster, emitter),
+    the live q_before of its pdf, v, the frozen total and the radiance
+    (rlc_pass_samples), in the layout of the oracle's OracleRun.samples()."""
+    lib = _lib.load()
+    n = C.c_uint64()
+    _check(lib.rlc_pass_samples(ctx.handle, 0, None, C.byref(n)))
+    rec = np.zeros(n.value, SAMPLE_DTYPE)
+    if n.value:
+        _check(lib.rlc_pass_samples(ctx.handle, n.value, rec.ctypes.data_as(C.c_void_p),
+                                    C.byref(n)))
+    rec = rec[(rec["flags"] & SAMPLE_VALID) != 0]
+    per_pixel = (config.spp // config.passes) * max(config.max_depth, 1)
+    pixel = (rec["vertex"] // per_pixel + row_begin * ctx.scene.camera.width).astype(np.uint32)
+    return {"pixel": pixel, "cluster": rec["cluster"], "emitter": rec["emitter"],
+            "fallback": (rec["flags"] & SAMPLE_FALLBACK) != 0, "q_before": rec["q_before"],
+            "v": rec["v"], "radiance": rec["radiance"], "total": rec["total"],
+            "ray": (rec["flags"] & SAMPLE_RAY) != 0, "nonzero": (rec["flags"] & SAMPLE_NONZERO) != 0}
 
 
 def pass_trace(ctx: RenderContext, config: RenderConfig, pass_index: int, grid: HashGrid,

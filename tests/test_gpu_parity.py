@@ -310,8 +310,9 @@ def test_full_resolution_c3_properties():
 def test_hash_grid_host_views_match_reference(ref):
     """HashGrid's host accessors (hash_grid.hpp:87-110) served from the device
     grid: dump_stats text, memory_records, the touched slots between
-    render_pass and end_of_pass_update (compared by CellKey: slot positions
-    depend on insertion order under probing), key_of, fallback_cut."""
+    render_pass and end_of_pass_update, key_of, fallback_cut.  New keys go in
+    in the reference's canonical insertion order, so slot positions are the
+    reference's too."""
     scene = scenes.cornell_grid(2, 1, dome_triangles=64, width=48, height=36)
     cfg = rlcuts.RenderConfig(spp=3, passes=3, sampler=RL,
                               cut=rlcuts.CutConfig(cut_size=32))
@@ -328,9 +329,43 @@ def test_hash_grid_host_views_match_reference(ref):
     assert grid.dump_stats() == text
     assert grid.memory_records() == mem
     got = [grid.key_of(s) for s in grid.touched_slots()]
-    assert sorted(got) == sorted(touched) and len(got) > 50
+    assert got == touched and len(got) > 50
+    assert [(s, k) for s, _, k, _ in grid.slots()] == rr.slots()
     assert grid.key_of(2**31) is None
     tmpl = grid.fallback_cut()
     assert tmpl["q"].shape == (32,) and tmpl["visits"].min() == 1
     rlcuts.end_of_pass_update(grid, ctx, cfg.cut)
     assert grid.touched_slots() == []
+
+
+@pytest.mark.parametrize("capacity,probe_limit,jitter", [(256, 32, 0.0), (700, 4, 1.0), (97, 97, 0.0)])
+def test_hash_grid_overflow_matches_reference(ref, capacity, probe_limit, jitter):
+    """A table far too small for the scene's cells: which keys are refused
+    (the fallback cut: sampled from, never updated) depends on the order keys
+    are inserted in (hash_grid.cpp:113-141).  The GPU inserts each pass's new
+    keys in canonical lookup order, so fallback hits, the slot layout, the
+    learned cuts and the image all equal the reference's."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=64, height=48)
+    cfg = rlcuts.RenderConfig(spp=4, passes=4, sampler=RL,
+                              hash=rlcuts.HashConfig(capacity=capacity, probe_limit=probe_limit,
+                                                     jitter_scale=jitter),
+                              cut=rlcuts.CutConfig(cut_size=32))
+    ctx, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+    st = grid.stats()
+    assert st["fallback_hits"] > 1000 and st["occupied"] >= 0.9 * capacity
+    assert [(s, k) for s, _, k, _ in grid.slots()] == rr.slots()
+
+
+@pytest.mark.parametrize("depth", [2, 3])
+def test_hash_grid_overflow_multi_bounce(ref, depth):
+    """Overflow with several vertices per path: the canonical insertion order
+    is (pixel, sample, depth), across the bounce launches."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=40)
+    cfg = rlcuts.RenderConfig(spp=2, passes=2, sampler=RL, max_depth=depth,
+                              hash=rlcuts.HashConfig(capacity=300, probe_limit=8),
+                              cut=rlcuts.CutConfig(cut_size=16))
+    _, grid, fb, rr = run_both(ref, scene, cfg)
+    assert_same_state(grid, fb, rr)
+    assert grid.fallback_hits() > 100
+    assert [(s, k) for s, _, k, _ in grid.slots()] == rr.slots()

@@ -43,3 +43,40 @@ def test_sharded_gpu_matches_single(ref, world, depth):
                 assert np.array_equal(cells[k][f], v[f])
         lookups += e.grid.lookup_count()
     assert lookups == rr.stats()["lookups"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_overflow_matches_reference(ref, world):
+    """A hash table too small for the scene: every rank inserts the new keys
+    of all ranks' records in canonical order, so the refused keys, the slot
+    layout and the learned state equal the single-GPU reference's."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+                              hash=rlcuts.HashConfig(capacity=200, probe_limit=16),
+                              cut=rlcuts.CutConfig(cut_size=32, split_threshold=2.0))
+    dev = torch.device("cuda", 0)
+    engines = []
+    for r in range(world):
+        ctx = rlcuts.build_context(scene, cfg)
+        engines.append(rdist.GpuEngine(ctx, rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx),
+                                       cfg, dev))
+    rows = [rdist.band(scene.camera.height, r, world) for r in range(world)]
+    rr = ref.RefRun(scene, cfg)
+    for p in range(cfg.passes):
+        changes = rdist.local_exchange(engines, rows, p)
+        rch, _ = rr.run_pass(p)
+        assert changes == [rch] * world
+    rs, rc = rr.framebuffer()
+    rcells = rr.export()
+    fallback = 0
+    for e, (r0, r1) in zip(engines, rows):
+        s, c = e.fb.download()
+        assert np.array_equal(s[r0:r1], rs[r0:r1]) and np.array_equal(c[r0:r1], rc[r0:r1])
+        cells = e.grid.export()
+        assert cells.keys() == rcells.keys()
+        for k, v in rcells.items():
+            for f in v:
+                assert np.array_equal(cells[k][f], v[f])
+        assert [(s_, k) for s_, _, k, _ in e.grid.slots()] == rr.slots()
+        fallback += e.grid.fallback_hits()
+    assert fallback == rr.stats()["fallback_hits"] > 100
