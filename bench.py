@@ -125,23 +125,7 @@ class ClockSampler:
 # roofline bookkeeping
 # ---------------------------------------------------------------------------
 NODE_B, TRI_B = 64, 72  # reference BVH node / Moller-Trumbore triangle bytes
-
-
-def algorithmic_bytes(trav: dict) -> dict:
-    """Bytes each kernel must move per unit of work (DESIGN.md "Algorithmic
-    bytes"), with the traversal counts of the reference BVH and traversal
-    order (profiles/traversal_stats.json, measured by the oracle)."""
-    sh = trav["shadow_rays_per_sample"]
-    return {
-        # per path: G-buffer write 64 + hash probe 24 + closest-hit traversal
-        "primary": ("path", 64 + 24 + NODE_B * trav["primary_nodes"] + TRI_B * trav["primary_tris"]),
-        # per light sample: G-buffer read 64, cdf search 8x8, cluster record 24,
-        # order + triangle id 8, triangle + emission 96, sample record 64,
-        # update record 8, shadow-ray record 64 per traced ray
-        "sample": ("light sample", 64 + 64 + 24 + 8 + 96 + 64 + 8 + 64 * sh),
-        # per traced shadow ray: ray record 64 + any-hit traversal + result 12
-        "shadow": ("shadow ray", 64 + NODE_B * trav["shadow_nodes"] + TRI_B * trav["shadow_tris"] + 12),
-    }
+RAY_B, WIDE_NODE_B, TRIACCEL_B = 64, 64, 80  # ShadowRay, quantized 4-wide node, TriAccel
 
 
 def traversal_stats(name: str) -> dict | None:
@@ -186,26 +170,36 @@ def ncu_traffic(config: str, kernel: str) -> float | None:
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref: the unmodified reference library)
 # ---------------------------------------------------------------------------
-def cpu_reference_run(scene, cfg, passes: int, warmup: int, min_seconds: float,
-                      downscale: int, dynamic: bool = False):
-    """Times the reference render_pass + end_of_pass_update (workers = all
-    host cores) on the same scene at 1/downscale^2 of the pixels; for the
-    dynamic workloads also the per-frame context rebuild (build_context with
-    the frozen light tree, the semantics of rlc_context_update_scene)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference_run(scene, cfg, workers: int, min_frames: int, min_seconds: float,
+                      max_seconds: float = 1e9, warmup: int = 1, dynamic: bool = False):
+    """Times the stock reference render_pass + end_of_pass_update
+    (render.cpp:159-200, the loop body of render_frame) on the SAME scene,
+    raster and per-frame schedule as our arm, `workers` host threads
+    (render.cpp:23-38); frames until both min_frames and min_seconds are
+    met (or max_seconds passed).  Dynamic workloads add the per-frame
+    context rebuild (build_context with the frozen light tree, the semantics
+    of rlc_context_update_scene)."""
     import oracle
     from paper_1911_10217_b200 import rlcuts, scenes
-    cores = os.cpu_count() or 1
-    cam = scene.camera
-    small = scene.with_resolution(max(cam.width // downscale, 1), max(cam.height // downscale, 1))
     rcfg = rlcuts.RenderConfig(spp=cfg.spp, passes=cfg.passes, sampler=cfg.sampler, cut=cfg.cut,
-                               hash=cfg.hash, seed=cfg.seed, workers=cores,
+                               hash=cfg.hash, seed=cfg.seed, workers=workers,
                                max_depth=cfg.max_depth)
-    run = oracle.RefRun(small, rcfg)
+    run = oracle.RefRun(scene, rcfg)
 
     def update(p):
         if not dynamic or p == 0:
             return 0.0
-        s = scenes.displace_emitters(small, p)
+        s = scenes.displace_emitters(scene, p)
         t0 = time.perf_counter()
         run.update_scene(s)
         return (time.perf_counter() - t0) * 1e3
@@ -214,43 +208,47 @@ def cpu_reference_run(scene, cfg, passes: int, warmup: int, min_seconds: float,
         update(p)
         run.run_pass(p)
     l0 = run.stats()["lookups"]
-    total_ms = 0.0
-    done = 0
-    per_step = []
-    for p in range(warmup, warmup + max(passes, 1) + 10000):
-        before = run.stats()["lookups"]
+    total_ms, done = 0.0, 0
+    p = warmup
+    while True:
         ums = update(p)
         _, ms = run.run_pass(p)
-        ms += ums
-        total_ms += ms
-        per_step.append((run.stats()["lookups"] - before, ms))
+        total_ms += ms + ums
         done += 1
-        if done >= passes and total_ms / 1e3 >= min_seconds:
+        p += 1
+        if done >= min_frames and total_ms / 1e3 >= min_seconds:
             break
-        if done >= passes and min_seconds <= 0:
+        if done >= 1 and total_ms / 1e3 >= max_seconds:
             break
     lookups = run.stats()["lookups"] - l0
-    value = lookups / (total_ms / 1e3)
-    sample = (f"{done} frames of the {small.name} scene at {small.camera.width}x"
-              f"{small.camera.height} (1/{downscale * downscale} of the pixels), "
+    cam = scene.camera
+    sample = (f"frames {warmup}..{warmup + done - 1} of the {scene.name} scene at "
+              f"{cam.width}x{cam.height} (the same raster and schedule as our arm), "
               f"{lookups} light samples, reference render_pass + end_of_pass_update, "
-              f"workers={cores}")
-    return value, cores, sample, total_ms / done, per_step
+              f"workers={workers}")
+    return lookups / (total_ms / 1e3), sample, total_ms / done, done
 
 
 def run_reference_arm(args, rank: int, world: int):
+    """The reference's own CPU implementation of the path (oracle/_ref: the
+    unmodified library, compiled in place) on all host cores, on our arm's
+    workload: the same scene, raster and frame schedule.  The timed frames are
+    bounded to about a minute of host time."""
     if rank != 0:
         return
     scene, cfg = make_config(args.config, args.max_depth)
-    value, cores, sample, ms_step, _ = cpu_reference_run(
-        scene, cfg, passes=args.steps, warmup=args.warmup, min_seconds=0.0,
-        downscale=args.cpu_downscale, dynamic=args.config in DYNAMIC)
+    cores = os.cpu_count() or 1
+    value, sample, ms_step, done = cpu_reference_run(
+        scene, cfg, workers=cores, min_frames=args.steps, min_seconds=0.0,
+        max_seconds=args.ref_seconds, warmup=args.warmup, dynamic=args.config in DYNAMIC)
+    if done < args.steps:
+        sample += f" (the first {done} of the {args.steps} requested frames: time bound)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "steps": done, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload(args)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -329,7 +327,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # (render_frame's pass loop; CUDA-graph replays for launch-bound frames),
     # the per-kernel CUDA-event times come from a separate untimed run below
     batch = world == 1 and not dynamic
-    ctx.enable_timing(not batch)
+    ctx.enable_timing(False)
     l0 = grid.lookup_count()
     ins0 = grid.insertion_stats()
     launches0 = rlcuts.kernel_launches()
@@ -352,19 +350,26 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if dist is not None:
         dist.barrier()
     clk = clocks.stop()
+    update_timed_ms = update_ms[0]
     launches = rlcuts.kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
     lookups = grid.lookup_count() - l0
     ins1 = grid.insertion_stats()
     grid_insert_stats = {f"{k}_per_frame": (ins1[k] - ins0[k]) / args.steps for k in ins1}
-    stage_frames = args.steps
-    if batch:  # per-kernel times: a few more frames with CUDA events around every stage
-        stage_frames = min(args.steps, 20)
-        ctx.stage_times()
-        ctx.enable_timing(True)
-        for p in range(args.warmup + args.steps, args.warmup + args.steps + stage_frames):
-            step(p)
-        ctx.synchronize()
+    # per-kernel times and work counts: a few more frames with CUDA events
+    # around every stage and k_shadow counting its work
+    stage_frames = min(args.steps, 20)
+    ctx.stage_times()
+    ctx.enable_timing(True)
+    ctx.count_work(True)
+    l_st = grid.lookup_count()
+    rlcuts.work_counters(reset=True)
+    for p in range(args.warmup + args.steps, args.warmup + args.steps + stage_frames):
+        step(p)
+    ctx.synchronize()
+    work = rlcuts.work_counters(reset=True)
+    stage_lookups = grid.lookup_count() - l_st
+    ctx.count_work(False)
     stages = ctx.stage_times()
     ctx.enable_timing(False)
     if dist is not None:
@@ -378,43 +383,54 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     value = lookups / (ms / 1e3)
     st = grid.stats()
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel (k_shadow): its own work this run --
+    # rays, node steps, triangle tests from the always-on work counters over
+    # the timed frames -- in bytes, over its CUDA-event launch time, against
+    # the measured HBM copy bandwidth and the measured L2 read bandwidth
     peak, peak_src = measured_peaks()
-    trav = traversal_stats(args.config)
+    l2_gbs = rlcuts.measure_l2_bandwidth(local_rank)
+    k_ms, k_n = stages["shadow"]
     roof = None
-    per_kernel = {}
-    if trav is not None:
-        paths = scene.camera.width * (r1 - r0) * (cfg.spp // cfg.passes)
-        samples = (lookups / world if world > 1 else lookups) / args.steps
-        units = {"primary": paths, "sample": samples,
-                 "shadow": samples * trav["shadow_rays_per_sample"]}
-        for k, (uname, per_unit) in algorithmic_bytes(trav).items():
-            k_ms, k_n = stages[k]
-            if k_n == 0:
-                continue
-            b_launch = per_unit * units[k]
-            per_kernel[k] = {"unit_of_work": uname, "bytes_per_unit": per_unit,
-                             "units_per_launch": units[k], "avg_launch_ms": k_ms / k_n,
-                             "achieved_gbs": b_launch / (k_ms / k_n / 1e3) / 1e9}
-        dom = max(per_kernel, key=lambda k: per_kernel[k]["avg_launch_ms"])
-        pk = per_kernel[dom]
-        roof = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": pk["achieved_gbs"],
-                "peak": peak, "unit": "GB/s", "frac": pk["achieved_gbs"] / peak,
-                "peak_source": peak_src, "traffic": ncu_traffic(args.config, dom),
-                "bytes_per_unit": pk["bytes_per_unit"], "unit_of_work": pk["unit_of_work"],
-                "units_per_launch": pk["units_per_launch"], "avg_launch_ms": pk["avg_launch_ms"],
-                "per_kernel": per_kernel,
-                "note": "achieved = algorithmic bytes with the reference BVH's node/triangle "
-                        "counts per ray (SURVEY 8(d)); our trees serve them mostly from L1/L2 "
-                        "or skip them, so frac > 1; dram_achieved = ncu DRAM bytes per launch "
-                        "(traffic) / live launch time (profiles/r01_ncu_summary.md)"}
+    if k_n > 0 and work["shadow_rays"] > 0:
+        t_launch = k_ms / k_n / 1e3
+        rays = work["shadow_rays_queued"] / stage_frames
+        nodes = work["shadow_nodes"] / stage_frames
+        tris = work["shadow_tris"] / stage_frames
+        own = rays * (RAY_B + 4) + nodes * WIDE_NODE_B + tris * TRIACCEL_B
+        achieved = own / t_launch / 1e9
+        tr = ncu_traffic(args.config, "shadow")
+        roof = {"bound": "hbm", "kernel": "k_shadow", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": tr, "unit_of_work": "shadow ray",
+                "bytes_per_unit": own / rays, "units_per_launch": rays,
+                "avg_launch_ms": k_ms / k_n,
+                "own_work": {"node_steps_per_ray": nodes / rays, "tri_tests_per_ray": tris / rays,
+                             "rays_past_root_per_ray": work["shadow_rays"] / stage_frames / rays,
+                             "rays_per_light_sample": rays / (stage_lookups / stage_frames),
+                             "bytes": f"{RAY_B + 4} per ray (record + order) + {WIDE_NODE_B} per "
+                                      f"node step + {TRIACCEL_B} per triangle test",
+                             "source": "rlc_work_counters over the stage-timing frames "
+                                       "(k_shadow's counting instance, the launches timed)"},
+                "l2": {"peak": l2_gbs, "frac": achieved / l2_gbs if l2_gbs else None,
+                       "peak_source": "measured here (rlc_measure_l2_bandwidth: 16-byte .cg "
+                                      "loads over a 48 MB L2-resident buffer)"},
+                "limiter": "latency of dependent node loads (L1/L2-served): ncu issue-active "
+                           "~32%, ~18 of 32 lanes active per instruction "
+                           "(profiles/r01_ncu_summary.md); HBM and L2 fractions are both low"}
+        if tr:
+            roof["dram_achieved"] = tr / t_launch / 1e9
+            roof["dram_frac"] = roof["dram_achieved"] / peak
+        trav = traversal_stats(args.config)
+        if trav is not None:  # the reference BVH's traversal work, per ray
+            ref_b = 64 + NODE_B * trav["shadow_nodes"] + TRI_B * trav["shadow_tris"] + 12
+            roof["reference_equivalent"] = {
+                "bytes_per_ray": ref_b, "gbs": ref_b * rays / t_launch / 1e9,
+                "note": "work-normalised speed: the reference BVH's node and triangle "
+                        "bytes per ray (SURVEY 8(d)) / our launch time; not a roofline "
+                        "fraction (our tree does far less work per ray)"}
         fh = frame_hbm(args.config, value, peak) if args.max_depth == 1 else None
         if fh:
             roof["frame_hbm"] = fh
-        tr = roof["traffic"]
-        if tr:
-            roof["dram_achieved"] = tr / (pk["avg_launch_ms"] / 1e3) / 1e9
-            roof["dram_frac"] = roof["dram_achieved"] / peak
 
     # end to end through the C-ABI render_frame: host image out, grid created
     # inside the call (the reference's render_frame, render.cpp:202-240)
@@ -454,11 +470,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
         try:
-            v, cores, sample, _, _ = cpu_reference_run(
-                scene, cfg, passes=2, warmup=1, min_seconds=args.cpu_seconds,
-                downscale=args.cpu_downscale, dynamic=args.config in DYNAMIC)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
+            v, sample, _, _ = cpu_reference_run(
+                scene, cfg, workers=cores, min_frames=2, min_seconds=args.cpu_seconds,
+                dynamic=dynamic)
+            v1, sample1, _, _ = cpu_reference_run(
+                scene, cfg, workers=1, min_frames=1, min_seconds=0.0, dynamic=dynamic)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": sample, "cpu_model": cpu_model(), "same_config": True,
+                   "workers_1": {"value": v1, "cores": 1, "sample": sample1}}
         except Exception as ex:  # the reference library is test infrastructure
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -478,9 +499,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
             "stage_ms_per_step": {k: v[0] / stage_frames for k, v in stages.items()},
-            "stage_source": ("CUDA events around every stage in %d further frames" % stage_frames
-                             if batch else "CUDA events around every stage in the timed frames"),
-            "scene_update_ms_per_step": update_ms[0] / args.steps if dynamic else None,
+            "stage_source": "CUDA events around every stage in %d further frames" % stage_frames,
+            "scene_update_ms_per_step": update_timed_ms / args.steps if dynamic else None,
             "context_build_s": build_s,
         }
         print(json.dumps(line), flush=True)
@@ -500,7 +520,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--cpu-downscale", type=int, default=4)
+    ap.add_argument("--ref-seconds", type=float, default=60.0,
+                    help="--impl reference: bound on the timed host time")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo stages the record exchange through host memory (functional "
                          "multi-rank runs with fewer GPUs than ranks)")

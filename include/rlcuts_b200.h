@@ -177,11 +177,11 @@ rlc_status rlc_context_synchronize(rlc_context* ctx);
 /* Per-stage device timing with CUDA events on the context stream (bench
  * evidence).  Stages: 0 primary, 1 sample, 2 sort, 3 fold, 4 accumulate,
  * 5 split-collapse, 6 shadow (any-hit traversal), 7 insert (the pass's new
- * hash-grid keys, in canonical order).  Stage 0 includes the
+ * hash-grid keys, in canonical order), 8 ray compaction.  Stage 0 includes the
  * bounce rays of max_depth > 1.  rlc_context_stage_times synchronizes,
  * returns accumulated milliseconds and launch counts per stage since the
  * last call, and resets them. */
-#define RLC_NUM_STAGES 8
+#define RLC_NUM_STAGES 9
 rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable);
 rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts);
 
@@ -201,6 +201,17 @@ rlc_status rlc_intersect_batch(const rlc_context* ctx, uint32_t n, const double*
  * hit, out8[6] shadow rays finished on the exact path after a stack
  * overflow.  reset != 0 clears them after reading. */
 rlc_status rlc_debug_trav_stats(int32_t reset, uint64_t* out8);
+/* Work counters (the bench's own-work roofline bytes), kept while a
+ * context counts (rlc_context_count_work: k_shadow's counting instance,
+ * ~1.5% slower on c3): out4[0..2] = shadow rays traversed by k_shadow's tree, its node steps
+ * (64-byte nodes) and triangle tests (80-byte triangles), out4[3] = shadow
+ * rays queued, summed over the process since the last reset.  reset != 0
+ * clears them. */
+rlc_status rlc_work_counters(int32_t reset, uint64_t* out4);
+rlc_status rlc_context_count_work(rlc_context* ctx, int enable);
+/* Measured L2 read bandwidth of `device` in GB/s (16-byte L2 loads over a
+ * 48 MB L2-resident buffer): the bench's second roofline denominator. */
+rlc_status rlc_measure_l2_bandwidth(int device, double* gbs);
 /* Diagnostic (parity tests): the closest-hit decision of the SAH tree alone
  * (DESIGN.md 5.4): as rlc_intersect_batch, but tri_out = -2 where the SAH
  * traversal defers to the reference-order traversal (exact tie, or the hit's

@@ -98,6 +98,9 @@ SIGNATURES = {
     "rlc_intersect_batch": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.c_double, _dp,
                                       C.POINTER(C.c_int32)]),
     "rlc_debug_trav_stats": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
+    "rlc_work_counters": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
+    "rlc_context_count_work": (C.c_int, [_P, C.c_int]),
+    "rlc_measure_l2_bandwidth": (C.c_int, [C.c_int, _dp]),
     "rlc_render_passes_async": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, C.c_uint32,
                                           _P, _P]),
     "rlc_grid_slots": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),

@@ -606,8 +606,8 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
     });
     RLC_CK(cudaEventRecord(ctx->ev_sort_done, ctx->sstream));
   }
+  ctx->stage(8, [&] { rlc::launch_ray_compact(ctx->pb, nullptr, S.nv, st); });
   ctx->stage(6, [&] {
-    rlc::launch_ray_compact(ctx->pb, nullptr, S.nv, st);
     rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, S.g.counters, st, rl);
   });
   if (rl) RLC_CK(cudaStreamWaitEvent(st, ctx->ev_sort_done, 0));
@@ -824,6 +824,7 @@ rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scen
     ctx->sync_all();  // the previous frame's kernels read the buffers
     lap("sync");
     rlc::DevScene d{};
+    d.count_work = ctx->dev.count_work;
     upload_scene(h, ctx->scene_bufs, d, ctx->stream, true);
     // the copies complete before the host buffers are reused or freed and
     // before any stream reads the new scene
@@ -917,6 +918,30 @@ rlc_status rlc_debug_trav_stats(int32_t reset, uint64_t* out8) {
   return guarded([&] {
     require(out8 != nullptr, "rlc_debug_trav_stats: null argument");
     rlc::trav_stats(out8, reset != 0);
+  });
+}
+
+rlc_status rlc_context_count_work(rlc_context* ctx, int enable) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_count_work: null context");
+    ctx->dev.count_work = enable ? 1u : 0u;
+    ++ctx->scene_gen;  // captured pass graphs hold the old kernel choice
+  });
+}
+
+rlc_status rlc_work_counters(int32_t reset, uint64_t* out4) {
+  return guarded([&] {
+    require(out4 != nullptr, "rlc_work_counters: null argument");
+    rlc::work_counters(out4, reset != 0);
+  });
+}
+
+rlc_status rlc_measure_l2_bandwidth(int device, double* gbs) {
+  return guarded([&] {
+    require(gbs != nullptr, "rlc_measure_l2_bandwidth: null argument");
+    check_device(device);
+    *gbs = rlc::measure_l2_gbs(size_t(48) << 20, 40);
+    RLC_CK(cudaGetLastError());
   });
 }
 

@@ -46,6 +46,63 @@ __device__ unsigned long long g_trav[8];
 #else
 #define RLC_STAT(i, v) ((void)0)
 #endif
+// Work counters of the dominant kernel (the roofline's own-work bytes,
+// bench.py), kept while a context counts (rlc_context_count_work):
+// k_shadow's rays traversed by the tree, node steps and triangle tests,
+// summed per lane in registers and added once per warp, and the rays queued
+// for it.
+__device__ unsigned long long g_work[4];
+void work_counters(uint64_t out[4], bool reset) {
+  cudaMemcpyFromSymbol(out, g_work, sizeof(uint64_t) * 4);
+  if (reset) {
+    const unsigned long long z[4] = {};
+    cudaMemcpyToSymbol(g_work, z, sizeof(z));
+  }
+}
+
+// L2 read bandwidth probe (the bench's second roofline denominator): every
+// block streams the whole L2-resident buffer with 16-byte L2 loads (.cg, no
+// L1), `reps` times.
+__global__ void __launch_bounds__(256) k_l2_probe(const uint4* __restrict__ buf, size_t n16,
+                                                  uint32_t reps, uint32_t* __restrict__ sink) {
+  uint32_t acc = 0;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (uint32_t r = 0; r < reps; ++r)
+    for (size_t i = (size_t(blockIdx.x) * blockDim.x + threadIdx.x + r * 4099u) % n16, k = 0;
+         k < (n16 + stride - 1) / stride; ++k, i = (i + stride) % n16) {
+      const uint4 v = __ldcg(buf + i);
+      acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+  if (acc == 0x9e3779b9u) *sink = acc;  // keeps the loads
+}
+
+double measure_l2_gbs(size_t bytes, uint32_t reps) {
+  uint4* buf = nullptr;
+  uint32_t* sink = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess || cudaMalloc(&sink, 4) != cudaSuccess) return 0;
+  cudaMemset(buf, 1, bytes);
+  const size_t n16 = bytes / 16;
+  const uint32_t blocks = 148 * 8;
+  k_l2_probe<<<blocks, 256>>>(buf, n16, 1, sink);  // warm: the buffer into L2
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_l2_probe<<<blocks, 256>>>(buf, n16, reps, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const size_t stride = size_t(blocks) * 256;
+  const double moved = double(reps) * double((n16 + stride - 1) / stride) * double(stride) * 16.0;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  cudaFree(sink);
+  count_launch(2);
+  return ms > 0 ? moved / (ms * 1e-3) / 1e9 : 0;
+}
+
 void trav_stats(uint64_t out[8], bool reset) {
   cudaMemcpyFromSymbol(out, g_trav, sizeof(uint64_t) * 8);
   if (reset) {
@@ -1613,7 +1670,7 @@ __device__ __forceinline__ void mark_occluded(SampleRec* srec, uint32_t idx) {
 #ifndef RLC_SHADOW_BLOCKS
 #define RLC_SHADOW_BLOCKS 8  // blocks per SM (64 registers) with the 12-entry stack: c3 1.058 -> 1.045 ms (c5: 16.4 -> 16.8 ms; 7 was best with 32 entries)
 #endif
-template <bool QUANT>
+template <bool QUANT, bool COUNT>
 __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(DevScene sc,
                                                            const ShadowRay* __restrict__ rays,
                                                            const uint32_t* __restrict__ order,
@@ -1639,6 +1696,9 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
   __shared__ uint32_t stack_mem[kShadowStack * kShadowThreads];
   uint32_t* stack = stack_mem + threadIdx.x;
   int sp = 0;
+  uint32_t w_rays = 0, w_nodes = 0, w_tris = 0;  // g_work (COUNT instances only)
+#define RLC_WORK(x) \
+  if constexpr (COUNT) (x)
   while (true) {
     const unsigned need = __ballot_sync(kFull, !active);
     if (need && !exhausted) {
@@ -1685,6 +1745,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
             } else {
               cur = 0;
               active = true;
+              RLC_WORK(++w_rays);
               RLC_STAT(0, 1);
             }
           }
@@ -1700,6 +1761,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
     // register; the first leaf met is postponed and traversal continues
     // while some lane of the warp has not found a leaf yet
     while (cur != kDone && !(cur & kWideLeaf)) {
+      RLC_WORK(++w_nodes);
       RLC_STAT(1, 1);
       float tn[kWide];
       uint32_t mi, m;
@@ -1812,6 +1874,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
     bool hit = false;
     while (leaf != 0) {
       const uint32_t first = leaf_first(leaf), cnt = leaf_count(leaf);
+      RLC_WORK(w_tris += cnt);
       RLC_STAT(2, cnt);
       if (leaf & kLeafPure) {  // one reference leaf: one exact test for the leaf
         for (uint32_t i = first; i < first + cnt; ++i)
@@ -1841,6 +1904,15 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
       }
       active = false;
     }
+  }
+  if constexpr (!COUNT) return;
+  const uint32_t r = __reduce_add_sync(kFull, w_rays), nd = __reduce_add_sync(kFull, w_nodes),
+                 tr = __reduce_add_sync(kFull, w_tris);
+  if (lane == 0) {
+    atomicAdd(&g_work[0], (unsigned long long)r);
+    atomicAdd(&g_work[1], (unsigned long long)nd);
+    atomicAdd(&g_work[2], (unsigned long long)tr);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_work[3], (unsigned long long)n);
   }
 }
 
@@ -2700,7 +2772,7 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   static int per_sm = 0, sms = 0;
   if (per_sm == 0) {
     int dev = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shadow<true>, kShadowThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shadow<true, false>, kShadowThreads, 0);
     if (const char* e = getenv("RLC_SHADOW_BLOCKS_PER_SM"))  // tuning knob (co-residency)
       if (atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
     if (per_sm < 1) per_sm = 1;
@@ -2715,7 +2787,10 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
     return e ? atoi(e) : 1;
   }();
   const int use = leave_room && per_sm > room ? per_sm - room : per_sm;
-  auto kern = sc.wide_q ? k_shadow<true> : k_shadow<false>;
+  // the work-counting instances run only while the context counts (the
+  // bench's roofline frames); counting costs ~1.5% of a c3 frame
+  auto kern = sc.count_work ? (sc.wide_q ? k_shadow<true, true> : k_shadow<false, true>)
+                            : (sc.wide_q ? k_shadow<true, false> : k_shadow<false, false>);
   kern<<<use * sms, kShadowThreads, 0, st>>>(
       sc, b.rays, order, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
   count_launch();

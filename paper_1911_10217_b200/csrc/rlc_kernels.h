@@ -102,6 +102,7 @@ struct DevScene {
   uint32_t nodes_root_leaf;  // the reference BVH is a single leaf (no wide trees apply)
   uint32_t shadow_stack_limit;  // test knob RLC_SHADOW_STACK_LIMIT: a smaller k_shadow stack (0: full)
   uint32_t libm_fma; // host libm build whose sin/cos the bounce sampler restates (rlc_libm.h)
+  uint32_t count_work;  // k_shadow's counting instance (rlc_context_count_work)
   double shadow_eps;
   double coord_bound;  // S: k_shadow's lean test holds for ray origins within S
   double base_tile;
@@ -229,6 +230,9 @@ void launch_end_pass(const uint32_t* pass_dev, uint32_t offset, uint32_t* change
 void launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t st);  // *p = v
 void launch_add_u32(uint32_t* p, uint32_t v, cudaStream_t st);  // *p += v
 void trav_stats(uint64_t out[8], bool reset);
+void work_counters(uint64_t out[4], bool reset);  // k_shadow rays, node steps, triangle tests
+// Measured L2 read bandwidth (GB/s) over an L2-resident buffer of `bytes`.
+double measure_l2_gbs(size_t bytes, uint32_t reps);
 
 void launch_primary(const DevScene& sc, const DevGrid& g, const PassParams& p,
                     const PassBuffers& b, cudaStream_t st);

@@ -144,7 +144,11 @@ class RenderContext:
         _check(_lib.load().rlc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
     STAGES = ("primary", "sample", "sort", "fold", "accumulate", "split_collapse", "shadow",
-              "insert")
+              "insert", "compact")
+
+    def count_work(self, on: bool = True):
+        """k_shadow's counting instance on/off (rlc_context_count_work)."""
+        _check(_lib.load().rlc_context_count_work(self.handle, 1 if on else 0))
 
     def enable_timing(self, on: bool = True):
         _check(_lib.load().rlc_context_enable_timing(self.handle, 1 if on else 0))
@@ -628,6 +632,23 @@ def libm_sincos_host(x: np.ndarray, variant: int):
 
 def kernel_launches() -> int:
     return int(_lib.load().rlc_kernel_launches())
+
+
+def work_counters(reset: bool = True) -> dict:
+    """k_shadow's own work since the last reset (rlc_work_counters): rays
+    traversed by its tree, node steps, triangle tests."""
+    out = np.zeros(4, np.uint64)
+    _check(_lib.load().rlc_work_counters(1 if reset else 0,
+                                         out.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return {"shadow_rays": int(out[0]), "shadow_nodes": int(out[1]), "shadow_tris": int(out[2]),
+            "shadow_rays_queued": int(out[3])}
+
+
+def measure_l2_bandwidth(device: int = 0) -> float:
+    """Measured L2 read bandwidth of the device, GB/s (rlc_measure_l2_bandwidth)."""
+    out = C.c_double()
+    _check(_lib.load().rlc_measure_l2_bandwidth(device, C.byref(out)))
+    return out.value
 
 
 def trav_stats(reset: bool = True) -> dict:

@@ -138,6 +138,26 @@ def test_render_frame_matches_reference(ref):
             rres["occupied"], rres["lookups"], rres["fallback_hits"])
 
 
+def test_render_frame_repeated_c3_matches_reference(ref):
+    """render_frame called back to back on the c3 scene (full-size tables,
+    the next pass's primary rays overlapping each pass's tail): every call
+    resets the cached grid on the main stream, and the first pass's primary
+    rays (side stream) must see the reset table -- each call equals a fresh
+    reference render_frame."""
+    scene, st = scenes.config_scene("c3")
+    scene = scene.with_resolution(320, 180)
+    cfg = rlcuts.RenderConfig(spp=3, passes=3, sampler=RL,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    ctx = rlcuts.build_context(scene, cfg)
+    rres = ref.ref_render_frame(scene, cfg)
+    for _ in range(4):
+        res = rlcuts.render_frame(ctx, cfg)
+        assert np.array_equal(res.image, rres["image"])
+        assert res.sc_changes == rres["sc_changes"]
+        assert (res.occupied_cells, res.lookups, res.fallback_hits) == (
+            rres["occupied"], rres["lookups"], rres["fallback_hits"])
+
+
 @pytest.mark.parametrize("depth", [1, 2])
 def test_async_passes_bit_exact(ref, depth):
     """Passes enqueued back to back without host synchronisation (as the
