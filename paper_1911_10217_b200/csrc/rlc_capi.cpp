@@ -242,6 +242,7 @@ const char* device_error_message(uint32_t bits) {
   if (bits & rlc::kErrBadAreaPdf) return "level_for_footprint: area pdf must be positive";
   if (bits & rlc::kErrStackOverflow) return "scene BVH deeper than the 64-entry traversal stack";
   if (bits & rlc::kErrNewKeyOverflow) return "hash grid: new-key table of the pass overflowed";
+  if (bits & rlc::kErrCheck) return "device bounds check failed (RLC_DEBUG_CHECKS build)";
   return "device error";
 }
 
@@ -486,7 +487,7 @@ uint32_t read_and_clear_err(cudaStream_t st, unsigned long long* counters) {
 }
 
 void throw_device_error(uint32_t bits) {
-  if (bits & (rlc::kErrStackOverflow | rlc::kErrNewKeyOverflow))
+  if (bits & (rlc::kErrStackOverflow | rlc::kErrNewKeyOverflow | rlc::kErrCheck))
     throw std::runtime_error(device_error_message(bits));
   throw rlc::InvalidArgument(device_error_message(bits));
 }

@@ -113,6 +113,20 @@ void trav_stats(uint64_t out[8], bool reset) {
 
 static inline uint32_t blocks_for(uint32_t n, uint32_t t) { return (n + t - 1) / t; }
 
+// Debug build (EXTRA=-DRLC_DEBUG_CHECKS): device bounds checks on the
+// indices the hash grid, cut sampling, shadow queue and fold compute; a
+// failure raises kErrCheck, reported by the host as an exception.  (The
+// pool's compute-sanitizer is closed; tests/run_checked.sh runs the GPU
+// suite against this build.)
+#ifdef RLC_DEBUG_CHECKS
+#define RLC_CHECK(cond, errp)                                                 \
+  do {                                                                        \
+    if (!(cond)) atomicOr(reinterpret_cast<unsigned int*>(errp), kErrCheck); \
+  } while (0)
+#else
+#define RLC_CHECK(cond, errp) ((void)0)
+#endif
+
 // ---------------------------------------------------------------------------
 // geometry helpers
 // ---------------------------------------------------------------------------
@@ -682,6 +696,7 @@ __global__ void __launch_bounds__(256) k_commit(DevGrid g, NewKeys nk) {
     uint32_t cid = 0;
     if (lane == 0) {
       cid = uint32_t(atomicAdd(g.counters + kCntCells, 1ull));
+      RLC_CHECK(cid < g.capacity && slot < g.capacity, g.counters + kCntErr);
       g.claim[slot] = ~0ull;
       g.slot_keys[2 * size_t(slot)] = lo;
       g.slot_keys[2 * size_t(slot) + 1] = hi;
@@ -1053,6 +1068,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
     const double span = cdf[s] - clo;
     const double frac = span > 0 ? clampd((u1 * total - clo) / span, 0.0, 1.0) : 0.0;
     const uint32_t offset = min(size - 1, uint32_t(frac * double(size)));
+    RLC_CHECK(s < g.M && size >= 1 && begin + offset < sc.num_lights, err);
     e = sc.order[begin + offset];
     if (P.export_samples) emit[idx] = e;
     r.pin = 1.0 / double(size);
@@ -1092,6 +1108,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
     r.pin = sc.emitter_energy[e] / back;
   }
 
+  RLC_CHECK(e < sc.num_lights, err);
   const LightRec& L = sc.lights[e];
   r.pdf_area = L.pdf_area;
   if (!(L.pdf_area > 0)) atomicOr(err, kErrDegenerateLight);
@@ -2087,6 +2104,8 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
   if (k == kInvalidKey) return;
   if (i > 0 && keys[i - 1] == k) return;
   const uint32_t cell = k / g.M;
+  RLC_CHECK(cell < g.capacity && cell < uint32_t(g.counters[kCntCells]),
+            g.counters + kCntErr);
   const size_t at = size_t(k);
   double q = g.q[at];
   uint32_t vis = g.visits[at];

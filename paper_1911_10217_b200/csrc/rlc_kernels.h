@@ -35,6 +35,7 @@ enum : uint32_t {
   kErrBadAreaPdf = 8u,        // level_for_footprint, hash_grid.cpp:35-37
   kErrStackOverflow = 16u,    // BVH deeper than the traversal stack
   kErrNewKeyOverflow = 32u,   // more distinct new keys in one pass than the dedup table holds
+  kErrCheck = 64u,            // a device bounds check failed (RLC_DEBUG_CHECKS builds)
 };
 
 // Counters block (u64 each).
