@@ -184,6 +184,13 @@ rlc_status rlc_context_synchronize(rlc_context* ctx);
 #define RLC_NUM_STAGES 9
 rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable);
 rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts);
+/* The timeline behind rlc_context_stage_times (call it first): per stage
+ * launch, out[3i..3i+2] = stage, start, end in ms from the first mark, on
+ * the stream the stage ran on (the overlap of the streams made visible).
+ * *n_out = marks recorded; synchronizes.  Marks are kept until the next
+ * rlc_context_stage_times. */
+rlc_status rlc_context_stage_marks(rlc_context* ctx, uint32_t max_marks, double* out,
+                                   uint32_t* n_out);
 
 /* ---- scene visibility, batched ---------------------------------------- */
 /* occluded (proj/include/rlcuts/bvh.hpp:38-40, proj/src/bvh.cpp:159-188):

@@ -91,6 +91,7 @@ SIGNATURES = {
     "rlc_context_synchronize": (C.c_int, [_P]),
     "rlc_context_enable_timing": (C.c_int, [_P, C.c_int]),
     "rlc_context_stage_times": (C.c_int, [_P, _dp, _u32p]),
+    "rlc_context_stage_marks": (C.c_int, [_P, C.c_uint32, _dp, _u32p]),
     "rlc_occluded_batch": (C.c_int, [_P, C.c_uint32, _dp, _dp, C.POINTER(C.c_uint8)]),
     "rlc_libm_variant": (C.c_int, [C.POINTER(C.c_int32)]),
     "rlc_libm_sincos": (C.c_int, [_P, C.c_uint32, _dp, _dp, _dp]),

@@ -303,6 +303,10 @@ struct rlc_context {
   cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
   rlc::GBuf* gslot[2] = {nullptr, nullptr};
   unsigned long long* pkey_slot[2] = {nullptr, nullptr};  // pending keys, per G-buffer slot
+  // sample records and q_before per G-buffer slot: pass p's accumulation
+  // (side stream) reads them while pass p + 1 samples and folds
+  rlc::SampleRec* srec_slot[2] = {nullptr, nullptr};
+  double* qb_slot[2] = {nullptr, nullptr};
   void sync_all() {
     RLC_CK(cudaStreamSynchronize(stream));
     if (pstream) RLC_CK(cudaStreamSynchronize(pstream));
@@ -377,7 +381,7 @@ struct rlc_context {
     xb.vals = xarena.alloc<uint32_t>(cap);
     xb.keys_alt = xarena.alloc<uint32_t>(cap);
     xb.vals_alt = xarena.alloc<uint32_t>(cap);
-    xb.hist = xarena.alloc<uint32_t>((size_t(cap) / 4096 + 2) * 256);
+    xb.hist = xarena.alloc<uint32_t>((size_t(cap) / 1024 + 2) * 256);  // sort tile: 1024 keys
     xb.q_rec = xarena.alloc<double>(cap);
     xb.nk = alloc_new_keys(xarena, cap, stream);
     xb.cap = cap;
@@ -419,7 +423,8 @@ struct rlc_context {
   // rlc_pass_samples: the last pass's parameters and G-buffer slot
   bool export_samples = false;
   rlc::PassParams last_pass{};
-  rlc::GBuf* last_gbuf = nullptr;
+  rlc::PassBuffers last_pb{};
+  bool last_valid = false;
 
   void ensure_scratch(uint32_t n) {
     if (n <= pb_cap) return;
@@ -435,13 +440,17 @@ struct rlc_context {
     pb.pkey = pkey_slot[0];
     pb.nk = alloc_new_keys(scratch, cap, stream);
     pb.emit = scratch.alloc<uint32_t>(cap);
-    pb.srec = scratch.alloc<rlc::SampleRec>(cap);
+    srec_slot[0] = scratch.alloc<rlc::SampleRec>(cap);
+    srec_slot[1] = scratch.alloc<rlc::SampleRec>(cap);
+    pb.srec = srec_slot[0];
     pb.rflag = scratch.alloc<uint8_t>(cap);
     pb.keys = scratch.alloc<uint32_t>(cap);
     pb.vals = scratch.alloc<uint32_t>(cap);
     pb.keys_alt = scratch.alloc<uint32_t>(cap);
     pb.vals_alt = scratch.alloc<uint32_t>(cap);
-    pb.q_before = scratch.alloc<double>(cap);
+    qb_slot[0] = scratch.alloc<double>(cap);
+    qb_slot[1] = scratch.alloc<double>(cap);
+    pb.q_before = qb_slot[0];
     pb.rays = scratch.alloc<rlc::ShadowRay>(cap);
     pb.ray_count = scratch.alloc<unsigned int>(2);
     pb.ray_order = scratch.alloc<uint32_t>(cap);
@@ -449,7 +458,9 @@ struct rlc_context {
     pb.rec_count = scratch.alloc<unsigned int>(2);
     rec_out = scratch.alloc<rlc::UpdateRecord>(cap);
     pb.block_counts = scratch.alloc<uint32_t>(cap / 2048 + 2);
-    pb.sort_hist_cap = ((cap + 4095u) / 4096u + 2u) * 256u;  // rows + digit totals
+    pb.block_counts2 = scratch.alloc<uint32_t>(cap / 2048 + 2);
+    pb.sort_count = scratch.alloc<unsigned int>(2);
+    pb.sort_hist_cap = ((cap + 1023u) / 1024u + 2u) * 256u;  // rows + digit totals (1024-key tiles)
     pb.sort_hist = scratch.alloc<uint32_t>(pb.sort_hist_cap);
     pb_cap = cap;
   }
@@ -516,7 +527,8 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
           "render_pass: framebuffer size must match the camera");
   require(r0 <= r1 && r1 <= uint32_t(ctx->host.cam.height), "render_pass: bad row range");
   require(grid == nullptr || grid->ctx == ctx, "render_pass: grid belongs to another context");
-  ctx->join_acc();  // the pass buffers and the framebuffer are free again
+  // no join with the previous pass's accumulation: it reads only its own
+  // G-buffer slot's buffers (the next pass's primary rays wait for them)
   PassSetup S;
   const uint32_t spp_pp = cfg->spp / cfg->passes;
   const uint64_t n64 = uint64_t(r1 - r0) * uint64_t(ctx->host.cam.width) * spp_pp;
@@ -556,6 +568,8 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   const int slot = int(S.p.pass_index & 1u);
   ctx->pb.gbuf = ctx->gslot[slot];
   ctx->pb.pkey = ctx->pkey_slot[slot];
+  ctx->pb.srec = ctx->srec_slot[slot];
+  ctx->pb.q_before = ctx->qb_slot[slot];
   const bool rl = S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
   // The pass's new keys go in after all its lookups, in canonical order
   // (k_insert / k_commit, the reference's sequential insertion), right behind
@@ -569,7 +583,8 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   auto insert_new_keys = [&](cudaStream_t s) {
     ctx->stage_on(s, 7, [&] { rlc::launch_insert_new_keys(S.g, ctx->pb.nk, s); });
   };
-  if (ctx->overlap) RLC_CK(cudaStreamWaitEvent(ps, ctx->ev_gbuf_free[slot], 0));
+  // the slot's buffers are free once pass - 2's accumulation has read them
+  RLC_CK(cudaStreamWaitEvent(ps, ctx->ev_gbuf_free[slot], 0));
   if (rl) RLC_CK(cudaMemsetAsync(ctx->pb.nk.count, 0, sizeof(unsigned int), ps));
   ctx->stage_on(ps, 0, [&] { rlc::launch_primary(ctx->dev, S.g, S.p, ctx->pb, ps); });
   if (insert && S.p.depth == 1) insert_new_keys(ps);
@@ -623,7 +638,8 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
   uint32_t *k = nullptr, *v = nullptr;
   if (S.nv > 0) enqueue_trace(ctx, S, grid, &k, &v);  // max_depth 0: empty paths
   ctx->last_pass = S.p;
-  ctx->last_gbuf = ctx->pb.gbuf;
+  ctx->last_pb = ctx->pb;
+  ctx->last_valid = true;
   cudaStream_t st = ctx->stream;
   if (cfg->sampler == RLC_SAMPLER_RL_LIGHTCUTS && S.nv > 0) {
     ctx->stage(3, [&] { rlc::launch_fold(S.g, S.p, k, v, ctx->pb, st); });
@@ -665,7 +681,6 @@ void enqueue_eop(rlc_grid* grid, const rlc_context* ctx, const rlc_cut_config* c
     rlc::launch_split_collapse(ctx->dev, grid->dev, cut->split_threshold, cut->iterations,
                                d_changes, ctx->stream);
   });
-  c->join_acc();  // the pass's accumulation ran beside split-collapse; the frame ends here
   RLC_CK(cudaGetLastError());
 }
 
@@ -915,6 +930,25 @@ rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* count
   });
 }
 
+rlc_status rlc_context_stage_marks(rlc_context* ctx, uint32_t max_marks, double* out,
+                                   uint32_t* n_out) {
+  return guarded([&] {
+    require(ctx != nullptr && n_out != nullptr, "rlc_context_stage_marks: null argument");
+    ctx->sync_all();
+    *n_out = uint32_t(ctx->marks.size());
+    if (!out || ctx->marks.empty()) return;
+    const cudaEvent_t t0 = ctx->marks.front().a;
+    for (size_t i = 0; i < ctx->marks.size() && i < max_marks; ++i) {
+      float a = 0, b = 0;
+      RLC_CK(cudaEventElapsedTime(&a, t0, ctx->marks[i].a));
+      RLC_CK(cudaEventElapsedTime(&b, t0, ctx->marks[i].b));
+      out[3 * i] = ctx->marks[i].stage;
+      out[3 * i + 1] = a;
+      out[3 * i + 2] = b;
+    }
+  });
+}
+
 rlc_status rlc_debug_trav_stats(int32_t reset, uint64_t* out8) {
   return guarded([&] {
     require(out8 != nullptr, "rlc_debug_trav_stats: null argument");
@@ -994,6 +1028,7 @@ rlc_status rlc_occluded_batch(const rlc_context* cctx, uint32_t n, const double*
     if (n == 0) return;
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     RLC_CK(cudaSetDevice(ctx->device));
+    ctx->join_acc();  // the shadow queue and sample records are reused below
     ctx->ensure_scratch(n);
     DeviceArena tmp;
     double* da = tmp.alloc<double>(3 * size_t(n));
@@ -1332,7 +1367,8 @@ rlc_status rlc_pass_trace(const rlc_context* cctx, const rlc_render_config* conf
     uint32_t *k, *v;
     enqueue_trace(ctx, S, grid, &k, &v);
     ctx->last_pass = S.p;
-    ctx->last_gbuf = ctx->pb.gbuf;
+    ctx->last_pb = ctx->pb;
+    ctx->last_valid = true;
     rlc::launch_export_records(S.g, ctx->pb, S.nv, ctx->rec_out, ctx->stream);
     unsigned int c = 0;
     RLC_CK(cudaMemcpyAsync(&c, ctx->pb.rec_count, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1395,15 +1431,13 @@ rlc_status rlc_pass_samples(const rlc_context* cctx, uint64_t max_n, rlc_sample_
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     const rlc::PassParams& p = ctx->last_pass;
     *n_out = p.nv;
-    if (out == nullptr || max_n == 0 || p.nv == 0 || ctx->last_gbuf == nullptr) return;
+    if (out == nullptr || max_n == 0 || p.nv == 0 || !ctx->last_valid) return;
     RLC_CK(cudaSetDevice(ctx->device));
     ctx->sync_all();
     const uint64_t n = std::min<uint64_t>(max_n, p.nv);
     DeviceArena tmp;
     rlc::SampleExport* d = tmp.alloc<rlc::SampleExport>(p.nv);
-    rlc::PassBuffers b = ctx->pb;
-    b.gbuf = ctx->last_gbuf;
-    rlc::launch_export_samples(p, b, d, ctx->stream);
+    rlc::launch_export_samples(p, ctx->last_pb, d, ctx->stream);
     RLC_CK(cudaGetLastError());
     RLC_CK(cudaMemcpyAsync(out, d, n * sizeof(rlc_sample_record), cudaMemcpyDeviceToHost,
                            ctx->stream));

@@ -1019,7 +1019,6 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
   const GBuf gb = gbuf[idx];
   keys[idx] = kInvalidKey;
-  vals[idx] = idx;
   if (!(gb.flags & kGReflective)) {
     srec[idx].flags = 0;
     rflag[idx] = 0;  // read by the compactions
@@ -1936,17 +1935,22 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
 // ---------------------------------------------------------------------------
 // stable LSD radix sort of (key, val) pairs, 8-bit digits
 // ---------------------------------------------------------------------------
-constexpr int kRsThreads = 256;
+// Sized to run beside k_shadow: with 7 shadow blocks per SM (64 registers
+// x 128 threads each) an SM has 8,192 registers left, so every kernel of the
+// record sort keeps a block at <= 8,192 registers (128 threads x <= 64);
+// a block that does not fit waits for the shadow blocks to retire.
+constexpr int kRsThreads = 128;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsItems = 16;  // per thread
+constexpr int kRsItems = 8;  // per thread
 constexpr int kRsTile = kRsThreads * kRsItems;
 constexpr int kRsWarpSpan = 32 * kRsItems;
 
 __global__ void __launch_bounds__(kRsThreads) rs_hist(const uint32_t* __restrict__ keys,
-                                                      uint32_t n, int shift,
-                                                      uint32_t* __restrict__ hist) {
+                                                      uint32_t n, const unsigned* __restrict__ n_dev,
+                                                      int shift, uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
+  if (n_dev) n = min(n, *n_dev);  // the device-side count of the compacted records
+  for (int d = threadIdx.x; d < 256; d += kRsThreads) h[d] = 0;
   __syncthreads();
   const uint32_t base = blockIdx.x * kRsTile;
   for (int i = 0; i < kRsItems; ++i) {
@@ -1954,14 +1958,16 @@ __global__ void __launch_bounds__(kRsThreads) rs_hist(const uint32_t* __restrict
     if (j < n) atomicAdd(&h[(keys[j] >> shift) & 255u], 1u);
   }
   __syncthreads();
-  hist[threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+  for (int d = threadIdx.x; d < 256; d += kRsThreads) hist[d * gridDim.x + blockIdx.x] = h[d];
 }
 
-// Exclusive scan of `total` counters in place, one block.
-__global__ void __launch_bounds__(1024) rs_scan(uint32_t* __restrict__ hist, uint32_t total) {
+// Exclusive scan of `total` counters in place, one block of kScanThreads
+// (sized to fit beside k_shadow, see kRsThreads).
+constexpr uint32_t kScanThreads = 256;
+__global__ void __launch_bounds__(kScanThreads) rs_scan(uint32_t* __restrict__ hist, uint32_t total) {
   __shared__ uint32_t warp_sums[32];
   const uint32_t t = threadIdx.x;
-  const uint32_t per = (total + 1023u) / 1024u;
+  const uint32_t per = (total + kScanThreads - 1u) / kScanThreads;
   const uint32_t b = t * per, e = min(total, b + per);
   uint32_t sum = 0;
   for (uint32_t i = b; i < e; ++i) sum += hist[i];
@@ -1975,7 +1981,7 @@ __global__ void __launch_bounds__(1024) rs_scan(uint32_t* __restrict__ hist, uin
   if (lane == 31) warp_sums[w] = x;
   __syncthreads();
   if (w == 0) {
-    uint32_t ws = warp_sums[lane];
+    uint32_t ws = lane < kScanThreads / 32 ? warp_sums[lane] : 0u;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, ws, o);
       if (lane >= uint32_t(o)) ws += y;
@@ -2025,17 +2031,22 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restr
                                                          const uint32_t* __restrict__ vin,
                                                          uint32_t* __restrict__ kout,
                                                          uint32_t* __restrict__ vout,
-                                                         uint32_t n, int shift,
+                                                         uint32_t n, const unsigned* __restrict__ n_dev,
+                                                         int shift,
                                                          const uint32_t* __restrict__ offs,
                                                          const uint32_t* __restrict__ totals) {
   __shared__ uint32_t wh[kRsWarps][256];
+  if (n_dev) n = min(n, *n_dev);
   __shared__ uint32_t base_off[256];
   __shared__ uint32_t dsum[kRsWarps];
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
   for (int d = lane; d < 256; d += 32) wh[w][d] = 0;
   {  // digit base = exclusive prefix of the digit totals, + this block's row offset
-    const uint32_t t = totals[threadIdx.x];
-    uint32_t x = t;
+    // (two digits per thread: digits 2t, 2t + 1)
+    const uint32_t d0 = 2 * threadIdx.x;
+    const uint32_t t0 = totals[d0], t1 = totals[d0 + 1];
+    const uint32_t pair = t0 + t1;
+    uint32_t x = pair;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, x, o);
       if (lane >= uint32_t(o)) x += y;
@@ -2044,7 +2055,9 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restr
     __syncthreads();
     uint32_t before = 0;
     for (uint32_t q = 0; q < w; ++q) before += dsum[q];
-    base_off[threadIdx.x] = before + x - t + offs[threadIdx.x * gridDim.x + blockIdx.x];
+    const uint32_t ex = before + x - pair;
+    base_off[d0] = ex + offs[d0 * gridDim.x + blockIdx.x];
+    base_off[d0 + 1] = ex + t0 + offs[(d0 + 1) * gridDim.x + blockIdx.x];
   }
   __syncwarp();
   const uint32_t base = blockIdx.x * kRsTile + w * kRsWarpSpan;
@@ -2065,8 +2078,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restr
     __syncwarp();
   }
   __syncthreads();
-  {  // cross-warp exclusive prefix per digit
-    const uint32_t d = threadIdx.x;
+  for (uint32_t d = threadIdx.x; d < 256; d += kRsThreads) {  // cross-warp exclusive prefix per digit
     uint32_t run = 0;
     for (int ww = 0; ww < kRsWarps; ++ww) {
       const uint32_t c = wh[ww][d];
@@ -2097,8 +2109,10 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
                                               const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ vals,
                                               const char* __restrict__ vbase, uint32_t vstride,
-                                              double* __restrict__ q_before) {
+                                              double* __restrict__ q_before,
+                                              const unsigned* __restrict__ n_dev) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n_dev) P.n = min(P.n, *n_dev);
   if (i >= P.n) return;
   const uint32_t k = keys[i];
   if (k == kInvalidKey) return;
@@ -2437,7 +2451,9 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
 }
 
 static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, uint32_t mask,
-                           uint32_t* out, unsigned int* count_out, cudaStream_t st);
+                           uint32_t* out, unsigned int* count_out, cudaStream_t st,
+                           uint32_t* block_counts = nullptr, const uint32_t* key_src = nullptr,
+                           uint32_t* key_out = nullptr);
 
 // ---------------------------------------------------------------------------
 // Screen-band sharding with an exact exchange: every
@@ -2593,12 +2609,13 @@ void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const 
                                                           x.vals, x.q_rec);
     count_launch();
     uint32_t *k = nullptr, *v = nullptr;
-    launch_sort_buffers(x.keys, x.vals, x.keys_alt, x.vals_alt, x.hist, total, key_bits, st, &k, &v);
+    launch_sort_buffers(x.keys, x.vals, x.keys_alt, x.vals_alt, x.hist, total, key_bits, st, &k, &v,
+                        nullptr);
     PassParams p = fold_params;
     p.n = total;
     k_fold<<<blocks_for(total, 256), 256, 0, st>>>(
         g, p, k, v, reinterpret_cast<const char*>(x.contig) + offsetof(UpdateRecord, v),
-        uint32_t(sizeof(UpdateRecord)), x.q_rec);
+        uint32_t(sizeof(UpdateRecord)), x.q_rec, nullptr);
     count_launch();
   }
   if (local_n == 0) return;
@@ -2744,7 +2761,9 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const uint8_t* __re
                                                              uint32_t n, uint32_t mask,
                                                              const uint32_t* __restrict__ offs,
                                                              uint32_t* __restrict__ out,
-                                                             unsigned int* __restrict__ count_out) {
+                                                             unsigned int* __restrict__ count_out,
+                                                             const uint32_t* __restrict__ key_src,
+                                                             uint32_t* __restrict__ key_out) {
   __shared__ uint32_t wsum[kCmpThreads / 32];
   __shared__ uint32_t base;
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
@@ -2761,7 +2780,12 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const uint8_t* __re
       before += q < w ? wsum[q] : 0u;
       total += wsum[q];
     }
-    if (f) out[base + before + __popc(b & ((1u << lane) - 1u))] = order ? order[j] : j;
+    if (f) {
+      const uint32_t at = base + before + __popc(b & ((1u << lane) - 1u));
+      const uint32_t i = order ? order[j] : j;
+      out[at] = i;
+      if (key_out) key_out[at] = key_src[i];
+    }
     __syncthreads();
     if (threadIdx.x == 0) base += total;
     __syncthreads();
@@ -2772,13 +2796,19 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const uint8_t* __re
   }
 }
 
+// Stable compaction of the vertices whose rflag has `mask`, in the order of
+// `order` (canonical when null), into out[]; the count goes to count_out[0].
+// With key_out, key_src[vertex] is gathered alongside.  block_counts: a
+// scratch of its own per concurrent stream (null: b.block_counts).
 static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, uint32_t mask,
-                           uint32_t* out, unsigned int* count_out, cudaStream_t st) {
+                           uint32_t* out, unsigned int* count_out, cudaStream_t st,
+                           uint32_t* block_counts, const uint32_t* key_src, uint32_t* key_out) {
   const uint32_t nb = blocks_for(n > 0 ? n : 1, kCmpTile);
-  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, b.block_counts);
-  rs_scan<<<1, 1024, 0, st>>>(b.block_counts, nb);
-  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, b.block_counts, out,
-                                            count_out);
+  uint32_t* bc = block_counts ? block_counts : b.block_counts;
+  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, bc);
+  rs_scan<<<1, kScanThreads, 0, st>>>(bc, nb);
+  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, bc, out, count_out, key_src,
+                                            key_out);
   count_launch(3);
 }
 
@@ -2817,14 +2847,14 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
 
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
-                         uint32_t** vals_out) {
+                         uint32_t** vals_out, const unsigned* n_dev) {
   if (n > 1) {
     const uint32_t nb = blocks_for(n, kRsTile);
     for (uint32_t shift = 0; shift < key_bits; shift += 8) {
-      rs_hist<<<nb, kRsThreads, 0, st>>>(ka, n, int(shift), hist);
+      rs_hist<<<nb, kRsThreads, 0, st>>>(ka, n, n_dev, int(shift), hist);
       uint32_t* totals = hist + size_t(nb) * 256u;
       rs_scan_rows<<<256, 256, 0, st>>>(hist, nb, totals);
-      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, int(shift), hist, totals);
+      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, n_dev, int(shift), hist, totals);
       count_launch(3);
       uint32_t* t = ka;
       ka = kb;
@@ -2840,8 +2870,13 @@ void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb,
 
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out) {
-  launch_sort_buffers(b.keys, b.vals, b.keys_alt, b.vals_alt, b.sort_hist, n, key_bits, st,
-                      keys_out, vals_out);
+  // only the vertices that carry an update record are sorted (c3: 1.48M of
+  // 2.07M): a stable compaction gathers their keys in canonical order, and
+  // the digit passes read the count on the device
+  launch_compact(b, nullptr, n, kSRecord, b.vals_alt, b.sort_count, st, b.block_counts2, b.keys,
+                 b.keys_alt);
+  launch_sort_buffers(b.keys_alt, b.vals_alt, b.keys, b.vals, b.sort_hist, n, key_bits, st,
+                      keys_out, vals_out, b.sort_count);
 }
 
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
@@ -2851,7 +2886,7 @@ void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
   q.n = p.nv;  // k_fold runs over the update records of all path vertices
   k_fold<<<blocks_for(q.n, 256), 256, 0, st>>>(
       g, q, keys, vals, reinterpret_cast<const char*>(b.srec) + offsetof(SampleRec, v),
-      uint32_t(sizeof(SampleRec)), b.q_before);
+      uint32_t(sizeof(SampleRec)), b.q_before, b.sort_count);
   count_launch();
 }
 

@@ -190,6 +190,8 @@ struct PassBuffers {
   uint32_t* rec_path;       // path index of each update record (canonical order)
   unsigned int* rec_count;  // [0] update records of the pass
   uint32_t* block_counts;   // compaction scratch
+  uint32_t* block_counts2;  // compaction scratch of the record sort (side stream)
+  unsigned int* sort_count; // update records of the pass (the record sort's device count)
   uint32_t* sort_hist;
   uint32_t sort_hist_cap;  // entries
 };
@@ -255,9 +257,10 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
                    unsigned long long* counters, cudaStream_t st, bool leave_room = false);
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out);
+// n_dev (may be null): a device-side count <= n of the valid entries.
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
-                         uint32_t** vals_out);
+                         uint32_t** vals_out, const unsigned* n_dev);
 void launch_export_records(const DevGrid& g, const PassBuffers& b, uint32_t n,
                            UpdateRecord* out, cudaStream_t st);
 void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const PassBuffers& b,

@@ -160,6 +160,17 @@ class RenderContext:
         _check(_lib.load().rlc_context_stage_times(self.handle, _dptr(ms), _uptr(cnt)))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.STAGES)}
 
+    def stage_marks(self) -> list:
+        """[(stage name, start ms, end ms)] of every timed stage launch since
+        the last stage_times() (read before calling it), from the first."""
+        lib = _lib.load()
+        n = C.c_uint32()
+        _check(lib.rlc_context_stage_marks(self.handle, 0, None, C.byref(n)))
+        out = np.zeros(3 * max(n.value, 1))
+        _check(lib.rlc_context_stage_marks(self.handle, n.value, _dptr(out), C.byref(n)))
+        return [(self.STAGES[int(out[3 * i])], out[3 * i + 1], out[3 * i + 2])
+                for i in range(n.value)]
+
     def libm_sincos(self, x: np.ndarray):
         """The bounce sampler's sin/cos on the device (rlc_libm.h)."""
         x = np.ascontiguousarray(x, np.float64).ravel()
