@@ -216,6 +216,11 @@ rlc_status rlc_debug_trav_stats(int32_t reset, uint64_t* out8);
  * clears them. */
 rlc_status rlc_work_counters(int32_t reset, uint64_t* out4);
 rlc_status rlc_context_count_work(rlc_context* ctx, int enable);
+/* Diagnostic, host only (no device needed): the reference scene BVH build
+ * (build_scene_bvh, bvh.cpp:64-122) of `scene`, `reps` times; *ms_out =
+ * mean milliseconds, *nodes_out = node count (may be NULL). */
+rlc_status rlc_debug_host_bvh(const rlc_scene_desc* scene, uint32_t reps, double* ms_out,
+                              uint32_t* nodes_out);
 /* Measured L2 read bandwidth of `device` in GB/s (16-byte L2 loads over a
  * 48 MB L2-resident buffer): the bench's second roofline denominator. */
 rlc_status rlc_measure_l2_bandwidth(int device, double* gbs);

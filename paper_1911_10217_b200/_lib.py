@@ -101,6 +101,7 @@ SIGNATURES = {
     "rlc_debug_trav_stats": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
     "rlc_work_counters": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
     "rlc_context_count_work": (C.c_int, [_P, C.c_int]),
+    "rlc_debug_host_bvh": (C.c_int, [C.POINTER(SceneDescC), C.c_uint32, _dp, _u32p]),
     "rlc_measure_l2_bandwidth": (C.c_int, [C.c_int, _dp]),
     "rlc_render_passes_async": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, C.c_uint32,
                                           _P, _P]),

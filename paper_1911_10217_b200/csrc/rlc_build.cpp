@@ -48,18 +48,28 @@ class WorkerPool {
   }
   unsigned threads() const { return unsigned(workers_.size()) + 1; }
   // Runs job(c) for c in [0, chunks); returns when all are done.
+  // Submissions from a thread that set low priority (background work beside
+  // a critical path, e.g. the shadow-tree refit beside the reference BVH)
+  // are taken by the workers only when no normal batch has chunks left.
+  static int& priority() {
+    thread_local int p = 1;
+    return p;
+  }
   void run(size_t chunks, const std::function<void(size_t)>& job) {
     auto batch = std::make_shared<Batch>();
     batch->job = &job;
     batch->chunks = chunks;
+    batch->prio = priority();
     {
       std::lock_guard<std::mutex> lk(m_);
       queue_.push_back(batch);
+      has_work_.store(true, std::memory_order_release);
     }
     cv_.notify_all();
     work(*batch);  // the submitter takes chunks too
-    std::unique_lock<std::mutex> lk(batch->m);
-    batch->cv.wait(lk, [&] { return batch->done == batch->chunks; });
+    // the last chunks are short: spin on the count instead of sleeping on a
+    // condition variable (a futex wake costs tens of microseconds per loop)
+    while (batch->done.load(std::memory_order_acquire) != batch->chunks) cpu_relax();
     if (batch->error) std::rethrow_exception(batch->error);
   }
   ~WorkerPool() {
@@ -76,46 +86,69 @@ class WorkerPool {
     const std::function<void(size_t)>* job = nullptr;
     size_t chunks = 0;
     std::atomic<size_t> next{0};
-    size_t done = 0;  // under m
-    std::exception_ptr error;
+    std::atomic<size_t> done{0};
+    int prio = 1;
+    std::exception_ptr error;  // under m
     std::mutex m;
-    std::condition_variable cv;
   };
+  static void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#else
+    std::this_thread::yield();
+#endif
+  }
   WorkerPool() {
     const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
     for (unsigned i = 0; i + 1 < hw; ++i) workers_.emplace_back([this] { loop(); });
   }
   static void work(Batch& b) {
     for (size_t c; (c = b.next.fetch_add(1)) < b.chunks;) {
-      std::exception_ptr err;
       try {
         (*b.job)(c);
       } catch (...) {
-        err = std::current_exception();
+        std::lock_guard<std::mutex> lk(b.m);
+        if (!b.error) b.error = std::current_exception();
       }
-      std::lock_guard<std::mutex> lk(b.m);
-      if (err && !b.error) b.error = err;
-      if (++b.done == b.chunks) b.cv.notify_all();
+      b.done.fetch_add(1, std::memory_order_acq_rel);
     }
   }
   void loop() {
     while (true) {
+      // per-frame scene updates submit loops back to back: spin ~50 us for
+      // the next batch before sleeping on the condition variable (longer
+      // spins steal the cores of the build's own threads)
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int i = 0; !has_work_.load(std::memory_order_acquire); ++i) {
+        cpu_relax();
+        if ((i & 63) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(50))
+          break;
+      }
       std::shared_ptr<Batch> b;
       {
         std::unique_lock<std::mutex> lk(m_);
         cv_.wait(lk, [&] { return stop_ || !queue_.empty(); });
         if (stop_) return;
-        b = queue_.front();
-        if (b->next.load() >= b->chunks) {  // fully claimed: retire it
-          queue_.pop_front();
+        // retire fully claimed batches, then take the first of the highest priority
+        for (auto it = queue_.begin(); it != queue_.end();)
+          it = (*it)->next.load() >= (*it)->chunks ? queue_.erase(it) : std::next(it);
+        if (queue_.empty()) {
+          has_work_.store(false, std::memory_order_release);
           continue;
         }
+        b = queue_.front();
+        for (const auto& c : queue_)
+          if (c->prio > b->prio) {
+            b = c;
+            break;
+          }
       }
       work(*b);
     }
   }
   std::vector<std::thread> workers_;
   std::deque<std::shared_ptr<Batch>> queue_;
+  std::atomic<bool> has_work_{false};
   std::mutex m_;
   std::condition_variable cv_;
   bool stop_ = false;
@@ -200,9 +233,27 @@ uint32_t spread10(uint32_t x) {  // 10 bits -> every third bit
 // membership and triangle order are those of the sequential build (only the
 // internal node numbering differs; siblings stay adjacent).
 void build_bvh(const rlc_scene_desc& d, HostScene& out) {
+  PhaseTimer pt;
+  pt.on = std::getenv("RLC_BVH_TIMING") != nullptr;
   const uint32_t n = d.num_triangles;
-  std::vector<Box> tb(n);
-  std::vector<V3> cen(n);
+  // scratch kept per thread across builds (per-frame rebuilds touch no
+  // fresh pages)
+  // (local references: the worker threads' lambdas must see this thread's
+  // instances, not their own thread_local ones)
+  thread_local std::vector<Box> tl_tb;
+  thread_local std::vector<V3> tl_cen;
+  thread_local std::vector<double> tl_ckey[3];
+  thread_local std::vector<uint32_t> tl_perm;
+  std::vector<Box>& tb = tl_tb;
+  std::vector<V3>& cen = tl_cen;
+  // centroid coordinates per axis, contiguous: the nth_element comparator
+  // reads 8-byte keys instead of a strided V3 and an axis switch (the same
+  // doubles, so the same comparisons and the same permutation)
+  std::vector<double>(&ckey)[3] = tl_ckey;
+  tb.resize(n);
+  cen.resize(n);
+  for (auto& k : ckey) k.resize(n);
+  pt.lap("bvh scratch");
   parallel_for(n, [&](size_t i) {
     Box b;
     b.grow(vert(d, uint32_t(i), 0));
@@ -210,9 +261,14 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
     b.grow(vert(d, uint32_t(i), 2));
     tb[i] = b;
     cen[i] = b.center();
+    ckey[0][i] = cen[i].x;
+    ckey[1][i] = cen[i].y;
+    ckey[2][i] = cen[i].z;
   });
-  std::vector<uint32_t> perm(n);
+  std::vector<uint32_t>& perm = tl_perm;
+  perm.resize(n);
   std::iota(perm.begin(), perm.end(), 0u);
+  pt.lap("bvh centroids");
 
   struct Todo {
     uint32_t node, begin, end;
@@ -246,8 +302,9 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
       }
       const int axis = cb.longest_axis();
       const uint32_t mid = t.begin + count / 2;
+      const double* key = ckey[axis].data();
       std::nth_element(perm.begin() + t.begin, perm.begin() + mid, perm.begin() + t.end,
-                       [&](uint32_t x, uint32_t y) { return comp(cen[x], axis) < comp(cen[y], axis); });
+                       [key](uint32_t x, uint32_t y) { return key[x] < key[y]; });
       const uint32_t child = uint32_t(nodes.size());
       nodes.push_back(BvhNode{});
       nodes.push_back(BvhNode{});
@@ -309,8 +366,9 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
         }
         const int axis = cb.longest_axis();
         const uint32_t mid = t.begin + count / 2;
+        const double* key = ckey[axis].data();
         std::nth_element(perm.begin() + t.begin, perm.begin() + mid, perm.begin() + t.end,
-                         [&](uint32_t x, uint32_t y) { return comp(cen[x], axis) < comp(cen[y], axis); });
+                         [key](uint32_t x, uint32_t y) { return key[x] < key[y]; });
         split[k] = {mid, 0u, count};
       }, 1);
       std::vector<Todo> next;
@@ -329,25 +387,19 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
         }
       }
       level.swap(next);
+      pt.lap("bvh level");
     }
   }
   if (!deferred.empty()) {
     // subtrees in parallel, each into a private array whose element 0 is the
     // subtree root (a node already allocated in `nodes`)
     std::vector<std::vector<BvhNode>> local(deferred.size());
-    std::vector<std::future<void>> jobs;
-    std::atomic<size_t> next{0};
-    const unsigned nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    for (unsigned w = 0; w < nthreads; ++w)
-      jobs.push_back(std::async(std::launch::async, [&] {
-        for (size_t k; (k = next.fetch_add(1)) < deferred.size();) {
-          std::vector<BvhNode>& L = local[k];
-          L.reserve(size_t(2) * (deferred[k].end - deferred[k].begin));
-          L.push_back(BvhNode{});
-          build(L, 0, deferred[k].begin, deferred[k].end, 0, nullptr);
-        }
-      }));
-    for (auto& j : jobs) j.get();
+    parallel_for(deferred.size(), [&](size_t k) {  // on the persistent worker pool
+      std::vector<BvhNode>& L = local[k];
+      L.reserve(size_t(2) * (deferred[k].end - deferred[k].begin));
+      L.push_back(BvhNode{});
+      build(L, 0, deferred[k].begin, deferred[k].end, 0, nullptr);
+    }, 1);
     for (size_t k = 0; k < deferred.size(); ++k) {
       const std::vector<BvhNode>& L = local[k];
       const uint32_t base = uint32_t(nodes.size()) - 1;  // local index i >= 1 -> base + i
@@ -363,6 +415,7 @@ void build_bvh(const rlc_scene_desc& d, HostScene& out) {
       for (size_t i = 1; i < L.size(); ++i) nodes.push_back(remap(L[i]));
     }
   }
+  pt.lap("bvh subtrees");
   out.tris.resize(n);
   parallel_for(n, [&](size_t i) {
     const uint32_t id = perm[i];
@@ -837,9 +890,129 @@ void bin_levels(const std::vector<BvhNode>& bin, std::vector<uint32_t>& order,
   for (size_t k = 0; k < bin.size(); ++k) order[at[maxd - depth[k]]++] = uint32_t(k);
 }
 
-void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
+// Dynamic update, phase A (no reference BVH needed, so it runs beside its
+// build): the creation SAH topology refitted to the moved triangles (any
+// conservative tree is exact) -- shadow-order triangle
+// records, binary node boxes bottom up by levels (leaves from their
+// triangles' vertices, internal nodes from their children), every wide child
+// box padded by S 2^-21 and rounded outward, and the quantized nodes.
+// Leaf words keep the previous frame's kLeafPure bits until phase B.
+void refit_shadow_boxes(const rlc_scene_desc& d, HostScene& out, HostScene& keep) {
   PhaseTimer pt;
-  out.wide.clear();
+  double S = 0;  // = max |coordinate| of the reference BVH's root box
+  {
+    std::vector<double> part(64, 0.0);
+    const size_t nv = size_t(d.num_triangles) * 9;
+    parallel_for(64, [&](size_t c) {
+      double m = 0;
+      for (size_t i = nv * c / 64; i < nv * (c + 1) / 64; ++i) m = std::max(m, std::fabs(d.vertices[i]));
+      part[c] = m;
+    }, 1);
+    for (double m : part) S = std::max(S, m);
+  }
+  out.coord_bound = S;
+  const size_t nt = keep.tris_s.size();
+  out.tris_s = std::move(keep.tris_s);  // positions rewritten, triangle ids kept
+  parallel_for(nt, [&](size_t i) {
+    TriAccel& ta = out.tris_s[i];
+    const uint32_t id = ta.tri_id;
+    const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
+    put3(ta.p0, p0);
+    put3(ta.e1, p1 - p0);
+    put3(ta.e2, p2 - p0);
+  });
+  pt.lap("refit tris");
+  const auto& kids = out.wide_kids;  // the creation topology (moved into `out` by the caller)
+  const auto& bin = out.shadow_bin;
+  std::vector<double>& nb = out.refit_box;
+  nb = std::move(keep.refit_box);
+  nb.resize(6 * bin.size());
+  const auto& order = out.bin_order;
+  const auto& lstart = out.bin_level_start;
+  for (size_t l = 0; l + 1 < lstart.size(); ++l) {
+    const uint32_t l0 = lstart[l], l1 = lstart[l + 1];
+    parallel_for(l1 - l0, [&](size_t q) {
+      const uint32_t k = order[l0 + q];
+      const BvhNode& nd = bin[k];
+      Box bx;
+      if (nd.count > 0) {
+        for (uint32_t i = nd.a; i < nd.a + nd.count; ++i) {
+          const uint32_t id = out.tris_s[i].tri_id;
+          bx.grow(vert(d, id, 0));
+          bx.grow(vert(d, id, 1));
+          bx.grow(vert(d, id, 2));
+        }
+      } else {
+        for (const uint32_t ch : {nd.a, nd.b}) {
+          const double* c = &nb[6 * size_t(ch)];
+          bx.grow(V3{c[0], c[1], c[2]});
+          bx.grow(V3{c[3], c[4], c[5]});
+        }
+      }
+      double* o = &nb[6 * size_t(k)];
+      o[0] = bx.lo.x, o[1] = bx.lo.y, o[2] = bx.lo.z, o[3] = bx.hi.x, o[4] = bx.hi.y, o[5] = bx.hi.z;
+    }, 512);
+  }
+  pt.lap("refit boxes");
+  const double pad = S * 0x1.0p-21;
+  out.wide = std::move(keep.wide);  // rewritten in place: boxes (leaf bits in phase B)
+  parallel_for(kids.size(), [&](size_t w) {
+    Wide4& n = out.wide[w];
+    for (int c = 0; c < kWide; ++c) {
+      const uint32_t b = kids[w][c];
+      if (b == kWideEmpty) {
+        n.child[c] = kWideEmpty;
+        for (int a = 0; a < 3; ++a) {
+          n.lo[a][c] = HUGE_VALF;
+          n.hi[a][c] = -HUGE_VALF;
+        }
+        continue;
+      }
+      const double* bx = &nb[6 * size_t(b)];
+      for (int a = 0; a < 3; ++a) {  // as collapse_wide (no origin, no growth)
+        n.lo[a][c] = round_down(bx[a] - pad);
+        n.hi[a][c] = round_up(bx[3 + a] + pad);
+      }
+    }
+  }, 512);
+  pt.lap("wide refit");
+  const char* q = std::getenv("RLC_SHADOW_QUANT");
+  if (q && std::string(q) == "0") out.wide_q.clear();
+  else quantize_wide(out.wide, out.wide_q);
+  pt.lap("quantize");
+}
+
+// Phase B, after the reference BVH: the reference leaf of every shadow-order
+// triangle, and kLeafPure on the leaves whose triangles all lie in one
+// reference leaf (patched into the wide and the quantized nodes).
+void refit_shadow_leaves(HostScene& out) {
+  std::vector<uint32_t>& leaf_of_id = out.refit_leaf;  // scratch reused across updates
+  leaf_of_id.resize(out.tris.size());
+  parallel_for(out.tris.size(), [&](size_t j) { leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j]; });
+  const size_t nt = out.tris_s.size();
+  out.tri_leaf_s.resize(nt);
+  parallel_for(nt, [&](size_t i) { out.tri_leaf_s[i] = leaf_of_id[out.tris_s[i].tri_id]; });
+  const auto& kids = out.wide_kids;
+  const auto& bin = out.shadow_bin;
+  const bool quant = !out.wide_q.empty();
+  parallel_for(kids.size(), [&](size_t w) {
+    for (int c = 0; c < kWide; ++c) {
+      const uint32_t b = kids[w][c];
+      if (b == kWideEmpty) continue;
+      const BvhNode& bn = bin[b];
+      if (bn.count == 0) continue;  // internal: the creation numbering, already in place
+      bool pure = true;
+      for (uint32_t k = 1; k < bn.count; ++k) pure &= out.tri_leaf_s[bn.a + k] == out.tri_leaf_s[bn.a];
+      const uint32_t word = kWideLeaf | ((bn.count - 1) << 28) | (pure ? kLeafPure : 0u) | bn.a;
+      out.wide[w].child[c] = word;
+      if (quant) out.wide_q[w].child[c] = word;
+    }
+  }, 512);
+}
+
+void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep, bool refit) {
+  PhaseTimer pt;
+  if (!refit) out.wide.clear();  // (refit: the boxes of refit_shadow_boxes)
   out.wide_ref.clear();
   out.tri_leaf.assign(out.tris.size(), 0);
   parallel_for(out.nodes.size(), [&](size_t i) {
@@ -874,92 +1047,8 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
     out.tri_leaf_s = out.tri_leaf;
     out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
                              S * 0x1.0p-21);
-  } else if (keep != nullptr && !keep->shadow_bin.empty() && !keep->wide_kids.empty()) {
-    // dynamic update: the creation SAH topology refitted to the moved
-    // triangles (any conservative tree is exact): every wide
-    // child box is the union of its moved triangles' boxes (its tris_s
-    // range); leaves whose triangles now lie in different reference leaves
-    // lose kLeafPure
-    std::vector<uint32_t>& leaf_of_id = out.refit_leaf;  // scratch reused across updates
-    leaf_of_id = std::move(keep->refit_leaf);
-    leaf_of_id.resize(out.tris.size());
-    parallel_for(out.tris.size(), [&](size_t j) { leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j]; });
-    const size_t nt = keep->tris_s.size();
-    out.tris_s = std::move(keep->tris_s);  // positions and triangle ids kept; the
-    out.tri_leaf_s.resize(nt);             // vertices are rewritten below
-    parallel_for(nt, [&](size_t i) {
-      TriAccel& ta = out.tris_s[i];
-      const uint32_t id = ta.tri_id;
-      const V3 p0 = vert(d, id, 0), p1 = vert(d, id, 1), p2 = vert(d, id, 2);
-      put3(ta.p0, p0);
-      put3(ta.e1, p1 - p0);
-      put3(ta.e2, p2 - p0);
-      out.tri_leaf_s[i] = leaf_of_id[id];
-    });
-    pt.lap("refit tris");
-    const auto& kids = keep->wide_kids;
-    const auto& bin = keep->shadow_bin;
-    // binary node boxes bottom up, one level at a time (leaves from their
-    // triangles' vertices, internal nodes from their children): O(n) work
-    std::vector<double>& nb = out.refit_box;
-    nb = std::move(keep->refit_box);
-    nb.resize(6 * bin.size());
-    const auto& order = keep->bin_order;
-    const auto& lstart = keep->bin_level_start;
-    for (size_t l = 0; l + 1 < lstart.size(); ++l) {
-      const uint32_t l0 = lstart[l], l1 = lstart[l + 1];
-      parallel_for(l1 - l0, [&](size_t q) {
-        const uint32_t k = order[l0 + q];
-        const BvhNode& nd = bin[k];
-        Box bx;
-        if (nd.count > 0) {
-          for (uint32_t i = nd.a; i < nd.a + nd.count; ++i) {
-            const uint32_t id = out.tris_s[i].tri_id;
-            bx.grow(vert(d, id, 0));
-            bx.grow(vert(d, id, 1));
-            bx.grow(vert(d, id, 2));
-          }
-        } else {
-          for (const uint32_t ch : {nd.a, nd.b}) {
-            const double* c = &nb[6 * size_t(ch)];
-            bx.grow(V3{c[0], c[1], c[2]});
-            bx.grow(V3{c[3], c[4], c[5]});
-          }
-        }
-        double* o = &nb[6 * size_t(k)];
-        o[0] = bx.lo.x, o[1] = bx.lo.y, o[2] = bx.lo.z, o[3] = bx.hi.x, o[4] = bx.hi.y, o[5] = bx.hi.z;
-      }, 512);
-    }
-    pt.lap("refit boxes");
-    const double pad = S * 0x1.0p-21;
-    out.wide = std::move(keep->wide);  // rewritten in place: boxes and leaf bits
-    parallel_for(kids.size(), [&](size_t w) {
-      Wide4& n = out.wide[w];
-      for (int c = 0; c < kWide; ++c) {
-        const uint32_t b = kids[w][c];
-        if (b == kWideEmpty) {
-          n.child[c] = kWideEmpty;
-          for (int a = 0; a < 3; ++a) {
-            n.lo[a][c] = HUGE_VALF;
-            n.hi[a][c] = -HUGE_VALF;
-          }
-          continue;
-        }
-        const double* bx = &nb[6 * size_t(b)];
-        for (int a = 0; a < 3; ++a) {  // as collapse_wide (no origin, no growth)
-          n.lo[a][c] = round_down(bx[a] - pad);
-          n.hi[a][c] = round_up(bx[3 + a] + pad);
-        }
-        const BvhNode& bn = bin[b];
-        if (bn.count > 0) {
-          bool pure = true;
-          for (uint32_t k = 1; k < bn.count; ++k)
-            pure &= out.tri_leaf_s[bn.a + k] == out.tri_leaf_s[bn.a];
-          n.child[c] = kWideLeaf | ((bn.count - 1) << 28) | (pure ? kLeafPure : 0u) | bn.a;
-        }  // internal: the creation numbering, already in place
-      }
-    }, 512);
-    pt.lap("wide refit");
+  } else if (refit) {
+    refit_shadow_leaves(out);  // the boxes were refitted beside the reference BVH
   } else {
     std::vector<uint32_t> perm;
     out.tris_s.resize(out.tris.size());
@@ -976,6 +1065,7 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep) {
   }
   f_ref.get();
   pt.lap("wide_ref");
+  if (refit) return;  // quantized in refit_shadow_boxes, leaf bits patched above
   const char* q = std::getenv("RLC_SHADOW_QUANT");
   if (q && std::string(q) == "0") out.wide_q.clear();
   if (!(q && std::string(q) == "0")) quantize_wide(out.wide, out.wide_q);
@@ -1121,6 +1211,8 @@ void level_thresholds(double out[kMaxLevel + 1]) {
   }
 }
 
+void build_reference_bvh(const rlc_scene_desc& d, HostScene& out) { build_bvh(d, out); }
+
 void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, HostScene& out,
                       HostScene* keep) {
   PhaseTimer pt;
@@ -1165,12 +1257,34 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
          normalize(cross(vert(d, uint32_t(t), 1) - p0, vert(d, uint32_t(t), 2) - p0)));
   });
   pt.lap("normals");
+  // A dynamic update refits the creation shadow tree; its boxes do not
+  // depend on the reference BVH, so they are refitted beside its build.
+  const char* tree_env = std::getenv("RLC_SHADOW_TREE");
+  const bool refit = keep != nullptr && !keep->shadow_bin.empty() && !keep->wide_kids.empty() &&
+                     !(tree_env && (std::string(tree_env) == "reference" ||
+                                    std::string(tree_env) == "leaves"));
+  std::future<void> f_boxes;
+  if (refit) {
+    out.wide_kids = std::move(keep->wide_kids);
+    out.shadow_bin = std::move(keep->shadow_bin);
+    out.bin_first = std::move(keep->bin_first);
+    out.bin_end = std::move(keep->bin_end);
+    out.bin_order = std::move(keep->bin_order);
+    out.bin_level_start = std::move(keep->bin_level_start);
+    out.refit_leaf = std::move(keep->refit_leaf);
+    f_boxes = std::async(std::launch::async, [&] {
+      WorkerPool::priority() = 0;  // the reference BVH's loops go first
+      refit_shadow_boxes(d, out, *keep);
+    });
+  }
   build_bvh(d, out);  // render.cpp:145
   pt.lap("reference bvh");
+  if (refit) f_boxes.get();
+  pt.lap("refit join");
   // The rest depends only on the scene and the reference BVH and writes
   // disjoint parts of `out`: the traversal trees, the emitters and light
   // tree, and the camera-relative copies run concurrently.
-  auto f_wide = std::async(std::launch::async, [&] { build_wide(d, out, keep); });
+  auto f_wide = std::async(std::launch::async, [&] { build_wide(d, out, keep, refit); });
   auto f_emit = std::async(std::launch::async, [&] {
     if (keep == nullptr) {  // fp32 reference-tree copy: deferred closest-hit rays only
       out.nodes_f.resize(out.nodes.size());
@@ -1223,6 +1337,8 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
         if (out.mats[d.material_ids[t]].is_emitter) out.emitter_tri.push_back(t);
     }
     const size_t ne = out.emitter_tri.size();
+    out.emitter_mat.resize(ne);
+    for (size_t k = 0; k < ne; ++k) out.emitter_mat[k] = d.material_ids[out.emitter_tri[k]];
     out.lights.resize(ne);
     out.emitter_energy.resize(ne);
     out.emitter_centroid.resize(3 * ne);
@@ -1303,7 +1419,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
     out.lt_nodes = std::move(keep->lt_nodes);
     out.lt_begin = std::move(keep->lt_begin);
     out.lt_energy = std::move(keep->lt_energy);
-    if (out.wide_kids.empty() && !keep->wide_kids.empty()) {  // refitted, not rebuilt
+    if (!refit && out.wide_kids.empty() && !keep->wide_kids.empty()) {  // refitted, not rebuilt
       out.shadow_bin = std::move(keep->shadow_bin);
       out.wide_kids = std::move(keep->wide_kids);
       out.bin_first = std::move(keep->bin_first);

@@ -58,6 +58,7 @@ struct HostScene {
   // emitters + light tree (light_tree.cpp:30-119)
   std::vector<LightRec> lights;          // by emitter index
   std::vector<uint32_t> emitter_tri;     // emitter index -> triangle id
+  std::vector<uint32_t> emitter_mat;     // emitter index -> material id
   std::vector<double> emitter_energy;    // luminance(emission) * area
   std::vector<double> emitter_centroid;  // [3] per emitter
   std::vector<uint32_t> order;           // sorted position -> emitter index
@@ -77,6 +78,9 @@ struct HostScene {
 // replaced) and the shadow tree refitted instead of rebuilt; the fp32 copies
 // of the reference tree that only deferred closest-hit rays use are not
 // built (the device then runs those rays on the fp64 reference tree).
+// The reference scene BVH alone (build_scene_bvh, bvh.cpp:64-122) into
+// out.nodes / out.tris (diagnostics: rlc_debug_host_bvh times it).
+void build_reference_bvh(const rlc_scene_desc& d, HostScene& out);
 void build_host_scene(const rlc_scene_desc& desc, const rlc_render_config& cfg, HostScene& out,
                       HostScene* keep = nullptr);
 

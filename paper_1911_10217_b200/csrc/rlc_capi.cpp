@@ -270,6 +270,17 @@ struct rlc_context {
   rlc::DevScene dev{};
   rlc_render_config create_cfg{};  // build_context's config (rlc_context_update_scene)
   SceneBuffers scene_bufs;  // the device scene (upload_scene)
+  DeviceArena lights_ord_arena;  // dev.lights_ord, rebuilt on the device after every upload
+  size_t lights_ord_cap = 0;
+  void build_light_order() {
+    if (dev.num_lights > lights_ord_cap) {
+      lights_ord_arena.release();
+      dev.lights_ord = lights_ord_arena.alloc<rlc::LightOrd>(dev.num_lights);
+      lights_ord_cap = dev.num_lights;
+    }
+    rlc::launch_light_order(dev, const_cast<rlc::LightOrd*>(dev.lights_ord), stream);
+    RLC_CK(cudaGetLastError());
+  }
   DeviceArena arena;
   unsigned long long* counters = nullptr;  // error bits for grid-less passes
   // primary rays of the next pass overlap the tail of the current one: they
@@ -716,6 +727,7 @@ void upload_scene(const rlc::HostScene& h, SceneBuffers& A, rlc::DevScene& d, cu
   d.order = A.put(h.order, !update);
   d.lt = A.put(h.lt_nodes, !update);
   d.energy_cdf = A.put(h.energy_cdf);
+  d.emitter_mat = A.put(h.emitter_mat, !update);
   d.emitter_energy = A.put(h.emitter_energy);
   d.num_lights = uint32_t(h.lights.size());
   d.num_tris = uint32_t(h.tri_mat.size());
@@ -779,6 +791,7 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     upload_scene(ctx->host, ctx->scene_bufs, ctx->dev, ctx->stream);
+    ctx->build_light_order();
     ctx->counters = ctx->arena.alloc<unsigned long long>(rlc::kCntNum);
     RLC_CK(cudaMemsetAsync(ctx->counters, 0, sizeof(unsigned long long) * rlc::kCntNum, ctx->stream));
     RLC_CK(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking));
@@ -841,11 +854,13 @@ rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scen
     lap("sync");
     rlc::DevScene d{};
     d.count_work = ctx->dev.count_work;
+    d.lights_ord = ctx->dev.lights_ord;
     upload_scene(h, ctx->scene_bufs, d, ctx->stream, true);
+    ctx->dev = d;
+    ctx->build_light_order();
     // the copies complete before the host buffers are reused or freed and
     // before any stream reads the new scene
     RLC_CK(cudaStreamSynchronize(ctx->stream));
-    ctx->dev = d;
     ctx->host = std::move(h);
     ++ctx->scene_gen;  // captured pass graphs hold the old scene's pointers
     lap("upload");
@@ -961,6 +976,22 @@ rlc_status rlc_context_count_work(rlc_context* ctx, int enable) {
     require(ctx != nullptr, "rlc_context_count_work: null context");
     ctx->dev.count_work = enable ? 1u : 0u;
     ++ctx->scene_gen;  // captured pass graphs hold the old kernel choice
+  });
+}
+
+rlc_status rlc_debug_host_bvh(const rlc_scene_desc* scene, uint32_t reps, double* ms_out,
+                              uint32_t* nodes_out) {
+  return guarded([&] {
+    require(scene != nullptr && ms_out != nullptr && reps > 0, "rlc_debug_host_bvh: bad argument");
+    rlc::HostScene h;
+    double total = 0;
+    for (uint32_t r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      rlc::build_reference_bvh(*scene, h);
+      total += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    *ms_out = total / reps;
+    if (nodes_out) *nodes_out = uint32_t(h.nodes.size());
   });
 }
 

@@ -152,6 +152,18 @@ struct alignas(128) LightRec {
   double pdf_area;     // 1 / triangle_area
 };
 
+// An emitter at its light-tree position (tree.order[pos], light_tree.hpp):
+// the learned sampler's pick reads one line instead of order[] then the
+// record.  Built on the device from LightRec and order (k_light_order).
+struct alignas(128) LightOrd {
+  double p0[3], p1[3], p2[3];
+  double n[3];
+  double pdf_area;
+  uint32_t mat;      // material (emission)
+  uint32_t emitter;  // emitter index (tree.order[pos])
+  double pad[2];
+};
+
 // Material flags precomputed with the reference predicates.
 struct alignas(16) MatRec {
   double albedo[3];

@@ -46,7 +46,7 @@ struct alignas(16) GBuf {  // 64 B per path vertex
   double pos[3];
   double ns[3];
   uint64_t rng;
-  uint32_t slot;
+  uint32_t cell;   // dense cell id of the vertex's lookup, or kPending / kFallback / kNoSlot
   uint32_t flags;
 };
 
@@ -93,6 +93,8 @@ struct DevScene {
   const uint32_t* tri_mat;
   const double* tri_normal;
   const LightRec* lights;
+  const LightOrd* lights_ord;  // emitters in light-tree order (order[] folded in)
+  const uint32_t* emitter_mat; // material id per emitter (emission of lights_ord)
   const uint32_t* order;
   const LtNode* lt;
   const double* energy_cdf;
@@ -285,6 +287,8 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
                             double tmin, double* t_out, int32_t* tri_out,
                             unsigned long long* counters, cudaStream_t st, bool sah_only = false);
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
+// sc.lights_ord from sc.lights, sc.order and sc.emitter_mat.
+void launch_light_order(const DevScene& sc, LightOrd* out, cudaStream_t st);
 // Per-vertex parity records of the pass in `p` (rlc_pass_samples).
 void launch_export_samples(const PassParams& p, const PassBuffers& b, SampleExport* out,
                            cudaStream_t st);
