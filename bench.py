@@ -305,13 +305,18 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             rlcuts.render_pass(ctx, cfg, p, grid, fb, sync=False)
             rlcuts.end_of_pass_update(grid, ctx, cfg.cut, sync=False)
     else:
-        # screen bands with the exact record exchange over NCCL
+        # screen bands with the exact record exchange: over the
+        # C++ NCCL data plane (one rlc_shard_frame call per frame, owner-folded
+        # cells, no host synchronization), or over gloo with host staging
         from paper_1911_10217_b200 import dist as rdist
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.Stream()
         ctx.set_stream(stream.cuda_stream)
-        frame = rdist.ShardedFrame(rdist.GpuEngine(ctx, grid, fb, cfg,
-                                                   torch.device("cuda", local_rank)),
-                                   H, rank, world, host_staging=args.dist_backend == "gloo")
+        eng = rdist.GpuEngine(ctx, grid, fb, cfg, torch.device("cuda", local_rank), world=world)
+        if args.dist_backend == "nccl":
+            frame = rdist.NcclFrame(eng, H, rank, world, local_rank, owner=not args.replicated_fold)
+        else:
+            frame = rdist.ShardedFrame(eng, H, rank, world, host_staging=True,
+                                       owner=not args.replicated_fold)
         r0, r1 = frame.rows
 
         def step(p):
@@ -493,7 +498,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "frames_timed": args.steps,
                        "l2": "no flush: resident scene+cut+pass buffers exceed the 126 MB L2",
                        "parallelism": (f"screen bands x{world}, exact update-record all-gather "
-                                       f"over {args.dist_backend}" if world > 1 else "single GPU"),
+                                       f"over {args.dist_backend}, "
+                                       f"{'replicated' if args.replicated_fold else 'owner'}-folded"
+                                       if world > 1 else "single GPU"),
                        "cells": st["occupied"], "fallback_hits": st["fallback_hits"],
                        **grid_insert_stats},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -522,6 +529,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: bound on the timed host time")
+    ap.add_argument("--replicated-fold", action="store_true",
+                    help="N > 1: every rank folds every record (default: the cell's owner folds)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo stages the record exchange through host memory (functional "
                          "multi-rank runs with fewer GPUs than ranks)")

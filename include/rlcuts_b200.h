@@ -177,11 +177,13 @@ rlc_status rlc_context_synchronize(rlc_context* ctx);
 /* Per-stage device timing with CUDA events on the context stream (bench
  * evidence).  Stages: 0 primary, 1 sample, 2 sort, 3 fold, 4 accumulate,
  * 5 split-collapse, 6 shadow (any-hit traversal), 7 insert (the pass's new
- * hash-grid keys, in canonical order), 8 ray compaction.  Stage 0 includes the
+ * hash-grid keys, in canonical order), 8 ray compaction, 9 the sharded fold's
+ * gather of all ranks' records and key insertion (stage 3 of a sharded pass:
+ * its sort and update_q).  Stage 0 includes the
  * bounce rays of max_depth > 1.  rlc_context_stage_times synchronizes,
  * returns accumulated milliseconds and launch counts per stage since the
  * last call, and resets them. */
-#define RLC_NUM_STAGES 9
+#define RLC_NUM_STAGES 10
 rlc_status rlc_context_enable_timing(rlc_context* ctx, int enable);
 rlc_status rlc_context_stage_times(rlc_context* ctx, double* ms, uint32_t* counts);
 /* The timeline behind rlc_context_stage_times (call it first): per stage
@@ -307,7 +309,7 @@ rlc_status rlc_render_passes_async(const rlc_context* ctx, const rlc_render_conf
 rlc_status rlc_end_of_pass_update_async(rlc_grid* grid, const rlc_context* ctx,
                                         const rlc_cut_config* cut);
 rlc_status rlc_grid_last_changes(const rlc_grid* grid, uint32_t* changes);
-/* ---- screen-band sharding with an exact exchange --
+/* ---- screen-band sharding: the exchanged update record ------------------
  * One learned update (the update_q call of render.cpp:111-117) as exchanged
  * between ranks: the cell key, the cluster and the feedback value.  32 B. */
 typedef struct rlc_update_record {
@@ -315,21 +317,52 @@ typedef struct rlc_update_record {
   uint32_t qn, level, cluster;
   double v;
 } rlc_update_record;
-/* Traces rows [row_begin, row_end) of pass `pass_index` (primary rays, cut
- * samples, shadow rays) without applying updates.  *records receives a
- * device pointer to the band's update records in canonical order and
- * *count their number; valid until the next call on this context. */
-rlc_status rlc_pass_trace(const rlc_context* ctx, const rlc_render_config* config,
-                          uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
-                          uint32_t row_end, const void** records, uint64_t* count);
-/* Folds the update records of all ranks (device memory: rank k's counts[k]
- * records at all_records + k*stride, ranks owning consecutive row bands in
- * rank order), inserting foreign cells, then accumulates this rank's band
- * (traced by the preceding rlc_pass_trace) into fb.  Every rank ends with
- * the learned state a single render_pass over all rows produces. */
-rlc_status rlc_pass_fold(const rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
-                         rlc_framebuffer* fb, const void* all_records, const uint64_t* counts,
-                         uint32_t nranks, uint32_t rank, uint64_t stride);
+/* ---- sharded frames (multi-GPU) -------------------
+ * Rank `rank` of `nranks` renders rows [row_begin, row_end) of a pass; the
+ * bands are consecutive in rank order.  The learned state stays identical
+ * on every rank and equal to a single render_pass over all rows.  All calls
+ * enqueue on the context stream and return without a host synchronization.
+ *
+ * 1. rlc_shard_trace: traces the band and files its update records in
+ *    canonical order into a device block of *block_bytes (a 16-byte header
+ *    with the count, then `cap_records` 32-byte slots; cap_records >= the
+ *    band's path vertices, the same on every rank).
+ * 2. the caller all-gathers the blocks of all ranks, rank-major (NCCL
+ *    ncclAllGather of block_bytes, or any transport);
+ * 3. rlc_shard_fold: inserts the pass's new keys in canonical order and
+ *    folds, in canonical order per cut entry, the records of every cell
+ *    (owner_fold = 0) or of the cells this rank owns (hash(CellKey) % nranks
+ *    == rank); *q_before_slots (device, *slots doubles) holds q_before per
+ *    record slot, zero for the records other ranks fold;
+ * 4. owner_fold: the caller sums q_before_slots over the ranks (ncclAllReduce);
+ * 5. rlc_shard_finish: replays the other ranks' records onto this rank's
+ *    cut entries (owner_fold) and accumulates the band's radiance;
+ * 6. rlc_end_of_pass_update(_async): split-collapse, identical on every rank.
+ * rlc_shard_frame does 1-6 with NCCL on the context stream (one call per
+ * frame per rank, no host synchronization; errors surface at the next
+ * synchronizing call, e.g. rlc_shard_sync). */
+typedef struct rlc_comm rlc_comm;
+rlc_status rlc_shard_trace(const rlc_context* ctx, const rlc_render_config* config,
+                           uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
+                           uint32_t row_end, uint64_t cap_records, void** block,
+                           uint64_t* block_bytes);
+rlc_status rlc_shard_fold(const rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
+                          const void* blocks, uint32_t nranks, uint32_t rank, int owner_fold,
+                          double** q_before_slots, uint64_t* slots);
+rlc_status rlc_shard_finish(const rlc_context* ctx, rlc_grid* grid, rlc_framebuffer* fb,
+                            uint32_t rank, int owner_fold);
+/* Waits for the context's work and reports device errors of the grid. */
+rlc_status rlc_shard_sync(const rlc_context* ctx, rlc_grid* grid);
+/* NCCL communicator of a rank (libnccl.so.2 loaded on first use): id128 is
+ * ncclGetUniqueId's 128 bytes from rank 0, shared by the caller. */
+rlc_status rlc_comm_unique_id(uint8_t* id128);
+rlc_status rlc_comm_create(int device, uint32_t nranks, uint32_t rank, const uint8_t* id128,
+                           rlc_comm** out);
+rlc_status rlc_comm_destroy(rlc_comm* comm);
+rlc_status rlc_shard_frame(const rlc_context* ctx, const rlc_render_config* config,
+                           uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb,
+                           rlc_comm* comm, uint32_t row_begin, uint32_t row_end,
+                           uint64_t cap_records, int owner_fold);
 
 /* ---- per-sample parity export (SURVEY 8(b) "opt-in per-sample record
  * dump") ---------------------------------------------------------------

@@ -127,10 +127,17 @@ SIGNATURES = {
     "rlc_render_pass_async": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, _P]),
     "rlc_end_of_pass_update_async": (C.c_int, [_P, _P, C.POINTER(CutConfigC)]),
     "rlc_grid_last_changes": (C.c_int, [_P, _u32p]),
-    "rlc_pass_trace": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, C.c_uint32,
-                                 C.c_uint32, C.POINTER(C.c_void_p), _u64p]),
-    "rlc_pass_fold": (C.c_int, [_P, C.POINTER(RenderConfigC), _P, _P, _P, _u64p, C.c_uint32,
-                                C.c_uint32, C.c_uint64]),
+    "rlc_shard_trace": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, C.c_uint32,
+                                  C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), _u64p]),
+    "rlc_shard_fold": (C.c_int, [_P, C.POINTER(RenderConfigC), _P, _P, C.c_uint32, C.c_uint32,
+                                 C.c_int, C.POINTER(C.c_void_p), _u64p]),
+    "rlc_shard_finish": (C.c_int, [_P, _P, _P, C.c_uint32, C.c_int]),
+    "rlc_shard_sync": (C.c_int, [_P, _P]),
+    "rlc_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "rlc_comm_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8), _PP]),
+    "rlc_comm_destroy": (C.c_int, [_P]),
+    "rlc_shard_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, _P, _P, C.c_uint32,
+                                  C.c_uint32, C.c_uint64, C.c_int]),
     "rlc_render_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.POINTER(RenderResultC)]),
     "rlc_context_enable_sample_export": (C.c_int, [_P, C.c_int]),
     "rlc_pass_samples": (C.c_int, [_P, C.c_uint64, C.c_void_p, _u64p]),

@@ -3,6 +3,8 @@
 // and the per-pass launch sequence.  There is no CPU fallback: without an
 // sm_100 device every create call fails with RLC_ERR_NO_DEVICE.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <atomic>
 #include <chrono>
@@ -374,30 +376,51 @@ struct rlc_context {
       if (e) cudaEventDestroy(e);
     if (pstream) cudaStreamDestroy(pstream);
   }
-  // sharded pass state (rlc_pass_trace -> rlc_pass_fold)
+  // sharded pass state (rlc_shard_trace -> rlc_shard_fold -> rlc_shard_finish)
   PassParamsHolder shard;
+  bool shard_folded = false;
   DeviceArena xarena;
   rlc::ExchangeBuffers xb{};
-  unsigned long long* d_counts = nullptr;
-  uint32_t d_counts_cap = 0;
-  void ensure_exchange(uint32_t total, uint32_t nranks) {
-    if (total <= xb.cap && nranks <= d_counts_cap) return;
-    RLC_CK(cudaStreamSynchronize(stream));
-    xarena.release();
-    const uint32_t cap = total > xb.cap ? total : xb.cap;
-    const uint32_t nr = nranks > d_counts_cap ? nranks : d_counts_cap;
-    xb.contig = xarena.alloc<rlc::UpdateRecord>(cap);
-    xb.slots = xarena.alloc<uint32_t>(cap);
-    xb.keys = xarena.alloc<uint32_t>(cap);
-    xb.vals = xarena.alloc<uint32_t>(cap);
-    xb.keys_alt = xarena.alloc<uint32_t>(cap);
-    xb.vals_alt = xarena.alloc<uint32_t>(cap);
-    xb.hist = xarena.alloc<uint32_t>((size_t(cap) / 1024 + 2) * 256);  // sort tile: 1024 keys
-    xb.q_rec = xarena.alloc<double>(cap);
-    xb.nk = alloc_new_keys(xarena, cap, stream);
+  // sharded passes (rlc_shard_*): this rank's record block and the buffers
+  // of the fold over nranks x cap gathered record slots
+  DeviceArena blockarena;
+  void* block = nullptr;
+  uint64_t block_cap = 0;  // record slots of `block`
+  uint64_t xb_slots = 0, xb_entries = 0;
+  void ensure_block(uint64_t cap) {
+    if (cap <= block_cap && block) return;
+    sync_all();
+    blockarena.release();
+    block = blockarena.alloc<unsigned char>(sizeof(rlc::RecordBlockHeader) + cap * 32);
+    block_cap = cap;
+  }
+  void ensure_exchange(uint32_t nranks, uint32_t cap, uint64_t entries) {
+    const uint64_t slots = uint64_t(nranks) * cap;
+    xb.nranks = nranks;
     xb.cap = cap;
-    d_counts = xarena.alloc<unsigned long long>(nr);
-    d_counts_cap = nr;
+    if (slots <= xb_slots && entries <= xb_entries) return;
+    sync_all();
+    xarena.release();
+    const uint64_t n = std::max(slots, xb_slots), m = std::max(entries, xb_entries);
+    xb.contig = xarena.alloc<rlc::UpdateRecord>(n);
+    xb.slots = xarena.alloc<uint32_t>(n);
+    xb.cellx = xarena.alloc<uint32_t>(n);
+    xb.kflag = xarena.alloc<uint8_t>(n);
+    xb.keys = xarena.alloc<uint32_t>(n);
+    xb.vals = xarena.alloc<uint32_t>(n);
+    xb.keys_alt = xarena.alloc<uint32_t>(n);
+    xb.vals_alt = xarena.alloc<uint32_t>(n);
+    xb.hist = xarena.alloc<uint32_t>((size_t(n) / 1024 + 2) * 256);  // sort tile: 1024 keys
+    xb.block_counts = xarena.alloc<uint32_t>(n / 2048 + 2);
+    xb.sort_count = xarena.alloc<unsigned int>(2);
+    xb.q_rec = xarena.alloc<double>(n);
+    xb.seg_count = xarena.alloc<uint32_t>(m);
+    xb.seg_last = xarena.alloc<uint32_t>(m);
+    RLC_CK(cudaMemsetAsync(xb.seg_count, 0, 4 * m, stream));
+    RLC_CK(cudaMemsetAsync(xb.seg_last, 0, 4 * m, stream));
+    xb.nk = alloc_new_keys(xarena, n, stream);
+    xb_slots = n;
+    xb_entries = m;
   }
   // render_frame cache (prepare_frame_cache)
   rlc_grid* frame_grid = nullptr;
@@ -430,7 +453,6 @@ struct rlc_context {
   void* h_stage = nullptr;
   size_t h_stage_cap = 0;
   uint32_t* d_changes = nullptr;  // device change count of graph replays
-  rlc::UpdateRecord* rec_out = nullptr;  // this rank's exported update records
   // rlc_pass_samples: the last pass's parameters and G-buffer slot
   bool export_samples = false;
   rlc::PassParams last_pass{};
@@ -467,7 +489,6 @@ struct rlc_context {
     pb.ray_order = scratch.alloc<uint32_t>(cap);
     pb.rec_path = scratch.alloc<uint32_t>(cap);
     pb.rec_count = scratch.alloc<unsigned int>(2);
-    rec_out = scratch.alloc<rlc::UpdateRecord>(cap);
     pb.block_counts = scratch.alloc<uint32_t>(cap / 2048 + 2);
     pb.block_counts2 = scratch.alloc<uint32_t>(cap / 2048 + 2);
     pb.sort_count = scratch.alloc<unsigned int>(2);
@@ -625,7 +646,7 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   // on c3).  The any-hit result does not depend on the order.
   *k = nullptr;
   *v = nullptr;
-  if (rl) {
+  if (rl && !S.p.defer_insert) {  // (a sharded trace sorts all ranks' records in rlc_shard_fold)
     RLC_CK(cudaEventRecord(ctx->ev_sample_done, st));
     RLC_CK(cudaStreamWaitEvent(ctx->sstream, ctx->ev_sample_done, 0));
     ctx->stage_on(ctx->sstream, 2, [&] {
@@ -637,7 +658,7 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   ctx->stage(6, [&] {
     rlc::launch_shadow(ctx->dev, ctx->pb, ctx->pb.ray_order, S.g.counters, st, rl);
   });
-  if (rl) RLC_CK(cudaStreamWaitEvent(st, ctx->ev_sort_done, 0));
+  if (rl && !S.p.defer_insert) RLC_CK(cudaStreamWaitEvent(st, ctx->ev_sort_done, 0));
 }
 
 // render_pass body (proj/src/render.cpp:159-183) for rows [r0, r1).
@@ -1379,71 +1400,226 @@ rlc_status rlc_render_pass_async(const rlc_context* ctx, const rlc_render_config
   });
 }
 
-rlc_status rlc_pass_trace(const rlc_context* cctx, const rlc_render_config* config,
-                          uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
-                          uint32_t row_end, const void** records, uint64_t* count) {
-  return guarded([&] {
-    require(cctx != nullptr && config != nullptr && records != nullptr && count != nullptr,
-            "rlc_pass_trace: null argument");
-    require(config->sampler == RLC_SAMPLER_RL_LIGHTCUTS && grid != nullptr,
-            "rlc_pass_trace: the sharded pass is the learned sampler's");
-    rlc_context* ctx = const_cast<rlc_context*>(cctx);
-    RLC_CK(cudaSetDevice(ctx->device));
-    PassSetup S = setup_pass(ctx, config, pass_index, grid, nullptr, false, row_begin, row_end);
-    S.p.defer_insert = 1;  // new keys go in with all ranks' records (rlc_pass_fold)
-    ctx->shard = PassParamsHolder{S.p, S.g, S.n, S.nv, grid, true};
-    *records = ctx->rec_out;
-    *count = 0;
-    if (S.nv == 0) return;
+namespace {
+
+void shard_trace(rlc_context* ctx, const rlc_render_config* config, uint32_t pass_index,
+                 rlc_grid* grid, uint32_t row_begin, uint32_t row_end, uint64_t cap) {
+  require(config->sampler == RLC_SAMPLER_RL_LIGHTCUTS && grid != nullptr,
+          "rlc_shard_trace: the sharded pass is the learned sampler's");
+  require(cap > 0 && cap < (1ull << 31), "rlc_shard_trace: bad record capacity");
+  RLC_CK(cudaSetDevice(ctx->device));
+  PassSetup S = setup_pass(ctx, config, pass_index, grid, nullptr, false, row_begin, row_end);
+  require(S.nv <= cap, "rlc_shard_trace: the band has more path vertices than the record capacity");
+  S.p.defer_insert = 1;  // new keys go in with all ranks' records (rlc_shard_fold)
+  ctx->shard = PassParamsHolder{S.p, S.g, S.n, S.nv, grid, true};
+  ctx->shard_folded = false;
+  ctx->ensure_block(cap);
+  if (S.nv > 0) {
     uint32_t *k, *v;
     enqueue_trace(ctx, S, grid, &k, &v);
-    ctx->last_pass = S.p;
-    ctx->last_pb = ctx->pb;
-    ctx->last_valid = true;
-    rlc::launch_export_records(S.g, ctx->pb, S.nv, ctx->rec_out, ctx->stream);
-    unsigned int c = 0;
-    RLC_CK(cudaMemcpyAsync(&c, ctx->pb.rec_count, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    finish_sync(ctx, grid);
-    *count = c;
+  }
+  ctx->last_pass = S.p;
+  ctx->last_pb = ctx->pb;
+  ctx->last_valid = true;
+  rlc::launch_export_block(S.g, ctx->pb, S.nv, ctx->block, uint32_t(cap), ctx->stream);
+  RLC_CK(cudaGetLastError());
+}
+
+void shard_fold(rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
+                const void* blocks, uint32_t nranks, uint32_t rank, int owner_fold) {
+  require(nranks > 0 && rank < nranks, "rlc_shard_fold: bad rank");
+  require(ctx->shard.valid && ctx->shard.grid == grid && !ctx->shard_folded,
+          "rlc_shard_fold: no matching rlc_shard_trace on this grid");
+  require(blocks != nullptr, "rlc_shard_fold: null blocks");
+  (void)config;
+  RLC_CK(cudaSetDevice(ctx->device));
+  const PassParamsHolder& S = ctx->shard;
+  ctx->ensure_exchange(nranks, uint32_t(ctx->block_cap), uint64_t(grid->dev.capacity) * grid->dev.M);
+  ctx->stage(9, [&] {
+    rlc::launch_shard_fold(S.g, S.p, blocks, sizeof(rlc::RecordBlockHeader) + ctx->block_cap * 32,
+                           rank, owner_fold != 0, grid->key_bits, ctx->xb, ctx->stream);
+  });
+  ctx->stage(3, [&] {
+    rlc::launch_shard_sortfold(S.g, S.p, grid->key_bits, ctx->xb, ctx->stream);
+  });
+  ctx->shard_folded = true;
+  RLC_CK(cudaGetLastError());
+}
+
+void shard_finish(rlc_context* ctx, rlc_grid* grid, rlc_framebuffer* fb, uint32_t rank,
+                  int owner_fold) {
+  require(ctx->shard.valid && ctx->shard.grid == grid && ctx->shard_folded,
+          "rlc_shard_finish: no matching rlc_shard_fold on this grid");
+  require(fb != nullptr && fb->width == ctx->host.cam.width && fb->height == ctx->host.cam.height,
+          "render_pass: framebuffer size must match the camera");
+  RLC_CK(cudaSetDevice(ctx->device));
+  const PassParamsHolder S = ctx->shard;
+  ctx->shard.valid = false;
+  cudaStream_t st = ctx->stream;
+  if (owner_fold) ctx->stage(3, [&] { rlc::launch_shard_apply(S.g, S.p, ctx->xb, st); });
+  rlc::launch_shard_scatter(S.g, ctx->pb, S.nv, rank, ctx->xb, st);
+  if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
+  RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));
+  RLC_CK(cudaGetLastError());
+}
+
+}  // namespace
+
+rlc_status rlc_shard_trace(const rlc_context* cctx, const rlc_render_config* config,
+                           uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
+                           uint32_t row_end, uint64_t cap_records, void** block,
+                           uint64_t* block_bytes) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr && block != nullptr && block_bytes != nullptr,
+            "rlc_shard_trace: null argument");
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
+    *block = ctx->block;
+    *block_bytes = sizeof(rlc::RecordBlockHeader) + ctx->block_cap * 32;
   });
 }
 
-rlc_status rlc_pass_fold(const rlc_context* cctx, const rlc_render_config* config,
-                         rlc_grid* grid, rlc_framebuffer* fb, const void* all_records,
-                         const uint64_t* counts, uint32_t nranks, uint32_t rank,
-                         uint64_t stride) {
+rlc_status rlc_shard_fold(const rlc_context* cctx, const rlc_render_config* config,
+                          rlc_grid* grid, const void* blocks, uint32_t nranks, uint32_t rank,
+                          int owner_fold, double** q_before_slots, uint64_t* slots) {
   return guarded([&] {
-    require(cctx != nullptr && config != nullptr && counts != nullptr && nranks > 0 &&
-                rank < nranks, "rlc_pass_fold: bad argument");
+    require(cctx != nullptr && config != nullptr, "rlc_shard_fold: null argument");
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
-    require(ctx->shard.valid && ctx->shard.grid == grid,
-            "rlc_pass_fold: no matching rlc_pass_trace on this grid");
-    require(fb != nullptr && fb->width == ctx->host.cam.width && fb->height == ctx->host.cam.height,
-            "render_pass: framebuffer size must match the camera");
-    RLC_CK(cudaSetDevice(ctx->device));
-    uint64_t total = 0, own_offset = 0;
-    for (uint32_t r = 0; r < nranks; ++r) {
-      require(counts[r] <= stride, "rlc_pass_fold: count exceeds the per-rank stride");
-      if (r < rank) own_offset += counts[r];
-      total += counts[r];
+    shard_fold(ctx, config, grid, blocks, nranks, rank, owner_fold);
+    if (q_before_slots) *q_before_slots = ctx->xb.q_rec;
+    if (slots) *slots = uint64_t(nranks) * ctx->block_cap;
+  });
+}
+
+rlc_status rlc_shard_finish(const rlc_context* cctx, rlc_grid* grid, rlc_framebuffer* fb,
+                            uint32_t rank, int owner_fold) {
+  return guarded([&] {
+    require(cctx != nullptr, "rlc_shard_finish: null argument");
+    shard_finish(const_cast<rlc_context*>(cctx), grid, fb, rank, owner_fold);
+  });
+}
+
+rlc_status rlc_shard_sync(const rlc_context* cctx, rlc_grid* grid) {
+  return guarded([&] {
+    require(cctx != nullptr, "rlc_shard_sync: null argument");
+    finish_sync(cctx, grid);
+  });
+}
+
+// ---- NCCL data plane of sharded frames -----------------------------------
+// libnccl is loaded at the first communicator (dlopen of the soname torch
+// also uses, so one process shares one NCCL): single-GPU use needs no NCCL.
+namespace {
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    return a;
+  }();
+  if (!api.init_rank || !api.all_gather || !api.all_reduce)
+    throw std::runtime_error("rlcuts_b200: libnccl.so.2 could not be loaded (multi-GPU frames)");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw std::runtime_error(std::string(what) + ": " +
+                             (nccl().error_string ? nccl().error_string(r) : "NCCL error"));
+}
+}  // namespace
+
+struct rlc_comm {
+  ncclComm_t comm = nullptr;
+  uint32_t nranks = 1, rank = 0;
+  int device = 0;
+  DeviceArena arena;
+  void* gathered = nullptr;  // nranks record blocks
+  uint64_t gathered_bytes = 0;
+  ~rlc_comm() {
+    if (comm) nccl().destroy(comm);
+  }
+};
+
+rlc_status rlc_comm_unique_id(uint8_t* id128) {
+  return guarded([&] {
+    require(id128 != nullptr, "rlc_comm_unique_id: null argument");
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+rlc_status rlc_comm_create(int device, uint32_t nranks, uint32_t rank, const uint8_t* id128,
+                           rlc_comm** out) {
+  return guarded([&] {
+    require(id128 != nullptr && out != nullptr && nranks > 0 && rank < nranks,
+            "rlc_comm_create: bad argument");
+    *out = nullptr;
+    check_device(device);
+    auto c = std::make_unique<rlc_comm>();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    nccl_check(nccl().init_rank(&c->comm, int(nranks), id, int(rank)), "ncclCommInitRank");
+    *out = c.release();
+  });
+}
+
+rlc_status rlc_comm_destroy(rlc_comm* comm) {
+  return guarded([&] { delete comm; });
+}
+
+rlc_status rlc_shard_frame(const rlc_context* cctx, const rlc_render_config* config,
+                           uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb,
+                           rlc_comm* comm, uint32_t row_begin, uint32_t row_end,
+                           uint64_t cap_records, int owner_fold) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr && comm != nullptr && grid != nullptr,
+            "rlc_shard_frame: null argument");
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    require(comm->device == ctx->device, "rlc_shard_frame: communicator on another device");
+    shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
+    const uint64_t bb = sizeof(rlc::RecordBlockHeader) + ctx->block_cap * 32;
+    if (comm->gathered_bytes < bb * comm->nranks) {
+      ctx->sync_all();
+      comm->arena.release();
+      comm->gathered = comm->arena.alloc<unsigned char>(bb * comm->nranks);
+      comm->gathered_bytes = bb * comm->nranks;
     }
-    require(total < (1ull << 31), "rlc_pass_fold: too many records");
-    require(total == 0 || all_records != nullptr, "rlc_pass_fold: null records");
-    const PassParamsHolder S = ctx->shard;
-    ctx->shard.valid = false;
-    ctx->ensure_exchange(uint32_t(total) > 0 ? uint32_t(total) : 1u, nranks);
     cudaStream_t st = ctx->stream;
-    RLC_CK(cudaMemcpyAsync(ctx->d_counts, counts, 8 * size_t(nranks), cudaMemcpyHostToDevice, st));
-    ctx->stage(3, [&] {
-      rlc::launch_fold_records(S.g, S.p, ctx->pb,
-                               static_cast<const rlc::UpdateRecord*>(all_records), ctx->d_counts,
-                               nranks, stride, uint32_t(total), own_offset, counts[rank],
-                               grid->key_bits, ctx->xb, S.nv, st);
-    });
-    if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
-    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));
-    RLC_CK(cudaGetLastError());
-    finish_sync(ctx, grid);
+    // the exchange: every rank's block to every rank (fixed size: no host count)
+    nccl_check(nccl().all_gather(ctx->block, comm->gathered, bb, ncclUint8, comm->comm, st),
+               "ncclAllGather");
+    shard_fold(ctx, config, grid, comm->gathered, comm->nranks, comm->rank, owner_fold);
+    if (owner_fold && comm->nranks > 1)  // q_before of every record from its cell's owner
+      nccl_check(nccl().all_reduce(ctx->xb.q_rec, ctx->xb.q_rec,
+                                   size_t(comm->nranks) * ctx->block_cap, ncclFloat64, ncclSum,
+                                   comm->comm, st),
+                 "ncclAllReduce");
+    shard_finish(ctx, grid, fb, comm->rank, owner_fold);
+    RLC_CK(cudaMemsetAsync(grid->d_changes, 0, 4, st));
+    enqueue_eop(grid, ctx, &config->cut, grid->d_changes);  // split-collapse: identical on every rank
   });
 }
 

@@ -2477,25 +2477,33 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
 static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, uint32_t mask,
                            uint32_t* out, unsigned int* count_out, cudaStream_t st,
                            uint32_t* block_counts = nullptr, const uint32_t* key_src = nullptr,
-                           uint32_t* key_out = nullptr);
+                           uint32_t* key_out = nullptr, const uint8_t* flags = nullptr);
 
 // ---------------------------------------------------------------------------
-// Screen-band sharding with an exact exchange: every
-// rank folds the update records of all ranks in canonical order, so the
-// learned state stays identical on every rank and to a single-GPU run.
+// Screen-band sharding with an exact exchange.  Every
+// rank traces its band and files its update records (CellKey, cluster, v) in
+// canonical order into a fixed-size block; the blocks of all ranks are
+// all-gathered (rank-major = canonical order, bands being consecutive); every
+// rank inserts the pass's new keys in that order (identical tables); the
+// records are folded in canonical order per (cell, cluster) -- by every rank
+// (replicated) or by the owner of the cell, hash(CellKey) % nranks, whose
+// q_before values are then summed over the ranks and replayed by the others
+// onto their copies -- so every rank ends with the single-GPU state.
 // ---------------------------------------------------------------------------
-__global__ void k_write_records(DevGrid g, const GBuf* __restrict__ gbuf,
-                                const SampleRec* __restrict__ srec,
-                                const uint32_t* __restrict__ rec_path,
-                                const unsigned int* __restrict__ count, uint32_t n,
-                                const unsigned long long* __restrict__ pkey,
-                                UpdateRecord* __restrict__ out) {
+__global__ void k_write_block(DevGrid g, const GBuf* __restrict__ gbuf,
+                              const SampleRec* __restrict__ srec,
+                              const uint32_t* __restrict__ rec_path,
+                              const unsigned int* __restrict__ count, uint32_t n,
+                              const unsigned long long* __restrict__ pkey, uint32_t cap,
+                              unsigned char* __restrict__ block) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n || k >= *count) return;
+  const uint32_t c = min(*count, cap);
+  if (k == 0) reinterpret_cast<RecordBlockHeader*>(block)->count = c;
+  if (k >= n || k >= c) return;
   const uint32_t idx = rec_path[k];
   const uint32_t cell = gbuf[idx].cell;
   UpdateRecord r;
-  if (cell == kPending) {  // new this pass: inserted by the fold of all ranks
+  if (cell == kPending) {  // new this pass: inserted with all ranks' records
     const Key key = unpack_key(pkey[2 * size_t(idx)], pkey[2 * size_t(idx) + 1]);
     r.qx = key.qx;
     r.qy = key.qy;
@@ -2512,39 +2520,46 @@ __global__ void k_write_records(DevGrid g, const GBuf* __restrict__ gbuf,
   }
   r.cluster = srec[idx].s;
   r.v = srec[idx].v;
-  out[k] = r;
+  reinterpret_cast<UpdateRecord*>(block + sizeof(RecordBlockHeader))[k] = r;
 }
 
-// Gathers all ranks' records (rank-major = canonical order, ranks own
-// contiguous row bands) into one array and looks their keys up; keys new
-// this pass are filed with their smallest record index, the canonical order
-// in which the single-GPU reference inserts them.
-__global__ void __launch_bounds__(128) k_gather_records(DevGrid g, const UpdateRecord* __restrict__ all,
-                                                        const unsigned long long* __restrict__ counts,
-                                                        uint32_t nranks, unsigned long long stride,
-                                                        uint32_t total, NewKeys nk,
-                                                        UpdateRecord* __restrict__ contig,
-                                                        uint32_t* __restrict__ slots) {
+void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, void* block,
+                         uint32_t cap, cudaStream_t st) {
+  launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);
+  k_write_block<<<blocks_for(n > 0 ? n : 1, 256), 256, 0, st>>>(
+      g, b.gbuf, b.srec, b.rec_path, b.rec_count, n, b.pkey, cap,
+      static_cast<unsigned char*>(block));
+  count_launch();
+}
+
+__device__ __forceinline__ const UpdateRecord* block_records(const unsigned char* blocks,
+                                                             uint64_t block_bytes, uint32_t r) {
+  return reinterpret_cast<const UpdateRecord*>(blocks + r * block_bytes + sizeof(RecordBlockHeader));
+}
+
+// Gathers the record slots t = rank * cap + k of all blocks and looks their
+// keys up; keys new this pass are filed with their smallest slot index -- the
+// canonical order in which the single-GPU reference inserts them.
+__global__ void __launch_bounds__(128) k_gather_blocks(DevGrid g, const unsigned char* __restrict__ blocks,
+                                                       uint64_t block_bytes, ExchangeBuffers x) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t lane = threadIdx.x & 31u;
-  bool need = t < total;
+  const uint32_t r = t / x.cap, k = t - r * x.cap;
+  bool need = false;
   Key key{};
   uint64_t lo = 0, hi = 0, h = 0;
-  if (need) {
-    unsigned long long off = 0, k = t;
-    uint32_t rank = 0;
-    for (; rank < nranks; ++rank) {
-      if (t < off + counts[rank]) {
-        k = t - off;
-        break;
-      }
-      off += counts[rank];
+  if (r < x.nranks) {
+    const auto* hdr = reinterpret_cast<const RecordBlockHeader*>(blocks + r * block_bytes);
+    if (k < hdr->count) {
+      const UpdateRecord rec = block_records(blocks, block_bytes, r)[k];
+      x.contig[t] = rec;
+      key = Key{rec.qx, rec.qy, rec.qz, rec.qn, rec.level};
+      pack_key(key, lo, hi);
+      h = hash_key(key);
+      need = true;
+    } else {
+      x.slots[t] = kNoSlot;  // padding of the block
     }
-    const UpdateRecord r = all[rank * stride + k];
-    contig[t] = r;
-    key = Key{r.qx, r.qy, r.qz, r.qn, r.level};
-    pack_key(key, lo, hi);
-    h = hash_key(key);
   }
   const unsigned need_mask = __ballot_sync(kFull, need);
   if (!need) return;
@@ -2561,90 +2576,148 @@ __global__ void __launch_bounds__(128) k_gather_records(DevGrid g, const UpdateR
   if (same) {
     if (slot == kPending) {
       const uint32_t first = __reduce_min_sync(same_mask, t);
-      if (int(lane) == leader) nk_register(nk, lo, hi, h, first, err);
+      if (int(lane) == leader) nk_register(x.nk, lo, hi, h, first, err);
     }
   } else {
     slot = probe_find(g, lo, hi, h);
-    if (slot == kPending) nk_register(nk, lo, hi, h, t, err);
+    if (slot == kPending) nk_register(x.nk, lo, hi, h, t, err);
   }
-  slots[t] = slot;
+  x.slots[t] = slot;
 }
 
-// Sort keys of the gathered records once the new keys are in: a record whose
-// key was refused has no update (the fallback cut, never updated): its
-// q_before is the template's.  Fallback hits of this rank's own records are
-// counted here.
-__global__ void k_record_keys(DevGrid g, const UpdateRecord* __restrict__ contig,
-                              uint32_t* __restrict__ slots, uint32_t total,
-                              unsigned long long own_begin, unsigned long long own_end,
-                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                              double* __restrict__ q_rec) {
+// After the insertion: each slot's cell (or the fallback for a refused key,
+// whose record updates nothing), its owner, and the sort keys of the records
+// this rank folds.  Fallback hits of this rank's own records are counted.
+__global__ void k_block_keys(DevGrid g, uint32_t rank, uint32_t owner_fold, ExchangeBuffers x) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= total) return;
-  uint32_t slot = slots[t];
-  const UpdateRecord r = contig[t];
+  if (t >= x.nranks * x.cap) return;
+  uint32_t slot = x.slots[t];
+  x.vals[t] = t;
+  if (slot == kNoSlot) {
+    x.kflag[t] = 0;
+    x.keys[t] = kInvalidKey;
+    return;
+  }
+  const UpdateRecord r = x.contig[t];
+  const Key key{r.qx, r.qy, r.qz, r.qn, r.level};
+  const uint64_t h = hash_key(key);
   if (slot == kPending) {
     uint64_t lo, hi;
-    pack_key(Key{r.qx, r.qy, r.qz, r.qn, r.level}, lo, hi);
-    slot = probe_find(g, lo, hi, hash_key(Key{r.qx, r.qy, r.qz, r.qn, r.level}));
-    if (slot == kPending) slot = kFallback;
-    if (slot == kFallback && t >= own_begin && t < own_end)
-      atomicAdd(g.counters + kCntFallback, 1ull);
+    pack_key(key, lo, hi);
+    slot = probe_find(g, lo, hi, h);
   }
-  vals[t] = t;
-  if (slot == kFallback) {
-    keys[t] = kInvalidKey;
-    q_rec[t] = g.t_q[r.cluster];
-  } else {
-    keys[t] = g.slot_cell[slot] * g.M + r.cluster;
+  uint8_t f = kXValid;
+  uint32_t cell = kFallback;
+  if (slot < kPending) {
+    cell = g.slot_cell[slot];
+  } else {  // refused: a full window (hash_grid.cpp:140)
+    f |= kXFallback;
+    if (t / x.cap == rank) atomicAdd(g.counters + kCntFallback, 1ull);
   }
+  x.cellx[t] = cell;
+  if (!(f & kXFallback)) {
+    const bool owned = !owner_fold || uint32_t(h % x.nranks) == rank;
+    if (owned) f |= kXOwned | kXSort;
+  }
+  x.kflag[t] = f;
+  x.keys[t] = (f & kXSort) ? cell * g.M + r.cluster : kInvalidKey;
 }
 
-__global__ void k_scatter_qbefore(const double* __restrict__ q_rec, uint64_t own_offset,
-                                  const uint32_t* __restrict__ rec_path,
-                                  const unsigned int* __restrict__ count, uint32_t n,
-                                  double* __restrict__ q_before) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n || k >= *count) return;
-  q_before[rec_path[k]] = q_rec[own_offset + k];
-}
-
-void launch_export_records(const DevGrid& g, const PassBuffers& b, uint32_t n,
-                           UpdateRecord* out, cudaStream_t st) {
-  launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);
-  k_write_records<<<blocks_for(n, 256), 256, 0, st>>>(g, b.gbuf, b.srec, b.rec_path, b.rec_count,
-                                                      n, b.pkey, out);
+void launch_shard_fold(const DevGrid& g, const PassParams& fold_params, const void* blocks,
+                       uint64_t block_bytes, uint32_t rank, bool owner_fold, uint32_t key_bits,
+                       ExchangeBuffers& x, cudaStream_t st) {
+  const uint32_t total = x.nranks * x.cap;
+  if (total == 0) return;
+  cudaMemsetAsync(x.nk.count, 0, sizeof(unsigned int), st);
+  cudaMemsetAsync(x.q_rec, 0, sizeof(double) * total, st);
+  k_gather_blocks<<<blocks_for(total, 128), 128, 0, st>>>(
+      g, static_cast<const unsigned char*>(blocks), block_bytes, x);
+  count_launch();
+  launch_insert_new_keys(g, x.nk, st);
+  k_block_keys<<<blocks_for(total, 256), 256, 0, st>>>(g, rank, owner_fold ? 1u : 0u, x);
   count_launch();
 }
 
-void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const PassBuffers& b,
-                         const UpdateRecord* all, const unsigned long long* d_counts,
-                         uint32_t nranks, unsigned long long stride, uint32_t total,
-                         unsigned long long own_offset, unsigned long long local_records,
-                         uint32_t key_bits, ExchangeBuffers& x, uint32_t local_n, cudaStream_t st) {
-  if (total > 0) {
-    cudaMemsetAsync(x.nk.count, 0, sizeof(unsigned int), st);
-    k_gather_records<<<blocks_for(total, 128), 128, 0, st>>>(g, all, d_counts, nranks, stride,
-                                                             total, x.nk, x.contig, x.slots);
-    count_launch();
-    launch_insert_new_keys(g, x.nk, st);
-    k_record_keys<<<blocks_for(total, 256), 256, 0, st>>>(g, x.contig, x.slots, total, own_offset,
-                                                          own_offset + local_records, x.keys,
-                                                          x.vals, x.q_rec);
-    count_launch();
-    uint32_t *k = nullptr, *v = nullptr;
-    launch_sort_buffers(x.keys, x.vals, x.keys_alt, x.vals_alt, x.hist, total, key_bits, st, &k, &v,
-                        nullptr);
-    PassParams p = fold_params;
-    p.n = total;
-    k_fold<<<blocks_for(total, 256), 256, 0, st>>>(
-        g, p, k, v, reinterpret_cast<const char*>(x.contig) + offsetof(UpdateRecord, v),
-        uint32_t(sizeof(UpdateRecord)), x.q_rec, nullptr);
-    count_launch();
-  }
-  if (local_n == 0) return;
-  k_scatter_qbefore<<<blocks_for(local_n, 256), 256, 0, st>>>(x.q_rec, own_offset, b.rec_path,
-                                                              b.rec_count, local_n, b.q_before);
+void launch_shard_sortfold(const DevGrid& g, const PassParams& fold_params, uint32_t key_bits,
+                           ExchangeBuffers& x, cudaStream_t st) {
+  const uint32_t total = x.nranks * x.cap;
+  if (total == 0) return;
+  // the folded records, compacted in slot (= canonical) order, sorted stably
+  // by (cell, cluster) with the device count, folded in canonical order
+  PassBuffers cb{};
+  launch_compact(cb, nullptr, total, kXSort, x.vals_alt, x.sort_count, st, x.block_counts, x.keys,
+                 x.keys_alt, x.kflag);
+  uint32_t *k = nullptr, *v = nullptr;
+  launch_sort_buffers(x.keys_alt, x.vals_alt, x.keys, x.vals, x.hist, total, key_bits, st, &k, &v,
+                      x.sort_count);
+  PassParams p = fold_params;
+  p.n = total;
+  k_fold<<<blocks_for(total, 256), 256, 0, st>>>(
+      g, p, k, v, reinterpret_cast<const char*>(x.contig) + offsetof(UpdateRecord, v),
+      uint32_t(sizeof(UpdateRecord)), x.q_rec, x.sort_count);
+  count_launch();
+}
+
+// Owner mode: the records of cells another rank folded.  Pass 1 counts each
+// cut entry's records and finds its last (highest slot = latest canonical);
+// pass 2 advances the entry from that record's summed q_before exactly as
+// update_q does (cut.cpp:76-86): q = max((1 - a) q_before + a v, eps), a the
+// harmonic weight of the record's own visit count, visits += count.
+__global__ void k_apply_count(DevGrid g, ExchangeBuffers x) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= x.nranks * x.cap) return;
+  const uint8_t f = x.kflag[t];
+  if (!(f & kXValid) || (f & (kXFallback | kXOwned))) return;
+  const size_t e = size_t(x.cellx[t]) * g.M + x.contig[t].cluster;
+  atomicAdd(x.seg_count + e, 1u);
+  atomicMax(x.seg_last + e, t);
+}
+
+__global__ void k_apply_last(DevGrid g, PassParams P, ExchangeBuffers x) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= x.nranks * x.cap) return;
+  const uint8_t f = x.kflag[t];
+  if (!(f & kXValid) || (f & (kXFallback | kXOwned))) return;
+  const uint32_t cell = x.cellx[t];
+  const size_t e = size_t(cell) * g.M + x.contig[t].cluster;
+  const double v = x.contig[t].v;
+  if (!(v >= 0 && isfinite(v)))  // update_q's argument check, cut.cpp:78-80
+    atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrBadValue);
+  g.touched[cell] = 1u;
+  if (x.seg_last[e] != t) return;
+  const uint32_t c = x.seg_count[e];
+  const uint32_t vis_before = g.visits[e] + c - 1u;  // visits seen by the last record
+  const double a = P.harmonic ? 1.0 / (1.0 + double(vis_before)) : P.alpha;
+  g.q[e] = smax((1.0 - a) * x.q_rec[t] + a * v, g.eps_q);
+  g.visits[e] = vis_before + 1u;
+  x.seg_count[e] = 0;  // clean for the next pass
+  x.seg_last[e] = 0;
+}
+
+void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, ExchangeBuffers& x,
+                        cudaStream_t st) {
+  const uint32_t total = x.nranks * x.cap;
+  if (total == 0) return;
+  k_apply_count<<<blocks_for(total, 256), 256, 0, st>>>(g, x);
+  k_apply_last<<<blocks_for(total, 256), 256, 0, st>>>(g, fold_params, x);
+  count_launch(2);
+}
+
+__global__ void k_shard_scatter(DevGrid g, const uint32_t* __restrict__ rec_path,
+                                const unsigned int* __restrict__ count, uint32_t n, uint32_t rank,
+                                ExchangeBuffers x, double* __restrict__ q_before) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || k >= *count || k >= x.cap) return;
+  const uint32_t t = rank * x.cap + k;
+  q_before[rec_path[k]] =
+      (x.kflag[t] & kXFallback) ? g.t_q[x.contig[t].cluster] : x.q_rec[t];  // fallback: never updated
+}
+
+void launch_shard_scatter(const DevGrid& g, const PassBuffers& b, uint32_t n, uint32_t rank,
+                          const ExchangeBuffers& x, cudaStream_t st) {
+  if (n == 0) return;
+  k_shard_scatter<<<blocks_for(n, 256), 256, 0, st>>>(g, b.rec_path, b.rec_count, n, rank, x,
+                                                      b.q_before);
   count_launch();
 }
 
@@ -2851,12 +2924,14 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_scatter(const uint8_t* __re
 // scratch of its own per concurrent stream (null: b.block_counts).
 static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, uint32_t mask,
                            uint32_t* out, unsigned int* count_out, cudaStream_t st,
-                           uint32_t* block_counts, const uint32_t* key_src, uint32_t* key_out) {
+                           uint32_t* block_counts, const uint32_t* key_src, uint32_t* key_out,
+                           const uint8_t* flags) {
   const uint32_t nb = blocks_for(n > 0 ? n : 1, kCmpTile);
   uint32_t* bc = block_counts ? block_counts : b.block_counts;
-  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, bc);
+  const uint8_t* fl = flags ? flags : b.rflag;
+  k_cmp_count<<<nb, kCmpThreads, 0, st>>>(fl, order, n, mask, bc);
   rs_scan<<<1, kScanThreads, 0, st>>>(bc, nb);
-  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.rflag, order, n, mask, bc, out, count_out, key_src,
+  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(fl, order, n, mask, bc, out, count_out, key_src,
                                             key_out);
   count_launch(3);
 }

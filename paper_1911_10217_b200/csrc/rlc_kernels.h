@@ -199,18 +199,35 @@ struct PassBuffers {
 };
 
 // Buffers of the sharded fold, sized for the records of all ranks.
+// A rank's update records of one sharded pass, as all-gathered: a 16-byte
+// header (the record count) and `cap` record slots.  Every rank's block has
+// the same size, so the gather needs no count on the host.
+struct alignas(16) RecordBlockHeader {
+  unsigned long long count;
+  unsigned long long pad;
+};
+
+// Buffers of the sharded fold, for nranks * cap gathered record slots.
 struct ExchangeBuffers {
-  UpdateRecord* contig;
-  uint32_t* slots;
+  UpdateRecord* contig;  // [slot t = rank * cap + k] the gathered records
+  uint32_t* slots;       // [t] the record's table slot (kNoSlot: padding)
+  uint32_t* cellx;       // [t] its dense cell id (kFallback: refused key)
+  uint8_t* kflag;        // [t] kXValid | kXFallback | kXOwned | kXSort
   uint32_t* keys;
   uint32_t* vals;
   uint32_t* keys_alt;
   uint32_t* vals_alt;
   uint32_t* hist;
-  double* q_rec;
+  uint32_t* block_counts;
+  unsigned int* sort_count;
+  double* q_rec;         // [t] q_before of record t (the all-reduced array in owner mode)
+  uint32_t* seg_count;   // [cell * M + cluster] records per cut entry (owner mode apply)
+  uint32_t* seg_last;    // [cell * M + cluster] slot of the entry's last record
   NewKeys nk;
-  uint32_t cap;
+  uint32_t cap;          // record slots per rank
+  uint32_t nranks;
 };
+enum : uint8_t { kXValid = 1, kXFallback = 2, kXOwned = 4, kXSort = 8 };
 
 // == rlc_sample_record (include/rlcuts_b200.h)
 struct alignas(8) SampleExport {
@@ -263,13 +280,29 @@ void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
                          uint32_t** vals_out, const unsigned* n_dev);
-void launch_export_records(const DevGrid& g, const PassBuffers& b, uint32_t n,
-                           UpdateRecord* out, cudaStream_t st);
-void launch_fold_records(const DevGrid& g, const PassParams& fold_params, const PassBuffers& b,
-                         const UpdateRecord* all, const unsigned long long* d_counts,
-                         uint32_t nranks, unsigned long long stride, uint32_t total,
-                         unsigned long long own_offset, unsigned long long local_records,
-                         uint32_t key_bits, ExchangeBuffers& x, uint32_t local_n, cudaStream_t st);
+// Sharded passes.  The rank's update records of the
+// traced band, in canonical order, into `block` (header + cap slots).
+void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, void* block,
+                         uint32_t cap, cudaStream_t st);
+// The fold of all ranks' gathered blocks (nranks x block_bytes): the pass's
+// new keys inserted in canonical order (identical tables on every rank),
+// then update_q for the records of the cells this rank folds -- all of them
+// (owner_fold = 0) or those with hash(CellKey) % nranks == rank -- in
+// canonical order; q_before per record slot into x.q_rec (zero elsewhere).
+void launch_shard_fold(const DevGrid& g, const PassParams& fold_params, const void* blocks,
+                       uint64_t block_bytes, uint32_t rank, bool owner_fold, uint32_t key_bits,
+                       ExchangeBuffers& x, cudaStream_t st);  // gather, insert, keys
+void launch_shard_sortfold(const DevGrid& g, const PassParams& fold_params, uint32_t key_bits,
+                           ExchangeBuffers& x, cudaStream_t st);  // compact, sort, update_q
+// Owner mode, after x.q_rec was summed over the ranks: the cut entries of the
+// cells other ranks folded, advanced to the state their last record leaves
+// (q from its q_before and v, visits by the record count), touched flags.
+void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, ExchangeBuffers& x,
+                        cudaStream_t st);
+// q_before of this rank's own records (fallback: the template's) for the
+// accumulation of its band.
+void launch_shard_scatter(const DevGrid& g, const PassBuffers& b, uint32_t n, uint32_t rank,
+                          const ExchangeBuffers& x, cudaStream_t st);
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
                  const uint32_t* vals, const PassBuffers& b, cudaStream_t st);
 void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffers& b,

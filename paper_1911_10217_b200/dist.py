@@ -2,16 +2,27 @@
 
 Each rank renders a contiguous band of image rows.  The learned cut state
 must evolve exactly as in one render_pass over the whole image, and the
-ordered, floored EMA of update_q (proj/src/cut.cpp:76-86) cannot be merged
-by summing deltas.  So every rank all-gathers the ranks' update records
-(cell key, cluster, v; 32 B each) and folds all of them in canonical order
--- rank-major order is canonical because bands are consecutive -- which
-keeps the cut tables bit-identical on every rank.  Each rank then forms the
-radiance of its own band.
+ordered, floored EMA of update_q (proj/src/cut.cpp:76-86) cannot be merged by
+summing deltas.  Each rank files its update records (cell key, cluster, v;
+32 B) in canonical order into a fixed-size block; the blocks are all-gathered
+(rank-major order is canonical order: bands are consecutive); every rank
+inserts the pass's new keys in that order, so the hash tables stay identical.
+The records are then folded in canonical order per cut entry, either by every
+rank (replicated) or only by the owner of the cell, hash(CellKey) % nranks
+(owner mode): the owners' per-record q_before values are summed over the
+ranks and every rank replays the other owners' entries onto its copy.  Each
+rank then forms the radiance of its own band.
 
-The protocol is written once over an *engine* (GpuEngine: the B200 path,
-NCCL over NVLink; OracleEngine: the CPU restatement, gloo) so the multi-rank
-logic is exercised on CPU by the test-suite.
+Three drivers of the same protocol:
+  * NcclFrame -- the C++ data plane (rlc_shard_frame): NCCL all-gather and
+    all-reduce on the context stream, no host synchronization per frame;
+  * ShardedFrame -- the same steps with torch.distributed collectives (gloo
+    stages through host memory: functional multi-process runs);
+  * local_exchange -- N ranks emulated as N contexts on one device, the
+    collectives done by the host between the steps (no kernel waits on
+    another rank);
+and OracleFrame, the CPU restatement's model of the replicated protocol over
+gloo (tests/test_dist.py).
 """
 from __future__ import annotations
 
@@ -29,52 +40,150 @@ def band(height: int, rank: int, world: int) -> tuple[int, int]:
     return (height * rank) // world, (height * (rank + 1)) // world
 
 
+def record_capacity(cfg, width: int, height: int, world: int) -> int:
+    """Record slots per rank block: the largest band's path vertices."""
+    rows = max(b - a for a, b in (band(height, r, world) for r in range(world)))
+    return max(1, rows * width * (cfg.spp // cfg.passes) * max(cfg.max_depth, 1))
+
+
 class _CudaView:
     """Zero-copy torch view of device memory owned by the C library."""
 
-    def __init__(self, ptr: int, nbytes: int):
-        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+    def __init__(self, ptr: int, nbytes: int, typestr: str = "|u1"):
+        self.__cuda_array_interface__ = {"shape": (nbytes // int(typestr[-1]),), "typestr": typestr,
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
 class GpuEngine:
-    """The B200 path: rlc_pass_trace / rlc_pass_fold / rlc_end_of_pass_update."""
+    """One rank's B200 path: rlc_shard_trace / _fold / _finish, end_of_pass."""
 
-    def __init__(self, ctx, grid, fb, cfg, device: torch.device):
+    def __init__(self, ctx, grid, fb, cfg, device: torch.device, cap: int | None = None,
+                 world: int = 1):
         self.ctx, self.grid, self.fb, self.cfg, self.device = ctx, grid, fb, cfg, device
-        self._ptr, self._n = 0, 0
+        cam = ctx.scene.camera
+        self.cap = cap or record_capacity(cfg, cam.width, cam.height, world)
 
-    def trace(self, pass_index: int, rows) -> int:
-        self._ptr, self._n = rlcuts.pass_trace(self.ctx, self.cfg, pass_index, self.grid, rows)
-        return self._n
+    def trace(self, pass_index: int, rows) -> torch.Tensor:
+        ptr, nbytes = rlcuts.shard_trace(self.ctx, self.cfg, pass_index, self.grid, rows, self.cap)
+        return torch.as_tensor(_CudaView(ptr, nbytes), device=self.device)
 
-    def records(self) -> torch.Tensor:
-        if self._n == 0:
-            return torch.zeros(0, dtype=torch.uint8, device=self.device)
-        return torch.as_tensor(_CudaView(self._ptr, self._n * RECORD_BYTES), device=self.device)
+    def fold(self, gathered: torch.Tensor, nranks: int, rank: int, owner: bool) -> torch.Tensor:
+        ptr, n = rlcuts.shard_fold(self.ctx, self.cfg, self.grid, gathered.data_ptr(), nranks,
+                                   rank, owner)
+        return torch.as_tensor(_CudaView(ptr, 8 * n, "<f8"), device=self.device)
 
-    def fold(self, all_records: torch.Tensor, counts, rank: int, stride: int):
-        # the gather ran on torch's stream; the library works on its own stream
-        torch.cuda.current_stream(self.device).synchronize()
-        rlcuts.pass_fold(self.ctx, self.cfg, self.grid, self.fb, all_records.data_ptr(), counts,
-                         rank, stride)
+    def finish(self, rank: int, owner: bool):
+        rlcuts.shard_finish(self.ctx, self.grid, self.fb, rank, owner)
 
     def end_of_pass(self) -> int:
         return rlcuts.end_of_pass_update(self.grid, self.ctx, self.cfg.cut)
 
 
+class ShardedFrame:
+    """One rank's share of a sharded frame over torch.distributed."""
+
+    def __init__(self, engine: GpuEngine, height: int, rank: int, world: int, group=None,
+                 host_staging: bool = False, owner: bool = True):
+        self.engine, self.rank, self.world, self.group = engine, rank, world, group
+        self.rows = band(height, rank, world)
+        self.owner = owner
+        # gloo cannot all-gather device tensors: stage through host memory
+        self.host_staging = host_staging
+
+    def _sync(self):
+        # the library's stream -> torch's collective (same stream under the
+        # bench; a full sync keeps the functional gloo path simple)
+        self.engine.ctx.synchronize()
+
+    def step(self, pass_index: int) -> int:
+        """render_pass + end_of_pass_update for this rank's band; returns the
+        split-collapse change count (identical on every rank)."""
+        e = self.engine
+        block = e.trace(pass_index, self.rows)
+        self._sync()
+        dev = torch.device("cpu") if self.host_staging else e.device
+        send = block.to(dev)
+        parts = [torch.empty_like(send) for _ in range(self.world)]
+        dist.all_gather(parts, send, group=self.group)
+        gathered = torch.cat(parts).to(e.device)
+        torch.cuda.synchronize(e.device)
+        q = e.fold(gathered, self.world, self.rank, self.owner)
+        if self.owner and self.world > 1:
+            self._sync()
+            qs = q.to(dev)
+            dist.all_reduce(qs, group=self.group)
+            q.copy_(qs.to(e.device))
+            torch.cuda.synchronize(e.device)
+        e.finish(self.rank, self.owner)
+        return e.end_of_pass()
+
+
+class NcclFrame:
+    """One rank's share of a sharded frame over the C++ NCCL data plane
+    (rlc_shard_frame): one library call per frame, no host synchronization."""
+
+    def __init__(self, engine: GpuEngine, height: int, rank: int, world: int, device_index: int,
+                 owner: bool = True):
+        self.engine, self.rank, self.world = engine, rank, world
+        self.rows = band(height, rank, world)
+        self.owner = owner
+        obj = [rlcuts.Comm.unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        self.comm = rlcuts.Comm(device_index, world, rank, obj[0])
+
+    def step(self, pass_index: int) -> None:
+        e = self.engine
+        rlcuts.shard_frame(e.ctx, e.cfg, pass_index, e.grid, e.fb, self.comm, self.rows, e.cap,
+                           self.owner)
+
+
+def local_exchange(engines, heights_rows, pass_index: int, owner: bool = True,
+                   serial: bool = False):
+    """Single-process emulation of the exchange for N engines (tests on one
+    device): every engine traces its band, the blocks are concatenated in
+    rank order, every engine folds; in owner mode the per-slot q_before
+    arrays are summed and handed back.  No kernel waits on another.
+    serial: one rank's work at a time (per-rank timing without the other
+    ranks' kernels sharing the device)."""
+    n = len(engines)
+    blocks = []
+    for e, rows in zip(engines, heights_rows):
+        blocks.append(e.trace(pass_index, rows))
+        if serial:
+            e.ctx.synchronize()
+    for e in engines:
+        e.ctx.synchronize()
+    gathered = torch.cat([b.clone() for b in blocks])
+    torch.cuda.synchronize()
+    qs = []
+    for r, e in enumerate(engines):
+        qs.append(e.fold(gathered, n, r, owner))
+        if serial:
+            e.ctx.synchronize()
+    for e in engines:
+        e.ctx.synchronize()
+    if owner and n > 1:
+        total = torch.stack([q.clone() for q in qs]).sum(0)
+        for q in qs:
+            q.copy_(total)
+        torch.cuda.synchronize()
+    for r, e in enumerate(engines):
+        e.finish(r, owner)
+        if serial:
+            e.ctx.synchronize()
+    return [e.end_of_pass() for e in engines]
+
+
 class OracleEngine:
-    """The CPU restatement (oracle/): the same protocol on host memory."""
+    """The CPU restatement (oracle/): the replicated protocol on host memory."""
 
     def __init__(self, run):
         self.run = run
-        self.device = torch.device("cpu")
 
-    def trace(self, pass_index: int, rows) -> int:
-        return self.run.trace(pass_index, rows)
-
-    def records(self) -> torch.Tensor:
-        return torch.from_numpy(self.run.records().view(np.uint8).copy())
+    def trace(self, pass_index: int, rows) -> torch.Tensor:
+        n = self.run.trace(pass_index, rows)
+        return torch.from_numpy(self.run.records().view(np.uint8).copy()), n
 
     def fold(self, all_records: torch.Tensor, counts, rank: int, stride: int):
         self.run.fold(all_records.numpy().view(rlcuts.RECORD_DTYPE), counts, rank, stride)
@@ -83,54 +192,24 @@ class OracleEngine:
         return self.run.end_of_pass()
 
 
-class ShardedFrame:
-    """One rank's share of a sharded frame."""
+class OracleFrame:
+    """One rank's share of a sharded frame of the CPU model over gloo."""
 
-    def __init__(self, engine, height: int, rank: int, world: int, group=None,
-                 host_staging: bool = False):
+    def __init__(self, engine: OracleEngine, height: int, rank: int, world: int, group=None):
         self.engine, self.rank, self.world, self.group = engine, rank, world, group
         self.rows = band(height, rank, world)
-        self.last_counts = [0] * world
-        # gloo cannot all-gather device tensors: stage through host memory
-        self.host_staging = host_staging
 
-    def exchange(self, n: int) -> tuple[torch.Tensor, list, int]:
-        dev = torch.device("cpu") if self.host_staging else self.engine.device
-        cnt = torch.tensor([n], dtype=torch.int64, device=dev)
+    def step(self, pass_index: int) -> int:
+        recs, n = self.engine.trace(pass_index, self.rows)
+        cnt = torch.tensor([n], dtype=torch.int64)
         counts_t = [torch.zeros_like(cnt) for _ in range(self.world)]
         dist.all_gather(counts_t, cnt, group=self.group)
         counts = [int(c.item()) for c in counts_t]
         stride = max(max(counts), 1)
-        send = torch.zeros(stride * RECORD_BYTES, dtype=torch.uint8, device=dev)
+        send = torch.zeros(stride * RECORD_BYTES, dtype=torch.uint8)
         if n:
-            send[: n * RECORD_BYTES] = self.engine.records().to(dev)
+            send[: n * RECORD_BYTES] = recs
         parts = [torch.empty_like(send) for _ in range(self.world)]
         dist.all_gather(parts, send, group=self.group)
-        return torch.cat(parts).to(self.engine.device), counts, stride
-
-    def step(self, pass_index: int) -> int:
-        """render_pass + end_of_pass_update for this rank's band; returns the
-        split-collapse change count (identical on every rank)."""
-        n = self.engine.trace(pass_index, self.rows)
-        all_records, counts, stride = self.exchange(n)
-        self.last_counts = counts
-        self.engine.fold(all_records, counts, self.rank, stride)
+        self.engine.fold(torch.cat(parts), counts, self.rank, stride)
         return self.engine.end_of_pass()
-
-
-def local_exchange(engines, heights_rows, pass_index: int):
-    """Single-process emulation of the exchange for N engines (tests on one
-    device): every engine traces its band, records are concatenated in rank
-    order, every engine folds all of them.  No kernel waits on another."""
-    counts = [e.trace(pass_index, rows) for e, rows in zip(engines, heights_rows)]
-    stride = max(max(counts), 1)
-    parts = []
-    for e, n in zip(engines, counts):
-        buf = torch.zeros(stride * RECORD_BYTES, dtype=torch.uint8, device=e.device)
-        if n:
-            buf[: n * RECORD_BYTES] = e.records()
-        parts.append(buf)
-    all_records = torch.cat(parts)
-    for r, e in enumerate(engines):
-        e.fold(all_records, counts, r, stride)
-    return [e.end_of_pass() for e in engines]

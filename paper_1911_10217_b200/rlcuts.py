@@ -144,7 +144,7 @@ class RenderContext:
         _check(_lib.load().rlc_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
     STAGES = ("primary", "sample", "sort", "fold", "accumulate", "split_collapse", "shadow",
-              "insert", "compact")
+              "insert", "compact", "exchange_keys")
 
     def count_work(self, on: bool = True):
         """k_shadow's counting instance on/off (rlc_context_count_work)."""
@@ -466,27 +466,77 @@ def pass_samples(ctx: RenderContext, config: RenderConfig, row_begin: int = 0) -
             "ray": (rec["flags"] & SAMPLE_RAY) != 0, "nonzero": (rec["flags"] & SAMPLE_NONZERO) != 0}
 
 
-def pass_trace(ctx: RenderContext, config: RenderConfig, pass_index: int, grid: HashGrid,
-               rows: tuple) -> tuple[int, int]:
-    """rlc_pass_trace: trace a band without applying updates.  Returns
-    (device pointer, count) of the band's update records (32 B each)."""
+def shard_trace(ctx: RenderContext, config: RenderConfig, pass_index: int, grid: HashGrid,
+                rows: tuple, cap_records: int) -> tuple[int, int]:
+    """rlc_shard_trace: trace a band and file its update records into the
+    context's record block.  Returns (device pointer, bytes) of the block."""
     cfg = config.c()
     ptr = C.c_void_p()
     n = C.c_uint64()
-    _check(_lib.load().rlc_pass_trace(ctx.handle, C.byref(cfg), pass_index, grid.handle,
-                                      rows[0], rows[1], C.byref(ptr), C.byref(n)))
+    _check(_lib.load().rlc_shard_trace(ctx.handle, C.byref(cfg), pass_index, grid.handle,
+                                       rows[0], rows[1], cap_records, C.byref(ptr), C.byref(n)))
     return int(ptr.value or 0), int(n.value)
 
 
-def pass_fold(ctx: RenderContext, config: RenderConfig, grid: HashGrid, framebuffer: Framebuffer,
-              all_records_ptr: int, counts, rank: int, stride: int):
-    """rlc_pass_fold: fold every rank's records (device memory, rank-major,
-    `stride` records per rank) and accumulate this rank's band."""
+def shard_fold(ctx: RenderContext, config: RenderConfig, grid: HashGrid, blocks_ptr: int,
+               nranks: int, rank: int, owner_fold: bool) -> tuple[int, int]:
+    """rlc_shard_fold over the all-gathered blocks (device memory, rank-major).
+    Returns (device pointer, count) of the per-slot q_before doubles."""
     cfg = config.c()
-    c = np.ascontiguousarray(counts, np.uint64)
-    _check(_lib.load().rlc_pass_fold(ctx.handle, C.byref(cfg), grid.handle, framebuffer.handle,
-                                     C.c_void_p(all_records_ptr), c.ctypes.data_as(C.POINTER(C.c_uint64)),
-                                     len(c), rank, stride))
+    ptr = C.c_void_p()
+    n = C.c_uint64()
+    _check(_lib.load().rlc_shard_fold(ctx.handle, C.byref(cfg), grid.handle, C.c_void_p(blocks_ptr),
+                                      nranks, rank, int(owner_fold), C.byref(ptr), C.byref(n)))
+    return int(ptr.value or 0), int(n.value)
+
+
+def shard_finish(ctx: RenderContext, grid: HashGrid, framebuffer: Framebuffer, rank: int,
+                 owner_fold: bool):
+    _check(_lib.load().rlc_shard_finish(ctx.handle, grid.handle, framebuffer.handle, rank,
+                                        int(owner_fold)))
+
+
+def shard_sync(ctx: RenderContext, grid: HashGrid):
+    _check(_lib.load().rlc_shard_sync(ctx.handle, grid.handle))
+
+
+class Comm:
+    """NCCL communicator of one rank (rlc_comm_*); rank 0's unique id is
+    shared by the caller (e.g. torch.distributed.broadcast_object_list)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(_lib.load().rlc_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, device: int, nranks: int, rank: int, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(_lib.load().rlc_comm_create(device, nranks, rank, buf, C.byref(h)))
+        self.handle, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.load().rlc_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard_frame(ctx: RenderContext, config: RenderConfig, pass_index: int, grid: HashGrid,
+                framebuffer: Framebuffer, comm: Comm, rows: tuple, cap_records: int,
+                owner_fold: bool = True):
+    """rlc_shard_frame: this rank's band of one frame with the exchange over
+    NCCL, enqueued without a host synchronization."""
+    cfg = config.c()
+    _check(_lib.load().rlc_shard_frame(ctx.handle, C.byref(cfg), pass_index, grid.handle,
+                                       framebuffer.handle, comm.handle, rows[0], rows[1],
+                                       cap_records, int(owner_fold)))
 
 
 @dataclass

@@ -37,7 +37,7 @@ def _worker(rank: int, world: int, port: int, outdir: str, depth: int):
                             world_size=world)
     scene, cfg = _case(depth)
     run = OracleRun(scene, cfg)
-    frame = rdist.ShardedFrame(rdist.OracleEngine(run), scene.camera.height, rank, world)
+    frame = rdist.OracleFrame(rdist.OracleEngine(run), scene.camera.height, rank, world)
     changes = [frame.step(p) for p in range(cfg.passes)]
     s, c = run.framebuffer()
     with open(os.path.join(outdir, f"rank{rank}.pkl"), "wb") as f:

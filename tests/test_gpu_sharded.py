@@ -1,7 +1,9 @@
-"""GPU: the sharded pass (rlc_pass_trace / rlc_pass_fold) with N ranks
+"""GPU: the sharded pass (rlc_shard_trace / _fold / _finish) with N ranks
 emulated as N contexts on one device and a host-driven exchange (no kernel
 waits on another rank) must reproduce the single-context pass and the
-reference bit for bit."""
+reference bit for bit, with the fold replicated on every rank or done by the
+owner of each cell; the NCCL data plane (rlc_shard_frame) at one rank; and
+two processes sharing the device over gloo through ShardedFrame."""
 import numpy as np
 import pytest
 import torch
@@ -13,8 +15,9 @@ pytestmark = pytest.mark.gpu
 RL = rlcuts.SamplerKind.rl_lightcuts
 
 
-@pytest.mark.parametrize("world,depth", [(1, 1), (2, 1), (3, 1), (2, 3)])
-def test_sharded_gpu_matches_single(ref, world, depth):
+@pytest.mark.parametrize("owner", [False, True])
+@pytest.mark.parametrize("world,depth", [(1, 1), (2, 1), (3, 1), (2, 3), (4, 1)])
+def test_sharded_gpu_matches_single(ref, world, depth, owner):
     scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
     cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL, max_depth=depth,
                               cut=rlcuts.CutConfig(cut_size=64, split_threshold=2.0))
@@ -27,7 +30,7 @@ def test_sharded_gpu_matches_single(ref, world, depth):
     rows = [rdist.band(scene.camera.height, r, world) for r in range(world)]
     rr = ref.RefRun(scene, cfg)
     for p in range(cfg.passes):
-        changes = rdist.local_exchange(engines, rows, p)
+        changes = rdist.local_exchange(engines, rows, p, owner)
         rch, _ = rr.run_pass(p)
         assert changes == [rch] * world
     rs, rc = rr.framebuffer()
@@ -45,8 +48,9 @@ def test_sharded_gpu_matches_single(ref, world, depth):
     assert lookups == rr.stats()["lookups"]
 
 
+@pytest.mark.parametrize("owner", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_overflow_matches_reference(ref, world):
+def test_sharded_overflow_matches_reference(ref, world, owner):
     """A hash table too small for the scene: every rank inserts the new keys
     of all ranks' records in canonical order, so the refused keys, the slot
     layout and the learned state equal the single-GPU reference's."""
@@ -63,7 +67,7 @@ def test_sharded_overflow_matches_reference(ref, world):
     rows = [rdist.band(scene.camera.height, r, world) for r in range(world)]
     rr = ref.RefRun(scene, cfg)
     for p in range(cfg.passes):
-        changes = rdist.local_exchange(engines, rows, p)
+        changes = rdist.local_exchange(engines, rows, p, owner)
         rch, _ = rr.run_pass(p)
         assert changes == [rch] * world
     rs, rc = rr.framebuffer()
@@ -80,3 +84,30 @@ def test_sharded_overflow_matches_reference(ref, world):
         assert [(s_, k) for s_, _, k, _ in e.grid.slots()] == rr.slots()
         fallback += e.grid.fallback_hits()
     assert fallback == rr.stats()["fallback_hits"] > 100
+
+
+@pytest.mark.parametrize("owner", [False, True])
+def test_nccl_frame_one_rank_matches_render_pass(ref, owner):
+    """rlc_shard_frame through a real one-rank NCCL communicator (all-gather
+    and all-reduce on the context stream) equals render_pass + end_of_pass."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+                              cut=rlcuts.CutConfig(cut_size=64, split_threshold=2.0))
+    ctx = rlcuts.build_context(scene, cfg)
+    grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+    eng = rdist.GpuEngine(ctx, grid, fb, cfg, torch.device("cuda", 0))
+    frame = rdist.NcclFrame(eng, scene.camera.height, 0, 1, 0, owner)
+    rr = ref.RefRun(scene, cfg)
+    for p in range(cfg.passes):
+        frame.step(p)
+        rr.run_pass(p)
+    rlcuts.shard_sync(ctx, grid)
+    s, c = fb.download()
+    rs, rc = rr.framebuffer()
+    assert np.array_equal(s, rs) and np.array_equal(c, rc)
+    cells, rcells = grid.export(), rr.export()
+    assert cells.keys() == rcells.keys()
+    for k, v in rcells.items():
+        for f in v:
+            assert np.array_equal(cells[k][f], v[f])
+    assert grid.stats() == rr.stats()
