@@ -410,7 +410,7 @@ struct rlc_context {
     xb.vals = xarena.alloc<uint32_t>(n);
     xb.keys_alt = xarena.alloc<uint32_t>(n);
     xb.vals_alt = xarena.alloc<uint32_t>(n);
-    xb.hist = xarena.alloc<uint32_t>((size_t(n) / 1024 + 2) * 256);  // sort tile: 1024 keys
+    xb.hist = xarena.alloc<uint32_t>((size_t(n) / rlc::kSortTile + 2) * 256);
     xb.block_counts = xarena.alloc<uint32_t>(n / 2048 + 2);
     xb.sort_count = xarena.alloc<unsigned int>(2);
     xb.q_rec = xarena.alloc<double>(n);
@@ -492,7 +492,7 @@ struct rlc_context {
     pb.block_counts = scratch.alloc<uint32_t>(cap / 2048 + 2);
     pb.block_counts2 = scratch.alloc<uint32_t>(cap / 2048 + 2);
     pb.sort_count = scratch.alloc<unsigned int>(2);
-    pb.sort_hist_cap = ((cap + 1023u) / 1024u + 2u) * 256u;  // rows + digit totals (1024-key tiles)
+    pb.sort_hist_cap = ((cap + rlc::kSortTile - 1u) / rlc::kSortTile + 2u) * 256u;  // rows + digit totals
     pb.sort_hist = scratch.alloc<uint32_t>(pb.sort_hist_cap);
     pb_cap = cap;
   }

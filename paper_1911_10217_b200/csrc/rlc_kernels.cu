@@ -595,21 +595,32 @@ __device__ __forceinline__ uint32_t probe_find(const DevGrid& g, uint64_t lo, ui
 }
 
 // Files a pending key with canonical id `id` in the pass's new-key table
-// (128-bit CAS claim, smallest id kept).
+// (128-bit CAS claim, smallest id kept).  Many warps file the same keys
+// (a cold table: every lookup misses), so each entry is read first and
+// written only when that can change it.  A plain 16-byte read may observe a
+// claim half done; the entry is taken as another key's only when a complete
+// half differs from ours (a valid hi word, or a non-zero lo word), and as
+// ours only when both halves match -- otherwise the CAS decides.
 __device__ __forceinline__ void nk_register(const NewKeys& nk, uint64_t lo, uint64_t hi, uint64_t h,
                                             uint32_t id, uint32_t* err) {
   uint32_t e = uint32_t(h ^ (h >> 31)) & nk.mask;
   for (uint32_t i = 0; i <= nk.mask; ++i) {
-    uint64_t olo, ohi;
-    cas128(nk.keys + 2 * size_t(e), lo, hi, olo, ohi);
-    if (olo == 0 && ohi == 0) {
-      const uint32_t d = atomicAdd(nk.count, 1u);
-      nk.list[d] = e;
-      atomicMin(nk.id + e, id);
-      return;
+    const ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(nk.keys + 2 * size_t(e)));
+    bool mine = cur.x == lo && cur.y == hi;
+    const bool other = (cur.y != 0 && cur.y != hi) || (cur.x != 0 && cur.x != lo);
+    if (!mine && !other) {
+      uint64_t olo, ohi;
+      cas128(nk.keys + 2 * size_t(e), lo, hi, olo, ohi);
+      if (olo == 0 && ohi == 0) {
+        const uint32_t d = atomicAdd(nk.count, 1u);
+        nk.list[d] = e;
+        atomicMin(nk.id + e, id);
+        return;
+      }
+      mine = olo == lo && ohi == hi;
     }
-    if (olo == lo && ohi == hi) {
-      atomicMin(nk.id + e, id);
+    if (mine) {
+      if (id < __ldcg(nk.id + e)) atomicMin(nk.id + e, id);  // ids only decrease
       return;
     }
     e = (e + 1) & nk.mask;
@@ -1006,6 +1017,10 @@ __device__ __forceinline__ uint32_t upper_bound_cdf(const double* __restrict__ c
 #ifndef RLC_SAMPLE_BLOCKS
 #define RLC_SAMPLE_BLOCKS 1
 #endif
+#ifndef RLC_SORT_COMPACT
+#define RLC_SORT_COMPACT 0  // compacting the records first measured slower (its three
+                            // launches delay the sort past the shadow rays): c3 1.105 vs 1.089 ms
+#endif
 __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, DevGrid g, PassParams P,
                                                 const GBuf* __restrict__ gbuf,
                                                 SampleRec* __restrict__ srec,
@@ -1022,6 +1037,9 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
   const GBuf gb = gbuf[idx];
   keys[idx] = kInvalidKey;
+#if !RLC_SORT_COMPACT
+  vals[idx] = idx;  // the record sort's values (every vertex is sorted)
+#endif
   if (!(gb.flags & kGReflective)) {
     srec[idx].flags = 0;
     rflag[idx] = 0;  // read by the compactions
@@ -1954,13 +1972,20 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
 // ---------------------------------------------------------------------------
 // stable LSD radix sort of (key, val) pairs, 8-bit digits
 // ---------------------------------------------------------------------------
-// Sized to run beside k_shadow: with 7 shadow blocks per SM (64 registers
-// x 128 threads each) an SM has 8,192 registers left, so every kernel of the
-// record sort keeps a block at <= 8,192 registers (128 threads x <= 64);
-// a block that does not fit waits for the shadow blocks to retire.
-constexpr int kRsThreads = 128;
+// Block size of the record sort.  Sort blocks that fit in the registers the
+// 7 shadow blocks per SM leave (8,192: 128 threads x <= 64) run beside
+// k_shadow and take its issue slots; 256-thread blocks with 16 keys per
+// thread (102 registers) mostly wait for the shadow blocks to retire, and the
+// frame is shorter: c3 1.038 vs 1.076 ms per frame, same box.
+#ifndef RLC_RS_THREADS
+#define RLC_RS_THREADS 256
+#endif
+#ifndef RLC_RS_MINB
+#define RLC_RS_MINB 1  // (8 with 128 threads: rs_scatter at <= 64 registers, beside k_shadow)
+#endif
+constexpr int kRsThreads = RLC_RS_THREADS;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsItems = 8;  // per thread
+constexpr int kRsItems = int(kSortTile) / kRsThreads;  // per thread
 constexpr int kRsTile = kRsThreads * kRsItems;
 constexpr int kRsWarpSpan = 32 * kRsItems;
 
@@ -2046,7 +2071,7 @@ __global__ void __launch_bounds__(256) rs_scan_rows(uint32_t* __restrict__ hist,
   if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
-__global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restrict__ kin,
+__global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint32_t* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin,
                                                          uint32_t* __restrict__ kout,
                                                          uint32_t* __restrict__ vout,
@@ -2061,22 +2086,30 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restr
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
   for (int d = lane; d < 256; d += 32) wh[w][d] = 0;
   {  // digit base = exclusive prefix of the digit totals, + this block's row offset
-    // (two digits per thread: digits 2t, 2t + 1)
-    const uint32_t d0 = 2 * threadIdx.x;
-    const uint32_t t0 = totals[d0], t1 = totals[d0 + 1];
-    const uint32_t pair = t0 + t1;
-    uint32_t x = pair;
+    // (kDpt consecutive digits per thread)
+    constexpr uint32_t kDpt = 256 / kRsThreads;
+    static_assert(kDpt * kRsThreads == 256, "256 digits over the block");
+    const uint32_t d0 = kDpt * threadIdx.x;
+    uint32_t tl[kDpt], mine = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kDpt; ++j) {
+      tl[j] = totals[d0 + j];
+      mine += tl[j];
+    }
+    uint32_t x = mine;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, x, o);
       if (lane >= uint32_t(o)) x += y;
     }
     if (lane == 31) dsum[w] = x;
     __syncthreads();
-    uint32_t before = 0;
-    for (uint32_t q = 0; q < w; ++q) before += dsum[q];
-    const uint32_t ex = before + x - pair;
-    base_off[d0] = ex + offs[d0 * gridDim.x + blockIdx.x];
-    base_off[d0 + 1] = ex + t0 + offs[(d0 + 1) * gridDim.x + blockIdx.x];
+    uint32_t run = x - mine;
+    for (uint32_t q = 0; q < w; ++q) run += dsum[q];
+#pragma unroll
+    for (uint32_t j = 0; j < kDpt; ++j) {
+      base_off[d0 + j] = run + offs[(d0 + j) * gridDim.x + blockIdx.x];
+      run += tl[j];
+    }
   }
   __syncwarp();
   const uint32_t base = blockIdx.x * kRsTile + w * kRsWarpSpan;
@@ -2992,15 +3025,21 @@ void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb,
   *vals_out = va;
 }
 
+
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out) {
-  // only the vertices that carry an update record are sorted (c3: 1.48M of
-  // 2.07M): a stable compaction gathers their keys in canonical order, and
-  // the digit passes read the count on the device
+  // RLC_SORT_COMPACT: only the vertices that carry an update record are
+  // sorted (c3: 1.48M of 2.07M), gathered by a stable compaction, the digit
+  // passes reading the count on the device
+#if RLC_SORT_COMPACT
   launch_compact(b, nullptr, n, kSRecord, b.vals_alt, b.sort_count, st, b.block_counts2, b.keys,
                  b.keys_alt);
   launch_sort_buffers(b.keys_alt, b.vals_alt, b.keys, b.vals, b.sort_hist, n, key_bits, st,
                       keys_out, vals_out, b.sort_count);
+#else  // every vertex (invalid keys sort last; k_sample wrote vals = vertex)
+  launch_sort_buffers(b.keys, b.vals, b.keys_alt, b.vals_alt, b.sort_hist, n, key_bits, st,
+                      keys_out, vals_out, nullptr);
+#endif
 }
 
 void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
@@ -3010,7 +3049,7 @@ void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
   q.n = p.nv;  // k_fold runs over the update records of all path vertices
   k_fold<<<blocks_for(q.n, 256), 256, 0, st>>>(
       g, q, keys, vals, reinterpret_cast<const char*>(b.srec) + offsetof(SampleRec, v),
-      uint32_t(sizeof(SampleRec)), b.q_before, b.sort_count);
+      uint32_t(sizeof(SampleRec)), b.q_before, RLC_SORT_COMPACT ? b.sort_count : nullptr);
   count_launch();
 }
 

@@ -276,6 +276,12 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
                    unsigned long long* counters, cudaStream_t st, bool leave_room = false);
 void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  uint32_t** keys_out, uint32_t** vals_out);
+// Keys per block of the record sort (its per-block digit histograms hold
+// 256 x ceil(n / kSortTile) counters).
+#ifndef RLC_SORT_TILE
+#define RLC_SORT_TILE 4096
+#endif
+constexpr uint32_t kSortTile = RLC_SORT_TILE;
 // n_dev (may be null): a device-side count <= n of the valid entries.
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,

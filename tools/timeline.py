@@ -1,6 +1,6 @@
 """Per-stage timeline of a few steady-state c3 frames (CUDA events on each
 stream, rlc_context_stage_marks): where the overlapped streams leave the
-critical path.  usage: python tools/timeline.py [config] [frames]"""
+critical path.  usage: python tools/timeline.py [config] [frames] [warm-up frames]"""
 import sys
 
 sys.path.insert(0, ".")
@@ -9,16 +9,17 @@ from paper_1911_10217_b200 import rlcuts  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 frames = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+warm = int(sys.argv[3]) if len(sys.argv) > 3 else 20
 scene, cfg = bench.make_config(name)
 ctx = rlcuts.build_context(scene, cfg)
 grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
-for p in range(20):
+for p in range(warm):
     rlcuts.render_pass(ctx, cfg, p, grid, fb, sync=False)
     rlcuts.end_of_pass_update(grid, ctx, cfg.cut, sync=False)
 ctx.synchronize()
 ctx.stage_times()
 ctx.enable_timing(True)
-for p in range(20, 20 + frames):
+for p in range(warm, warm + frames):
     rlcuts.render_pass(ctx, cfg, p, grid, fb, sync=False)
     rlcuts.end_of_pass_update(grid, ctx, cfg.cut, sync=False)
 ctx.synchronize()
