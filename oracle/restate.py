@@ -142,7 +142,7 @@ class OracleRun:
                 "fallback": u[:n, 3].astype(bool), "q_before": f[:n, 0], "v": f[:n, 1],
                 "radiance": f[:n, 2:5], "total": f[:n, 5]}
 
-    # ---- sharded pass (CPU model of rlc_pass_trace / rlc_pass_fold) ----
+    # ---- sharded pass (CPU model of the replicated rlc_shard_* protocol) ----
     def trace(self, pass_index: int, rows: tuple) -> int:
         r = oracle_lib().orc_run_trace(self.h, pass_index, rows[0], rows[1])
         if r < 0:

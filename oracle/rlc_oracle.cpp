@@ -968,7 +968,8 @@ int64_t orc_run_pass(void* h, uint32_t pass_index) {
   }
 }
 
-// Sharded pass (oracle model of rlc_pass_trace / rlc_pass_fold).
+// Sharded pass (oracle model of the replicated protocol of rlc_shard_trace / rlc_shard_fold:
+// records exchanged between ranks, every rank folding all of them).
 int64_t orc_run_trace(void* h, uint32_t pass_index, uint32_t r0, uint32_t r1) {
   Run* r = static_cast<Run*>(h);
   try {
