@@ -289,10 +289,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
               if dynamic else None)
     update_ms = [0.0]
 
+    # the scenes of the next frames are prepared ahead (their host builds run
+    # beside this frame's GPU work and each other: rlc_context_prepare_scene)
+    ahead, tokens = max(0, args.scene_ahead), {}
+
     def update(p):
         if dynamic and p > 0:
             t = time.perf_counter()
-            ctx.update_scene(frames[p % len(frames)])
+            for q in range(p, p + ahead + 1):
+                if q not in tokens:
+                    tokens[q] = ctx.prepare_scene(frames[q % len(frames)])
+            ctx.commit_scene(tokens.pop(p))
             update_ms[0] += (time.perf_counter() - t) * 1e3
 
     if world == 1:
@@ -448,8 +455,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ctx.set_stream(None)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        for q in sorted(tokens):  # scenes still prepared ahead by the loops above
+            ctx.commit_scene(tokens.pop(q))
+        toks = {}
         for p in range(args.steps):
-            ctx.update_scene(frames[p % len(frames)])
+            for q in range(p, p + ahead + 1):
+                if q not in toks:
+                    toks[q] = ctx.prepare_scene(frames[q % len(frames)])
+            ctx.commit_scene(toks.pop(p))
             rlcuts.render_pass(ctx, cfg, p, g2, f2, sync=False)
             rlcuts.end_of_pass_update(g2, ctx, cfg.cut, sync=False)
             n_done = g2.lookup_count()
@@ -458,7 +471,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e = {"value": n_done / wall, "unit": UNIT,
                "h2d_bytes_per_step": 76 * ntri + 48 * scene.materials.shape[0] + 128,
                "d2h_bytes_per_step": 8, "wall_ms": wall * 1e3,
-               "call": "rlc_context_update_scene + rlc_render_pass + rlc_end_of_pass_update"}
+               "call": "rlc_context_prepare_scene (frames ahead) + rlc_context_commit_scene + "
+                    "rlc_render_pass + rlc_end_of_pass_update"}
     elif not args.no_e2e and world == 1:
         ecfg = rlcuts.RenderConfig(spp=args.steps * (cfg.spp // cfg.passes), passes=args.steps,
                                    sampler=cfg.sampler, cut=cfg.cut, hash=cfg.hash,
@@ -529,6 +543,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: bound on the timed host time")
+    ap.add_argument("--scene-ahead", type=int, default=3,
+                    help="dynamic workloads: frames whose scenes are prepared ahead")
     ap.add_argument("--replicated-fold", action="store_true",
                     help="N > 1: every rank folds every record (default: the cell's owner folds)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",

@@ -169,6 +169,15 @@ rlc_status rlc_context_destroy(rlc_context* ctx);
  * change; the triangle count, material ids, materials and the camera
  * resolution must not (RLC_ERR_INVALID_ARGUMENT).  Synchronizes. */
 rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scene);
+/* rlc_context_update_scene in two steps, so the host builds of later frames
+ * overlap this frame's GPU work and each other: prepare copies the scene's
+ * vertices and starts its host build on a worker thread (at most 4 in
+ * flight), *token identifies it; commit waits for that build, uploads it
+ * and makes it the context's scene (synchronizes).  Tokens are committed in
+ * any order; update_scene = prepare + commit. */
+rlc_status rlc_context_prepare_scene(rlc_context* ctx, const rlc_scene_desc* scene,
+                                     uint64_t* token);
+rlc_status rlc_context_commit_scene(rlc_context* ctx, uint64_t token);
 rlc_status rlc_context_info_get(const rlc_context* ctx, rlc_context_info* info);
 /* Issue device work on `stream` (a cudaStream_t); NULL = the context's own. */
 rlc_status rlc_context_set_stream(rlc_context* ctx, void* stream);

@@ -142,6 +142,8 @@ SIGNATURES = {
     "rlc_context_enable_sample_export": (C.c_int, [_P, C.c_int]),
     "rlc_pass_samples": (C.c_int, [_P, C.c_uint64, C.c_void_p, _u64p]),
     "rlc_context_update_scene": (C.c_int, [_P, C.POINTER(SceneDescC)]),
+    "rlc_context_prepare_scene": (C.c_int, [_P, C.POINTER(SceneDescC), _u64p]),
+    "rlc_context_commit_scene": (C.c_int, [_P, C.c_uint64]),
     "rlc_render_frame_scored": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.c_int32, C.c_int32,
                                           _dp, C.POINTER(RenderResultC), _dp]),
     "rlc_image_write_pfm": (C.c_int, [_dp, C.c_int32, C.c_int32, C.c_char_p]),

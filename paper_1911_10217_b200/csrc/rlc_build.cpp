@@ -67,9 +67,15 @@ class WorkerPool {
     }
     cv_.notify_all();
     work(*batch);  // the submitter takes chunks too
-    // the last chunks are short: spin on the count instead of sleeping on a
-    // condition variable (a futex wake costs tens of microseconds per loop)
-    while (batch->done.load(std::memory_order_acquire) != batch->chunks) cpu_relax();
+    // the last chunks are usually short: spin briefly on the count, then sleep
+    // (several builds share the pool: a spinning submitter would hold a core
+    // the other builds' chunks need)
+    for (int i = 0; i < 2000 && batch->done.load(std::memory_order_acquire) != batch->chunks; ++i)
+      cpu_relax();
+    if (batch->done.load(std::memory_order_acquire) != batch->chunks) {
+      std::unique_lock<std::mutex> lk(batch->m);
+      batch->cv.wait(lk, [&] { return batch->done.load() == batch->chunks; });
+    }
     if (batch->error) std::rethrow_exception(batch->error);
   }
   ~WorkerPool() {
@@ -90,6 +96,7 @@ class WorkerPool {
     int prio = 1;
     std::exception_ptr error;  // under m
     std::mutex m;
+    std::condition_variable cv;
   };
   static void cpu_relax() {
 #if defined(__x86_64__) || defined(__i386__)
@@ -110,7 +117,10 @@ class WorkerPool {
         std::lock_guard<std::mutex> lk(b.m);
         if (!b.error) b.error = std::current_exception();
       }
-      b.done.fetch_add(1, std::memory_order_acq_rel);
+      if (b.done.fetch_add(1, std::memory_order_acq_rel) + 1 == b.chunks) {
+        std::lock_guard<std::mutex> lk(b.m);
+        b.cv.notify_all();
+      }
     }
   }
   void loop() {
@@ -897,7 +907,7 @@ void bin_levels(const std::vector<BvhNode>& bin, std::vector<uint32_t>& order,
 // triangles' vertices, internal nodes from their children), every wide child
 // box padded by S 2^-21 and rounded outward, and the quantized nodes.
 // Leaf words keep the previous frame's kLeafPure bits until phase B.
-void refit_shadow_boxes(const rlc_scene_desc& d, HostScene& out, HostScene& keep) {
+void refit_shadow_boxes(const rlc_scene_desc& d, HostScene& out, const HostScene& base) {
   PhaseTimer pt;
   double S = 0;  // = max |coordinate| of the reference BVH's root box
   {
@@ -911,8 +921,8 @@ void refit_shadow_boxes(const rlc_scene_desc& d, HostScene& out, HostScene& keep
     for (double m : part) S = std::max(S, m);
   }
   out.coord_bound = S;
-  const size_t nt = keep.tris_s.size();
-  out.tris_s = std::move(keep.tris_s);  // positions rewritten, triangle ids kept
+  const size_t nt = base.tris_s.size();
+  if (out.tris_s.size() != nt) out.tris_s = base.tris_s;  // triangle ids of the creation order
   parallel_for(nt, [&](size_t i) {
     TriAccel& ta = out.tris_s[i];
     const uint32_t id = ta.tri_id;
@@ -922,13 +932,12 @@ void refit_shadow_boxes(const rlc_scene_desc& d, HostScene& out, HostScene& keep
     put3(ta.e2, p2 - p0);
   });
   pt.lap("refit tris");
-  const auto& kids = out.wide_kids;  // the creation topology (moved into `out` by the caller)
-  const auto& bin = out.shadow_bin;
-  std::vector<double>& nb = out.refit_box;
-  nb = std::move(keep.refit_box);
+  const auto& kids = base.wide_kids;  // the creation topology
+  const auto& bin = base.shadow_bin;
+  std::vector<double>& nb = out.refit_box;  // scratch of this output scene
   nb.resize(6 * bin.size());
-  const auto& order = out.bin_order;
-  const auto& lstart = out.bin_level_start;
+  const auto& order = base.bin_order;
+  const auto& lstart = base.bin_level_start;
   for (size_t l = 0; l + 1 < lstart.size(); ++l) {
     const uint32_t l0 = lstart[l], l1 = lstart[l + 1];
     parallel_for(l1 - l0, [&](size_t q) {
@@ -955,7 +964,9 @@ void refit_shadow_boxes(const rlc_scene_desc& d, HostScene& out, HostScene& keep
   }
   pt.lap("refit boxes");
   const double pad = S * 0x1.0p-21;
-  out.wide = std::move(keep.wide);  // rewritten in place: boxes (leaf bits in phase B)
+  // internal child words: the creation numbering; boxes rewritten below, leaf
+  // words in phase B
+  if (out.wide.size() != base.wide.size()) out.wide = base.wide;
   parallel_for(kids.size(), [&](size_t w) {
     Wide4& n = out.wide[w];
     for (int c = 0; c < kWide; ++c) {
@@ -985,15 +996,15 @@ void refit_shadow_boxes(const rlc_scene_desc& d, HostScene& out, HostScene& keep
 // Phase B, after the reference BVH: the reference leaf of every shadow-order
 // triangle, and kLeafPure on the leaves whose triangles all lie in one
 // reference leaf (patched into the wide and the quantized nodes).
-void refit_shadow_leaves(HostScene& out) {
+void refit_shadow_leaves(HostScene& out, const HostScene& base) {
   std::vector<uint32_t>& leaf_of_id = out.refit_leaf;  // scratch reused across updates
   leaf_of_id.resize(out.tris.size());
   parallel_for(out.tris.size(), [&](size_t j) { leaf_of_id[out.tris[j].tri_id] = out.tri_leaf[j]; });
   const size_t nt = out.tris_s.size();
   out.tri_leaf_s.resize(nt);
   parallel_for(nt, [&](size_t i) { out.tri_leaf_s[i] = leaf_of_id[out.tris_s[i].tri_id]; });
-  const auto& kids = out.wide_kids;
-  const auto& bin = out.shadow_bin;
+  const auto& kids = base.wide_kids;
+  const auto& bin = base.shadow_bin;
   const bool quant = !out.wide_q.empty();
   parallel_for(kids.size(), [&](size_t w) {
     for (int c = 0; c < kWide; ++c) {
@@ -1010,7 +1021,7 @@ void refit_shadow_leaves(HostScene& out) {
   }, 512);
 }
 
-void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep, bool refit) {
+void build_wide(const rlc_scene_desc& d, HostScene& out, const HostScene* keep, bool refit) {
   PhaseTimer pt;
   if (!refit) out.wide.clear();  // (refit: the boxes of refit_shadow_boxes)
   out.wide_ref.clear();
@@ -1047,8 +1058,17 @@ void build_wide(const rlc_scene_desc& d, HostScene& out, HostScene* keep, bool r
     out.tri_leaf_s = out.tri_leaf;
     out.wide = collapse_wide(use_ref ? out.nodes : sah_over_leaves(out.nodes), nullptr, 0.0,
                              S * 0x1.0p-21);
+  } else if (refit && out.gpu_refit) {
+    // the device refits the tree (launch_refit_shadow): it needs the reference
+    // leaf of every triangle id
+    out.refit_leaf.resize(out.tris.size());
+    parallel_for(out.tris.size(), [&](size_t j) { out.refit_leaf[out.tris[j].tri_id] = out.tri_leaf[j]; });
+    out.tris_s.clear();
+    out.tri_leaf_s.clear();
+    out.wide.clear();
+    out.wide_q.clear();
   } else if (refit) {
-    refit_shadow_leaves(out);  // the boxes were refitted beside the reference BVH
+    refit_shadow_leaves(out, *keep);  // the boxes were refitted beside the reference BVH
   } else {
     std::vector<uint32_t> perm;
     out.tris_s.resize(out.tris.size());
@@ -1214,7 +1234,7 @@ void level_thresholds(double out[kMaxLevel + 1]) {
 void build_reference_bvh(const rlc_scene_desc& d, HostScene& out) { build_bvh(d, out); }
 
 void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, HostScene& out,
-                      HostScene* keep) {
+                      const HostScene* keep) {
   PhaseTimer pt;
   if (d.num_triangles == 0 || d.vertices == nullptr || d.material_ids == nullptr)
     throw InvalidArgument("build_scene_bvh: empty scene");
@@ -1225,18 +1245,9 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
     if (d.material_ids[t] >= d.num_materials)
       throw OutOfRange("build_context: material id out of range");
 
-  if (keep != nullptr) {  // the replaced scene's output buffers: no fresh pages per update
-    out.nodes = std::move(keep->nodes);
-    out.tris = std::move(keep->tris);
-    out.wide_q = std::move(keep->wide_q);
-    out.tri_leaf = std::move(keep->tri_leaf);
-    out.tri_leaf_s = std::move(keep->tri_leaf_s);
-    out.tri_normal = std::move(keep->tri_normal);
-    out.lights = std::move(keep->lights);
-    out.emitter_energy = std::move(keep->emitter_energy);
-    out.emitter_centroid = std::move(keep->emitter_centroid);
-    out.energy_cdf = std::move(keep->energy_cdf);
-  }
+  // A dynamic update (keep = the context's creation scene, read only) writes
+  // into `out`'s own buffers: an output scene recycled from an earlier update
+  // touches no fresh pages, and several updates can be built at once.
   out.mat_values.assign(d.materials, d.materials + size_t(d.num_materials) * 6);
   out.mats.resize(d.num_materials);
   for (uint32_t m = 0; m < d.num_materials; ++m) {
@@ -1263,15 +1274,11 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   const bool refit = keep != nullptr && !keep->shadow_bin.empty() && !keep->wide_kids.empty() &&
                      !(tree_env && (std::string(tree_env) == "reference" ||
                                     std::string(tree_env) == "leaves"));
+  // RLC_HOST_REFIT=1: the shadow tree refitted here instead of on the device
+  const bool host_refit = std::getenv("RLC_HOST_REFIT") != nullptr;
+  out.gpu_refit = refit && !host_refit;
   std::future<void> f_boxes;
-  if (refit) {
-    out.wide_kids = std::move(keep->wide_kids);
-    out.shadow_bin = std::move(keep->shadow_bin);
-    out.bin_first = std::move(keep->bin_first);
-    out.bin_end = std::move(keep->bin_end);
-    out.bin_order = std::move(keep->bin_order);
-    out.bin_level_start = std::move(keep->bin_level_start);
-    out.refit_leaf = std::move(keep->refit_leaf);
+  if (refit && !out.gpu_refit) {
     f_boxes = std::async(std::launch::async, [&] {
       WorkerPool::priority() = 0;  // the reference BVH's loops go first
       refit_shadow_boxes(d, out, *keep);
@@ -1279,7 +1286,7 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   }
   build_bvh(d, out);  // render.cpp:145
   pt.lap("reference bvh");
-  if (refit) f_boxes.get();
+  if (refit && !out.gpu_refit) f_boxes.get();
   pt.lap("refit join");
   // The rest depends only on the scene and the reference BVH and writes
   // disjoint parts of `out`: the traversal trees, the emitters and light
@@ -1414,20 +1421,6 @@ void build_host_scene(const rlc_scene_desc& d, const rlc_render_config& cfg, Hos
   pt.lap("wide join");
   f_emit.get();
   pt.lap("emit join");
-  if (keep != nullptr) {  // the creation light tree and shadow topology, moved on
-    out.order = std::move(keep->order);
-    out.lt_nodes = std::move(keep->lt_nodes);
-    out.lt_begin = std::move(keep->lt_begin);
-    out.lt_energy = std::move(keep->lt_energy);
-    if (!refit && out.wide_kids.empty() && !keep->wide_kids.empty()) {  // refitted, not rebuilt
-      out.shadow_bin = std::move(keep->shadow_bin);
-      out.wide_kids = std::move(keep->wide_kids);
-      out.bin_first = std::move(keep->bin_first);
-      out.bin_end = std::move(keep->bin_end);
-      out.bin_order = std::move(keep->bin_order);
-      out.bin_level_start = std::move(keep->bin_level_start);
-    }
-  }
 }
 
 void parallel_copy(void* dst, const void* src, size_t bytes) {

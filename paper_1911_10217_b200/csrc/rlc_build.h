@@ -49,6 +49,9 @@ struct HostScene {
   std::vector<uint32_t> bin_order, bin_level_start;
   std::vector<double> refit_box;    // [6] per shadow_bin node
   std::vector<uint32_t> refit_leaf; // reference leaf per triangle id
+  // dynamic update whose shadow tree is refitted on the device (the host
+  // leaves tris_s / tri_leaf_s / wide / wide_q empty; refit_leaf is the input)
+  bool gpu_refit = false;
   double scene_lo[3], scene_hi[3];
   double shadow_eps = 0;
   // materials / triangles
@@ -73,16 +76,19 @@ struct HostScene {
 
 // Whole-context build (proj/src/render.cpp:143-157).  Throws InvalidArgument
 // with the reference's messages for empty scenes / no emitters.
-// With `keep` (rlc_context_update_scene): the light tree and the shadow
-// tree's topology are taken from it (moved: `keep` is the scene being
-// replaced) and the shadow tree refitted instead of rebuilt; the fp32 copies
-// of the reference tree that only deferred closest-hit rays use are not
-// built (the device then runs those rays on the fp64 reference tree).
+// With `keep` (rlc_context_update_scene / _prepare_scene: the context's
+// creation scene, read only, so several updates can be built at once): the
+// light tree, emitter list and the shadow tree's topology are those of
+// `keep` (not copied into `out`: the device keeps them) and the shadow tree
+// is refitted instead of rebuilt; the fp32 copies of the reference tree that
+// only deferred closest-hit rays use are not built (the device then runs
+// those rays on the fp64 reference tree).  `out` may be a scene recycled
+// from an earlier update: its buffers are reused.
 // The reference scene BVH alone (build_scene_bvh, bvh.cpp:64-122) into
 // out.nodes / out.tris (diagnostics: rlc_debug_host_bvh times it).
 void build_reference_bvh(const rlc_scene_desc& d, HostScene& out);
 void build_host_scene(const rlc_scene_desc& desc, const rlc_render_config& cfg, HostScene& out,
-                      HostScene* keep = nullptr);
+                      const HostScene* keep = nullptr);
 
 // memcpy on the host build's worker pool (1 MB chunks): moves large device
 // downloads out of pinned staging at host memory bandwidth.

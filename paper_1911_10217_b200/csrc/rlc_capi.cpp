@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -125,28 +126,39 @@ struct SceneBuffers {
   struct Buf {
     void* p = nullptr;
     size_t cap = 0;
-    const void* host = nullptr;  // page-locked host source (cudaHostRegister), if any
-    size_t host_bytes = 0;
   };
   std::vector<Buf> bufs;
   size_t next = 0;
   uint64_t bytes = 0;
-  // Dynamic scene updates reuse the replaced scene's host buffers, so their
-  // addresses are stable from one update to the next: large ones are
-  // page-locked once (cudaHostRegister) and then DMA'd at full rate instead of
-  // being staged by the driver.
+  // Dynamic scene updates write into recycled host scenes (one per update in
+  // flight), whose buffers keep their addresses from one update to the next:
+  // the large ones are page-locked once each (cudaHostRegister) and then
+  // DMA'd at full rate instead of being staged by the driver.
   bool pin = false;
   cudaStream_t stream = nullptr;  // the context stream the copies are ordered on
+  std::vector<std::pair<const void*, size_t>> pinned;
   void begin(cudaStream_t st, bool pin_sources = false) {
     next = 0;
     stream = st;
     pin = pin_sources;
   }
-  void unpin(Buf& b) {
-    if (b.host) cudaHostUnregister(const_cast<void*>(b.host));
-    cudaGetLastError();  // an already-freed source: nothing to undo
-    b.host = nullptr;
-    b.host_bytes = 0;
+  void ensure_pinned(const void* src, size_t n) {
+    for (auto& pr : pinned) {
+      if (pr.first != src) continue;
+      if (pr.second >= n) return;
+      cudaHostUnregister(const_cast<void*>(pr.first));  // grown in place: re-register
+      cudaGetLastError();
+      pr.second = 0;
+      if (cudaHostRegister(const_cast<void*>(src), n, cudaHostRegisterDefault) == cudaSuccess)
+        pr.second = n;
+      else
+        cudaGetLastError();
+      return;
+    }
+    if (cudaHostRegister(const_cast<void*>(src), n, cudaHostRegisterDefault) == cudaSuccess)
+      pinned.emplace_back(src, n);
+    else
+      cudaGetLastError();  // not pinnable: the pageable copy still works
   }
   // copy = false: the contents are known unchanged since the last upload
   // into this slot (a dynamic scene update's frozen arrays)
@@ -167,24 +179,21 @@ struct SceneBuffers {
     }
     if (copy && !v.empty()) {
       const size_t n = v.size() * sizeof(T);
-      if (pin && n >= (size_t(1) << 20) && (b.host != v.data() || b.host_bytes != n)) {
-        unpin(b);
-        if (cudaHostRegister(const_cast<T*>(v.data()), n, cudaHostRegisterDefault) == cudaSuccess) {
-          b.host = v.data();
-          b.host_bytes = n;
-        } else {
-          cudaGetLastError();  // not pinnable: the pageable copy below still works
-        }
-      }
+      if (pin && n >= (size_t(1) << 20)) ensure_pinned(v.data(), n);
       RLC_CK(cudaMemcpyAsync(b.p, v.data(), n, cudaMemcpyHostToDevice, stream));
     }
     return static_cast<T*>(b.p);
   }
+  // host memory pinned for this context must be released before it is freed
+  void unpin_all() {
+    for (auto& pr : pinned) cudaHostUnregister(const_cast<void*>(pr.first));
+    cudaGetLastError();
+    pinned.clear();
+  }
   ~SceneBuffers() {
-    for (Buf& b : bufs) {
-      unpin(b);
+    unpin_all();
+    for (Buf& b : bufs)
       if (b.p) cudaFree(b.p);
-    }
   }
 };
 
@@ -271,6 +280,73 @@ struct rlc_context {
   rlc::HostScene host;
   rlc::DevScene dev{};
   rlc_render_config create_cfg{};  // build_context's config (rlc_context_update_scene)
+  // dynamic updates built ahead (rlc_context_prepare_scene): each builds on a
+  // worker thread from its own copy of the vertices, against the creation
+  // scene `host` (read only), into its own recycled output scene
+  struct FrameScene {
+    rlc::HostScene h;
+    std::vector<double> vertices;
+    rlc_scene_desc desc{};
+    std::future<void> build;
+    uint64_t token = 0;
+    bool busy = false;
+  };
+  std::vector<std::unique_ptr<FrameScene>> frame_scenes;
+  // device refit of the shadow tree for dynamic updates: the creation
+  // topology (uploaded at the first update) and the refitted arrays
+  DeviceArena refit_arena;
+  rlc::RefitTopo refit{};
+  rlc::TriAccel* refit_tris_s = nullptr;
+  uint32_t* refit_tri_leaf_s = nullptr;
+  rlc::Wide4* refit_wide = nullptr;
+  rlc::WideQ* refit_wide_q = nullptr;
+  void ensure_refit_topology() {
+    if (refit.num_wide) return;
+    const rlc::HostScene& h = host;
+    const uint32_t nb = uint32_t(h.shadow_bin.size()), nw = uint32_t(h.wide_kids.size());
+    const uint32_t nt = uint32_t(h.tris_s.size());
+    std::vector<uint32_t> a(nb), b(nb), cnt(nb), parent(nb, 0xffffffffu), leaves;
+    for (uint32_t k = 0; k < nb; ++k) {
+      const rlc::BvhNode& n = h.shadow_bin[k];
+      a[k] = n.a;
+      b[k] = n.b;
+      cnt[k] = n.count;
+      if (n.count > 0) {
+        leaves.push_back(k);
+      } else {
+        parent[n.a] = k;
+        parent[n.b] = k;
+      }
+    }
+    std::vector<uint32_t> kids(4 * size_t(nw)), base(4 * size_t(nw)), ids(nt);
+    for (uint32_t w = 0; w < nw; ++w)
+      for (int c = 0; c < 4; ++c) {
+        kids[4 * size_t(w) + c] = h.wide_kids[w][c];
+        base[4 * size_t(w) + c] = h.wide[w].child[c];
+      }
+    for (uint32_t i = 0; i < nt; ++i) ids[i] = h.tris_s[i].tri_id;
+    DeviceArena& A = refit_arena;
+    refit.bin_a = A.upload(a, stream);
+    refit.bin_b = A.upload(b, stream);
+    refit.bin_count = A.upload(cnt, stream);
+    refit.bin_parent = A.upload(parent, stream);
+    refit.bin_leaves = A.upload(leaves, stream);
+    refit.num_bin = nb;
+    refit.num_leaves = uint32_t(leaves.size());
+    refit.kids = A.upload(kids, stream);
+    refit.base_child = A.upload(base, stream);
+    refit.tri_ids = A.upload(ids, stream);
+    refit.num_tris = nt;
+    refit.box = A.alloc<double>(6 * size_t(nb));
+    refit.arrive = A.alloc<unsigned int>(nb);
+    refit_tris_s = A.alloc<rlc::TriAccel>(nt);
+    refit_tri_leaf_s = A.alloc<uint32_t>(nt);
+    if (h.wide_q.empty()) refit_wide = A.alloc<rlc::Wide4>(nw);
+    else refit_wide_q = A.alloc<rlc::WideQ>(nw);
+    RLC_CK(cudaStreamSynchronize(stream));  // the host vectors above go out of scope
+    refit.num_wide = nw;
+  }
+  uint64_t next_scene_token = 1;
   SceneBuffers scene_bufs;  // the device scene (upload_scene)
   DeviceArena lights_ord_arena;  // dev.lights_ord, rebuilt on the device after every upload
   size_t lights_ord_cap = 0;
@@ -842,49 +918,130 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
   });
 }
 
+namespace {
+
+// rlc_context_update_scene's argument checks (the reference's build_context
+// has no such call; DESIGN.md 5.10 defines the semantics).
+void check_update(const rlc_context* ctx, const rlc_scene_desc* scene) {
+  require(ctx != nullptr && scene != nullptr, "rlc_context_update_scene: null argument");
+  const rlc::HostScene& old = ctx->host;
+  require(scene->num_triangles == old.tri_mat.size() &&
+              scene->num_materials * 6 == old.mat_values.size() &&
+              scene->width == old.cam.width && scene->height == old.cam.height,
+          "rlc_context_update_scene: triangle count, materials and resolution must not change");
+  require(scene->vertices != nullptr, "rlc_context_update_scene: null vertices");
+  for (uint32_t t = 0; t < scene->num_triangles; ++t)
+    require(scene->material_ids[t] == old.tri_mat[t],
+            "rlc_context_update_scene: material ids must not change");
+  for (size_t i = 0; i < old.mat_values.size(); ++i)
+    require(scene->materials[i] == old.mat_values[i],
+            "rlc_context_update_scene: materials must not change");
+}
+
+// build_context(scene) (render.cpp:143-157) with the light tree of the
+// context's creation (same emitter order, topology and node energies), on a
+// worker thread; returns its token.
+uint64_t prepare_scene(rlc_context* ctx, const rlc_scene_desc* scene) {
+  check_update(ctx, scene);
+  rlc_context::FrameScene* f = nullptr;
+  for (auto& p : ctx->frame_scenes)
+    if (!p->busy) {
+      f = p.get();
+      break;
+    }
+  if (!f) {
+    require(ctx->frame_scenes.size() < 4, "rlc_context_prepare_scene: at most 4 scenes in flight");
+    ctx->frame_scenes.push_back(std::make_unique<rlc_context::FrameScene>());
+    f = ctx->frame_scenes.back().get();
+  }
+  f->vertices.assign(scene->vertices, scene->vertices + size_t(scene->num_triangles) * 9);
+  f->desc = *scene;
+  f->desc.vertices = f->vertices.data();
+  f->desc.material_ids = ctx->host.tri_mat.data();  // validated equal, frozen
+  f->desc.materials = ctx->host.mat_values.data();
+  f->token = ctx->next_scene_token++;
+  f->busy = true;
+  const rlc_render_config cfg = ctx->create_cfg;
+  const rlc::HostScene* base = &ctx->host;
+  f->build = std::async(std::launch::async,
+                        [f, cfg, base] { rlc::build_host_scene(f->desc, cfg, f->h, base); });
+  return f->token;
+}
+
+void commit_scene(rlc_context* ctx, uint64_t token) {
+  rlc_context::FrameScene* f = nullptr;
+  for (auto& p : ctx->frame_scenes)
+    if (p->busy && p->token == token) f = p.get();
+  require(f != nullptr, "rlc_context_commit_scene: no prepared scene with this token");
+  const bool report = std::getenv("RLC_UPDATE_TIMING") != nullptr;
+  auto t = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!report) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "update_scene %s %.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  };
+  try {
+    f->build.get();
+  } catch (...) {
+    f->busy = false;
+    throw;
+  }
+  lap("host build wait");
+  RLC_CK(cudaSetDevice(ctx->device));
+  ctx->sync_all();  // the previous frame's kernels read the buffers
+  lap("sync");
+  rlc::DevScene d{};
+  d.count_work = ctx->dev.count_work;
+  d.lights_ord = ctx->dev.lights_ord;
+  upload_scene(f->h, ctx->scene_bufs, d, ctx->stream, true);
+  if (f->h.gpu_refit) {  // the shadow tree refitted on the device
+    ctx->ensure_refit_topology();
+    const double* verts = ctx->scene_bufs.put(f->vertices);
+    const uint32_t* leaf_of_id = ctx->scene_bufs.put(f->h.refit_leaf);
+    rlc::launch_refit_shadow(ctx->refit, verts, leaf_of_id, f->h.coord_bound * 0x1.0p-21,
+                             ctx->refit_tris_s, ctx->refit_tri_leaf_s, ctx->refit_wide,
+                             ctx->refit_wide_q,
+                             reinterpret_cast<unsigned int*>(ctx->counters + rlc::kCntErr),
+                             ctx->stream);
+    RLC_CK(cudaGetLastError());
+    d.tris_s = ctx->refit_tris_s;
+    d.tri_leaf_s = ctx->refit_tri_leaf_s;
+    d.wide = ctx->refit_wide;
+    d.wide_q = ctx->refit_wide_q;
+  }
+  ctx->dev = d;
+  ctx->build_light_order();
+  // the copies complete before the output scene is recycled and before any
+  // stream reads the new scene
+  RLC_CK(cudaStreamSynchronize(ctx->stream));
+  f->busy = false;
+  ++ctx->scene_gen;  // captured pass graphs hold the old scene's pointers
+  lap("upload");
+}
+
+}  // namespace
+
 rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scene) {
   return guarded([&] {
-    require(ctx != nullptr && scene != nullptr, "rlc_context_update_scene: null argument");
-    rlc::HostScene& old = ctx->host;
-    require(scene->num_triangles == old.tri_mat.size() &&
-                scene->num_materials * 6 == old.mat_values.size() &&
-                scene->width == old.cam.width && scene->height == old.cam.height,
-            "rlc_context_update_scene: triangle count, materials and resolution must not change");
-    for (uint32_t t = 0; t < scene->num_triangles; ++t)
-      require(scene->material_ids[t] == old.tri_mat[t],
-              "rlc_context_update_scene: material ids must not change");
-    for (size_t i = 0; i < old.mat_values.size(); ++i)
-      require(scene->materials[i] == old.mat_values[i],
-              "rlc_context_update_scene: materials must not change");
-    RLC_CK(cudaSetDevice(ctx->device));
-    const bool report = std::getenv("RLC_UPDATE_TIMING") != nullptr;
-    auto t = std::chrono::steady_clock::now();
-    auto lap = [&](const char* what) {
-      if (!report) return;
-      const auto n = std::chrono::steady_clock::now();
-      std::fprintf(stderr, "update_scene %s %.2f ms\n", what,
-                   std::chrono::duration<double, std::milli>(n - t).count());
-      t = n;
-    };
-    // build_context(scene) (render.cpp:143-157) with the light tree of the
-    // context's creation: same emitter order, topology and node energies
-    rlc::HostScene h;
-    rlc::build_host_scene(*scene, ctx->create_cfg, h, &old);
-    lap("host build");
-    ctx->sync_all();  // the previous frame's kernels read the buffers
-    lap("sync");
-    rlc::DevScene d{};
-    d.count_work = ctx->dev.count_work;
-    d.lights_ord = ctx->dev.lights_ord;
-    upload_scene(h, ctx->scene_bufs, d, ctx->stream, true);
-    ctx->dev = d;
-    ctx->build_light_order();
-    // the copies complete before the host buffers are reused or freed and
-    // before any stream reads the new scene
-    RLC_CK(cudaStreamSynchronize(ctx->stream));
-    ctx->host = std::move(h);
-    ++ctx->scene_gen;  // captured pass graphs hold the old scene's pointers
-    lap("upload");
+    RLC_CK(cudaSetDevice(ctx ? ctx->device : 0));
+    commit_scene(ctx, prepare_scene(ctx, scene));
+  });
+}
+
+rlc_status rlc_context_prepare_scene(rlc_context* ctx, const rlc_scene_desc* scene,
+                                     uint64_t* token) {
+  return guarded([&] {
+    require(token != nullptr, "rlc_context_prepare_scene: null token");
+    *token = prepare_scene(ctx, scene);
+  });
+}
+
+rlc_status rlc_context_commit_scene(rlc_context* ctx, uint64_t token) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_commit_scene: null context");
+    commit_scene(ctx, token);
   });
 }
 

@@ -2823,6 +2823,167 @@ __global__ void k_resolve(Framebuf fb, uint32_t npix, double* __restrict__ image
   for (int a = 0; a < 3; ++a) image[3 * i + a] = c > 0 ? fb.sum[3 * i + a] / double(c) : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Device refit of the shadow tree for a dynamic update (the host refit of
+// rlc_build.cpp, same arithmetic): shadow-order triangle records and their
+// reference leaves, binary node boxes bottom up (the second child to finish
+// builds its parent's box), 4-wide child boxes padded by S 2^-21 and rounded
+// outward, leaf words with kLeafPure, and the quantized nodes.  Any
+// conservative tree is exact.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ V3 vtx(const double* v, uint32_t t, int k) {
+  return V3{v[size_t(t) * 9 + 3 * k], v[size_t(t) * 9 + 3 * k + 1], v[size_t(t) * 9 + 3 * k + 2]};
+}
+
+__global__ void k_refit_tris(RefitTopo t, const double* __restrict__ vertices,
+                             const uint32_t* __restrict__ leaf_of_id, TriAccel* __restrict__ tris_s,
+                             uint32_t* __restrict__ tri_leaf_s) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.num_tris) return;
+  const uint32_t id = t.tri_ids[i];
+  const V3 p0 = vtx(vertices, id, 0), p1 = vtx(vertices, id, 1), p2 = vtx(vertices, id, 2);
+  const V3 e1 = p1 - p0, e2 = p2 - p0;
+  TriAccel a;
+  a.p0[0] = p0.x, a.p0[1] = p0.y, a.p0[2] = p0.z;
+  a.e1[0] = e1.x, a.e1[1] = e1.y, a.e1[2] = e1.z;
+  a.e2[0] = e2.x, a.e2[1] = e2.y, a.e2[2] = e2.z;
+  a.tri_id = id;
+  a.pad = 0;
+  tris_s[i] = a;
+  tri_leaf_s[i] = leaf_of_id[id];
+}
+
+__global__ void k_refit_boxes(RefitTopo t, const double* __restrict__ vertices) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= t.num_leaves) return;
+  uint32_t k = t.bin_leaves[q];
+  double lo[3] = {HUGE_VAL, HUGE_VAL, HUGE_VAL}, hi[3] = {-HUGE_VAL, -HUGE_VAL, -HUGE_VAL};
+  const uint32_t a = t.bin_a[k], n = t.bin_count[k];
+  for (uint32_t i = a; i < a + n; ++i) {
+    const uint32_t id = t.tri_ids[i];
+    for (int c = 0; c < 3; ++c) {
+      const V3 p = vtx(vertices, id, c);
+      lo[0] = smin(lo[0], p.x), lo[1] = smin(lo[1], p.y), lo[2] = smin(lo[2], p.z);
+      hi[0] = smax(hi[0], p.x), hi[1] = smax(hi[1], p.y), hi[2] = smax(hi[2], p.z);
+    }
+  }
+  while (true) {
+    double* o = t.box + 6 * size_t(k);
+    for (int c = 0; c < 3; ++c) {
+      o[c] = lo[c];
+      o[3 + c] = hi[c];
+    }
+    const uint32_t p = t.bin_parent[k];
+    if (p == 0xffffffffu) return;
+    __threadfence();
+    if (atomicAdd(t.arrive + p, 1u) == 0) return;  // the sibling builds the parent
+    __threadfence();
+    const volatile double* ba = t.box + 6 * size_t(t.bin_a[p]);
+    const volatile double* bb = t.box + 6 * size_t(t.bin_b[p]);
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = smin(ba[c], bb[c]);
+      hi[c] = smax(ba[3 + c], bb[3 + c]);
+    }
+    k = p;
+  }
+}
+
+// quantize_wide (rlc_build.cpp) for one node: the same planes.
+__device__ void quantize_node(const Wide4& n, WideQ& q, unsigned int* err) {
+  for (int c = 0; c < 4; ++c) {
+    q.child[c] = n.child[c];
+    q.valid |= n.child[c] != kWideEmpty ? (1u << c) : 0u;
+  }
+  for (int a = 0; a < 3; ++a) {
+    float lo = HUGE_VALF, hi = -HUGE_VALF;
+    for (int c = 0; c < 4; ++c)
+      if (n.child[c] != kWideEmpty) {
+        lo = fminf(lo, n.lo[a][c]);
+        hi = fmaxf(hi, n.hi[a][c]);
+      }
+    if (!(lo <= hi)) lo = hi = 0.f;
+    q.origin[a] = lo;
+    const double ext = double(hi) - double(lo);
+    int e = -126;
+    if (ext > 0) {
+      frexp(ext / 250.0, &e);
+      while (e > -126 && ldexp(250.0, e - 1) >= ext) --e;
+      while (e < 127 && ldexp(250.0, e) < ext) ++e;
+      e = max(-126, min(127, e));
+    }
+    q.ex[a] = uint8_t(e + 127);
+    const float scale = ldexpf(1.0f, e);
+    for (int c = 0; c < 4; ++c) {
+      if (n.child[c] == kWideEmpty) {
+        q.qlo[a][c] = 255;
+        q.qhi[a][c] = 0;
+        continue;
+      }
+      const double L = double(n.lo[a][c]), Hh = double(n.hi[a][c]);
+      int ql = int(floor((L - double(lo)) / double(scale)));
+      ql = max(0, min(255, ql));
+      while (ql > 0 && double(lo) + double(ql) * double(scale) > L) --ql;
+      int qh = int(ceil((Hh - double(lo)) / double(scale)));
+      qh = max(0, min(255, qh));
+      while (qh < 255 && double(lo) + double(qh) * double(scale) < Hh) ++qh;
+      if (double(lo) + double(ql) * double(scale) > L || double(lo) + double(qh) * double(scale) < Hh)
+        atomicOr(err, kErrCheck);  // (cannot happen: 250 steps span the extent)
+      q.qlo[a][c] = uint8_t(ql);
+      q.qhi[a][c] = uint8_t(qh);
+    }
+  }
+}
+
+__global__ void k_refit_wide(RefitTopo t, const uint32_t* __restrict__ tri_leaf_s, double pad,
+                             Wide4* __restrict__ wide, WideQ* __restrict__ wide_q,
+                             unsigned int* err) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= t.num_wide) return;
+  Wide4 n{};
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t b = t.kids[4 * size_t(w) + c];
+    if (b == kWideEmpty) {
+      n.child[c] = kWideEmpty;
+      for (int a = 0; a < 3; ++a) {
+        n.lo[a][c] = HUGE_VALF;
+        n.hi[a][c] = -HUGE_VALF;
+      }
+      continue;
+    }
+    const double* bx = t.box + 6 * size_t(b);
+    for (int a = 0; a < 3; ++a) {  // as collapse_wide (no origin, no growth)
+      n.lo[a][c] = __double2float_rd(bx[a] - pad);
+      n.hi[a][c] = __double2float_ru(bx[3 + a] + pad);
+    }
+    const uint32_t cnt = t.bin_count[b];
+    if (cnt > 0) {
+      const uint32_t first = t.bin_a[b];
+      bool pure = true;
+      for (uint32_t k = 1; k < cnt; ++k) pure &= tri_leaf_s[first + k] == tri_leaf_s[first];
+      n.child[c] = kWideLeaf | ((cnt - 1) << 28) | (pure ? kLeafPure : 0u) | first;
+    } else {
+      n.child[c] = t.base_child[4 * size_t(w) + c];  // internal: the creation numbering
+    }
+  }
+  if (wide) wide[w] = n;
+  if (wide_q) {
+    WideQ q{};
+    quantize_node(n, q, err);
+    wide_q[w] = q;
+  }
+}
+
+void launch_refit_shadow(const RefitTopo& t, const double* vertices, const uint32_t* leaf_of_id,
+                         double pad, TriAccel* tris_s, uint32_t* tri_leaf_s, Wide4* wide,
+                         WideQ* wide_q, unsigned int* err, cudaStream_t st) {
+  cudaMemsetAsync(t.arrive, 0, sizeof(unsigned int) * t.num_bin, st);
+  k_refit_tris<<<blocks_for(t.num_tris, 256), 256, 0, st>>>(t, vertices, leaf_of_id, tris_s,
+                                                           tri_leaf_s);
+  k_refit_boxes<<<blocks_for(t.num_leaves, 128), 128, 0, st>>>(t, vertices);
+  k_refit_wide<<<blocks_for(t.num_wide, 128), 128, 0, st>>>(t, tri_leaf_s, pad, wide, wide_q, err);
+  count_launch(3);
+}
+
 // LightOrd at every light-tree position: the record of emitter order[pos].
 __global__ void k_light_order(DevScene sc, LightOrd* __restrict__ out) {
   const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;

@@ -326,6 +326,26 @@ void launch_intersect_batch(const DevScene& sc, uint32_t n, const double* org, c
                             double tmin, double* t_out, int32_t* tri_out,
                             unsigned long long* counters, cudaStream_t st, bool sah_only = false);
 void launch_resolve(const Framebuf& fb, uint32_t npix, double* image, cudaStream_t st);
+// Dynamic updates: the creation shadow tree refitted on the device to the
+// moved triangles.  Topology arrays are the creation's.
+struct RefitTopo {
+  const uint32_t* bin_a;       // [bin node] leaf: first tris_s position; internal: left child
+  const uint32_t* bin_b;       // internal: right child
+  const uint32_t* bin_count;   // leaf: triangles (> 0); internal: 0
+  const uint32_t* bin_parent;  // parent bin node (0xffffffff: the root)
+  const uint32_t* bin_leaves;  // the leaf bin nodes
+  uint32_t num_bin, num_leaves;
+  const uint32_t* kids;        // [wide node][4] bin node of each child, or kWideEmpty
+  const uint32_t* base_child;  // [wide node][4] the creation's child words
+  uint32_t num_wide;
+  const uint32_t* tri_ids;     // [tris_s position] triangle id (creation order)
+  uint32_t num_tris;
+  double* box;                 // [bin node][6] scratch
+  unsigned int* arrive;        // [bin node] scratch (zeroed by the launcher)
+};
+void launch_refit_shadow(const RefitTopo& t, const double* vertices, const uint32_t* leaf_of_id,
+                         double pad, TriAccel* tris_s, uint32_t* tri_leaf_s, Wide4* wide,
+                         WideQ* wide_q, unsigned int* err, cudaStream_t st);
 // sc.lights_ord from sc.lights, sc.order and sc.emitter_mat.
 void launch_light_order(const DevScene& sc, LightOrd* out, cudaStream_t st);
 // Per-vertex parity records of the pass in `p` (rlc_pass_samples).

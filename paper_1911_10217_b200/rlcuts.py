@@ -136,6 +136,20 @@ class RenderContext:
         _check(_lib.load().rlc_context_update_scene(self.handle, C.byref(desc)))
         self.scene, self._desc = scene, desc
 
+    def prepare_scene(self, scene: Scene) -> int:
+        """Start the host build of a later frame's scene (rlc_context_prepare_scene);
+        returns the token commit_scene takes."""
+        desc = scene.desc()
+        tok = C.c_uint64()
+        _check(_lib.load().rlc_context_prepare_scene(self.handle, C.byref(desc), C.byref(tok)))
+        return tok.value
+
+    def commit_scene(self, token: int, scene: Scene | None = None):
+        """Make a prepared scene the context's (rlc_context_commit_scene)."""
+        _check(_lib.load().rlc_context_commit_scene(self.handle, token))
+        if scene is not None:
+            self.scene = scene
+
     @property
     def base_tile(self) -> float:
         return self.info()["base_tile"]

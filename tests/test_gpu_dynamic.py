@@ -85,3 +85,32 @@ def test_c4_scene_many_updates_bit_exact(ref):
         rlcuts.render_pass(ctx, cfg, f, grid, fb)
         assert rlcuts.end_of_pass_update(grid, ctx, cfg.cut) == rr.run_pass(f)[0]
     assert_same_state(grid, fb, rr)
+
+
+@pytest.mark.parametrize("ahead", [1, 3])
+def test_prepared_scenes_match_reference(ref, ahead):
+    """rlc_context_prepare_scene / _commit_scene: the host builds of the next
+    `ahead` frames run concurrently with each other and the GPU; every frame
+    must still equal the reference driven through update_scene."""
+    scene0 = scenes.maze(4096, seed=11, width=64, height=48)
+    cfg = rlcuts.RenderConfig(spp=6, passes=6, sampler=RL,
+                              hash=rlcuts.HashConfig(base_tile=0.05))
+    ctx = rlcuts.build_context(scene0, cfg)
+    grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+    rr = ref.RefRun(scene0, cfg)
+    frames = [scene0] + [scenes.displace_emitters(scene0, f, amplitude=0.05) for f in range(1, 6)]
+    tokens = {}
+    for f in range(6):
+        if f > 0:
+            for q in range(f, min(6, f + ahead + 1)):
+                if q not in tokens:
+                    tokens[q] = ctx.prepare_scene(frames[q])
+            ctx.commit_scene(tokens.pop(f), frames[f])
+            rr.update_scene(frames[f])
+        rlcuts.render_pass(ctx, cfg, f, grid, fb)
+        ch = rlcuts.end_of_pass_update(grid, ctx, cfg.cut)
+        rch, _ = rr.run_pass(f)
+        assert ch == rch, f
+    assert_same_state(grid, fb, rr)
+    with pytest.raises(ValueError, match="token"):
+        ctx.commit_scene(123456)
