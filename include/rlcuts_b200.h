@@ -171,7 +171,7 @@ rlc_status rlc_context_destroy(rlc_context* ctx);
 rlc_status rlc_context_update_scene(rlc_context* ctx, const rlc_scene_desc* scene);
 /* rlc_context_update_scene in two steps, so the host builds of later frames
  * overlap this frame's GPU work and each other: prepare copies the scene's
- * vertices and starts its host build on a worker thread (at most 4 in
+ * vertices and starts its host build on a worker thread (at most 8 in
  * flight), *token identifies it; commit waits for that build, uploads it
  * and makes it the context's scene (synchronizes).  Tokens are committed in
  * any order; update_scene = prepare + commit. */

@@ -950,7 +950,7 @@ uint64_t prepare_scene(rlc_context* ctx, const rlc_scene_desc* scene) {
       break;
     }
   if (!f) {
-    require(ctx->frame_scenes.size() < 4, "rlc_context_prepare_scene: at most 4 scenes in flight");
+    require(ctx->frame_scenes.size() < 8, "rlc_context_prepare_scene: at most 8 scenes in flight");
     ctx->frame_scenes.push_back(std::make_unique<rlc_context::FrameScene>());
     f = ctx->frame_scenes.back().get();
   }
