@@ -318,9 +318,13 @@ rlc_status rlc_render_passes_async(const rlc_context* ctx, const rlc_render_conf
 rlc_status rlc_end_of_pass_update_async(rlc_grid* grid, const rlc_context* ctx,
                                         const rlc_cut_config* cut);
 rlc_status rlc_grid_last_changes(const rlc_grid* grid, uint32_t* changes);
-/* ---- screen-band sharding: the exchanged update record ------------------
- * One learned update (the update_q call of render.cpp:111-117) as exchanged
- * between ranks: the cell key, the cluster and the feedback value.  32 B. */
+/* ---- screen-band sharding: one learned update -----------------------------
+ * One update_q call of render.cpp:111-117 -- the cell key, the cluster and
+ * the feedback value, 32 B -- as the CPU model of the exchange
+ * (oracle/restate.py, rlcuts.RECORD_DTYPE) files it.  The device blocks of
+ * rlc_shard_trace carry the same update naming the cell by its table slot
+ * (the tables are identical on every rank) and the key only for cells new
+ * in the pass; their layout is the library's. */
 typedef struct rlc_update_record {
   int32_t qx, qy, qz;
   uint32_t qn, level, cluster;
@@ -333,19 +337,25 @@ typedef struct rlc_update_record {
  * enqueue on the context stream and return without a host synchronization.
  *
  * 1. rlc_shard_trace: traces the band and files its update records in
- *    canonical order into a device block of *block_bytes (a 16-byte header
- *    with the count, then `cap_records` 32-byte slots; cap_records >= the
- *    band's path vertices, the same on every rank).
+ *    canonical order into a device block of *block_bytes = 32 (cap_records
+ *    + 1) bytes (a 32-byte header slot with the count, then `cap_records`
+ *    32-byte record slots; cap_records >= the band's path vertices, the
+ *    same on every rank).
  * 2. the caller all-gathers the blocks of all ranks, rank-major (NCCL
- *    ncclAllGather of block_bytes, or any transport);
+ *    ncclAllGather of block_bytes, or any transport), into device memory
+ *    that stays valid until rlc_shard_finish;
  * 3. rlc_shard_fold: inserts the pass's new keys in canonical order and
  *    folds, in canonical order per cut entry, the records of every cell
- *    (owner_fold = 0) or of the cells this rank owns (hash(CellKey) % nranks
- *    == rank); *q_before_slots (device, *slots doubles) holds q_before per
- *    record slot, zero for the records other ranks fold;
- * 4. owner_fold: the caller sums q_before_slots over the ranks (ncclAllReduce);
- * 5. rlc_shard_finish: replays the other ranks' records onto this rank's
- *    cut entries (owner_fold) and accumulates the band's radiance;
+ *    (owner_fold = 0) or of the cells this rank owns (table slot % nranks
+ *    == rank).  Per exchange slot (*slots of them, device arrays):
+ *    *q_before_slots, the record's q_before, and *seg_counts, at the last
+ *    record of each cut entry the entry's record count -- both zero for the
+ *    records other ranks fold;
+ * 4. owner_fold: the caller sums q_before_slots and seg_counts over the
+ *    ranks (ncclAllReduce);
+ * 5. rlc_shard_finish: advances the cut entries other ranks folded to the
+ *    state their last record leaves (owner_fold) and accumulates the band's
+ *    radiance;
  * 6. rlc_end_of_pass_update(_async): split-collapse, identical on every rank.
  * rlc_shard_frame does 1-6 with NCCL on the context stream (one call per
  * frame per rank, no host synchronization; errors surface at the next
@@ -357,7 +367,7 @@ rlc_status rlc_shard_trace(const rlc_context* ctx, const rlc_render_config* conf
                            uint64_t* block_bytes);
 rlc_status rlc_shard_fold(const rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
                           const void* blocks, uint32_t nranks, uint32_t rank, int owner_fold,
-                          double** q_before_slots, uint64_t* slots);
+                          double** q_before_slots, uint32_t** seg_counts, uint64_t* slots);
 rlc_status rlc_shard_finish(const rlc_context* ctx, rlc_grid* grid, rlc_framebuffer* fb,
                             uint32_t rank, int owner_fold);
 /* Waits for the context's work and reports device errors of the grid. */

@@ -461,42 +461,44 @@ struct rlc_context {
   // of the fold over nranks x cap gathered record slots
   DeviceArena blockarena;
   void* block = nullptr;
-  uint64_t block_cap = 0;  // record slots of `block`
-  uint64_t xb_slots = 0, xb_entries = 0;
+  uint64_t block_cap = 0;    // record slots of this pass's block (the caller's cap)
+  uint64_t block_alloc = 0;  // record slots allocated
+  uint64_t xb_slots = 0;
+  // block bytes: a header slot and cap record slots of 32 B
+  uint64_t block_bytes() const { return (block_cap + 1) * sizeof(rlc::ExchangeRecord); }
   void ensure_block(uint64_t cap) {
-    if (cap <= block_cap && block) return;
+    block_cap = cap;
+    if (cap <= block_alloc && block) return;
     sync_all();
     blockarena.release();
-    block = blockarena.alloc<unsigned char>(sizeof(rlc::RecordBlockHeader) + cap * 32);
-    block_cap = cap;
+    block = blockarena.alloc<rlc::ExchangeRecord>(cap + 1);
+    block_alloc = cap;
   }
-  void ensure_exchange(uint32_t nranks, uint32_t cap, uint64_t entries) {
-    const uint64_t slots = uint64_t(nranks) * cap;
+  // exchange slots of nranks blocks of cap + 1 slots (header + records)
+  void ensure_exchange(uint32_t nranks, uint32_t cap) {
+    const uint64_t slots = uint64_t(nranks) * (uint64_t(cap) + 1);
     xb.nranks = nranks;
-    xb.cap = cap;
-    if (slots <= xb_slots && entries <= xb_entries) return;
+    xb.stride = cap + 1;
+    if (slots <= xb_slots) return;
     sync_all();
     xarena.release();
-    const uint64_t n = std::max(slots, xb_slots), m = std::max(entries, xb_entries);
-    xb.contig = xarena.alloc<rlc::UpdateRecord>(n);
-    xb.slots = xarena.alloc<uint32_t>(n);
+    const uint64_t n = slots;
+    xb.rec = nullptr;
     xb.cellx = xarena.alloc<uint32_t>(n);
     xb.kflag = xarena.alloc<uint8_t>(n);
     xb.keys = xarena.alloc<uint32_t>(n);
     xb.vals = xarena.alloc<uint32_t>(n);
     xb.keys_alt = xarena.alloc<uint32_t>(n);
     xb.vals_alt = xarena.alloc<uint32_t>(n);
-    xb.hist = xarena.alloc<uint32_t>((size_t(n) / rlc::kSortTile + 2) * 256);
+    xb.hist = xarena.alloc<uint32_t>((size_t(n) / rlc::kSortTileSmall + 2) * 256);
     xb.block_counts = xarena.alloc<uint32_t>(n / 2048 + 2);
     xb.sort_count = xarena.alloc<unsigned int>(2);
     xb.q_rec = xarena.alloc<double>(n);
-    xb.seg_count = xarena.alloc<uint32_t>(m);
-    xb.seg_last = xarena.alloc<uint32_t>(m);
-    RLC_CK(cudaMemsetAsync(xb.seg_count, 0, 4 * m, stream));
-    RLC_CK(cudaMemsetAsync(xb.seg_last, 0, 4 * m, stream));
+    xb.seg_n = xarena.alloc<uint32_t>(n);
+    xb.pend = xarena.alloc<uint32_t>(n);
+    xb.pend_count = xarena.alloc<unsigned int>(1);
     xb.nk = alloc_new_keys(xarena, n, stream);
     xb_slots = n;
-    xb_entries = m;
   }
   // render_frame cache (prepare_frame_cache)
   rlc_grid* frame_grid = nullptr;
@@ -1325,6 +1327,7 @@ rlc_status rlc_grid_create(const rlc_context* ctx, const rlc_render_config* cfg,
     d.cdf = A.alloc<double>(cap * M);
     d.visits = A.alloc<uint32_t>(cap * M);
     d.cell_key = A.alloc<uint32_t>(5 * cap);
+    d.cell_slot = A.alloc<uint32_t>(cap);
     d.touched = A.alloc<uint32_t>(cap);
     // cuts too large for k_split's shared-memory rows work in global scratch
     d.split_scratch = size_t(M) * 32 > rlc::kSplitSmemMax
@@ -1591,13 +1594,13 @@ void shard_fold(rlc_context* ctx, const rlc_render_config* config, rlc_grid* gri
   (void)config;
   RLC_CK(cudaSetDevice(ctx->device));
   const PassParamsHolder& S = ctx->shard;
-  ctx->ensure_exchange(nranks, uint32_t(ctx->block_cap), uint64_t(grid->dev.capacity) * grid->dev.M);
+  ctx->ensure_exchange(nranks, uint32_t(ctx->block_cap));
+  ctx->xb.rec = static_cast<const rlc::ExchangeRecord*>(blocks);
   ctx->stage(9, [&] {
-    rlc::launch_shard_fold(S.g, S.p, blocks, sizeof(rlc::RecordBlockHeader) + ctx->block_cap * 32,
-                           rank, owner_fold != 0, grid->key_bits, ctx->xb, ctx->stream);
+    rlc::launch_shard_fold(S.g, S.p, rank, owner_fold != 0, ctx->xb, ctx->stream);
   });
   ctx->stage(3, [&] {
-    rlc::launch_shard_sortfold(S.g, S.p, grid->key_bits, ctx->xb, ctx->stream);
+    rlc::launch_shard_sortfold(S.g, S.p, grid->key_bits, owner_fold != 0, ctx->xb, ctx->stream);
   });
   ctx->shard_folded = true;
   RLC_CK(cudaGetLastError());
@@ -1632,19 +1635,21 @@ rlc_status rlc_shard_trace(const rlc_context* cctx, const rlc_render_config* con
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
     *block = ctx->block;
-    *block_bytes = sizeof(rlc::RecordBlockHeader) + ctx->block_cap * 32;
+    *block_bytes = ctx->block_bytes();
   });
 }
 
 rlc_status rlc_shard_fold(const rlc_context* cctx, const rlc_render_config* config,
                           rlc_grid* grid, const void* blocks, uint32_t nranks, uint32_t rank,
-                          int owner_fold, double** q_before_slots, uint64_t* slots) {
+                          int owner_fold, double** q_before_slots, uint32_t** seg_counts,
+                          uint64_t* slots) {
   return guarded([&] {
     require(cctx != nullptr && config != nullptr, "rlc_shard_fold: null argument");
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     shard_fold(ctx, config, grid, blocks, nranks, rank, owner_fold);
     if (q_before_slots) *q_before_slots = ctx->xb.q_rec;
-    if (slots) *slots = uint64_t(nranks) * ctx->block_cap;
+    if (seg_counts) *seg_counts = ctx->xb.seg_n;
+    if (slots) *slots = uint64_t(nranks) * ctx->xb.stride;
   });
 }
 
@@ -1757,7 +1762,7 @@ rlc_status rlc_shard_frame(const rlc_context* cctx, const rlc_render_config* con
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     require(comm->device == ctx->device, "rlc_shard_frame: communicator on another device");
     shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
-    const uint64_t bb = sizeof(rlc::RecordBlockHeader) + ctx->block_cap * 32;
+    const uint64_t bb = ctx->block_bytes();
     if (comm->gathered_bytes < bb * comm->nranks) {
       ctx->sync_all();
       comm->arena.release();
@@ -1769,11 +1774,15 @@ rlc_status rlc_shard_frame(const rlc_context* cctx, const rlc_render_config* con
     nccl_check(nccl().all_gather(ctx->block, comm->gathered, bb, ncclUint8, comm->comm, st),
                "ncclAllGather");
     shard_fold(ctx, config, grid, comm->gathered, comm->nranks, comm->rank, owner_fold);
-    if (owner_fold && comm->nranks > 1)  // q_before of every record from its cell's owner
-      nccl_check(nccl().all_reduce(ctx->xb.q_rec, ctx->xb.q_rec,
-                                   size_t(comm->nranks) * ctx->block_cap, ncclFloat64, ncclSum,
+    if (owner_fold && comm->nranks > 1) {  // q_before and entry counts from the cells' owners
+      const size_t slots = size_t(comm->nranks) * ctx->xb.stride;
+      nccl_check(nccl().all_reduce(ctx->xb.q_rec, ctx->xb.q_rec, slots, ncclFloat64, ncclSum,
                                    comm->comm, st),
                  "ncclAllReduce");
+      nccl_check(nccl().all_reduce(ctx->xb.seg_n, ctx->xb.seg_n, slots, ncclUint32, ncclSum,
+                                   comm->comm, st),
+                 "ncclAllReduce");
+    }
     shard_finish(ctx, grid, fb, comm->rank, owner_fold);
     RLC_CK(cudaMemsetAsync(grid->d_changes, 0, 4, st));
     enqueue_eop(grid, ctx, &config->cut, grid->d_changes);  // split-collapse: identical on every rank

@@ -712,6 +712,7 @@ __global__ void __launch_bounds__(256) k_commit(DevGrid g, NewKeys nk) {
       g.slot_keys[2 * size_t(slot)] = lo;
       g.slot_keys[2 * size_t(slot) + 1] = hi;
       g.slot_cell[slot] = cid;
+      g.cell_slot[cid] = slot;
       const Key k = unpack_key(lo, hi);
       uint32_t* ck = g.cell_key + size_t(5) * cid;
       ck[0] = uint32_t(k.qx);
@@ -1986,23 +1987,32 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
 constexpr int kRsThreads = RLC_RS_THREADS;
 constexpr int kRsWarps = kRsThreads / 32;
 constexpr int kRsItems = int(kSortTile) / kRsThreads;  // per thread
-constexpr int kRsTile = kRsThreads * kRsItems;
-constexpr int kRsWarpSpan = 32 * kRsItems;
 
+// Tiles of ITEMS keys per thread over the n valid keys (n_dev: a device-side
+// count); the per-block digit histograms are laid out [digit][tile].
+template <int ITEMS>
+__device__ __forceinline__ uint32_t rs_tiles(uint32_t& n, const unsigned* n_dev) {
+  if (n_dev) n = min(n, *n_dev);
+  constexpr uint32_t tile = kRsThreads * ITEMS;
+  return n_dev ? (n + tile - 1) / tile : gridDim.x;
+}
+
+template <int ITEMS>
 __global__ void __launch_bounds__(kRsThreads) rs_hist(const uint32_t* __restrict__ keys,
                                                       uint32_t n, const unsigned* __restrict__ n_dev,
                                                       int shift, uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[256];
-  if (n_dev) n = min(n, *n_dev);  // the device-side count of the compacted records
+  const uint32_t nt = rs_tiles<ITEMS>(n, n_dev);
+  if (blockIdx.x >= nt) return;
   for (int d = threadIdx.x; d < 256; d += kRsThreads) h[d] = 0;
   __syncthreads();
-  const uint32_t base = blockIdx.x * kRsTile;
-  for (int i = 0; i < kRsItems; ++i) {
+  const uint32_t base = blockIdx.x * kRsThreads * ITEMS;
+  for (int i = 0; i < ITEMS; ++i) {
     const uint32_t j = base + i * kRsThreads + threadIdx.x;
     if (j < n) atomicAdd(&h[(keys[j] >> shift) & 255u], 1u);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < 256; d += kRsThreads) hist[d * gridDim.x + blockIdx.x] = h[d];
+  for (int d = threadIdx.x; d < 256; d += kRsThreads) hist[d * nt + blockIdx.x] = h[d];
 }
 
 // Exclusive scan of `total` counters in place, one block of kScanThreads
@@ -2043,9 +2053,15 @@ __global__ void __launch_bounds__(kScanThreads) rs_scan(uint32_t* __restrict__ h
 
 // Exclusive scan of one digit's row of per-block counts (hist[d][0..nb)) in
 // place; the digit total goes to totals[d].  One block per digit.
+template <int ITEMS>
 __global__ void __launch_bounds__(256) rs_scan_rows(uint32_t* __restrict__ hist, uint32_t nb,
+                                                    uint32_t n, const unsigned* __restrict__ n_dev,
                                                     uint32_t* __restrict__ totals) {
   __shared__ uint32_t ws[8];
+  if (n_dev) {  // the tiles of the device count (rs_tiles)
+    n = min(n, *n_dev);
+    nb = (n + kRsThreads * ITEMS - 1) / (kRsThreads * ITEMS);
+  }
   uint32_t* row = hist + size_t(blockIdx.x) * nb;
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
   uint32_t carry = 0;
@@ -2071,6 +2087,7 @@ __global__ void __launch_bounds__(256) rs_scan_rows(uint32_t* __restrict__ hist,
   if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
+template <int ITEMS>
 __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint32_t* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin,
                                                          uint32_t* __restrict__ kout,
@@ -2080,7 +2097,8 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
                                                          const uint32_t* __restrict__ offs,
                                                          const uint32_t* __restrict__ totals) {
   __shared__ uint32_t wh[kRsWarps][256];
-  if (n_dev) n = min(n, *n_dev);
+  const uint32_t nt = rs_tiles<ITEMS>(n, n_dev);
+  if (blockIdx.x >= nt) return;
   __shared__ uint32_t base_off[256];
   __shared__ uint32_t dsum[kRsWarps];
   const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
@@ -2107,16 +2125,16 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
     for (uint32_t q = 0; q < w; ++q) run += dsum[q];
 #pragma unroll
     for (uint32_t j = 0; j < kDpt; ++j) {
-      base_off[d0 + j] = run + offs[(d0 + j) * gridDim.x + blockIdx.x];
+      base_off[d0 + j] = run + offs[(d0 + j) * nt + blockIdx.x];
       run += tl[j];
     }
   }
   __syncwarp();
-  const uint32_t base = blockIdx.x * kRsTile + w * kRsWarpSpan;
+  const uint32_t base = blockIdx.x * (kRsThreads * ITEMS) + w * (32 * ITEMS);
   const unsigned lt_mask = (1u << lane) - 1u;
-  uint32_t k[kRsItems], v[kRsItems], rank[kRsItems];
+  uint32_t k[ITEMS], v[ITEMS], rank[ITEMS];
 #pragma unroll
-  for (int r = 0; r < kRsItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     const uint32_t j = base + r * 32 + lane;
     const bool ok = j < n;
     k[r] = ok ? kin[j] : 0u;
@@ -2140,7 +2158,7 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kRsItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     const uint32_t j = base + r * 32 + lane;
     if (j < n) {
       const uint32_t d = (k[r] >> shift) & 255u;
@@ -2156,13 +2174,15 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
 // canonical order; q_before feeds the deferred radiance.
 // ---------------------------------------------------------------------------
 // v of record `idx` is at vbase + idx * vstride (sample records or exchanged
-// update records); q_before is written per record index.
+// update records); q_before is written per record index, and with seg_n the
+// segment's record count at its last record index.
 __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
                                               const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ vals,
                                               const char* __restrict__ vbase, uint32_t vstride,
                                               double* __restrict__ q_before,
-                                              const unsigned* __restrict__ n_dev) {
+                                              const unsigned* __restrict__ n_dev,
+                                              uint32_t* __restrict__ seg_n = nullptr) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (n_dev) P.n = min(P.n, *n_dev);
   if (i >= P.n) return;
@@ -2178,7 +2198,7 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
   // The update chain is sequential (bit-exact order); the record loads are
   // not, so they are issued kBatch at a time ahead of the arithmetic.
   constexpr int kBatch = 8;
-  uint32_t j = i;
+  uint32_t j = i, last = 0;
   while (true) {
     uint32_t ids[kBatch];
     int cnt = 0;
@@ -2206,10 +2226,12 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
       const double a = P.harmonic ? 1.0 / (1.0 + double(vis)) : P.alpha;
       q = smax((1.0 - a) * q + a * v, g.eps_q);
       ++vis;
+      last = ids[b];
     }
     j += uint32_t(cnt);
     if (cnt < kBatch) break;
   }
+  if (seg_n) seg_n[last] = j - i;
   g.q[at] = q;
   g.visits[at] = vis;
   g.touched[cell] = 1u;
@@ -2514,46 +2536,46 @@ static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t
 
 // ---------------------------------------------------------------------------
 // Screen-band sharding with an exact exchange.  Every
-// rank traces its band and files its update records (CellKey, cluster, v) in
+// rank traces its band and files its update records (cell, cluster, v) in
 // canonical order into a fixed-size block; the blocks of all ranks are
-// all-gathered (rank-major = canonical order, bands being consecutive); every
-// rank inserts the pass's new keys in that order (identical tables); the
-// records are folded in canonical order per (cell, cluster) -- by every rank
-// (replicated) or by the owner of the cell, hash(CellKey) % nranks, whose
-// q_before values are then summed over the ranks and replayed by the others
-// onto their copies -- so every rank ends with the single-GPU state.
+// all-gathered (rank-major = canonical order, bands being consecutive).  The
+// tables are identical on every rank, so a record names its cell by table
+// slot; only keys new this pass travel as keys, and every rank inserts them
+// in canonical order (identical tables again).  The records are folded in
+// canonical order per (cell, cluster) -- by every rank (replicated) or by
+// the owner of the cell, slot % nranks, whose q_before values and per-entry
+// record counts are then summed over the ranks and applied by the others to
+// their copies -- so every rank ends with the single-GPU state.
 // ---------------------------------------------------------------------------
 __global__ void k_write_block(DevGrid g, const GBuf* __restrict__ gbuf,
                               const SampleRec* __restrict__ srec,
                               const uint32_t* __restrict__ rec_path,
                               const unsigned int* __restrict__ count, uint32_t n,
                               const unsigned long long* __restrict__ pkey, uint32_t cap,
-                              unsigned char* __restrict__ block) {
+                              ExchangeRecord* __restrict__ block) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t c = min(*count, cap);
-  if (k == 0) reinterpret_cast<RecordBlockHeader*>(block)->count = c;
+  if (k == 0) {
+    RecordBlockHeader h{};
+    h.count = c;
+    *reinterpret_cast<RecordBlockHeader*>(block) = h;
+  }
   if (k >= n || k >= c) return;
   const uint32_t idx = rec_path[k];
   const uint32_t cell = gbuf[idx].cell;
-  UpdateRecord r;
-  if (cell == kPending) {  // new this pass: inserted with all ranks' records
-    const Key key = unpack_key(pkey[2 * size_t(idx)], pkey[2 * size_t(idx) + 1]);
-    r.qx = key.qx;
-    r.qy = key.qy;
-    r.qz = key.qz;
-    r.qn = key.qn;
-    r.level = key.level;
-  } else {
-    const uint32_t* ck = g.cell_key + size_t(5) * cell;
-    r.qx = int32_t(ck[0]);
-    r.qy = int32_t(ck[1]);
-    r.qz = int32_t(ck[2]);
-    r.qn = ck[3];
-    r.level = ck[4];
-  }
+  ExchangeRecord r;
   r.cluster = srec[idx].s;
   r.v = srec[idx].v;
-  reinterpret_cast<UpdateRecord*>(block + sizeof(RecordBlockHeader))[k] = r;
+  if (cell == kPending) {  // new this pass: inserted with all ranks' records
+    r.slot = kPending;
+    r.klo = pkey[2 * size_t(idx)];
+    r.khi = pkey[2 * size_t(idx) + 1];
+  } else {
+    r.slot = g.cell_slot[cell];
+    r.klo = 0;
+    r.khi = 0;
+  }
+  block[1 + k] = r;
 }
 
 void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, void* block,
@@ -2561,189 +2583,162 @@ void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, voi
   launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);
   k_write_block<<<blocks_for(n > 0 ? n : 1, 256), 256, 0, st>>>(
       g, b.gbuf, b.srec, b.rec_path, b.rec_count, n, b.pkey, cap,
-      static_cast<unsigned char*>(block));
+      static_cast<ExchangeRecord*>(block));
   count_launch();
 }
 
-__device__ __forceinline__ const UpdateRecord* block_records(const unsigned char* blocks,
-                                                             uint64_t block_bytes, uint32_t r) {
-  return reinterpret_cast<const UpdateRecord*>(blocks + r * block_bytes + sizeof(RecordBlockHeader));
-}
-
-// Gathers the record slots t = rank * cap + k of all blocks and looks their
-// keys up; keys new this pass are filed with their smallest slot index -- the
-// canonical order in which the single-GPU reference inserts them.
-__global__ void __launch_bounds__(128) k_gather_blocks(DevGrid g, const unsigned char* __restrict__ blocks,
-                                                       uint64_t block_bytes, ExchangeBuffers x) {
+// Each exchange slot t of the gathered blocks: padding (a header slot or
+// past its block's count), a record of an existing cell (its cell, owner and
+// sort key), or a record whose key was new at trace time -- filed with the
+// smallest slot index that holds it (the canonical order in which the
+// single-GPU reference inserts keys) and listed for k_resolve_pending.
+__global__ void __launch_bounds__(256) k_classify(DevGrid g, uint32_t rank, uint32_t owner_fold,
+                                                  ExchangeBuffers x) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t r = t / x.cap, k = t - r * x.cap;
-  bool need = false;
-  Key key{};
-  uint64_t lo = 0, hi = 0, h = 0;
-  if (r < x.nranks) {
-    const auto* hdr = reinterpret_cast<const RecordBlockHeader*>(blocks + r * block_bytes);
-    if (k < hdr->count) {
-      const UpdateRecord rec = block_records(blocks, block_bytes, r)[k];
-      x.contig[t] = rec;
-      key = Key{rec.qx, rec.qy, rec.qz, rec.qn, rec.level};
-      pack_key(key, lo, hi);
-      h = hash_key(key);
-      need = true;
-    } else {
-      x.slots[t] = kNoSlot;  // padding of the block
+  const uint32_t r = t / x.stride, j = t - r * x.stride;
+  bool valid = false;
+  ExchangeRecord rec{};
+  if (r < x.nranks && j > 0) {
+    const auto* hdr = reinterpret_cast<const RecordBlockHeader*>(x.rec + size_t(r) * x.stride);
+    if (j <= hdr->count) {
+      rec = x.rec[t];
+      valid = true;
     }
   }
-  const unsigned need_mask = __ballot_sync(kFull, need);
-  if (!need) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
-  const unsigned peers = __match_any_sync(need_mask, h) & need_mask;
+  const bool pending = valid && rec.slot == kPending;
+  if (valid && !pending) {
+    RLC_CHECK(rec.slot < g.capacity, g.counters + kCntErr);
+    const uint32_t cell = g.slot_cell[rec.slot];
+    const bool owned = !owner_fold || rec.slot % x.nranks == rank;
+    x.cellx[t] = cell;
+    x.kflag[t] = owned ? uint8_t(kXValid | kXOwned | kXSort) : kXValid;
+    if (owned) x.keys[t] = cell * g.M + rec.cluster;
+  } else if (r < x.nranks) {
+    x.kflag[t] = pending ? uint8_t(kXValid | kXPending) : uint8_t(0);
+  }
+  if (valid && !(rec.v >= 0 && isfinite(rec.v)))  // update_q's argument check, cut.cpp:78-80
+    atomicOr(err, kErrBadValue);
+  const unsigned pmask = __ballot_sync(kFull, pending);
+  if (!pending) return;
+  // list the record for the resolution after the insertion
+  const uint32_t leader0 = __ffs(pmask) - 1;
+  uint32_t base = 0;
+  if (lane == leader0) base = atomicAdd(x.pend_count, uint32_t(__popc(pmask)));
+  base = __shfl_sync(pmask, base, leader0);
+  x.pend[base + __popc(pmask & ((1u << lane) - 1u))] = t;
+  // file the key once per warp (lanes of one key agree on the smallest slot)
+  const uint64_t h = hash_key(unpack_key(rec.klo, rec.khi));
+  const unsigned peers = __match_any_sync(pmask, h) & pmask;
   const int leader = __ffs(peers) - 1;
-  uint32_t slot = 0;
-  if (int(lane) == leader) slot = probe_find(g, lo, hi, h);
-  slot = __shfl_sync(peers, slot, leader);
-  const uint64_t llo = __shfl_sync(peers, lo, leader);
-  const uint64_t lhi = __shfl_sync(peers, hi, leader);
-  const bool same = llo == lo && lhi == hi;
+  const uint64_t llo = __shfl_sync(peers, rec.klo, leader);
+  const uint64_t lhi = __shfl_sync(peers, rec.khi, leader);
+  const bool same = llo == rec.klo && lhi == rec.khi;
   const unsigned same_mask = __ballot_sync(peers, same);
   if (same) {
-    if (slot == kPending) {
-      const uint32_t first = __reduce_min_sync(same_mask, t);
-      if (int(lane) == leader) nk_register(x.nk, lo, hi, h, first, err);
-    }
+    const uint32_t first = __reduce_min_sync(same_mask, t);
+    if (int(lane) == leader) nk_register(x.nk, rec.klo, rec.khi, h, first, err);
   } else {
-    slot = probe_find(g, lo, hi, h);
-    if (slot == kPending) nk_register(x.nk, lo, hi, h, t, err);
+    nk_register(x.nk, rec.klo, rec.khi, h, t, err);
   }
-  x.slots[t] = slot;
 }
 
-// After the insertion: each slot's cell (or the fallback for a refused key,
-// whose record updates nothing), its owner, and the sort keys of the records
-// this rank folds.  Fallback hits of this rank's own records are counted.
-__global__ void k_block_keys(DevGrid g, uint32_t rank, uint32_t owner_fold, ExchangeBuffers x) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= x.nranks * x.cap) return;
-  uint32_t slot = x.slots[t];
-  x.vals[t] = t;
-  if (slot == kNoSlot) {
-    x.kflag[t] = 0;
-    x.keys[t] = kInvalidKey;
-    return;
+// After the insertion: the cell of each record whose key was new at trace
+// time, or the fallback for a refused key (its record updates nothing);
+// fallback hits of this rank's own records are counted.
+__global__ void k_resolve_pending(DevGrid g, uint32_t rank, uint32_t owner_fold, ExchangeBuffers x) {
+  const uint32_t n = *x.pend_count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t t = x.pend[i];
+    const ExchangeRecord rec = x.rec[t];
+    const uint32_t slot = probe_find(g, rec.klo, rec.khi, hash_key(unpack_key(rec.klo, rec.khi)));
+    if (slot < kPending) {
+      const uint32_t cell = g.slot_cell[slot];
+      const bool owned = !owner_fold || slot % x.nranks == rank;
+      x.cellx[t] = cell;
+      x.kflag[t] = owned ? uint8_t(kXValid | kXOwned | kXSort) : kXValid;
+      if (owned) x.keys[t] = cell * g.M + rec.cluster;
+    } else {  // refused: a full window (hash_grid.cpp:140)
+      x.cellx[t] = kFallback;
+      x.kflag[t] = kXValid | kXFallback;
+      if (t / x.stride == rank) atomicAdd(g.counters + kCntFallback, 1ull);
+    }
   }
-  const UpdateRecord r = x.contig[t];
-  const Key key{r.qx, r.qy, r.qz, r.qn, r.level};
-  const uint64_t h = hash_key(key);
-  if (slot == kPending) {
-    uint64_t lo, hi;
-    pack_key(key, lo, hi);
-    slot = probe_find(g, lo, hi, h);
-  }
-  uint8_t f = kXValid;
-  uint32_t cell = kFallback;
-  if (slot < kPending) {
-    cell = g.slot_cell[slot];
-  } else {  // refused: a full window (hash_grid.cpp:140)
-    f |= kXFallback;
-    if (t / x.cap == rank) atomicAdd(g.counters + kCntFallback, 1ull);
-  }
-  x.cellx[t] = cell;
-  if (!(f & kXFallback)) {
-    const bool owned = !owner_fold || uint32_t(h % x.nranks) == rank;
-    if (owned) f |= kXOwned | kXSort;
-  }
-  x.kflag[t] = f;
-  x.keys[t] = (f & kXSort) ? cell * g.M + r.cluster : kInvalidKey;
 }
 
-void launch_shard_fold(const DevGrid& g, const PassParams& fold_params, const void* blocks,
-                       uint64_t block_bytes, uint32_t rank, bool owner_fold, uint32_t key_bits,
-                       ExchangeBuffers& x, cudaStream_t st) {
-  const uint32_t total = x.nranks * x.cap;
+void launch_shard_fold(const DevGrid& g, const PassParams& fold_params, uint32_t rank,
+                       bool owner_fold, ExchangeBuffers& x, cudaStream_t st) {
+  (void)fold_params;
+  const uint32_t total = x.nranks * x.stride;
   if (total == 0) return;
   cudaMemsetAsync(x.nk.count, 0, sizeof(unsigned int), st);
+  cudaMemsetAsync(x.pend_count, 0, sizeof(unsigned int), st);
   cudaMemsetAsync(x.q_rec, 0, sizeof(double) * total, st);
-  k_gather_blocks<<<blocks_for(total, 128), 128, 0, st>>>(
-      g, static_cast<const unsigned char*>(blocks), block_bytes, x);
+  if (owner_fold) cudaMemsetAsync(x.seg_n, 0, sizeof(uint32_t) * total, st);
+  k_classify<<<blocks_for(total, 256), 256, 0, st>>>(g, rank, owner_fold ? 1u : 0u, x);
   count_launch();
   launch_insert_new_keys(g, x.nk, st);
-  k_block_keys<<<blocks_for(total, 256), 256, 0, st>>>(g, rank, owner_fold ? 1u : 0u, x);
+  k_resolve_pending<<<148, 256, 0, st>>>(g, rank, owner_fold ? 1u : 0u, x);
   count_launch();
 }
 
 void launch_shard_sortfold(const DevGrid& g, const PassParams& fold_params, uint32_t key_bits,
-                           ExchangeBuffers& x, cudaStream_t st) {
-  const uint32_t total = x.nranks * x.cap;
+                           bool owner_fold, ExchangeBuffers& x, cudaStream_t st) {
+  const uint32_t total = x.nranks * x.stride;
   if (total == 0) return;
   // the folded records, compacted in slot (= canonical) order, sorted stably
-  // by (cell, cluster) with the device count, folded in canonical order
+  // by (cell, cluster) over the device count, folded in canonical order
   PassBuffers cb{};
   launch_compact(cb, nullptr, total, kXSort, x.vals_alt, x.sort_count, st, x.block_counts, x.keys,
                  x.keys_alt, x.kflag);
   uint32_t *k = nullptr, *v = nullptr;
   launch_sort_buffers(x.keys_alt, x.vals_alt, x.keys, x.vals, x.hist, total, key_bits, st, &k, &v,
-                      x.sort_count);
+                      x.sort_count, true);
   PassParams p = fold_params;
   p.n = total;
   k_fold<<<blocks_for(total, 256), 256, 0, st>>>(
-      g, p, k, v, reinterpret_cast<const char*>(x.contig) + offsetof(UpdateRecord, v),
-      uint32_t(sizeof(UpdateRecord)), x.q_rec, x.sort_count);
+      g, p, k, v, reinterpret_cast<const char*>(x.rec) + offsetof(ExchangeRecord, v),
+      uint32_t(sizeof(ExchangeRecord)), x.q_rec, x.sort_count, owner_fold ? x.seg_n : nullptr);
   count_launch();
 }
 
-// Owner mode: the records of cells another rank folded.  Pass 1 counts each
-// cut entry's records and finds its last (highest slot = latest canonical);
-// pass 2 advances the entry from that record's summed q_before exactly as
-// update_q does (cut.cpp:76-86): q = max((1 - a) q_before + a v, eps), a the
-// harmonic weight of the record's own visit count, visits += count.
-__global__ void k_apply_count(DevGrid g, ExchangeBuffers x) {
+// Owner mode: the cut entries of the cells other ranks folded, from each
+// entry's last record t (seg_n[t] = the entry's record count, summed over
+// the ranks with its q_before): q = max((1 - a) q_before + a v, eps), a the
+// harmonic weight of that record's visit count, visits += count -- the
+// arithmetic of update_q (cut.cpp:76-86) the owner ran record by record.
+__global__ void k_apply(DevGrid g, PassParams P, ExchangeBuffers x) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= x.nranks * x.cap) return;
-  const uint8_t f = x.kflag[t];
-  if (!(f & kXValid) || (f & (kXFallback | kXOwned))) return;
-  const size_t e = size_t(x.cellx[t]) * g.M + x.contig[t].cluster;
-  atomicAdd(x.seg_count + e, 1u);
-  atomicMax(x.seg_last + e, t);
-}
-
-__global__ void k_apply_last(DevGrid g, PassParams P, ExchangeBuffers x) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= x.nranks * x.cap) return;
-  const uint8_t f = x.kflag[t];
-  if (!(f & kXValid) || (f & (kXFallback | kXOwned))) return;
+  if (t >= x.nranks * x.stride) return;
+  const uint32_t c = x.seg_n[t];
+  if (c == 0 || (x.kflag[t] & kXOwned)) return;
   const uint32_t cell = x.cellx[t];
-  const size_t e = size_t(cell) * g.M + x.contig[t].cluster;
-  const double v = x.contig[t].v;
-  if (!(v >= 0 && isfinite(v)))  // update_q's argument check, cut.cpp:78-80
-    atomicOr(reinterpret_cast<unsigned int*>(g.counters + kCntErr), kErrBadValue);
+  const ExchangeRecord rec = x.rec[t];
+  const size_t e = size_t(cell) * g.M + rec.cluster;
   g.touched[cell] = 1u;
-  if (x.seg_last[e] != t) return;
-  const uint32_t c = x.seg_count[e];
   const uint32_t vis_before = g.visits[e] + c - 1u;  // visits seen by the last record
   const double a = P.harmonic ? 1.0 / (1.0 + double(vis_before)) : P.alpha;
-  g.q[e] = smax((1.0 - a) * x.q_rec[t] + a * v, g.eps_q);
+  g.q[e] = smax((1.0 - a) * x.q_rec[t] + a * rec.v, g.eps_q);
   g.visits[e] = vis_before + 1u;
-  x.seg_count[e] = 0;  // clean for the next pass
-  x.seg_last[e] = 0;
 }
 
 void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, ExchangeBuffers& x,
                         cudaStream_t st) {
-  const uint32_t total = x.nranks * x.cap;
+  const uint32_t total = x.nranks * x.stride;
   if (total == 0) return;
-  k_apply_count<<<blocks_for(total, 256), 256, 0, st>>>(g, x);
-  k_apply_last<<<blocks_for(total, 256), 256, 0, st>>>(g, fold_params, x);
-  count_launch(2);
+  k_apply<<<blocks_for(total, 256), 256, 0, st>>>(g, fold_params, x);
+  count_launch();
 }
 
 __global__ void k_shard_scatter(DevGrid g, const uint32_t* __restrict__ rec_path,
                                 const unsigned int* __restrict__ count, uint32_t n, uint32_t rank,
                                 ExchangeBuffers x, double* __restrict__ q_before) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n || k >= *count || k >= x.cap) return;
-  const uint32_t t = rank * x.cap + k;
-  q_before[rec_path[k]] =
-      (x.kflag[t] & kXFallback) ? g.t_q[x.contig[t].cluster] : x.q_rec[t];  // fallback: never updated
+  if (k >= n || k >= *count || k + 1 >= x.stride) return;
+  const uint32_t t = rank * x.stride + 1 + k;
+  q_before[rec_path[k]] =  // fallback: never updated
+      (x.kflag[t] & kXFallback) ? g.t_q[x.rec[t].cluster] : x.q_rec[t];
 }
 
 void launch_shard_scatter(const DevGrid& g, const PassBuffers& b, uint32_t n, uint32_t rank,
@@ -3192,24 +3187,30 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   count_launch();
 }
 
+template <int ITEMS>
+static void sort_passes(uint32_t*& ka, uint32_t*& va, uint32_t*& kb, uint32_t*& vb,
+                        uint32_t* hist, uint32_t n, uint32_t key_bits, cudaStream_t st,
+                        const unsigned* n_dev) {
+  const uint32_t nb = blocks_for(n, kRsThreads * ITEMS);
+  for (uint32_t shift = 0; shift < key_bits; shift += 8) {
+    rs_hist<ITEMS><<<nb, kRsThreads, 0, st>>>(ka, n, n_dev, int(shift), hist);
+    uint32_t* totals = hist + size_t(nb) * 256u;
+    rs_scan_rows<ITEMS><<<256, 256, 0, st>>>(hist, nb, n, n_dev, totals);
+    rs_scatter<ITEMS><<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, n_dev, int(shift), hist, totals);
+    count_launch(3);
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+}
+
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
-                         uint32_t** vals_out, const unsigned* n_dev) {
+                         uint32_t** vals_out, const unsigned* n_dev, bool small_tiles) {
   if (n > 1) {
-    const uint32_t nb = blocks_for(n, kRsTile);
-    for (uint32_t shift = 0; shift < key_bits; shift += 8) {
-      rs_hist<<<nb, kRsThreads, 0, st>>>(ka, n, n_dev, int(shift), hist);
-      uint32_t* totals = hist + size_t(nb) * 256u;
-      rs_scan_rows<<<256, 256, 0, st>>>(hist, nb, totals);
-      rs_scatter<<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, n_dev, int(shift), hist, totals);
-      count_launch(3);
-      uint32_t* t = ka;
-      ka = kb;
-      kb = t;
-      t = va;
-      va = vb;
-      vb = t;
-    }
+    if (small_tiles)
+      sort_passes<int(kSortTileSmall) / kRsThreads>(ka, va, kb, vb, hist, n, key_bits, st, n_dev);
+    else
+      sort_passes<kRsItems>(ka, va, kb, vb, hist, n, key_bits, st, n_dev);
   }
   *keys_out = ka;
   *vals_out = va;

@@ -70,11 +70,14 @@ struct alignas(16) ShadowRay {
   uint32_t pad;
 };
 
-// One update_q record exchanged between ranks (== rlc_update_record).
-struct alignas(16) UpdateRecord {
-  int32_t qx, qy, qz;
-  uint32_t qn, level, cluster;
+// One update_q record as exchanged between ranks (32 B): the cell named by
+// its table slot -- the tables are identical on every rank, slot for slot --
+// or kPending with the packed CellKey for a key new this pass.
+struct alignas(16) ExchangeRecord {
+  uint32_t slot;     // table slot, or kPending (key in klo/khi)
+  uint32_t cluster;
   double v;
+  unsigned long long klo, khi;  // packed CellKey (pending records only)
 };
 
 struct DevScene {
@@ -128,6 +131,7 @@ struct DevGrid {
   double* cdf;
   uint32_t* visits;
   uint32_t* cell_key;             // [cell][5]
+  uint32_t* cell_slot;            // [cell] its table slot
   uint32_t* touched;              // [cell]
   // template cut == fallback cut [M]
   const uint32_t* t_node;
@@ -198,36 +202,38 @@ struct PassBuffers {
   uint32_t sort_hist_cap;  // entries
 };
 
-// Buffers of the sharded fold, sized for the records of all ranks.
-// A rank's update records of one sharded pass, as all-gathered: a 16-byte
-// header (the record count) and `cap` record slots.  Every rank's block has
-// the same size, so the gather needs no count on the host.
+// A rank's update records of one sharded pass, as all-gathered: cap + 1
+// slots of 32 B, slot 0 the header (the record count), record k in slot
+// k + 1.  Every rank's block has the same size, so the gather needs no count
+// on the host, and the gathered blocks are one array of exchange slots
+// t = rank * (cap + 1) + 1 + k in canonical order.
 struct alignas(16) RecordBlockHeader {
   unsigned long long count;
-  unsigned long long pad;
+  unsigned long long pad[3];
 };
+static_assert(sizeof(RecordBlockHeader) == sizeof(ExchangeRecord), "block slot size");
 
-// Buffers of the sharded fold, for nranks * cap gathered record slots.
+// Buffers of the sharded fold, for nranks * (cap + 1) exchange slots.
 struct ExchangeBuffers {
-  UpdateRecord* contig;  // [slot t = rank * cap + k] the gathered records
-  uint32_t* slots;       // [t] the record's table slot (kNoSlot: padding)
-  uint32_t* cellx;       // [t] its dense cell id (kFallback: refused key)
-  uint8_t* kflag;        // [t] kXValid | kXFallback | kXOwned | kXSort
-  uint32_t* keys;
-  uint32_t* vals;
+  const ExchangeRecord* rec;  // [t] the gathered blocks (header slots included)
+  uint32_t* cellx;       // [t] the record's dense cell id (kFallback: refused key)
+  uint8_t* kflag;        // [t] kXValid | kXFallback | kXOwned | kXSort | kXPending
+  uint32_t* keys;        // [t] sort key (cell * M + cluster) of the records this rank folds
   uint32_t* keys_alt;
+  uint32_t* vals;
   uint32_t* vals_alt;
   uint32_t* hist;
   uint32_t* block_counts;
   unsigned int* sort_count;
   double* q_rec;         // [t] q_before of record t (the all-reduced array in owner mode)
-  uint32_t* seg_count;   // [cell * M + cluster] records per cut entry (owner mode apply)
-  uint32_t* seg_last;    // [cell * M + cluster] slot of the entry's last record
+  uint32_t* seg_n;       // [t] records of the cut entry at its last record t, else 0 (owner mode)
+  uint32_t* pend;        // slots of the records whose key was new at trace time
+  unsigned int* pend_count;
   NewKeys nk;
-  uint32_t cap;          // record slots per rank
+  uint32_t stride;       // exchange slots per rank block (cap + 1)
   uint32_t nranks;
 };
-enum : uint8_t { kXValid = 1, kXFallback = 2, kXOwned = 4, kXSort = 8 };
+enum : uint8_t { kXValid = 1, kXFallback = 2, kXOwned = 4, kXSort = 8, kXPending = 16 };
 
 // == rlc_sample_record (include/rlcuts_b200.h)
 struct alignas(8) SampleExport {
@@ -282,26 +288,33 @@ void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
 #define RLC_SORT_TILE 4096
 #endif
 constexpr uint32_t kSortTile = RLC_SORT_TILE;
-// n_dev (may be null): a device-side count <= n of the valid entries.
+// Keys per block of the sharded fold's sort (a rank folds a fraction of the
+// gathered records, so smaller tiles keep the SMs busy).
+constexpr uint32_t kSortTileSmall = 1024;
+// n_dev (may be null): a device-side count <= n of the valid entries; the
+// digit passes then cover ceil(*n_dev / tile) tiles only.  small_tiles:
+// kSortTileSmall keys per block instead of kSortTile.
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
-                         uint32_t** vals_out, const unsigned* n_dev);
+                         uint32_t** vals_out, const unsigned* n_dev, bool small_tiles = false);
 // Sharded passes.  The rank's update records of the
-// traced band, in canonical order, into `block` (header + cap slots).
+// traced band, in canonical order, into `block` (header slot + cap slots).
 void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, void* block,
                          uint32_t cap, cudaStream_t st);
-// The fold of all ranks' gathered blocks (nranks x block_bytes): the pass's
-// new keys inserted in canonical order (identical tables on every rank),
-// then update_q for the records of the cells this rank folds -- all of them
-// (owner_fold = 0) or those with hash(CellKey) % nranks == rank -- in
-// canonical order; q_before per record slot into x.q_rec (zero elsewhere).
-void launch_shard_fold(const DevGrid& g, const PassParams& fold_params, const void* blocks,
-                       uint64_t block_bytes, uint32_t rank, bool owner_fold, uint32_t key_bits,
-                       ExchangeBuffers& x, cudaStream_t st);  // gather, insert, keys
+// The fold of all ranks' gathered blocks (x.rec: nranks x x.stride slots,
+// valid until the pass's launch_shard_scatter): the pass's new keys inserted
+// in canonical order (identical tables on every rank), then each record's
+// cell and owner -- this rank for every record (owner_fold = 0), else the
+// rank slot % nranks of its table slot.
+void launch_shard_fold(const DevGrid& g, const PassParams& fold_params, uint32_t rank,
+                       bool owner_fold, ExchangeBuffers& x, cudaStream_t st);
+// update_q for the records this rank folds, per cut entry in canonical
+// order: q_before per record slot into x.q_rec and, in owner mode, the
+// entry's record count at its last record into x.seg_n (zero elsewhere).
 void launch_shard_sortfold(const DevGrid& g, const PassParams& fold_params, uint32_t key_bits,
-                           ExchangeBuffers& x, cudaStream_t st);  // compact, sort, update_q
-// Owner mode, after x.q_rec was summed over the ranks: the cut entries of the
-// cells other ranks folded, advanced to the state their last record leaves
+                           bool owner_fold, ExchangeBuffers& x, cudaStream_t st);
+// Owner mode, after x.q_rec and x.seg_n were summed over the ranks: the cut
+// entries other ranks folded, advanced to the state their last record leaves
 // (q from its q_before and v, visits by the record count), touched flags.
 void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, ExchangeBuffers& x,
                         cudaStream_t st);

@@ -3,14 +3,15 @@
 Each rank renders a contiguous band of image rows.  The learned cut state
 must evolve exactly as in one render_pass over the whole image, and the
 ordered, floored EMA of update_q (proj/src/cut.cpp:76-86) cannot be merged by
-summing deltas.  Each rank files its update records (cell key, cluster, v;
+summing deltas.  Each rank files its update records (cell, cluster, v;
 32 B) in canonical order into a fixed-size block; the blocks are all-gathered
 (rank-major order is canonical order: bands are consecutive); every rank
-inserts the pass's new keys in that order, so the hash tables stay identical.
-The records are then folded in canonical order per cut entry, either by every
-rank (replicated) or only by the owner of the cell, hash(CellKey) % nranks
-(owner mode): the owners' per-record q_before values are summed over the
-ranks and every rank replays the other owners' entries onto its copy.  Each
+inserts the pass's new keys in that order, so the hash tables stay identical
+(and a record can name its cell by table slot).  The records are then folded
+in canonical order per cut entry, either by every rank (replicated) or only
+by the owner of the cell, table slot % nranks (owner mode): the owners'
+per-record q_before values and per-entry record counts are summed over the
+ranks and every rank advances the other owners' entries on its copy.  Each
 rank then forms the radiance of its own band.
 
 Three drivers of the same protocol:
@@ -67,10 +68,14 @@ class GpuEngine:
         ptr, nbytes = rlcuts.shard_trace(self.ctx, self.cfg, pass_index, self.grid, rows, self.cap)
         return torch.as_tensor(_CudaView(ptr, nbytes), device=self.device)
 
-    def fold(self, gathered: torch.Tensor, nranks: int, rank: int, owner: bool) -> torch.Tensor:
-        ptr, n = rlcuts.shard_fold(self.ctx, self.cfg, self.grid, gathered.data_ptr(), nranks,
-                                   rank, owner)
-        return torch.as_tensor(_CudaView(ptr, 8 * n, "<f8"), device=self.device)
+    def fold(self, gathered: torch.Tensor, nranks: int, rank: int, owner: bool):
+        """-> (q_before per exchange slot, records per cut entry at its last
+        slot): the two arrays owner mode sums over the ranks.  `gathered`
+        must stay alive until finish()."""
+        ptr, seg, n = rlcuts.shard_fold(self.ctx, self.cfg, self.grid, gathered.data_ptr(), nranks,
+                                        rank, owner)
+        return (torch.as_tensor(_CudaView(ptr, 8 * n, "<f8"), device=self.device),
+                torch.as_tensor(_CudaView(seg, 4 * n, "<i4"), device=self.device))
 
     def finish(self, rank: int, owner: bool):
         rlcuts.shard_finish(self.ctx, self.grid, self.fb, rank, owner)
@@ -107,15 +112,18 @@ class ShardedFrame:
         dist.all_gather(parts, send, group=self.group)
         gathered = torch.cat(parts).to(e.device)
         torch.cuda.synchronize(e.device)
-        q = e.fold(gathered, self.world, self.rank, self.owner)
+        arrays = e.fold(gathered, self.world, self.rank, self.owner)
         if self.owner and self.world > 1:
             self._sync()
-            qs = q.to(dev)
-            dist.all_reduce(qs, group=self.group)
-            q.copy_(qs.to(e.device))
+            for a in arrays:  # (the uint32 counts viewed as int32: they stay below 2^31)
+                t = a.to(dev)
+                dist.all_reduce(t, group=self.group)
+                a.copy_(t.to(e.device))
             torch.cuda.synchronize(e.device)
         e.finish(self.rank, self.owner)
-        return e.end_of_pass()
+        out = e.end_of_pass()
+        del gathered  # read by finish() on the context stream (end_of_pass synchronized)
+        return out
 
 
 class NcclFrame:
@@ -156,17 +164,18 @@ def local_exchange(engines, heights_rows, pass_index: int, owner: bool = True,
         e.ctx.synchronize()
     gathered = torch.cat([b.clone() for b in blocks])
     torch.cuda.synchronize()
-    qs = []
+    arrays = []
     for r, e in enumerate(engines):
-        qs.append(e.fold(gathered, n, r, owner))
+        arrays.append(e.fold(gathered, n, r, owner))
         if serial:
             e.ctx.synchronize()
     for e in engines:
         e.ctx.synchronize()
     if owner and n > 1:
-        total = torch.stack([q.clone() for q in qs]).sum(0)
-        for q in qs:
-            q.copy_(total)
+        for k in range(2):  # q_before, entry counts
+            total = torch.stack([a[k].clone() for a in arrays]).sum(0)
+            for a in arrays:
+                a[k].copy_(total.to(a[k].dtype))
         torch.cuda.synchronize()
     for r, e in enumerate(engines):
         e.finish(r, owner)

@@ -493,15 +493,19 @@ def shard_trace(ctx: RenderContext, config: RenderConfig, pass_index: int, grid:
 
 
 def shard_fold(ctx: RenderContext, config: RenderConfig, grid: HashGrid, blocks_ptr: int,
-               nranks: int, rank: int, owner_fold: bool) -> tuple[int, int]:
-    """rlc_shard_fold over the all-gathered blocks (device memory, rank-major).
-    Returns (device pointer, count) of the per-slot q_before doubles."""
+               nranks: int, rank: int, owner_fold: bool) -> tuple[int, int, int]:
+    """rlc_shard_fold over the all-gathered blocks (device memory, rank-major,
+    valid until shard_finish).  Returns (q_before doubles, entry-count
+    uint32s, count): the device arrays per exchange slot that owner mode
+    sums over the ranks."""
     cfg = config.c()
     ptr = C.c_void_p()
+    seg = C.c_void_p()
     n = C.c_uint64()
     _check(_lib.load().rlc_shard_fold(ctx.handle, C.byref(cfg), grid.handle, C.c_void_p(blocks_ptr),
-                                      nranks, rank, int(owner_fold), C.byref(ptr), C.byref(n)))
-    return int(ptr.value or 0), int(n.value)
+                                      nranks, rank, int(owner_fold), C.byref(ptr), C.byref(seg),
+                                      C.byref(n)))
+    return int(ptr.value or 0), int(seg.value or 0), int(n.value)
 
 
 def shard_finish(ctx: RenderContext, grid: HashGrid, framebuffer: Framebuffer, rank: int,

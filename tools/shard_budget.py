@@ -4,7 +4,7 @@ the collectives are done by the host between the steps).  Prints, per mode,
 each rank's device time per frame by stage (CUDA events) and the exchange
 volumes; the NCCL transfer time is estimated from the measured NVLink
 bandwidths of B200_PROFILING.md (all-gather bus 725 GB/s).
-usage: python tools/shard_budget.py [N] [frames] [config]"""
+usage: python tools/shard_budget.py [N] [frames] [config] [owner|replicated|both]"""
 import sys
 import time
 
@@ -18,10 +18,12 @@ from paper_1911_10217_b200 import rlcuts  # noqa: E402
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 frames = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 name = sys.argv[3] if len(sys.argv) > 3 else "c3"
+which = sys.argv[4] if len(sys.argv) > 4 else "both"
+modes = {"owner": (True,), "replicated": (False,), "both": (True, False)}[which]
 scene, cfg = bench.make_config(name)
 H, W = scene.camera.height, scene.camera.width
 dev = torch.device("cuda", 0)
-for owner in (True, False):
+for owner in modes:
     engines = []
     for r in range(N):
         ctx = rlcuts.build_context(scene, cfg)
@@ -52,11 +54,11 @@ for owner in (True, False):
     for r, d in enumerate(per_rank):
         print(f"{r:4d} " + " ".join(f"{d.get(k, 0.0):14.4f}" for k in keys))
     e0 = engines[0]
-    block = 16 + e0.cap * 32
+    block = 32 * (e0.cap + 1)
     print(f"record block {block / 1e6:.2f} MB per rank; all-gather receives "
           f"{(N - 1) * block / 1e6:.1f} MB per rank (~{(N - 1) * block / 725e9 * 1e6:.0f} us at 725 GB/s);"
-          + (f" q_before all-reduce {N * e0.cap * 8 / 1e6:.1f} MB "
-             f"(~{2 * (N - 1) / N * N * e0.cap * 8 / 725e9 * 1e6:.0f} us)" if owner else ""))
+          + (f" q_before + entry-count all-reduce {N * (e0.cap + 1) * 12 / 1e6:.1f} MB "
+             f"(~{2 * (N - 1) / N * N * (e0.cap + 1) * 12 / 725e9 * 1e6:.0f} us)" if owner else ""))
     print(f"emulation wall time {wall / frames * 1e3:.1f} ms per frame (all {N} ranks, serial)")
     del engines
     torch.cuda.empty_cache()
