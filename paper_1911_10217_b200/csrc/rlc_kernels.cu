@@ -2176,13 +2176,14 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
 // v of record `idx` is at vbase + idx * vstride (sample records or exchanged
 // update records); q_before is written per record index, and with seg_n the
 // segment's record count at its last record index.
+template <bool SEG>
 __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
                                               const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ vals,
                                               const char* __restrict__ vbase, uint32_t vstride,
                                               double* __restrict__ q_before,
                                               const unsigned* __restrict__ n_dev,
-                                              uint32_t* __restrict__ seg_n = nullptr) {
+                                              uint32_t* __restrict__ seg_n) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (n_dev) P.n = min(P.n, *n_dev);
   if (i >= P.n) return;
@@ -2226,12 +2227,12 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
       const double a = P.harmonic ? 1.0 / (1.0 + double(vis)) : P.alpha;
       q = smax((1.0 - a) * q + a * v, g.eps_q);
       ++vis;
-      last = ids[b];
+      if constexpr (SEG) last = ids[b];
     }
     j += uint32_t(cnt);
     if (cnt < kBatch) break;
   }
-  if (seg_n) seg_n[last] = j - i;
+  if constexpr (SEG) seg_n[last] = j - i;
   g.q[at] = q;
   g.visits[at] = vis;
   g.touched[cell] = 1u;
@@ -2697,9 +2698,14 @@ void launch_shard_sortfold(const DevGrid& g, const PassParams& fold_params, uint
                       x.sort_count, true);
   PassParams p = fold_params;
   p.n = total;
-  k_fold<<<blocks_for(total, 256), 256, 0, st>>>(
-      g, p, k, v, reinterpret_cast<const char*>(x.rec) + offsetof(ExchangeRecord, v),
-      uint32_t(sizeof(ExchangeRecord)), x.q_rec, x.sort_count, owner_fold ? x.seg_n : nullptr);
+  const char* vb = reinterpret_cast<const char*>(x.rec) + offsetof(ExchangeRecord, v);
+  const uint32_t vs = uint32_t(sizeof(ExchangeRecord));
+  if (owner_fold)
+    k_fold<true><<<blocks_for(total, 256), 256, 0, st>>>(g, p, k, v, vb, vs, x.q_rec, x.sort_count,
+                                                         x.seg_n);
+  else
+    k_fold<false><<<blocks_for(total, 256), 256, 0, st>>>(g, p, k, v, vb, vs, x.q_rec,
+                                                          x.sort_count, nullptr);
   count_launch();
 }
 
@@ -3023,7 +3029,7 @@ static void set_carveouts() {
   const int pct = e ? std::atoi(e) : 0, pct_shadow = e2 ? std::atoi(e2) : 25;
   if (pct >= 0)
     for (const void* f : {reinterpret_cast<const void*>(k_primary), reinterpret_cast<const void*>(k_sample),
-                          reinterpret_cast<const void*>(k_bounce), reinterpret_cast<const void*>(k_fold),
+                          reinterpret_cast<const void*>(k_bounce), reinterpret_cast<const void*>(k_fold<false>),
                           reinterpret_cast<const void*>(k_accumulate)})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   if (pct_shadow >= 0)
@@ -3238,9 +3244,9 @@ void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
   if (p.nv == 0) return;
   PassParams q = p;
   q.n = p.nv;  // k_fold runs over the update records of all path vertices
-  k_fold<<<blocks_for(q.n, 256), 256, 0, st>>>(
+  k_fold<false><<<blocks_for(q.n, 256), 256, 0, st>>>(
       g, q, keys, vals, reinterpret_cast<const char*>(b.srec) + offsetof(SampleRec, v),
-      uint32_t(sizeof(SampleRec)), b.q_before, RLC_SORT_COMPACT ? b.sort_count : nullptr);
+      uint32_t(sizeof(SampleRec)), b.q_before, RLC_SORT_COMPACT ? b.sort_count : nullptr, nullptr);
   count_launch();
 }
 
