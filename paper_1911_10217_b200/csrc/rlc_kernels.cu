@@ -9,7 +9,8 @@
 //   k_fold         sequential update_q per (cell, cluster) segment in canonical
 //                  order -> live q, visits and per-sample q_before
 //   k_accumulate   deferred radiance with q_before, Framebuffer::add_sample
-//   k_split        split-collapse + ends + serial cdf per touched cell (one warp/cell)
+//   k_split        split-collapse + ends per touched cell (one warp/cell),
+//                  then the serial cdf (one lane/cell)
 //
 // All FP64 arithmetic keeps the reference's operand order and this file is
 // compiled with --fmad=false: the path is bit-exact with the reference
@@ -2295,9 +2296,9 @@ __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
 }
 
 // ---------------------------------------------------------------------------
-// k_split: split_collapse (cut.cpp:119-190) + rebuild_ends + serial
-// rebuild_cdf for every touched cell (render.cpp:185-200).  One warp per
-// cell, cut rows staged in shared memory.
+// k_split: split_collapse (cut.cpp:119-190) + rebuild_ends for every
+// touched cell (render.cpp:185-200), one warp per cell, cut rows staged in
+// shared memory; then the serial rebuild_cdf, one lane per cell.
 // ---------------------------------------------------------------------------
 struct WarpArg {
   double val;
@@ -2327,6 +2328,30 @@ __device__ __forceinline__ WarpArg warp_argmin(WarpArg a) {
       a = b;
   }
   return a;
+}
+
+// The cdf row of a cell from its q row (rebuild_cdf, cut.cpp:88-95).
+__device__ __forceinline__ void cdf_row(const DevGrid& g, uint32_t cell) {
+  const uint32_t M = g.M;
+  const size_t row = size_t(cell) * M;
+  double run = 0;
+  if ((M & 1u) == 0) {  // rows of 16-byte pairs
+    const double2* q2 = reinterpret_cast<const double2*>(g.q + row);
+    double2* c2 = reinterpret_cast<double2*>(g.cdf + row);
+#pragma unroll 8
+    for (uint32_t i = 0; i < M / 2; ++i) {
+      const double2 v = q2[i];
+      run += v.x;
+      const double a = run;
+      run += v.y;
+      c2[i] = make_double2(a, run);
+    }
+  } else {
+    for (uint32_t i = 0; i < M; ++i) {
+      run += g.q[row + i];
+      g.cdf[row + i] = run;
+    }
+  }
 }
 
 template <bool GLOBAL_ROWS>
@@ -2432,20 +2457,19 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
         g.ends[row + i] = sc.lt[nA[i]].range_end;
       }
     }
-    // rebuild_cdf: the serial left-to-right sum (bit-exact order) by lane 0
-    // into shared memory, then the row stored by the whole warp
-    if (lane == 0) {
-      double run = 0;
-#pragma unroll 8
-      for (uint32_t i = 0; i < M; ++i) {
-        run += qA[i];
-        qB[i] = run;
-      }
-    }
-    __syncwarp();
-    for (uint32_t i = lane; i < M; i += 32) g.cdf[row + i] = qB[i];
-    if (lane == 0) g.touched[cell] = 0u;
-    __syncwarp();
+    __syncwarp();  // (the rows are refilled for the next cell)
+  }
+  // rebuild_cdf (cut.cpp:88-95) of the warp's cells: the serial
+  // left-to-right sum, bit-exact, one lane per cell -- the warp's cells at
+  // once instead of one lane summing while 31 wait (the serial sum by lane 0
+  // was 40% of this kernel's instructions).  The rows this warp wrote are
+  // visible to its lanes after the __syncwarp above.
+  const uint32_t wstride = gridDim.x * wpb;
+  for (uint32_t cell = blockIdx.x * wpb + wib + lane * wstride; cell < ncells;
+       cell += 32 * wstride) {
+    if (!g.touched[cell]) continue;
+    cdf_row(g, cell);
+    g.touched[cell] = 0u;
   }
   if (lane == 0 && my_changes) atomicAdd(changes_out, my_changes);
 }
