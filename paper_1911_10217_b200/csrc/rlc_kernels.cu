@@ -133,6 +133,21 @@ static inline uint32_t blocks_for(uint32_t n, uint32_t t) { return (n + t - 1) /
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ V3 ld3(const double* p) { return V3{p[0], p[1], p[2]}; }
 
+// A 16-byte-aligned record of read-only data in 128-bit loads (scattered
+// records cost one L1 wavefront per load instruction and lane).
+template <typename T>
+__device__ __forceinline__ T ldg_vec(const T* p) {
+  static_assert(sizeof(T) % 16 == 0 && alignof(T) >= 16, "16-byte records");
+  union {
+    T t;
+    double2 d[sizeof(T) / 16];
+  } u;
+  const double2* s = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < int(sizeof(T) / 16); ++i) u.d[i] = __ldg(s + i);
+  return u.t;
+}
+
 struct NodeView {
   double lo0, lo1, lo2, hi0, hi1, hi2;
   uint32_t a, b, count;
@@ -1037,7 +1052,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // path vertex
   if (idx >= P.nv) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
-  const GBuf gb = gbuf[idx];
+  const GBuf gb = ldg_vec(gbuf + idx);
   keys[idx] = kInvalidKey;
 #if !RLC_SORT_COMPACT
   vals[idx] = idx;  // the record sort's values (every vertex is sorted)
@@ -1135,9 +1150,16 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   V3 p0, p1, p2, nl, emission;
   double pdf_area;
   if (lpos != 0xffffffffu) {  // the pick's record at its tree position (order[] folded in)
-    const LightOrd& L = sc.lights_ord[lpos];
+    // (the fields up to `emitter`, 112 B, in 128-bit loads)
+    struct alignas(16) Head {
+      double p[12];
+      double pdf_area;
+      uint32_t mat, emitter;
+    };
+    static_assert(sizeof(Head) == 112 && offsetof(LightOrd, emitter) == 108, "LightOrd layout");
+    const Head L = ldg_vec(reinterpret_cast<const Head*>(sc.lights_ord + lpos));
     e = L.emitter;
-    p0 = ld3(L.p0), p1 = ld3(L.p1), p2 = ld3(L.p2), nl = ld3(L.n);
+    p0 = ld3(L.p), p1 = ld3(L.p + 3), p2 = ld3(L.p + 6), nl = ld3(L.p + 9);
     pdf_area = L.pdf_area;
     emission = ld3(sc.mats[L.mat].emission);
   } else {
@@ -2270,7 +2292,7 @@ __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
       const MatRec& m = sc.mats[flags & kGMatMask];
       if (flags & kGEmit) L = L + ld3(m.emission);
       if (!(flags & kGReflective)) break;
-      const SampleRec& r = srec[idx];
+      const SampleRec r = ldg_vec(srec + idx);
       V3 rad{0.0, 0.0, 0.0};
       if (r.flags & kSNonzero) {
         double pdf_sel;
