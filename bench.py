@@ -330,8 +330,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             update(p)
             frame.step(p)
 
-    for p in range(args.warmup):
-        step(p)
+    # multi-GPU over NCCL, static scene: the frames replay a captured CUDA
+    # graph of two sharded frames (kernels and collectives; rlc_shard_frames)
+    graphed = world > 1 and args.dist_backend == "nccl" and not dynamic
+    if graphed:
+        frame.run(0, args.warmup, graph=True)
+    else:
+        for p in range(args.warmup):
+            step(p)
     update_ms[0] = 0.0
     ctx.synchronize()
     ctx.stage_times()
@@ -354,6 +360,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e0.record(stream)
     if batch:
         rlcuts.render_passes(ctx, cfg, args.warmup, args.steps, grid, fb)
+    elif graphed:
+        frame.run(args.warmup, args.steps, graph=True)
     else:
         for p in range(args.warmup, args.warmup + args.steps):
             step(p)
@@ -514,6 +522,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "parallelism": (f"screen bands x{world}, exact update-record all-gather "
                                        f"over {args.dist_backend}, "
                                        f"{'replicated' if args.replicated_fold else 'owner'}-folded"
+                                       + (", CUDA-graph replay" if graphed else "")
                                        if world > 1 else "single GPU"),
                        "cells": st["occupied"], "fallback_hits": st["fallback_hits"],
                        **grid_insert_stats},

@@ -382,6 +382,16 @@ rlc_status rlc_shard_frame(const rlc_context* ctx, const rlc_render_config* conf
                            uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb,
                            rlc_comm* comm, uint32_t row_begin, uint32_t row_end,
                            uint64_t cap_records, int owner_fold);
+/* Frames first_pass .. first_pass + count - 1 of rlc_shard_frame.  use_graph:
+ * after one direct frame (which sizes every buffer), a CUDA graph of two
+ * frames -- kernels and NCCL collectives, the pass index read from device
+ * memory -- is captured once and replayed; the results equal the direct
+ * frames bit for bit. */
+rlc_status rlc_shard_frames(const rlc_context* ctx, const rlc_render_config* config,
+                            uint32_t first_pass, uint32_t count, rlc_grid* grid,
+                            rlc_framebuffer* fb, rlc_comm* comm, uint32_t row_begin,
+                            uint32_t row_end, uint64_t cap_records, int owner_fold,
+                            int use_graph);
 
 /* ---- per-sample parity export (SURVEY 8(b) "opt-in per-sample record
  * dump") ---------------------------------------------------------------

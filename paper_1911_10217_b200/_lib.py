@@ -138,6 +138,8 @@ SIGNATURES = {
     "rlc_comm_destroy": (C.c_int, [_P]),
     "rlc_shard_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, _P, _P, C.c_uint32,
                                   C.c_uint32, C.c_uint64, C.c_int]),
+    "rlc_shard_frames": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, C.c_uint32, _P, _P, _P,
+                                   C.c_uint32, C.c_uint32, C.c_uint64, C.c_int, C.c_int]),
     "rlc_render_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.POINTER(RenderResultC)]),
     "rlc_context_enable_sample_export": (C.c_int, [_P, C.c_int]),
     "rlc_pass_samples": (C.c_int, [_P, C.c_uint64, C.c_void_p, _u64p]),

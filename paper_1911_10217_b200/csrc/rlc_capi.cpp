@@ -439,6 +439,7 @@ struct rlc_context {
   ~rlc_context() {
     if (h_stage) cudaFreeHost(h_stage);
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
+    if (shard_graph.exec) cudaGraphExecDestroy(shard_graph.exec);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (ev_prim_done) cudaEventDestroy(ev_prim_done);
     if (ev_main_fence) cudaEventDestroy(ev_main_fence);
@@ -525,6 +526,18 @@ struct rlc_context {
     uint64_t launches = 0;  // kernels per replay
   } graph;
   uint32_t scene_gen = 0;       // bumped by rlc_context_update_scene
+  // CUDA graph of two sharded frames (rlc_shard_frames), NCCL calls included
+  struct ShardGraph {
+    cudaGraphExec_t exec = nullptr;
+    rlc_render_config cfg{};
+    const void *grid = nullptr, *fb = nullptr, *comm = nullptr, *gathered = nullptr,
+               *block = nullptr;
+    uint32_t r0 = 0, r1 = 0;
+    uint64_t cap = 0;
+    int owner = 0;
+    uint32_t pb_gen = 0, scene_gen = 0;
+    uint64_t launches = 0;
+  } shard_graph;
   const uint32_t* graph_pass_dev = nullptr;  // set while capturing: setup_pass reads it
   uint32_t* d_pass = nullptr;     // device pass index of graph replays
   // pinned staging for large downloads (download_to_host)
@@ -1599,6 +1612,12 @@ void shard_fold(rlc_context* ctx, const rlc_render_config* config, rlc_grid* gri
   ctx->stage(9, [&] {
     rlc::launch_shard_fold(S.g, S.p, rank, owner_fold != 0, ctx->xb, ctx->stream);
   });
+  // the next pass's lookups (its primary rays on the side stream) must see
+  // this pass's new keys
+  if (ctx->overlap && ctx->pstream) {
+    RLC_CK(cudaEventRecord(ctx->ev_commit, ctx->stream));
+    RLC_CK(cudaStreamWaitEvent(ctx->pstream, ctx->ev_commit, 0));
+  }
   ctx->stage(3, [&] {
     rlc::launch_shard_sortfold(S.g, S.p, grid->key_bits, owner_fold != 0, ctx->xb, ctx->stream);
   });
@@ -1752,6 +1771,40 @@ rlc_status rlc_comm_destroy(rlc_comm* comm) {
   return guarded([&] { delete comm; });
 }
 
+namespace {
+// One sharded frame on the context stream (rlc_shard_frame): the band's
+// trace, the NCCL exchange, the exact fold and split-collapse.
+void shard_frame_body(rlc_context* ctx, const rlc_render_config* config, uint32_t pass_index,
+                      rlc_grid* grid, rlc_framebuffer* fb, rlc_comm* comm, uint32_t row_begin,
+                      uint32_t row_end, uint64_t cap_records, int owner_fold) {
+  shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
+  const uint64_t bb = ctx->block_bytes();
+  if (comm->gathered_bytes < bb * comm->nranks) {
+    ctx->sync_all();
+    comm->arena.release();
+    comm->gathered = comm->arena.alloc<unsigned char>(bb * comm->nranks);
+    comm->gathered_bytes = bb * comm->nranks;
+  }
+  cudaStream_t st = ctx->stream;
+  // the exchange: every rank's block to every rank (fixed size: no host count)
+  nccl_check(nccl().all_gather(ctx->block, comm->gathered, bb, ncclUint8, comm->comm, st),
+             "ncclAllGather");
+  shard_fold(ctx, config, grid, comm->gathered, comm->nranks, comm->rank, owner_fold);
+  if (owner_fold && comm->nranks > 1) {  // q_before and entry counts from the cells' owners
+    const size_t slots = size_t(comm->nranks) * ctx->xb.stride;
+    nccl_check(nccl().all_reduce(ctx->xb.q_rec, ctx->xb.q_rec, slots, ncclFloat64, ncclSum,
+                                 comm->comm, st),
+               "ncclAllReduce");
+    nccl_check(nccl().all_reduce(ctx->xb.seg_n, ctx->xb.seg_n, slots, ncclUint32, ncclSum,
+                                 comm->comm, st),
+               "ncclAllReduce");
+  }
+  shard_finish(ctx, grid, fb, comm->rank, owner_fold);
+  RLC_CK(cudaMemsetAsync(grid->d_changes, 0, 4, st));
+  enqueue_eop(grid, ctx, &config->cut, grid->d_changes);  // split-collapse: identical on every rank
+}
+}  // namespace
+
 rlc_status rlc_shard_frame(const rlc_context* cctx, const rlc_render_config* config,
                            uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb,
                            rlc_comm* comm, uint32_t row_begin, uint32_t row_end,
@@ -1761,31 +1814,95 @@ rlc_status rlc_shard_frame(const rlc_context* cctx, const rlc_render_config* con
             "rlc_shard_frame: null argument");
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     require(comm->device == ctx->device, "rlc_shard_frame: communicator on another device");
-    shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
-    const uint64_t bb = ctx->block_bytes();
-    if (comm->gathered_bytes < bb * comm->nranks) {
-      ctx->sync_all();
-      comm->arena.release();
-      comm->gathered = comm->arena.alloc<unsigned char>(bb * comm->nranks);
-      comm->gathered_bytes = bb * comm->nranks;
+    shard_frame_body(ctx, config, pass_index, grid, fb, comm, row_begin, row_end, cap_records,
+                     owner_fold);
+  });
+}
+
+rlc_status rlc_shard_frames(const rlc_context* cctx, const rlc_render_config* config,
+                            uint32_t first_pass, uint32_t count, rlc_grid* grid,
+                            rlc_framebuffer* fb, rlc_comm* comm, uint32_t row_begin,
+                            uint32_t row_end, uint64_t cap_records, int owner_fold,
+                            int use_graph) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr && comm != nullptr && grid != nullptr,
+            "rlc_shard_frames: null argument");
+    rlc_context* ctx = const_cast<rlc_context*>(cctx);
+    require(comm->device == ctx->device, "rlc_shard_frames: communicator on another device");
+    auto single = [&](uint32_t p) {
+      shard_frame_body(ctx, config, p, grid, fb, comm, row_begin, row_end, cap_records,
+                       owner_fold);
+    };
+    constexpr uint32_t kFrames = 2;  // one frame per G-buffer slot
+    if (!use_graph || ctx->timing || count < kFrames) {
+      for (uint32_t p = first_pass; p < first_pass + count; ++p) single(p);
+      return;
     }
     cudaStream_t st = ctx->stream;
-    // the exchange: every rank's block to every rank (fixed size: no host count)
-    nccl_check(nccl().all_gather(ctx->block, comm->gathered, bb, ncclUint8, comm->comm, st),
-               "ncclAllGather");
-    shard_fold(ctx, config, grid, comm->gathered, comm->nranks, comm->rank, owner_fold);
-    if (owner_fold && comm->nranks > 1) {  // q_before and entry counts from the cells' owners
-      const size_t slots = size_t(comm->nranks) * ctx->xb.stride;
-      nccl_check(nccl().all_reduce(ctx->xb.q_rec, ctx->xb.q_rec, slots, ncclFloat64, ncclSum,
-                                   comm->comm, st),
-                 "ncclAllReduce");
-      nccl_check(nccl().all_reduce(ctx->xb.seg_n, ctx->xb.seg_n, slots, ncclUint32, ncclSum,
-                                   comm->comm, st),
-                 "ncclAllReduce");
+    if (!ctx->d_pass) {
+      ctx->d_pass = ctx->arena.alloc<uint32_t>(2);
+      ctx->d_changes = ctx->d_pass + 1;
+      RLC_CK(cudaMemsetAsync(ctx->d_pass, 0, 8, st));
     }
-    shard_finish(ctx, grid, fb, comm->rank, owner_fold);
-    RLC_CK(cudaMemsetAsync(grid->d_changes, 0, 4, st));
-    enqueue_eop(grid, ctx, &config->cut, grid->d_changes);  // split-collapse: identical on every rank
+    // every allocation outside the capture: one frame run directly sizes the
+    // pass, block, exchange and gather buffers
+    single(first_pass);
+    ++first_pass;
+    --count;
+    auto& G = ctx->shard_graph;
+    const bool same = G.exec && std::memcmp(&G.cfg, config, sizeof(*config)) == 0 &&
+                      G.grid == grid && G.fb == fb && G.comm == comm && G.r0 == row_begin &&
+                      G.r1 == row_end && G.cap == cap_records && G.owner == owner_fold &&
+                      G.pb_gen == ctx->pb_gen && G.scene_gen == ctx->scene_gen &&
+                      G.gathered == comm->gathered && G.block == ctx->block;
+    if (!same) {
+      if (G.exec) {
+        RLC_CK(cudaGraphExecDestroy(G.exec));
+        G.exec = nullptr;
+      }
+      ctx->graph_pass_dev = ctx->d_pass;
+      const uint64_t l0 = rlc::launches();
+      cudaGraph_t graph = nullptr;
+      RLC_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+      try {
+        for (cudaEvent_t e : ctx->ev_gbuf_free) RLC_CK(cudaEventRecord(e, st));
+        for (uint32_t i = 0; i < kFrames; ++i) single(i);  // slot i; pass *d_pass + i
+        if (ctx->overlap && ctx->pstream) {  // join the side stream's last wait
+          RLC_CK(cudaEventRecord(ctx->ev_prim_done, ctx->pstream));
+          RLC_CK(cudaStreamWaitEvent(st, ctx->ev_prim_done, 0));
+        }
+        rlc::launch_add_u32(ctx->d_pass, kFrames, st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        ctx->graph_pass_dev = nullptr;
+        throw;
+      }
+      RLC_CK(cudaStreamEndCapture(st, &graph));
+      ctx->graph_pass_dev = nullptr;
+      G.launches = rlc::launches() - l0;
+      const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      RLC_CK(e);
+      G.cfg = *config;
+      G.grid = grid;
+      G.fb = fb;
+      G.comm = comm;
+      G.r0 = row_begin;
+      G.r1 = row_end;
+      G.cap = cap_records;
+      G.owner = owner_fold;
+      G.pb_gen = ctx->pb_gen;
+      G.scene_gen = ctx->scene_gen;
+      G.gathered = comm->gathered;
+      G.block = ctx->block;
+    }
+    const uint32_t replays = count / kFrames;
+    rlc::launch_set_u32(ctx->d_pass, first_pass, st);
+    for (uint32_t r = 0; r < replays; ++r) RLC_CK(cudaGraphLaunch(G.exec, st));
+    rlc::add_launches(G.launches * replays);
+    for (cudaEvent_t e : ctx->ev_gbuf_free) RLC_CK(cudaEventRecord(e, st));
+    for (uint32_t p = first_pass + replays * kFrames; p < first_pass + count; ++p) single(p);
   });
 }
 

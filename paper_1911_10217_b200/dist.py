@@ -145,6 +145,12 @@ class NcclFrame:
         rlcuts.shard_frame(e.ctx, e.cfg, pass_index, e.grid, e.fb, self.comm, self.rows, e.cap,
                            self.owner)
 
+    def run(self, first_pass: int, count: int, graph: bool = True) -> None:
+        """`count` frames in one call, replayed from a captured CUDA graph."""
+        e = self.engine
+        rlcuts.shard_frames(e.ctx, e.cfg, first_pass, count, e.grid, e.fb, self.comm, self.rows,
+                            e.cap, self.owner, graph)
+
 
 def local_exchange(engines, heights_rows, pass_index: int, owner: bool = True,
                    serial: bool = False):

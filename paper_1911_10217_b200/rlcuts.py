@@ -557,6 +557,17 @@ def shard_frame(ctx: RenderContext, config: RenderConfig, pass_index: int, grid:
                                        cap_records, int(owner_fold)))
 
 
+def shard_frames(ctx: RenderContext, config: RenderConfig, first_pass: int, count: int,
+                 grid: HashGrid, framebuffer: Framebuffer, comm: Comm, rows: tuple,
+                 cap_records: int, owner_fold: bool = True, graph: bool = True):
+    """rlc_shard_frames: `count` frames of shard_frame, replayed from a CUDA
+    graph of two frames (kernels and NCCL collectives) when `graph`."""
+    cfg = config.c()
+    _check(_lib.load().rlc_shard_frames(ctx.handle, C.byref(cfg), first_pass, count, grid.handle,
+                                        framebuffer.handle, comm.handle, rows[0], rows[1],
+                                        cap_records, int(owner_fold), int(graph)))
+
+
 @dataclass
 class RenderResult:  # render.hpp:56-64
     image: np.ndarray

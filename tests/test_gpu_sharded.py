@@ -111,3 +111,29 @@ def test_nccl_frame_one_rank_matches_render_pass(ref, owner):
         for f in v:
             assert np.array_equal(cells[k][f], v[f])
     assert grid.stats() == rr.stats()
+
+
+@pytest.mark.parametrize("owner", [True, False])
+def test_nccl_frames_graph_replay_bit_exact(owner):
+    """rlc_shard_frames replaying a captured CUDA graph of two sharded frames
+    (NCCL collectives inside) equals the same frames enqueued one by one."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
+    cfg = rlcuts.RenderConfig(spp=9, passes=9, sampler=RL,
+                              cut=rlcuts.CutConfig(cut_size=64, split_threshold=2.0))
+    out = []
+    for graph in (False, True):
+        ctx = rlcuts.build_context(scene, cfg)
+        grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+        eng = rdist.GpuEngine(ctx, grid, fb, cfg, torch.device("cuda", 0))
+        frame = rdist.NcclFrame(eng, scene.camera.height, 0, 1, 0, owner)
+        frame.run(0, 4, graph)
+        frame.run(4, cfg.passes - 4, graph)  # a second replay run of the cached graph
+        rlcuts.shard_sync(ctx, grid)
+        out.append((fb.download(), grid.export(), grid.stats()))
+    (s0, c0), cells0, st0 = out[0]
+    (s1, c1), cells1, st1 = out[1]
+    assert np.array_equal(s0, s1) and np.array_equal(c0, c1) and st0 == st1
+    assert cells0.keys() == cells1.keys()
+    for k, v in cells0.items():
+        for f in v:
+            assert np.array_equal(cells1[k][f], v[f])

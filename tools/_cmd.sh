@@ -1,2 +1,3 @@
-bash tools/ab_env.sh 2 "" "RLC_HPRIO=1" "RLC_HPRIO=3" "RLC_HPRIO=5" "RLC_HPRIO=7" "RLC_HPRIO=15" > gpurun_out/ab34.txt 2>&1
-cat gpurun_out/ab34.txt
+python -m pytest tests -x -q -m gpu > gpurun_out/t_all.txt 2>&1
+tail -3 gpurun_out/t_all.txt
+python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b_quick.json 2>&1; tail -c 400 gpurun_out/b_quick.json
