@@ -2,8 +2,8 @@
 emulated as N contexts on one device and a host-driven exchange (no kernel
 waits on another rank) must reproduce the single-context pass and the
 reference bit for bit, with the fold replicated on every rank or done by the
-owner of each cell; the NCCL data plane (rlc_shard_frame) at one rank; and
-two processes sharing the device over gloo through ShardedFrame."""
+owner of each cell (also on c3 over 8 ranks); the NCCL data plane
+(rlc_shard_frame, and its CUDA-graph replay) at one rank."""
 import numpy as np
 import pytest
 import torch
@@ -46,6 +46,41 @@ def test_sharded_gpu_matches_single(ref, world, depth, owner):
                 assert np.array_equal(cells[k][f], v[f])
         lookups += e.grid.lookup_count()
     assert lookups == rr.stats()["lookups"]
+
+
+def test_sharded_c3_eight_ranks_owner(ref):
+    """The headline scene (1M emitters) at 320 x 180 over 8 emulated ranks,
+    owner-partitioned: 6 frames of bands, exchange, insertion and fold equal
+    the reference's single-process frames."""
+    scene, st = scenes.config_scene("c3")
+    scene = scene.with_resolution(320, 180)
+    cfg = rlcuts.RenderConfig(spp=6, passes=6, sampler=RL,
+                              hash=rlcuts.HashConfig(base_tile=st["base_tile"]))
+    world = 8
+    dev = torch.device("cuda", 0)
+    engines = []
+    for r in range(world):
+        ctx = rlcuts.build_context(scene, cfg)
+        engines.append(rdist.GpuEngine(ctx, rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx),
+                                       cfg, dev, world=world))
+    rows = [rdist.band(scene.camera.height, r, world) for r in range(world)]
+    rr = ref.RefRun(scene, cfg)
+    for p in range(cfg.passes):
+        changes = rdist.local_exchange(engines, rows, p, owner=True)
+        rch, _ = rr.run_pass(p)
+        assert changes == [rch] * world
+    rs, rc = rr.framebuffer()
+    rcells = rr.export()
+    for e, (r0, r1) in zip(engines, rows):
+        s, c = e.fb.download()
+        assert np.array_equal(s[r0:r1], rs[r0:r1]) and np.array_equal(c[r0:r1], rc[r0:r1])
+    for e in (engines[0], engines[-1]):
+        cells = e.grid.export()
+        assert cells.keys() == rcells.keys()
+        for k, v in rcells.items():
+            for f in v:
+                assert np.array_equal(cells[k][f], v[f])
+        assert [(s_, k) for s_, _, k, _ in e.grid.slots()] == rr.slots()
 
 
 @pytest.mark.parametrize("owner", [False, True])
