@@ -567,6 +567,7 @@ struct rlc_context {
     srec_slot[0] = scratch.alloc<rlc::SampleRec>(cap);
     srec_slot[1] = scratch.alloc<rlc::SampleRec>(cap);
     pb.srec = srec_slot[0];
+    pb.vdense = scratch.alloc<double>(cap);
     pb.rflag = scratch.alloc<uint8_t>(cap);
     pb.keys = scratch.alloc<uint32_t>(cap);
     pb.vals = scratch.alloc<uint32_t>(cap);

@@ -1048,7 +1048,8 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
                                                 ShadowRay* __restrict__ rays,
                                                 unsigned int* __restrict__ ray_count,
                                                 const unsigned long long* __restrict__ pkey,
-                                                uint32_t* __restrict__ emit) {
+                                                uint32_t* __restrict__ emit,
+                                                double* __restrict__ vdense) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // path vertex
   if (idx >= P.nv) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
@@ -1224,6 +1225,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
     }
   }
   srec[idx] = r;
+  vdense[idx] = r.v;
   rflag[idx] = uint8_t(r.flags & (kSRay | kSRecord));
 }
 
@@ -1733,8 +1735,9 @@ __device__ __forceinline__ bool tri_any(const TriAccel* tris, uint32_t i, V3 o, 
          !(t <= tmin || t >= tmax);
 }
 
-__device__ __forceinline__ void mark_occluded(SampleRec* srec, uint32_t idx) {
+__device__ __forceinline__ void mark_occluded(SampleRec* srec, double* vdense, uint32_t idx) {
   srec[idx].v = 0.0;  // nee_estimate returns the zero result (estimators.cpp:95)
+  vdense[idx] = 0.0;
   srec[idx].flags &= ~kSNonzero;
 }
 
@@ -1753,6 +1756,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
                                                            const uint32_t* __restrict__ order,
                                                            unsigned int* __restrict__ ray_count,
                                                            SampleRec* __restrict__ srec,
+                                                           double* __restrict__ vdense,
                                                            unsigned int* __restrict__ err) {
   const uint32_t lane = threadIdx.x & 31u;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -1818,7 +1822,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
             rf.tmin_in = __double2float_ru(tmin);
             rf.tmax_in = __double2float_rd(tmax);
             if (exact) {  // tiny scene or fp32-range ray: the exact fp64 path
-              if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, idx);
+              if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, vdense, idx);
             } else {
               cur = 0;
               active = true;
@@ -1971,12 +1975,12 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
       }
     }
     if (hit) {
-      mark_occluded(srec, idx);
+      mark_occluded(srec, vdense, idx);
       active = false;
     } else if (cur == kDone && leaf == 0) {
       if (overflow) {  // rare: the whole segment again, exactly as the reference
         RLC_STAT(6, 1);
-        if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, idx);
+        if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, vdense, idx);
         overflow = false;
       }
       active = false;
@@ -3114,7 +3118,7 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
   cudaMemsetAsync(b.ray_count, 0, 2 * sizeof(unsigned int), st);
   k_sample<<<blocks_for(p.nv, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.rflag, b.keys, b.vals,
                                                   b.q_before, b.rays, b.ray_count, b.pkey,
-                                                  b.emit);
+                                                  b.emit, b.vdense);
   count_launch();
 }
 
@@ -3235,7 +3239,8 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   auto kern = sc.count_work ? (sc.wide_q ? k_shadow<true, true> : k_shadow<false, true>)
                             : (sc.wide_q ? k_shadow<true, false> : k_shadow<false, false>);
   kern<<<use * sms, kShadowThreads, 0, st>>>(
-      sc, b.rays, order, b.ray_count, b.srec, reinterpret_cast<unsigned int*>(counters + kCntErr));
+      sc, b.rays, order, b.ray_count, b.srec, b.vdense,
+      reinterpret_cast<unsigned int*>(counters + kCntErr));
   count_launch();
 }
 
@@ -3291,8 +3296,8 @@ void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
   PassParams q = p;
   q.n = p.nv;  // k_fold runs over the update records of all path vertices
   k_fold<false><<<blocks_for(q.n, 256), 256, 0, st>>>(
-      g, q, keys, vals, reinterpret_cast<const char*>(b.srec) + offsetof(SampleRec, v),
-      uint32_t(sizeof(SampleRec)), b.q_before, RLC_SORT_COMPACT ? b.sort_count : nullptr, nullptr);
+      g, q, keys, vals, reinterpret_cast<const char*>(b.vdense), uint32_t(sizeof(double)),
+      b.q_before, RLC_SORT_COMPACT ? b.sort_count : nullptr, nullptr);
   count_launch();
 }
 

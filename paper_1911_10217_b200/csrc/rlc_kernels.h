@@ -184,6 +184,7 @@ struct PassBuffers {
   NewKeys nk;
   uint32_t* emit;            // [vertex] emitter index (P.export_samples)
   SampleRec* srec;
+  double* vdense;        // [vertex] srec's v, dense: the fold's gathers stay in L2
   uint8_t* rflag;        // per vertex: the kSRay | kSRecord bits of srec (compaction input)
   uint32_t* keys;
   uint32_t* vals;

@@ -1,1 +1,4 @@
-for v in 1 0; do RLC_ONESWEEP=$v python tools/shard_budget.py 8 8 c3 both > gpurun_out/sb_os$v.txt 2>&1; echo "ONESWEEP=$v"; grep -A3 "rank " gpurun_out/sb_os$v.txt | grep "^   4\|rank"; done
+bash tools/ab3.sh 3 > gpurun_out/ab36.txt 2>&1
+cat gpurun_out/ab36.txt
+python -m pytest tests -x -q -m gpu > gpurun_out/t_all.txt 2>&1
+tail -3 gpurun_out/t_all.txt
