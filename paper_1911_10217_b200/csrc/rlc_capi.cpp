@@ -395,6 +395,7 @@ struct rlc_context {
   // sample records and q_before per G-buffer slot: pass p's accumulation
   // (side stream) reads them while pass p + 1 samples and folds
   rlc::SampleRec* srec_slot[2] = {nullptr, nullptr};
+  uint8_t* rflag_slot[2] = {nullptr, nullptr};  // (the occluded bits k_accumulate reads)
   double* qb_slot[2] = {nullptr, nullptr};
   void sync_all() {
     RLC_CK(cudaStreamSynchronize(stream));
@@ -568,7 +569,9 @@ struct rlc_context {
     srec_slot[1] = scratch.alloc<rlc::SampleRec>(cap);
     pb.srec = srec_slot[0];
     pb.vdense = scratch.alloc<double>(cap);
-    pb.rflag = scratch.alloc<uint8_t>(cap);
+    rflag_slot[0] = scratch.alloc<uint8_t>(cap);
+    rflag_slot[1] = scratch.alloc<uint8_t>(cap);
+    pb.rflag = rflag_slot[0];
     pb.keys = scratch.alloc<uint32_t>(cap);
     pb.vals = scratch.alloc<uint32_t>(cap);
     pb.keys_alt = scratch.alloc<uint32_t>(cap);
@@ -693,6 +696,7 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   ctx->pb.gbuf = ctx->gslot[slot];
   ctx->pb.pkey = ctx->pkey_slot[slot];
   ctx->pb.srec = ctx->srec_slot[slot];
+  ctx->pb.rflag = ctx->rflag_slot[slot];
   ctx->pb.q_before = ctx->qb_slot[slot];
   const bool rl = S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
   // The pass's new keys go in after all its lookups, in canonical order

@@ -1735,10 +1735,10 @@ __device__ __forceinline__ bool tri_any(const TriAccel* tris, uint32_t i, V3 o, 
          !(t <= tmin || t >= tmax);
 }
 
-__device__ __forceinline__ void mark_occluded(SampleRec* srec, double* vdense, uint32_t idx) {
-  srec[idx].v = 0.0;  // nee_estimate returns the zero result (estimators.cpp:95)
+// nee_estimate returns the zero result (estimators.cpp:95)
+__device__ __forceinline__ void mark_occluded(uint8_t* rflag, double* vdense, uint32_t idx) {
   vdense[idx] = 0.0;
-  srec[idx].flags &= ~kSNonzero;
+  rflag[idx] |= kROccluded;
 }
 
 // Any-hit traversal of the queued shadow segments (occluded(), bvh.cpp:
@@ -1755,7 +1755,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
                                                            const ShadowRay* __restrict__ rays,
                                                            const uint32_t* __restrict__ order,
                                                            unsigned int* __restrict__ ray_count,
-                                                           SampleRec* __restrict__ srec,
+                                                           uint8_t* __restrict__ rflag,
                                                            double* __restrict__ vdense,
                                                            unsigned int* __restrict__ err) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -1822,7 +1822,7 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
             rf.tmin_in = __double2float_ru(tmin);
             rf.tmax_in = __double2float_rd(tmax);
             if (exact) {  // tiny scene or fp32-range ray: the exact fp64 path
-              if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, vdense, idx);
+              if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(rflag, vdense, idx);
             } else {
               cur = 0;
               active = true;
@@ -1975,12 +1975,12 @@ __global__ void __launch_bounds__(kShadowThreads, RLC_SHADOW_BLOCKS) k_shadow(De
       }
     }
     if (hit) {
-      mark_occluded(srec, vdense, idx);
+      mark_occluded(rflag, vdense, idx);
       active = false;
     } else if (cur == kDone && leaf == 0) {
       if (overflow) {  // rare: the whole segment again, exactly as the reference
         RLC_STAT(6, 1);
-        if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(srec, vdense, idx);
+        if (occluded_ray(sc, o, d, inv, tmin, tmax, err)) mark_occluded(rflag, vdense, idx);
         overflow = false;
       }
       active = false;
@@ -2273,6 +2273,7 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
 __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
                                                     const GBuf* __restrict__ gbuf,
                                                     const SampleRec* __restrict__ srec,
+                                                    const uint8_t* __restrict__ rflag,
                                                     const double* __restrict__ q_before,
                                                     Framebuf fb) {
   const uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2298,7 +2299,7 @@ __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
       if (!(flags & kGReflective)) break;
       const SampleRec r = ldg_vec(srec + idx);
       V3 rad{0.0, 0.0, 0.0};
-      if (r.flags & kSNonzero) {
+      if ((r.flags & kSNonzero) && !(rflag[idx] & kROccluded)) {
         double pdf_sel;
         if (r.flags & kSLearned) {
           const double p = q_before[idx] / r.total;
@@ -2503,15 +2504,14 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
 // Batch entry points of occluded() / intersect() (bvh.hpp:38-40).
 __global__ void k_segments(DevScene sc, uint32_t n, const double* __restrict__ a,
                            const double* __restrict__ b, ShadowRay* __restrict__ rays,
-                           unsigned int* __restrict__ ray_count, SampleRec* __restrict__ srec) {
+                           unsigned int* __restrict__ ray_count, uint8_t* __restrict__ rflag) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const V3 pa = ld3(a + 3 * size_t(i)), pb = ld3(b + 3 * size_t(i));
   const V3 dd = pb - pa;
   const double len = length(dd);
-  srec[i].flags = 0;
+  rflag[i] = 0;  // k_shadow sets kROccluded
   if (len <= 2 * sc.shadow_eps) return;  // bvh.cpp:162
-  srec[i].flags = kSNonzero;
   const V3 dir = dd / len;
   const unsigned slot = atomicAdd(ray_count, 1u);
   ShadowRay r;
@@ -2527,13 +2527,13 @@ __global__ void k_segments(DevScene sc, uint32_t n, const double* __restrict__ a
   rays[slot] = r;
 }
 
-__global__ void k_segments_out(uint32_t n, const SampleRec* __restrict__ srec,
-                               const double* __restrict__ a, const double* __restrict__ b,
-                               double eps2, uint8_t* __restrict__ out) {
+// occluded: a queued segment k_shadow found blocked (a segment of length
+// <= 2 shadow_eps is never queued nor occluded, bvh.cpp:162)
+__global__ void k_segments_out(uint32_t n, const uint8_t* __restrict__ rflag,
+                               uint8_t* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const V3 dd = ld3(b + 3 * size_t(i)) - ld3(a + 3 * size_t(i));
-  out[i] = (length(dd) > eps2 && !(srec[i].flags & kSNonzero)) ? 1 : 0;
+  out[i] = (rflag[i] & kROccluded) ? 1 : 0;
 }
 
 __global__ void k_intersect_batch(DevScene sc, uint32_t n, const double* __restrict__ org,
@@ -2564,9 +2564,9 @@ void launch_occluded_batch(const DevScene& sc, uint32_t n, const double* a, cons
                            cudaStream_t st) {
   if (n == 0) return;
   cudaMemsetAsync(pb.ray_count, 0, 2 * sizeof(unsigned int), st);
-  k_segments<<<blocks_for(n, 256), 256, 0, st>>>(sc, n, a, b, pb.rays, pb.ray_count, pb.srec);
+  k_segments<<<blocks_for(n, 256), 256, 0, st>>>(sc, n, a, b, pb.rays, pb.ray_count, pb.rflag);
   launch_shadow(sc, pb, nullptr, counters, st);
-  k_segments_out<<<blocks_for(n, 256), 256, 0, st>>>(n, pb.srec, a, b, 2 * sc.shadow_eps, out);
+  k_segments_out<<<blocks_for(n, 256), 256, 0, st>>>(n, pb.rflag, out);
   count_launch(2);
 }
 
@@ -2600,6 +2600,7 @@ static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t
 // ---------------------------------------------------------------------------
 __global__ void k_write_block(DevGrid g, const GBuf* __restrict__ gbuf,
                               const SampleRec* __restrict__ srec,
+                              const double* __restrict__ vdense,
                               const uint32_t* __restrict__ rec_path,
                               const unsigned int* __restrict__ count, uint32_t n,
                               const unsigned long long* __restrict__ pkey, uint32_t cap,
@@ -2616,7 +2617,7 @@ __global__ void k_write_block(DevGrid g, const GBuf* __restrict__ gbuf,
   const uint32_t cell = gbuf[idx].cell;
   ExchangeRecord r;
   r.cluster = srec[idx].s;
-  r.v = srec[idx].v;
+  r.v = vdense[idx];
   if (cell == kPending) {  // new this pass: inserted with all ranks' records
     r.slot = kPending;
     r.klo = pkey[2 * size_t(idx)];
@@ -2633,7 +2634,7 @@ void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, voi
                          uint32_t cap, cudaStream_t st) {
   launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);
   k_write_block<<<blocks_for(n > 0 ? n : 1, 256), 256, 0, st>>>(
-      g, b.gbuf, b.srec, b.rec_path, b.rec_count, n, b.pkey, cap,
+      g, b.gbuf, b.srec, b.vdense, b.rec_path, b.rec_count, n, b.pkey, cap,
       static_cast<ExchangeRecord*>(block));
   count_launch();
 }
@@ -2833,6 +2834,8 @@ void launch_add_u32(uint32_t* p, uint32_t v, cudaStream_t st) {
 // forms it (estimators.cpp:100-101 with the live q_before, cut.cpp:105).
 __global__ void k_export_samples(PassParams P, const GBuf* __restrict__ gbuf,
                                  const SampleRec* __restrict__ srec,
+                                 const uint8_t* __restrict__ rflag,
+                                 const double* __restrict__ vdense,
                                  const double* __restrict__ q_before,
                                  const uint32_t* __restrict__ emit, SampleExport* __restrict__ out) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2842,14 +2845,15 @@ __global__ void k_export_samples(PassParams P, const GBuf* __restrict__ gbuf,
   if (gbuf[idx].flags & kGReflective) {
     const SampleRec r = srec[idx];
     const bool learned = r.flags & kSLearned;
+    const bool nonzero = (r.flags & kSNonzero) && !(rflag[idx] & kROccluded);
     e.flags = 1u | (learned && !(r.flags & kSRecord) ? 2u : 0u) | (r.flags & kSRay ? 4u : 0u) |
-              (r.flags & kSNonzero ? 8u : 0u) | (learned ? 16u : 0u);
+              (nonzero ? 8u : 0u) | (learned ? 16u : 0u);
     e.cluster = learned ? r.s : 0u;
     e.emitter = P.export_samples ? emit[idx] : 0xffffffffu;
-    e.v = r.v;
+    e.v = vdense[idx];
     e.total = r.total;
     if (learned) e.q_before = q_before[idx];
-    if (r.flags & kSNonzero) {
+    if (nonzero) {
       const double pdf_sel = learned ? (e.q_before / r.total) * r.pin : r.pin;
       const double den = pdf_sel * r.pdf_area;
       e.radiance[0] = r.c[0] / den;
@@ -2863,7 +2867,8 @@ __global__ void k_export_samples(PassParams P, const GBuf* __restrict__ gbuf,
 void launch_export_samples(const PassParams& p, const PassBuffers& b, SampleExport* out,
                            cudaStream_t st) {
   if (p.nv == 0) return;
-  k_export_samples<<<blocks_for(p.nv, 256), 256, 0, st>>>(p, b.gbuf, b.srec, b.q_before, b.emit, out);
+  k_export_samples<<<blocks_for(p.nv, 256), 256, 0, st>>>(p, b.gbuf, b.srec, b.rflag, b.vdense,
+                                                          b.q_before, b.emit, out);
   count_launch();
 }
 
@@ -3239,7 +3244,7 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
   auto kern = sc.count_work ? (sc.wide_q ? k_shadow<true, true> : k_shadow<false, true>)
                             : (sc.wide_q ? k_shadow<true, false> : k_shadow<false, false>);
   kern<<<use * sms, kShadowThreads, 0, st>>>(
-      sc, b.rays, order, b.ray_count, b.srec, b.vdense,
+      sc, b.rays, order, b.ray_count, b.rflag, b.vdense,
       reinterpret_cast<unsigned int*>(counters + kCntErr));
   count_launch();
 }
@@ -3305,7 +3310,8 @@ void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffer
                        const Framebuf& fb, cudaStream_t st) {
   const uint32_t npix = p.spp_pp ? p.n / p.spp_pp : 0;
   if (npix == 0) return;
-  k_accumulate<<<blocks_for(npix, 256), 256, 0, st>>>(sc, p, b.gbuf, b.srec, b.q_before, fb);
+  k_accumulate<<<blocks_for(npix, 256), 256, 0, st>>>(sc, p, b.gbuf, b.srec, b.rflag, b.q_before,
+                                                      fb);
   count_launch();
 }
 

@@ -26,6 +26,10 @@ enum : uint32_t {
 // Sample-record flags
 // kSRay: rays[idx] valid; kSRecord: the sample carries an update_q record
 enum : uint32_t { kSNonzero = 1u, kSLearned = 2u, kSRay = 4u, kSRecord = 8u };
+// rflag bit set by k_shadow for an occluded segment (srec keeps the visible
+// contribution; its v is zeroed in vdense): a byte in a 2 MB array instead of
+// a read-modify-write of the 64-byte sample record
+constexpr uint8_t kROccluded = 0x80;
 
 // Device error bits (mapped to the reference's exceptions by the host).
 enum : uint32_t {
@@ -185,7 +189,7 @@ struct PassBuffers {
   uint32_t* emit;            // [vertex] emitter index (P.export_samples)
   SampleRec* srec;
   double* vdense;        // [vertex] srec's v, dense: the fold's gathers stay in L2
-  uint8_t* rflag;        // per vertex: the kSRay | kSRecord bits of srec (compaction input)
+  uint8_t* rflag;        // per vertex: the kSRay | kSRecord bits of srec (compaction input), kROccluded
   uint32_t* keys;
   uint32_t* vals;
   uint32_t* keys_alt;
