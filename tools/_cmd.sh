@@ -1,4 +1,2 @@
-bash tools/ab3.sh 3 > gpurun_out/ab38.txt 2>&1
-cat gpurun_out/ab38.txt
-python -m pytest tests -x -q -m gpu > gpurun_out/t_all.txt 2>&1
-tail -3 gpurun_out/t_all.txt
+bash tools/ab_env.sh 3 "" "RLC_PRIMARY_GATE=1" "RLC_PRIMARY_GATE=1 RLC_SHADOW_ROOM=2" > gpurun_out/ab40.txt 2>&1
+cat gpurun_out/ab40.txt
