@@ -1,2 +1,4 @@
-bash tools/ab_env.sh 3 "" "RLC_PRIMARY_GATE=1" "RLC_PRIMARY_GATE=1 RLC_SHADOW_ROOM=2" > gpurun_out/ab40.txt 2>&1
-cat gpurun_out/ab40.txt
+bash tools/ab.sh 3 > gpurun_out/ab43.txt 2>&1
+cat gpurun_out/ab43.txt
+python -m pytest tests -x -q -m gpu > gpurun_out/t_all.txt 2>&1
+tail -3 gpurun_out/t_all.txt
