@@ -153,15 +153,15 @@ struct alignas(128) LightRec {
 };
 
 // An emitter at its light-tree position (tree.order[pos], light_tree.hpp):
-// the learned sampler's pick reads one line instead of order[] then the
-// record.  Built on the device from LightRec and order (k_light_order).
-struct alignas(128) LightOrd {
+// the learned sampler's pick reads one record instead of order[] then the
+// LightRec.  Built on the device from LightRec and order (k_light_order).
+// 80 B, three 32-byte sectors per random pick: the normal and 1 / area are
+// recomputed from the vertices with the expressions that built LightRec
+// (rlc_build.cpp, emitter()), so they are the same doubles.
+struct alignas(16) LightOrd {
   double p0[3], p1[3], p2[3];
-  double n[3];
-  double pdf_area;
   uint32_t mat;      // material (emission)
   uint32_t emitter;  // emitter index (tree.order[pos])
-  double pad[2];
 };
 
 // Material flags precomputed with the reference predicates.

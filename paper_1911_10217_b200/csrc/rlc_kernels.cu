@@ -1151,17 +1151,15 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   V3 p0, p1, p2, nl, emission;
   double pdf_area;
   if (lpos != 0xffffffffu) {  // the pick's record at its tree position (order[] folded in)
-    // (the fields up to `emitter`, 112 B, in 128-bit loads)
-    struct alignas(16) Head {
-      double p[12];
-      double pdf_area;
-      uint32_t mat, emitter;
-    };
-    static_assert(sizeof(Head) == 112 && offsetof(LightOrd, emitter) == 108, "LightOrd layout");
-    const Head L = ldg_vec(reinterpret_cast<const Head*>(sc.lights_ord + lpos));
+    static_assert(sizeof(LightOrd) == 80, "LightOrd layout");
+    const LightOrd L = ldg_vec(sc.lights_ord + lpos);  // 5 128-bit loads
     e = L.emitter;
-    p0 = ld3(L.p), p1 = ld3(L.p + 3), p2 = ld3(L.p + 6), nl = ld3(L.p + 9);
-    pdf_area = L.pdf_area;
+    p0 = ld3(L.p0), p1 = ld3(L.p1), p2 = ld3(L.p2);
+    // triangle_normal and 1 / area exactly as LightRec holds them
+    const V3 cr = cross(p1 - p0, p2 - p0);
+    nl = normalize(cr);
+    const double area = 0.5 * length(cr);
+    pdf_area = area > 0 ? 1.0 / area : 0.0;
     emission = ld3(sc.mats[L.mat].emission);
   } else {
     RLC_CHECK(e < sc.num_lights, err);
@@ -3051,9 +3049,7 @@ __global__ void k_light_order(DevScene sc, LightOrd* __restrict__ out) {
     o.p0[a] = L.p0[a];
     o.p1[a] = L.p1[a];
     o.p2[a] = L.p2[a];
-    o.n[a] = L.n[a];
   }
-  o.pdf_area = L.pdf_area;
   o.mat = sc.emitter_mat[e];
   o.emitter = e;
   out[pos] = o;

@@ -1,4 +1,4 @@
-bash tools/ab.sh 3 > gpurun_out/ab43.txt 2>&1
-cat gpurun_out/ab43.txt
+bash tools/ab.sh 3 > gpurun_out/ab45.txt 2>&1
+cat gpurun_out/ab45.txt
 python -m pytest tests -x -q -m gpu > gpurun_out/t_all.txt 2>&1
 tail -3 gpurun_out/t_all.txt
