@@ -2032,9 +2032,16 @@ __global__ void __launch_bounds__(kRsThreads) rs_hist(const uint32_t* __restrict
   for (int d = threadIdx.x; d < 256; d += kRsThreads) h[d] = 0;
   __syncthreads();
   const uint32_t base = blockIdx.x * kRsThreads * ITEMS;
+  uint32_t kk[ITEMS];
+#pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const uint32_t j = base + i * kRsThreads + threadIdx.x;
-    if (j < n) atomicAdd(&h[(keys[j] >> shift) & 255u], 1u);
+    kk[i] = j < n ? __ldg(keys + j) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t j = base + i * kRsThreads + threadIdx.x;
+    if (j < n) atomicAdd(&h[(kk[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
   for (int d = threadIdx.x; d < 256; d += kRsThreads) hist[d * nt + blockIdx.x] = h[d];
@@ -2158,12 +2165,19 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
   const uint32_t base = blockIdx.x * (kRsThreads * ITEMS) + w * (32 * ITEMS);
   const unsigned lt_mask = (1u << lane) - 1u;
   uint32_t k[ITEMS], v[ITEMS], rank[ITEMS];
+  // all of the tile's loads in flight before the ranking (the warp-level
+  // ranking's __syncwarp would otherwise serialise one load latency per item)
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
     const uint32_t j = base + r * 32 + lane;
     const bool ok = j < n;
-    k[r] = ok ? kin[j] : 0u;
-    v[r] = ok ? vin[j] : 0u;
+    k[r] = ok ? __ldg(kin + j) : 0u;
+    v[r] = ok ? __ldg(vin + j) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const uint32_t j = base + r * 32 + lane;
+    const bool ok = j < n;
     const uint32_t d = ok ? (k[r] >> shift) & 255u : 256u + lane;
     const unsigned peers = __match_any_sync(kFull, d);
     const uint32_t before = ok ? wh[w][d] : 0u;
