@@ -396,6 +396,7 @@ struct rlc_context {
   // (side stream) reads them while pass p + 1 samples and folds
   rlc::SampleRec* srec_slot[2] = {nullptr, nullptr};
   uint8_t* rflag_slot[2] = {nullptr, nullptr};  // (the occluded bits k_accumulate reads)
+  uint32_t* gflags_slot[2] = {nullptr, nullptr};
   double* qb_slot[2] = {nullptr, nullptr};
   void sync_all() {
     RLC_CK(cudaStreamSynchronize(stream));
@@ -569,6 +570,9 @@ struct rlc_context {
     srec_slot[1] = scratch.alloc<rlc::SampleRec>(cap);
     pb.srec = srec_slot[0];
     pb.vdense = scratch.alloc<double>(cap);
+    gflags_slot[0] = scratch.alloc<uint32_t>(cap);
+    gflags_slot[1] = scratch.alloc<uint32_t>(cap);
+    pb.gflags = gflags_slot[0];
     rflag_slot[0] = scratch.alloc<uint8_t>(cap);
     rflag_slot[1] = scratch.alloc<uint8_t>(cap);
     pb.rflag = rflag_slot[0];
@@ -697,6 +701,7 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   ctx->pb.pkey = ctx->pkey_slot[slot];
   ctx->pb.srec = ctx->srec_slot[slot];
   ctx->pb.rflag = ctx->rflag_slot[slot];
+  ctx->pb.gflags = ctx->gflags_slot[slot];
   ctx->pb.q_before = ctx->qb_slot[slot];
   const bool rl = S.p.sampler == RLC_SAMPLER_RL_LIGHTCUTS;
   // The pass's new keys go in after all its lookups, in canonical order

@@ -1049,11 +1049,13 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
                                                 unsigned int* __restrict__ ray_count,
                                                 const unsigned long long* __restrict__ pkey,
                                                 uint32_t* __restrict__ emit,
-                                                double* __restrict__ vdense) {
+                                                double* __restrict__ vdense,
+                                                uint32_t* __restrict__ gflags) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // path vertex
   if (idx >= P.nv) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
   const GBuf gb = ldg_vec(gbuf + idx);
+  gflags[idx] = gb.flags;
   keys[idx] = kInvalidKey;
 #if !RLC_SORT_COMPACT
   vals[idx] = idx;  // the record sort's values (every vertex is sorted)
@@ -1224,7 +1226,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   }
   srec[idx] = r;
   vdense[idx] = r.v;
-  rflag[idx] = uint8_t(r.flags & (kSRay | kSRecord));
+  rflag[idx] = uint8_t(r.flags & (kSNonzero | kSLearned | kSRay | kSRecord));
 }
 
 // ---------------------------------------------------------------------------
@@ -2283,7 +2285,7 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
 // (image.hpp:56-60) in per-pixel sample order.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
-                                                    const GBuf* __restrict__ gbuf,
+                                                    const uint32_t* __restrict__ gflags,
                                                     const SampleRec* __restrict__ srec,
                                                     const uint8_t* __restrict__ rflag,
                                                     const double* __restrict__ q_before,
@@ -2304,14 +2306,15 @@ __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
     const size_t v0 = size_t(pix * P.spp_pp + s) * P.depth;
     for (uint32_t d = 0; d < P.depth; ++d) {
       const size_t idx = v0 + d;
-      const uint32_t flags = gbuf[idx].flags;
+      const uint32_t flags = gflags[idx];
       if (!(flags & kGHit)) break;
       const MatRec& m = sc.mats[flags & kGMatMask];
       if (flags & kGEmit) L = L + ld3(m.emission);
       if (!(flags & kGReflective)) break;
-      const SampleRec r = ldg_vec(srec + idx);
       V3 rad{0.0, 0.0, 0.0};
-      if ((r.flags & kSNonzero) && !(rflag[idx] & kROccluded)) {
+      const uint8_t rf = rflag[idx];  // the sample record only for a visible contribution
+      if ((rf & kSNonzero) && !(rf & kROccluded)) {
+        const SampleRec r = ldg_vec(srec + idx);
         double pdf_sel;
         if (r.flags & kSLearned) {
           const double p = q_before[idx] / r.total;
@@ -3133,7 +3136,7 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
   cudaMemsetAsync(b.ray_count, 0, 2 * sizeof(unsigned int), st);
   k_sample<<<blocks_for(p.nv, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.rflag, b.keys, b.vals,
                                                   b.q_before, b.rays, b.ray_count, b.pkey,
-                                                  b.emit, b.vdense);
+                                                  b.emit, b.vdense, b.gflags);
   count_launch();
 }
 
@@ -3320,8 +3323,8 @@ void launch_accumulate(const DevScene& sc, const PassParams& p, const PassBuffer
                        const Framebuf& fb, cudaStream_t st) {
   const uint32_t npix = p.spp_pp ? p.n / p.spp_pp : 0;
   if (npix == 0) return;
-  k_accumulate<<<blocks_for(npix, 256), 256, 0, st>>>(sc, p, b.gbuf, b.srec, b.rflag, b.q_before,
-                                                      fb);
+  k_accumulate<<<blocks_for(npix, 256), 256, 0, st>>>(sc, p, b.gflags, b.srec, b.rflag,
+                                                      b.q_before, fb);
   count_launch();
 }
 

@@ -189,7 +189,9 @@ struct PassBuffers {
   uint32_t* emit;            // [vertex] emitter index (P.export_samples)
   SampleRec* srec;
   double* vdense;        // [vertex] srec's v, dense: the fold's gathers stay in L2
-  uint8_t* rflag;        // per vertex: the kSRay | kSRecord bits of srec (compaction input), kROccluded
+  uint32_t* gflags;      // [vertex] the G-buffer flags, dense (k_accumulate; per slot)
+  uint8_t* rflag;        // per vertex: srec's kSNonzero | kSLearned | kSRay | kSRecord bits (compaction
+                         // input), kROccluded; per slot
   uint32_t* keys;
   uint32_t* vals;
   uint32_t* keys_alt;

@@ -1,2 +1,4 @@
-python tools/shard_budget.py 8 8 c3 both > gpurun_out/sb_new.txt 2>&1
-cd ab/prev && python tools/shard_budget.py 8 8 c3 both > ../../gpurun_out/sb_old.txt 2>&1
+bash tools/ab3.sh 3 > gpurun_out/ab47.txt 2>&1
+cat gpurun_out/ab47.txt
+python -m pytest tests -x -q -m gpu > gpurun_out/t_all.txt 2>&1
+tail -3 gpurun_out/t_all.txt
