@@ -1057,9 +1057,6 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   const GBuf gb = ldg_vec(gbuf + idx);
   gflags[idx] = gb.flags;
   keys[idx] = kInvalidKey;
-#if !RLC_SORT_COMPACT
-  vals[idx] = idx;  // the record sort's values (every vertex is sorted)
-#endif
   if (!(gb.flags & kGReflective)) {
     srec[idx].flags = 0;
     rflag[idx] = 0;  // read by the compactions
@@ -2174,7 +2171,7 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
     const uint32_t j = base + r * 32 + lane;
     const bool ok = j < n;
     k[r] = ok ? __ldg(kin + j) : 0u;
-    v[r] = ok ? __ldg(vin + j) : 0u;
+    v[r] = ok ? (vin ? __ldg(vin + j) : j) : 0u;  // vin null: the identity (vertex ids)
   }
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
@@ -3265,13 +3262,14 @@ void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* ord
 template <int ITEMS>
 static void sort_passes(uint32_t*& ka, uint32_t*& va, uint32_t*& kb, uint32_t*& vb,
                         uint32_t* hist, uint32_t n, uint32_t key_bits, cudaStream_t st,
-                        const unsigned* n_dev) {
+                        const unsigned* n_dev, bool identity_vals) {
   const uint32_t nb = blocks_for(n, kRsThreads * ITEMS);
   for (uint32_t shift = 0; shift < key_bits; shift += 8) {
     rs_hist<ITEMS><<<nb, kRsThreads, 0, st>>>(ka, n, n_dev, int(shift), hist);
     uint32_t* totals = hist + size_t(nb) * 256u;
     rs_scan_rows<ITEMS><<<256, 256, 0, st>>>(hist, nb, n, n_dev, totals);
-    rs_scatter<ITEMS><<<nb, kRsThreads, 0, st>>>(ka, va, kb, vb, n, n_dev, int(shift), hist, totals);
+    const uint32_t* vin = identity_vals && shift == 0 ? nullptr : va;
+    rs_scatter<ITEMS><<<nb, kRsThreads, 0, st>>>(ka, vin, kb, vb, n, n_dev, int(shift), hist, totals);
     count_launch(3);
     std::swap(ka, kb);
     std::swap(va, vb);
@@ -3280,12 +3278,14 @@ static void sort_passes(uint32_t*& ka, uint32_t*& va, uint32_t*& kb, uint32_t*& 
 
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
-                         uint32_t** vals_out, const unsigned* n_dev, bool small_tiles) {
+                         uint32_t** vals_out, const unsigned* n_dev, bool small_tiles,
+                         bool identity_vals) {
   if (n > 1) {
     if (small_tiles)
-      sort_passes<int(kSortTileSmall) / kRsThreads>(ka, va, kb, vb, hist, n, key_bits, st, n_dev);
+      sort_passes<int(kSortTileSmall) / kRsThreads>(ka, va, kb, vb, hist, n, key_bits, st, n_dev,
+                                                     identity_vals);
     else
-      sort_passes<kRsItems>(ka, va, kb, vb, hist, n, key_bits, st, n_dev);
+      sort_passes<kRsItems>(ka, va, kb, vb, hist, n, key_bits, st, n_dev, identity_vals);
   }
   *keys_out = ka;
   *vals_out = va;
@@ -3302,9 +3302,9 @@ void launch_sort(PassBuffers& b, uint32_t n, uint32_t key_bits, cudaStream_t st,
                  b.keys_alt);
   launch_sort_buffers(b.keys_alt, b.vals_alt, b.keys, b.vals, b.sort_hist, n, key_bits, st,
                       keys_out, vals_out, b.sort_count);
-#else  // every vertex (invalid keys sort last; k_sample wrote vals = vertex)
+#else  // every vertex (invalid keys sort last; the values start as the vertex ids)
   launch_sort_buffers(b.keys, b.vals, b.keys_alt, b.vals_alt, b.sort_hist, n, key_bits, st,
-                      keys_out, vals_out, nullptr);
+                      keys_out, vals_out, nullptr, false, true);
 #endif
 }
 

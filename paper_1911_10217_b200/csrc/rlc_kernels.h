@@ -300,10 +300,12 @@ constexpr uint32_t kSortTile = RLC_SORT_TILE;
 constexpr uint32_t kSortTileSmall = 1024;
 // n_dev (may be null): a device-side count <= n of the valid entries; the
 // digit passes then cover ceil(*n_dev / tile) tiles only.  small_tiles:
-// kSortTileSmall keys per block instead of kSortTile.
+// kSortTileSmall keys per block instead of kSortTile.  identity_vals: va is
+// not read, the values start as 0 .. n - 1.
 void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, uint32_t* hist,
                          uint32_t n, uint32_t key_bits, cudaStream_t st, uint32_t** keys_out,
-                         uint32_t** vals_out, const unsigned* n_dev, bool small_tiles = false);
+                         uint32_t** vals_out, const unsigned* n_dev, bool small_tiles = false,
+                         bool identity_vals = false);
 // Sharded passes.  The rank's update records of the
 // traced band, in canonical order, into `block` (header slot + cap slots).
 void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, void* block,
