@@ -1,3 +1,3 @@
-bash tools/ab3.sh 3 > gpurun_out/ab48.txt 2>&1
-cat gpurun_out/ab48.txt
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_samples.py -x -q > gpurun_out/t_p.txt 2>&1; tail -2 gpurun_out/t_p.txt
+python tools/shard_budget.py 8 4 c5 both > gpurun_out/sb_c5.txt 2>&1
+cat gpurun_out/sb_c5.txt | tail -30
+python bench.py --config c5 --steps 16 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/c5_bench.json 2>&1; tail -c 600 gpurun_out/c5_bench.json
