@@ -9,7 +9,7 @@ except Exception as e: print(sys.argv[2], 'no result', e)" $1 "$2"; }
 for r in $(seq $reps); do
   i=0
   for setting in "$@"; do
-    env $setting python bench.py --no-cpu-baseline --no-e2e > gpurun_out/abenv_$i.json 2>&1
+    env $setting python bench.py --no-cpu-baseline --no-e2e $BENCH_ARGS > gpurun_out/abenv_$i.json 2>&1
     summ gpurun_out/abenv_$i.json "[$setting]"
     i=$((i+1))
   done
