@@ -1031,6 +1031,9 @@ __device__ __forceinline__ uint32_t upper_bound_cdf(const double* __restrict__ c
   return lo == M ? M - 1 : lo;
 }
 
+// stable compaction tiles (k_cmp_*): 256 threads x 8 vertices
+constexpr int kCmpThreads = 256, kCmpItems = 8, kCmpTile = kCmpThreads * kCmpItems;
+
 #ifndef RLC_SAMPLE_BLOCKS
 #define RLC_SAMPLE_BLOCKS 7  // 72 registers, 7 blocks per SM: c3 0.880 vs 0.886 ms at 84 (6 blocks)
 #endif
@@ -1050,7 +1053,8 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
                                                 const unsigned long long* __restrict__ pkey,
                                                 uint32_t* __restrict__ emit,
                                                 double* __restrict__ vdense,
-                                                uint32_t* __restrict__ gflags) {
+                                                uint32_t* __restrict__ gflags,
+                                                uint32_t* __restrict__ ray_tile_counts) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // path vertex
   if (idx >= P.nv) return;
   uint32_t* err = reinterpret_cast<uint32_t*>(g.counters + kCntErr);
@@ -1224,6 +1228,12 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   srec[idx] = r;
   vdense[idx] = r.v;
   rflag[idx] = uint8_t(r.flags & (kSNonzero | kSLearned | kSRay | kSRecord));
+  // the ray compaction's per-tile counts (k_cmp_count's work): one atomic per
+  // group of converged lanes; a warp's 32 vertices lie in one tile
+  const unsigned am = __activemask();
+  const unsigned rm = __ballot_sync(am, (r.flags & kSRay) != 0);
+  if ((threadIdx.x & 31u) == uint32_t(__ffs(am) - 1) && rm)
+    atomicAdd(ray_tile_counts + idx / kCmpTile, uint32_t(__popc(rm)));
 }
 
 // ---------------------------------------------------------------------------
@@ -3131,14 +3141,14 @@ void launch_sample(const DevScene& sc, const DevGrid& g, const PassParams& p,
                    const PassBuffers& b, cudaStream_t st) {
   if (p.nv == 0) return;
   cudaMemsetAsync(b.ray_count, 0, 2 * sizeof(unsigned int), st);
+  cudaMemsetAsync(b.block_counts, 0, sizeof(uint32_t) * blocks_for(p.nv, kCmpTile), st);
   k_sample<<<blocks_for(p.nv, 128), 128, 0, st>>>(sc, g, p, b.gbuf, b.srec, b.rflag, b.keys, b.vals,
                                                   b.q_before, b.rays, b.ray_count, b.pkey,
-                                                  b.emit, b.vdense, b.gflags);
+                                                  b.emit, b.vdense, b.gflags, b.block_counts);
   count_launch();
 }
 
 // ---- stable compaction of ray-bearing paths -------------------------------
-constexpr int kCmpThreads = 256, kCmpItems = 8, kCmpTile = kCmpThreads * kCmpItems;
 
 __device__ __forceinline__ bool has_flag(const uint8_t* rflag, const uint32_t* order, uint32_t j,
                                          uint32_t mask) {
@@ -3225,8 +3235,17 @@ static void launch_compact(const PassBuffers& b, const uint32_t* order, uint32_t
   count_launch(3);
 }
 
+// k_sample counted the rays of every tile (b.block_counts): scan and scatter
 void launch_ray_compact(const PassBuffers& b, const uint32_t* order, uint32_t n, cudaStream_t st) {
-  launch_compact(b, order, n, kSRay, b.ray_order, b.ray_count, st);
+  if (order) {
+    launch_compact(b, order, n, kSRay, b.ray_order, b.ray_count, st);
+    return;
+  }
+  const uint32_t nb = blocks_for(n > 0 ? n : 1, kCmpTile);
+  rs_scan<<<1, kScanThreads, 0, st>>>(b.block_counts, nb);
+  k_cmp_scatter<<<nb, kCmpThreads, 0, st>>>(b.rflag, nullptr, n, kSRay, b.block_counts, b.ray_order,
+                                            b.ray_count, nullptr, nullptr);
+  count_launch(2);
 }
 
 void launch_shadow(const DevScene& sc, const PassBuffers& b, const uint32_t* order,

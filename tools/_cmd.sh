@@ -1,2 +1,4 @@
-RLC_LIB_PATH=$PWD/ab/lib_checked.so python -m pytest tests -m gpu -q > gpurun_out/t_checked.txt 2>&1
-tail -3 gpurun_out/t_checked.txt
+bash tools/ab3.sh 3 > gpurun_out/ab54.txt 2>&1
+cat gpurun_out/ab54.txt
+python -m pytest tests -x -q -m gpu > gpurun_out/t_all.txt 2>&1
+tail -3 gpurun_out/t_all.txt
