@@ -368,6 +368,15 @@ rlc_status rlc_shard_trace(const rlc_context* ctx, const rlc_render_config* conf
 rlc_status rlc_shard_fold(const rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
                           const void* blocks, uint32_t nranks, uint32_t rank, int owner_fold,
                           double** q_before_slots, uint32_t** seg_counts, uint64_t* slots);
+/* Owner mode's entry exchange, chosen by rlc_shard_fold when the records far
+ * outnumber the cut entries (3 * capacity * M < 2 * slots; RLC_SHARD_ENTRY=0/1
+ * forces it): *seg_counts is then null, and the caller instead sums these
+ * per-entry arrays over the ranks -- each entry's final q and record count
+ * from its owner, zero elsewhere -- while each rank needs only its own band's
+ * block of q_before_slots summed (ncclReduceScatter).  Null / 0 in the
+ * per-slot mode. */
+rlc_status rlc_shard_entry_arrays(const rlc_context* ctx, double** entry_q,
+                                  uint32_t** entry_counts, uint64_t* entries);
 rlc_status rlc_shard_finish(const rlc_context* ctx, rlc_grid* grid, rlc_framebuffer* fb,
                             uint32_t rank, int owner_fold);
 /* Waits for the context's work and reports device errors of the grid. */

@@ -503,6 +503,18 @@ struct rlc_context {
     xb.nk = alloc_new_keys(xarena, n, stream);
     xb_slots = n;
   }
+  // per-entry arrays of the owner-mode entry exchange (capacity * M entries)
+  DeviceArena entarena;
+  uint64_t ent_cap = 0;
+  void ensure_entries(uint64_t entries) {
+    xb.entries = entries;
+    if (entries <= ent_cap) return;
+    sync_all();
+    entarena.release();
+    xb.ent_q = entarena.alloc<double>(entries);
+    xb.ent_n = entarena.alloc<uint32_t>(entries);
+    ent_cap = entries;
+  }
   // render_frame cache (prepare_frame_cache)
   rlc_grid* frame_grid = nullptr;
   rlc_framebuffer* frame_fb = nullptr;
@@ -1619,6 +1631,19 @@ void shard_fold(rlc_context* ctx, const rlc_render_config* config, rlc_grid* gri
   const PassParamsHolder& S = ctx->shard;
   ctx->ensure_exchange(nranks, uint32_t(ctx->block_cap));
   ctx->xb.rec = static_cast<const rlc::ExchangeRecord*>(blocks);
+  // Owner mode exchanges either per-slot values (q_before and the entry's
+  // record count at its last record: 12 B per slot, all-reduced) or, when
+  // the records far outnumber the cut entries (c5), per-entry final values
+  // (12 B per entry, all-reduced) plus q_before reduce-scattered to each
+  // band: the one with fewer bytes per rank.  RLC_SHARD_ENTRY=0/1 forces it.
+  {
+    const uint64_t S = uint64_t(nranks) * ctx->xb.stride;
+    const uint64_t E = uint64_t(grid->dev.capacity) * grid->dev.M;
+    bool entry = owner_fold != 0 && nranks > 1 && 3 * E < 2 * S;
+    if (const char* e = std::getenv("RLC_SHARD_ENTRY")) entry = owner_fold != 0 && std::atoi(e) != 0;
+    ctx->xb.entry_mode = entry ? 1u : 0u;
+    if (entry) ctx->ensure_entries(E);
+  }
   ctx->stage(9, [&] {
     rlc::launch_shard_fold(S.g, S.p, rank, owner_fold != 0, ctx->xb, ctx->stream);
   });
@@ -1645,7 +1670,7 @@ void shard_finish(rlc_context* ctx, rlc_grid* grid, rlc_framebuffer* fb, uint32_
   const PassParamsHolder S = ctx->shard;
   ctx->shard.valid = false;
   cudaStream_t st = ctx->stream;
-  if (owner_fold) ctx->stage(3, [&] { rlc::launch_shard_apply(S.g, S.p, ctx->xb, st); });
+  if (owner_fold) ctx->stage(3, [&] { rlc::launch_shard_apply(S.g, S.p, rank, ctx->xb, st); });
   rlc::launch_shard_scatter(S.g, ctx->pb, S.nv, rank, ctx->xb, st);
   if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
   RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));
@@ -1677,8 +1702,19 @@ rlc_status rlc_shard_fold(const rlc_context* cctx, const rlc_render_config* conf
     rlc_context* ctx = const_cast<rlc_context*>(cctx);
     shard_fold(ctx, config, grid, blocks, nranks, rank, owner_fold);
     if (q_before_slots) *q_before_slots = ctx->xb.q_rec;
-    if (seg_counts) *seg_counts = ctx->xb.seg_n;
+    if (seg_counts) *seg_counts = ctx->xb.entry_mode ? nullptr : ctx->xb.seg_n;
     if (slots) *slots = uint64_t(nranks) * ctx->xb.stride;
+  });
+}
+
+rlc_status rlc_shard_entry_arrays(const rlc_context* cctx, double** entry_q,
+                                  uint32_t** entry_counts, uint64_t* entries) {
+  return guarded([&] {
+    require(cctx != nullptr, "rlc_shard_entry_arrays: null context");
+    const bool on = cctx->xb.entry_mode != 0;
+    if (entry_q) *entry_q = on ? cctx->xb.ent_q : nullptr;
+    if (entry_counts) *entry_counts = on ? cctx->xb.ent_n : nullptr;
+    if (entries) *entries = on ? cctx->xb.entries : 0;
   });
 }
 
@@ -1708,6 +1744,8 @@ struct NcclApi {
                              cudaStream_t) = nullptr;
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
+  ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                 ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*destroy)(ncclComm_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
 };
@@ -1722,6 +1760,8 @@ const NcclApi& nccl() {
     a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
     a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
     a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.reduce_scatter =
+        reinterpret_cast<decltype(a.reduce_scatter)>(dlsym(h, "ncclReduceScatter"));
     a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
     a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
     return a;
@@ -1800,7 +1840,21 @@ void shard_frame_body(rlc_context* ctx, const rlc_render_config* config, uint32_
   nccl_check(nccl().all_gather(ctx->block, comm->gathered, bb, ncclUint8, comm->comm, st),
              "ncclAllGather");
   shard_fold(ctx, config, grid, comm->gathered, comm->nranks, comm->rank, owner_fold);
-  if (owner_fold && comm->nranks > 1) {  // q_before and entry counts from the cells' owners
+  if (owner_fold && comm->nranks > 1 && ctx->xb.entry_mode) {
+    // each band's q_before from the owners (reduce-scatter, in place: this
+    // rank's block of slots), every entry's final q and count (all-reduce)
+    const size_t stride = ctx->xb.stride;
+    require(nccl().reduce_scatter != nullptr, "rlc_shard_frame: libnccl lacks ncclReduceScatter");
+    nccl_check(nccl().reduce_scatter(ctx->xb.q_rec, ctx->xb.q_rec + size_t(comm->rank) * stride,
+                                     stride, ncclFloat64, ncclSum, comm->comm, st),
+               "ncclReduceScatter");
+    nccl_check(nccl().all_reduce(ctx->xb.ent_q, ctx->xb.ent_q, ctx->xb.entries, ncclFloat64,
+                                 ncclSum, comm->comm, st),
+               "ncclAllReduce");
+    nccl_check(nccl().all_reduce(ctx->xb.ent_n, ctx->xb.ent_n, ctx->xb.entries, ncclUint32,
+                                 ncclSum, comm->comm, st),
+               "ncclAllReduce");
+  } else if (owner_fold && comm->nranks > 1) {  // q_before and entry counts from the cells' owners
     const size_t slots = size_t(comm->nranks) * ctx->xb.stride;
     nccl_check(nccl().all_reduce(ctx->xb.q_rec, ctx->xb.q_rec, slots, ncclFloat64, ncclSum,
                                  comm->comm, st),

@@ -2224,14 +2224,20 @@ __global__ void __launch_bounds__(kRsThreads, RLC_RS_MINB) rs_scatter(const uint
 // v of record `idx` is at vbase + idx * vstride (sample records or exchanged
 // update records); q_before is written per record index, and with seg_n the
 // segment's record count at its last record index.
-template <bool SEG>
+// SEG: 0 the single-GPU fold; 1 (owner mode, per-slot exchange) the
+// segment's record count at its last record's index into seg_n; 2 (owner
+// mode, per-entry exchange) the entry's final q and record count into
+// ent_q / ent_n.
+template <int SEG>
 __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
                                               const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ vals,
                                               const char* __restrict__ vbase, uint32_t vstride,
                                               double* __restrict__ q_before,
                                               const unsigned* __restrict__ n_dev,
-                                              uint32_t* __restrict__ seg_n) {
+                                              uint32_t* __restrict__ seg_n,
+                                              double* __restrict__ ent_q = nullptr,
+                                              uint32_t* __restrict__ ent_n = nullptr) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (n_dev) P.n = min(P.n, *n_dev);
   if (i >= P.n) return;
@@ -2275,12 +2281,17 @@ __global__ void __launch_bounds__(256) k_fold(DevGrid g, PassParams P,
       const double a = P.harmonic ? 1.0 / (1.0 + double(vis)) : P.alpha;
       q = smax((1.0 - a) * q + a * v, g.eps_q);
       ++vis;
-      if constexpr (SEG) last = ids[b];
+      if constexpr (SEG == 1) last = ids[b];
     }
     j += uint32_t(cnt);
     if (cnt < kBatch) break;
   }
-  if constexpr (SEG) seg_n[last] = j - i;
+  if constexpr (SEG == 1) seg_n[last] = j - i;
+  if constexpr (SEG == 2) {  // indexed by table slot: dense cell ids differ between ranks
+    const size_t ent = size_t(g.cell_slot[cell]) * g.M + (k - cell * g.M);
+    ent_q[ent] = q;
+    ent_n[ent] = j - i;
+  }
   g.q[at] = q;
   g.visits[at] = vis;
   g.touched[cell] = 1u;
@@ -2749,7 +2760,12 @@ void launch_shard_fold(const DevGrid& g, const PassParams& fold_params, uint32_t
   cudaMemsetAsync(x.nk.count, 0, sizeof(unsigned int), st);
   cudaMemsetAsync(x.pend_count, 0, sizeof(unsigned int), st);
   cudaMemsetAsync(x.q_rec, 0, sizeof(double) * total, st);
-  if (owner_fold) cudaMemsetAsync(x.seg_n, 0, sizeof(uint32_t) * total, st);
+  if (owner_fold && x.entry_mode) {
+    cudaMemsetAsync(x.ent_q, 0, sizeof(double) * x.entries, st);
+    cudaMemsetAsync(x.ent_n, 0, sizeof(uint32_t) * x.entries, st);
+  } else if (owner_fold) {
+    cudaMemsetAsync(x.seg_n, 0, sizeof(uint32_t) * total, st);
+  }
   k_classify<<<blocks_for(total, 256), 256, 0, st>>>(g, rank, owner_fold ? 1u : 0u, x);
   count_launch();
   launch_insert_new_keys(g, x.nk, st);
@@ -2773,12 +2789,15 @@ void launch_shard_sortfold(const DevGrid& g, const PassParams& fold_params, uint
   p.n = total;
   const char* vb = reinterpret_cast<const char*>(x.rec) + offsetof(ExchangeRecord, v);
   const uint32_t vs = uint32_t(sizeof(ExchangeRecord));
-  if (owner_fold)
-    k_fold<true><<<blocks_for(total, 256), 256, 0, st>>>(g, p, k, v, vb, vs, x.q_rec, x.sort_count,
-                                                         x.seg_n);
+  if (owner_fold && x.entry_mode)
+    k_fold<2><<<blocks_for(total, 256), 256, 0, st>>>(g, p, k, v, vb, vs, x.q_rec, x.sort_count,
+                                                      nullptr, x.ent_q, x.ent_n);
+  else if (owner_fold)
+    k_fold<1><<<blocks_for(total, 256), 256, 0, st>>>(g, p, k, v, vb, vs, x.q_rec, x.sort_count,
+                                                      x.seg_n);
   else
-    k_fold<false><<<blocks_for(total, 256), 256, 0, st>>>(g, p, k, v, vb, vs, x.q_rec,
-                                                          x.sort_count, nullptr);
+    k_fold<0><<<blocks_for(total, 256), 256, 0, st>>>(g, p, k, v, vb, vs, x.q_rec, x.sort_count,
+                                                      nullptr);
   count_launch();
 }
 
@@ -2802,11 +2821,33 @@ __global__ void k_apply(DevGrid g, PassParams P, ExchangeBuffers x) {
   g.visits[e] = vis_before + 1u;
 }
 
-void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, ExchangeBuffers& x,
-                        cudaStream_t st) {
+// Owner mode, per-entry exchange: the cut entries other ranks folded take
+// the owner's final q (summed over the ranks: one non-zero term) and advance
+// their visits by its record count.  Entries are indexed slot * M + cluster:
+// table slots are the same on every rank, dense cell ids need not be.
+__global__ void k_apply_entries(DevGrid g, uint32_t rank, ExchangeBuffers x) {
+  const size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // slot * M + cluster
+  if (e >= x.entries) return;
+  const uint32_t c = x.ent_n[e];
+  if (c == 0) return;
+  const uint32_t slot = uint32_t(e / g.M);
+  if (slot % x.nranks == rank) return;  // this rank folded it
+  const uint32_t cell = g.slot_cell[slot];
+  const size_t at = size_t(cell) * g.M + (e - size_t(slot) * g.M);
+  g.q[at] = x.ent_q[e];
+  g.visits[at] += c;
+  g.touched[cell] = 1u;
+}
+
+void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, uint32_t rank,
+                        ExchangeBuffers& x, cudaStream_t st) {
   const uint32_t total = x.nranks * x.stride;
   if (total == 0) return;
-  k_apply<<<blocks_for(total, 256), 256, 0, st>>>(g, fold_params, x);
+  if (x.entry_mode) {
+    k_apply_entries<<<uint32_t((x.entries + 255) / 256), 256, 0, st>>>(g, rank, x);
+  } else {
+    k_apply<<<blocks_for(total, 256), 256, 0, st>>>(g, fold_params, x);
+  }
   count_launch();
 }
 
@@ -3104,7 +3145,7 @@ static void set_carveouts() {
   const int pct = e ? std::atoi(e) : 0, pct_shadow = e2 ? std::atoi(e2) : 25;
   if (pct >= 0)
     for (const void* f : {reinterpret_cast<const void*>(k_primary), reinterpret_cast<const void*>(k_sample),
-                          reinterpret_cast<const void*>(k_bounce), reinterpret_cast<const void*>(k_fold<false>),
+                          reinterpret_cast<const void*>(k_bounce), reinterpret_cast<const void*>(k_fold<0>),
                           reinterpret_cast<const void*>(k_accumulate)})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   if (pct_shadow >= 0)
@@ -3332,7 +3373,7 @@ void launch_fold(const DevGrid& g, const PassParams& p, const uint32_t* keys,
   if (p.nv == 0) return;
   PassParams q = p;
   q.n = p.nv;  // k_fold runs over the update records of all path vertices
-  k_fold<false><<<blocks_for(q.n, 256), 256, 0, st>>>(
+  k_fold<0><<<blocks_for(q.n, 256), 256, 0, st>>>(
       g, q, keys, vals, reinterpret_cast<const char*>(b.vdense), uint32_t(sizeof(double)),
       b.q_before, RLC_SORT_COMPACT ? b.sort_count : nullptr, nullptr);
   count_launch();

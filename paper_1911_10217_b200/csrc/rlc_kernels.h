@@ -234,6 +234,10 @@ struct ExchangeBuffers {
   unsigned int* sort_count;
   double* q_rec;         // [t] q_before of record t (the all-reduced array in owner mode)
   uint32_t* seg_n;       // [t] records of the cut entry at its last record t, else 0 (owner mode)
+  double* ent_q;         // [slot * M + cluster] the owner's final q (owner mode, entry exchange)
+  uint32_t* ent_n;       // [slot * M + cluster] its record count (zero: not folded this pass)
+  uint64_t entries;      // capacity * M
+  uint32_t entry_mode;   // owner mode exchanges per-entry finals instead of per-slot counts
   uint32_t* pend;        // slots of the records whose key was new at trace time
   unsigned int* pend_count;
   NewKeys nk;
@@ -325,8 +329,10 @@ void launch_shard_sortfold(const DevGrid& g, const PassParams& fold_params, uint
 // Owner mode, after x.q_rec and x.seg_n were summed over the ranks: the cut
 // entries other ranks folded, advanced to the state their last record leaves
 // (q from its q_before and v, visits by the record count), touched flags.
-void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, ExchangeBuffers& x,
-                        cudaStream_t st);
+// Entry exchange (x.entry_mode): the entries other ranks folded take the
+// summed final q and record counts of x.ent_q / x.ent_n instead.
+void launch_shard_apply(const DevGrid& g, const PassParams& fold_params, uint32_t rank,
+                        ExchangeBuffers& x, cudaStream_t st);
 // q_before of this rank's own records (fallback: the template's) for the
 // accumulation of its band.
 void launch_shard_scatter(const DevGrid& g, const PassBuffers& b, uint32_t n, uint32_t rank,

@@ -69,13 +69,21 @@ class GpuEngine:
         return torch.as_tensor(_CudaView(ptr, nbytes), device=self.device)
 
     def fold(self, gathered: torch.Tensor, nranks: int, rank: int, owner: bool):
-        """-> (q_before per exchange slot, records per cut entry at its last
-        slot): the two arrays owner mode sums over the ranks.  `gathered`
+        """-> the arrays owner mode sums over the ranks: q_before per exchange
+        slot, then either the records per cut entry at its last slot or (the
+        entry exchange) each entry's final q and record count.  `gathered`
         must stay alive until finish()."""
         ptr, seg, n = rlcuts.shard_fold(self.ctx, self.cfg, self.grid, gathered.data_ptr(), nranks,
                                         rank, owner)
-        return (torch.as_tensor(_CudaView(ptr, 8 * n, "<f8"), device=self.device),
-                torch.as_tensor(_CudaView(seg, 4 * n, "<i4"), device=self.device))
+        out = [torch.as_tensor(_CudaView(ptr, 8 * n, "<f8"), device=self.device)]
+        if seg:
+            out.append(torch.as_tensor(_CudaView(seg, 4 * n, "<i4"), device=self.device))
+        else:
+            eq, en, m = rlcuts.shard_entry_arrays(self.ctx)
+            if m:
+                out.append(torch.as_tensor(_CudaView(eq, 8 * m, "<f8"), device=self.device))
+                out.append(torch.as_tensor(_CudaView(en, 4 * m, "<i4"), device=self.device))
+        return out
 
     def finish(self, rank: int, owner: bool):
         rlcuts.shard_finish(self.ctx, self.grid, self.fb, rank, owner)
@@ -178,7 +186,7 @@ def local_exchange(engines, heights_rows, pass_index: int, owner: bool = True,
     for e in engines:
         e.ctx.synchronize()
     if owner and n > 1:
-        for k in range(2):  # q_before, entry counts
+        for k in range(len(arrays[0])):  # q_before, then the counts (or entry finals)
             total = torch.stack([a[k].clone() for a in arrays]).sum(0)
             for a in arrays:
                 a[k].copy_(total.to(a[k].dtype))

@@ -508,6 +508,16 @@ def shard_fold(ctx: RenderContext, config: RenderConfig, grid: HashGrid, blocks_
     return int(ptr.value or 0), int(seg.value or 0), int(n.value)
 
 
+def shard_entry_arrays(ctx: RenderContext) -> tuple[int, int, int]:
+    """rlc_shard_entry_arrays: (final-q doubles, count uint32s, entries) of
+    owner mode's entry exchange after shard_fold; (0, 0, 0) in per-slot mode."""
+    q = C.c_void_p()
+    n = C.c_void_p()
+    cnt = C.c_uint64()
+    _check(_lib.load().rlc_shard_entry_arrays(ctx.handle, C.byref(q), C.byref(n), C.byref(cnt)))
+    return int(q.value or 0), int(n.value or 0), int(cnt.value)
+
+
 def shard_finish(ctx: RenderContext, grid: HashGrid, framebuffer: Framebuffer, rank: int,
                  owner_fold: bool):
     _check(_lib.load().rlc_shard_finish(ctx.handle, grid.handle, framebuffer.handle, rank,

@@ -48,10 +48,50 @@ def test_sharded_gpu_matches_single(ref, world, depth, owner):
     assert lookups == rr.stats()["lookups"]
 
 
-def test_sharded_c3_eight_ranks_owner(ref):
+@pytest.mark.parametrize("world,capacity", [(2, 1 << 16), (3, 1 << 16), (3, 200)])
+def test_sharded_entry_exchange(ref, monkeypatch, world, capacity):
+    """Owner mode's entry exchange (each entry's final q and record count
+    summed over the ranks, q_before per band) -- chosen for passes whose
+    records far outnumber the cut entries, forced here -- equals the
+    reference, also with an overflowing table."""
+    monkeypatch.setenv("RLC_SHARD_ENTRY", "1")
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+                              hash=rlcuts.HashConfig(capacity=capacity, probe_limit=16),
+                              cut=rlcuts.CutConfig(cut_size=32, split_threshold=2.0))
+    dev = torch.device("cuda", 0)
+    engines = []
+    for r in range(world):
+        ctx = rlcuts.build_context(scene, cfg)
+        engines.append(rdist.GpuEngine(ctx, rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx),
+                                       cfg, dev))
+    rows = [rdist.band(scene.camera.height, r, world) for r in range(world)]
+    rr = ref.RefRun(scene, cfg)
+    for p in range(cfg.passes):
+        changes = rdist.local_exchange(engines, rows, p, owner=True)
+        assert rlcuts.shard_entry_arrays(engines[0].ctx)[2] == capacity * 32
+        rch, _ = rr.run_pass(p)
+        assert changes == [rch] * world
+    rs, rc = rr.framebuffer()
+    rcells = rr.export()
+    for e, (r0, r1) in zip(engines, rows):
+        s, c = e.fb.download()
+        assert np.array_equal(s[r0:r1], rs[r0:r1]) and np.array_equal(c[r0:r1], rc[r0:r1])
+        cells = e.grid.export()
+        assert cells.keys() == rcells.keys()
+        for k, v in rcells.items():
+            for f in v:
+                assert np.array_equal(cells[k][f], v[f])
+        assert [(s_, k) for s_, _, k, _ in e.grid.slots()] == rr.slots()
+
+
+@pytest.mark.parametrize("entry", ["0", "1"])
+def test_sharded_c3_eight_ranks_owner(ref, monkeypatch, entry):
     """The headline scene (1M emitters) at 320 x 180 over 8 emulated ranks,
-    owner-partitioned: 6 frames of bands, exchange, insertion and fold equal
-    the reference's single-process frames."""
+    owner-partitioned, per-slot and per-entry exchange: 6 frames of bands,
+    exchange, insertion and fold equal the reference's single-process
+    frames."""
+    monkeypatch.setenv("RLC_SHARD_ENTRY", entry)
     scene, st = scenes.config_scene("c3")
     scene = scene.with_resolution(320, 180)
     cfg = rlcuts.RenderConfig(spp=6, passes=6, sampler=RL,

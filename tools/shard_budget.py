@@ -55,10 +55,21 @@ for owner in modes:
         print(f"{r:4d} " + " ".join(f"{d.get(k, 0.0):14.4f}" for k in keys))
     e0 = engines[0]
     block = 32 * (e0.cap + 1)
+    slots = N * (e0.cap + 1)
+    entries = rlcuts.shard_entry_arrays(e0.ctx)[2]
+    if not owner:
+        comm = ""
+    elif entries:  # entry exchange: q_before reduce-scattered, per-entry finals all-reduced
+        rs, ar = (N - 1) / N * slots * 8, 2 * (N - 1) / N * entries * 12
+        comm = (f" entry exchange: q_before reduce-scatter {slots * 8 / 1e6:.1f} MB (~{rs / 725e9 * 1e6:.0f} us)"
+                f" + per-entry all-reduce {entries * 12 / 1e6:.1f} MB (~{ar / 725e9 * 1e6:.0f} us)")
+    else:
+        ar = 2 * (N - 1) / N * slots * 12
+        comm = (f" q_before + entry-count all-reduce {slots * 12 / 1e6:.1f} MB "
+                f"(~{ar / 725e9 * 1e6:.0f} us)")
     print(f"record block {block / 1e6:.2f} MB per rank; all-gather receives "
           f"{(N - 1) * block / 1e6:.1f} MB per rank (~{(N - 1) * block / 725e9 * 1e6:.0f} us at 725 GB/s);"
-          + (f" q_before + entry-count all-reduce {N * (e0.cap + 1) * 12 / 1e6:.1f} MB "
-             f"(~{2 * (N - 1) / N * N * (e0.cap + 1) * 12 / 725e9 * 1e6:.0f} us)" if owner else ""))
+          + comm)
     print(f"emulation wall time {wall / frames * 1e3:.1f} ms per frame (all {N} ranks, serial)")
     del engines
     torch.cuda.empty_cache()
