@@ -1715,8 +1715,14 @@ __device__ int closest_sah(const DevScene& sc, V3 o, V3 d, double tmin, double* 
   RLC_STAT(4, st_nodes);
   RLC_STAT(5, st_tris);
   if (hit == kNoSlot) return 0;
-  if (tie) return 2;
-  if (!box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf_s + hit)), o, inv, tmin, closest)) return 2;
+  if (tie) {
+    RLC_STAT(7, 1);  // deferred to the reference-order traversal: an exact tie
+    return 2;
+  }
+  if (!box_hit(load_node(sc.nodes, __ldg(sc.tri_leaf_s + hit)), o, inv, tmin, closest)) {
+    RLC_STAT(7, 1);  // deferred: the reference's own box test misses the hit's leaf
+    return 2;
+  }
   *t_out = closest;
   *tri_out = sc.tris_s[hit].tri_id;
   return 1;

@@ -758,4 +758,4 @@ def trav_stats(reset: bool = True) -> dict:
     v = list(out)
     return {"shadow_rays": v[0], "shadow_nodes": v[1], "shadow_tris": v[2],
             "closest_rays": v[3], "closest_nodes": v[4], "closest_tris": v[5],
-            "shadow_overflows": v[6]}
+            "shadow_overflows": v[6], "closest_deferred": v[7]}
