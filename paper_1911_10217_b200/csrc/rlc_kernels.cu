@@ -2,15 +2,22 @@
 //
 // Per pass (render_pass + end_of_pass_update, proj/src/render.cpp:159-200):
 //   k_primary      camera ray, closest hit, shading point, footprint level,
-//                  5-D cell key and hash-grid lookup/insert      (one thread/path)
+//                  5-D cell key and hash-grid lookup (find only)  (one thread/path)
+//   k_insert,      the pass's new keys into the table in canonical order,
+//   k_commit       published with template cuts
 //   k_sample       cut sampling from the pass-frozen cdf, emitter point,
-//                  NEE geometry, any-hit shadow ray, feedback v  (one thread/path)
-//   radix sort     stable, update records by (cell, cluster)     (hand-written)
+//                  NEE geometry, shadow segment, feedback v, the ray
+//                  compaction's tile counts                       (one thread/vertex)
+//   k_cmp_scatter  stable compaction of the shadow segments
+//   k_shadow       any-hit traversal of the segments (persistent warps)
+//   radix sort     stable, update records by (cell, cluster)      (beside k_shadow)
 //   k_fold         sequential update_q per (cell, cluster) segment in canonical
 //                  order -> live q, visits and per-sample q_before
 //   k_accumulate   deferred radiance with q_before, Framebuffer::add_sample
 //   k_split        split-collapse + ends per touched cell (one warp/cell),
 //                  then the serial cdf (one lane/cell)
+// Sharded passes add k_write_block, k_classify, k_resolve_pending, k_apply /
+// k_apply_entries and k_shard_scatter.
 //
 // All FP64 arithmetic keeps the reference's operand order and this file is
 // compiled with --fmad=false: the path is bit-exact with the reference
