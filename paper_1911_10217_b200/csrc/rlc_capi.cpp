@@ -389,15 +389,19 @@ struct rlc_context {
     if (pstream) RLC_CK(cudaStreamWaitEvent(pstream, ev_main_fence, 0));
     if (sstream) RLC_CK(cudaStreamWaitEvent(sstream, ev_main_fence, 0));
   }
-  cudaEvent_t ev_gbuf_free[2] = {nullptr, nullptr};
-  rlc::GBuf* gslot[2] = {nullptr, nullptr};
-  unsigned long long* pkey_slot[2] = {nullptr, nullptr};  // pending keys, per G-buffer slot
+  // G-buffer slots (passes in flight): RLC_GSLOTS, 2 (default) or 3
+  static constexpr int kMaxSlots = 3;
+  int nslots = 2;
+  int slot_of(uint32_t pass) const { return int(pass % uint32_t(nslots)); }
+  cudaEvent_t ev_gbuf_free[kMaxSlots] = {nullptr, nullptr, nullptr};
+  rlc::GBuf* gslot[kMaxSlots] = {nullptr, nullptr, nullptr};
+  unsigned long long* pkey_slot[kMaxSlots] = {};  // pending keys, per G-buffer slot
   // sample records and q_before per G-buffer slot: pass p's accumulation
   // (side stream) reads them while pass p + 1 samples and folds
-  rlc::SampleRec* srec_slot[2] = {nullptr, nullptr};
-  uint8_t* rflag_slot[2] = {nullptr, nullptr};  // (the occluded bits k_accumulate reads)
-  uint32_t* gflags_slot[2] = {nullptr, nullptr};
-  double* qb_slot[2] = {nullptr, nullptr};
+  rlc::SampleRec* srec_slot[kMaxSlots] = {};
+  uint8_t* rflag_slot[kMaxSlots] = {};  // (the occluded bits k_accumulate reads)
+  uint32_t* gflags_slot[kMaxSlots] = {};
+  double* qb_slot[kMaxSlots] = {};
   void sync_all() {
     RLC_CK(cudaStreamSynchronize(stream));
     if (pstream) RLC_CK(cudaStreamSynchronize(pstream));
@@ -570,30 +574,26 @@ struct rlc_context {
     ++pb_gen;
     scratch.release();
     const uint32_t cap = n;
-    gslot[0] = scratch.alloc<rlc::GBuf>(cap);
-    gslot[1] = scratch.alloc<rlc::GBuf>(cap);
+    for (int k = 0; k < nslots; ++k) {
+      gslot[k] = scratch.alloc<rlc::GBuf>(cap);
+      pkey_slot[k] = scratch.alloc<unsigned long long>(2 * size_t(cap));
+      srec_slot[k] = scratch.alloc<rlc::SampleRec>(cap);
+      gflags_slot[k] = scratch.alloc<uint32_t>(cap);
+      rflag_slot[k] = scratch.alloc<uint8_t>(cap);
+      qb_slot[k] = scratch.alloc<double>(cap);
+    }
     pb.gbuf = gslot[0];
-    pkey_slot[0] = scratch.alloc<unsigned long long>(2 * size_t(cap));
-    pkey_slot[1] = scratch.alloc<unsigned long long>(2 * size_t(cap));
     pb.pkey = pkey_slot[0];
     pb.nk = alloc_new_keys(scratch, cap, stream);
     pb.emit = scratch.alloc<uint32_t>(cap);
-    srec_slot[0] = scratch.alloc<rlc::SampleRec>(cap);
-    srec_slot[1] = scratch.alloc<rlc::SampleRec>(cap);
     pb.srec = srec_slot[0];
     pb.vdense = scratch.alloc<double>(cap);
-    gflags_slot[0] = scratch.alloc<uint32_t>(cap);
-    gflags_slot[1] = scratch.alloc<uint32_t>(cap);
     pb.gflags = gflags_slot[0];
-    rflag_slot[0] = scratch.alloc<uint8_t>(cap);
-    rflag_slot[1] = scratch.alloc<uint8_t>(cap);
     pb.rflag = rflag_slot[0];
     pb.keys = scratch.alloc<uint32_t>(cap);
     pb.vals = scratch.alloc<uint32_t>(cap);
     pb.keys_alt = scratch.alloc<uint32_t>(cap);
     pb.vals_alt = scratch.alloc<uint32_t>(cap);
-    qb_slot[0] = scratch.alloc<double>(cap);
-    qb_slot[1] = scratch.alloc<double>(cap);
     pb.q_before = qb_slot[0];
     pb.rays = scratch.alloc<rlc::ShadowRay>(cap);
     pb.ray_count = scratch.alloc<unsigned int>(2);
@@ -708,7 +708,7 @@ void enqueue_trace(rlc_context* ctx, const PassSetup& S, rlc_grid* grid, uint32_
   // (new cells get fresh ids with touched = 0, which the running
   // split-collapse skips), so they run on the side stream as soon as their
   // G-buffer slot is free and overlap the previous pass's tail.
-  const int slot = int(S.p.pass_index & 1u);
+  const int slot = ctx->slot_of(S.p.pass_index);
   ctx->pb.gbuf = ctx->gslot[slot];
   ctx->pb.pkey = ctx->pkey_slot[slot];
   ctx->pb.srec = ctx->srec_slot[slot];
@@ -797,11 +797,11 @@ void enqueue_pass(const rlc_context* cctx, const rlc_render_config* cfg, uint32_
       rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, ctx->sstream);
     });
     RLC_CK(cudaEventRecord(ctx->ev_acc_done, ctx->sstream));
-    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], ctx->sstream));
+    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[ctx->slot_of(S.p.pass_index)], ctx->sstream));
     ctx->acc_pending = true;
   } else {
     ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
-    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));  // last G-buffer reader
+    RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[ctx->slot_of(S.p.pass_index)], st));  // last G-buffer reader
   }
   RLC_CK(cudaGetLastError());
 }
@@ -920,6 +920,8 @@ rlc_status rlc_context_create(const rlc_scene_desc* scene, const rlc_render_conf
     check_device(device);
     auto ctx = std::make_unique<rlc_context>();
     ctx->device = device;
+    if (const char* e = std::getenv("RLC_GSLOTS"))  // G-buffer slots: 2 or 3 (A/B)
+      ctx->nslots = std::min(rlc_context::kMaxSlots, std::max(2, std::atoi(e)));
     ctx->create_cfg = *config;
     rlc::build_host_scene(*scene, *config, ctx->host);
     RLC_CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
@@ -1673,7 +1675,7 @@ void shard_finish(rlc_context* ctx, rlc_grid* grid, rlc_framebuffer* fb, uint32_
   if (owner_fold) ctx->stage(3, [&] { rlc::launch_shard_apply(S.g, S.p, rank, ctx->xb, st); });
   rlc::launch_shard_scatter(S.g, ctx->pb, S.nv, rank, ctx->xb, st);
   if (S.n > 0) ctx->stage(4, [&] { rlc::launch_accumulate(ctx->dev, S.p, ctx->pb, fb->fb, st); });
-  RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[S.p.pass_index & 1u], st));
+  RLC_CK(cudaEventRecord(ctx->ev_gbuf_free[ctx->slot_of(S.p.pass_index)], st));
   RLC_CK(cudaGetLastError());
 }
 
