@@ -2456,10 +2456,27 @@ __global__ void k_split(DevScene sc, DevGrid g, double threshold, uint32_t itera
   for (uint32_t cell = blockIdx.x * wpb + wib; cell < ncells; cell += gridDim.x * wpb) {
     if (!g.touched[cell]) continue;  // warp-uniform
     const size_t row = size_t(cell) * M;
-    for (uint32_t i = lane; i < M; i += 32) {
-      qA[i] = g.q[row + i];
-      nA[i] = g.node_ids[row + i];
-      vA[i] = g.visits[row + i];
+    for (uint32_t i0 = 0; i0 < M; i0 += 128) {  // all of a chunk's loads in flight first
+      double qv[4];
+      uint32_t nv[4], vv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t i = i0 + lane + 32u * k;
+        if (i < M) {
+          qv[k] = __ldcg(g.q + row + i);
+          nv[k] = __ldcg(g.node_ids + row + i);
+          vv[k] = __ldcg(g.visits + row + i);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t i = i0 + lane + 32u * k;
+        if (i < M) {
+          qA[i] = qv[k];
+          nA[i] = nv[k];
+          vA[i] = vv[k];
+        }
+      }
     }
     __syncwarp();
     const uint32_t changes_before = my_changes;
