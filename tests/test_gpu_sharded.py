@@ -188,10 +188,12 @@ def test_nccl_frame_one_rank_matches_render_pass(ref, owner):
     assert grid.stats() == rr.stats()
 
 
-@pytest.mark.parametrize("owner", [True, False])
-def test_nccl_frames_graph_replay_bit_exact(owner):
+@pytest.mark.parametrize("owner,entry", [(True, "0"), (False, "0"), (True, "1")])
+def test_nccl_frames_graph_replay_bit_exact(monkeypatch, owner, entry):
     """rlc_shard_frames replaying a captured CUDA graph of two sharded frames
-    (NCCL collectives inside) equals the same frames enqueued one by one."""
+    (NCCL collectives inside) equals the same frames enqueued one by one
+    (owner mode also with the entry exchange)."""
+    monkeypatch.setenv("RLC_SHARD_ENTRY", entry)
     scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
     cfg = rlcuts.RenderConfig(spp=9, passes=9, sampler=RL,
                               cut=rlcuts.CutConfig(cut_size=64, split_threshold=2.0))
