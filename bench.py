@@ -320,7 +320,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ctx.set_stream(stream.cuda_stream)
         eng = rdist.GpuEngine(ctx, grid, fb, cfg, torch.device("cuda", local_rank), world=world)
         if args.dist_backend == "nccl":
-            frame = rdist.NcclFrame(eng, H, rank, world, local_rank, owner=not args.replicated_fold)
+            frame = rdist.NcclFrame(eng, H, rank, world, local_rank, owner=not args.replicated_fold,
+                                    peer=args.peer_exchange)
         else:
             frame = rdist.ShardedFrame(eng, H, rank, world, host_staging=True,
                                        owner=not args.replicated_fold)
@@ -522,6 +523,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "parallelism": (f"screen bands x{world}, exact update-record all-gather "
                                        f"over {args.dist_backend}, "
                                        f"{'replicated' if args.replicated_fold else 'owner'}-folded"
+                                       + (", peer-memory record exchange" if args.peer_exchange else "")
                                        + (", CUDA-graph replay" if graphed else "")
                                        if world > 1 else "single GPU"),
                        "cells": st["occupied"], "fallback_hits": st["fallback_hits"],
@@ -552,6 +554,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: bound on the timed host time")
+    ap.add_argument("--peer-exchange", action="store_true",
+                    help="N > 1 over NCCL: records stored straight into every rank's receive "
+                         "buffer over NVLink (CUDA IPC) instead of ncclAllGather")
     ap.add_argument("--scene-ahead", type=int, default=3,
                     help="dynamic workloads: frames whose scenes are prepared ahead")
     ap.add_argument("--replicated-fold", action="store_true",

@@ -365,6 +365,16 @@ rlc_status rlc_shard_trace(const rlc_context* ctx, const rlc_render_config* conf
                            uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
                            uint32_t row_end, uint64_t cap_records, void** block,
                            uint64_t* block_bytes);
+/* rlc_shard_trace with the block stored straight into ndst (<= 16) gathered
+ * buffers of nranks * block_bytes each, at block `rank` -- every rank's
+ * receive buffer (peer memory over NVLink, or buffers of emulated ranks):
+ * only the records that exist are written.  The caller orders the stores
+ * before any rank's rlc_shard_fold (a barrier collective) and keeps a buffer
+ * unwritten until its readers' rlc_shard_finish. */
+rlc_status rlc_shard_trace_to(const rlc_context* ctx, const rlc_render_config* config,
+                              uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
+                              uint32_t row_end, uint64_t cap_records, uint32_t rank,
+                              void* const* dst_buffers, uint32_t ndst);
 rlc_status rlc_shard_fold(const rlc_context* ctx, const rlc_render_config* config, rlc_grid* grid,
                           const void* blocks, uint32_t nranks, uint32_t rank, int owner_fold,
                           double** q_before_slots, uint32_t** seg_counts, uint64_t* slots);
@@ -387,6 +397,12 @@ rlc_status rlc_comm_unique_id(uint8_t* id128);
 rlc_status rlc_comm_create(int device, uint32_t nranks, uint32_t rank, const uint8_t* id128,
                            rlc_comm** out);
 rlc_status rlc_comm_destroy(rlc_comm* comm);
+/* Collective (every rank calls it): rlc_shard_frame then moves the records
+ * by peer memory instead of ncclAllGather -- each rank stores its band's
+ * records straight into every rank's receive buffer (CUDA IPC handles over
+ * NVLink; two halves by pass parity), then one int all-reduce is the
+ * barrier.  cap_records as rlc_shard_frame's; enable = 0 returns to NCCL. */
+rlc_status rlc_comm_enable_peer_exchange(rlc_comm* comm, uint64_t cap_records, int enable);
 rlc_status rlc_shard_frame(const rlc_context* ctx, const rlc_render_config* config,
                            uint32_t pass_index, rlc_grid* grid, rlc_framebuffer* fb,
                            rlc_comm* comm, uint32_t row_begin, uint32_t row_end,

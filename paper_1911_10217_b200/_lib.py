@@ -131,6 +131,10 @@ SIGNATURES = {
                                   C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), _u64p]),
     "rlc_shard_fold": (C.c_int, [_P, C.POINTER(RenderConfigC), _P, _P, C.c_uint32, C.c_uint32,
                                  C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _u64p]),
+    "rlc_shard_trace_to": (C.c_int, [_P, C.POINTER(RenderConfigC), C.c_uint32, _P, C.c_uint32,
+                                     C.c_uint32, C.c_uint64, C.c_uint32, C.POINTER(C.c_void_p),
+                                     C.c_uint32]),
+    "rlc_comm_enable_peer_exchange": (C.c_int, [_P, C.c_uint64, C.c_int]),
     "rlc_shard_entry_arrays": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _u64p]),
     "rlc_shard_finish": (C.c_int, [_P, _P, _P, C.c_uint32, C.c_int]),
     "rlc_shard_sync": (C.c_int, [_P, _P]),

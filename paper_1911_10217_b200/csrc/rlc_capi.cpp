@@ -549,7 +549,7 @@ struct rlc_context {
     cudaGraphExec_t exec = nullptr;
     rlc_render_config cfg{};
     const void *grid = nullptr, *fb = nullptr, *comm = nullptr, *gathered = nullptr,
-               *block = nullptr;
+               *block = nullptr, *peer_recv = nullptr;
     uint32_t r0 = 0, r1 = 0;
     uint64_t cap = 0;
     int owner = 0;
@@ -1600,7 +1600,8 @@ rlc_status rlc_render_pass_async(const rlc_context* ctx, const rlc_render_config
 namespace {
 
 void shard_trace(rlc_context* ctx, const rlc_render_config* config, uint32_t pass_index,
-                 rlc_grid* grid, uint32_t row_begin, uint32_t row_end, uint64_t cap) {
+                 rlc_grid* grid, uint32_t row_begin, uint32_t row_end, uint64_t cap,
+                 const rlc::PeerDsts* dsts = nullptr, uint32_t ndst = 0, uint32_t rank = 0) {
   require(config->sampler == RLC_SAMPLER_RL_LIGHTCUTS && grid != nullptr,
           "rlc_shard_trace: the sharded pass is the learned sampler's");
   require(cap > 0 && cap < (1ull << 31), "rlc_shard_trace: bad record capacity");
@@ -1618,7 +1619,10 @@ void shard_trace(rlc_context* ctx, const rlc_render_config* config, uint32_t pas
   ctx->last_pass = S.p;
   ctx->last_pb = ctx->pb;
   ctx->last_valid = true;
-  rlc::launch_export_block(S.g, ctx->pb, S.nv, ctx->block, uint32_t(cap), ctx->stream);
+  if (dsts)  // the records straight into the gathered buffers (peer memory)
+    rlc::launch_export_block_to(S.g, ctx->pb, S.nv, *dsts, ndst, rank, uint32_t(cap), ctx->stream);
+  else
+    rlc::launch_export_block(S.g, ctx->pb, S.nv, ctx->block, uint32_t(cap), ctx->stream);
   RLC_CK(cudaGetLastError());
 }
 
@@ -1692,6 +1696,24 @@ rlc_status rlc_shard_trace(const rlc_context* cctx, const rlc_render_config* con
     shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
     *block = ctx->block;
     *block_bytes = ctx->block_bytes();
+  });
+}
+
+rlc_status rlc_shard_trace_to(const rlc_context* cctx, const rlc_render_config* config,
+                              uint32_t pass_index, rlc_grid* grid, uint32_t row_begin,
+                              uint32_t row_end, uint64_t cap_records, uint32_t rank,
+                              void* const* dst_buffers, uint32_t ndst) {
+  return guarded([&] {
+    require(cctx != nullptr && config != nullptr && dst_buffers != nullptr,
+            "rlc_shard_trace_to: null argument");
+    require(ndst >= 1 && ndst <= rlc::kMaxPeers, "rlc_shard_trace_to: bad destination count");
+    rlc::PeerDsts d{};
+    for (uint32_t k = 0; k < ndst; ++k) {
+      require(dst_buffers[k] != nullptr, "rlc_shard_trace_to: null destination");
+      d.p[k] = static_cast<rlc::ExchangeRecord*>(dst_buffers[k]);
+    }
+    shard_trace(const_cast<rlc_context*>(cctx), config, pass_index, grid, row_begin, row_end,
+                cap_records, &d, ndst, rank);
   });
 }
 
@@ -1787,7 +1809,25 @@ struct rlc_comm {
   DeviceArena arena;
   void* gathered = nullptr;  // nranks record blocks
   uint64_t gathered_bytes = 0;
+  // peer exchange (rlc_comm_enable_peer_exchange): this rank's receive buffer
+  // (its own cudaMalloc, exported by CUDA IPC) and every rank's, opened here
+  bool peer = false;
+  uint64_t peer_cap = 0;
+  void* peer_recv = nullptr;
+  rlc::PeerDsts peer_dst{};
+  int* barrier = nullptr;  // one int all-reduced after the stores
+  void release_peer() {
+    for (uint32_t r = 0; r < nranks && r < rlc::kMaxPeers; ++r)
+      if (r != rank && peer_dst.p[r]) cudaIpcCloseMemHandle(peer_dst.p[r]);
+    if (peer_recv) cudaFree(peer_recv);
+    if (barrier) cudaFree(barrier);
+    peer_recv = nullptr;
+    barrier = nullptr;
+    peer_dst = {};
+    peer = false;
+  }
   ~rlc_comm() {
+    release_peer();
     if (comm) nccl().destroy(comm);
   }
 };
@@ -1823,12 +1863,74 @@ rlc_status rlc_comm_destroy(rlc_comm* comm) {
   return guarded([&] { delete comm; });
 }
 
+rlc_status rlc_comm_enable_peer_exchange(rlc_comm* comm, uint64_t cap_records, int enable) {
+  return guarded([&] {
+    require(comm != nullptr, "rlc_comm_enable_peer_exchange: null communicator");
+    require(comm->nranks <= rlc::kMaxPeers, "rlc_comm_enable_peer_exchange: too many ranks");
+    RLC_CK(cudaSetDevice(comm->device));
+    RLC_CK(cudaDeviceSynchronize());
+    comm->release_peer();
+    if (!enable) return;
+    require(cap_records > 0, "rlc_comm_enable_peer_exchange: bad record capacity");
+    // two halves by pass parity: a rank writes pass p + 1's records while
+    // the others may still read pass p's (the per-pass barrier then orders
+    // pass p + 2's writes after every rank's reads of pass p)
+    const size_t bytes =
+        2 * size_t(comm->nranks) * (cap_records + 1) * sizeof(rlc::ExchangeRecord);
+    RLC_CK(cudaMalloc(&comm->peer_recv, bytes));
+    RLC_CK(cudaMemset(comm->peer_recv, 0, bytes));
+    RLC_CK(cudaMalloc(&comm->barrier, sizeof(int)));
+    RLC_CK(cudaMemset(comm->barrier, 0, sizeof(int)));
+    comm->peer_dst.p[comm->rank] = static_cast<rlc::ExchangeRecord*>(comm->peer_recv);
+    if (comm->nranks > 1) {  // every rank's IPC handle to every rank (setup, synchronizing)
+      cudaIpcMemHandle_t mine;
+      RLC_CK(cudaIpcGetMemHandle(&mine, comm->peer_recv));
+      const size_t hb = sizeof(cudaIpcMemHandle_t);
+      unsigned char* dev = nullptr;
+      RLC_CK(cudaMalloc(&dev, hb * (comm->nranks + 1)));
+      RLC_CK(cudaMemcpy(dev + hb * comm->nranks, &mine, hb, cudaMemcpyHostToDevice));
+      nccl_check(nccl().all_gather(dev + hb * comm->nranks, dev, hb, ncclUint8, comm->comm, 0),
+                 "ncclAllGather");
+      std::vector<cudaIpcMemHandle_t> all(comm->nranks);
+      RLC_CK(cudaMemcpy(all.data(), dev, hb * comm->nranks, cudaMemcpyDeviceToHost));
+      cudaFree(dev);
+      for (uint32_t r = 0; r < comm->nranks; ++r) {
+        if (r == comm->rank) continue;
+        void* p = nullptr;
+        RLC_CK(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+        comm->peer_dst.p[r] = static_cast<rlc::ExchangeRecord*>(p);
+      }
+    }
+    comm->peer_cap = cap_records;
+    comm->peer = true;
+  });
+}
+
 namespace {
 // One sharded frame on the context stream (rlc_shard_frame): the band's
 // trace, the NCCL exchange, the exact fold and split-collapse.
 void shard_frame_body(rlc_context* ctx, const rlc_render_config* config, uint32_t pass_index,
                       rlc_grid* grid, rlc_framebuffer* fb, rlc_comm* comm, uint32_t row_begin,
                       uint32_t row_end, uint64_t cap_records, int owner_fold) {
+  cudaStream_t st = ctx->stream;
+  if (comm->peer) {
+    // the records stored straight into every rank's receive buffer over
+    // NVLink, then one all-reduce of an int as the barrier: each rank's
+    // stores precede its part of the collective on its stream
+    require(cap_records == comm->peer_cap,
+            "rlc_shard_frame: record capacity differs from the peer exchange's");
+    const size_t half = size_t(pass_index & 1u) * comm->nranks * (cap_records + 1);
+    rlc::PeerDsts d = comm->peer_dst;
+    for (uint32_t r = 0; r < comm->nranks; ++r) d.p[r] += half;
+    shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records, &d, comm->nranks,
+                comm->rank);
+    if (comm->nranks > 1)
+      nccl_check(nccl().all_reduce(comm->barrier, comm->barrier, 1, ncclInt32, ncclSum, comm->comm,
+                                   st),
+                 "ncclAllReduce");
+    shard_fold(ctx, config, grid, static_cast<rlc::ExchangeRecord*>(comm->peer_recv) + half,
+               comm->nranks, comm->rank, owner_fold);
+  } else {
   shard_trace(ctx, config, pass_index, grid, row_begin, row_end, cap_records);
   const uint64_t bb = ctx->block_bytes();
   if (comm->gathered_bytes < bb * comm->nranks) {
@@ -1837,11 +1939,11 @@ void shard_frame_body(rlc_context* ctx, const rlc_render_config* config, uint32_
     comm->gathered = comm->arena.alloc<unsigned char>(bb * comm->nranks);
     comm->gathered_bytes = bb * comm->nranks;
   }
-  cudaStream_t st = ctx->stream;
   // the exchange: every rank's block to every rank (fixed size: no host count)
   nccl_check(nccl().all_gather(ctx->block, comm->gathered, bb, ncclUint8, comm->comm, st),
              "ncclAllGather");
   shard_fold(ctx, config, grid, comm->gathered, comm->nranks, comm->rank, owner_fold);
+  }
   if (owner_fold && comm->nranks > 1 && ctx->xb.entry_mode) {
     // each band's q_before from the owners (reduce-scatter, in place: this
     // rank's block of slots), every entry's final q and count (all-reduce)
@@ -1920,7 +2022,8 @@ rlc_status rlc_shard_frames(const rlc_context* cctx, const rlc_render_config* co
                       G.grid == grid && G.fb == fb && G.comm == comm && G.r0 == row_begin &&
                       G.r1 == row_end && G.cap == cap_records && G.owner == owner_fold &&
                       G.pb_gen == ctx->pb_gen && G.scene_gen == ctx->scene_gen &&
-                      G.gathered == comm->gathered && G.block == ctx->block;
+                      G.gathered == comm->gathered && G.block == ctx->block &&
+                      G.peer_recv == comm->peer_recv;
     if (!same) {
       if (G.exec) {
         RLC_CK(cudaGraphExecDestroy(G.exec));
@@ -1961,6 +2064,7 @@ rlc_status rlc_shard_frames(const rlc_context* cctx, const rlc_render_config* co
       G.pb_gen = ctx->pb_gen;
       G.scene_gen = ctx->scene_gen;
       G.gathered = comm->gathered;
+      G.peer_recv = comm->peer_recv;
       G.block = ctx->block;
     }
     const uint32_t replays = count / kFrames;

@@ -2693,6 +2693,55 @@ __global__ void k_write_block(DevGrid g, const GBuf* __restrict__ gbuf,
   block[1 + k] = r;
 }
 
+// k_write_block with the block written into every destination's slot range
+// of rank `rank` (stride cap + 1): peer receive buffers over NVLink.  The
+// system-scope fence orders the stores before the barrier collective that
+// follows on the stream.
+__global__ void k_write_block_to(DevGrid g, const GBuf* __restrict__ gbuf,
+                                 const SampleRec* __restrict__ srec,
+                                 const double* __restrict__ vdense,
+                                 const uint32_t* __restrict__ rec_path,
+                                 const unsigned int* __restrict__ count, uint32_t n,
+                                 const unsigned long long* __restrict__ pkey, uint32_t cap,
+                                 PeerDsts dst, uint32_t ndst, uint32_t rank) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t c = min(*count, cap);
+  const size_t base = size_t(rank) * (cap + 1);
+  if (k == 0) {
+    RecordBlockHeader h{};
+    h.count = c;
+    for (uint32_t d = 0; d < ndst; ++d)
+      *reinterpret_cast<RecordBlockHeader*>(dst.p[d] + base) = h;
+  }
+  if (k < n && k < c) {
+    const uint32_t idx = rec_path[k];
+    const uint32_t cell = gbuf[idx].cell;
+    ExchangeRecord r;
+    r.cluster = srec[idx].s;
+    r.v = vdense[idx];
+    if (cell == kPending) {
+      r.slot = kPending;
+      r.klo = pkey[2 * size_t(idx)];
+      r.khi = pkey[2 * size_t(idx) + 1];
+    } else {
+      r.slot = g.cell_slot[cell];
+      r.klo = 0;
+      r.khi = 0;
+    }
+    for (uint32_t d = 0; d < ndst; ++d) dst.p[d][base + 1 + k] = r;
+  }
+  __threadfence_system();
+}
+
+void launch_export_block_to(const DevGrid& g, const PassBuffers& b, uint32_t n,
+                            const PeerDsts& dst, uint32_t ndst, uint32_t rank, uint32_t cap,
+                            cudaStream_t st) {
+  launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);
+  k_write_block_to<<<blocks_for(n > 0 ? n : 1, 256), 256, 0, st>>>(
+      g, b.gbuf, b.srec, b.vdense, b.rec_path, b.rec_count, n, b.pkey, cap, dst, ndst, rank);
+  count_launch();
+}
+
 void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, void* block,
                          uint32_t cap, cudaStream_t st) {
   launch_compact(b, nullptr, n, kSRecord, b.rec_path, b.rec_count, st);

@@ -314,6 +314,17 @@ void launch_sort_buffers(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb,
 // traced band, in canonical order, into `block` (header slot + cap slots).
 void launch_export_block(const DevGrid& g, const PassBuffers& b, uint32_t n, void* block,
                          uint32_t cap, cudaStream_t st);
+// The same records stored straight into `ndst` (<= kMaxPeers) gathered
+// buffers at block `rank` -- peers' receive buffers over NVLink (CUDA IPC) or,
+// for emulated ranks, buffers on this device: only the records that exist
+// cross, then one barrier collective orders them before the fold.
+constexpr uint32_t kMaxPeers = 16;
+struct PeerDsts {
+  ExchangeRecord* p[kMaxPeers];
+};
+void launch_export_block_to(const DevGrid& g, const PassBuffers& b, uint32_t n,
+                            const PeerDsts& dst, uint32_t ndst, uint32_t rank, uint32_t cap,
+                            cudaStream_t st);
 // The fold of all ranks' gathered blocks (x.rec: nranks x x.stride slots,
 // valid until the pass's launch_shard_scatter): the pass's new keys inserted
 // in canonical order (identical tables on every rank), then each record's

@@ -16,7 +16,9 @@ rank then forms the radiance of its own band.
 
 Three drivers of the same protocol:
   * NcclFrame -- the C++ data plane (rlc_shard_frame): NCCL all-gather and
-    all-reduce on the context stream, no host synchronization per frame;
+    all-reduce on the context stream, no host synchronization per frame; or
+    (peer=True) every rank storing its records straight into every rank's
+    receive buffer over NVLink, one barrier all-reduce per frame;
   * ShardedFrame -- the same steps with torch.distributed collectives (gloo
     stages through host memory: functional multi-process runs);
   * local_exchange -- N ranks emulated as N contexts on one device, the
@@ -67,6 +69,12 @@ class GpuEngine:
     def trace(self, pass_index: int, rows) -> torch.Tensor:
         ptr, nbytes = rlcuts.shard_trace(self.ctx, self.cfg, pass_index, self.grid, rows, self.cap)
         return torch.as_tensor(_CudaView(ptr, nbytes), device=self.device)
+
+    def trace_to(self, pass_index: int, rows, rank: int, dsts) -> None:
+        """The band's records stored straight into every buffer of `dsts`
+        (each nranks blocks) at block `rank`."""
+        rlcuts.shard_trace_to(self.ctx, self.cfg, pass_index, self.grid, rows, self.cap, rank,
+                              [d.data_ptr() for d in dsts])
 
     def fold(self, gathered: torch.Tensor, nranks: int, rank: int, owner: bool):
         """-> the arrays owner mode sums over the ranks: q_before per exchange
@@ -139,7 +147,7 @@ class NcclFrame:
     (rlc_shard_frame): one library call per frame, no host synchronization."""
 
     def __init__(self, engine: GpuEngine, height: int, rank: int, world: int, device_index: int,
-                 owner: bool = True):
+                 owner: bool = True, peer: bool = False):
         self.engine, self.rank, self.world = engine, rank, world
         self.rows = band(height, rank, world)
         self.owner = owner
@@ -147,6 +155,8 @@ class NcclFrame:
         if world > 1:
             dist.broadcast_object_list(obj, src=0)
         self.comm = rlcuts.Comm(device_index, world, rank, obj[0])
+        if peer:  # records by peer memory (CUDA IPC), one barrier all-reduce per frame
+            self.comm.enable_peer_exchange(engine.cap)
 
     def step(self, pass_index: int) -> None:
         e = self.engine
@@ -161,7 +171,7 @@ class NcclFrame:
 
 
 def local_exchange(engines, heights_rows, pass_index: int, owner: bool = True,
-                   serial: bool = False):
+                   serial: bool = False, peer_buffers=None):
     """Single-process emulation of the exchange for N engines (tests on one
     device): every engine traces its band, the blocks are concatenated in
     rank order, every engine folds; in owner mode the per-slot q_before
@@ -169,18 +179,30 @@ def local_exchange(engines, heights_rows, pass_index: int, owner: bool = True,
     serial: one rank's work at a time (per-rank timing without the other
     ranks' kernels sharing the device)."""
     n = len(engines)
-    blocks = []
-    for e, rows in zip(engines, heights_rows):
-        blocks.append(e.trace(pass_index, rows))
-        if serial:
+    if peer_buffers is not None:
+        # the peer exchange's data path: every rank stores its records into
+        # every rank's buffer (here all on one device), each folds its own
+        for r, (e, rows) in enumerate(zip(engines, heights_rows)):
+            e.trace_to(pass_index, rows, r, peer_buffers)
+            if serial:
+                e.ctx.synchronize()
+        for e in engines:
             e.ctx.synchronize()
-    for e in engines:
-        e.ctx.synchronize()
-    gathered = torch.cat([b.clone() for b in blocks])
+        sources = list(peer_buffers)
+    else:
+        blocks = []
+        for e, rows in zip(engines, heights_rows):
+            blocks.append(e.trace(pass_index, rows))
+            if serial:
+                e.ctx.synchronize()
+        for e in engines:
+            e.ctx.synchronize()
+        gathered = torch.cat([b.clone() for b in blocks])
+        sources = [gathered] * n
     torch.cuda.synchronize()
     arrays = []
     for r, e in enumerate(engines):
-        arrays.append(e.fold(gathered, n, r, owner))
+        arrays.append(e.fold(sources[r], n, r, owner))
         if serial:
             e.ctx.synchronize()
     for e in engines:

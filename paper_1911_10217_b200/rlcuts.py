@@ -492,6 +492,16 @@ def shard_trace(ctx: RenderContext, config: RenderConfig, pass_index: int, grid:
     return int(ptr.value or 0), int(n.value)
 
 
+def shard_trace_to(ctx: RenderContext, config: RenderConfig, pass_index: int, grid: HashGrid,
+                   rows: tuple, cap_records: int, rank: int, dst_ptrs: list) -> None:
+    """rlc_shard_trace_to: the band's records stored straight into every
+    destination buffer (device pointers) at block `rank`."""
+    cfg = config.c()
+    arr = (C.c_void_p * len(dst_ptrs))(*dst_ptrs)
+    _check(_lib.load().rlc_shard_trace_to(ctx.handle, C.byref(cfg), pass_index, grid.handle,
+                                          rows[0], rows[1], cap_records, rank, arr, len(dst_ptrs)))
+
+
 def shard_fold(ctx: RenderContext, config: RenderConfig, grid: HashGrid, blocks_ptr: int,
                nranks: int, rank: int, owner_fold: bool) -> tuple[int, int, int]:
     """rlc_shard_fold over the all-gathered blocks (device memory, rank-major,
@@ -537,6 +547,11 @@ class Comm:
         buf = (C.c_uint8 * 128)()
         _check(_lib.load().rlc_comm_unique_id(buf))
         return bytes(buf)
+
+    def enable_peer_exchange(self, cap_records: int, enable: bool = True):
+        """Collective: rlc_shard_frame moves records by peer memory (CUDA IPC)
+        instead of ncclAllGather."""
+        _check(_lib.load().rlc_comm_enable_peer_exchange(self.handle, cap_records, int(enable)))
 
     def __init__(self, device: int, nranks: int, rank: int, uid: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)

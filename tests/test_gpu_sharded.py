@@ -48,6 +48,44 @@ def test_sharded_gpu_matches_single(ref, world, depth, owner):
     assert lookups == rr.stats()["lookups"]
 
 
+@pytest.mark.parametrize("world,owner,capacity", [(2, True, 1 << 16), (3, False, 1 << 16),
+                                                  (3, True, 200)])
+def test_sharded_peer_exchange(ref, world, owner, capacity):
+    """The peer exchange's data path: every rank stores its band's records
+    straight into every rank's receive buffer (rlc_shard_trace_to; buffers
+    kept across passes, so stale records past a block's count must be
+    ignored) and folds its own -- equal to the reference."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+                              hash=rlcuts.HashConfig(capacity=capacity, probe_limit=16),
+                              cut=rlcuts.CutConfig(cut_size=32, split_threshold=2.0))
+    dev = torch.device("cuda", 0)
+    engines = []
+    for r in range(world):
+        ctx = rlcuts.build_context(scene, cfg)
+        engines.append(rdist.GpuEngine(ctx, rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx),
+                                       cfg, dev, world=world))
+    rows = [rdist.band(scene.camera.height, r, world) for r in range(world)]
+    nbytes = world * 32 * (engines[0].cap + 1)
+    bufs = [torch.full((nbytes,), 0x5A, dtype=torch.uint8, device=dev) for _ in range(world)]
+    rr = ref.RefRun(scene, cfg)
+    for p in range(cfg.passes):
+        changes = rdist.local_exchange(engines, rows, p, owner, peer_buffers=bufs)
+        rch, _ = rr.run_pass(p)
+        assert changes == [rch] * world
+    rs, rc = rr.framebuffer()
+    rcells = rr.export()
+    for e, (r0, r1) in zip(engines, rows):
+        s, c = e.fb.download()
+        assert np.array_equal(s[r0:r1], rs[r0:r1]) and np.array_equal(c[r0:r1], rc[r0:r1])
+        cells = e.grid.export()
+        assert cells.keys() == rcells.keys()
+        for k, v in rcells.items():
+            for f in v:
+                assert np.array_equal(cells[k][f], v[f])
+        assert [(s_, k) for s_, _, k, _ in e.grid.slots()] == rr.slots()
+
+
 @pytest.mark.parametrize("world,capacity", [(2, 1 << 16), (3, 1 << 16), (3, 200)])
 def test_sharded_entry_exchange(ref, monkeypatch, world, capacity):
     """Owner mode's entry exchange (each entry's final q and record count
@@ -186,6 +224,34 @@ def test_nccl_frame_one_rank_matches_render_pass(ref, owner):
         for f in v:
             assert np.array_equal(cells[k][f], v[f])
     assert grid.stats() == rr.stats()
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_nccl_peer_exchange_one_rank(ref, peer):
+    """rlc_shard_frame over a one-rank communicator with the peer exchange
+    (records stored into the IPC-exported receive buffer, two halves by pass
+    parity) equals the reference, frame by frame and from a CUDA graph."""
+    scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
+    cfg = rlcuts.RenderConfig(spp=7, passes=7, sampler=RL,
+                              cut=rlcuts.CutConfig(cut_size=64, split_threshold=2.0))
+    ctx = rlcuts.build_context(scene, cfg)
+    grid, fb = rlcuts.HashGrid(ctx, cfg), rlcuts.Framebuffer(ctx)
+    eng = rdist.GpuEngine(ctx, grid, fb, cfg, torch.device("cuda", 0))
+    frame = rdist.NcclFrame(eng, scene.camera.height, 0, 1, 0, True, peer=True)
+    rr = ref.RefRun(scene, cfg)
+    frame.step(0)
+    frame.run(1, cfg.passes - 1, graph=peer)
+    for p in range(cfg.passes):
+        rr.run_pass(p)
+    rlcuts.shard_sync(ctx, grid)
+    s, c = fb.download()
+    rs, rc = rr.framebuffer()
+    assert np.array_equal(s, rs) and np.array_equal(c, rc)
+    cells, rcells = grid.export(), rr.export()
+    assert cells.keys() == rcells.keys()
+    for k, v in rcells.items():
+        for f in v:
+            assert np.array_equal(cells[k][f], v[f])
 
 
 @pytest.mark.parametrize("owner,entry", [(True, "0"), (False, "0"), (True, "1")])
