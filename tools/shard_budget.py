@@ -56,6 +56,12 @@ for owner in modes:
     e0 = engines[0]
     block = 32 * (e0.cap + 1)
     slots = N * (e0.cap + 1)
+    # the records that exist this frame (block headers): what the peer exchange moves
+    heads = [e.trace(warm + frames, rr) for e, rr in zip(engines, rows)]
+    for e in engines:
+        e.ctx.synchronize()
+    counts = [int(h[:8].view(torch.int64).item()) for h in heads]
+    peer_out = max(counts) * 32 * (N - 1)
     entries = rlcuts.shard_entry_arrays(e0.ctx)[2]
     if not owner:
         comm = ""
@@ -70,6 +76,8 @@ for owner in modes:
     print(f"record block {block / 1e6:.2f} MB per rank; all-gather receives "
           f"{(N - 1) * block / 1e6:.1f} MB per rank (~{(N - 1) * block / 725e9 * 1e6:.0f} us at 725 GB/s);"
           + comm)
+    print(f"records per rank {min(counts)}..{max(counts)} of {e0.cap} slots: the peer exchange "
+          f"stores {peer_out / 1e6:.1f} MB from the busiest rank (~{peer_out / 725e9 * 1e6:.0f} us)")
     print(f"emulation wall time {wall / frames * 1e3:.1f} ms per frame (all {N} ranks, serial)")
     del engines
     torch.cuda.empty_cache()
