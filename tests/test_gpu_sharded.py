@@ -48,15 +48,16 @@ def test_sharded_gpu_matches_single(ref, world, depth, owner):
     assert lookups == rr.stats()["lookups"]
 
 
-@pytest.mark.parametrize("world,owner,capacity", [(2, True, 1 << 16), (3, False, 1 << 16),
-                                                  (3, True, 200)])
-def test_sharded_peer_exchange(ref, world, owner, capacity):
+@pytest.mark.parametrize("world,owner,capacity,depth", [(2, True, 1 << 16, 1),
+                                                        (3, False, 1 << 16, 1),
+                                                        (3, True, 200, 1), (2, True, 1 << 16, 3)])
+def test_sharded_peer_exchange(ref, world, owner, capacity, depth):
     """The peer exchange's data path: every rank stores its band's records
     straight into every rank's receive buffer (rlc_shard_trace_to; buffers
     kept across passes, so stale records past a block's count must be
     ignored) and folds its own -- equal to the reference."""
     scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
-    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL, max_depth=depth,
                               hash=rlcuts.HashConfig(capacity=capacity, probe_limit=16),
                               cut=rlcuts.CutConfig(cut_size=32, split_threshold=2.0))
     dev = torch.device("cuda", 0)
@@ -86,15 +87,16 @@ def test_sharded_peer_exchange(ref, world, owner, capacity):
         assert [(s_, k) for s_, _, k, _ in e.grid.slots()] == rr.slots()
 
 
-@pytest.mark.parametrize("world,capacity", [(2, 1 << 16), (3, 1 << 16), (3, 200)])
-def test_sharded_entry_exchange(ref, monkeypatch, world, capacity):
+@pytest.mark.parametrize("world,capacity,depth", [(2, 1 << 16, 1), (3, 1 << 16, 1), (3, 200, 1),
+                                                  (2, 1 << 16, 3)])
+def test_sharded_entry_exchange(ref, monkeypatch, world, capacity, depth):
     """Owner mode's entry exchange (each entry's final q and record count
     summed over the ranks, q_before per band) -- chosen for passes whose
     records far outnumber the cut entries, forced here -- equals the
     reference, also with an overflowing table."""
     monkeypatch.setenv("RLC_SHARD_ENTRY", "1")
     scene = scenes.cornell_grid(2, 1, dome_triangles=128, width=48, height=36)
-    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL,
+    cfg = rlcuts.RenderConfig(spp=6, passes=3, sampler=RL, max_depth=depth,
                               hash=rlcuts.HashConfig(capacity=capacity, probe_limit=16),
                               cut=rlcuts.CutConfig(cut_size=32, split_threshold=2.0))
     dev = torch.device("cuda", 0)
