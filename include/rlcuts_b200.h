@@ -435,7 +435,8 @@ enum {
   RLC_SAMPLE_FALLBACK = 2,   /* the cell lookup fell back (hash_grid.cpp:140) */
   RLC_SAMPLE_RAY = 4,        /* a shadow segment was traced (bvh.cpp:159-188) */
   RLC_SAMPLE_NONZERO = 8,    /* unoccluded, front-facing: nonzero contribution */
-  RLC_SAMPLE_LEARNED = 16    /* drawn from a cut (rl_lightcuts) */
+  RLC_SAMPLE_LEARNED = 16,   /* drawn from a cut (rl_lightcuts) */
+  RLC_SAMPLE_FROZEN = 32     /* radiance weighted by the frozen-cdf pdf (rlc_context_set_pdf_mode) */
 };
 typedef struct rlc_sample_record {
   uint32_t vertex;  /* canonical index within the pass's rows */
@@ -448,6 +449,16 @@ typedef struct rlc_sample_record {
   double radiance[3];
 } rlc_sample_record;
 rlc_status rlc_context_enable_sample_export(rlc_context* ctx, int enable);
+/* ---- pdf mode (SURVEY 8 notes, 0 fact 2) --------------------------------
+ * The reference weights a learned sample's radiance by the LIVE q of its
+ * cluster at the moment its update lands (cut.cpp:105: q_before), while the
+ * cluster was drawn from the pass-frozen cdf -- the estimator is biased.
+ * RLC_PDF_FROZEN_CDF (a non-parity mode) weights it by the probability the
+ * selection used, the cluster's share of the frozen cdf; selection and
+ * learning are unchanged.  Default RLC_PDF_LIVE_Q (bit-exact with the
+ * reference).  Samples exported in the frozen mode carry RLC_SAMPLE_FROZEN. */
+enum { RLC_PDF_LIVE_Q = 0, RLC_PDF_FROZEN_CDF = 1 };
+rlc_status rlc_context_set_pdf_mode(rlc_context* ctx, int mode);
 /* out [max_n] may be NULL (count only); *n_out = path vertices of the pass. */
 rlc_status rlc_pass_samples(const rlc_context* ctx, uint64_t max_n, rlc_sample_record* out,
                             uint64_t* n_out);

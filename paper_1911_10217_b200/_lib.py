@@ -147,6 +147,7 @@ SIGNATURES = {
                                    C.c_uint32, C.c_uint32, C.c_uint64, C.c_int, C.c_int]),
     "rlc_render_frame": (C.c_int, [_P, C.POINTER(RenderConfigC), _dp, C.POINTER(RenderResultC)]),
     "rlc_context_enable_sample_export": (C.c_int, [_P, C.c_int]),
+    "rlc_context_set_pdf_mode": (C.c_int, [_P, C.c_int]),
     "rlc_pass_samples": (C.c_int, [_P, C.c_uint64, C.c_void_p, _u64p]),
     "rlc_context_update_scene": (C.c_int, [_P, C.POINTER(SceneDescC)]),
     "rlc_context_prepare_scene": (C.c_int, [_P, C.POINTER(SceneDescC), _u64p]),

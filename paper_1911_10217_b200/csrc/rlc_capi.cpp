@@ -564,6 +564,7 @@ struct rlc_context {
   uint32_t* d_changes = nullptr;  // device change count of graph replays
   // rlc_pass_samples: the last pass's parameters and G-buffer slot
   bool export_samples = false;
+  bool frozen_pdf = false;  // rlc_context_set_pdf_mode
   rlc::PassParams last_pass{};
   rlc::PassBuffers last_pb{};
   bool last_valid = false;
@@ -692,6 +693,7 @@ PassSetup setup_pass(rlc_context* ctx, const rlc_render_config* cfg, uint32_t pa
   S.p.harmonic = grid ? grid->harmonic : 0u;
   S.p.pass_dev = ctx->graph_pass_dev;
   S.p.export_samples = ctx->export_samples ? 1u : 0u;
+  S.p.frozen_pdf = ctx->frozen_pdf ? 1u : 0u;
   if (grid) S.g = grid->dev;
   else S.g.counters = ctx->counters;
   if (S.nv > 0) ctx->ensure_scratch(S.nv);
@@ -2073,6 +2075,15 @@ rlc_status rlc_shard_frames(const rlc_context* cctx, const rlc_render_config* co
     rlc::add_launches(G.launches * replays);
     for (cudaEvent_t e : ctx->ev_gbuf_free) RLC_CK(cudaEventRecord(e, st));
     for (uint32_t p = first_pass + replays * kFrames; p < first_pass + count; ++p) single(p);
+  });
+}
+
+rlc_status rlc_context_set_pdf_mode(rlc_context* ctx, int mode) {
+  return guarded([&] {
+    require(ctx != nullptr, "rlc_context_set_pdf_mode: null context");
+    require(mode == RLC_PDF_LIVE_Q || mode == RLC_PDF_FROZEN_CDF, "rlc_context_set_pdf_mode: bad mode");
+    ctx->frozen_pdf = mode == RLC_PDF_FROZEN_CDF;
+    ++ctx->scene_gen;  // captured pass graphs hold the old pass parameters
   });
 }
 

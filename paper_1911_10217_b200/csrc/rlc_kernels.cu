@@ -1083,6 +1083,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   r.s = 0;
   r.total = 0;
   uint32_t e = 0;
+  double frozen_share = 0;      // learned: the cluster's share of the frozen cdf
   uint32_t lpos = 0xffffffffu;  // learned: light-tree position of the pick
   if (P.sampler == 2u) {
     // A key new this pass (kPending) has been inserted in canonical order
@@ -1121,6 +1122,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
     const double clo = s == 0 ? 0.0 : cdf[s - 1];
     const double span = cdf[s] - clo;
     const double frac = span > 0 ? clampd((u1 * total - clo) / span, 0.0, 1.0) : 0.0;
+    if (P.frozen_pdf) frozen_share = span / total;
     const uint32_t offset = min(size - 1, uint32_t(frac * double(size)));
     RLC_CHECK(s < M && size >= 1 && begin + offset < sc.num_lights, err);
     lpos = begin + offset;  // tree.order[begin + offset] is the emitter (lights_ord)
@@ -1211,6 +1213,13 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
         r.flags |= kSNonzero;
         // estimators.cpp:103-104; pdf_in_cluster is 1 for the baselines
         r.v = luminance(contrib) / ((P.sampler == 2u ? r.pin : 1.0) * r.pdf_area);
+        if (P.frozen_pdf && (r.flags & kSLearned)) {
+          // pdf_mode frozen_cdf: the probability the selection used -- the
+          // cluster's share of the frozen cdf -- not the live q;
+          // the learning (v, the fold) is unchanged
+          r.pin = frozen_share * r.pin;
+          r.flags |= kSFrozen;
+        }
         // the shadow segment (pos, point) of occluded(): bvh.cpp:160-167
         const V3 dd = point - pos;
         const double len = length(dd);
@@ -2347,7 +2356,7 @@ __global__ void __launch_bounds__(256) k_accumulate(DevScene sc, PassParams P,
       if ((rf & kSNonzero) && !(rf & kROccluded)) {
         const SampleRec r = ldg_vec(srec + idx);
         double pdf_sel;
-        if (r.flags & kSLearned) {
+        if ((r.flags & kSLearned) && !(r.flags & kSFrozen)) {
           const double p = q_before[idx] / r.total;
           pdf_sel = p * r.pin;
         } else {
@@ -2989,14 +2998,15 @@ __global__ void k_export_samples(PassParams P, const GBuf* __restrict__ gbuf,
     const bool learned = r.flags & kSLearned;
     const bool nonzero = (r.flags & kSNonzero) && !(rflag[idx] & kROccluded);
     e.flags = 1u | (learned && !(r.flags & kSRecord) ? 2u : 0u) | (r.flags & kSRay ? 4u : 0u) |
-              (nonzero ? 8u : 0u) | (learned ? 16u : 0u);
+              (nonzero ? 8u : 0u) | (learned ? 16u : 0u) | (r.flags & kSFrozen ? 32u : 0u);
     e.cluster = learned ? r.s : 0u;
     e.emitter = P.export_samples ? emit[idx] : 0xffffffffu;
     e.v = vdense[idx];
     e.total = r.total;
     if (learned) e.q_before = q_before[idx];
     if (nonzero) {
-      const double pdf_sel = learned ? (e.q_before / r.total) * r.pin : r.pin;
+      const double pdf_sel =
+          learned && !(r.flags & kSFrozen) ? (e.q_before / r.total) * r.pin : r.pin;
       const double den = pdf_sel * r.pdf_area;
       e.radiance[0] = r.c[0] / den;
       e.radiance[1] = r.c[1] / den;

@@ -25,7 +25,9 @@ enum : uint32_t {
 };
 // Sample-record flags
 // kSRay: rays[idx] valid; kSRecord: the sample carries an update_q record
-enum : uint32_t { kSNonzero = 1u, kSLearned = 2u, kSRay = 4u, kSRecord = 8u };
+enum : uint32_t { kSNonzero = 1u, kSLearned = 2u, kSRay = 4u, kSRecord = 8u, kSFrozen = 16u };
+// kSFrozen (pdf_mode frozen_cdf): srec.pin holds the whole selection pdf,
+// (cdf[s] - cdf[s - 1]) / total * pin, instead of the live q_before's
 // rflag bit set by k_shadow for an occluded segment (srec keeps the visible
 // contribution; its v is zeroed in vdense): a byte in a 2 MB array instead of
 // a read-modify-write of the 64-byte sample record
@@ -168,6 +170,7 @@ struct PassParams {
   const uint32_t* pass_dev;  // non-null (CUDA-graph replays): the pass index is read here
   uint32_t defer_insert;     // sharded trace: new keys are inserted by the fold of all ranks
   uint32_t export_samples;   // k_sample files each vertex's emitter index (rlc_pass_samples)
+  uint32_t frozen_pdf;       // radiance with the pass-frozen cdf's pdf (non-parity, unbiased)
 };
 
 // The distinct keys missing from the table in one pass, each with the

@@ -451,6 +451,14 @@ SAMPLE_DTYPE = np.dtype([("vertex", "<u4"), ("cluster", "<u4"), ("emitter", "<u4
                          ("flags", "<u4"), ("q_before", "<f8"), ("v", "<f8"), ("total", "<f8"),
                          ("radiance", "<f8", (3,))])  # rlc_sample_record
 SAMPLE_VALID, SAMPLE_FALLBACK, SAMPLE_RAY, SAMPLE_NONZERO, SAMPLE_LEARNED = 1, 2, 4, 8, 16
+SAMPLE_FROZEN = 32
+PDF_LIVE_Q, PDF_FROZEN_CDF = 0, 1
+
+
+def set_pdf_mode(ctx: RenderContext, mode: int) -> None:
+    """rlc_context_set_pdf_mode: PDF_LIVE_Q (the reference's estimator,
+    bit-exact) or PDF_FROZEN_CDF (unbiased, non-parity)."""
+    _check(_lib.load().rlc_context_set_pdf_mode(ctx.handle, int(mode)))
 
 
 def enable_sample_export(ctx: RenderContext, enable: bool = True) -> None:
@@ -477,7 +485,9 @@ def pass_samples(ctx: RenderContext, config: RenderConfig, row_begin: int = 0) -
     return {"pixel": pixel, "cluster": rec["cluster"], "emitter": rec["emitter"],
             "fallback": (rec["flags"] & SAMPLE_FALLBACK) != 0, "q_before": rec["q_before"],
             "v": rec["v"], "radiance": rec["radiance"], "total": rec["total"],
-            "ray": (rec["flags"] & SAMPLE_RAY) != 0, "nonzero": (rec["flags"] & SAMPLE_NONZERO) != 0}
+            "ray": (rec["flags"] & SAMPLE_RAY) != 0, "nonzero": (rec["flags"] & SAMPLE_NONZERO) != 0,
+            "learned": (rec["flags"] & SAMPLE_LEARNED) != 0,
+            "frozen": (rec["flags"] & SAMPLE_FROZEN) != 0}
 
 
 def shard_trace(ctx: RenderContext, config: RenderConfig, pass_index: int, grid: HashGrid,
