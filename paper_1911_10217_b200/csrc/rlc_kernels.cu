@@ -1068,8 +1068,7 @@ __global__ void __launch_bounds__(128, RLC_SAMPLE_BLOCKS) k_sample(DevScene sc, 
   const GBuf gb = ldg_vec(gbuf + idx);
   gflags[idx] = gb.flags;
   keys[idx] = kInvalidKey;
-  if (!(gb.flags & kGReflective)) {
-    srec[idx].flags = 0;
+  if (!(gb.flags & kGReflective)) {  // (its sample record is never read: no partial store)
     rflag[idx] = 0;  // read by the compactions
     return;
   }
